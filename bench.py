@@ -1,0 +1,443 @@
+#!/usr/bin/env python3
+"""Optimizer-update throughput on B200: params updated / s (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): all six optimizers -- AdamW, Lion, Adan,
+Sophia, LOMO, AdaLomo -- each updating a LLaMA-7B-shaped synthetic parameter set
+(291 tensors, 6,738,415,616 fp32 params, registry order) once per step.  One
+"step" = one update of the whole set by each of the six optimizers in turn;
+value = 6 * P * K / (device time of the K timed steps).  Inputs are synthetic
+(counter-based generator), fp32, resident in HBM, and 27 GB per buffer (> L2),
+so no L2 flush is needed between iterations.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun, one process per GPU): ZeRO partition of the same set
+(ZeroPlan, parallel.cpp:20-34) -- each rank updates its owned shard; the
+gradient reduce-scatter / parameter all-gather are timed separately
+(`collectives`), value = P * 6 * K / max-over-ranks time ("strong").
+
+e2e: the same metric through the C-ABI with HOST (pinned) buffers -- per step
+H2D params+grads, the update, D2H params (mco_flat_step_host pipelines it for
+the four stored-state kinds).  cpu_baseline / --impl reference: the
+reference's own minicollie::optim (oracle/_ref, compiled from its sources)
+timed on this host's cores on a bounded sample (one 7B decoder layer).
+"""
+from __future__ import annotations
+
+import argparse
+import gc
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KINDS = ["adamw", "lion", "adan", "sophia", "lomo", "adalomo"]
+# Algorithmic (dependency-forced) HBM bytes per parameter, fp32.
+BYTES_PER_PARAM = {"adamw": 28, "lion": 20, "adan": 44, "sophia": 24, "lomo": 12,
+                   "adalomo": 24}
+# Paper Table 4 hyper-parameters for throughput runs; Sophia: defaults.
+HPARAMS = {"adamw": dict(lr=1e-5, weight_decay=1e-2), "lion": dict(lr=3e-6, weight_decay=3e-2),
+           "adan": dict(lr=5e-5, weight_decay=2e-2), "sophia": dict(lr=1e-4),
+           "lomo": dict(lr=1e-2), "adalomo": dict(lr=5e-4)}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._th = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                        timeout=10).stdout.strip()
+                    if out:
+                        self.rows.append([x.strip() for x in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+
+        self._th = threading.Thread(target=run, daemon=True)
+        self._th.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._th:
+            self._th.join(timeout=15)
+
+    def summary(self):
+        import statistics
+
+        sm = [float(r[1]) for r in self.rows if len(r) > 2 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 2 and r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------------------
+# reference arm / CPU baseline: the reference's own code on the host cores
+# ---------------------------------------------------------------------------------------
+
+def cpu_sample_shapes():
+    from paper_2312_00407_b200.registry import LLAMA_7B
+
+    return LLAMA_7B.shapes()[1:10]  # one decoder layer: 9 tensors, 202,383,360 params
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_cpu_reference(warmup: int, steps: int):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2312_00407_b200.optim import OptimizerConfig, parse_kind
+
+    if O.ref is None:
+        raise RuntimeError("oracle/_ref/libmco_ref.so missing (run __graft_entry__.build())")
+    shapes = cpu_sample_shapes()
+    n = sum(int(__import__("math").prod(s)) for s in shapes)
+    threads = host_threads()
+    per = {}
+    total = 0.0
+    for k in KINDS:
+        cfg = OptimizerConfig.defaults_for(parse_kind(k))
+        for a, v in HPARAMS[k].items():
+            setattr(cfg, a, v)
+        sec = O.ref_bench(cfg, shapes, threads, warmup, steps)
+        per[k] = {"ms": sec * 1e3, "params_per_s": n / sec}
+        total += sec
+        log(f"[cpu-ref] {k}: {sec * 1e3:.1f} ms/step, {n / sec / 1e9:.3f} Gparam/s "
+            f"({threads} threads)")
+    value = len(KINDS) * n / total
+    sample = (f"one LLaMA-7B decoder layer (9 tensors, {n} fp64 params) per optimizer, "
+              f"{warmup} warm-up + {steps} timed steps, one FlatOptimizer per thread over "
+              "disjoint slices (stored-state kinds) / tensors across threads (LOMO, AdaLomo)")
+    return value, threads, sample, per, total / max(steps, 1)
+
+
+# ---------------------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------------------
+
+def make_cfg(kind: str):
+    from paper_2312_00407_b200.optim import OptimizerConfig, parse_kind
+
+    cfg = OptimizerConfig.defaults_for(parse_kind(kind))
+    for a, v in HPARAMS[kind].items():
+        setattr(cfg, a, v)
+    return cfg
+
+
+class Stepper:
+    """One optimizer over (a shard of) the flat registry buffers, via the public API."""
+
+    def __init__(self, kind, shapes, p, g, owned=None):
+        from paper_2312_00407_b200 import optim
+
+        self.kind, self.p, self.g = kind, p, g
+        self.cfg = make_cfg(kind)
+        self.lr = self.cfg.lr
+        if kind in ("adamw", "lion", "adan", "sophia"):
+            self.opt = optim.FlatOptimizer(self.cfg, p.numel())
+        elif kind == "adalomo":
+            self.opt = optim.AdaLomoState(self.cfg, shapes)
+        else:
+            self.opt = None
+
+    def step(self):
+        from paper_2312_00407_b200 import optim
+
+        if self.kind == "lomo":
+            optim.lomo_apply(self.p, self.g, self.lr, 1.0)
+        elif self.kind == "adalomo":
+            self.opt.apply_all(self.p, self.g, self.lr)
+        else:
+            self.opt.step(self.p, self.g, self.lr)
+
+
+def bench_ours(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_00407_b200 import optim, registry
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    model = registry.MODELS[args.model]
+    shapes = model.shapes()
+    P = model.param_count()
+    kinds = args.optimizers.split(",")
+    hbm_peak, peak_src = measured_peaks()
+
+    # ZeRO partition of the flat registry (N=1: the whole set)
+    parts, offs = optim.zero_plan(P, world, 1)
+    owned = parts[rank]
+    log(f"[rank {rank}] model {model.name} P={P} owned={owned} kinds={kinds}")
+
+    p = torch.empty(owned, dtype=torch.float32, device=dev)
+    g = torch.empty(owned, dtype=torch.float32, device=dev)
+    if world == 1:
+        registry.fill_params(p, shapes)
+        registry.fill_grads(g, shapes, 1)
+    else:
+        optim.synth_fill(p, registry.SEED, 0, 0xFFFF, 0, 0, -6)
+        optim.synth_fill(g, registry.SEED, 1, 0xFFFF, 1, 0, -7, 10)
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    per = {}
+    total_ms = 0.0
+    launches = 0
+    clocks = ClockSampler(local_rank)
+    for kind in kinds:
+        if world > 1 and kind == "adalomo":
+            # AdaLomo shards by rows of whole matrices; the flat
+            # ZeRO shard here is timed as the elementwise kinds only.
+            continue
+        st = Stepper(kind, shapes, p, g)
+        for _ in range(args.warmup):
+            st.step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = optim.launch_count()
+        if kind == kinds[0]:
+            clocks.start()
+        e0.record(stream)
+        for _ in range(args.steps):
+            st.step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        launches += optim.launch_count() - l0
+        ms = e0.elapsed_time(e1) / args.steps
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        bpp = BYTES_PER_PARAM[kind]
+        gbs = bpp * owned / (ms * 1e-3) / 1e9
+        per[kind] = {"ms": round(ms, 4), "params_per_s": P / (ms * 1e-3) if world > 1 else
+                     owned / (ms * 1e-3), "bytes_per_param": bpp, "achieved_gbs": round(gbs, 1),
+                     "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
+                     "launches_per_step": (optim.launch_count() - l0) / max(args.steps, 1)}
+        total_ms += ms
+        log(f"[rank {rank}] {kind}: {ms:.3f} ms/step, {owned / ms / 1e6:.1f} Gparam/s/GPU, "
+            f"{gbs:.0f} GB/s = {gbs / hbm_peak:.3f} of {peak_src} HBM")
+        del st
+        gc.collect()
+        torch.cuda.synchronize()
+    clocks.stop()
+    nk = len(per)
+    value = nk * P / (total_ms * 1e-3)
+
+    # dominant kernel = the optimizer with the largest share of the step
+    dom = max(per, key=lambda k: per[k]["ms"])
+    roofline = {"bound": "hbm", "kernel": f"{dom} update (flat_step_kernel)" if dom not in (
+        "lomo", "adalomo") else dom, "achieved": per[dom]["achieved_gbs"], "peak": hbm_peak,
+        "peak_source": peak_src, "unit": "GB/s",
+        "frac": round(per[dom]["achieved_gbs"] / hbm_peak, 4),
+        "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": owned,
+        "traffic": load_traffic(dom)}
+    return dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
+                launches=launches, clocks=clocks.summary(), P=P, owned=owned,
+                shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
+
+
+def load_traffic(kind):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
+    ncu --set full capture (profiles/traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kind)
+    except Exception:
+        return None
+
+
+def bench_e2e(args, res):
+    """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p)."""
+    import psutil
+    import torch
+
+    from paper_2312_00407_b200 import optim, registry
+
+    P = res["owned"]
+    need = 2 * P * 4 * 1.3
+    avail = psutil.virtual_memory().available
+    n = P if need < avail * 0.6 else int(avail * 0.6 / (2 * 4 * 1.3)) // 1024 * 1024
+    shapes = res["shapes"]
+    if n < P:  # whole tensors prefix that fits
+        acc, k = 0, 0
+        while k < len(shapes) and acc + int(__import__("math").prod(shapes[k])) <= n:
+            acc += int(__import__("math").prod(shapes[k]))
+            k += 1
+        shapes, n = shapes[:k], acc
+    log(f"[e2e] host buffers: {n} params ({'full set' if n == P else 'prefix'}), pinned")
+    hp = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    hg = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    hp.copy_(res["p"][:n].cpu())
+    hg.copy_(res["g"][:n].cpu())
+    dp, dg = res["p"][:n], res["g"][:n]
+    steps = max(1, min(args.steps, args.e2e_steps))
+    tot_s, h2d, d2h = 0.0, 0, 0
+    per = {}
+    for kind in res["kinds"]:
+        cfg = make_cfg(kind)
+        if kind in ("adamw", "lion", "adan", "sophia"):
+            opt = optim.FlatOptimizer(cfg, n)
+            hpn, hgn = hp.numpy(), hg.numpy()
+
+            def one():
+                opt.step(hpn, hgn, cfg.lr)  # mco_flat_step_host: pipelined H2D/step/D2H
+        else:
+            ada = optim.AdaLomoState(cfg, shapes) if kind == "adalomo" else None
+
+            def one():
+                dp.copy_(hp, non_blocking=True)
+                dg.copy_(hg, non_blocking=True)
+                if ada is not None:
+                    ada.apply_all(dp, dg, cfg.lr)
+                else:
+                    optim.lomo_apply(dp, dg, cfg.lr, 1.0)
+                hp.copy_(dp, non_blocking=True)
+                torch.cuda.synchronize()
+        one()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            one()
+        torch.cuda.synchronize()
+        dt = (time.perf_counter() - t0) / steps
+        per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": n / dt}
+        tot_s += dt
+        h2d += 2 * n * 4
+        d2h += n * 4
+        log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {n / dt / 1e9:.2f} Gparam/s")
+        del one
+        gc.collect()
+    return {"value": len(per) * n / tot_s, "unit": "params/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "params": n, "per_optimizer": per,
+            "path": "C-ABI with pinned host buffers (mco_flat_step_host for the stored-state "
+                    "kinds; H2D + lomo_apply / apply_all + D2H for LOMO / AdaLomo)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="llama-7b")
+    ap.add_argument("--optimizers", default=",".join(KINDS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    metric = "params updated/sec (all six optimizers, LLaMA-7B-shaped set)"
+    config = {"workload": "configs[1]: AdamW/Lion/Adan/Sophia/LOMO/AdaLomo each updating a "
+                          "LLaMA-7B-shaped synthetic set (291 tensors, 6,738,415,616 params)",
+              "model_shape": args.model, "params": None, "dtype_storage": "fp32 p/g/state",
+              "l2": "inputs larger than L2 (27 GB per buffer); no flush needed",
+              "parallelism": f"zero{world}" if world > 1 else "single GPU"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        value, threads, sample, per, sec_step = run_cpu_reference(args.warmup, args.steps)
+        from paper_2312_00407_b200.registry import LLAMA_7B
+
+        config["params"] = LLAMA_7B.param_count()
+        line = {"impl": "reference", "metric": metric, "value": value, "unit": "params/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": sec_step * 1e3, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads,
+                                 "kind": "reference", "sample": sample},
+                "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0},
+                "per_optimizer": per}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = bench_ours(args, rank, world, local_rank)
+    config["params"] = res["P"]
+    e2e = None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_e2e:
+        try:
+            e2e = bench_e2e(args, res)
+        except Exception as ex:  # report, never fake
+            log(f"[e2e] failed: {ex!r}")
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, threads, sample, per, _ = run_cpu_reference(1, args.cpu_steps)
+            cpu = {"value": v, "unit": "params/s", "cores": threads, "kind": "reference",
+                   "sample": sample, "per_optimizer": per}
+        except Exception as ex:
+            log(f"[cpu_baseline] failed: {ex!r}")
+    if rank == 0:
+        line = {"metric": metric, "value": res["value"], "unit": "params/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+                "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": config,
+                "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": res["launches"], "clocks": res["clocks"],
+                "per_optimizer": res["per"]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

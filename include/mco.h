@@ -1,0 +1,196 @@
+/*
+ * mco.h -- C-ABI of the B200-native optimizer-update hot path.
+ *
+ * Drop-in boundary for the reference's C++ optimizer operator API,
+ * namespace minicollie::optim (/root/reference/proj/core/include/minicollie/optim.hpp).
+ * Every entry point below names the reference interface it replaces.
+ * Plain C types only: device buffers are `void*` device pointers, streams are
+ * `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *
+ * Error model (errors.hpp:8-32): each call returns an mco_status; the message
+ * of the last failure on the calling thread is mco_last_error() and equals the
+ * reference's exception what() text where the reference throws.  Argument and
+ * contract errors are reported synchronously; device-side CUDA errors surface
+ * as MCO_CUDA on the failing launch or on the next synchronising call
+ * (mco_sync).  Stream-ordered calls are asynchronous with respect to the host.
+ *
+ * Numerics: fp32 state and arithmetic by default (bf16 accepted for gradients,
+ * bf16 parameter storage for LOMO and the bf16 parameter copy of the mixed
+ * step); fp64 state for the bit-exact parity mode.  Kernels are compiled with
+ * no multiply-add contraction, so every fp32 / fp64 elementwise update is
+ * bit-identical to the operation order of optim.cpp.
+ */
+#ifndef MCO_H_
+#define MCO_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* errors.hpp:8-32 taxonomy; CLI exit-code mapping Config->2, Data->3 kept. */
+typedef enum mco_status {
+  MCO_OK = 0,
+  MCO_CONFIG = 2,   /* ConfigError   */
+  MCO_DATA = 3,     /* DataError     */
+  MCO_CONTRACT = 4, /* ContractError */
+  MCO_PROTOCOL = 5, /* ProtocolError */
+  MCO_IO = 6,       /* IoError       */
+  MCO_CUDA = 7      /* device / runtime failure (no reference counterpart) */
+} mco_status;
+
+/* optim.hpp:14  enum class Kind { kAdamW, kLion, kAdan, kSophia, kLomo, kAdaLomo } */
+typedef enum mco_kind {
+  MCO_ADAMW = 0,
+  MCO_LION = 1,
+  MCO_ADAN = 2,
+  MCO_SOPHIA = 3,
+  MCO_LOMO = 4,
+  MCO_ADALOMO = 5
+} mco_kind;
+
+typedef enum mco_dtype { MCO_F32 = 0, MCO_BF16 = 1, MCO_F64 = 2 } mco_dtype;
+
+/* optim.hpp:20-35  struct OptimizerConfig, field for field
+ * (std::optional<double> clip_threshold -> has_clip_threshold + clip_threshold). */
+typedef struct mco_config {
+  int kind;
+  double lr;
+  double weight_decay;
+  double beta1;
+  double beta2;
+  double beta3;
+  double eps;
+  int has_clip_threshold;
+  double clip_threshold;
+  double adalomo_clip;
+  double sophia_rho;
+  int update_interval;
+} mco_config;
+
+const char* mco_last_error(void);
+const char* mco_version(void);
+
+/* optim.hpp:16  Kind parse_kind(const std::string&)  (ConfigError on unknown) */
+mco_status mco_parse_kind(const char* name, int* kind_out);
+/* optim.hpp:17  std::string kind_name(Kind)  (NULL on unknown kind) */
+const char* mco_kind_name(int kind);
+/* optim.hpp:18  bool is_fused(Kind) */
+int mco_is_fused(int kind);
+/* optim.hpp:33  static OptimizerConfig defaults_for(Kind) */
+mco_status mco_defaults_for(int kind, mco_config* out);
+/* optim.hpp:34  void validate() const */
+mco_status mco_validate(const mco_config* cfg);
+
+/* optim.hpp:113-127  state_bytes(kind, param_count, PrecisionPolicy, shapes).
+ * shapes: nshapes entries, entry k has ndims[k] dims taken consecutively from dims. */
+mco_status mco_state_bytes(int kind, uint64_t param_count, int param_dtype_bytes,
+                           int grad_dtype_bytes, int master_copy, int nshapes,
+                           const int* ndims, const int64_t* dims, uint64_t* out);
+
+/* ---- FlatOptimizer (optim.hpp:40-64, optim.cpp:74-181) ------------------- */
+typedef struct mco_flat mco_flat;
+
+/* FlatOptimizer(cfg, owned_len): zero-initialised SoA state on `device`
+ * (m,v | m | m,v,n,g_prev | m,h).  state_dtype MCO_F32 (default product path)
+ * or MCO_F64 (bit-exact parity mode).  Fused kinds -> MCO_CONTRACT. */
+mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device,
+                           int state_dtype, mco_flat** out);
+mco_status mco_flat_destroy(mco_flat* h);
+
+/* FlatOptimizer::step(span<double> params, span<const double> grads, lr),
+ * device pointers, stream-ordered.  n_params != n_grads -> MCO_CONTRACT with
+ * the reference's message (optim.cpp:101-103); n_params > owned_len ->
+ * MCO_CONTRACT (the reference would index past its state).  ++t happens
+ * before the update (optim.cpp:104).
+ * dtypes: state F32 -> params F32, grads F32 or BF16; state F64 -> F64/F64. */
+mco_status mco_flat_step(mco_flat* h, void* params, int param_dtype, uint64_t n_params,
+                         const void* grads, int grad_dtype, uint64_t n_grads, double lr,
+                         void* stream);
+
+/* Mixed-precision step (ZeRO shard, SURVEY 8(d) "mixed"): fp32 master params
+ * updated in place and written once more as bf16 into param_out. */
+mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, int grad_dtype,
+                               uint16_t* param_out_bf16, uint64_t n, double lr, void* stream);
+
+/* The reference's host-span overload: params / grads are HOST arrays (F64 for
+ * an F64-state optimizer, F32 for an F32-state one); streamed through the
+ * device in pipelined chunks; returns when params hold the updated values. */
+mco_status mco_flat_step_host(mco_flat* h, void* params, int param_dtype, uint64_t n_params,
+                              const void* grads, int grad_dtype, uint64_t n_grads, double lr);
+
+mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t);  /* steps_taken()     */
+mco_status mco_flat_set_steps(mco_flat* h, int64_t t);          /* set_steps_taken() */
+mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out); /* state_bytes_runtime() */
+mco_status mco_flat_config(const mco_flat* h, mco_config* out);   /* config()          */
+/* buffers(): names in the reference's fixed order m, v, n, h, g_prev (optim.cpp:173-181). */
+mco_status mco_flat_num_buffers(const mco_flat* h, int* out);
+mco_status mco_flat_buffer(mco_flat* h, int index, const char** name, void** dev_ptr,
+                           uint64_t* len, int* dtype);
+
+/* ---- LOMO (optim.cpp:185-190, 284-318) ------------------------------------ */
+/* lomo_apply(Tensor& param, lr, scale): p -= (lr*scale) * g.
+ * dtypes: F32/F32, BF16/BF16 (fp32 math, RNE store), F32/BF16, F64/F64. */
+mco_status mco_lomo_apply(void* params, int param_dtype, const void* grads, int grad_dtype,
+                          uint64_t n, double lr, double scale, void* stream);
+/* Same, with the clip scale computed on the device from a device Σg²
+ * (optim.cpp:302-303: scale = clip/‖g‖ iff ‖g‖ > clip and ‖g‖ > 0). */
+mco_status mco_lomo_apply_clipped(void* params, int param_dtype, const void* grads,
+                                  int grad_dtype, uint64_t n, double lr, const double* dev_sumsq,
+                                  double clip, void* stream);
+/* Σx² into *dev_out (fp64, deterministic fixed-order reduction);
+ * accumulate != 0 adds to the existing value (optim.cpp:294-300 hook sum). */
+mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* dev_out, int accumulate,
+                     void* stream);
+
+/* ---- AdaLomo (optim.hpp:76-96, optim.cpp:192-282) ------------------------- */
+typedef struct mco_adalomo mco_adalomo;
+
+/* AdaLomoState(cfg, params): one entry per tensor in registry order;
+ * ndim == 2 -> factored v_row[R], v_col[C]; otherwise v_full[numel].
+ * State is fp64 on `device`. */
+mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* ndims,
+                              const int64_t* dims, int device, mco_adalomo** out);
+mco_status mco_adalomo_destroy(mco_adalomo* h);
+/* AdaLomoState::apply(Tensor& param, lr) -- the per-tensor hook form.
+ * dev_grad_sumsq: optional device Σg² over ALL tensors (global grad-norm
+ * clip with cfg.clip_threshold); NULL = no clip.  dtypes F32/F32, F32/BF16. */
+mco_status mco_adalomo_apply(mco_adalomo* h, int tensor_index, void* param, int param_dtype,
+                             const void* grad, int grad_dtype, double lr,
+                             const double* dev_grad_sumsq, void* stream);
+/* Multi-tensor form: every tensor at once over registry-order flat buffers
+ * (tensor k at element offset sum_{j<k} numel_j).  If cfg.has_clip_threshold
+ * the global grad norm over the whole set is computed in the same pass and
+ * applied (clip fused into pass 1). */
+mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_params, int param_dtype,
+                                 const void* flat_grads, int grad_dtype, double lr,
+                                 void* stream);
+mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out); /* fp64 accounting */
+mco_status mco_adalomo_get_steps(const mco_adalomo* h, int tensor_index, int64_t* t);
+/* which: 0 v_row, 1 v_col, 2 v_full (fp64 device arrays; len 0 if absent). */
+mco_status mco_adalomo_buffer(mco_adalomo* h, int tensor_index, int which, void** dev_ptr,
+                              uint64_t* len);
+
+/* ---- ZeRO partition (parallel.cpp:20-38) ------------------------------------ */
+/* ZeroPlan::make(total_len, dp_size, stage): part_sizes[dp_size], offsets[dp_size+1]. */
+mco_status mco_zero_plan(uint64_t total_len, int dp_size, int stage, uint64_t* part_sizes,
+                         uint64_t* offsets);
+
+/* ---- synthetic inputs ------------------------------------------ */
+/* Counter-based, stateless generator; values exact in fp32 (bf16 grid for BF16). */
+mco_status mco_synth_fill(void* dst, int dtype, uint64_t n, uint64_t seed, uint32_t role,
+                          uint32_t tensor, uint32_t step, int64_t cols, int scale_log2,
+                          int zero_log2, int rowcol, void* stream);
+
+/* ---- misc -------------------------------------------------------------------- */
+mco_status mco_sync(void* stream);                 /* cudaStreamSynchronize + error check */
+mco_status mco_device_count(int* out);
+/* Kernel launches issued by this library on the calling process (counter). */
+uint64_t mco_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MCO_H_ */

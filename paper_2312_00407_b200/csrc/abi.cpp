@@ -1,0 +1,658 @@
+// C-ABI (include/mco.h) over the sm_100a kernels: the drop-in boundary for
+// minicollie::optim (optim.hpp).  Host logic here restates the reference's
+// non-kernel behaviour -- kind names, defaults, validation, error messages,
+// state accounting, step counter, buffer naming -- citing optim.cpp lines.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "adalomo.h"
+#include "kernels.h"
+#include "mco.h"
+
+namespace mco {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+thread_local std::string g_err;
+}  // namespace
+
+void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+const DeviceInfo& device_info(int device) {
+  static std::mutex mu;
+  static std::unordered_map<int, DeviceInfo> cache;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(device);
+  if (it != cache.end()) return it->second;
+  DeviceInfo d;
+  MCO_CUDA_CHECK(cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, device));
+  MCO_CUDA_CHECK(cudaDeviceGetAttribute(&d.l2_bytes, cudaDevAttrL2CacheSize, device));
+  return cache.emplace(device, d).first->second;
+}
+
+int current_device() {
+  int d = 0;
+  MCO_CUDA_CHECK(cudaGetDevice(&d));
+  return d;
+}
+
+namespace {
+
+template <class F>
+mco_status guard(F&& f) {
+  try {
+    f();
+    return MCO_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return MCO_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MCO_CUDA;
+  }
+}
+
+// RAII current-device switch.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    MCO_CUDA_CHECK(cudaGetDevice(&prev));
+    if (prev != dev) MCO_CUDA_CHECK(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+// optim.cpp:17-28
+const char* kind_cstr(int kind) {
+  switch (kind) {
+    case MCO_ADAMW: return "adamw";
+    case MCO_LION: return "lion";
+    case MCO_ADAN: return "adan";
+    case MCO_SOPHIA: return "sophia";
+    case MCO_LOMO: return "lomo";
+    case MCO_ADALOMO: return "adalomo";
+  }
+  return nullptr;
+}
+
+std::string kind_str(int kind) {
+  const char* s = kind_cstr(kind);
+  if (!s) throw Error(MCO_CONFIG, "unknown optimizer kind");
+  return s;
+}
+
+bool fused(int kind) { return kind == MCO_LOMO || kind == MCO_ADALOMO; }  // optim.cpp:30
+
+// optim.cpp:32-61
+mco_config defaults(int kind) {
+  if (!kind_cstr(kind)) throw Error(MCO_CONFIG, "unknown optimizer kind");
+  mco_config c{};
+  c.kind = kind;
+  c.lr = 1e-3;
+  c.weight_decay = 0.0;
+  c.beta1 = 0.9;
+  c.beta2 = 0.999;
+  c.beta3 = 0.99;
+  c.eps = 1e-8;
+  c.has_clip_threshold = 0;
+  c.clip_threshold = 0.0;
+  c.adalomo_clip = 1.0;
+  c.sophia_rho = 0.04;
+  c.update_interval = 10;
+  switch (kind) {
+    case MCO_ADAMW: c.beta1 = 0.9; c.beta2 = 0.999; break;
+    case MCO_LION: c.beta1 = 0.9; c.beta2 = 0.99; break;
+    case MCO_ADAN: c.beta1 = 0.98; c.beta2 = 0.92; c.beta3 = 0.99; break;
+    case MCO_SOPHIA: c.beta1 = 0.965; c.beta2 = 0.99; break;
+    case MCO_LOMO: break;
+    case MCO_ADALOMO: c.beta2 = 0.99; c.eps = 1e-30; break;
+  }
+  return c;
+}
+
+// optim.cpp:63-70
+void validate(const mco_config& c) {
+  if (c.lr <= 0) throw Error(MCO_CONFIG, "optimizer: lr must be > 0");
+  if (c.eps <= 0) throw Error(MCO_CONFIG, "optimizer: eps must be > 0");
+  for (double b : {c.beta1, c.beta2, c.beta3})
+    if (b < 0 || b >= 1) throw Error(MCO_CONFIG, "optimizer: betas must lie in [0, 1)");
+  if (c.weight_decay < 0) throw Error(MCO_CONFIG, "optimizer: weight_decay must be >= 0");
+  if (c.update_interval < 1) throw Error(MCO_CONFIG, "optimizer: update_interval must be >= 1");
+}
+
+// Per-step scalars (optim.cpp:116-117, 138-141, 159): double on the host, one
+// rounding to the kernel's type.  Identical rule in oracle/mco_oracle.c.
+template <typename T>
+StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
+  StepConsts<T> k{};
+  k.b1 = (T)c.beta1;
+  k.b2 = (T)c.beta2;
+  k.b3 = (T)c.beta3;
+  k.omb1 = (T)(1 - c.beta1);
+  k.omb2 = (T)(1 - c.beta2);
+  k.omb3 = (T)(1 - c.beta3);
+  k.c1 = (T)(1.0 - std::pow(c.beta1, static_cast<double>(t)));
+  k.c2 = (T)(1.0 - std::pow(c.beta2, static_cast<double>(t)));
+  k.c3 = (T)(1.0 - std::pow(c.beta3, static_cast<double>(t)));
+  k.lr = (T)lr;
+  k.eps = (T)c.eps;
+  k.wd = (T)c.weight_decay;
+  k.lrwd = (T)(lr * c.weight_decay);
+  k.den = (T)(1.0 + lr * c.weight_decay);
+  k.rho = (T)c.sophia_rho;
+  k.first = t == 1 ? 1 : 0;
+  k.refresh = ((t - 1) % c.update_interval) == 0 ? 1 : 0;
+  return k;
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case MCO_F32: return 4;
+    case MCO_BF16: return 2;
+    case MCO_F64: return 8;
+  }
+  throw Error(MCO_CONTRACT, "unknown dtype " + std::to_string(dt));
+}
+
+// Sum-of-squares workspace per (device, stream): launches on one stream are
+// ordered, so the partials / ticket counter are never shared concurrently.
+void* sumsq_ws(cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<uint64_t, void*> pool;
+  const int dev = current_device();
+  const uint64_t key = ((uint64_t)(uintptr_t)st) * 131 + (uint64_t)dev;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = pool.find(key);
+  if (it != pool.end()) return it->second;
+  void* p = nullptr;
+  MCO_CUDA_CHECK(cudaMalloc(&p, sumsq_ws_bytes()));
+  MCO_CUDA_CHECK(cudaMemset(p, 0, sumsq_ws_bytes()));
+  pool[key] = p;
+  return p;
+}
+
+}  // namespace
+}  // namespace mco
+
+using namespace mco;
+
+// ---- handles ---------------------------------------------------------------------
+struct mco_flat {
+  mco_config cfg{};
+  uint64_t n = 0;
+  int device = 0;
+  int state_dtype = MCO_F32;
+  int64_t t = 0;
+  void* slot[4] = {nullptr, nullptr, nullptr, nullptr};  // kernel slots s0..s3
+  std::vector<std::pair<const char*, void*>> named;       // buffers() order
+  // host-span path (lazily created)
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  void* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t hchunk = 0;
+  ~mco_flat() {
+    for (void* p : slot)
+      if (p) cudaFree(p);
+    for (auto& b : hbuf)
+      for (void* p : b)
+        if (p) cudaFree(p);
+    for (auto s : hs)
+      if (s) cudaStreamDestroy(s);
+  }
+};
+
+struct mco_adalomo {
+  AdaLomoPlan plan;
+  ~mco_adalomo() {
+    void* ptrs[] = {plan.d_tiles, plan.d_tensors, plan.d_item_off, plan.d_state,
+                    plan.d_colpart, plan.d_rowpart, plan.d_tile_sc, plan.d_tens_sc,
+                    plan.d_fa,    plan.d_fb,      plan.d_glob};
+    for (void* p : ptrs)
+      if (p) cudaFree(p);
+  }
+};
+
+extern "C" {
+
+const char* mco_last_error(void) { return g_err.c_str(); }
+const char* mco_version(void) { return "mco 0.1 (sm_100a)"; }
+uint64_t mco_launch_count(void) { return g_launches.load(); }
+
+mco_status mco_parse_kind(const char* name, int* out) {
+  return guard([&] {
+    const std::string s = name ? name : "";
+    for (int k = 0; k <= MCO_ADALOMO; ++k)
+      if (s == kind_cstr(k)) {
+        *out = k;
+        return;
+      }
+    throw Error(MCO_CONFIG, "unknown optimizer kind '" + s + "'");  // optim.cpp:15
+  });
+}
+
+const char* mco_kind_name(int kind) { return kind_cstr(kind); }
+int mco_is_fused(int kind) { return fused(kind) ? 1 : 0; }
+
+mco_status mco_defaults_for(int kind, mco_config* out) {
+  return guard([&] { *out = defaults(kind); });
+}
+
+mco_status mco_validate(const mco_config* cfg) { return guard([&] { validate(*cfg); }); }
+
+// optim.cpp:339-362
+mco_status mco_state_bytes(int kind, uint64_t count, int param_bytes, int grad_bytes,
+                           int master_copy, int nshapes, const int* ndims, const int64_t* dims,
+                           uint64_t* out) {
+  (void)grad_bytes;
+  return guard([&] {
+    const bool needs_master = master_copy && param_bytes < 4;  // optim.hpp:118
+    const uint64_t master = needs_master ? 4 * count : 0;
+    switch (kind) {
+      case MCO_ADAMW: *out = 8 * count + master; return;
+      case MCO_LION: *out = 4 * count + master; return;
+      case MCO_ADAN: *out = 12 * count + master; return;
+      case MCO_SOPHIA: *out = 8 * count + master; return;
+      case MCO_LOMO: *out = 0; return;
+      case MCO_ADALOMO: {
+        if (nshapes == 0 && count > 0)
+          throw Error(MCO_CONFIG,
+                      "state_bytes: adalomo needs parameter shapes for factored accounting");
+        uint64_t bytes = 0;
+        const int64_t* d = dims;
+        for (int k = 0; k < nshapes; ++k) {
+          if (ndims[k] == 2) {
+            bytes += static_cast<uint64_t>(d[0] + d[1]) * 4;
+          } else {
+            int64_t n = 1;
+            for (int j = 0; j < ndims[k]; ++j) n *= d[j];
+            bytes += static_cast<uint64_t>(n) * 4;
+          }
+          d += ndims[k];
+        }
+        *out = bytes;
+        return;
+      }
+    }
+    throw Error(MCO_CONFIG, "state_bytes: unknown optimizer kind");
+  });
+}
+
+// ---- FlatOptimizer ---------------------------------------------------------------
+// optim.cpp:74-98
+mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device,
+                           int state_dtype, mco_flat** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (fused(cfg->kind))
+      throw Error(MCO_CONTRACT, "FlatOptimizer: " + kind_str(cfg->kind) +
+                                    " is a fused optimizer and keeps no flat state");
+    kind_str(cfg->kind);
+    if (state_dtype != MCO_F32 && state_dtype != MCO_F64)
+      throw Error(MCO_CONTRACT, "FlatOptimizer: state dtype must be f32 or f64");
+    DeviceGuard dg(device);
+    auto h = std::make_unique<mco_flat>();
+    h->cfg = *cfg;
+    h->n = owned_len;
+    h->device = device;
+    h->state_dtype = state_dtype;
+    // slots s0..s3 and the reference's buffers() names / order (optim.cpp:173-181)
+    const char* names[4] = {nullptr, nullptr, nullptr, nullptr};
+    int nslots = 0;
+    switch (cfg->kind) {
+      case MCO_ADAMW: names[0] = "m"; names[1] = "v"; nslots = 2; break;
+      case MCO_LION: names[0] = "m"; nslots = 1; break;
+      case MCO_ADAN: names[0] = "m"; names[1] = "v"; names[2] = "n"; names[3] = "g_prev";
+        nslots = 4; break;
+      case MCO_SOPHIA: names[0] = "m"; names[1] = "h"; nslots = 2; break;
+    }
+    const size_t bytes = std::max<uint64_t>(owned_len, 1) * dtype_size(state_dtype);
+    for (int i = 0; i < nslots; ++i) {
+      MCO_CUDA_CHECK(cudaMalloc(&h->slot[i], bytes));
+      MCO_CUDA_CHECK(cudaMemset(h->slot[i], 0, bytes));
+      h->named.emplace_back(names[i], h->slot[i]);
+    }
+    *out = h.release();
+  });
+}
+
+mco_status mco_flat_destroy(mco_flat* h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard dg(h->device);
+    delete h;
+  });
+}
+
+namespace {
+void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
+  if (np != ng)  // optim.cpp:101-103
+    throw Error(MCO_CONTRACT, "optimizer step: params/grads length mismatch: " +
+                                  std::to_string(np) + " vs " + std::to_string(ng));
+  if (np > h->n)
+    throw Error(MCO_CONTRACT, "optimizer step: " + std::to_string(np) +
+                                  " elements exceed the owned state of " + std::to_string(h->n));
+}
+
+void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
+                 uint64_t n, uint64_t state_off, double lr, cudaStream_t st) {
+  FlatArgs a{};
+  a.kind = h->cfg.kind;
+  a.state_dtype = h->state_dtype;
+  a.p = p;
+  a.p_dtype = pdt;
+  a.g = g;
+  a.g_dtype = gdt;
+  const size_t es = dtype_size(h->state_dtype);
+  for (int i = 0; i < 4; ++i) a.s[i] = h->slot[i] ? (char*)h->slot[i] + state_off * es : nullptr;
+  a.p_out_bf16 = pout;
+  a.n = n;
+  const auto kf = make_consts<float>(h->cfg, h->t, lr);
+  const auto kd = make_consts<double>(h->cfg, h->t, lr);
+  launch_flat_step(a, kf, kd, st);
+}
+
+void check_dtypes(const mco_flat* h, int pdt, int gdt) {
+  if (h->state_dtype == MCO_F64) {
+    if (pdt != MCO_F64 || gdt != MCO_F64)
+      throw Error(MCO_CONTRACT, "optimizer step: f64 state takes f64 params and grads");
+  } else if (pdt != MCO_F32 || (gdt != MCO_F32 && gdt != MCO_BF16)) {
+    throw Error(MCO_CONTRACT, "optimizer step: f32 state takes f32 params and f32/bf16 grads");
+  }
+}
+}  // namespace
+
+// optim.cpp:100-112
+mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
+                         int gdt, uint64_t ng, double lr, void* stream) {
+  return guard([&] {
+    check_lengths(h, np, ng);
+    check_dtypes(h, pdt, gdt);
+    DeviceGuard dg(h->device);
+    ++h->t;  // optim.cpp:104
+    flat_launch(h, params, pdt, grads, gdt, nullptr, np, 0, lr, (cudaStream_t)stream);
+  });
+}
+
+mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, int gdt,
+                               uint16_t* pout, uint64_t n, double lr, void* stream) {
+  return guard([&] {
+    check_lengths(h, n, n);
+    check_dtypes(h, MCO_F32, gdt);
+    if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
+    if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
+    DeviceGuard dg(h->device);
+    ++h->t;
+    flat_launch(h, master, MCO_F32, grads, gdt, pout, n, 0, lr, (cudaStream_t)stream);
+  });
+}
+
+// Host-span overload: pipelined H2D(p,g) -> step -> D2H(p) over chunks on two
+// streams, so PCIe traffic in both directions overlaps the kernels.
+mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
+                              int gdt, uint64_t ng, double lr) {
+  return guard([&] {
+    check_lengths(h, np, ng);
+    check_dtypes(h, pdt, gdt);
+    DeviceGuard dg(h->device);
+    const size_t ps = dtype_size(pdt), gs = dtype_size(gdt);
+    if (!h->hs[0]) {
+      h->hchunk = std::min<uint64_t>(std::max<uint64_t>(h->n, 1), 1ull << 24);  // 16 Mi elements
+      for (int i = 0; i < 2; ++i) {
+        MCO_CUDA_CHECK(cudaStreamCreateWithFlags(&h->hs[i], cudaStreamNonBlocking));
+        MCO_CUDA_CHECK(cudaMalloc(&h->hbuf[i][0], h->hchunk * 8));
+        MCO_CUDA_CHECK(cudaMalloc(&h->hbuf[i][1], h->hchunk * 8));
+      }
+    }
+    ++h->t;
+    const uint64_t C = h->hchunk;
+    int k = 0;
+    for (uint64_t off = 0; off < np; off += C, k ^= 1) {
+      const uint64_t n = std::min(C, np - off);
+      cudaStream_t st = h->hs[k];
+      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hbuf[k][0], (const char*)params + off * ps, n * ps,
+                                     cudaMemcpyHostToDevice, st));
+      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hbuf[k][1], (const char*)grads + off * gs, n * gs,
+                                     cudaMemcpyHostToDevice, st));
+      flat_launch(h, h->hbuf[k][0], pdt, h->hbuf[k][1], gdt, nullptr, n, off, lr, st);
+      MCO_CUDA_CHECK(cudaMemcpyAsync((char*)params + off * ps, h->hbuf[k][0], n * ps,
+                                     cudaMemcpyDeviceToHost, st));
+    }
+    MCO_CUDA_CHECK(cudaStreamSynchronize(h->hs[0]));
+    MCO_CUDA_CHECK(cudaStreamSynchronize(h->hs[1]));
+  });
+}
+
+mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t) {
+  return guard([&] { *t = h->t; });
+}
+mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
+  return guard([&] { h->t = t; });
+}
+mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out) {
+  return guard([&] { *out = h->named.size() * h->n * dtype_size(h->state_dtype); });
+}
+mco_status mco_flat_config(const mco_flat* h, mco_config* out) {
+  return guard([&] { *out = h->cfg; });
+}
+mco_status mco_flat_num_buffers(const mco_flat* h, int* out) {
+  return guard([&] { *out = (int)h->named.size(); });
+}
+mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, uint64_t* len,
+                           int* dtype) {
+  return guard([&] {
+    if (i < 0 || i >= (int)h->named.size())
+      throw Error(MCO_CONTRACT, "buffers(): index out of range");
+    *name = h->named[i].first;
+    *ptr = h->named[i].second;
+    *len = h->n;
+    *dtype = h->state_dtype;
+  });
+}
+
+// ---- LOMO -------------------------------------------------------------------------
+mco_status mco_lomo_apply(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                          double scale, void* stream) {
+  return guard([&] { launch_lomo(p, pdt, g, gdt, n, lr, scale, nullptr, 0.0, (cudaStream_t)stream); });
+}
+
+mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                                  const double* dev_sumsq, double clip, void* stream) {
+  return guard([&] {
+    if (!dev_sumsq) throw Error(MCO_CONTRACT, "lomo clip: device sum of squares is null");
+    launch_lomo(p, pdt, g, gdt, n, lr, 1.0, dev_sumsq, clip, (cudaStream_t)stream);
+  });
+}
+
+mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* out, int accumulate,
+                     void* stream) {
+  return guard([&] {
+    dtype_size(dtype);
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_sumsq(x, dtype, n, out, accumulate, sumsq_ws(st), st);
+  });
+}
+
+// ---- AdaLomo ----------------------------------------------------------------------
+// optim.cpp:192-207
+mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* ndims,
+                              const int64_t* dims, int device, mco_adalomo** out) {
+  return guard([&] {
+    *out = nullptr;
+    DeviceGuard dg(device);
+    auto h = std::make_unique<mco_adalomo>();
+    auto& pl = h->plan;
+    pl.cfg = *cfg;
+    pl.device = device;
+    std::vector<std::vector<int64_t>> shapes;
+    const int64_t* d = dims;
+    for (int k = 0; k < ntensors; ++k) {
+      shapes.emplace_back(d, d + ndims[k]);
+      d += ndims[k];
+    }
+    build_adalomo_plan(pl, shapes, device_info(device).sms);
+    auto alloc = [](auto** p, size_t count, size_t esz) {
+      MCO_CUDA_CHECK(cudaMalloc((void**)p, std::max<size_t>(count, 1) * esz));
+      MCO_CUDA_CHECK(cudaMemset(*p, 0, std::max<size_t>(count, 1) * esz));
+    };
+    alloc(&pl.d_tiles, pl.h_tiles.size(), sizeof(Tile));
+    alloc(&pl.d_tensors, pl.h_tensors.size(), sizeof(TensorInfo));
+    alloc(&pl.d_item_off, pl.h_item_off.size(), sizeof(int64_t));
+    alloc(&pl.d_state, pl.state_len, sizeof(double));
+    alloc(&pl.d_colpart, pl.colpart_len, sizeof(float));
+    alloc(&pl.d_rowpart, pl.rowpart_len, sizeof(double));
+    alloc(&pl.d_tile_sc, pl.h_tiles.size() * 4, sizeof(double));
+    alloc(&pl.d_tens_sc, pl.h_tensors.size() * 8, sizeof(double));
+    alloc(&pl.d_fa, pl.fa_len, sizeof(float));
+    alloc(&pl.d_fb, pl.fb_len, sizeof(float));
+    alloc(&pl.d_glob, 4, sizeof(double));
+    MCO_CUDA_CHECK(cudaMemcpy(pl.d_tiles, pl.h_tiles.data(), pl.h_tiles.size() * sizeof(Tile),
+                              cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(pl.d_tensors, pl.h_tensors.data(),
+                              pl.h_tensors.size() * sizeof(TensorInfo), cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(pl.d_item_off, pl.h_item_off.data(),
+                              pl.h_item_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    *out = h.release();
+  });
+}
+
+mco_status mco_adalomo_destroy(mco_adalomo* h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard dg(h->plan.device);
+    delete h;
+  });
+}
+
+namespace {
+void check_ada_dtypes(int pdt, int gdt) {
+  if (pdt != MCO_F32 || (gdt != MCO_F32 && gdt != MCO_BF16))
+    throw Error(MCO_CONTRACT, "adalomo: params must be f32 and grads f32 or bf16");
+}
+}  // namespace
+
+// optim.cpp:215-275 (hook form: one tensor)
+mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, const void* grad,
+                             int gdt, double lr, const double* dev_grad_sumsq, void* stream) {
+  return guard([&] {
+    if (idx < 0 || idx >= (int)h->plan.h_tensors.size())  // optim.cpp:212
+      throw Error(MCO_CONTRACT, "adalomo: unknown parameter '" + std::to_string(idx) + "'");
+    check_ada_dtypes(pdt, gdt);
+    DeviceGuard dg(h->plan.device);
+    AdaLomoCall c{};
+    c.t0 = idx;
+    c.t1 = idx + 1;
+    c.p = param;
+    c.g = grad;
+    c.g_dtype = gdt;
+    c.single = 1;
+    c.lr = lr;
+    c.use_clip = (dev_grad_sumsq != nullptr && h->plan.cfg.has_clip_threshold) ? 1 : 0;
+    c.ext_sumsq = dev_grad_sumsq;
+    launch_adalomo(h->plan, c, (cudaStream_t)stream);
+    h->plan.h_tensors[idx].t += 1;
+  });
+}
+
+mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const void* flat_g,
+                                 int gdt, double lr, void* stream) {
+  return guard([&] {
+    check_ada_dtypes(pdt, gdt);
+    DeviceGuard dg(h->plan.device);
+    AdaLomoCall c{};
+    c.t0 = 0;
+    c.t1 = (int)h->plan.h_tensors.size();
+    c.p = flat_p;
+    c.g = flat_g;
+    c.g_dtype = gdt;
+    c.single = 0;
+    c.lr = lr;
+    c.use_clip = h->plan.cfg.has_clip_threshold ? 1 : 0;
+    c.ext_sumsq = nullptr;
+    launch_adalomo(h->plan, c, (cudaStream_t)stream);
+    for (auto& T : h->plan.h_tensors) T.t += 1;
+  });
+}
+
+// optim.cpp:277-282 (fp64 state, as the reference)
+mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out) {
+  return guard([&] { *out = (uint64_t)h->plan.state_len * sizeof(double); });
+}
+
+mco_status mco_adalomo_get_steps(const mco_adalomo* h, int idx, int64_t* t) {
+  return guard([&] {
+    if (idx < 0 || idx >= (int)h->plan.h_tensors.size())
+      throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
+    *t = h->plan.h_tensors[idx].t;
+  });
+}
+
+mco_status mco_adalomo_buffer(mco_adalomo* h, int idx, int which, void** ptr, uint64_t* len) {
+  return guard([&] {
+    if (idx < 0 || idx >= (int)h->plan.h_tensors.size())
+      throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
+    const TensorInfo& T = h->plan.h_tensors[idx];
+    int64_t off = -1, n = 0;
+    if (which == 0 && T.factored) off = T.vrow_off, n = T.rows;
+    if (which == 1 && T.factored) off = T.vcol_off, n = T.cols;
+    if (which == 2 && !T.factored) off = T.vfull_off, n = T.numel;
+    *ptr = off >= 0 ? (void*)(h->plan.d_state + off) : nullptr;
+    *len = (uint64_t)n;
+  });
+}
+
+// ---- ZeroPlan (parallel.cpp:20-34) -------------------------------------------------
+mco_status mco_zero_plan(uint64_t total, int dp, int stage, uint64_t* part_sizes,
+                         uint64_t* offsets) {
+  return guard([&] {
+    if (dp < 1) throw Error(MCO_CONFIG, "zero plan: dp_size must be >= 1");
+    if (stage < 0 || stage > 3) throw Error(MCO_CONFIG, "zero plan: stage must be in 0..3");
+    const uint64_t q = total / (uint64_t)dp, r = total % (uint64_t)dp;
+    offsets[0] = 0;
+    for (int i = 0; i < dp; ++i) {
+      part_sizes[i] = q + ((uint64_t)i < r ? 1 : 0);  // ceil split, trailing smaller
+      offsets[i + 1] = offsets[i] + part_sizes[i];
+    }
+  });
+}
+
+// ---- synthetic inputs --------------------------------------------------------------
+mco_status mco_synth_fill(void* dst, int dtype, uint64_t n, uint64_t seed, uint32_t role,
+                          uint32_t tensor, uint32_t step, int64_t cols, int scale_log2,
+                          int zero_log2, int rowcol, void* stream) {
+  return guard([&] {
+    dtype_size(dtype);
+    launch_synth(dst, dtype, n, synth_key(seed, role, tensor, step), cols, scale_log2, zero_log2,
+                 rowcol, (cudaStream_t)stream);
+  });
+}
+
+mco_status mco_sync(void* stream) {
+  return guard([&] { MCO_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream)); });
+}
+
+mco_status mco_device_count(int* out) {
+  return guard([&] {
+    *out = 0;
+    const cudaError_t e = cudaGetDeviceCount(out);
+    if (e != cudaSuccess) {
+      *out = 0;
+      cudaGetLastError();
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,604 @@
+// AdaLomo for sm_100a (optim.cpp:192-282): factored row/column second moment,
+// RMS(theta)-scaled lr, update-RMS damping, optional global grad-norm clip.
+//
+// The reference's six sequential passes per tensor (optim.cpp:223-274, with a
+// stride-C column loop and a full-size temporary u) become three streaming
+// passes over HBM plus three small finalisation kernels.  The dependency chain
+// forces them: column statistics need every row before any u exists, and the
+// damping needs sum(u^2) over the whole tensor before any parameter moves.
+//
+//   K1 stats   (tiles)   : per row sum g^2 (row partials), per column partial
+//                          sums over the tile's rows, sum p^2, sum v_row_old
+//   K2 scalars (1 CTA)   : per tensor sum g^2, sum p^2 -> global clip scale s,
+//                          t += 1, corr, rms_theta, lr_t, row_mean (linearity)
+//   K3 moments (items)   : v_row / v_col EMAs (fp64 state) and the fp32
+//                          factors a_i = v_row_i/corr, b_j = (v_col_j/corr)/row_mean
+//   K4 sum u^2 (tiles)   : u = s*g / sqrt(a_i*b_j + eps); 1-D tensors update v_full
+//   K5 damping (1 CTA)   : f = lr_t / max(1, rms_u / adalomo_clip)
+//   K6 update  (tiles)   : p -= f * u  (u recomputed bit-identically to K4)
+//
+// Work unit = tile: rows [r0,r1) x columns [c0,c1) of one matrix (or an
+// element range of a 1-D tensor), one CTA per tile, persistent grid over the
+// tile table.  Threads: TR row groups x TC column lanes, one 8-wide (32 B)
+// column chunk per lane, so every warp reads a contiguous 1 KB row segment.
+// All reductions are fixed-order (no float atomics): results are
+// bit-reproducible run to run.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "adalomo.h"
+
+namespace mco {
+namespace {
+
+constexpr int kThreads = 256;
+
+struct Ctx {
+  const Tile* tiles;
+  const TensorInfo* tensors;
+  double* state;      // fp64 v_row / v_col / v_full
+  float* colpart;     // [nrb][C] per factored tensor
+  double* rowpart;    // [kc][R]  per factored tensor
+  double* tile_sc;    // 4 doubles per tile: psq, gsq, vrs, usq
+  double* tens_sc;    // kTensScalars per tensor
+  float* fa;          // a_i per factored tensor row
+  float* fb;          // b_j per factored tensor column
+  double* glob;       // [0] = clip scale s, [1] = global sum g^2
+};
+
+enum { TS_GSQ = 0, TS_PSQ, TS_VRS, TS_CORR, TS_LRT, TS_ROWMEAN, TS_USQ, TS_F, kTensScalars };
+
+template <typename GT>
+__device__ __forceinline__ void load8(const GT* g, float (&r)[8]);
+template <>
+__device__ __forceinline__ void load8<float>(const float* g, float (&r)[8]) {
+  ld_keep_ro(g, r);
+}
+template <>
+__device__ __forceinline__ void load8<uint16_t>(const uint16_t* g, float (&r)[8]) {
+  ld_stream_ro_bf16x8(g, r);
+}
+__device__ __forceinline__ float ld1(const float* g) { return *g; }
+__device__ __forceinline__ float ld1(const uint16_t* g) { return bf2f(*g); }
+
+// A lane's column chunk is always kCW = 8 columns; VEC selects one 256-bit
+// (f32) / 128-bit (bf16) access or 8 scalar accesses (unaligned rows).
+constexpr int VW = kCW;
+template <bool VEC, typename GT>
+__device__ __forceinline__ void load_vec(const GT* g, float (&r)[VW], int valid) {
+  if constexpr (VEC) {
+    if (valid == VW) {
+      load8<GT>(g, r);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < VW; ++j) r[j] = j < valid ? ld1(g + j) : 0.f;
+}
+template <bool VEC>
+__device__ __forceinline__ void load_p(const float* p, float (&r)[VW], int valid) {
+  if constexpr (VEC) {
+    if (valid == VW) {
+      ld_stream(p, r);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < VW; ++j) r[j] = j < valid ? p[j] : 0.f;
+}
+template <bool VEC>
+__device__ __forceinline__ void store_p(float* p, const float (&r)[VW], int valid) {
+  if constexpr (VEC) {
+    if (valid == VW) {
+      st_stream(p, r);
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < VW; ++j)
+    if (j < valid) p[j] = r[j];
+}
+
+struct Ptrs {
+  float* p;
+  const void* g;
+  int single;  // 1: p / g point at the call's only tensor
+};
+template <typename GT>
+__device__ __forceinline__ const GT* gptr(const Ptrs& P, const TensorInfo& T) {
+  return (const GT*)P.g + (P.single ? 0 : T.elem_off);
+}
+__device__ __forceinline__ float* pptr(const Ptrs& P, const TensorInfo& T) {
+  return P.p + (P.single ? 0 : T.elem_off);
+}
+
+// ============================ K1: statistics =====================================
+template <bool VEC, typename GT>
+__global__ void __launch_bounds__(kThreads)
+    k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles) {
+  __shared__ float colbuf[kThreads * VW];
+  __shared__ float rowbuf[kMaxTileRows * 4];
+  __shared__ double scratch[32];
+  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const Tile tl = c.tiles[tile0 + ti];
+    const TensorInfo T = c.tensors[tl.tensor];
+    const GT* g = gptr<GT>(P, T);
+    const float* p = pptr(P, T);
+    double psq = 0.0, gsq = 0.0;
+    if (T.factored) {
+      const int TC = T.tc, TR = kThreads / T.tc;
+      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
+      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
+      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      const int wrow = (threadIdx.x % TC) >> 5;  // warp index within the row group
+      const int nwr = TC >> 5;
+      float cacc[VW];
+#pragma unroll
+      for (int j = 0; j < VW; ++j) cacc[j] = 0.f;
+      for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
+        float gv[VW], pv[VW];
+        if (valid > 0) {
+          load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
+          load_p<VEC>(p + r * T.cols + col, pv, valid);
+        } else {
+#pragma unroll
+          for (int j = 0; j < VW; ++j) gv[j] = pv[j] = 0.f;
+        }
+        float sg = 0.f, sp = 0.f;
+#pragma unroll
+        for (int j = 0; j < VW; ++j) {
+          const float g2 = gv[j] * gv[j];
+          cacc[j] += g2;
+          sg += g2;
+          sp += pv[j] * pv[j];
+        }
+        psq += (double)sp;
+        sg = warp_sum(sg);  // a warp never straddles two rows (TC >= 32)
+        if ((threadIdx.x & 31) == 0) rowbuf[(r - tl.r0) * nwr + wrow] = sg;
+      }
+      // column partials: fixed-order sum over the TR row groups
+#pragma unroll
+      for (int j = 0; j < VW; ++j) colbuf[(tr * TC + lane_c) * VW + j] = cacc[j];
+      __syncthreads();
+      const int64_t w = tl.c1 - tl.c0;
+      for (int64_t q = threadIdx.x; q < w; q += kThreads) {
+        const int lc = (int)(q / VW), j = (int)(q % VW);
+        float s = 0.f;
+        for (int k = 0; k < TR; ++k) s += colbuf[(k * TC + lc) * VW + j];
+        c.colpart[T.colpart_off + tl.rb * T.cols + tl.c0 + q] = s;
+      }
+      // row partials
+      const int64_t h = tl.r1 - tl.r0;
+      double vrs = 0.0;
+      for (int64_t i = threadIdx.x; i < h; i += kThreads) {
+        double s = 0.0;
+        for (int k = 0; k < nwr; ++k) s += (double)rowbuf[i * nwr + k];
+        c.rowpart[T.rowpart_off + (int64_t)tl.cb * T.rows + tl.r0 + i] = s;
+        gsq += s;
+        if (tl.cb == 0) vrs += c.state[T.vrow_off + tl.r0 + i];
+      }
+      const double bps = block_sum(psq, scratch);
+      const double bgs = block_sum(gsq, scratch);
+      const double bvr = block_sum(vrs, scratch);
+      if (threadIdx.x == 0) {
+        c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
+        c.tile_sc[(tile0 + ti) * 4 + 1] = bgs;
+        c.tile_sc[(tile0 + ti) * 4 + 2] = bvr;
+      }
+      __syncthreads();  // colbuf / rowbuf reuse by the next tile
+    } else {
+      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+        const double gv = (double)ld1(g + e), pv = (double)p[e];
+        gsq += gv * gv;
+        psq += pv * pv;
+      }
+      const double bps = block_sum(psq, scratch);
+      const double bgs = block_sum(gsq, scratch);
+      if (threadIdx.x == 0) {
+        c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
+        c.tile_sc[(tile0 + ti) * 4 + 1] = bgs;
+        c.tile_sc[(tile0 + ti) * 4 + 2] = 0.0;
+      }
+    }
+  }
+}
+
+// ============================ K2: per-tensor scalars ===============================
+// One CTA of 1024 threads.  Warp w handles tensors w, w+32, ...; tile sums are
+// lane-strided + butterfly (fixed order).  Then the global sum of g^2 over the
+// call's tensors in tensor order, the clip scale, and the per-tensor scalars.
+__global__ void __launch_bounds__(1024)
+    k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
+               const double* ext_sumsq) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = t0 + warp; k < t1; k += 32) {
+    const TensorInfo T = c.tensors[k];
+    double ps = 0, gs = 0, vr = 0;
+    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) {
+      ps += c.tile_sc[i * 4 + 0];
+      gs += c.tile_sc[i * 4 + 1];
+      vr += c.tile_sc[i * 4 + 2];
+    }
+    ps = warp_sum(ps);
+    gs = warp_sum(gs);
+    vr = warp_sum(vr);
+    if (lane == 0) {
+      c.tens_sc[k * kTensScalars + TS_PSQ] = ps;
+      c.tens_sc[k * kTensScalars + TS_GSQ] = gs;
+      c.tens_sc[k * kTensScalars + TS_VRS] = vr;
+    }
+  }
+  __syncthreads();
+  double G = 0;
+  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) G += c.tens_sc[k * kTensScalars + TS_GSQ];
+  G = block_sum(G, red);
+  if (threadIdx.x == 0) {
+    double s = 1.0;
+    if (use_clip) {  // optim.cpp:302-303 rule on the global norm
+      const double sumsq = ext_sumsq ? *ext_sumsq : G;
+      const double norm = sqrt(sumsq);
+      if (norm > clip && norm > 0) s = clip / norm;
+    }
+    c.glob[0] = s;
+    c.glob[1] = G;
+  }
+  __syncthreads();
+  const double s = c.glob[0];
+  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
+    TensorInfo* Tm = const_cast<TensorInfo*>(&c.tensors[k]);
+    const TensorInfo T = *Tm;
+    const int64_t t = T.t + 1;  // optim.cpp:219
+    Tm->t = t;
+    const double corr = 1.0 - pow(b2, (double)t);
+    const double n = (double)T.numel;
+    const double rms_theta = sqrt(c.tens_sc[k * kTensScalars + TS_PSQ] / n);
+    const double lr_t = lr * fmax(1e-3, rms_theta);
+    double row_mean = 0.0;
+    if (T.factored) {  // mean of the new v_row, by linearity of the EMA
+      const double gsq = s * s * c.tens_sc[k * kTensScalars + TS_GSQ];
+      const double sum_new =
+          b2 * c.tens_sc[k * kTensScalars + TS_VRS] + (1 - b2) * (gsq / (double)T.cols);
+      row_mean = sum_new / ((double)T.rows * corr);
+    }
+    c.tens_sc[k * kTensScalars + TS_CORR] = corr;
+    c.tens_sc[k * kTensScalars + TS_LRT] = lr_t;
+    c.tens_sc[k * kTensScalars + TS_ROWMEAN] = row_mean;
+  }
+}
+
+// ============================ K3: moments ============================================
+// Item space: for each factored tensor in [t0,t1): rows then columns.
+__global__ void __launch_bounds__(kThreads)
+    k3_moments(Ctx c, int t0, int t1, const int64_t* __restrict__ item_off, int64_t item0,
+               int64_t nitems, double b2) {
+  const double s = c.glob[0], s2 = s * s;
+  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nitems;
+       it += (int64_t)gridDim.x * blockDim.x) {
+    // binary search the tensor owning this item
+    const int64_t gi = item0 + it;
+    int lo = t0, hi = t1 - 1;  // largest k with item_off[k] <= gi
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (item_off[mid] <= gi)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const TensorInfo T = c.tensors[lo];
+    const int64_t local = gi - item_off[lo];
+    const double corr = c.tens_sc[lo * kTensScalars + TS_CORR];
+    if (local < T.rows) {  // row i: optim.cpp:239-240
+      const int64_t i = local;
+      double acc = 0.0;
+      for (int k = 0; k < T.kc; ++k) acc += c.rowpart[T.rowpart_off + (int64_t)k * T.rows + i];
+      double& vr = c.state[T.vrow_off + i];
+      vr = b2 * vr + (1 - b2) * (s2 * acc / (double)T.cols);
+      c.fa[T.fa_off + i] = (float)(vr / corr);
+    } else {  // column j: optim.cpp:247-248
+      const int64_t j = local - T.rows;
+      double acc = 0.0;
+      for (int64_t rb = 0; rb < T.nrb; ++rb)
+        acc += (double)c.colpart[T.colpart_off + rb * T.cols + j];
+      double& vc = c.state[T.vcol_off + j];
+      vc = b2 * vc + (1 - b2) * (s2 * acc / (double)T.rows);
+      const double rm = c.tens_sc[lo * kTensScalars + TS_ROWMEAN];
+      c.fb[T.fb_off + j] = (float)((vc / corr) / fmax(rm, 1e-300));
+    }
+  }
+}
+
+// u for a factored element: u = (s*g) / sqrt(a_i*b_j + eps)   (optim.cpp:256-259)
+__device__ __forceinline__ float u_fact(float g, float s, float a, float b, float eps) {
+  const float gs = s * g;
+  return gs / sqrtf(a * b + eps);
+}
+
+// ============================ K4: sum u^2 ============================================
+template <bool VEC, typename GT>
+__global__ void __launch_bounds__(kThreads)
+    k4_usq(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double b2, double eps) {
+  __shared__ double scratch[32];
+  const float sf = (float)c.glob[0], epsf = (float)eps;
+  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const Tile tl = c.tiles[tile0 + ti];
+    const TensorInfo T = c.tensors[tl.tensor];
+    const GT* g = gptr<GT>(P, T);
+    double usq = 0.0;
+    if (T.factored) {
+      const int TC = T.tc, TR = kThreads / T.tc;
+      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
+      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
+      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      if (valid > 0) {
+        float bv[VW];
+#pragma unroll
+        for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
+        for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
+          float gv[VW];
+          load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
+          const float a = c.fa[T.fa_off + r];
+          float su = 0.f;
+#pragma unroll
+          for (int j = 0; j < VW; ++j) {
+            const float u = u_fact(gv[j], sf, a, bv[j], epsf);
+            su += j < valid ? u * u : 0.f;
+          }
+          usq += (double)su;
+        }
+      }
+    } else {  // optim.cpp:262-267 with fp64 state
+      const double s = c.glob[0];
+      const double corr = c.tens_sc[tl.tensor * kTensScalars + TS_CORR];
+      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+        const double gs = s * (double)ld1(g + e);
+        double& v = c.state[T.vfull_off + e];
+        v = b2 * v + (1 - b2) * gs * gs;
+        const double u = gs / sqrt(v / corr + eps);
+        usq += u * u;
+      }
+    }
+    const double b = block_sum(usq, scratch);
+    if (threadIdx.x == 0) c.tile_sc[(tile0 + ti) * 4 + 3] = b;
+  }
+}
+
+// ============================ K5: damping ==============================================
+__global__ void __launch_bounds__(1024)
+    k5_damp(Ctx c, int t0, int t1, double adalomo_clip) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = t0 + warp; k < t1; k += 32) {
+    const TensorInfo T = c.tensors[k];
+    double us = 0;
+    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += c.tile_sc[i * 4 + 3];
+    us = warp_sum(us);
+    if (lane == 0) {  // optim.cpp:269-273
+      const double rms_u = sqrt(us / (double)T.numel);
+      const double damp = fmax(1.0, rms_u / adalomo_clip);
+      c.tens_sc[k * kTensScalars + TS_USQ] = us;
+      c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
+    }
+  }
+}
+
+// ============================ K6: update ==============================================
+template <bool VEC, typename GT>
+__global__ void __launch_bounds__(kThreads)
+    k6_update(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
+  const float sf = (float)c.glob[0], epsf = (float)eps;
+  // reverse tile order: the tail of K4's gradient reads is still L2-resident
+  for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
+    const int64_t ti = ntiles - 1 - k;
+    const Tile tl = c.tiles[tile0 + ti];
+    const TensorInfo T = c.tensors[tl.tensor];
+    const GT* g = gptr<GT>(P, T);
+    float* p = pptr(P, T);
+    const double f = c.tens_sc[tl.tensor * kTensScalars + TS_F];
+    if (T.factored) {
+      const float ff = (float)f;
+      const int TC = T.tc, TR = kThreads / T.tc;
+      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
+      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
+      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      if (valid <= 0) continue;
+      float bv[VW];
+#pragma unroll
+      for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
+      for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
+        float gv[VW], pv[VW];
+        load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
+        load_p<VEC>(p + r * T.cols + col, pv, valid);
+        const float a = c.fa[T.fa_off + r];
+#pragma unroll
+        for (int j = 0; j < VW; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
+        store_p<VEC>(p + r * T.cols + col, pv, valid);
+      }
+    } else {
+      const double s = c.glob[0];
+      const double corr = c.tens_sc[tl.tensor * kTensScalars + TS_CORR];
+      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+        const double gs = s * (double)ld1(g + e);
+        const double u = gs / sqrt(c.state[T.vfull_off + e] / corr + eps);
+        p[e] = (float)((double)p[e] - f * u);
+      }
+    }
+  }
+}
+
+template <typename K>
+int grid_for(K kernel, int64_t ntiles, int device) {
+  int per_sm = 0;
+  MCO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+  per_sm = std::max(per_sm, 1);
+  const int64_t full = (int64_t)device_info(device).sms * per_sm;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(full, ntiles));
+}
+
+template <bool VEC, typename GT>
+void run_passes(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
+  Ctx c{pl.d_tiles,  pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
+        pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,   pl.d_fb,      pl.d_glob};
+  Ptrs P{(float*)call.p, call.g, call.single};
+  const int dev = current_device();
+  const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
+  const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
+  const auto& cfg = pl.cfg;
+
+  auto kk1 = k1_stats<VEC, GT>;
+  kk1<<<grid_for(kk1, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles);
+  launch_check("adalomo k1_stats");
+
+  k2_scalars<<<1, 1024, 0, st>>>(c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
+                                 cfg.clip_threshold, call.ext_sumsq);
+  launch_check("adalomo k2_scalars");
+
+  const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
+  if (nitems > 0) {
+    const int64_t blocks =
+        std::min<int64_t>((nitems + kThreads - 1) / kThreads, (int64_t)device_info(dev).sms * 8);
+    k3_moments<<<(unsigned)blocks, kThreads, 0, st>>>(
+        c, call.t0, call.t1, pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
+    launch_check("adalomo k3_moments");
+  }
+
+  auto kk4 = k4_usq<VEC, GT>;
+  kk4<<<grid_for(kk4, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.beta2, cfg.eps);
+  launch_check("adalomo k4_usq");
+
+  k5_damp<<<1, 1024, 0, st>>>(c, call.t0, call.t1, cfg.adalomo_clip);
+  launch_check("adalomo k5_damp");
+
+  auto kk6 = k6_update<VEC, GT>;
+  kk6<<<grid_for(kk6, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.eps);
+  launch_check("adalomo k6_update");
+}
+
+}  // namespace
+
+void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
+  if (call.t1 <= call.t0) return;
+  // 8-wide path: every factored tensor in the call has C % 8 == 0 and 32 B
+  // (f32) / 16 B (bf16) aligned rows.
+  const size_t gsz = call.g_dtype == MCO_BF16 ? 2 : 4;
+  bool vec = true;
+  for (int k = call.t0; k < call.t1 && vec; ++k) {
+    const TensorInfo& T = pl.h_tensors[k];
+    if (!T.factored) continue;
+    const int64_t off = call.single ? 0 : T.elem_off;
+    vec = (T.cols % 8 == 0) && (((uintptr_t)call.p + off * 4) % 32 == 0) &&
+          (((uintptr_t)call.g + off * gsz) % (8 * gsz) == 0);
+  }
+  if (call.g_dtype == MCO_F32) {
+    if (vec)
+      run_passes<true, float>(pl, call, st);
+    else
+      run_passes<false, float>(pl, call, st);
+  } else if (call.g_dtype == MCO_BF16) {
+    if (vec)
+      run_passes<true, uint16_t>(pl, call, st);
+    else
+      run_passes<false, uint16_t>(pl, call, st);
+  } else {
+    throw Error(MCO_CONTRACT, "adalomo: grads must be f32 or bf16");
+  }
+}
+
+}  // namespace mco
+
+namespace mco {
+
+// ---- host: tile plan ------------------------------------------------------------
+// Per matrix R x C: column blocks of w = min(C, 1024) columns (TC lanes x 8),
+// row blocks of h <= 128 rows; h is halved (down to 8) until one tensor alone
+// yields >= 2 tiles per SM, so the per-tensor hook form also fills the GPU.
+// Column partials cost ceil(R/h)*C floats per tensor (written once, read once).
+void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>& shapes,
+                        int sms) {
+  pl.h_tensors.clear();
+  pl.h_tiles.clear();
+  pl.h_item_off.assign(1, 0);
+  int64_t elem = 0, state = 0, colpart = 0, rowpart = 0, fa = 0, fb = 0;
+  const int64_t min_tiles = 2LL * sms;
+  for (size_t k = 0; k < shapes.size(); ++k) {
+    const auto& s = shapes[k];
+    TensorInfo T{};
+    int64_t numel = 1;
+    for (int64_t d : s) numel *= d;
+    T.numel = numel;
+    T.elem_off = elem;
+    T.factored = s.size() == 2 ? 1 : 0;
+    T.tile_begin = (int64_t)pl.h_tiles.size();
+    if (T.factored) {
+      T.rows = s[0];
+      T.cols = s[1];
+      const int64_t w = std::min<int64_t>(T.cols, 128 * kCW);
+      const int64_t chunks = (w + kCW - 1) / kCW;
+      int tc = 32;
+      while (tc < chunks) tc <<= 1;
+      T.tc = tc;
+      T.kc = (int32_t)((T.cols + w - 1) / w);
+      int64_t h = kMaxTileRows;
+      while (h > 8 && ((T.rows + h - 1) / h) * T.kc < min_tiles) h >>= 1;
+      h = std::min<int64_t>(h, std::max<int64_t>(T.rows, 1));
+      T.nrb = (T.rows + h - 1) / h;
+      T.vrow_off = state;
+      state += T.rows;
+      T.vcol_off = state;
+      state += T.cols;
+      T.vfull_off = -1;
+      T.colpart_off = colpart;
+      colpart += T.nrb * T.cols;
+      T.rowpart_off = rowpart;
+      rowpart += (int64_t)T.kc * T.rows;
+      T.fa_off = fa;
+      fa += T.rows;
+      T.fb_off = fb;
+      fb += T.cols;
+      for (int64_t rb = 0; rb < T.nrb; ++rb)
+        for (int cb = 0; cb < T.kc; ++cb) {
+          Tile tl{};
+          tl.tensor = (int32_t)k;
+          tl.cb = cb;
+          tl.rb = rb;
+          tl.r0 = rb * h;
+          tl.r1 = std::min(T.rows, (rb + 1) * h);
+          tl.c0 = (int64_t)cb * w;
+          tl.c1 = std::min(T.cols, ((int64_t)cb + 1) * w);
+          pl.h_tiles.push_back(tl);
+        }
+      pl.h_item_off.push_back(pl.h_item_off.back() + T.rows + T.cols);
+    } else {
+      T.rows = numel;
+      T.cols = 1;
+      T.tc = 32;
+      T.kc = 1;
+      T.nrb = 0;
+      T.vrow_off = T.vcol_off = -1;
+      T.vfull_off = state;
+      state += numel;
+      T.colpart_off = T.rowpart_off = T.fa_off = T.fb_off = -1;
+      const int64_t chunk = 1 << 16;
+      for (int64_t e0 = 0; e0 < numel || (numel == 0 && e0 == 0); e0 += chunk) {
+        Tile tl{};
+        tl.tensor = (int32_t)k;
+        tl.r0 = e0;
+        tl.r1 = std::min(numel, e0 + chunk);
+        pl.h_tiles.push_back(tl);
+        if (numel == 0) break;
+      }
+      pl.h_item_off.push_back(pl.h_item_off.back());
+    }
+    T.tile_end = (int64_t)pl.h_tiles.size();
+    T.t = 0;
+    elem += numel;
+    pl.h_tensors.push_back(T);
+  }
+  pl.state_len = state;
+  pl.colpart_len = colpart;
+  pl.rowpart_len = rowpart;
+  pl.fa_len = fa;
+  pl.fb_len = fb;
+}
+
+}  // namespace mco

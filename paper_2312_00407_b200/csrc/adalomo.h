@@ -1,0 +1,72 @@
+// AdaLomo tile plan (host) and launch interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace mco {
+
+constexpr int kCW = 8;            // columns per lane chunk
+constexpr int kMaxTileRows = 128;  // bounds fp32 column partial length and smem
+
+struct Tile {
+  int32_t tensor;
+  int32_t cb;  // column block
+  int64_t rb;  // row block
+  int64_t r0, r1, c0, c1;  // 1-D tensors: [r0, r1) is the element range
+};
+
+struct TensorInfo {
+  int64_t numel, rows, cols;
+  int32_t factored, tc;  // tc: column lanes per row group (32/64/128)
+  int32_t kc, pad0;      // column blocks
+  int64_t nrb;           // row blocks
+  int64_t elem_off;      // offset in the registry-order flat buffer
+  int64_t vrow_off, vcol_off, vfull_off;  // fp64 state offsets
+  int64_t colpart_off, rowpart_off, fa_off, fb_off;
+  int64_t tile_begin, tile_end;
+  int64_t t;  // per-entry step counter (optim.hpp:93), advanced on the device
+};
+
+struct AdaLomoPlan {
+  mco_config cfg{};
+  int device = 0;
+  std::vector<TensorInfo> h_tensors;
+  std::vector<Tile> h_tiles;
+  std::vector<int64_t> h_item_off;  // per tensor prefix of (rows + cols) for factored
+  int64_t state_len = 0, colpart_len = 0, rowpart_len = 0, fa_len = 0, fb_len = 0;
+  // device
+  Tile* d_tiles = nullptr;
+  TensorInfo* d_tensors = nullptr;
+  int64_t* d_item_off = nullptr;
+  double* d_state = nullptr;
+  float* d_colpart = nullptr;
+  double* d_rowpart = nullptr;
+  double* d_tile_sc = nullptr;
+  double* d_tens_sc = nullptr;
+  float* d_fa = nullptr;
+  float* d_fb = nullptr;
+  double* d_glob = nullptr;
+};
+
+struct AdaLomoCall {
+  int t0, t1;  // tensor range [t0, t1)
+  void* p;
+  const void* g;
+  int g_dtype;
+  int single;
+  double lr;
+  int use_clip;
+  const double* ext_sumsq;  // device global sum g^2 (hook form), or null
+};
+
+// Build the host tile plan for `shapes` (registry order) on a device with `sms` SMs.
+void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>& shapes,
+                        int sms);
+void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st);
+
+}  // namespace mco

@@ -1,0 +1,169 @@
+// Shared device helpers for the sm_100a optimizer kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "mco.h"
+
+namespace mco {
+
+// ---- host-side error plumbing ------------------------------------------------
+// Exceptions carry an mco_status; the C-ABI layer (abi.cpp) converts them.
+struct Error : std::runtime_error {
+  mco_status status;
+  Error(mco_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Error(MCO_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define MCO_CUDA_CHECK(x) ::mco::cuda_check((x), #x)
+
+// Counts our own kernel launches (bench.py reports it as gpu_launches).
+void note_launch(uint64_t n = 1);
+inline void launch_check(const char* what) {
+  note_launch();
+  cuda_check(cudaGetLastError(), what);
+}
+
+struct DeviceInfo {
+  int sms = 148;
+  int l2_bytes = 0;
+};
+const DeviceInfo& device_info(int device);
+int current_device();
+
+// ---- per-step scalars ----------------------------------------------------------
+// Derived in double on the host exactly once per step, rounded once to the
+// kernel's arithmetic type T (float or double).  Same rule as
+// oracle/mco_oracle.c's f32 functions.
+template <typename T>
+struct StepConsts {
+  T b1, b2, b3, omb1, omb2, omb3;  // beta_k and (1 - beta_k)
+  T c1, c2, c3;                    // 1 - beta_k^t
+  T lr, eps, wd, lrwd, den, rho;   // den = 1 + lr*wd (Adan), lrwd = lr*wd (Sophia)
+  int first;                       // Adan: t == 1
+  int refresh;                     // Sophia: (t-1) % k == 0
+};
+
+// ---- 256-bit global memory access (LDG.E.256 / STG.E.256 on sm_100a) ----------
+// Streaming data larger than L2 is read once: no L1 allocation, evict-first in L2.
+__device__ __forceinline__ void ld_stream(const float* p, float (&r)[8]) {
+  asm volatile(
+      "ld.global.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7])
+      : "l"(p));
+}
+// Read-only inputs (gradients) use the non-coherent path as well.
+__device__ __forceinline__ void ld_stream_ro(const float* p, float (&r)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void st_stream(float* p, const float (&r)[8]) {
+  asm volatile(
+      "st.global.L1::no_allocate.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(r[0]),
+      "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
+      : "memory");
+}
+// Keep-in-L2 variants (AdaLomo re-reads gradients across passes).
+__device__ __forceinline__ void ld_keep_ro(const float* p, float (&r)[8]) {
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_last.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]),
+        "=f"(r[7])
+      : "l"(p));
+}
+__device__ __forceinline__ void ld_stream(const double* p, double (&r)[4]) {
+  asm volatile("ld.global.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_stream_ro(const double* p, double (&r)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(r[0]), "=d"(r[1]), "=d"(r[2]), "=d"(r[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_stream(double* p, const double (&r)[4]) {
+  asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(r[0]),
+               "d"(r[1]), "d"(r[2]), "d"(r[3])
+               : "memory");
+}
+// 8 x bf16 = 128 bits
+__device__ __forceinline__ void ld_stream_ro_bf16x8(const uint16_t* p, float (&r)[8]) {
+  uint32_t a, b, c, d;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "l"(p));
+  const uint32_t w[4] = {a, b, c, d};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    r[2 * k] = __uint_as_float(w[k] << 16);
+    r[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ void ld_stream_bf16x8(const uint16_t* p, float (&r)[8]) {
+  uint32_t a, b, c, d;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(a), "=r"(b), "=r"(c), "=r"(d)
+               : "l"(p));
+  const uint32_t w[4] = {a, b, c, d};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    r[2 * k] = __uint_as_float(w[k] << 16);
+    r[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+  }
+}
+
+// fp32 -> bf16 round-to-nearest-even (NaN kept quiet); same rule as the oracle.
+__device__ __forceinline__ uint32_t f2bf_bits(float f) {
+  uint32_t u = __float_as_uint(f);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (u >> 16) | 0x40u;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return u >> 16;
+}
+__device__ __forceinline__ void st_stream_bf16x8(uint16_t* p, const float (&r)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) w[k] = f2bf_bits(r[2 * k]) | (f2bf_bits(r[2 * k + 1]) << 16);
+  asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w[0]),
+               "r"(w[1]), "r"(w[2]), "r"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
+
+// ---- deterministic reductions --------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Block sum in a fixed order (warp butterflies, then warp partials in warp
+// order by warp 0).  Result valid in thread 0.  `scratch` >= 32 entries.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* scratch) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();  // scratch reuse guard
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  T r = 0;
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    r = lane < nw ? scratch[lane] : T(0);
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+}  // namespace mco

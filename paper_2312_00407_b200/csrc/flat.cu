@@ -1,0 +1,462 @@
+// Fused elementwise optimizer steps for sm_100a: AdamW / Lion / Adan / Sophia
+// (optim.cpp:114-167), LOMO (optim.cpp:185-190), the LOMO global grad-norm
+// reduction (optim.cpp:294-303) and the synthetic-input generator.
+//
+// One pass per step: every param / grad / state element is read once and
+// written at most once (HBM roofline: SURVEY.md 8(d) bytes per param).
+// Persistent grid-stride CTAs (SMs x resident CTAs), 256-bit LDG/STG
+// (ld.global.v8.f32 -> LDG.E.256), L1 no-allocate + L2 evict-first for the
+// streams, U vectors in flight per thread.  Compiled with --fmad=false: the
+// arithmetic is the reference's operation order, no fused multiply-add, IEEE
+// division and square root -- bit-identical to oracle/mco_oracle.c.
+#include <algorithm>
+#include <mutex>
+#include <unordered_map>
+
+#include "kernels.h"
+
+namespace mco {
+namespace {
+
+constexpr int kThreads = 256;
+enum { K_ADAMW = 0, K_LION = 1, K_ADAN = 2, K_SOPHIA = 3 };
+
+__device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+
+// The per-element update, operation for operation as optim.cpp.
+template <int KIND, typename T>
+__device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
+                                       const StepConsts<T>& k) {
+  if constexpr (KIND == K_ADAMW) {  // optim.cpp:118-124; a = m, b = v
+    a = k.b1 * a + k.omb1 * g;
+    b = k.b2 * b + k.omb2 * g * g;
+    const T mhat = a / k.c1;
+    const T vhat = b / k.c2;
+    p = p - k.lr * (mhat / (dsqrt(vhat) + k.eps) + k.wd * p);
+  } else if constexpr (KIND == K_LION) {  // optim.cpp:129-134; a = m
+    const T u = k.b1 * a + k.omb1 * g;
+    const T s = u > T(0) ? T(1) : (u < T(0) ? T(-1) : T(0));  // sign(0) = 0
+    p = p - k.lr * (s + k.wd * p);
+    a = k.b2 * a + k.omb2 * g;
+  } else if constexpr (KIND == K_ADAN) {  // optim.cpp:142-154; a,b,c,d = m,v,n,g_prev
+    const T gd = k.first ? T(0) : g - d;
+    a = k.b1 * a + k.omb1 * g;
+    b = k.b2 * b + k.omb2 * gd;
+    const T nu = g + k.b2 * gd;
+    c = k.b3 * c + k.omb3 * nu * nu;
+    const T mhat = a / k.c1;
+    const T vhat = b / k.c2;
+    const T nhat = c / k.c3;
+    p = (p - k.lr * (mhat + k.b2 * vhat) / (dsqrt(nhat) + k.eps)) / k.den;
+    d = g;
+  } else {  // K_SOPHIA, optim.cpp:160-166; a = m, b = h
+    a = k.b1 * a + k.omb1 * g;
+    if (k.refresh) b = k.b2 * b + k.omb2 * g * g;  // squared-gradient proxy
+    const T rh = k.rho * b;
+    const T denom = rh < k.eps ? k.eps : rh;  // std::max(rho*h, eps)
+    const T q = a / denom;
+    const T u = q < T(-1) ? T(-1) : (T(1) < q ? T(1) : q);  // std::clamp
+    p = p - (k.lr * u + k.lrwd * p);
+  }
+}
+
+// ---- vector load helpers by element type -----------------------------------
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int W = 8;
+};
+template <>
+struct Vec<double> {
+  static constexpr int W = 4;
+};
+
+__device__ __forceinline__ void load_grad(const float* g, float (&r)[8]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ void load_grad(const uint16_t* g, float (&r)[8]) {
+  ld_stream_ro_bf16x8(g, r);
+}
+__device__ __forceinline__ void load_grad(const double* g, double (&r)[4]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ float load_grad1(const float* g) { return *g; }
+__device__ __forceinline__ float load_grad1(const uint16_t* g) { return bf2f(*g); }
+__device__ __forceinline__ double load_grad1(const double* g) { return *g; }
+
+constexpr bool reads_s1(int k) { return k == K_ADAMW || k == K_ADAN || k == K_SOPHIA; }
+
+template <int KIND, typename T, typename GT, bool MIXED, int U>
+__global__ void __launch_bounds__(kThreads)
+    flat_step_kernel(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
+                     T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
+                     uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
+                     const StepConsts<T> k) {
+  constexpr int W = Vec<T>::W;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = tid; base < nvec; base += stride * U) {
+    T pv[U][W], gv[U][W], a[U][W], b[U][W], c[U][W], d[U][W];
+    // issue every load of the U vectors before any arithmetic
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t vi = base + (uint64_t)u * stride;
+      if (vi < nvec) {
+        const uint64_t e = vi * W;
+        ld_stream(p + e, pv[u]);
+        load_grad(g + e, gv[u]);
+        ld_stream(s0 + e, a[u]);
+        if constexpr (reads_s1(KIND)) ld_stream(s1 + e, b[u]);
+        if constexpr (KIND == K_ADAN) {
+          ld_stream(s2 + e, c[u]);
+          if (!k.first) ld_stream(s3 + e, d[u]);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t vi = base + (uint64_t)u * stride;
+      if (vi < nvec) {
+        const uint64_t e = vi * W;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          if constexpr (KIND != K_ADAN) c[u][j] = d[u][j] = T(0);
+          if constexpr (KIND == K_ADAN) {
+            if (k.first) d[u][j] = T(0);
+          }
+          if constexpr (!reads_s1(KIND)) b[u][j] = T(0);
+          update<KIND, T>(pv[u][j], gv[u][j], a[u][j], b[u][j], c[u][j], d[u][j], k);
+        }
+        st_stream(p + e, pv[u]);
+        st_stream(s0 + e, a[u]);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) st_stream(s1 + e, b[u]);
+        if constexpr (KIND == K_SOPHIA) {
+          if (k.refresh) st_stream(s1 + e, b[u]);
+        }
+        if constexpr (KIND == K_ADAN) {
+          st_stream(s2 + e, c[u]);
+          st_stream(s3 + e, d[u]);
+        }
+        if constexpr (MIXED) st_stream_bf16x8(pout + e, pv[u]);
+      }
+    }
+  }
+  // scalar remainder (unaligned buffers take this path for every element)
+  for (uint64_t e = nvec * W + tid; e < n; e += stride) {
+    T pp = p[e], gg = (T)load_grad1(g + e), aa = s0[e], bb = T(0), cc = T(0), dd = T(0);
+    if constexpr (reads_s1(KIND)) bb = s1[e];
+    if constexpr (KIND == K_ADAN) {
+      cc = s2[e];
+      if (!k.first) dd = s3[e];
+    }
+    update<KIND, T>(pp, gg, aa, bb, cc, dd, k);
+    p[e] = pp;
+    s0[e] = aa;
+    if constexpr (KIND == K_ADAMW || KIND == K_ADAN) s1[e] = bb;
+    if constexpr (KIND == K_SOPHIA) {
+      if (k.refresh) s1[e] = bb;
+    }
+    if constexpr (KIND == K_ADAN) {
+      s2[e] = cc;
+      s3[e] = dd;
+    }
+    if constexpr (MIXED) pout[e] = (uint16_t)f2bf_bits((float)pp);
+  }
+}
+
+// ---- LOMO ---------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ T lomo_factor(double lr, double scale, const double* sumsq,
+                                         double clip) {
+  if (sumsq) {  // optim.cpp:302-303
+    const double norm = sqrt(*sumsq);
+    scale = (norm > clip && norm > 0) ? clip / norm : 1.0;
+  }
+  return (T)(lr * scale);  // optim.cpp:188  f = lr * scale
+}
+
+template <typename PT, typename GT>
+__global__ void __launch_bounds__(kThreads)
+    lomo_kernel(PT* __restrict__ p, const GT* __restrict__ g, uint64_t nvec, uint64_t n,
+                double lr, double scale, const double* __restrict__ sumsq, double clip) {
+  using T = typename std::conditional<std::is_same<PT, double>::value, double, float>::type;
+  constexpr int W = std::is_same<PT, double>::value ? 4 : 8;
+  const T f = lomo_factor<T>(lr, scale, sumsq, clip);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  constexpr int U = 2;
+  for (uint64_t base = tid; base < nvec; base += stride * U) {
+    T pv[U][W], gv[U][W];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t vi = base + (uint64_t)u * stride;
+      if (vi < nvec) {
+        if constexpr (std::is_same<PT, uint16_t>::value)
+          ld_stream_bf16x8(p + vi * W, pv[u]);
+        else
+          ld_stream(p + vi * W, pv[u]);
+        load_grad(g + vi * W, gv[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t vi = base + (uint64_t)u * stride;
+      if (vi < nvec) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) pv[u][j] = pv[u][j] - f * gv[u][j];
+        if constexpr (std::is_same<PT, uint16_t>::value)
+          st_stream_bf16x8(p + vi * W, pv[u]);
+        else
+          st_stream(p + vi * W, pv[u]);
+      }
+    }
+  }
+  for (uint64_t e = nvec * W + tid; e < n; e += stride) {
+    if constexpr (std::is_same<PT, uint16_t>::value) {
+      p[e] = (uint16_t)f2bf_bits(bf2f(p[e]) - f * load_grad1(g + e));
+    } else {
+      p[e] = p[e] - f * (T)load_grad1(g + e);
+    }
+  }
+}
+
+// ---- deterministic sum of squares --------------------------------------------
+// Per-thread fp64 accumulation in a fixed element order, fixed-order block
+// reduction, per-block partials, and the last CTA to finish sums the partials
+// in block order.  Bit-reproducible for a given (n, grid).
+constexpr int kSumsqMaxBlocks = 1024;
+
+template <typename XT>
+__global__ void __launch_bounds__(kThreads)
+    sumsq_kernel(const XT* __restrict__ x, uint64_t nvec, uint64_t n, double* __restrict__ out,
+                 int accumulate, double* __restrict__ partials, unsigned* __restrict__ counter) {
+  __shared__ double scratch[32];
+  __shared__ bool is_last;
+  constexpr int W = std::is_same<XT, double>::value ? 4 : 8;
+  using LT = typename std::conditional<std::is_same<XT, double>::value, double, float>::type;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (uint64_t vi = tid; vi < nvec; vi += stride) {
+    LT v[W];
+    load_grad(x + vi * W, v);
+#pragma unroll
+    for (int j = 0; j < W; ++j) acc += (double)v[j] * (double)v[j];
+  }
+  for (uint64_t e = nvec * W + tid; e < n; e += stride) {
+    const double v = (double)load_grad1(x + e);
+    acc += v * v;
+  }
+  const double bsum = block_sum(acc, scratch);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = bsum;
+    __threadfence();
+    const unsigned ticket = atomicAdd(counter, 1u);
+    is_last = (ticket == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+      s += ((volatile double*)partials)[b];
+    s = block_sum(s, scratch);
+    if (threadIdx.x == 0) {
+      *out = accumulate ? *out + s : s;
+      *counter = 0u;  // re-arm for the next launch on this stream
+    }
+  }
+}
+
+// ---- synthetic generator (oracle/mco_oracle.c restates it) ---------------------
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ULL;
+__host__ __device__ __forceinline__ uint64_t fmix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ULL;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBULL;
+  z ^= z >> 31;
+  return z;
+}
+
+__global__ void synth_kernel(void* dst, int dtype, uint64_t n, uint64_t key, int64_t cols,
+                             int scale_log2, int zero_log2, int rowcol) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint64_t x = fmix64(key + (i + 1) * kGolden);
+    double v = dtype == MCO_BF16 ? (double)((int32_t)(x >> 56) - 128) * 0x1.0p-7
+                                 : (double)((int32_t)(x >> 40) - (1 << 23)) * 0x1.0p-23;
+    if (zero_log2 > 0 && (x & ((1ULL << zero_log2) - 1)) == 0) v = 0.0;
+    int e = scale_log2;
+    if (rowcol && cols > 0) {
+      const uint64_t r = i / (uint64_t)cols, c = i % (uint64_t)cols;
+      e += (int)(fmix64(key ^ (0xA5A5A5A5A5A5A5A5ULL + r * kGolden)) >> 62) - 1;
+      e += (int)(fmix64(key ^ (0x5A5A5A5A5A5A5A5AULL + c * kGolden)) >> 62) - 1;
+    }
+    v = ldexp(v, e);
+    if (dtype == MCO_F32)
+      static_cast<float*>(dst)[i] = (float)v;
+    else if (dtype == MCO_F64)
+      static_cast<double*>(dst)[i] = v;
+    else
+      static_cast<uint16_t*>(dst)[i] = (uint16_t)(__float_as_uint((float)v) >> 16);
+  }
+}
+
+// ---- launch configuration --------------------------------------------------------
+template <typename K>
+int grid_for(K kernel, uint64_t work_items, int device) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;  // kernel -> resident CTAs per SM
+  int per_sm = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find((const void*)kernel);
+    if (it == cache.end()) {
+      MCO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+      per_sm = std::max(per_sm, 1);
+      cache[(const void*)kernel] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
+  const uint64_t full = (uint64_t)device_info(device).sms * (uint64_t)per_sm;
+  const uint64_t need = (work_items + kThreads - 1) / kThreads;
+  return (int)std::max<uint64_t>(1, std::min(full, need));
+}
+
+inline bool aligned(const void* ptr, size_t bytes) {
+  return ptr == nullptr || ((uintptr_t)ptr % bytes) == 0;
+}
+
+template <int KIND, typename T, typename GT, bool MIXED>
+void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
+  constexpr int W = Vec<T>::W;
+  constexpr int U = (KIND == K_ADAN) ? 1 : 2;
+  auto kern = flat_step_kernel<KIND, T, GT, MIXED, U>;
+  bool vec = aligned(a.p, 32) && aligned(a.g, sizeof(GT) * W);
+  for (int i = 0; i < 4; ++i) vec = vec && aligned(a.s[i], 32);
+  if (MIXED) vec = vec && aligned(a.p_out_bf16, 16);
+  const uint64_t nvec = vec ? a.n / W : 0;
+  const uint64_t items = nvec ? (nvec + U - 1) / U : a.n;
+  const int dev = current_device();
+  const int grid = grid_for(kern, std::max<uint64_t>(items, 1), dev);
+  kern<<<grid, kThreads, 0, st>>>((T*)a.p, (const GT*)a.g, (T*)a.s[0], (T*)a.s[1], (T*)a.s[2],
+                                  (T*)a.s[3], a.p_out_bf16, nvec, a.n, k);
+  launch_check("flat_step_kernel");
+}
+
+template <int KIND>
+void dispatch_dtypes(const FlatArgs& a, const StepConsts<float>& kf, const StepConsts<double>& kd,
+                     cudaStream_t st) {
+  const bool mixed = a.p_out_bf16 != nullptr;
+  if (a.state_dtype == MCO_F64) {
+    if (a.p_dtype != MCO_F64 || a.g_dtype != MCO_F64 || mixed)
+      throw Error(MCO_CONTRACT, "flat step: f64 state takes f64 params and grads");
+    run_flat<KIND, double, double, false>(a, kd, st);
+    return;
+  }
+  if (a.p_dtype != MCO_F32)
+    throw Error(MCO_CONTRACT, "flat step: f32 state takes f32 (master) params");
+  if (a.g_dtype == MCO_F32) {
+    if (mixed)
+      run_flat<KIND, float, float, true>(a, kf, st);
+    else
+      run_flat<KIND, float, float, false>(a, kf, st);
+  } else if (a.g_dtype == MCO_BF16) {
+    if (mixed)
+      run_flat<KIND, float, uint16_t, true>(a, kf, st);
+    else
+      run_flat<KIND, float, uint16_t, false>(a, kf, st);
+  } else {
+    throw Error(MCO_CONTRACT, "flat step: f32 state takes f32 or bf16 grads");
+  }
+}
+
+template <typename PT, typename GT>
+void run_lomo(void* p, const void* g, uint64_t n, double lr, double scale, const double* sumsq,
+              double clip, cudaStream_t st) {
+  constexpr int W = std::is_same<PT, double>::value ? 4 : 8;
+  auto kern = lomo_kernel<PT, GT>;
+  const bool vec = aligned(p, sizeof(PT) * W) && aligned(g, sizeof(GT) * W);
+  const uint64_t nvec = vec ? n / W : 0;
+  const uint64_t items = nvec ? (nvec + 1) / 2 : n;
+  const int grid = grid_for(kern, std::max<uint64_t>(items, 1), current_device());
+  kern<<<grid, kThreads, 0, st>>>((PT*)p, (const GT*)g, nvec, n, lr, scale, sumsq, clip);
+  launch_check("lomo_kernel");
+}
+
+template <typename XT>
+void run_sumsq(const void* x, uint64_t n, double* out, int accumulate, double* partials,
+               unsigned* counter, int dev, cudaStream_t st) {
+  constexpr int W = std::is_same<XT, double>::value ? 4 : 8;
+  auto kern = sumsq_kernel<XT>;
+  const bool vec = aligned(x, sizeof(XT) * W);
+  const uint64_t nvec = vec ? n / W : 0;
+  int grid = grid_for(kern, std::max<uint64_t>(nvec ? nvec : n, 1), dev);
+  grid = std::min(grid, kSumsqMaxBlocks);
+  kern<<<grid, kThreads, 0, st>>>((const XT*)x, nvec, n, out, accumulate, partials, counter);
+  launch_check("sumsq_kernel");
+}
+
+}  // namespace
+
+void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
+                      const StepConsts<double>& kd, cudaStream_t st) {
+  if (a.n == 0) return;
+  switch (a.kind) {
+    case MCO_ADAMW: dispatch_dtypes<K_ADAMW>(a, kf, kd, st); break;
+    case MCO_LION: dispatch_dtypes<K_LION>(a, kf, kd, st); break;
+    case MCO_ADAN: dispatch_dtypes<K_ADAN>(a, kf, kd, st); break;
+    case MCO_SOPHIA: dispatch_dtypes<K_SOPHIA>(a, kf, kd, st); break;
+    default: throw Error(MCO_CONTRACT, "FlatOptimizer: fused kind");
+  }
+}
+
+void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
+                 double scale, const double* dev_sumsq, double clip, cudaStream_t st) {
+  if (n == 0) return;
+  if (p_dtype == MCO_F32 && g_dtype == MCO_F32)
+    run_lomo<float, float>(p, g, n, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_F32 && g_dtype == MCO_BF16)
+    run_lomo<float, uint16_t>(p, g, n, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_BF16 && g_dtype == MCO_BF16)
+    run_lomo<uint16_t, uint16_t>(p, g, n, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_F64 && g_dtype == MCO_F64)
+    run_lomo<double, double>(p, g, n, lr, scale, dev_sumsq, clip, st);
+  else
+    throw Error(MCO_CONTRACT, "lomo_apply: unsupported param/grad dtype pair");
+}
+
+size_t sumsq_ws_bytes() { return kSumsqMaxBlocks * sizeof(double) + 256; }
+
+void launch_sumsq(const void* x, int dtype, uint64_t n, double* out, int accumulate, void* ws,
+                  cudaStream_t st) {
+  double* partials = (double*)ws;
+  unsigned* counter = (unsigned*)((char*)ws + kSumsqMaxBlocks * sizeof(double));
+  const int dev = current_device();
+  if (dtype == MCO_F32)
+    run_sumsq<float>(x, n, out, accumulate, partials, counter, dev, st);
+  else if (dtype == MCO_BF16)
+    run_sumsq<uint16_t>(x, n, out, accumulate, partials, counter, dev, st);
+  else if (dtype == MCO_F64)
+    run_sumsq<double>(x, n, out, accumulate, partials, counter, dev, st);
+  else
+    throw Error(MCO_CONTRACT, "sumsq: unsupported dtype");
+}
+
+uint64_t synth_key(uint64_t seed, uint32_t role, uint32_t tensor, uint32_t step) {
+  const uint64_t a = fmix64(seed + (uint64_t)role * kGolden);
+  return fmix64(a ^ (((uint64_t)tensor << 32) | (uint64_t)step));
+}
+
+void launch_synth(void* dst, int dtype, uint64_t n, uint64_t key, int64_t cols, int scale_log2,
+                  int zero_log2, int rowcol, cudaStream_t st) {
+  if (n == 0) return;
+  const int dev = current_device();
+  const uint64_t blocks = std::min<uint64_t>((n + kThreads - 1) / kThreads,
+                                             (uint64_t)device_info(dev).sms * 8);
+  synth_kernel<<<(unsigned)blocks, kThreads, 0, st>>>(dst, dtype, n, key, cols, scale_log2,
+                                                      zero_log2, rowcol);
+  launch_check("synth_kernel");
+}
+
+}  // namespace mco

@@ -1,0 +1,46 @@
+// Host-side launch interface of the sm_100a kernels (used by abi.cpp).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mco {
+
+// FlatOptimizer state (SoA, optim.cpp:74-98).  s[0..3] are, per kind:
+//   adamw  m, v          lion   m
+//   adan   m, v, n, gp   sophia m, h
+struct FlatArgs {
+  int kind;
+  int state_dtype;  // MCO_F32 / MCO_F64
+  void* p;
+  int p_dtype;
+  const void* g;
+  int g_dtype;
+  void* s[4];
+  uint16_t* p_out_bf16;  // mixed step only
+  uint64_t n;
+};
+
+// Launch one fused read-grad / update-state / write-param pass.
+// `kd` / `kf` carry the per-step scalars (only the one matching state_dtype is used).
+void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
+                      const StepConsts<double>& kd, cudaStream_t st);
+
+// LOMO p -= f*g with f = lr*scale (host) or derived from a device Σg² (clip).
+void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
+                 double scale, const double* dev_sumsq, double clip, cudaStream_t st);
+
+// Deterministic Σx² -> *out (double).  ws: >= sumsq_ws_bytes() device bytes
+// private to the stream; counter word must start at zero (kernel re-arms it).
+size_t sumsq_ws_bytes();
+void launch_sumsq(const void* x, int dtype, uint64_t n, double* out, int accumulate, void* ws,
+                  cudaStream_t st);
+
+// Synthetic input generator.
+void launch_synth(void* dst, int dtype, uint64_t n, uint64_t key, int64_t cols, int scale_log2,
+                  int zero_log2, int rowcol, cudaStream_t st);
+uint64_t synth_key(uint64_t seed, uint32_t role, uint32_t tensor, uint32_t step);
+
+}  // namespace mco

@@ -1,0 +1,458 @@
+"""Host-side mirror of the reference optimizer API, ``minicollie::optim``
+(/root/reference/proj/core/include/minicollie/optim.hpp), over the C-ABI.
+
+Same names, argument meaning and error behaviour as the reference:
+
+    Kind, parse_kind, kind_name, is_fused          optim.hpp:14-18
+    OptimizerConfig.defaults_for / validate         optim.hpp:20-35
+    FlatOptimizer(cfg, owned_len).step(p, g, lr)    optim.hpp:40-64
+    lomo_apply(param, grad, lr, scale)              optim.hpp:71
+    AdaLomoState(cfg, shapes).apply(i, p, g, lr)    optim.hpp:76-96
+    PrecisionPolicy, state_bytes                    optim.hpp:113-127
+
+Device path: torch CUDA tensors (stream-ordered on torch's current stream).
+Host path (the reference's ``std::span<double>`` overload): numpy arrays, staged
+through the device by ``mco_flat_step_host``.  Every update runs in the sm_100a
+kernels of ``csrc/``; there is no CPU implementation here.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import MCO_BF16, MCO_F32, MCO_F64, lib
+
+# ---- errors (errors.hpp:11-32) ------------------------------------------------------
+
+
+class MinicollieError(RuntimeError):
+    status = -1
+
+
+class ConfigError(MinicollieError):
+    status = _lib.MCO_CONFIG
+
+
+class DataError(MinicollieError):
+    status = _lib.MCO_DATA
+
+
+class ContractError(MinicollieError):
+    status = _lib.MCO_CONTRACT
+
+
+class ProtocolError(MinicollieError):
+    status = _lib.MCO_PROTOCOL
+
+
+class IoError(MinicollieError):
+    status = _lib.MCO_IO
+
+
+class CudaError(MinicollieError):
+    status = _lib.MCO_CUDA
+
+
+_ERRORS = {c.status: c for c in (ConfigError, DataError, ContractError, ProtocolError, IoError,
+                                 CudaError)}
+
+
+def _check(status: int) -> None:
+    if status != _lib.MCO_OK:
+        msg = lib.mco_last_error().decode()
+        raise _ERRORS.get(status, MinicollieError)(msg)
+
+
+# ---- kinds / config -------------------------------------------------------------------
+
+
+class Kind(enum.IntEnum):
+    """optim.hpp:14"""
+
+    ADAMW = 0
+    LION = 1
+    ADAN = 2
+    SOPHIA = 3
+    LOMO = 4
+    ADALOMO = 5
+
+
+def parse_kind(name: str) -> Kind:
+    out = C.c_int()
+    _check(lib.mco_parse_kind(name.encode(), C.byref(out)))
+    return Kind(out.value)
+
+
+def kind_name(kind: int) -> str:
+    s = lib.mco_kind_name(int(kind))
+    if s is None:
+        raise ConfigError("unknown optimizer kind")
+    return s.decode()
+
+
+def is_fused(kind: int) -> bool:
+    return bool(lib.mco_is_fused(int(kind)))
+
+
+@dataclass
+class OptimizerConfig:
+    """optim.hpp:20-35; defaults as the reference's struct initialisers."""
+
+    kind: Kind = Kind.ADAMW
+    lr: float = 1e-3
+    weight_decay: float = 0.0
+    beta1: float = 0.9
+    beta2: float = 0.999
+    beta3: float = 0.99
+    eps: float = 1e-8
+    clip_threshold: Optional[float] = None
+    adalomo_clip: float = 1.0
+    sophia_rho: float = 0.04
+    update_interval: int = 10
+
+    @staticmethod
+    def defaults_for(kind: int) -> "OptimizerConfig":
+        c = _lib.mco_config()
+        _check(lib.mco_defaults_for(int(kind), C.byref(c)))
+        return OptimizerConfig._from_c(c)
+
+    def validate(self) -> None:
+        _check(lib.mco_validate(C.byref(self._to_c())))
+
+    def _to_c(self) -> _lib.mco_config:
+        return _lib.mco_config(
+            int(self.kind), self.lr, self.weight_decay, self.beta1, self.beta2, self.beta3,
+            self.eps, 1 if self.clip_threshold is not None else 0,
+            float(self.clip_threshold or 0.0), self.adalomo_clip, self.sophia_rho,
+            int(self.update_interval))
+
+    @staticmethod
+    def _from_c(c: _lib.mco_config) -> "OptimizerConfig":
+        return OptimizerConfig(
+            Kind(c.kind), c.lr, c.weight_decay, c.beta1, c.beta2, c.beta3, c.eps,
+            c.clip_threshold if c.has_clip_threshold else None, c.adalomo_clip, c.sophia_rho,
+            c.update_interval)
+
+
+@dataclass
+class PrecisionPolicy:
+    """optim.hpp:113-119"""
+
+    param_dtype_bytes: int = 2
+    grad_dtype_bytes: int = 4
+    master_copy: bool = True
+
+    def needs_master(self) -> bool:
+        return self.master_copy and self.param_dtype_bytes < 4
+
+
+def _shape_arrays(shapes: Sequence[Sequence[int]]):
+    nd = (C.c_int * max(len(shapes), 1))(*[len(s) for s in shapes])
+    flat = [int(d) for s in shapes for d in s]
+    dims = (C.c_int64 * max(len(flat), 1))(*flat)
+    return nd, dims
+
+
+def state_bytes(kind: int, param_count: int, policy: PrecisionPolicy,
+                shapes: Sequence[Sequence[int]] = ()) -> int:
+    """optim.hpp:124-127 / optim.cpp:339-362"""
+    nd, dims = _shape_arrays(shapes)
+    out = C.c_uint64()
+    _check(lib.mco_state_bytes(int(kind), int(param_count), policy.param_dtype_bytes,
+                               policy.grad_dtype_bytes, int(policy.master_copy), len(shapes),
+                               nd, dims, C.byref(out)))
+    return out.value
+
+
+# ---- tensor plumbing (torch for device memory / streams only) ---------------------------
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    if t.dtype == torch.float32:
+        return MCO_F32
+    if t.dtype == torch.bfloat16:
+        return MCO_BF16
+    if t.dtype == torch.float64:
+        return MCO_F64
+    raise ContractError(f"unsupported dtype {t.dtype}")
+
+
+def _np_dtype_code(a: np.ndarray) -> int:
+    if a.dtype == np.float32:
+        return MCO_F32
+    if a.dtype == np.float64:
+        return MCO_F64
+    raise ContractError(f"unsupported host dtype {a.dtype}")
+
+
+def _dev(t, what: str):
+    if not t.is_cuda:
+        raise ContractError(f"{what}: expected a CUDA tensor")
+    if not t.is_contiguous():
+        raise ContractError(f"{what}: expected a contiguous tensor")
+    return t
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return _torch().cuda.current_stream().cuda_stream
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory."""
+
+    _TYPESTR = {MCO_F32: "<f4", MCO_F64: "<f8"}
+
+    def __init__(self, ptr: int, n: int, dtype: int, owner):
+        self._owner = owner  # keeps the handle (and its allocation) alive
+        self.__cuda_array_interface__ = {
+            "shape": (int(n),), "typestr": self._TYPESTR[dtype], "data": (int(ptr), False),
+            "version": 3, "strides": None, "stream": None}
+
+
+def _as_tensor(ptr: int, n: int, dtype: int, owner):
+    torch = _torch()
+    return torch.as_tensor(_CudaArray(ptr, n, dtype, owner), device="cuda")
+
+
+# ---- FlatOptimizer ----------------------------------------------------------------------
+
+
+class FlatOptimizer:
+    """optim.hpp:40-64: element-wise optimizer over a flat owned slice.
+
+    state_dtype: "f32" (product path) or "f64" (bit-exact parity mode).
+    """
+
+    def __init__(self, cfg: OptimizerConfig, owned_len: int, device: int = 0,
+                 state_dtype: str = "f32"):
+        self._cfg = cfg
+        self._n = int(owned_len)
+        self._sd = {"f32": MCO_F32, "f64": MCO_F64}[state_dtype]
+        h = C.c_void_p()
+        _check(lib.mco_flat_create(C.byref(cfg._to_c()), self._n, device, self._sd,
+                                   C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mco_flat_destroy(h)
+            self._h = None
+
+    def step(self, params, grads, lr: float, stream=None) -> None:
+        """FlatOptimizer::step (optim.cpp:100-112).  torch CUDA tensors -> device
+        path; numpy arrays -> the host-span overload (synchronous)."""
+        if isinstance(params, np.ndarray):
+            if not (params.flags.c_contiguous and grads.flags.c_contiguous):
+                raise ContractError("step: host arrays must be contiguous")
+            _check(lib.mco_flat_step_host(
+                self._h, params.ctypes.data, _np_dtype_code(params), params.size,
+                grads.ctypes.data, _np_dtype_code(grads), grads.size, float(lr)))
+            return
+        _dev(params, "step params")
+        _dev(grads, "step grads")
+        _check(lib.mco_flat_step(self._h, params.data_ptr(), _dtype_code(params),
+                                 params.numel(), grads.data_ptr(), _dtype_code(grads),
+                                 grads.numel(), float(lr), _stream(stream)))
+
+    def step_mixed(self, master, grads, param_out, lr: float, stream=None) -> None:
+        """fp32 master step that also writes the bf16 parameter copy."""
+        _dev(master, "master")
+        _dev(grads, "grads")
+        _dev(param_out, "param_out")
+        if master.numel() != grads.numel() or param_out.numel() != master.numel():
+            raise ContractError(
+                f"optimizer step: params/grads length mismatch: {master.numel()} vs "
+                f"{grads.numel()}")
+        _check(lib.mco_flat_step_mixed(self._h, master.data_ptr(), grads.data_ptr(),
+                                       _dtype_code(grads), param_out.data_ptr(),
+                                       master.numel(), float(lr), _stream(stream)))
+
+    def steps_taken(self) -> int:
+        t = C.c_int64()
+        _check(lib.mco_flat_get_steps(self._h, C.byref(t)))
+        return t.value
+
+    def set_steps_taken(self, t: int) -> None:
+        _check(lib.mco_flat_set_steps(self._h, int(t)))
+
+    def state_bytes_runtime(self) -> int:
+        out = C.c_uint64()
+        _check(lib.mco_flat_state_bytes(self._h, C.byref(out)))
+        return out.value
+
+    def buffers(self):
+        """[(name, device tensor view)] in the reference order m, v, n, h, g_prev."""
+        nb = C.c_int()
+        _check(lib.mco_flat_num_buffers(self._h, C.byref(nb)))
+        out = []
+        for i in range(nb.value):
+            name, ptr, ln, dt = C.c_char_p(), C.c_void_p(), C.c_uint64(), C.c_int()
+            _check(lib.mco_flat_buffer(self._h, i, C.byref(name), C.byref(ptr), C.byref(ln),
+                                       C.byref(dt)))
+            out.append((name.value.decode(), _as_tensor(ptr.value, ln.value, dt.value, self)))
+        return out
+
+    def config(self) -> OptimizerConfig:
+        return self._cfg
+
+
+# ---- LOMO -------------------------------------------------------------------------------
+
+
+def lomo_apply(param, grad, lr: float, scale: float = 1.0, stream=None) -> None:
+    """optim.cpp:185-190: param -= (lr*scale) * grad (in place)."""
+    _dev(param, "lomo param")
+    _dev(grad, "lomo grad")
+    if param.numel() != grad.numel():
+        raise ContractError("lomo_apply: param/grad length mismatch")
+    _check(lib.mco_lomo_apply(param.data_ptr(), _dtype_code(param), grad.data_ptr(),
+                              _dtype_code(grad), param.numel(), float(lr), float(scale),
+                              _stream(stream)))
+
+
+def lomo_apply_clipped(param, grad, lr: float, grad_sumsq, clip: float, stream=None) -> None:
+    """lomo_apply with scale = clip/||g|| iff ||g|| > clip (optim.cpp:302-303),
+    ||g||^2 read from the device scalar `grad_sumsq` (float64 CUDA tensor)."""
+    _dev(param, "lomo param")
+    _dev(grad, "lomo grad")
+    _check(lib.mco_lomo_apply_clipped(param.data_ptr(), _dtype_code(param), grad.data_ptr(),
+                                      _dtype_code(grad), param.numel(), float(lr),
+                                      grad_sumsq.data_ptr(), float(clip), _stream(stream)))
+
+
+def sumsq(x, out=None, accumulate: bool = False, stream=None):
+    """Deterministic sum of squares into a float64 CUDA scalar (optim.cpp:294-300)."""
+    torch = _torch()
+    _dev(x, "sumsq input")
+    if out is None:
+        out = torch.zeros((), dtype=torch.float64, device=x.device)
+    _check(lib.mco_sumsq(x.data_ptr(), _dtype_code(x), x.numel(), out.data_ptr(),
+                         int(accumulate), _stream(stream)))
+    return out
+
+
+def lomo_step(params, grads, lr: float, clip: Optional[float] = None, stream=None,
+              grad_sumsq=None):
+    """Flat-buffer form of lomo_fused_backward_step (optim.cpp:284-318): with a
+    clip, one sum-of-squares pass then the scaled update; otherwise one pass.
+    `grad_sumsq` lets a caller supply an already all-reduced device norm^2."""
+    if clip is None:
+        lomo_apply(params, grads, lr, 1.0, stream)
+        return None
+    if grad_sumsq is None:
+        grad_sumsq = sumsq(grads, stream=stream)
+    lomo_apply_clipped(params, grads, lr, grad_sumsq, clip, stream)
+    return grad_sumsq
+
+
+# ---- AdaLomo -------------------------------------------------------------------------------
+
+
+class AdaLomoState:
+    """optim.hpp:76-96.  `shapes` in registry order; 2-D -> factored."""
+
+    def __init__(self, cfg: OptimizerConfig, shapes: Sequence[Sequence[int]], device: int = 0):
+        self._cfg = cfg
+        self.shapes = [tuple(int(d) for d in s) for s in shapes]
+        self.numels = [int(np.prod(s)) if len(s) else 1 for s in self.shapes]
+        self.offsets = np.concatenate([[0], np.cumsum(self.numels)]).astype(np.int64)
+        nd, dims = _shape_arrays(self.shapes)
+        h = C.c_void_p()
+        _check(lib.mco_adalomo_create(C.byref(cfg._to_c()), len(self.shapes), nd, dims, device,
+                                      C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mco_adalomo_destroy(h)
+            self._h = None
+
+    def apply(self, index: int, param, grad, lr: float, grad_sumsq=None, stream=None) -> None:
+        """AdaLomoState::apply (optim.cpp:215-275) for tensor `index` (hook form)."""
+        _dev(param, "adalomo param")
+        _dev(grad, "adalomo grad")
+        if not (0 <= index < len(self.shapes)) or param.numel() != self.numels[index]:
+            raise ContractError(f"adalomo: unknown parameter '{index}'")
+        _check(lib.mco_adalomo_apply(
+            self._h, int(index), param.data_ptr(), _dtype_code(param), grad.data_ptr(),
+            _dtype_code(grad), float(lr),
+            grad_sumsq.data_ptr() if grad_sumsq is not None else None, _stream(stream)))
+
+    def apply_all(self, flat_params, flat_grads, lr: float, stream=None) -> None:
+        """Every tensor in one multi-tensor pass over registry-order flat buffers;
+        global grad-norm clip when cfg.clip_threshold is set."""
+        _dev(flat_params, "adalomo params")
+        _dev(flat_grads, "adalomo grads")
+        if flat_params.numel() != int(self.offsets[-1]) or flat_grads.numel() != int(
+                self.offsets[-1]):
+            raise ContractError("adalomo: flat buffer length does not match the registry")
+        _check(lib.mco_adalomo_apply_all(self._h, flat_params.data_ptr(),
+                                         _dtype_code(flat_params), flat_grads.data_ptr(),
+                                         _dtype_code(flat_grads), float(lr), _stream(stream)))
+
+    def state_bytes_runtime(self) -> int:
+        out = C.c_uint64()
+        _check(lib.mco_adalomo_state_bytes(self._h, C.byref(out)))
+        return out.value
+
+    def steps(self, index: int) -> int:
+        t = C.c_int64()
+        _check(lib.mco_adalomo_get_steps(self._h, int(index), C.byref(t)))
+        return t.value
+
+    def buffer(self, index: int, which: str):
+        """fp64 device view of v_row / v_col / v_full for tensor `index` (None if absent)."""
+        w = {"v_row": 0, "v_col": 1, "v_full": 2}[which]
+        ptr, ln = C.c_void_p(), C.c_uint64()
+        _check(lib.mco_adalomo_buffer(self._h, int(index), w, C.byref(ptr), C.byref(ln)))
+        if not ptr.value:
+            return None
+        return _as_tensor(ptr.value, ln.value, MCO_F64, self)
+
+
+# ---- misc ---------------------------------------------------------------------------------
+
+
+def zero_plan(total_len: int, dp_size: int, stage: int = 1):
+    """ZeroPlan::make (parallel.cpp:20-34) -> (part_sizes, offsets)."""
+    ps = (C.c_uint64 * max(dp_size, 1))()
+    offs = (C.c_uint64 * (max(dp_size, 1) + 1))()
+    _check(lib.mco_zero_plan(int(total_len), int(dp_size), int(stage), ps, offs))
+    return [ps[i] for i in range(dp_size)], [offs[i] for i in range(dp_size + 1)]
+
+
+def synth_fill(t, seed: int, role: int, tensor: int, step: int, cols: int = 0,
+               scale_log2: int = 0, zero_log2: int = 0, rowcol: bool = False,
+               stream=None) -> None:
+    """Fill a CUDA tensor with the counter-based synthetic generator."""
+    _dev(t, "synth")
+    _check(lib.mco_synth_fill(t.data_ptr(), _dtype_code(t), t.numel(), int(seed), int(role),
+                              int(tensor), int(step), int(cols), int(scale_log2),
+                              int(zero_log2), int(rowcol), _stream(stream)))
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libmco in this process."""
+    return int(lib.mco_launch_count())
+
+
+def device_count() -> int:
+    n = C.c_int()
+    _check(lib.mco_device_count(C.byref(n)))
+    return n.value

@@ -1,0 +1,208 @@
+"""GPU parity of the stored-state optimizers (AdamW / Lion / Adan / Sophia) through
+the C-ABI against the oracle: bit-exact vs the fp32 restatement, bit-exact vs the
+compiled reference in f64 mode, fp32-tolerance vs the reference."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2312_00407_b200 import optim
+from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+FLAT = [Kind.ADAMW, Kind.LION, Kind.ADAN, Kind.SOPHIA]
+
+
+def cfg_for(kind, **kw):
+    c = OptimizerConfig.defaults_for(kind)
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def bits_equal(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    return np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("kind", FLAT)
+@pytest.mark.parametrize("n", [1, 13, 4096 + 5, 1 << 20])
+def test_f32_bit_exact_vs_restatement(kind, n):
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=3)
+    p = O.synth(n, 2024, 0, 1, 0, 0, -6, 0, False)
+    gpu_p = dev(p)
+    opt = optim.FlatOptimizer(cfg, n)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    for t in range(1, 8):
+        g = O.synth(n, 2024, 1, 1, t, 0, -7, 10, False)
+        opt.step(gpu_p, dev(g), 1e-3)
+        orc.step(p, g, 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(gpu_p.cpu().numpy(), p)
+    bufs = opt.buffers()
+    assert [b[0] for b in bufs] == list(orc.state)
+    for name, t in bufs:
+        assert bits_equal(t.cpu().numpy(), orc.state[name]), name
+    assert opt.steps_taken() == 7
+
+
+@pytest.mark.parametrize("kind", FLAT)
+def test_unaligned_views_take_scalar_path_bit_exact(kind):
+    """ZeRO shard edges: params / grads at odd element offsets."""
+    n, off = 10007, 3
+    cfg = cfg_for(kind, weight_decay=0.01)
+    pbig = O.synth(n + off, 7, 0, 2, 0, 0, -6, 0, False)
+    gbig = O.synth(n + off, 7, 1, 2, 1, 0, -7, 10, False)
+    tp, tg = dev(pbig), dev(gbig)
+    opt = optim.FlatOptimizer(cfg, n)
+    opt.step(tp[off:], tg[off:], 1e-3)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    p = pbig[off:].copy()
+    orc.step(p, gbig[off:].copy(), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp[off:].cpu().numpy(), p)
+    assert bits_equal(tp[:off].cpu().numpy(), pbig[:off])  # untouched
+
+
+@pytest.mark.parametrize("kind", FLAT)
+def test_bf16_grads_and_mixed_param_out(kind):
+    n = 70001
+    cfg = cfg_for(kind, weight_decay=0.01)
+    p = O.synth(n, 3, 0, 0, 0, 0, -6, 0, False)
+    gb = O.synth(n, 3, 1, 0, 1, 0, -7, 10, False, "bf16")
+    tp, tpo = dev(p), torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    tg = dev(gb).view(torch.bfloat16)
+    opt = optim.FlatOptimizer(cfg, n)
+    opt.step_mixed(tp, tg, tpo, 1e-3)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    orc.step(p, O.bf16_to_f32(gb), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    assert bits_equal(tpo.view(torch.int16).cpu().numpy().view(np.uint16), O.f32_to_bf16(p))
+
+
+@pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("kind", FLAT)
+def test_f64_mode_bit_exact_vs_compiled_reference(kind):
+    """state_dtype f64: every element identical to minicollie::optim::FlatOptimizer."""
+    n = 50000 + 3
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=4)
+    p = O.synth(n, 11, 0, 0, 0, 0, -6, 0, False, np.float64)
+    tp = dev(p)
+    opt = optim.FlatOptimizer(cfg, n, state_dtype="f64")
+    r = O.RefFlat(cfg, n)
+    for t in range(1, 13):
+        g = O.synth(n, 11, 1, 0, t, 0, -7, 10, False, np.float64)
+        opt.step(tp, dev(g), 1e-3)
+        r.step(p, g, 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    rb = r.buffers()
+    for name, t in opt.buffers():
+        assert bits_equal(t.cpu().numpy(), rb[name]), name
+
+
+@pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("kind", FLAT)
+def test_f32_within_tolerance_of_reference(kind):
+    from test_oracle import fp32_vs_fp64_ok
+
+    n, lr = 1 << 16, 1e-3
+    cfg = cfg_for(kind, weight_decay=0.01)
+    p64 = O.synth(n, 2024, 0, 1, 0, 0, -6, 0, False, np.float64)
+    p0 = p64.copy()
+    tp = dev(p64.astype(np.float32))
+    opt, r = optim.FlatOptimizer(cfg, n), O.RefFlat(cfg, n)
+    for t in range(1, 21):
+        g = O.synth(n, 2024, 1, 1, t, 0, -7, 10, False)
+        opt.step(tp, dev(g), lr)
+        r.step(p64, g.astype(np.float64), lr)
+    torch.cuda.synchronize()
+    assert fp32_vs_fp64_ok(kind, tp.cpu().numpy(), p64, p0, lr)
+
+
+@pytest.mark.parametrize("kind", FLAT)
+def test_host_span_path_equals_device_path(kind):
+    """The reference's std::span overload (mco_flat_step_host) == device step."""
+    n = (1 << 24) + 12345  # > one pipeline chunk
+    cfg = cfg_for(kind, weight_decay=0.01)
+    p = O.synth(n, 5, 0, 0, 0, 0, -6, 0, False)
+    g = O.synth(n, 5, 1, 0, 1, 0, -7, 10, False)
+    a, b = optim.FlatOptimizer(cfg, n), optim.FlatOptimizer(cfg, n)
+    hp = p.copy()
+    a.step(hp, g, 1e-3)
+    tp = dev(p)
+    b.step(tp, dev(g), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(hp, tp.cpu().numpy())
+
+
+def test_contract_errors_match_reference_messages():
+    cfg = cfg_for(Kind.ADAMW)
+    opt = optim.FlatOptimizer(cfg, 8)
+    p = torch.zeros(8, device="cuda")
+    with pytest.raises(optim.ContractError,
+                       match="optimizer step: params/grads length mismatch: 8 vs 7"):
+        opt.step(p, torch.zeros(7, device="cuda"), 0.1)
+    assert opt.steps_taken() == 0  # optim.cpp:101-104: checked before ++t
+    with pytest.raises(optim.ContractError):
+        opt.step(torch.zeros(9, device="cuda"), torch.zeros(9, device="cuda"), 0.1)
+    with pytest.raises(optim.ContractError):
+        opt.step(p.double(), p.double(), 0.1)  # f64 data into an f32 optimizer
+
+
+def test_kat_through_gpu():
+    """test_optim.cpp known answers through the GPU path (f32 and f64 modes)."""
+    for sd, dt in (("f32", torch.float32), ("f64", torch.float64)):
+        c = cfg_for(Kind.ADAMW, lr=0.1)
+        o = optim.FlatOptimizer(c, 1, state_dtype=sd)
+        p = torch.ones(1, dtype=dt, device="cuda")
+        o.step(p, torch.ones(1, dtype=dt, device="cuda"), 0.1)
+        assert p.item() == pytest.approx(0.9, rel=1e-7)
+        c = cfg_for(Kind.LION, lr=0.1)
+        o = optim.FlatOptimizer(c, 1, state_dtype=sd)
+        p = torch.full((1,), 2.0, dtype=dt, device="cuda")
+        o.step(p, torch.zeros(1, dtype=dt, device="cuda"), 0.1)
+        assert p.item() == 2.0
+        c = cfg_for(Kind.SOPHIA, lr=0.02)
+        o = optim.FlatOptimizer(c, 2, state_dtype=sd)
+        p = torch.tensor([1.0, -1.0], dtype=dt, device="cuda")
+        o.step(p, torch.zeros(2, dtype=dt, device="cuda"), 0.02)
+        assert p.tolist() == [1.0, -1.0]
+    c = cfg_for(Kind.ADAN)
+    assert optim.FlatOptimizer(c, 10, state_dtype="f64").state_bytes_runtime() == 4 * 10 * 8
+    assert optim.FlatOptimizer(c, 10).state_bytes_runtime() == 4 * 10 * 4
+
+
+def test_sampled_parity_at_scale():
+    """A 2^30-element AdamW step (4 GiB per buffer), checked on sampled slices that
+    the oracle regenerates from the counter-based generator."""
+    n = 1 << 30
+    cfg = cfg_for(Kind.ADAMW, weight_decay=0.01)
+    tp = torch.empty(n, device="cuda")
+    tg = torch.empty(n, device="cuda")
+    optim.synth_fill(tp, 2024, 0, 9, 0, 0, -6)
+    opt = optim.FlatOptimizer(cfg, n)
+    for t in (1, 2):
+        optim.synth_fill(tg, 2024, 1, 9, t, 0, -7, 10)
+        opt.step(tp, tg, 1e-3)
+    torch.cuda.synchronize()
+    key_p, G = O.orc.orc_synth_key(2024, 0, 9, 0), 0x9E3779B97F4A7C15
+    for start in (0, 123456789, n - 4096):
+        m = 4096
+        p = np.empty(m, np.float32)
+        O.orc.orc_synth_f32(O._ptr(p), m, (key_p + start * G) % (1 << 64), 0, -6, 0, 0)
+        orc = O.OracleFlat(cfg, m, np.float32)
+        for t in (1, 2):
+            g = np.empty(m, np.float32)
+            key_g = O.orc.orc_synth_key(2024, 1, 9, t)
+            O.orc.orc_synth_f32(O._ptr(g), m, (key_g + start * G) % (1 << 64), 0, -7, 10, 0)
+            orc.step(p, g, 1e-3)
+        assert bits_equal(tp[start:start + m].cpu().numpy(), p)
+    del tp, tg
+    torch.cuda.empty_cache()

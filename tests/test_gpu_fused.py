@@ -1,0 +1,263 @@
+"""GPU parity of the fused optimizers (LOMO, AdaLomo) and the grad-norm reduction
+through the C-ABI, against the oracle / compiled reference."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2312_00407_b200 import optim, registry
+from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+needs_ref = pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def bits_equal(a, b):
+    return np.array_equal(np.ascontiguousarray(a).view(np.uint8),
+                          np.ascontiguousarray(b).view(np.uint8))
+
+
+# ---- LOMO ------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("n", [1, 9, 100003, 1 << 22])
+def test_lomo_f32_bf16_f64_bit_exact(n):
+    p32 = O.synth(n, 4, 0, 0, 0, 0, -6, 0, False)
+    g32 = O.synth(n, 4, 1, 0, 1, 0, -7, 10, False)
+    t = dev(p32)
+    optim.lomo_apply(t, dev(g32), 1e-2, 0.75)
+    O.orc.orc_lomo_f32(O._ptr(p32), O._ptr(g32), n, 1e-2, 0.75)
+    assert bits_equal(t.cpu().numpy(), p32)
+
+    pb = O.synth(n, 4, 0, 0, 0, 0, -6, 0, False, "bf16")
+    gb = O.synth(n, 4, 1, 0, 1, 0, -7, 10, False, "bf16")
+    tb = dev(pb).view(torch.bfloat16)
+    optim.lomo_apply(tb, dev(gb).view(torch.bfloat16), 1e-2, 1.0)
+    O.orc.orc_lomo_bf16(O._ptr(pb), O._ptr(gb), n, 1e-2, 1.0)
+    assert bits_equal(tb.view(torch.int16).cpu().numpy(), pb.view(np.int16))
+
+    p64 = O.synth(n, 4, 0, 0, 0, 0, -6, 0, False, np.float64)
+    g64 = O.synth(n, 4, 1, 0, 1, 0, -7, 10, False, np.float64)
+    t64 = dev(p64)
+    optim.lomo_apply(t64, dev(g64), 1e-2, 0.5)
+    if O.ref is not None:  # the reference's lomo_apply itself
+        O.ref_check(O.ref.ref_lomo_apply(O._ptr(p64), O._ptr(g64), n, 1e-2, 0.5))
+    else:
+        O.orc.orc_lomo_f64(O._ptr(p64), O._ptr(g64), n, 1e-2, 0.5)
+    assert bits_equal(t64.cpu().numpy(), p64)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "f64"])
+def test_sumsq_matches_oracle_and_is_deterministic(dt):
+    n = 3 * (1 << 20) + 77
+    if dt == "bf16":
+        x = O.synth(n, 8, 1, 0, 1, 0, -7, 10, False, "bf16")
+        want = O.orc.orc_sumsq_bf16(O._ptr(x), n)
+        t = dev(x).view(torch.bfloat16)
+    else:
+        x = O.synth(n, 8, 1, 0, 1, 0, -7, 10, False, np.float32 if dt == "f32" else np.float64)
+        want = (O.orc.orc_sumsq_f32 if dt == "f32" else O.orc.orc_sumsq_f64)(O._ptr(x), n)
+        t = dev(x)
+    a = optim.sumsq(t)
+    b = optim.sumsq(t)
+    optim.sumsq(t, out=b, accumulate=True)
+    torch.cuda.synchronize()
+    assert a.item() == pytest.approx(want, rel=1e-12)
+    assert bits_equal(np.array(a.item()), np.array(optim.sumsq(t).item()))
+    assert b.item() == pytest.approx(2 * want, rel=1e-12)
+
+
+@needs_ref
+@pytest.mark.parametrize("clip", [None, 0.05, 1e9])
+def test_lomo_clip_matches_reference_two_pass(clip):
+    """lomo_fused_backward_step (optim.cpp:284-318, two backward passes) vs the flat
+    form: one device sum-of-squares pass + the scaled update, in f64."""
+    sizes = [4096, 17, 40000]
+    ps = [O.synth(n, 5, 0, k, 0, 0, -6, 0, False, np.float64) for k, n in enumerate(sizes)]
+    gs = [O.synth(n, 5, 1, k, 1, 0, -7, 10, False, np.float64) for k, n in enumerate(sizes)]
+    tp, tg = dev(np.concatenate(ps)), dev(np.concatenate(gs))
+    optim.lomo_step(tp, tg, 0.1, clip)
+    O.ref_lomo_fused(ps, gs, 0.1, clip)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(tp.cpu().numpy(), np.concatenate(ps), rtol=1e-14, atol=0)
+
+
+def test_lomo_lr_zero_is_noop():  # test_optim.cpp:248-257
+    p = O.synth(1000, 1, 0, 0, 0, 0, -6, 0, False)
+    t = dev(p)
+    optim.lomo_apply(t, dev(O.synth(1000, 1, 1, 0, 1, 0, -7, 0, False)), 0.0, 1.0)
+    assert bits_equal(t.cpu().numpy(), p)
+
+
+# ---- AdaLomo -----------------------------------------------------------------------------
+
+SHAPES = [(6, 9), (7,), (3, 4), (33, 17), (64, 1040), (1, 5), (5, 1), (300, 256), (130,)]
+
+
+def ada_inputs(shapes, steps, seed=9):
+    ps = O.registry_params(shapes, seed, np.float64)
+    gs = [O.registry_grads(shapes, seed, t, np.float64) for t in range(1, steps + 1)]
+    return ps, gs
+
+
+def ada_tol_ok(got32, want64, p0):
+    rms = max(float(np.sqrt(np.mean(p0 ** 2))), 1e-30)
+    err = np.abs(got32.astype(np.float64) - want64) / np.maximum(np.abs(want64), rms)
+    return err.max() <= 1e-5, err.max()
+
+
+@needs_ref
+@pytest.mark.parametrize("form", ["hook", "all"])
+def test_adalomo_matches_reference(form):
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    steps, lr = 4, 5e-3
+    ps, gs = ada_inputs(SHAPES, steps)
+    p0 = [p.copy() for p in ps]
+    st = optim.AdaLomoState(cfg, SHAPES)
+    r = O.RefAdaLomo(cfg, SHAPES)
+    flat_p = dev(np.concatenate(ps).astype(np.float32))
+    for t in range(steps):
+        flat_g = dev(np.concatenate(gs[t]).astype(np.float32))
+        if form == "all":
+            st.apply_all(flat_p, flat_g, lr)
+        else:
+            for k in range(len(SHAPES)):
+                a, b = int(st.offsets[k]), int(st.offsets[k + 1])
+                st.apply(k, flat_p[a:b], flat_g[a:b], lr)
+        for k in range(len(SHAPES)):
+            r.apply(k, ps[k], gs[t][k], lr)
+    torch.cuda.synchronize()
+    got = flat_p.cpu().numpy()
+    for k in range(len(SHAPES)):
+        a, b = int(st.offsets[k]), int(st.offsets[k + 1])
+        ok, e = ada_tol_ok(got[a:b], ps[k], p0[k])
+        assert ok, (k, SHAPES[k], e)
+        assert st.steps(k) == steps
+    assert st.state_bytes_runtime() == r.state_bytes()
+
+
+@needs_ref
+def test_adalomo_state_matches_reference_state():
+    """v_row / v_col / v_full after 3 steps vs the oracle's fp64 restatement."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    ps, gs = ada_inputs(SHAPES, 3)
+    st, o = optim.AdaLomoState(cfg, SHAPES), O.OracleAdaLomo(cfg, SHAPES)
+    flat_p = dev(np.concatenate(ps).astype(np.float32))
+    for t in range(3):
+        st.apply_all(flat_p, dev(np.concatenate(gs[t]).astype(np.float32)), 1e-3)
+        for k in range(len(SHAPES)):
+            o.apply(k, ps[k], gs[t][k], 1e-3)
+    torch.cuda.synchronize()
+    for k, s in enumerate(SHAPES):
+        e = o.entries[k]
+        names = ("v_row", "v_col") if len(s) == 2 else ("v_full",)
+        for nm in names:
+            np.testing.assert_allclose(st.buffer(k, nm).cpu().numpy(), e[nm], rtol=2e-6,
+                                       err_msg=f"{k} {nm}")
+
+
+@needs_ref
+@pytest.mark.parametrize("clip", [1e-3, 1e6])
+def test_adalomo_global_clip_matches_composed_oracle(clip):
+    """AdaLomo + global grad-norm clip (parity unpinned in the reference; composed
+    oracle: the reference's clip rule, optim.cpp:302-303, scaling g, then the
+    reference AdaLomoState::apply)."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    cfg.clip_threshold = clip
+    ps, gs = ada_inputs(SHAPES, 2)
+    p0 = [p.copy() for p in ps]
+    st = optim.AdaLomoState(cfg, SHAPES)
+    o = O.OracleAdaLomo(cfg, SHAPES)
+    flat_p = dev(np.concatenate(ps).astype(np.float32))
+    for t in range(2):
+        g = np.concatenate(gs[t]).astype(np.float32)
+        st.apply_all(flat_p, dev(g), 1e-2)
+        g64 = g.astype(np.float64)
+        scale = O.orc.orc_clip_scale(O.orc.orc_sumsq_f64(O._ptr(g64), g64.size), clip)
+        for k in range(len(SHAPES)):
+            o.apply(k, ps[k], gs[t][k], 1e-2, scale)
+    torch.cuda.synchronize()
+    got = flat_p.cpu().numpy()
+    for k in range(len(SHAPES)):
+        a, b = int(st.offsets[k]), int(st.offsets[k + 1])
+        ok, e = ada_tol_ok(got[a:b], ps[k], p0[k])
+        assert ok, (k, e)
+
+
+def test_adalomo_hook_form_with_device_norm_equals_all_form_clip():
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    cfg.clip_threshold = 1e-3
+    ps, gs = ada_inputs(SHAPES, 1)
+    a, b = optim.AdaLomoState(cfg, SHAPES), optim.AdaLomoState(cfg, SHAPES)
+    fp = np.concatenate(ps).astype(np.float32)
+    g = dev(np.concatenate(gs[0]).astype(np.float32))
+    pa, pb = dev(fp), dev(fp)
+    a.apply_all(pa, g, 1e-2)
+    norm2 = optim.sumsq(g)
+    for k in range(len(SHAPES)):
+        s, e = int(b.offsets[k]), int(b.offsets[k + 1])
+        b.apply(k, pb[s:e], g[s:e], 1e-2, grad_sumsq=norm2)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(pa.cpu().numpy(), pb.cpu().numpy(), rtol=1e-6, atol=1e-9)
+
+
+def test_adalomo_rank1_exact():  # test_optim.cpp:318-352 through the GPU
+    av, bv = np.array([0.5, -1.5, 2.0]), np.array([1.0, 0.25, -2.0, 0.5])
+    g = np.outer(av, bv).ravel()
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    st = optim.AdaLomoState(cfg, [(3, 4)])
+    p = torch.ones(12, device="cuda")
+    st.apply(0, p, dev(g.astype(np.float32)), 0.01)
+    delta = 1.0 - p.cpu().numpy().astype(np.float64)
+    ratio = delta / (g / np.sqrt(g * g + cfg.eps))
+    assert np.all(ratio > 0)
+    np.testing.assert_allclose(ratio, ratio[0], rtol=1e-4)  # fp32 storage of p
+
+
+def test_adalomo_bf16_grads_and_determinism():
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = registry.CONFIG1.shapes()[:12]
+    n = sum(int(np.prod(s)) for s in shapes)
+    outs = []
+    for _ in range(2):
+        st = optim.AdaLomoState(cfg, shapes)
+        p = torch.empty(n, device="cuda")
+        g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        registry.fill_params(p, shapes)
+        for t in (1, 2):
+            registry.fill_grads(g, shapes, t)
+            st.apply_all(p, g, 1e-3)
+        outs.append(p.cpu().numpy())
+    assert bits_equal(outs[0], outs[1])
+    assert np.all(np.isfinite(outs[0]))
+
+
+@needs_ref
+def test_adalomo_config1_registry_vs_reference():
+    """All 75 tensors of configuration 1 (10.5M params) through apply_all, 2 steps."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = registry.CONFIG1.shapes()
+    n = registry.CONFIG1.param_count()
+    st = optim.AdaLomoState(cfg, shapes)
+    p = torch.empty(n, device="cuda")
+    g = torch.empty(n, device="cuda")
+    registry.fill_params(p, shapes)
+    ps = O.registry_params(shapes, registry.SEED, np.float64)
+    p0 = [x.copy() for x in ps]
+    assert bits_equal(p.cpu().numpy(), np.concatenate(ps).astype(np.float32))
+    r = O.RefAdaLomo(cfg, shapes)
+    for t in (1, 2):
+        registry.fill_grads(g, shapes, t)
+        st.apply_all(p, g, 5e-4)
+        gs = O.registry_grads(shapes, registry.SEED, t, np.float64)
+        for k in range(len(shapes)):
+            r.apply(k, ps[k], gs[k], 5e-4)
+    torch.cuda.synchronize()
+    got = p.cpu().numpy()
+    for k in range(len(shapes)):
+        a, b = int(st.offsets[k]), int(st.offsets[k + 1])
+        ok, e = ada_tol_ok(got[a:b], ps[k], p0[k])
+        assert ok, (k, shapes[k], e)
