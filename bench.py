@@ -204,6 +204,8 @@ def bench_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     model = registry.MODELS[args.model]
+    if args.layers:
+        model = registry.layer_subset(model, args.layers)
     shapes = model.shapes()
     P = model.param_count()
     kinds = args.optimizers.split(",")
@@ -278,18 +280,20 @@ def bench_ours(args, rank, world, local_rank):
         "peak_source": peak_src, "unit": "GB/s",
         "frac": round(per[dom]["achieved_gbs"] / hbm_peak, 4),
         "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": owned,
-        "traffic": load_traffic(dom)}
+        "traffic": load_traffic(dom, owned)}
     return dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
                 launches=launches, clocks=clocks.summary(), P=P, owned=owned,
                 shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
 
 
-def load_traffic(kind):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed
-    ncu --set full capture (profiles/traffic.json), or None."""
+def load_traffic(kind, params_per_launch):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, from the committed
+    ncu --set full capture (profiles/traffic.json holds DRAM bytes per parameter per
+    step measured on a layer subset of the same shapes), scaled to this launch."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kind)
+            d = json.load(f)[kind]
+        return round(d["dram_bytes_per_param"] * params_per_launch)
     except Exception:
         return None
 
@@ -321,8 +325,11 @@ def bench_e2e(args, res):
     steps = max(1, min(args.steps, args.e2e_steps))
     tot_s, h2d, d2h = 0.0, 0, 0
     per = {}
+    opt = ada = one = None
     for kind in res["kinds"]:
         cfg = make_cfg(kind)
+        opt = ada = one = None  # free the previous optimizer's device state first
+        gc.collect()
         if kind in ("adamw", "lion", "adan", "sophia"):
             opt = optim.FlatOptimizer(cfg, n)
             hpn, hgn = hp.numpy(), hg.numpy()
@@ -353,8 +360,6 @@ def bench_e2e(args, res):
         h2d += 2 * n * 4
         d2h += n * 4
         log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {n / dt / 1e9:.2f} Gparam/s")
-        del one
-        gc.collect()
     return {"value": len(per) * n / tot_s, "unit": "params/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "params": n, "per_optimizer": per,
             "path": "C-ABI with pinned host buffers (mco_flat_step_host for the stored-state "
@@ -368,6 +373,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--model", default="llama-7b")
+    ap.add_argument("--layers", type=int, default=0,
+                    help="decoder-layer subset of --model (profiling runs only)")
     ap.add_argument("--optimizers", default=",".join(KINDS))
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")

@@ -65,9 +65,9 @@ def test_sumsq_matches_oracle_and_is_deterministic(dt):
     b = optim.sumsq(t)
     optim.sumsq(t, out=b, accumulate=True)
     torch.cuda.synchronize()
-    assert a.item() == pytest.approx(want, rel=1e-12)
+    assert a.item() == pytest.approx(want, rel=1e-10)  # fp64 sums, different order
     assert bits_equal(np.array(a.item()), np.array(optim.sumsq(t).item()))
-    assert b.item() == pytest.approx(2 * want, rel=1e-12)
+    assert b.item() == pytest.approx(2 * want, rel=1e-10)
 
 
 @needs_ref
