@@ -33,6 +33,8 @@ namespace mco {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kRB = 2;   // K1/K6: rows per thread per loop iteration (loads in flight)
+constexpr int kRB2 = 4;  // K4 reads one stream only: more rows in flight
 
 struct Ctx {
   const Tile* tiles;
@@ -136,26 +138,35 @@ __global__ void __launch_bounds__(kThreads)
       float cacc[VW];
 #pragma unroll
       for (int j = 0; j < VW; ++j) cacc[j] = 0.f;
-      for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
-        float gv[VW], pv[VW];
-        if (valid > 0) {
-          load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
-          load_p<VEC>(p + r * T.cols + col, pv, valid);
-        } else {
+      // RB rows per iteration: all their loads are in flight before any math
+      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB * TR) {
+        float gv[kRB][VW], pv[kRB][VW];
 #pragma unroll
-          for (int j = 0; j < VW; ++j) gv[j] = pv[j] = 0.f;
-        }
-        float sg = 0.f, sp = 0.f;
+        for (int b = 0; b < kRB; ++b) {
+          const int64_t r = r0 + (int64_t)b * TR;
+          if (valid > 0 && r < tl.r1) {
+            load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
+            load_p<VEC>(p + r * T.cols + col, pv[b], valid);
+          } else {
 #pragma unroll
-        for (int j = 0; j < VW; ++j) {
-          const float g2 = gv[j] * gv[j];
-          cacc[j] += g2;
-          sg += g2;
-          sp += pv[j] * pv[j];
+            for (int j = 0; j < VW; ++j) gv[b][j] = pv[b][j] = 0.f;
+          }
         }
-        psq += (double)sp;
-        sg = warp_sum(sg);  // a warp never straddles two rows (TC >= 32)
-        if ((threadIdx.x & 31) == 0) rowbuf[(r - tl.r0) * nwr + wrow] = sg;
+#pragma unroll
+        for (int b = 0; b < kRB; ++b) {
+          const int64_t r = r0 + (int64_t)b * TR;
+          float sg = 0.f, sp = 0.f;
+#pragma unroll
+          for (int j = 0; j < VW; ++j) {
+            const float g2 = gv[b][j] * gv[b][j];
+            cacc[j] += g2;
+            sg += g2;
+            sp += pv[b][j] * pv[b][j];
+          }
+          psq += (double)sp;
+          sg = warp_sum(sg);  // a warp never straddles two rows (TC >= 32)
+          if ((threadIdx.x & 31) == 0 && r < tl.r1) rowbuf[(r - tl.r0) * nwr + wrow] = sg;
+        }
       }
       // column partials: fixed-order sum over the TR row groups
 #pragma unroll
@@ -309,10 +320,13 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// u for a factored element: u = (s*g) / sqrt(a_i*b_j + eps)   (optim.cpp:256-259)
+// u for a factored element: u = (s*g) / sqrt(a_i*b_j + eps)   (optim.cpp:256-259),
+// evaluated as (s*g) * rsqrt(.) -- MUFU.RSQ, <= 2 ulp -- instead of an IEEE sqrt and
+// an IEEE division: K4 reads 4 B/element and would otherwise be issue-bound.
+// K4 and K6 evaluate the identical expression, so both see the same u.
 __device__ __forceinline__ float u_fact(float g, float s, float a, float b, float eps) {
   const float gs = s * g;
-  return gs / sqrtf(a * b + eps);
+  return gs * rsqrtf(a * b + eps);
 }
 
 // ============================ K4: sum u^2 ============================================
@@ -335,17 +349,27 @@ __global__ void __launch_bounds__(kThreads)
         float bv[VW];
 #pragma unroll
         for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
-        for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
-          float gv[VW];
-          load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
-          const float a = c.fa[T.fa_off + r];
-          float su = 0.f;
+        for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB2 * TR) {
+          float gv[kRB2][VW];
 #pragma unroll
-          for (int j = 0; j < VW; ++j) {
-            const float u = u_fact(gv[j], sf, a, bv[j], epsf);
-            su += j < valid ? u * u : 0.f;
+          for (int b = 0; b < kRB2; ++b) {
+            const int64_t r = r0 + (int64_t)b * TR;
+            if (r < tl.r1) load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
           }
-          usq += (double)su;
+#pragma unroll
+          for (int b = 0; b < kRB2; ++b) {
+            const int64_t r = r0 + (int64_t)b * TR;
+            if (r < tl.r1) {
+              const float a = c.fa[T.fa_off + r];
+              float su = 0.f;
+#pragma unroll
+              for (int j = 0; j < VW; ++j) {
+                const float u = u_fact(gv[b][j], sf, a, bv[j], epsf);
+                su += j < valid ? u * u : 0.f;
+              }
+              usq += (double)su;
+            }
+          }
         }
       }
     } else {  // optim.cpp:262-267 with fp64 state
@@ -405,14 +429,27 @@ __global__ void __launch_bounds__(kThreads)
       float bv[VW];
 #pragma unroll
       for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
-      for (int64_t r = tl.r0 + tr; r < tl.r1; r += TR) {
-        float gv[VW], pv[VW];
-        load_vec<VEC, GT>(g + r * T.cols + col, gv, valid);
-        load_p<VEC>(p + r * T.cols + col, pv, valid);
-        const float a = c.fa[T.fa_off + r];
+      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB * TR) {
+        float gv[kRB][VW], pv[kRB][VW];
 #pragma unroll
-        for (int j = 0; j < VW; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
-        store_p<VEC>(p + r * T.cols + col, pv, valid);
+        for (int b = 0; b < kRB; ++b) {
+          const int64_t r = r0 + (int64_t)b * TR;
+          if (r < tl.r1) {
+            load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
+            load_p<VEC>(p + r * T.cols + col, pv[b], valid);
+          }
+        }
+#pragma unroll
+        for (int b = 0; b < kRB; ++b) {
+          const int64_t r = r0 + (int64_t)b * TR;
+          if (r < tl.r1) {
+            const float a = c.fa[T.fa_off + r];
+#pragma unroll
+            for (int j = 0; j < VW; ++j)
+              pv[b][j] = pv[b][j] - ff * u_fact(gv[b][j], sf, a, bv[j], epsf);
+            store_p<VEC>(p + r * T.cols + col, pv[b], valid);
+          }
+        }
       }
     } else {
       const double s = c.glob[0];

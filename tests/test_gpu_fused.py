@@ -82,7 +82,11 @@ def test_lomo_clip_matches_reference_two_pass(clip):
     optim.lomo_step(tp, tg, 0.1, clip)
     O.ref_lomo_fused(ps, gs, 0.1, clip)
     torch.cuda.synchronize()
-    np.testing.assert_allclose(tp.cpu().numpy(), np.concatenate(ps), rtol=1e-14, atol=0)
+    want = np.concatenate(ps)
+    # the reference sums g^2 in hook order, the device in a fixed tree: the clip
+    # scale may differ in its last bit, i.e. each p by <= ~1 ulp of |p|_max
+    np.testing.assert_allclose(tp.cpu().numpy(), want, rtol=0,
+                               atol=4 * np.finfo(np.float64).eps * np.abs(want).max())
 
 
 def test_lomo_lr_zero_is_noop():  # test_optim.cpp:248-257
