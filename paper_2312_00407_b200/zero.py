@@ -1,0 +1,183 @@
+"""ZeRO sharding of the optimizer step across GPUs (one process per GPU).
+
+Reference: the optimizer section of ParallelWorker (parallel.cpp:326-339 creation,
+626-681 step) over ZeroPlan (parallel.cpp:20-38).  North-star flow
+("ZeRO-1 style ... RS grads, AG params") = the reference's stage-2 branch
+(parallel.cpp:656-666):
+
+    owned_grads = reduce_scatter(flat_grads, SUM, plan.part_sizes)   # :657-658
+    FlatOptimizer::step(params[owned], owned_grads, lr)                # :660
+    params = all_gather(params[owned])                                 # :661-663
+
+Partition bookkeeping is ZeroPlan's, bit for bit (first P % N ranks own one
+more element).  Collectives go through torch.distributed: NCCL over NVLink on
+B200, gloo in the CPU tests.  Equal parts use reduce_scatter_tensor /
+all_gather_into_tensor; unequal parts (P % N != 0) fall back to one
+reduce / broadcast per part, which keeps the reference's ownership exactly.
+The grad reduction is a SUM, as the reference's (the backward seed already
+carries 1/global_count, parallel.cpp:516-522, 602).
+
+The single-kernel alternative -- reduce-scatter, update and all-gather fused
+over NVLink peer memory -- is `PeerShardedOptimizer` (csrc/peer.cu).
+"""
+from __future__ import annotations
+
+from typing import Callable, Optional
+
+from . import optim
+
+
+def _dist():
+    import torch.distributed as dist
+
+    return dist
+
+
+class ZeroPlan:
+    """parallel.hpp:22-29 / parallel.cpp:20-38 (computed by the C-ABI, mco_zero_plan)."""
+
+    def __init__(self, total_len: int, dp_size: int, stage: int = 2):
+        self.stage = stage
+        self.part_sizes, self.offsets = optim.zero_plan(total_len, dp_size, stage)
+
+    @staticmethod
+    def make(total_len: int, dp_size: int, stage: int = 2) -> "ZeroPlan":
+        return ZeroPlan(total_len, dp_size, stage)
+
+    def owned_range(self, dp_index: int) -> tuple[int, int]:
+        return self.offsets[dp_index], self.offsets[dp_index + 1]
+
+    @property
+    def even(self) -> bool:
+        return len(set(self.part_sizes)) <= 1
+
+
+def reduce_scatter_owned(flat, plan: ZeroPlan, rank: int, group=None):
+    """SUM-reduce `flat` and return this rank's owned slice (comm.cpp:219-246 semantics)."""
+    import torch
+
+    dist = _dist()
+    lo, hi = plan.owned_range(rank)
+    world = len(plan.part_sizes)
+    if world == 1:
+        return flat[lo:hi]
+    if plan.even:
+        out = torch.empty(hi - lo, dtype=flat.dtype, device=flat.device)
+        dist.reduce_scatter_tensor(out, flat, op=dist.ReduceOp.SUM, group=group)
+        return out
+    out = None
+    for r in range(world):
+        a, b = plan.owned_range(r)
+        part = flat[a:b].clone()
+        dist.reduce(part, dst=dist.get_global_rank(group, r) if group else r,
+                    op=dist.ReduceOp.SUM, group=group)
+        if r == rank:
+            out = part
+    return out
+
+
+def all_gather_owned(flat, plan: ZeroPlan, rank: int, group=None) -> None:
+    """In place: every rank's owned slice of `flat` broadcast to all (comm.cpp:207-217)."""
+    dist = _dist()
+    world = len(plan.part_sizes)
+    if world == 1:
+        return
+    lo, hi = plan.owned_range(rank)
+    if plan.even:
+        dist.all_gather_into_tensor(flat[:plan.offsets[-1]], flat[lo:hi].clone(), group=group)
+        return
+    for r in range(world):
+        a, b = plan.owned_range(r)
+        view = flat[a:b]
+        buf = view.clone() if not view.is_contiguous() else view
+        dist.broadcast(buf, src=dist.get_global_rank(group, r) if group else r, group=group)
+
+
+class ZeroShardedOptimizer:
+    """Sharded stored-state optimizer (AdamW / Lion / Adan / Sophia).
+
+    Each rank keeps optimizer state (and, with `mixed`, an fp32 master copy) for
+    its ZeroPlan-owned slice only.  flat_params are replicated (fp32, or bf16 when
+    mixed); flat_grads are each rank's local (unreduced) gradients.
+
+    local_step(p_owned, g_owned, lr, p_out_owned) defaults to the CUDA
+    FlatOptimizer over the owned slice; tests on CPU inject the oracle.
+    """
+
+    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, group=None, stage: int = 2,
+                 mixed: bool = False, master_init=None, device: Optional[int] = None,
+                 local_step: Optional[Callable] = None):
+        dist = _dist()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.plan = ZeroPlan.make(total_len, self.world, stage)
+        self.lo, self.hi = self.plan.owned_range(self.rank)
+        self.mixed = mixed
+        self.master = None
+        if mixed:
+            if master_init is None:
+                raise optim.ContractError("mixed sharding needs the fp32 master init slice")
+            self.master = master_init[self.lo:self.hi].float().clone()
+        self._local = local_step
+        if local_step is None:
+            dev = device if device is not None else 0
+            self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=dev)
+        else:
+            self.opt = None
+
+    def step(self, flat_params, flat_grads, lr: float) -> None:
+        g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group)
+        p_owned = flat_params[self.lo:self.hi]
+        if self._local is not None:
+            self._local(self.master if self.mixed else p_owned, g_owned, lr,
+                        p_owned if self.mixed else None)
+        elif self.mixed:
+            self.opt.step_mixed(self.master, g_owned.contiguous(), p_owned, lr)
+        else:
+            self.opt.step(p_owned, g_owned.contiguous(), lr)
+        all_gather_owned(flat_params, self.plan, self.rank, self.group)
+
+    def owned_range(self) -> tuple[int, int]:
+        return self.lo, self.hi
+
+    # checkpoint hand-off by buffer name (parallel.cpp:820-862)
+    def extract_state(self) -> dict:
+        out = {"steps": self.opt.steps_taken() if self.opt else 0, "buffers": {}}
+        if self.opt is not None:
+            for name, t in self.opt.buffers():
+                out["buffers"][name] = t.clone()
+        return out
+
+    def load_state(self, state: dict) -> None:
+        if self.opt is None:
+            return
+        for name, t in self.opt.buffers():
+            src = state["buffers"].get(name)
+            if src is not None and src.numel() == t.numel():  # match by name and size
+                t.copy_(src)
+        self.opt.set_steps_taken(state["steps"])
+
+
+class _CudaLomoOps:
+    sumsq = staticmethod(optim.sumsq)
+    apply = staticmethod(optim.lomo_apply)
+    apply_clipped = staticmethod(optim.lomo_apply_clipped)
+
+
+def sharded_lomo_step(p_owned, g_owned, lr: float, clip: Optional[float], group=None,
+                      stream=None, ops=_CudaLomoOps):
+    """LOMO over ZeRO shards with the global grad-norm clip (C5): local sum of
+    squares -> all_reduce(SUM) of one fp64 scalar -> scaled update.  The
+    reference forbids clipping in parallel runs (parallel.cpp:335-337); this is
+    the serial rule (optim.cpp:291-303) on the concatenated gradient.
+    `ops` is the kernel set (CUDA by default; CPU tests inject the oracle)."""
+    dist = _dist()
+    if clip is None:
+        ops.apply(p_owned, g_owned, lr, 1.0, stream)
+        return None
+    s = ops.sumsq(g_owned, stream=stream)
+    if dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    ops.apply_clipped(p_owned, g_owned, lr, s, clip, stream)
+    return s
