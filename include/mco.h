@@ -130,6 +130,26 @@ mco_status mco_flat_num_buffers(const mco_flat* h, int* out);
 mco_status mco_flat_buffer(mco_flat* h, int index, const char** name, void** dev_ptr,
                            uint64_t* len, int* dtype);
 
+/* ---- ZeRO step fused with its collectives (parallel.cpp:656-666) ------------
+ * One kernel per rank over NVLink peer memory: for the owned flat range
+ * [offset, offset+n): g = sum over r of grad_bufs[r][offset+i] (rank order),
+ * update master (f32, n elements, may alias this rank's f32 replica) and the
+ * optimizer state, then store the new parameter into param_bufs[r][offset+i]
+ * for every r (param_dtype F32 or BF16).  grad_bufs / param_bufs are device
+ * pointers valid on this device (own buffers or mco_peer_import'ed peers).
+ * The caller orders the ranks around the call (grads final before; replicas
+ * not read until every rank's call completed). */
+mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int grad_dtype,
+                               void* const* param_bufs, int param_dtype, int npeers,
+                               float* master, uint64_t offset, uint64_t n, double lr,
+                               void* stream);
+/* Symmetric buffers: cudaMalloc'ed base allocations and their 64-byte CUDA IPC handles. */
+mco_status mco_peer_alloc(uint64_t bytes, int device, void** out);
+mco_status mco_peer_free(void* p);
+mco_status mco_peer_export(void* p, void* handle_out_64);
+mco_status mco_peer_import(const void* handle_64, int device, void** out);
+mco_status mco_peer_close(void* p);
+
 /* ---- LOMO (optim.cpp:185-190, 284-318) ------------------------------------ */
 /* lomo_apply(Tensor& param, lr, scale): p -= (lr*scale) * g.
  * dtypes: F32/F32, BF16/BF16 (fp32 math, RNE store), F32/BF16, F64/F64. */

@@ -73,6 +73,13 @@ _SIGS = {
     "mco_flat_num_buffers": (_i, [_p, C.POINTER(_i)]),
     "mco_flat_buffer": (_i, [_p, _i, C.POINTER(C.c_char_p), C.POINTER(_p), C.POINTER(_u64),
                              C.POINTER(_i)]),
+    "mco_flat_step_peers": (_i, [_p, C.POINTER(_p), _i, C.POINTER(_p), _i, _i, _p, _u64, _u64,
+                                 _d, _p]),
+    "mco_peer_alloc": (_i, [_u64, _i, C.POINTER(_p)]),
+    "mco_peer_free": (_i, [_p]),
+    "mco_peer_export": (_i, [_p, _p]),
+    "mco_peer_import": (_i, [_p, _i, C.POINTER(_p)]),
+    "mco_peer_close": (_i, [_p]),
     "mco_lomo_apply": (_i, [_p, _i, _p, _i, _u64, _d, _d, _p]),
     "mco_lomo_apply_clipped": (_i, [_p, _i, _p, _i, _u64, _d, _p, _d, _p]),
     "mco_sumsq": (_i, [_p, _i, _u64, _p, _i, _p]),

@@ -17,6 +17,7 @@
 #include "adalomo.h"
 #include "kernels.h"
 #include "mco.h"
+#include "peer.h"
 
 namespace mco {
 
@@ -461,6 +462,64 @@ mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, ui
     *len = h->n;
     *dtype = h->state_dtype;
   });
+}
+
+// ---- ZeRO step fused with RS / AG over peer memory (peer.cu) ------------------------
+mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int grad_dtype,
+                               void* const* param_bufs, int param_dtype, int npeers,
+                               float* master, uint64_t offset, uint64_t n, double lr,
+                               void* stream) {
+  return guard([&] {
+    check_lengths(h, n, n);
+    if (h->state_dtype != MCO_F32)
+      throw Error(MCO_CONTRACT, "peer step: f32 optimizer state required");
+    if (!master) throw Error(MCO_CONTRACT, "peer step: master is null");
+    if (npeers < 1 || npeers > kMaxPeers)
+      throw Error(MCO_CONTRACT, "peer step: npeers must be 1.." + std::to_string(kMaxPeers));
+    PeerPtrs pp{};
+    pp.n = npeers;
+    for (int r = 0; r < npeers; ++r) {
+      if (!grad_bufs[r] || !param_bufs[r])
+        throw Error(MCO_CONTRACT, "peer step: null peer buffer");
+      pp.g[r] = grad_bufs[r];
+      pp.p[r] = param_bufs[r];
+    }
+    DeviceGuard dg(h->device);
+    ++h->t;
+    const auto kf = make_consts<float>(h->cfg, h->t, lr);
+    launch_peer_step(h->cfg.kind, pp, grad_dtype, param_dtype, master, h->slot, offset, n, kf,
+                     (cudaStream_t)stream);
+  });
+}
+
+// Symmetric buffers for the peer step: allocation + CUDA IPC export / import.
+mco_status mco_peer_alloc(uint64_t bytes, int device, void** out) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    MCO_CUDA_CHECK(cudaMalloc(out, std::max<uint64_t>(bytes, 1)));
+  });
+}
+mco_status mco_peer_free(void* p) {
+  return guard([&] { MCO_CUDA_CHECK(cudaFree(p)); });
+}
+mco_status mco_peer_export(void* p, void* handle_out) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    MCO_CUDA_CHECK(cudaIpcGetMemHandle(&h, p));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+mco_status mco_peer_import(const void* handle, int device, void** out) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    MCO_CUDA_CHECK(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+mco_status mco_peer_close(void* p) {
+  return guard([&] { MCO_CUDA_CHECK(cudaIpcCloseMemHandle(p)); });
 }
 
 // ---- LOMO -------------------------------------------------------------------------

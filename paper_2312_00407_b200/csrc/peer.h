@@ -1,0 +1,23 @@
+// Peer-memory (NVLink) ZeRO step: launch interface.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace mco {
+
+constexpr int kMaxPeers = 8;  // one 8x B200 NVSwitch domain
+
+struct PeerPtrs {
+  const void* g[kMaxPeers];  // every rank's flat gradient buffer (mapped)
+  void* p[kMaxPeers];        // every rank's flat parameter replica (mapped)
+  int n;
+};
+
+void launch_peer_step(int kind, const PeerPtrs& pp, int grad_dtype, int replica_dtype,
+                      float* master, void* const* state, uint64_t off, uint64_t n,
+                      const StepConsts<float>& k, cudaStream_t st);
+
+}  // namespace mco

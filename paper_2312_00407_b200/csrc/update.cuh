@@ -1,0 +1,76 @@
+// The per-element optimizer updates shared by the flat kernels (flat.cu) and the
+// peer-memory ZeRO kernel (peer.cu).  Operation order = optim.cpp:114-167.
+#pragma once
+
+#include "common.cuh"
+
+namespace mco {
+namespace upd {
+
+enum { K_ADAMW = 0, K_LION = 1, K_ADAN = 2, K_SOPHIA = 3 };
+
+__device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
+__device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
+
+// The per-element update, operation for operation as optim.cpp.
+template <int KIND, typename T>
+__device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
+                                       const StepConsts<T>& k) {
+  if constexpr (KIND == K_ADAMW) {  // optim.cpp:118-124; a = m, b = v
+    a = k.b1 * a + k.omb1 * g;
+    b = k.b2 * b + k.omb2 * g * g;
+    const T mhat = a / k.c1;
+    const T vhat = b / k.c2;
+    p = p - k.lr * (mhat / (dsqrt(vhat) + k.eps) + k.wd * p);
+  } else if constexpr (KIND == K_LION) {  // optim.cpp:129-134; a = m
+    const T u = k.b1 * a + k.omb1 * g;
+    const T s = u > T(0) ? T(1) : (u < T(0) ? T(-1) : T(0));  // sign(0) = 0
+    p = p - k.lr * (s + k.wd * p);
+    a = k.b2 * a + k.omb2 * g;
+  } else if constexpr (KIND == K_ADAN) {  // optim.cpp:142-154; a,b,c,d = m,v,n,g_prev
+    const T gd = k.first ? T(0) : g - d;
+    a = k.b1 * a + k.omb1 * g;
+    b = k.b2 * b + k.omb2 * gd;
+    const T nu = g + k.b2 * gd;
+    c = k.b3 * c + k.omb3 * nu * nu;
+    const T mhat = a / k.c1;
+    const T vhat = b / k.c2;
+    const T nhat = c / k.c3;
+    p = (p - k.lr * (mhat + k.b2 * vhat) / (dsqrt(nhat) + k.eps)) / k.den;
+    d = g;
+  } else {  // K_SOPHIA, optim.cpp:160-166; a = m, b = h
+    a = k.b1 * a + k.omb1 * g;
+    if (k.refresh) b = k.b2 * b + k.omb2 * g * g;  // squared-gradient proxy
+    const T rh = k.rho * b;
+    const T denom = rh < k.eps ? k.eps : rh;  // std::max(rho*h, eps)
+    const T q = a / denom;
+    const T u = q < T(-1) ? T(-1) : (T(1) < q ? T(1) : q);  // std::clamp
+    p = p - (k.lr * u + k.lrwd * p);
+  }
+}
+
+// ---- vector load helpers by element type -----------------------------------
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int W = 8;
+};
+template <>
+struct Vec<double> {
+  static constexpr int W = 4;
+};
+
+__device__ __forceinline__ void load_grad(const float* g, float (&r)[8]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ void load_grad(const uint16_t* g, float (&r)[8]) {
+  ld_stream_ro_bf16x8(g, r);
+}
+__device__ __forceinline__ void load_grad(const double* g, double (&r)[4]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ float load_grad1(const float* g) { return *g; }
+__device__ __forceinline__ float load_grad1(const uint16_t* g) { return bf2f(*g); }
+__device__ __forceinline__ double load_grad1(const double* g) { return *g; }
+
+constexpr bool reads_s1(int k) { return k == K_ADAMW || k == K_ADAN || k == K_SOPHIA; }
+
+}  // namespace upd
+}  // namespace mco

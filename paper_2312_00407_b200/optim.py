@@ -310,6 +310,22 @@ class FlatOptimizer:
     def config(self) -> OptimizerConfig:
         return self._cfg
 
+    def step_peers(self, grad_bufs, param_bufs, master, offset: int, n: int, lr: float,
+                   grad_dtype=None, param_dtype=None, stream=None) -> None:
+        """ZeRO step fused with reduce-scatter / all-gather over peer memory
+        (mco_flat_step_peers).  grad_bufs / param_bufs: device pointers (ints) or
+        CUDA tensors of every rank's flat buffers, this device's view of them."""
+        def ptr(x):
+            return x.data_ptr() if hasattr(x, "data_ptr") else int(x)
+
+        npeers = len(grad_bufs)
+        gd = grad_dtype if grad_dtype is not None else _dtype_code(grad_bufs[0])
+        pd = param_dtype if param_dtype is not None else _dtype_code(param_bufs[0])
+        ga = (C.c_void_p * npeers)(*[ptr(x) for x in grad_bufs])
+        pa = (C.c_void_p * npeers)(*[ptr(x) for x in param_bufs])
+        _check(lib.mco_flat_step_peers(self._h, ga, gd, pa, pd, npeers, ptr(master), int(offset),
+                                       int(n), float(lr), _stream(stream)))
+
 
 # ---- LOMO -------------------------------------------------------------------------------
 

@@ -181,3 +181,134 @@ def sharded_lomo_step(p_owned, g_owned, lr: float, clip: Optional[float], group=
         dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
     ops.apply_clipped(p_owned, g_owned, lr, s, clip, stream)
     return s
+
+
+class _PeerBuffer:
+    """A cudaMalloc'ed flat buffer whose CUDA IPC handle can be shared."""
+
+    def __init__(self, numel: int, dtype, device: int):
+        import ctypes as C
+
+        from ._lib import lib
+
+        self.numel, self.dtype, self.device = numel, dtype, device
+        self.esize = {"float32": 4, "bfloat16": 2}[str(dtype).split(".")[-1]]
+        p = C.c_void_p()
+        optim._check(lib.mco_peer_alloc(numel * self.esize, device, C.byref(p)))
+        self.ptr = p.value
+
+    def tensor(self):
+        import torch
+
+        code = optim.MCO_F32 if self.esize == 4 else optim.MCO_BF16
+        if code == optim.MCO_F32:
+            return optim._as_tensor(self.ptr, self.numel, optim.MCO_F32, self)
+        raw = torch.as_tensor(_U16View(self.ptr, self.numel, self), device="cuda")
+        return raw.view(torch.bfloat16)
+
+    def handle(self) -> bytes:
+        import ctypes as C
+
+        from ._lib import lib
+
+        buf = (C.c_char * 64)()
+        optim._check(lib.mco_peer_export(self.ptr, buf))
+        return bytes(buf)
+
+    def __del__(self):
+        from ._lib import lib
+
+        if getattr(self, "ptr", None):
+            lib.mco_peer_free(self.ptr)
+            self.ptr = None
+
+
+class _U16View:
+    def __init__(self, ptr, n, owner):
+        self._owner = owner
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<i2",
+                                         "data": (int(ptr), False), "version": 3,
+                                         "strides": None, "stream": None}
+
+
+class PeerShardedOptimizer:
+    """ZeRO step as ONE kernel per rank over NVLink peer memory (csrc/peer.cu):
+    the owned slice's gradients are summed straight out of every rank's grad
+    buffer, the update runs, and the new parameters are stored straight into
+    every rank's replica -- no reduced-gradient buffer, no separate NCCL
+    reduce-scatter / all-gather.  Same ZeroPlan ownership and same result as
+    ZeroShardedOptimizer (SUM of grads in rank order).
+
+    Buffers: `self.params` (replica, f32 or bf16) and `self.grads` (f32 or bf16)
+    are this rank's symmetric flat buffers; write gradients into self.grads,
+    call step(lr), read parameters from self.params.
+    """
+
+    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, group=None,
+                 param_dtype=None, grad_dtype=None, master_init=None, device: int = 0):
+        import ctypes as C
+
+        import torch
+
+        from ._lib import lib
+
+        dist = _dist()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = device
+        param_dtype = param_dtype or torch.float32
+        grad_dtype = grad_dtype or torch.float32
+        self.plan = ZeroPlan.make(total_len, self.world, 2)
+        self.lo, self.hi = self.plan.owned_range(self.rank)
+        self._pbuf = _PeerBuffer(total_len, param_dtype, device)
+        self._gbuf = _PeerBuffer(total_len, grad_dtype, device)
+        self.params, self.grads = self._pbuf.tensor(), self._gbuf.tensor()
+        # exchange IPC handles, map every peer's buffers
+        mine = (self._pbuf.handle(), self._gbuf.handle())
+        if self.world > 1:
+            allh = [None] * self.world
+            dist.all_gather_object(allh, mine, group=group)
+        else:
+            allh = [mine]
+        self._opened = []
+        self.pptrs, self.gptrs = [], []
+        for r, (ph, gh) in enumerate(allh):
+            if r == self.rank:
+                self.pptrs.append(self._pbuf.ptr)
+                self.gptrs.append(self._gbuf.ptr)
+                continue
+            pp, gp = C.c_void_p(), C.c_void_p()
+            optim._check(lib.mco_peer_import(C.c_char_p(ph), device, C.byref(pp)))
+            optim._check(lib.mco_peer_import(C.c_char_p(gh), device, C.byref(gp)))
+            self._opened += [pp.value, gp.value]
+            self.pptrs.append(pp.value)
+            self.gptrs.append(gp.value)
+        self._pd = optim._dtype_code(self.params)
+        self._gd = optim._dtype_code(self.grads)
+        if self._pd == optim.MCO_F32 and master_init is None:
+            self.master = self.params[self.lo:self.hi]  # the f32 replica is the master
+        else:
+            src = master_init if master_init is not None else self.params
+            self.master = src[self.lo:self.hi].float().contiguous().clone()
+        self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=device)
+
+    def _barrier(self):
+        dist = _dist()
+        if self.world > 1:  # stream-ordered rendezvous (one element all-reduce)
+            import torch
+
+            t = torch.zeros(1, device=self.params.device)
+            dist.all_reduce(t, group=self.group)
+
+    def step(self, lr: float, stream=None) -> None:
+        self._barrier()  # every rank's gradients are final
+        self.opt.step_peers(self.gptrs, self.pptrs, self.master, self.lo, self.hi - self.lo, lr,
+                            grad_dtype=self._gd, param_dtype=self._pd, stream=stream)
+        self._barrier()  # every replica is complete
+
+    def __del__(self):
+        from ._lib import lib
+
+        for p in getattr(self, "_opened", []):
+            lib.mco_peer_close(p)

@@ -1,0 +1,151 @@
+"""GPU tests of the ZeRO sharder.  Only one GPU is available, so the multi-rank
+peer-memory kernel is exercised with N *virtual* ranks on one device: N separate
+flat grad buffers and N parameter replicas, the kernel launched once per rank
+with that rank's ZeroPlan range -- the same pointers-to-every-rank layout the
+IPC-mapped multi-GPU run uses.  The NCCL paths run at world size 1."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2312_00407_b200 import optim, zero
+from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def cfg_for(kind):
+    c = OptimizerConfig.defaults_for(kind)
+    c.weight_decay = 0.01
+    return c
+
+
+@pytest.mark.parametrize("kind", [Kind.ADAMW, Kind.LION, Kind.ADAN, Kind.SOPHIA])
+@pytest.mark.parametrize("world,P", [(2, 1 << 16), (4, 100003), (8, 999)])
+def test_peer_kernel_virtual_ranks_equals_serial(kind, world, P):
+    cfg = cfg_for(kind)
+    plan = zero.ZeroPlan.make(P, world)
+    p0 = O.synth(P, 5, 0, 0, 0, 0, -6, 0, False)
+    replicas = [dev(p0) for _ in range(world)]
+    opts = [optim.FlatOptimizer(cfg, plan.part_sizes[r]) for r in range(world)]
+    serial, ps = O.OracleFlat(cfg, P, np.float32), p0.copy()
+    for t in range(1, 4):
+        gs = [O.synth(P, 5, 1, r, t, 0, -7, 10, False) for r in range(world)]
+        grads = [dev(g) for g in gs]
+        for r in range(world):  # rank r's kernel, master = its own f32 replica slice
+            lo, hi = plan.owned_range(r)
+            opts[r].step_peers(grads, replicas, replicas[r][lo:hi], lo, hi - lo, 1e-3)
+        gsum = gs[0].copy()
+        for g in gs[1:]:
+            gsum = gsum + g  # the kernel's rank-order fp32 sum
+        serial.step(ps, gsum, 1e-3)
+    torch.cuda.synchronize()
+    for r in range(world):  # every replica holds the full, bit-identical result
+        assert np.array_equal(replicas[r].cpu().numpy().view(np.uint32), ps.view(np.uint32))
+    for r in range(world):
+        lo, hi = plan.owned_range(r)
+        for name, buf in opts[r].buffers():
+            assert np.array_equal(buf.cpu().numpy().view(np.uint32),
+                                  serial.state[name][lo:hi].view(np.uint32)), (r, name)
+
+
+def test_peer_kernel_bf16_replicas_and_grads():
+    world, P = 4, 50000
+    cfg = cfg_for(Kind.ADAN)
+    plan = zero.ZeroPlan.make(P, world)
+    p0 = O.synth(P, 6, 0, 0, 0, 0, -6, 0, False)
+    replicas = [dev(O.f32_to_bf16(p0)).view(torch.bfloat16) for _ in range(world)]
+    masters = [dev(p0[plan.offsets[r]:plan.offsets[r + 1]]) for r in range(world)]
+    opts = [optim.FlatOptimizer(cfg, plan.part_sizes[r]) for r in range(world)]
+    serial, ps = O.OracleFlat(cfg, P, np.float32), p0.copy()
+    for t in (1, 2):
+        gb = [O.synth(P, 6, 1, r, t, 0, -7, 10, False, "bf16") for r in range(world)]
+        grads = [dev(g).view(torch.bfloat16) for g in gb]
+        for r in range(world):
+            lo, hi = plan.owned_range(r)
+            opts[r].step_peers(grads, replicas, masters[r], lo, hi - lo, 1e-3)
+        gsum = O.bf16_to_f32(gb[0]).copy()
+        for g in gb[1:]:
+            gsum = gsum + O.bf16_to_f32(g)
+        serial.step(ps, gsum, 1e-3)
+    torch.cuda.synchronize()
+    want = O.f32_to_bf16(ps)
+    for r in range(world):
+        assert np.array_equal(replicas[r].view(torch.int16).cpu().numpy().view(np.uint16), want)
+    got_master = np.concatenate([m.cpu().numpy() for m in masters])
+    assert np.array_equal(got_master.view(np.uint32), ps.view(np.uint32))
+
+
+@pytest.fixture(scope="module")
+def nccl1():
+    import torch.distributed as dist
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield
+    dist.destroy_process_group()
+
+
+def test_zero_sharded_nccl_world1_equals_flat(nccl1):
+    P = 123457
+    cfg = cfg_for(Kind.ADAMW)
+    p0 = O.synth(P, 7, 0, 0, 0, 0, -6, 0, False)
+    a, b = dev(p0), dev(p0)
+    z = zero.ZeroShardedOptimizer(cfg, P)
+    f = optim.FlatOptimizer(cfg, P)
+    for t in (1, 2):
+        g = dev(O.synth(P, 7, 1, 0, t, 0, -7, 10, False))
+        z.step(a, g, 1e-3)
+        f.step(b, g, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    st = z.extract_state()
+    z2 = zero.ZeroShardedOptimizer(cfg, P)
+    z2.load_state(st)
+    assert z2.opt.steps_taken() == 2
+    assert all(torch.equal(x, y) for (_, x), (_, y) in zip(z.opt.buffers(), z2.opt.buffers()))
+
+
+def test_peer_sharded_optimizer_world1(nccl1):
+    P = 77777
+    cfg = cfg_for(Kind.SOPHIA)
+    ps = zero.PeerShardedOptimizer(cfg, P)
+    p0 = O.synth(P, 8, 0, 0, 0, 0, -6, 0, False)
+    ps.params.copy_(dev(p0))
+    serial, want = O.OracleFlat(cfg, P, np.float32), p0.copy()
+    for t in (1, 2, 3):
+        g = O.synth(P, 8, 1, 0, t, 0, -7, 10, False)
+        ps.grads.copy_(dev(g))
+        ps.step(1e-3)
+        serial.step(want, g, 1e-3)
+    torch.cuda.synchronize()
+    assert np.array_equal(ps.params.cpu().numpy().view(np.uint32), want.view(np.uint32))
+
+
+def test_sharded_lomo_clip_world1(nccl1):
+    P = 65536
+    p0 = O.synth(P, 9, 0, 0, 0, 0, -6, 0, False, "bf16")
+    g = O.synth(P, 9, 1, 0, 1, 0, -7, 10, False, "bf16")
+    tp = dev(p0).view(torch.bfloat16)
+    s = zero.sharded_lomo_step(tp, dev(g).view(torch.bfloat16), 1e-2, 0.01)
+    total = O.orc.orc_sumsq_bf16(O._ptr(g), P)
+    assert s.item() == pytest.approx(total, rel=1e-10)
+    scale = O.orc.orc_clip_scale(total, 0.01)
+    want = p0.copy()
+    O.orc.orc_lomo_bf16(O._ptr(want), O._ptr(g), P, 1e-2, scale)
+    torch.cuda.synchronize()
+    got = tp.view(torch.int16).cpu().numpy().view(np.uint16)
+    # the device norm differs from the sequential one in the last bits -> scale
+    # may differ by 1 ulp; bf16 results may then differ by 1 ulp in rare ties
+    assert np.mean(got != want) < 1e-3
