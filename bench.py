@@ -321,7 +321,6 @@ def bench_e2e(args, res):
     hg = torch.empty(n, dtype=torch.float32, pin_memory=True)
     hp.copy_(res["p"][:n].cpu())
     hg.copy_(res["g"][:n].cpu())
-    dp, dg = res["p"][:n], res["g"][:n]
     steps = max(1, min(args.steps, args.e2e_steps))
     tot_s, h2d, d2h = 0.0, 0, 0
     per = {}
@@ -330,24 +329,20 @@ def bench_e2e(args, res):
         cfg = make_cfg(kind)
         opt = ada = one = None  # free the previous optimizer's device state first
         gc.collect()
+        hpn, hgn = hp.numpy(), hg.numpy()
         if kind in ("adamw", "lion", "adan", "sophia"):
             opt = optim.FlatOptimizer(cfg, n)
-            hpn, hgn = hp.numpy(), hg.numpy()
 
             def one():
                 opt.step(hpn, hgn, cfg.lr)  # mco_flat_step_host: pipelined H2D/step/D2H
-        else:
-            ada = optim.AdaLomoState(cfg, shapes) if kind == "adalomo" else None
+        elif kind == "adalomo":
+            ada = optim.AdaLomoState(cfg, shapes)
 
             def one():
-                dp.copy_(hp, non_blocking=True)
-                dg.copy_(hg, non_blocking=True)
-                if ada is not None:
-                    ada.apply_all(dp, dg, cfg.lr)
-                else:
-                    optim.lomo_apply(dp, dg, cfg.lr, 1.0)
-                hp.copy_(dp, non_blocking=True)
-                torch.cuda.synchronize()
+                ada.apply_all(hpn, hgn, cfg.lr)  # per-tensor H2D / apply / D2H pipeline
+        else:
+            def one():
+                optim.lomo_apply(hpn, hgn, cfg.lr, 1.0)  # mco_lomo_apply_host
         one()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -362,8 +357,9 @@ def bench_e2e(args, res):
         log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {n / dt / 1e9:.2f} Gparam/s")
     return {"value": len(per) * n / tot_s, "unit": "params/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "params": n, "per_optimizer": per,
-            "path": "C-ABI with pinned host buffers (mco_flat_step_host for the stored-state "
-                    "kinds; H2D + lomo_apply / apply_all + D2H for LOMO / AdaLomo)"}
+            "path": "C-ABI host-span calls on pinned host buffers: mco_flat_step_host, "
+                    "mco_lomo_apply_host, mco_adalomo_apply_all_host (H2D p+g, update, D2H p "
+                    "pipelined per chunk / per tensor)"}
 
 
 def main():

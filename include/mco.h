@@ -160,6 +160,11 @@ mco_status mco_lomo_apply(void* params, int param_dtype, const void* grads, int 
 mco_status mco_lomo_apply_clipped(void* params, int param_dtype, const void* grads,
                                   int grad_dtype, uint64_t n, double lr, const double* dev_sumsq,
                                   double clip, void* stream);
+/* lomo_apply over HOST arrays (the reference's Tensor data is host memory),
+ * pipelined through the device in chunks; clip >= 0 adds the global-norm pass
+ * (lomo_fused_backward_step's two passes, optim.cpp:291-316). Synchronous. */
+mco_status mco_lomo_apply_host(void* params, int param_dtype, const void* grads, int grad_dtype,
+                               uint64_t n, double lr, double scale, double clip);
 /* Σx² into *dev_out (fp64, deterministic fixed-order reduction);
  * accumulate != 0 adds to the existing value (optim.cpp:294-300 hook sum). */
 mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* dev_out, int accumulate,
@@ -187,6 +192,10 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int tensor_index, void* param, int 
 mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_params, int param_dtype,
                                  const void* flat_grads, int grad_dtype, double lr,
                                  void* stream);
+/* apply_all over HOST arrays: per-tensor H2D -> apply -> D2H pipeline on three
+ * streams (whole-set upload first when cfg.has_clip_threshold).  Synchronous. */
+mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* flat_params, int param_dtype,
+                                      const void* flat_grads, int grad_dtype, double lr);
 mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out); /* fp64 accounting */
 mco_status mco_adalomo_get_steps(const mco_adalomo* h, int tensor_index, int64_t* t);
 /* which: 0 v_row, 1 v_col, 2 v_full (fp64 device arrays; len 0 if absent). */

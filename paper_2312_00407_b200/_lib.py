@@ -83,6 +83,8 @@ _SIGS = {
     "mco_lomo_apply": (_i, [_p, _i, _p, _i, _u64, _d, _d, _p]),
     "mco_lomo_apply_clipped": (_i, [_p, _i, _p, _i, _u64, _d, _p, _d, _p]),
     "mco_sumsq": (_i, [_p, _i, _u64, _p, _i, _p]),
+    "mco_lomo_apply_host": (_i, [_p, _i, _p, _i, _u64, _d, _d, _d]),
+    "mco_adalomo_apply_all_host": (_i, [_p, _p, _i, _p, _i, _d]),
     "mco_adalomo_create": (_i, [_cfgp, _i, C.POINTER(_i), C.POINTER(_i64), _i, C.POINTER(_p)]),
     "mco_adalomo_destroy": (_i, [_p]),
     "mco_adalomo_apply": (_i, [_p, _i, _p, _i, _p, _i, _d, _p, _p]),

@@ -187,6 +187,58 @@ void* sumsq_ws(cudaStream_t st) {
   return p;
 }
 
+// Host-span staging: [H2D a, H2D b] -> kernel -> D2H a, chunk by chunk on two
+// streams, so both PCIe directions and the kernels overlap.  One staging set
+// per device (host-span calls are synchronous; the mutex serialises them).
+struct HostStage {
+  std::mutex mu;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  void* buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  uint64_t chunk_bytes = 0;
+};
+
+HostStage& host_stage(int dev) {
+  static std::mutex mu;
+  static std::unordered_map<int, HostStage*> stages;
+  std::lock_guard<std::mutex> lock(mu);
+  auto& s = stages[dev];
+  if (!s) {
+    s = new HostStage;
+    s->chunk_bytes = 8ull << 24;  // 16 Mi elements of <= 8 bytes
+    for (int i = 0; i < 2; ++i) {
+      MCO_CUDA_CHECK(cudaStreamCreateWithFlags(&s->st[i], cudaStreamNonBlocking));
+      MCO_CUDA_CHECK(cudaMalloc(&s->buf[i][0], s->chunk_bytes));
+      MCO_CUDA_CHECK(cudaMalloc(&s->buf[i][1], s->chunk_bytes));
+    }
+  }
+  return *s;
+}
+
+// fn(dev_a, dev_b, offset, count, stream) runs the kernel(s) for one chunk.
+template <class F>
+void host_pipeline(int dev, void* a, size_t as, const void* b, size_t bs, uint64_t n,
+                   bool write_back, F&& fn) {
+  HostStage& hs = host_stage(dev);
+  std::lock_guard<std::mutex> lock(hs.mu);
+  const uint64_t C = hs.chunk_bytes / 8;
+  int k = 0;
+  for (uint64_t off = 0; off < n; off += C, k ^= 1) {
+    const uint64_t m = std::min(C, n - off);
+    cudaStream_t st = hs.st[k];
+    MCO_CUDA_CHECK(cudaMemcpyAsync(hs.buf[k][0], (const char*)a + off * as, m * as,
+                                   cudaMemcpyHostToDevice, st));
+    if (b)
+      MCO_CUDA_CHECK(cudaMemcpyAsync(hs.buf[k][1], (const char*)b + off * bs, m * bs,
+                                     cudaMemcpyHostToDevice, st));
+    fn(hs.buf[k][0], hs.buf[k][1], off, m, st);
+    if (write_back)
+      MCO_CUDA_CHECK(cudaMemcpyAsync((char*)a + off * as, hs.buf[k][0], m * as,
+                                     cudaMemcpyDeviceToHost, st));
+  }
+  MCO_CUDA_CHECK(cudaStreamSynchronize(hs.st[0]));
+  MCO_CUDA_CHECK(cudaStreamSynchronize(hs.st[1]));
+}
+
 }  // namespace
 }  // namespace mco
 
@@ -201,24 +253,27 @@ struct mco_flat {
   int64_t t = 0;
   void* slot[4] = {nullptr, nullptr, nullptr, nullptr};  // kernel slots s0..s3
   std::vector<std::pair<const char*, void*>> named;       // buffers() order
-  // host-span path (lazily created)
-  cudaStream_t hs[2] = {nullptr, nullptr};
-  void* hbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
-  uint64_t hchunk = 0;
   ~mco_flat() {
     for (void* p : slot)
       if (p) cudaFree(p);
-    for (auto& b : hbuf)
-      for (void* p : b)
-        if (p) cudaFree(p);
-    for (auto s : hs)
-      if (s) cudaStreamDestroy(s);
   }
 };
 
 struct mco_adalomo {
   AdaLomoPlan plan;
+  // host-span path (lazily created): device copies of the flat set, 3 streams,
+  // per-tensor events for the H2D -> apply -> D2H pipeline
+  float* hp = nullptr;
+  void* hg = nullptr;
+  cudaStream_t hst[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_in, ev_out;
   ~mco_adalomo() {
+    if (hp) cudaFree(hp);
+    if (hg) cudaFree(hg);
+    for (auto s : hst)
+      if (s) cudaStreamDestroy(s);
+    for (auto e : ev_in) cudaEventDestroy(e);
+    for (auto e : ev_out) cudaEventDestroy(e);
     void* ptrs[] = {plan.d_tiles, plan.d_tensors, plan.d_item_off, plan.d_state,
                     plan.d_colpart, plan.d_rowpart, plan.d_tile_sc, plan.d_tens_sc,
                     plan.d_fa,    plan.d_fb,      plan.d_glob};
@@ -409,31 +464,11 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, c
     check_lengths(h, np, ng);
     check_dtypes(h, pdt, gdt);
     DeviceGuard dg(h->device);
-    const size_t ps = dtype_size(pdt), gs = dtype_size(gdt);
-    if (!h->hs[0]) {
-      h->hchunk = std::min<uint64_t>(std::max<uint64_t>(h->n, 1), 1ull << 24);  // 16 Mi elements
-      for (int i = 0; i < 2; ++i) {
-        MCO_CUDA_CHECK(cudaStreamCreateWithFlags(&h->hs[i], cudaStreamNonBlocking));
-        MCO_CUDA_CHECK(cudaMalloc(&h->hbuf[i][0], h->hchunk * 8));
-        MCO_CUDA_CHECK(cudaMalloc(&h->hbuf[i][1], h->hchunk * 8));
-      }
-    }
     ++h->t;
-    const uint64_t C = h->hchunk;
-    int k = 0;
-    for (uint64_t off = 0; off < np; off += C, k ^= 1) {
-      const uint64_t n = std::min(C, np - off);
-      cudaStream_t st = h->hs[k];
-      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hbuf[k][0], (const char*)params + off * ps, n * ps,
-                                     cudaMemcpyHostToDevice, st));
-      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hbuf[k][1], (const char*)grads + off * gs, n * gs,
-                                     cudaMemcpyHostToDevice, st));
-      flat_launch(h, h->hbuf[k][0], pdt, h->hbuf[k][1], gdt, nullptr, n, off, lr, st);
-      MCO_CUDA_CHECK(cudaMemcpyAsync((char*)params + off * ps, h->hbuf[k][0], n * ps,
-                                     cudaMemcpyDeviceToHost, st));
-    }
-    MCO_CUDA_CHECK(cudaStreamSynchronize(h->hs[0]));
-    MCO_CUDA_CHECK(cudaStreamSynchronize(h->hs[1]));
+    host_pipeline(h->device, params, dtype_size(pdt), grads, dtype_size(gdt), np, true,
+                  [&](void* dp, void* dg_, uint64_t off, uint64_t m, cudaStream_t st) {
+                    flat_launch(h, dp, pdt, dg_, gdt, nullptr, m, off, lr, st);
+                  });
   });
 }
 
@@ -533,6 +568,47 @@ mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint
   return guard([&] {
     if (!dev_sumsq) throw Error(MCO_CONTRACT, "lomo clip: device sum of squares is null");
     launch_lomo(p, pdt, g, gdt, n, lr, 1.0, dev_sumsq, clip, (cudaStream_t)stream);
+  });
+}
+
+// lomo_apply on host spans (the reference's Tensor data is host memory).
+// clip >= 0: two passes over the gradient -- sum of squares, then the update.
+mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                               double scale, double clip) {
+  return guard([&] {
+    const int dev = current_device();
+    const double* dnorm = nullptr;
+    double* acc = nullptr;
+    if (clip >= 0) {
+      MCO_CUDA_CHECK(cudaMalloc(&acc, sizeof(double)));
+      MCO_CUDA_CHECK(cudaMemset(acc, 0, sizeof(double)));
+      HostStage& hs = host_stage(dev);
+      host_pipeline(dev, const_cast<void*>(g), dtype_size(gdt), nullptr, 0, n, false,
+                    [&](void* dg_, void*, uint64_t, uint64_t m, cudaStream_t st) {
+                      // one accumulator, chunks strictly ordered through stream 0
+                      if (st != hs.st[0]) {
+                        cudaEvent_t ev;
+                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                        MCO_CUDA_CHECK(cudaEventRecord(ev, hs.st[0]));
+                        MCO_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                      }
+                      launch_sumsq(dg_, gdt, m, acc, 1, sumsq_ws(st), st);
+                      if (st != hs.st[0]) {
+                        cudaEvent_t ev;
+                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                        MCO_CUDA_CHECK(cudaEventRecord(ev, st));
+                        MCO_CUDA_CHECK(cudaStreamWaitEvent(hs.st[0], ev, 0));
+                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                      }
+                    });
+      dnorm = acc;
+    }
+    host_pipeline(dev, p, dtype_size(pdt), g, dtype_size(gdt), n, true,
+                  [&](void* dp, void* dg_, uint64_t, uint64_t m, cudaStream_t st) {
+                    launch_lomo(dp, pdt, dg_, gdt, m, lr, scale, dnorm, clip, st);
+                  });
+    if (acc) cudaFree(acc);
   });
 }
 
@@ -643,6 +719,76 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
     c.ext_sumsq = nullptr;
     launch_adalomo(h->plan, c, (cudaStream_t)stream);
     for (auto& T : h->plan.h_tensors) T.t += 1;
+  });
+}
+
+// Host spans (the reference's Tensor data lives in host memory): per tensor,
+// H2D(p_k, g_k) -> hook-form apply(k) -> D2H(p_k) on three streams, so tensor
+// k+1's upload overlaps tensor k's update and tensor k-1's download.  With a
+// global clip every gradient must be seen first: upload all, apply_all, download.
+mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const void* g, int gdt,
+                                      double lr) {
+  return guard([&] {
+    check_ada_dtypes(pdt, gdt);
+    auto& pl = h->plan;
+    DeviceGuard dg(pl.device);
+    const int nt = (int)pl.h_tensors.size();
+    const uint64_t total = nt ? (uint64_t)(pl.h_tensors.back().elem_off +
+                                           pl.h_tensors.back().numel) : 0;
+    const size_t gs = dtype_size(gdt);
+    if (!h->hp) {
+      MCO_CUDA_CHECK(cudaMalloc(&h->hp, std::max<uint64_t>(total, 1) * 4));
+      MCO_CUDA_CHECK(cudaMalloc(&h->hg, std::max<uint64_t>(total, 1) * 4));
+      for (auto& st : h->hst) MCO_CUDA_CHECK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+      h->ev_in.resize(nt);
+      h->ev_out.resize(nt);
+      for (int k = 0; k < nt; ++k) {
+        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_in[k], cudaEventDisableTiming));
+        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_out[k], cudaEventDisableTiming));
+      }
+    }
+    cudaStream_t up = h->hst[0], comp = h->hst[1], down = h->hst[2];
+    AdaLomoCall c{};
+    c.g_dtype = gdt;
+    c.lr = lr;
+    if (pl.cfg.has_clip_threshold) {
+      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hp, p, total * 4, cudaMemcpyHostToDevice, up));
+      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hg, g, total * gs, cudaMemcpyHostToDevice, up));
+      MCO_CUDA_CHECK(cudaStreamSynchronize(up));
+      c.t0 = 0;
+      c.t1 = nt;
+      c.p = h->hp;
+      c.g = h->hg;
+      c.single = 0;
+      c.use_clip = 1;
+      launch_adalomo(pl, c, comp);
+      MCO_CUDA_CHECK(cudaStreamSynchronize(comp));
+      MCO_CUDA_CHECK(cudaMemcpyAsync(p, h->hp, total * 4, cudaMemcpyDeviceToHost, down));
+    } else {
+      for (int k = 0; k < nt; ++k) {
+        const TensorInfo& T = pl.h_tensors[k];
+        const uint64_t off = (uint64_t)T.elem_off, n = (uint64_t)T.numel;
+        float* dp = h->hp + off;
+        char* dgp = (char*)h->hg + off * gs;
+        MCO_CUDA_CHECK(cudaMemcpyAsync(dp, (const float*)p + off, n * 4, cudaMemcpyHostToDevice, up));
+        MCO_CUDA_CHECK(cudaMemcpyAsync(dgp, (const char*)g + off * gs, n * gs,
+                                       cudaMemcpyHostToDevice, up));
+        MCO_CUDA_CHECK(cudaEventRecord(h->ev_in[k], up));
+        MCO_CUDA_CHECK(cudaStreamWaitEvent(comp, h->ev_in[k], 0));
+        c.t0 = k;
+        c.t1 = k + 1;
+        c.p = dp;
+        c.g = dgp;
+        c.single = 1;
+        c.use_clip = 0;
+        launch_adalomo(pl, c, comp);
+        MCO_CUDA_CHECK(cudaEventRecord(h->ev_out[k], comp));
+        MCO_CUDA_CHECK(cudaStreamWaitEvent(down, h->ev_out[k], 0));
+        MCO_CUDA_CHECK(cudaMemcpyAsync((float*)p + off, dp, n * 4, cudaMemcpyDeviceToHost, down));
+      }
+    }
+    for (auto st : h->hst) MCO_CUDA_CHECK(cudaStreamSynchronize(st));
+    for (auto& T : pl.h_tensors) T.t += 1;
   });
 }
 

@@ -331,7 +331,13 @@ class FlatOptimizer:
 
 
 def lomo_apply(param, grad, lr: float, scale: float = 1.0, stream=None) -> None:
-    """optim.cpp:185-190: param -= (lr*scale) * grad (in place)."""
+    """optim.cpp:185-190: param -= (lr*scale) * grad (in place).  numpy (host)
+    arrays go through the pipelined host path (mco_lomo_apply_host)."""
+    if isinstance(param, np.ndarray):
+        _check(lib.mco_lomo_apply_host(param.ctypes.data, _np_dtype_code(param),
+                                       grad.ctypes.data, _np_dtype_code(grad), param.size,
+                                       float(lr), float(scale), -1.0))
+        return
     _dev(param, "lomo param")
     _dev(grad, "lomo grad")
     if param.numel() != grad.numel():
@@ -366,7 +372,13 @@ def lomo_step(params, grads, lr: float, clip: Optional[float] = None, stream=Non
               grad_sumsq=None):
     """Flat-buffer form of lomo_fused_backward_step (optim.cpp:284-318): with a
     clip, one sum-of-squares pass then the scaled update; otherwise one pass.
-    `grad_sumsq` lets a caller supply an already all-reduced device norm^2."""
+    `grad_sumsq` lets a caller supply an already all-reduced device norm^2.
+    numpy (host) arrays: pipelined through the device (mco_lomo_apply_host)."""
+    if isinstance(params, np.ndarray):
+        _check(lib.mco_lomo_apply_host(params.ctypes.data, _np_dtype_code(params),
+                                       grads.ctypes.data, _np_dtype_code(grads), params.size,
+                                       float(lr), 1.0, -1.0 if clip is None else float(clip)))
+        return None
     if clip is None:
         lomo_apply(params, grads, lr, 1.0, stream)
         return None
@@ -412,7 +424,15 @@ class AdaLomoState:
 
     def apply_all(self, flat_params, flat_grads, lr: float, stream=None) -> None:
         """Every tensor in one multi-tensor pass over registry-order flat buffers;
-        global grad-norm clip when cfg.clip_threshold is set."""
+        global grad-norm clip when cfg.clip_threshold is set.  numpy (host) arrays:
+        per-tensor H2D / apply / D2H pipeline (mco_adalomo_apply_all_host)."""
+        if isinstance(flat_params, np.ndarray):
+            if flat_params.size != int(self.offsets[-1]) or flat_grads.size != flat_params.size:
+                raise ContractError("adalomo: flat buffer length does not match the registry")
+            _check(lib.mco_adalomo_apply_all_host(
+                self._h, flat_params.ctypes.data, _np_dtype_code(flat_params),
+                flat_grads.ctypes.data, _np_dtype_code(flat_grads), float(lr)))
+            return
         _dev(flat_params, "adalomo params")
         _dev(flat_grads, "adalomo grads")
         if flat_params.numel() != int(self.offsets[-1]) or flat_grads.numel() != int(

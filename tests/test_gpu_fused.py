@@ -265,3 +265,43 @@ def test_adalomo_config1_registry_vs_reference():
         a, b = int(st.offsets[k]), int(st.offsets[k + 1])
         ok, e = ada_tol_ok(got[a:b], ps[k], p0[k])
         assert ok, (k, shapes[k], e)
+
+
+def test_lomo_host_path_equals_device_path():
+    n = (1 << 24) + 999
+    p = O.synth(n, 12, 0, 0, 0, 0, -6, 0, False)
+    g = O.synth(n, 12, 1, 0, 1, 0, -7, 10, False)
+    hp = p.copy()
+    optim.lomo_apply(hp, g, 1e-2, 0.5)
+    tp = dev(p)
+    optim.lomo_apply(tp, dev(g), 1e-2, 0.5)
+    torch.cuda.synchronize()
+    assert bits_equal(hp, tp.cpu().numpy())
+    # with the global-norm clip (two passes over the host gradient)
+    hp2, tp2 = p.copy(), dev(p)
+    optim.lomo_step(hp2, g, 1e-2, clip=0.1)
+    optim.lomo_step(tp2, dev(g), 1e-2, clip=0.1)
+    torch.cuda.synchronize()
+    np.testing.assert_allclose(hp2, tp2.cpu().numpy(), rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("clip", [None, 1e-3])
+def test_adalomo_host_path_equals_device_path(clip):
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    cfg.clip_threshold = clip
+    ps, gs = ada_inputs(SHAPES, 2)
+    a, b = optim.AdaLomoState(cfg, SHAPES), optim.AdaLomoState(cfg, SHAPES)
+    hp = np.concatenate(ps).astype(np.float32)
+    tp = dev(hp)
+    for t in range(2):
+        g = np.concatenate(gs[t]).astype(np.float32)
+        a.apply_all(hp, g, 1e-2)
+        if clip is None:  # host path = per-tensor hook form
+            for k in range(len(SHAPES)):
+                s, e = int(b.offsets[k]), int(b.offsets[k + 1])
+                b.apply(k, tp[s:e], dev(g[s:e]), 1e-2)
+        else:
+            b.apply_all(tp, dev(g), 1e-2)
+    torch.cuda.synchronize()
+    assert bits_equal(hp, tp.cpu().numpy())
+    assert a.steps(0) == 2
