@@ -197,6 +197,17 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_params, int param_dt
 mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* flat_params, int param_dtype,
                                       const void* flat_grads, int grad_dtype, double lr);
 mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out); /* fp64 accounting */
+/* Row-split sharding across GPUs: tensor idx is a row slice of a
+ * (global_rows x C) matrix or a 1-D replica; weight scales its contribution to
+ * the all-reduced statistics (1 for slices; 1 on one rank, 0 elsewhere for replicas). */
+mco_status mco_adalomo_set_shard(mco_adalomo* h, int tensor_index, int64_t global_rows,
+                                 double weight);
+/* apply_all in phases: 1 = pass 1 + statistics payload, 2 = moments + sum u^2
+ * payload, 3 = update.  Sharded callers all-reduce (SUM) payload 0 between
+ * phases 1 and 2 and payload 1 between phases 2 and 3. */
+mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_params, int param_dtype,
+                             const void* flat_grads, int grad_dtype, double lr, void* stream);
+mco_status mco_adalomo_payload(mco_adalomo* h, int which, double** dev_ptr, uint64_t* len);
 mco_status mco_adalomo_get_steps(const mco_adalomo* h, int tensor_index, int64_t* t);
 /* which: 0 v_row, 1 v_col, 2 v_full (fp64 device arrays; len 0 if absent). */
 mco_status mco_adalomo_buffer(mco_adalomo* h, int tensor_index, int which, void** dev_ptr,

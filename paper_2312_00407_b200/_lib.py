@@ -90,6 +90,9 @@ _SIGS = {
     "mco_adalomo_apply": (_i, [_p, _i, _p, _i, _p, _i, _d, _p, _p]),
     "mco_adalomo_apply_all": (_i, [_p, _p, _i, _p, _i, _d, _p]),
     "mco_adalomo_state_bytes": (_i, [_p, C.POINTER(_u64)]),
+    "mco_adalomo_set_shard": (_i, [_p, _i, _i64, _d]),
+    "mco_adalomo_phase": (_i, [_p, _i, _p, _i, _p, _i, _d, _p]),
+    "mco_adalomo_payload": (_i, [_p, _i, C.POINTER(_p), C.POINTER(_u64)]),
     "mco_adalomo_get_steps": (_i, [_p, _i, C.POINTER(_i64)]),
     "mco_adalomo_buffer": (_i, [_p, _i, _i, C.POINTER(_p), C.POINTER(_u64)]),
     "mco_zero_plan": (_i, [_u64, _i, _i, C.POINTER(_u64), C.POINTER(_u64)]),

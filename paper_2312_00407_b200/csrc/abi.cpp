@@ -274,7 +274,8 @@ struct mco_adalomo {
       if (s) cudaStreamDestroy(s);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
-    void* ptrs[] = {plan.d_tiles, plan.d_tensors, plan.d_item_off, plan.d_state,
+    void* ptrs[] = {plan.d_tiles, plan.d_tensors, plan.d_item_off, plan.d_col_off,
+                    plan.d_payload, plan.d_state,
                     plan.d_colpart, plan.d_rowpart, plan.d_tile_sc, plan.d_tens_sc,
                     plan.d_fa,    plan.d_fb,      plan.d_glob};
     for (void* p : ptrs)
@@ -646,6 +647,8 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
     alloc(&pl.d_tiles, pl.h_tiles.size(), sizeof(Tile));
     alloc(&pl.d_tensors, pl.h_tensors.size(), sizeof(TensorInfo));
     alloc(&pl.d_item_off, pl.h_item_off.size(), sizeof(int64_t));
+    alloc(&pl.d_col_off, pl.h_col_off.size(), sizeof(int64_t));
+    alloc(&pl.d_payload, pl.stats_len + pl.usq_len, sizeof(double));
     alloc(&pl.d_state, pl.state_len, sizeof(double));
     alloc(&pl.d_colpart, pl.colpart_len, sizeof(float));
     alloc(&pl.d_rowpart, pl.rowpart_len, sizeof(double));
@@ -658,6 +661,8 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
                               cudaMemcpyHostToDevice));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_tensors, pl.h_tensors.data(),
                               pl.h_tensors.size() * sizeof(TensorInfo), cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(pl.d_col_off, pl.h_col_off.data(),
+                              pl.h_col_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_item_off, pl.h_item_off.data(),
                               pl.h_item_off.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     *out = h.release();
@@ -789,6 +794,69 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
     }
     for (auto st : h->hst) MCO_CUDA_CHECK(cudaStreamSynchronize(st));
     for (auto& T : pl.h_tensors) T.t += 1;
+  });
+}
+
+// ---- AdaLomo row-split sharding ---------------------------------------------------
+// Tensor `idx` holds a row slice of a global (global_rows x C) matrix (or a
+// replica of a 1-D tensor): statistics normalise by the global shape and the
+// payload contribution is scaled by `weight` (1 for a row slice, 1 on exactly
+// one rank for a replica, 0 elsewhere).
+mco_status mco_adalomo_set_shard(mco_adalomo* h, int idx, int64_t global_rows, double weight) {
+  return guard([&] {
+    auto& pl = h->plan;
+    if (idx < 0 || idx >= (int)pl.h_tensors.size())
+      throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
+    TensorInfo& T = pl.h_tensors[idx];
+    if (global_rows < T.rows)
+      throw Error(MCO_CONTRACT, "adalomo: global rows smaller than the local slice");
+    DeviceGuard dg(pl.device);
+    // keep the device-side step counter (advanced by k2_scalars)
+    MCO_CUDA_CHECK(cudaMemcpy(&T.t, &pl.d_tensors[idx].t, sizeof(int64_t),
+                              cudaMemcpyDeviceToHost));
+    T.rows_global = global_rows;
+    T.numel_global = T.factored ? global_rows * T.cols : T.numel;
+    T.weight = weight;
+    MCO_CUDA_CHECK(cudaMemcpy(&pl.d_tensors[idx], &T, sizeof(TensorInfo),
+                              cudaMemcpyHostToDevice));
+  });
+}
+
+// One phase of apply_all (1: stats, 2: moments + sum u^2, 3: update).  A
+// row-split caller all-reduces payload 0 after phase 1 and payload 1 after phase 2.
+mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_p, int pdt,
+                             const void* flat_g, int gdt, double lr, void* stream) {
+  return guard([&] {
+    check_ada_dtypes(pdt, gdt);
+    if (phase < 1 || phase > 3) throw Error(MCO_CONTRACT, "adalomo: phase must be 1, 2 or 3");
+    DeviceGuard dg(h->plan.device);
+    AdaLomoCall c{};
+    c.t0 = 0;
+    c.t1 = (int)h->plan.h_tensors.size();
+    c.p = flat_p;
+    c.g = flat_g;
+    c.g_dtype = gdt;
+    c.single = 0;
+    c.lr = lr;
+    c.use_clip = h->plan.cfg.has_clip_threshold ? 1 : 0;
+    launch_adalomo_phase(h->plan, c, phase, (cudaStream_t)stream);
+    if (phase == 3)
+      for (auto& T : h->plan.h_tensors) T.t += 1;
+  });
+}
+
+// which 0: stats payload (3 per tensor + column sums), 1: sum u^2 payload.
+mco_status mco_adalomo_payload(mco_adalomo* h, int which, double** dev_ptr, uint64_t* len) {
+  return guard([&] {
+    if (which == 0) {
+      *dev_ptr = h->plan.d_payload;
+      *len = (uint64_t)h->plan.stats_len;
+    } else if (which == 1) {
+      *dev_ptr = h->plan.d_payload + h->plan.stats_len;
+      *len = (uint64_t)h->plan.usq_len;
+    } else {
+      throw Error(MCO_CONTRACT, "adalomo: payload must be 0 or 1");
+    }
   });
 }
 

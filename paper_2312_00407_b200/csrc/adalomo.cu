@@ -47,6 +47,9 @@ struct Ctx {
   float* fa;          // a_i per factored tensor row
   float* fb;          // b_j per factored tensor column
   double* glob;       // [0] = clip scale s, [1] = global sum g^2
+  double* pay;        // stats payload: 3 per tensor (gsq, psq, vrs) | column sums
+  double* pay_usq;    // usq payload: 1 per tensor
+  int64_t ntens;      // total tensors (payload layout)
 };
 
 enum { TS_GSQ = 0, TS_PSQ, TS_VRS, TS_CORR, TS_LRT, TS_ROWMEAN, TS_USQ, TS_F, kTensScalars };
@@ -215,16 +218,36 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// ============================ K2: per-tensor scalars ===============================
-// One CTA of 1024 threads.  Warp w handles tensors w, w+32, ...; tile sums are
-// lane-strided + butterfly (fixed order).  Then the global sum of g^2 over the
-// call's tensors in tensor order, the clip scale, and the per-tensor scalars.
-__global__ void __launch_bounds__(1024)
-    k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
-               const double* ext_sumsq) {
-  __shared__ double red[32];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = t0 + warp; k < t1; k += 32) {
+// ============================ KR: tile partials -> payload ===========================
+// Blocks [0, ncolblk): one thread per column of the factored tensors in [t0,t1):
+// fixed-order sum of the tile column partials.  Block ncolblk: one warp per
+// tensor, fixed-order sums of the tile scalars.  Everything is scaled by the
+// tensor's shard weight (1, or 0 on ranks that hold a replica another rank
+// already contributes), so an all-reduce of the payload yields global sums.
+__global__ void __launch_bounds__(kThreads)
+    kr_stats(Ctx c, int t0, int t1, const int64_t* __restrict__ col_off, int64_t ncols,
+             int ncolblk) {
+  if ((int)blockIdx.x < ncolblk) {
+    const int64_t gi = col_off[t0] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= col_off[t0] + ncols) return;
+    int lo = t0, hi = t1 - 1;  // largest k with col_off[k] <= gi
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (col_off[mid] <= gi)
+        lo = mid;
+      else
+        hi = mid - 1;
+    }
+    const TensorInfo T = c.tensors[lo];
+    const int64_t j = gi - col_off[lo];
+    double acc = 0.0;
+    for (int64_t rb = 0; rb < T.nrb; ++rb)
+      acc += (double)c.colpart[T.colpart_off + rb * T.cols + j];
+    c.pay[3 * c.ntens + T.fb_off + j] = T.weight * acc;
+    return;
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = t0 + warp; k < t1; k += nw) {
     const TensorInfo T = c.tensors[k];
     double ps = 0, gs = 0, vr = 0;
     for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) {
@@ -236,10 +259,37 @@ __global__ void __launch_bounds__(1024)
     gs = warp_sum(gs);
     vr = warp_sum(vr);
     if (lane == 0) {
-      c.tens_sc[k * kTensScalars + TS_PSQ] = ps;
-      c.tens_sc[k * kTensScalars + TS_GSQ] = gs;
-      c.tens_sc[k * kTensScalars + TS_VRS] = vr;
+      c.pay[k * 3 + 0] = T.weight * gs;
+      c.pay[k * 3 + 1] = T.weight * ps;
+      c.pay[k * 3 + 2] = T.weight * vr;
     }
+  }
+}
+
+__global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = t0 + warp; k < t1; k += 32) {
+    const TensorInfo T = c.tensors[k];
+    double us = 0;
+    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += c.tile_sc[i * 4 + 3];
+    us = warp_sum(us);
+    if (lane == 0) c.pay_usq[k] = T.weight * us;
+  }
+}
+
+// ============================ K2: per-tensor scalars ===============================
+// One CTA of 1024 threads.  Warp w handles tensors w, w+32, ...; tile sums are
+// lane-strided + butterfly (fixed order).  Then the global sum of g^2 over the
+// call's tensors in tensor order, the clip scale, and the per-tensor scalars.
+__global__ void __launch_bounds__(1024)
+    k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
+               const double* ext_sumsq) {
+  __shared__ double red[32];
+  // per-tensor sums arrive (already all-reduced across ranks when sharded) in the payload
+  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
+    c.tens_sc[k * kTensScalars + TS_GSQ] = c.pay[k * 3 + 0];
+    c.tens_sc[k * kTensScalars + TS_PSQ] = c.pay[k * 3 + 1];
+    c.tens_sc[k * kTensScalars + TS_VRS] = c.pay[k * 3 + 2];
   }
   __syncthreads();
   double G = 0;
@@ -263,7 +313,7 @@ __global__ void __launch_bounds__(1024)
     const int64_t t = T.t + 1;  // optim.cpp:219
     Tm->t = t;
     const double corr = 1.0 - pow(b2, (double)t);
-    const double n = (double)T.numel;
+    const double n = (double)T.numel_global;
     const double rms_theta = sqrt(c.tens_sc[k * kTensScalars + TS_PSQ] / n);
     const double lr_t = lr * fmax(1e-3, rms_theta);
     double row_mean = 0.0;
@@ -271,7 +321,7 @@ __global__ void __launch_bounds__(1024)
       const double gsq = s * s * c.tens_sc[k * kTensScalars + TS_GSQ];
       const double sum_new =
           b2 * c.tens_sc[k * kTensScalars + TS_VRS] + (1 - b2) * (gsq / (double)T.cols);
-      row_mean = sum_new / ((double)T.rows * corr);
+      row_mean = sum_new / ((double)T.rows_global * corr);
     }
     c.tens_sc[k * kTensScalars + TS_CORR] = corr;
     c.tens_sc[k * kTensScalars + TS_LRT] = lr_t;
@@ -309,11 +359,9 @@ __global__ void __launch_bounds__(kThreads)
       c.fa[T.fa_off + i] = (float)(vr / corr);
     } else {  // column j: optim.cpp:247-248
       const int64_t j = local - T.rows;
-      double acc = 0.0;
-      for (int64_t rb = 0; rb < T.nrb; ++rb)
-        acc += (double)c.colpart[T.colpart_off + rb * T.cols + j];
+      const double acc = c.pay[3 * c.ntens + T.fb_off + j];  // all-reduced column sum
       double& vc = c.state[T.vcol_off + j];
-      vc = b2 * vc + (1 - b2) * (s2 * acc / (double)T.rows);
+      vc = b2 * vc + (1 - b2) * (s2 * acc / (double)T.rows_global);
       const double rm = c.tens_sc[lo * kTensScalars + TS_ROWMEAN];
       c.fb[T.fb_off + j] = (float)((vc / corr) / fmax(rm, 1e-300));
     }
@@ -391,18 +439,13 @@ __global__ void __launch_bounds__(kThreads)
 // ============================ K5: damping ==============================================
 __global__ void __launch_bounds__(1024)
     k5_damp(Ctx c, int t0, int t1, double adalomo_clip) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = t0 + warp; k < t1; k += 32) {
+  for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
     const TensorInfo T = c.tensors[k];
-    double us = 0;
-    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += c.tile_sc[i * 4 + 3];
-    us = warp_sum(us);
-    if (lane == 0) {  // optim.cpp:269-273
-      const double rms_u = sqrt(us / (double)T.numel);
-      const double damp = fmax(1.0, rms_u / adalomo_clip);
-      c.tens_sc[k * kTensScalars + TS_USQ] = us;
-      c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
-    }
+    const double us = c.pay_usq[k];
+    const double rms_u = sqrt(us / (double)T.numel_global);
+    const double damp = fmax(1.0, rms_u / adalomo_clip);
+    c.tens_sc[k * kTensScalars + TS_USQ] = us;
+    c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
   }
 }
 
@@ -473,49 +516,56 @@ int grid_for(K kernel, int64_t ntiles, int device) {
 }
 
 template <bool VEC, typename GT>
-void run_passes(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
-  Ctx c{pl.d_tiles,  pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
-        pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,   pl.d_fb,      pl.d_glob};
+void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaStream_t st) {
+  Ctx c{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
+        pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
+        pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size()};
   Ptrs P{(float*)call.p, call.g, call.single};
   const int dev = current_device();
   const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
   const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
   const auto& cfg = pl.cfg;
+  const int64_t sms = device_info(dev).sms;
 
-  auto kk1 = k1_stats<VEC, GT>;
-  kk1<<<grid_for(kk1, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles);
-  launch_check("adalomo k1_stats");
-
-  k2_scalars<<<1, 1024, 0, st>>>(c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
-                                 cfg.clip_threshold, call.ext_sumsq);
-  launch_check("adalomo k2_scalars");
-
-  const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
-  if (nitems > 0) {
-    const int64_t blocks =
-        std::min<int64_t>((nitems + kThreads - 1) / kThreads, (int64_t)device_info(dev).sms * 8);
-    k3_moments<<<(unsigned)blocks, kThreads, 0, st>>>(
-        c, call.t0, call.t1, pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
-    launch_check("adalomo k3_moments");
+  if (phase == 1) {  // pass 1 over {g, p} + reduction of the tile partials into the payload
+    auto kk1 = k1_stats<VEC, GT>;
+    kk1<<<grid_for(kk1, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles);
+    launch_check("adalomo k1_stats");
+    const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
+    const int ncolblk = (int)((ncols + kThreads - 1) / kThreads);
+    kr_stats<<<ncolblk + 1, kThreads, 0, st>>>(c, call.t0, call.t1, pl.d_col_off, ncols, ncolblk);
+    launch_check("adalomo kr_stats");
+  } else if (phase == 2) {  // scalars, moments, pass 2 over {g}
+    k2_scalars<<<1, 1024, 0, st>>>(c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
+                                   cfg.clip_threshold, call.ext_sumsq);
+    launch_check("adalomo k2_scalars");
+    const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
+    if (nitems > 0) {
+      const int64_t blocks = std::min<int64_t>((nitems + kThreads - 1) / kThreads, sms * 8);
+      k3_moments<<<(unsigned)blocks, kThreads, 0, st>>>(
+          c, call.t0, call.t1, pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
+      launch_check("adalomo k3_moments");
+    }
+    auto kk4 = k4_usq<VEC, GT>;
+    kk4<<<grid_for(kk4, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.beta2, cfg.eps);
+    launch_check("adalomo k4_usq");
+    kr_usq<<<1, 1024, 0, st>>>(c, call.t0, call.t1);
+    launch_check("adalomo kr_usq");
+  } else {  // damping + pass 3 over {g, p -> p}
+    k5_damp<<<1, 1024, 0, st>>>(c, call.t0, call.t1, cfg.adalomo_clip);
+    launch_check("adalomo k5_damp");
+    auto kk6 = k6_update<VEC, GT>;
+    kk6<<<grid_for(kk6, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.eps);
+    launch_check("adalomo k6_update");
   }
-
-  auto kk4 = k4_usq<VEC, GT>;
-  kk4<<<grid_for(kk4, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.beta2, cfg.eps);
-  launch_check("adalomo k4_usq");
-
-  k5_damp<<<1, 1024, 0, st>>>(c, call.t0, call.t1, cfg.adalomo_clip);
-  launch_check("adalomo k5_damp");
-
-  auto kk6 = k6_update<VEC, GT>;
-  kk6<<<grid_for(kk6, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.eps);
-  launch_check("adalomo k6_update");
 }
 
 }  // namespace
 
-void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
+void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase,
+                          cudaStream_t st) {
   if (call.t1 <= call.t0) return;
-  // 8-wide path: every factored tensor in the call has C % 8 == 0 and 32 B
+  // 256-bit path: every factored tensor in the call has C % 8 == 0 and 32 B
   // (f32) / 16 B (bf16) aligned rows.
   const size_t gsz = call.g_dtype == MCO_BF16 ? 2 : 4;
   bool vec = true;
@@ -528,17 +578,21 @@ void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t
   }
   if (call.g_dtype == MCO_F32) {
     if (vec)
-      run_passes<true, float>(pl, call, st);
+      run_phase<true, float>(pl, call, phase, st);
     else
-      run_passes<false, float>(pl, call, st);
+      run_phase<false, float>(pl, call, phase, st);
   } else if (call.g_dtype == MCO_BF16) {
     if (vec)
-      run_passes<true, uint16_t>(pl, call, st);
+      run_phase<true, uint16_t>(pl, call, phase, st);
     else
-      run_passes<false, uint16_t>(pl, call, st);
+      run_phase<false, uint16_t>(pl, call, phase, st);
   } else {
     throw Error(MCO_CONTRACT, "adalomo: grads must be f32 or bf16");
   }
+}
+
+void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
+  for (int phase = 1; phase <= 3; ++phase) launch_adalomo_phase(pl, call, phase, st);
 }
 
 }  // namespace mco
@@ -555,6 +609,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
   pl.h_tensors.clear();
   pl.h_tiles.clear();
   pl.h_item_off.assign(1, 0);
+  pl.h_col_off.assign(1, 0);
   int64_t elem = 0, state = 0, colpart = 0, rowpart = 0, fa = 0, fb = 0;
   const int64_t min_tiles = 2LL * sms;
   for (size_t k = 0; k < shapes.size(); ++k) {
@@ -605,6 +660,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
           pl.h_tiles.push_back(tl);
         }
       pl.h_item_off.push_back(pl.h_item_off.back() + T.rows + T.cols);
+      pl.h_col_off.push_back(pl.h_col_off.back() + T.cols);
     } else {
       T.rows = numel;
       T.cols = 1;
@@ -625,9 +681,13 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
         if (numel == 0) break;
       }
       pl.h_item_off.push_back(pl.h_item_off.back());
+      pl.h_col_off.push_back(pl.h_col_off.back());
     }
     T.tile_end = (int64_t)pl.h_tiles.size();
     T.t = 0;
+    T.rows_global = T.rows;
+    T.numel_global = T.numel;
+    T.weight = 1.0;
     elem += numel;
     pl.h_tensors.push_back(T);
   }
@@ -636,6 +696,8 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
   pl.rowpart_len = rowpart;
   pl.fa_len = fa;
   pl.fb_len = fb;
+  pl.stats_len = 3 * (int64_t)pl.h_tensors.size() + fb;
+  pl.usq_len = (int64_t)pl.h_tensors.size();
 }
 
 }  // namespace mco

@@ -30,6 +30,10 @@ struct TensorInfo {
   int64_t colpart_off, rowpart_off, fa_off, fb_off;
   int64_t tile_begin, tile_end;
   int64_t t;  // per-entry step counter (optim.hpp:93), advanced on the device
+  // row-split sharding: statistics normalise by the global shape; the payload
+  // contribution is scaled by `weight` (0 on ranks holding a duplicate replica)
+  int64_t rows_global, numel_global;
+  double weight;
 };
 
 struct AdaLomoPlan {
@@ -38,11 +42,15 @@ struct AdaLomoPlan {
   std::vector<TensorInfo> h_tensors;
   std::vector<Tile> h_tiles;
   std::vector<int64_t> h_item_off;  // per tensor prefix of (rows + cols) for factored
+  std::vector<int64_t> h_col_off;   // per tensor prefix of cols for factored
   int64_t state_len = 0, colpart_len = 0, rowpart_len = 0, fa_len = 0, fb_len = 0;
+  int64_t stats_len = 0, usq_len = 0;  // payload: [3 per tensor | column sums] + [usq]
   // device
   Tile* d_tiles = nullptr;
   TensorInfo* d_tensors = nullptr;
   int64_t* d_item_off = nullptr;
+  int64_t* d_col_off = nullptr;
+  double* d_payload = nullptr;  // stats_len + usq_len doubles
   double* d_state = nullptr;
   float* d_colpart = nullptr;
   double* d_rowpart = nullptr;
@@ -67,6 +75,10 @@ struct AdaLomoCall {
 // Build the host tile plan for `shapes` (registry order) on a device with `sms` SMs.
 void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>& shapes,
                         int sms);
+// phase 1: K1 + payload reduction; phase 2: K2, K3, K4 + usq payload; phase 3: K5, K6.
+// Between phases a sharded caller all-reduces the payload (row-split tensors).
+void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase,
+                          cudaStream_t st);
 void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st);
 
 }  // namespace mco

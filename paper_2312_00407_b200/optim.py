@@ -447,6 +447,23 @@ class AdaLomoState:
         _check(lib.mco_adalomo_state_bytes(self._h, C.byref(out)))
         return out.value
 
+    # ---- row-split sharding (csrc: mco_adalomo_set_shard / _phase / _payload) ----
+    def set_shard(self, index: int, global_rows: int, weight: float) -> None:
+        _check(lib.mco_adalomo_set_shard(self._h, int(index), int(global_rows), float(weight)))
+
+    def phase(self, phase: int, flat_params, flat_grads, lr: float, stream=None) -> None:
+        _dev(flat_params, "adalomo params")
+        _dev(flat_grads, "adalomo grads")
+        _check(lib.mco_adalomo_phase(self._h, int(phase), flat_params.data_ptr(),
+                                     _dtype_code(flat_params), flat_grads.data_ptr(),
+                                     _dtype_code(flat_grads), float(lr), _stream(stream)))
+
+    def payload(self, which: int):
+        """fp64 device view of the statistics (0) or sum-u^2 (1) payload."""
+        ptr, ln = C.c_void_p(), C.c_uint64()
+        _check(lib.mco_adalomo_payload(self._h, int(which), C.byref(ptr), C.byref(ln)))
+        return _as_tensor(ptr.value, ln.value, MCO_F64, self)
+
     def steps(self, index: int) -> int:
         t = C.c_int64()
         _check(lib.mco_adalomo_get_steps(self._h, int(index), C.byref(t)))

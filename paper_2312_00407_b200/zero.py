@@ -312,3 +312,70 @@ class PeerShardedOptimizer:
 
         for p in getattr(self, "_opened", []):
             lib.mco_peer_close(p)
+
+
+class RowShardedAdaLomo:
+    """AdaLomo with every matrix split by rows across the ranks (SURVEY 8(e), C3 at
+    8 GPUs); 1-D tensors are replicated.  Row slices follow ZeroPlan over each
+    matrix's rows.  Per step, two all-reduces (SUM) of fp64 payloads:
+      1. per-tensor [sum g^2, sum p^2, sum v_row_old] + every matrix's column sums
+         (the column statistics of a row-split matrix, optim.cpp:241-249),
+      2. per-tensor sum u^2 (the update-RMS damping, optim.cpp:269-272).
+    Row statistics stay local (rows are whole on a rank).  Replicated tensors
+    contribute from rank 0 only (weight 0 elsewhere) and are updated identically
+    everywhere.  The reference's own TP variant computes stats per local shard
+    (parallel.cpp:334, 593-594) and is NOT serial AdaLomo; this is."""
+
+    def __init__(self, cfg: optim.OptimizerConfig, shapes, group=None, device: int = 0,
+                 rank: Optional[int] = None, world: Optional[int] = None):
+        dist = _dist()
+        self.group = group
+        if world is None:  # explicit rank/world: single-process (virtual-rank) use
+            world = dist.get_world_size(group) if dist.is_initialized() else 1
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world, self.rank = world, rank
+        self.global_shapes = [tuple(s) for s in shapes]
+        self.local_shapes, self.pieces, self._shard = [], [], []
+        goff = 0
+        for s in self.global_shapes:
+            n = 1
+            for d in s:
+                n *= d
+            if len(s) == 2:
+                parts, offs = optim.zero_plan(s[0], self.world, 1)
+                r0, r1 = offs[self.rank], offs[self.rank + 1]
+                self.local_shapes.append((r1 - r0, s[1]))
+                self.pieces.append((goff + r0 * s[1], (r1 - r0) * s[1]))
+                self._shard.append((s[0], 1.0))
+            else:
+                self.local_shapes.append(s)
+                self.pieces.append((goff, n))
+                self._shard.append((s[0] if s else 1, 1.0 if self.rank == 0 else 0.0))
+            goff += n
+        self.state = optim.AdaLomoState(cfg, self.local_shapes, device=device)
+        for k, (rows, w) in enumerate(self._shard):
+            self.state.set_shard(k, rows, w)
+        self.local_numel = int(self.state.offsets[-1])
+
+    def scatter(self, flat_global):
+        """This rank's local flat buffer (registry order of local slices)."""
+        import torch
+
+        return torch.cat([flat_global[a:a + n] for a, n in self.pieces])
+
+    def gather_into(self, local, flat_global) -> None:
+        off = 0
+        for a, n in self.pieces:
+            flat_global[a:a + n].copy_(local[off:off + n])
+            off += n
+
+    def step(self, local_p, local_g, lr: float, stream=None) -> None:
+        dist = _dist()
+        multi = self.world > 1 and dist.is_initialized()
+        self.state.phase(1, local_p, local_g, lr, stream)
+        if multi:
+            dist.all_reduce(self.state.payload(0), op=dist.ReduceOp.SUM, group=self.group)
+        self.state.phase(2, local_p, local_g, lr, stream)
+        if multi:
+            dist.all_reduce(self.state.payload(1), op=dist.ReduceOp.SUM, group=self.group)
+        self.state.phase(3, local_p, local_g, lr, stream)

@@ -149,3 +149,60 @@ def test_sharded_lomo_clip_world1(nccl1):
     # the device norm differs from the sequential one in the last bits -> scale
     # may differ by 1 ulp; bf16 results may then differ by 1 ulp in rare ties
     assert np.mean(got != want) < 1e-3
+
+
+@pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_row_sharded_adalomo_virtual_ranks_equals_serial(world):
+    """Row-split AdaLomo (column-statistic and sum-u^2 all-reduces) == serial AdaLomo
+    (the compiled reference) on the whole matrices."""
+    from test_gpu_fused import SHAPES, ada_inputs, ada_tol_ok
+
+    shapes = SHAPES + [(7, 24), (2, 16)]  # rows < world on some ranks
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    ranks = [zero.RowShardedAdaLomo(cfg, shapes, rank=r, world=world) for r in range(world)]
+    ps, gs = ada_inputs(shapes, 3)
+    p0 = [x.copy() for x in ps]
+    flat_p = dev(np.concatenate(ps).astype(np.float32))
+    ref = O.RefAdaLomo(cfg, shapes)
+    for t in range(3):
+        flat_g = dev(np.concatenate(gs[t]).astype(np.float32))
+        lp = [rk.scatter(flat_p) for rk in ranks]
+        lg = [rk.scatter(flat_g) for rk in ranks]
+        for phase in (1, 2, 3):
+            for r, rk in enumerate(ranks):
+                rk.state.phase(phase, lp[r], lg[r], 5e-3)
+            if phase < 3:  # the all-reduce, in rank order
+                pays = [rk.state.payload(phase - 1) for rk in ranks]
+                total = pays[0].clone()
+                for x in pays[1:]:
+                    total += x
+                for x in pays:
+                    x.copy_(total)
+        for r, rk in enumerate(ranks):
+            rk.gather_into(lp[r], flat_p)
+        for k in range(len(shapes)):
+            ref.apply(k, ps[k], gs[t][k], 5e-3)
+    torch.cuda.synchronize()
+    got = flat_p.cpu().numpy()
+    offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+    for k in range(len(shapes)):
+        ok, e = ada_tol_ok(got[offs[k]:offs[k + 1]], ps[k], p0[k])
+        assert ok, (k, shapes[k], e)
+
+
+def test_row_sharded_adalomo_world1_nccl(nccl1):
+    from test_gpu_fused import SHAPES, ada_inputs
+
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    rs = zero.RowShardedAdaLomo(cfg, SHAPES)
+    plain = optim.AdaLomoState(cfg, SHAPES)
+    ps, gs = ada_inputs(SHAPES, 2)
+    a = dev(np.concatenate(ps).astype(np.float32))
+    b = a.clone()
+    for t in range(2):
+        g = dev(np.concatenate(gs[t]).astype(np.float32))
+        rs.step(a, g, 1e-2)
+        plain.apply_all(b, g, 1e-2)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
