@@ -143,6 +143,18 @@ mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int gr
                                void* const* param_bufs, int param_dtype, int npeers,
                                float* master, uint64_t offset, uint64_t n, double lr,
                                void* stream);
+/* LOMO fused with its collectives (C5): sum of squares of the rank-summed
+ * gradient over the owned range (all-reduce it across ranks for the global
+ * norm), then p = p - f * sum_r g_r written into every rank's replica, f =
+ * lr*scale or the clip rule on dev_sumsq.  master: f32 owned copy or NULL
+ * (then param_bufs[0] supplies the current value). */
+mco_status mco_sumsq_peers(const void* const* grad_bufs, int grad_dtype, int npeers,
+                           uint64_t offset, uint64_t n, double* dev_out, void* stream);
+mco_status mco_lomo_apply_peers(const void* const* grad_bufs, int grad_dtype,
+                                void* const* param_bufs, int param_dtype, int npeers,
+                                float* master, uint64_t offset, uint64_t n, double lr,
+                                double scale, const double* dev_sumsq, double clip,
+                                void* stream);
 /* Symmetric buffers: cudaMalloc'ed base allocations and their 64-byte CUDA IPC handles. */
 mco_status mco_peer_alloc(uint64_t bytes, int device, void** out);
 mco_status mco_peer_free(void* p);

@@ -75,6 +75,9 @@ _SIGS = {
                              C.POINTER(_i)]),
     "mco_flat_step_peers": (_i, [_p, C.POINTER(_p), _i, C.POINTER(_p), _i, _i, _p, _u64, _u64,
                                  _d, _p]),
+    "mco_sumsq_peers": (_i, [C.POINTER(_p), _i, _i, _u64, _u64, _p, _p]),
+    "mco_lomo_apply_peers": (_i, [C.POINTER(_p), _i, C.POINTER(_p), _i, _i, _p, _u64, _u64, _d,
+                                  _d, _p, _d, _p]),
     "mco_peer_alloc": (_i, [_u64, _i, C.POINTER(_p)]),
     "mco_peer_free": (_i, [_p]),
     "mco_peer_export": (_i, [_p, _p]),

@@ -528,6 +528,47 @@ mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int gr
   });
 }
 
+namespace {
+PeerPtrs make_peers(const void* const* grad_bufs, void* const* param_bufs, int npeers) {
+  if (npeers < 1 || npeers > kMaxPeers)
+    throw Error(MCO_CONTRACT, "peer step: npeers must be 1.." + std::to_string(kMaxPeers));
+  PeerPtrs pp{};
+  pp.n = npeers;
+  for (int r = 0; r < npeers; ++r) {
+    if (!grad_bufs[r] || (param_bufs && !param_bufs[r]))
+      throw Error(MCO_CONTRACT, "peer step: null peer buffer");
+    pp.g[r] = grad_bufs[r];
+    pp.p[r] = param_bufs ? param_bufs[r] : nullptr;
+  }
+  return pp;
+}
+}  // namespace
+
+// (sum over ranks of g_r)^2 summed over this rank's owned range, into *dev_out.
+mco_status mco_sumsq_peers(const void* const* grad_bufs, int grad_dtype, int npeers,
+                           uint64_t offset, uint64_t n, double* dev_out, void* stream) {
+  return guard([&] {
+    const PeerPtrs pp = make_peers(grad_bufs, nullptr, npeers);
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_peer_sumsq(pp, grad_dtype, offset, n, dev_out, sumsq_ws(st), st);
+  });
+}
+
+// LOMO fused with its collectives: p = p - f * sum_r g_r over the owned range,
+// written into every rank's replica; f = lr*scale, or from the all-reduced
+// dev_sumsq and clip (optim.cpp:302-303) when dev_sumsq is not null.
+mco_status mco_lomo_apply_peers(const void* const* grad_bufs, int grad_dtype,
+                                void* const* param_bufs, int param_dtype, int npeers,
+                                float* master, uint64_t offset, uint64_t n, double lr,
+                                double scale, const double* dev_sumsq, double clip,
+                                void* stream) {
+  return guard([&] {
+    const PeerPtrs pp = make_peers(grad_bufs, param_bufs, npeers);
+    launch_peer_lomo(pp, grad_dtype, param_dtype, master, offset, n, lr, scale, dev_sumsq, clip,
+                     (cudaStream_t)stream);
+  });
+}
+
 // Symmetric buffers for the peer step: allocation + CUDA IPC export / import.
 mco_status mco_peer_alloc(uint64_t bytes, int device, void** out) {
   return guard([&] {

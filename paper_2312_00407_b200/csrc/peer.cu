@@ -106,6 +106,64 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// ---- LOMO over peer memory (C5: bf16 LOMO across 8 GPUs with the global clip) ---
+// pass A: sum over the owned range of (sum over ranks of g_r)^2 -> per-block fp64
+// partials -> last CTA sums them in block order (deterministic);
+// pass B: p_r[i] = p - f * sum_r g_r[i] for every rank's replica, f from the
+// all-reduced sum of squares (optim.cpp:302-303) or lr*scale.
+template <typename GT>
+__global__ void __launch_bounds__(kThreads)
+    peer_sumsq_kernel(PeerPtrs pp, uint64_t off, uint64_t n, double* out, double* partials,
+                      unsigned* counter) {
+  __shared__ double scratch[32];
+  __shared__ bool is_last;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  double acc = 0.0;
+  for (uint64_t e = tid; e < n; e += stride) {
+    float g = ldg1((const GT*)pp.g[0] + off + e);
+    for (int r = 1; r < pp.n; ++r) g = g + ldg1((const GT*)pp.g[r] + off + e);
+    acc += (double)g * (double)g;
+  }
+  const double b = block_sum(acc, scratch);
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = b;
+    __threadfence();
+    is_last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += ((volatile double*)partials)[i];
+    s = block_sum(s, scratch);
+    if (threadIdx.x == 0) {
+      *out = s;
+      *counter = 0u;
+    }
+  }
+}
+
+template <typename GT, typename RT>
+__global__ void __launch_bounds__(kThreads)
+    peer_lomo_kernel(PeerPtrs pp, float* master, uint64_t off, uint64_t n, double lr,
+                     double scale, const double* sumsq, double clip) {
+  if (sumsq) {
+    const double norm = sqrt(*sumsq);
+    scale = (norm > clip && norm > 0) ? clip / norm : 1.0;
+  }
+  const float f = (float)(lr * scale);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t e = tid; e < n; e += stride) {
+    float g = ldg1((const GT*)pp.g[0] + off + e);
+    for (int r = 1; r < pp.n; ++r) g = g + ldg1((const GT*)pp.g[r] + off + e);
+    const float p = (master ? master[e] : ldg1((const RT*)pp.p[0] + off + e)) - f * g;
+    if (master) master[e] = p;
+    for (int r = 0; r < pp.n; ++r) st1((RT*)pp.p[r] + off + e, p);
+  }
+}
+
 inline bool al(const void* p, size_t b) { return ((uintptr_t)p % b) == 0; }
 
 template <int KIND, typename GT, typename RT>
@@ -143,6 +201,45 @@ void dispatch(const PeerPtrs& pp, int gdt, int rdt, float* master, void* const* 
 }
 
 }  // namespace
+
+void launch_peer_lomo(const PeerPtrs& pp, int grad_dtype, int replica_dtype, float* master,
+                      uint64_t off, uint64_t n, double lr, double scale, const double* sumsq,
+                      double clip, cudaStream_t st) {
+  if (n == 0) return;
+  const uint64_t blocks = std::min<uint64_t>((n + kThreads - 1) / kThreads,
+                                             (uint64_t)device_info(current_device()).sms * 8);
+  auto go = [&](auto kern) {
+    kern<<<(unsigned)blocks, kThreads, 0, st>>>(pp, master, off, n, lr, scale, sumsq, clip);
+    launch_check("peer_lomo_kernel");
+  };
+  if (grad_dtype == MCO_F32 && replica_dtype == MCO_F32)
+    go(peer_lomo_kernel<float, float>);
+  else if (grad_dtype == MCO_BF16 && replica_dtype == MCO_BF16)
+    go(peer_lomo_kernel<uint16_t, uint16_t>);
+  else if (grad_dtype == MCO_F32 && replica_dtype == MCO_BF16)
+    go(peer_lomo_kernel<float, uint16_t>);
+  else if (grad_dtype == MCO_BF16 && replica_dtype == MCO_F32)
+    go(peer_lomo_kernel<uint16_t, float>);
+  else
+    throw Error(MCO_CONTRACT, "peer lomo: grads / replicas must be f32 or bf16");
+}
+
+void launch_peer_sumsq(const PeerPtrs& pp, int grad_dtype, uint64_t off, uint64_t n, double* out,
+                       void* ws, cudaStream_t st) {
+  double* partials = (double*)ws;
+  unsigned* counter = (unsigned*)((char*)ws + 1024 * sizeof(double));
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(
+      (n + kThreads - 1) / kThreads, std::min<uint64_t>(1024, device_info(current_device()).sms * 4)));
+  if (grad_dtype == MCO_F32)
+    peer_sumsq_kernel<float><<<(unsigned)blocks, kThreads, 0, st>>>(pp, off, n, out, partials,
+                                                                     counter);
+  else if (grad_dtype == MCO_BF16)
+    peer_sumsq_kernel<uint16_t><<<(unsigned)blocks, kThreads, 0, st>>>(pp, off, n, out, partials,
+                                                                        counter);
+  else
+    throw Error(MCO_CONTRACT, "peer sumsq: grads must be f32 or bf16");
+  launch_check("peer_sumsq_kernel");
+}
 
 void launch_peer_step(int kind, const PeerPtrs& pp, int grad_dtype, int replica_dtype,
                       float* master, void* const* state, uint64_t off, uint64_t n,

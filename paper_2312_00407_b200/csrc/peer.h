@@ -20,4 +20,13 @@ void launch_peer_step(int kind, const PeerPtrs& pp, int grad_dtype, int replica_
                       float* master, void* const* state, uint64_t off, uint64_t n,
                       const StepConsts<float>& k, cudaStream_t st);
 
+// LOMO fused with RS / AG: optional global-norm pass (peer_sumsq) then the update
+// written into every rank's replica.  master (f32, may be null -> rank 0's
+// replica is read as the current parameter).  ws: sumsq_ws_bytes() workspace.
+void launch_peer_sumsq(const PeerPtrs& pp, int grad_dtype, uint64_t off, uint64_t n, double* out,
+                       void* ws, cudaStream_t st);
+void launch_peer_lomo(const PeerPtrs& pp, int grad_dtype, int replica_dtype, float* master,
+                      uint64_t off, uint64_t n, double lr, double scale, const double* sumsq,
+                      double clip, cudaStream_t st);
+
 }  // namespace mco

@@ -231,21 +231,13 @@ class _U16View:
                                          "strides": None, "stream": None}
 
 
-class PeerShardedOptimizer:
-    """ZeRO step as ONE kernel per rank over NVLink peer memory (csrc/peer.cu):
-    the owned slice's gradients are summed straight out of every rank's grad
-    buffer, the update runs, and the new parameters are stored straight into
-    every rank's replica -- no reduced-gradient buffer, no separate NCCL
-    reduce-scatter / all-gather.  Same ZeroPlan ownership and same result as
-    ZeroShardedOptimizer (SUM of grads in rank order).
+class PeerBuffers:
+    """This rank's symmetric flat parameter replica + gradient buffer, and every
+    rank's mapping of them (CUDA IPC handles exchanged over the process group).
+    On one device with several processes (tests) the same IPC path is used."""
 
-    Buffers: `self.params` (replica, f32 or bf16) and `self.grads` (f32 or bf16)
-    are this rank's symmetric flat buffers; write gradients into self.grads,
-    call step(lr), read parameters from self.params.
-    """
-
-    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, group=None,
-                 param_dtype=None, grad_dtype=None, master_init=None, device: int = 0):
+    def __init__(self, total_len: int, group=None, param_dtype=None, grad_dtype=None,
+                 device: int = 0):
         import ctypes as C
 
         import torch
@@ -257,14 +249,10 @@ class PeerShardedOptimizer:
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device
-        param_dtype = param_dtype or torch.float32
-        grad_dtype = grad_dtype or torch.float32
-        self.plan = ZeroPlan.make(total_len, self.world, 2)
-        self.lo, self.hi = self.plan.owned_range(self.rank)
-        self._pbuf = _PeerBuffer(total_len, param_dtype, device)
-        self._gbuf = _PeerBuffer(total_len, grad_dtype, device)
+        self.total_len = total_len
+        self._pbuf = _PeerBuffer(total_len, param_dtype or torch.float32, device)
+        self._gbuf = _PeerBuffer(total_len, grad_dtype or torch.float32, device)
         self.params, self.grads = self._pbuf.tensor(), self._gbuf.tensor()
-        # exchange IPC handles, map every peer's buffers
         mine = (self._pbuf.handle(), self._gbuf.handle())
         if self.world > 1:
             allh = [None] * self.world
@@ -284,34 +272,92 @@ class PeerShardedOptimizer:
             self._opened += [pp.value, gp.value]
             self.pptrs.append(pp.value)
             self.gptrs.append(gp.value)
-        self._pd = optim._dtype_code(self.params)
-        self._gd = optim._dtype_code(self.grads)
-        if self._pd == optim.MCO_F32 and master_init is None:
-            self.master = self.params[self.lo:self.hi]  # the f32 replica is the master
-        else:
-            src = master_init if master_init is not None else self.params
-            self.master = src[self.lo:self.hi].float().contiguous().clone()
-        self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=device)
+        self.pdt = optim._dtype_code(self.params)
+        self.gdt = optim._dtype_code(self.grads)
 
-    def _barrier(self):
+    def barrier(self) -> None:
+        """Order the ranks around a peer kernel.  NCCL: a one-element all-reduce on
+        the stream (no host sync).  Other backends: host sync + barrier."""
+        import torch
+
         dist = _dist()
-        if self.world > 1:  # stream-ordered rendezvous (one element all-reduce)
-            import torch
-
-            t = torch.zeros(1, device=self.params.device)
-            dist.all_reduce(t, group=self.group)
-
-    def step(self, lr: float, stream=None) -> None:
-        self._barrier()  # every rank's gradients are final
-        self.opt.step_peers(self.gptrs, self.pptrs, self.master, self.lo, self.hi - self.lo, lr,
-                            grad_dtype=self._gd, param_dtype=self._pd, stream=stream)
-        self._barrier()  # every replica is complete
+        if self.world == 1:
+            return
+        if dist.get_backend(self.group) == "nccl":
+            dist.all_reduce(torch.zeros(1, device=self.params.device), group=self.group)
+        else:
+            torch.cuda.synchronize()
+            dist.barrier(group=self.group)
 
     def __del__(self):
         from ._lib import lib
 
         for p in getattr(self, "_opened", []):
             lib.mco_peer_close(p)
+
+
+class PeerShardedOptimizer:
+    """ZeRO step as ONE kernel per rank over NVLink peer memory (csrc/peer.cu):
+    the owned slice's gradients are summed straight out of every rank's grad
+    buffer, the update runs, and the new parameters are stored straight into
+    every rank's replica -- no reduced-gradient buffer, no separate NCCL
+    reduce-scatter / all-gather.  Same ZeroPlan ownership and same result as
+    ZeroShardedOptimizer (SUM of grads in rank order).
+
+    Write gradients into `self.grads`, call step(lr), read `self.params`.
+    Stored-state kinds keep state (+ fp32 master for bf16 replicas) for the owned
+    slice; LOMO keeps nothing (optionally the global-norm clip, C5).
+    """
+
+    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, group=None,
+                 param_dtype=None, grad_dtype=None, master_init=None, device: int = 0,
+                 buffers: Optional[PeerBuffers] = None):
+        self.cfg = cfg
+        self.buf = buffers or PeerBuffers(total_len, group, param_dtype, grad_dtype, device)
+        b = self.buf
+        self.world, self.rank = b.world, b.rank
+        self.params, self.grads = b.params, b.grads
+        self.plan = ZeroPlan.make(total_len, self.world, 2)
+        self.lo, self.hi = self.plan.owned_range(self.rank)
+        if b.pdt == optim.MCO_F32 and master_init is None:
+            self.master = self.params[self.lo:self.hi]  # the f32 replica is the master
+        else:
+            src = master_init if master_init is not None else self.params
+            self.master = src[self.lo:self.hi].float().contiguous().clone()
+        self.lomo = cfg.kind == optim.Kind.LOMO
+        self.opt = None if self.lomo else optim.FlatOptimizer(cfg, self.hi - self.lo,
+                                                              device=device)
+        self._norm = None
+
+    def step(self, lr: float, stream=None) -> None:
+        import ctypes as C
+
+        import torch
+
+        from ._lib import lib
+
+        b = self.buf
+        b.barrier()  # every rank's gradients are final
+        if self.lomo:
+            n = self.hi - self.lo
+            ga = (C.c_void_p * self.world)(*b.gptrs)
+            pa = (C.c_void_p * self.world)(*b.pptrs)
+            sumsq = None
+            if self.cfg.clip_threshold is not None:
+                if self._norm is None:
+                    self._norm = torch.zeros((), dtype=torch.float64, device=self.params.device)
+                optim._check(lib.mco_sumsq_peers(ga, b.gdt, self.world, self.lo, n,
+                                                 self._norm.data_ptr(), optim._stream(stream)))
+                if self.world > 1:
+                    _dist().all_reduce(self._norm, group=b.group)
+                sumsq = self._norm.data_ptr()
+            optim._check(lib.mco_lomo_apply_peers(
+                ga, b.gdt, pa, b.pdt, self.world, self.master.data_ptr(), self.lo, n, float(lr),
+                1.0, sumsq, float(self.cfg.clip_threshold or 0.0), optim._stream(stream)))
+        else:
+            self.opt.step_peers(b.gptrs, b.pptrs, self.master, self.lo, self.hi - self.lo, lr,
+                                grad_dtype=b.gdt, param_dtype=b.pdt, stream=stream)
+        b.barrier()  # every replica is complete
 
 
 class RowShardedAdaLomo:

@@ -206,3 +206,79 @@ def test_row_sharded_adalomo_world1_nccl(nccl1):
         plain.apply_all(b, g, 1e-2)
     torch.cuda.synchronize()
     assert torch.equal(a, b)
+
+
+def _ipc_worker(rank, world, port, kind, P, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in (root, os.path.join(root, "oracle")):
+        sys.path.insert(0, p)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    from paper_2312_00407_b200 import zero
+    from paper_2312_00407_b200.optim import OptimizerConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    try:
+        cfg = OptimizerConfig.defaults_for(kind)
+        cfg.weight_decay = 0.0
+        if kind == 4:
+            cfg.clip_threshold = 0.05
+        ps = zero.PeerShardedOptimizer(cfg, P)
+        ps.params.copy_(torch.from_numpy(O.synth(P, 21, 0, 0, 0, 0, -6, 0, False)).cuda())
+        for t in (1, 2, 3):
+            g = O.synth(P, 21, 1, rank, t, 0, -7, 10, False)
+            ps.grads.copy_(torch.from_numpy(g).cuda())
+            torch.cuda.synchronize()
+            ps.step(1e-3)
+        torch.cuda.synchronize()
+        q.put((rank, ps.params.cpu().numpy()))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kind", [Kind.ADAMW, Kind.LOMO])
+def test_peer_sharded_two_processes_ipc_one_gpu(kind):
+    """Two OS processes on one B200, each mapping the other's buffers through CUDA
+    IPC: the real multi-process PeerShardedOptimizer path (gloo control plane)."""
+    import torch.multiprocessing as mp
+
+    P, world = 100001, 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, world, port, int(kind), P, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    want = O.synth(P, 21, 0, 0, 0, 0, -6, 0, False)
+    cfg = OptimizerConfig.defaults_for(kind)
+    cfg.weight_decay = 0.0
+    orc = O.OracleFlat(cfg, P, np.float32) if kind != Kind.LOMO else None
+    for t in (1, 2, 3):
+        g = O.synth(P, 21, 1, 0, t, 0, -7, 10, False) + O.synth(P, 21, 1, 1, t, 0, -7, 10, False)
+        if orc is not None:
+            orc.step(want, g, 1e-3)
+        else:
+            scale = O.orc.orc_clip_scale(float(np.dot(g.astype(np.float64), g)), 0.05)
+            O.orc.orc_lomo_f32(O._ptr(want), O._ptr(g), P, 1e-3, scale)
+    for r in range(world):
+        if orc is not None:
+            assert np.array_equal(res[r].view(np.uint32), want.view(np.uint32))
+        else:  # the clip norm is summed in a different order than the oracle's
+            np.testing.assert_allclose(res[r], want, rtol=0, atol=1e-7)
+    assert np.array_equal(res[0], res[1])
