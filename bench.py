@@ -169,16 +169,30 @@ def make_cfg(kind: str):
 
 
 class Stepper:
-    """One optimizer over (a shard of) the flat registry buffers, via the public API."""
+    """One optimizer over (a shard of) the flat registry buffers, via the public API.
+    N > 1: stored-state kinds and LOMO update this rank's ZeroPlan slice (gradients
+    already reduced); AdaLomo runs row-split (zero.RowShardedAdaLomo) on its local
+    row slices with its two statistic all-reduces inside the step."""
 
-    def __init__(self, kind, shapes, p, g, owned=None):
-        from paper_2312_00407_b200 import optim
+    def __init__(self, kind, shapes, p, g, world=1):
+        import torch
+
+        from paper_2312_00407_b200 import optim, registry, zero
 
         self.kind, self.p, self.g = kind, p, g
         self.cfg = make_cfg(kind)
         self.lr = self.cfg.lr
+        self.rs = None
+        self.n = p.numel()
         if kind in ("adamw", "lion", "adan", "sophia"):
             self.opt = optim.FlatOptimizer(self.cfg, p.numel())
+        elif kind == "adalomo" and world > 1:
+            self.rs = zero.RowShardedAdaLomo(self.cfg, shapes)
+            self.n = self.rs.local_numel
+            self.lp = torch.empty(self.n, device=p.device)
+            self.lg = torch.empty(self.n, device=p.device)
+            optim.synth_fill(self.lp, registry.SEED, 0, 0xFFFE, 0, 0, -6)
+            optim.synth_fill(self.lg, registry.SEED, 1, 0xFFFE, 1, 0, -7, 10)
         elif kind == "adalomo":
             self.opt = optim.AdaLomoState(self.cfg, shapes)
         else:
@@ -189,6 +203,8 @@ class Stepper:
 
         if self.kind == "lomo":
             optim.lomo_apply(self.p, self.g, self.lr, 1.0)
+        elif self.rs is not None:
+            self.rs.step(self.lp, self.lg, self.lr)
         elif self.kind == "adalomo":
             self.opt.apply_all(self.p, self.g, self.lr)
         else:
@@ -232,11 +248,7 @@ def bench_ours(args, rank, world, local_rank):
     launches = 0
     clocks = ClockSampler(local_rank)
     for kind in kinds:
-        if world > 1 and kind == "adalomo":
-            # AdaLomo shards by rows of whole matrices; the flat
-            # ZeRO shard here is timed as the elementwise kinds only.
-            continue
-        st = Stepper(kind, shapes, p, g)
+        st = Stepper(kind, shapes, p, g, world)
         for _ in range(args.warmup):
             st.step()
         torch.cuda.synchronize()
@@ -258,14 +270,15 @@ def bench_ours(args, rank, world, local_rank):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = t.item()
         bpp = BYTES_PER_PARAM[kind]
-        gbs = bpp * owned / (ms * 1e-3) / 1e9
-        per[kind] = {"ms": round(ms, 4), "params_per_s": P / (ms * 1e-3) if world > 1 else
-                     owned / (ms * 1e-3), "bytes_per_param": bpp, "achieved_gbs": round(gbs, 1),
+        gbs = bpp * st.n / (ms * 1e-3) / 1e9  # per GPU (this rank's launch)
+        per[kind] = {"ms": round(ms, 4), "params_per_s": P / (ms * 1e-3),
+                     "bytes_per_param": bpp, "achieved_gbs_per_gpu": round(gbs, 1),
                      "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
+                     "params_per_launch": st.n,
                      "launches_per_step": (optim.launch_count() - l0) / max(args.steps, 1)}
         total_ms += ms
-        log(f"[rank {rank}] {kind}: {ms:.3f} ms/step, {owned / ms / 1e6:.1f} Gparam/s/GPU, "
-            f"{gbs:.0f} GB/s = {gbs / hbm_peak:.3f} of {peak_src} HBM")
+        log(f"[rank {rank}] {kind}: {ms:.3f} ms/step, {P / ms / 1e6:.1f} Gparam/s (all GPUs), "
+            f"{gbs:.0f} GB/s/GPU = {gbs / hbm_peak:.3f} of {peak_src} HBM")
         del st
         gc.collect()
         torch.cuda.synchronize()
@@ -275,15 +288,63 @@ def bench_ours(args, rank, world, local_rank):
 
     # dominant kernel = the optimizer with the largest share of the step
     dom = max(per, key=lambda k: per[k]["ms"])
+    npl = per[dom]["params_per_launch"]
     roofline = {"bound": "hbm", "kernel": f"{dom} update (flat_step_kernel)" if dom not in (
-        "lomo", "adalomo") else dom, "achieved": per[dom]["achieved_gbs"], "peak": hbm_peak,
-        "peak_source": peak_src, "unit": "GB/s",
-        "frac": round(per[dom]["achieved_gbs"] / hbm_peak, 4),
-        "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": owned,
-        "traffic": load_traffic(dom, owned)}
-    return dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
-                launches=launches, clocks=clocks.summary(), P=P, owned=owned,
-                shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
+        "lomo", "adalomo") else dom, "achieved": per[dom]["achieved_gbs_per_gpu"],
+        "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+        "frac": round(per[dom]["achieved_gbs_per_gpu"] / hbm_peak, 4),
+        "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": npl,
+        "traffic": load_traffic(dom, npl)}
+    out = dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
+               launches=launches, clocks=clocks.summary(), P=P, owned=owned,
+               shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
+    if world > 1 and not args.no_collectives:
+        del p, g
+        out["p"] = out["g"] = None
+        gc.collect()
+        torch.cuda.empty_cache()
+        out["collectives"] = bench_peer_step(args, P, rank, world, dev)
+    return out
+
+
+def bench_peer_step(args, P, rank, world, dev):
+    """ZeRO step fused with its collectives (csrc/peer.cu): AdamW over the whole 7B
+    set, grads summed from every rank's buffer over NVLink, params stored into every
+    replica.  Roofline = max(HBM bytes / HBM BW, NVLink bytes / 770 GB/s)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_00407_b200 import optim, registry, zero
+
+    cfg = make_cfg("adamw")
+    ps = zero.PeerShardedOptimizer(cfg, P, device=dev.index)
+    optim.synth_fill(ps.params, registry.SEED, 0, 0xFFFD, 0, 0, -6)
+    optim.synth_fill(ps.grads, registry.SEED, 1, 0xFFFD, 1, 0, -7, 10)
+    torch.cuda.synchronize()
+    for _ in range(args.warmup):
+        ps.step(cfg.lr)
+    torch.cuda.synchronize()
+    dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        ps.step(cfg.lr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item()
+    owned = ps.hi - ps.lo
+    nvl = owned * (world - 1) * 4 / 1e9  # GB in (grads) and out (params) per rank
+    hbm = owned * (28 + 4 * world) / 1e9  # local state + master + grads + replica traffic
+    bound_ms = max(nvl / 770.0, hbm / measured_peaks()[0]) * 1e3
+    log(f"[rank {rank}] fused RS+adamw+AG: {ms:.2f} ms/step, NVLink {nvl:.1f} GB/dir/rank, "
+        f"roofline {bound_ms:.2f} ms")
+    return {"kernel": "peer_step_kernel (adamw, RS + update + AG over NVLink)", "ms": ms,
+            "params_per_s": P / (ms * 1e-3), "nvlink_gb_per_direction_per_rank": round(nvl, 2),
+            "roofline_ms": round(bound_ms, 3), "frac": round(bound_ms / ms, 4),
+            "nvlink_peak_gbs": 770.0}
 
 
 def load_traffic(kind, params_per_launch):
@@ -375,6 +436,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-collectives", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
     args = ap.parse_args()
 
@@ -411,7 +473,12 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("MCO_BENCH_BACKEND", "nccl")  # gloo: test N ranks on 1 GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
+        local_rank = local_rank % max(torch.cuda.device_count(), 1)
     res = bench_ours(args, rank, world, local_rank)
     config["params"] = res["P"]
     e2e = None
@@ -436,6 +503,8 @@ def main():
                 "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "per_optimizer": res["per"]}
+        if "collectives" in res:
+            line["collectives"] = res["collectives"]
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

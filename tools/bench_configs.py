@@ -1,0 +1,114 @@
+#!/usr/bin/env python3
+"""Single-GPU measurements of BASELINE.json configs 3-5 (bench.py measures config 2).
+
+  c3        AdaLomo, factored moments + global grad-norm clip, LLaMA-13B shapes (1 GPU)
+  c4-shard  one rank's ZeRO shard at N=8 of the 65B set: Sophia, mixed precision
+            (fp32 master/state/grads, bf16 parameter copy written for the all-gather);
+            and Adan mixed on the 65B-L16 subset's N=8 shard (full 65B Adan state does
+            not fit 180 GB per rank at N=8)
+  c5-shard  one rank's shard at N=8 of the Llama-2-70B (GQA) set: LOMO with bf16
+            params/grads and the global grad-norm clip (sum of squares + clipped update;
+            the one-scalar all-reduce between them is not present on one GPU)
+
+Each line: params/s for that launch, algorithmic bytes, achieved GB/s, fraction of the
+measured HBM copy bandwidth.  Timed with CUDA events after warm-up; inputs > L2.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def timed(fn, warmup, steps):
+    import torch
+
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    s = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(s)
+    for _ in range(steps):
+        fn()
+    b.record(s)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / steps
+
+
+def line(name, n, ms, bpp, extra=None):
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    gbs = bpp * n / (ms * 1e-3) / 1e9
+    d = {"config": name, "params": n, "ms": round(ms, 3), "params_per_s": n / (ms * 1e-3),
+         "bytes_per_param": bpp, "achieved_gbs": round(gbs, 1), "hbm_peak_gbs": peak,
+         "frac": round(gbs / peak, 4)}
+    d.update(extra or {})
+    print(json.dumps(d), flush=True)
+
+
+def main():
+    import gc
+
+    import torch
+
+    from paper_2312_00407_b200 import optim, registry
+    from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+    W, K = 2, 5
+    which = sys.argv[1:] or ["c3", "c4", "c5"]
+
+    if "c3" in which:
+        m = registry.LLAMA_13B
+        shapes, n = m.shapes(), m.param_count()
+        p = torch.empty(n, device="cuda")
+        g = torch.empty(n, device="cuda")
+        registry.fill_params(p, shapes)
+        registry.fill_grads(g, shapes, 1)
+        cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+        cfg.lr, cfg.clip_threshold = 5e-4, 1.0
+        st = optim.AdaLomoState(cfg, shapes)
+        ms = timed(lambda: st.apply_all(p, g, cfg.lr), W, K)
+        line("c3 adalomo+clip llama-13b 1xB200", n, ms, 24,
+             {"tensors": len(shapes), "state_floats": st.state_bytes_runtime() // 8})
+        del st, p, g
+        gc.collect()
+        torch.cuda.empty_cache()
+
+    if "c4" in which:
+        for kind, model, bpp in ((Kind.SOPHIA, registry.LLAMA_65B, 26),
+                                 (Kind.ADAN, registry.LLAMA_65B_L16, 46)):
+            n = optim.zero_plan(model.param_count(), 8)[0][0]
+            master = torch.empty(n, device="cuda")
+            g = torch.empty(n, device="cuda")
+            out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+            optim.synth_fill(master, registry.SEED, 0, 1, 0, 0, -6)
+            optim.synth_fill(g, registry.SEED, 1, 1, 1, 0, -7, 10)
+            cfg = OptimizerConfig.defaults_for(kind)
+            cfg.lr = 1e-4 if kind == Kind.SOPHIA else 5e-5
+            opt = optim.FlatOptimizer(cfg, n)
+            ms = timed(lambda: opt.step_mixed(master, g, out, cfg.lr), W, K)
+            line(f"c4 {optim.kind_name(kind)} mixed, rank shard of {model.name} at N=8", n, ms,
+                 bpp, {"note": "Sophia: refresh steps every 10 write h (+4 B/param)"
+                       if kind == Kind.SOPHIA else "fp32 master/state/grads, bf16 out"})
+            del opt, master, g, out
+            gc.collect()
+            torch.cuda.empty_cache()
+
+    if "c5" in which:
+        model = registry.LLAMA2_70B
+        n = optim.zero_plan(model.param_count(), 8)[0][0]
+        p = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        optim.synth_fill(p, registry.SEED, 0, 2, 0, 0, -6)
+        optim.synth_fill(g, registry.SEED, 1, 2, 1, 0, -7, 10)
+        ms = timed(lambda: optim.lomo_step(p, g, 1e-2, clip=1.0), W, K)
+        line("c5 lomo bf16 + global clip, rank shard of llama2-70b at N=8", n, ms, 8,
+             {"passes": "sum of squares (2 B/param) + clipped update (6 B/param)"})
+        ms = timed(lambda: optim.lomo_apply(p, g, 1e-2, 1.0), W, K)
+        line("c5 lomo bf16 no clip, rank shard of llama2-70b at N=8", n, ms, 6)
+
+
+if __name__ == "__main__":
+    main()
