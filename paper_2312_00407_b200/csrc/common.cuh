@@ -123,6 +123,33 @@ __device__ __forceinline__ void ld_stream_bf16x8(const uint16_t* p, float (&r)[8
   }
 }
 
+// 16 x bf16 = 256 bits (LDG.E.256)
+__device__ __forceinline__ void unpack_bf16x16(const uint32_t (&w)[8], float (&r)[16]) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    r[2 * k] = __uint_as_float(w[k] << 16);
+    r[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+  }
+}
+__device__ __forceinline__ void ld_stream_bf16x16(const uint16_t* p, float (&r)[16]) {
+  uint32_t w[8];
+  asm volatile(
+      "ld.global.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7])
+      : "l"(p));
+  unpack_bf16x16(w, r);
+}
+__device__ __forceinline__ void ld_stream_ro_bf16x16(const uint16_t* p, float (&r)[16]) {
+  uint32_t w[8];
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.L2::evict_first.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]),
+        "=r"(w[7])
+      : "l"(p));
+  unpack_bf16x16(w, r);
+}
+
 // fp32 -> bf16 round-to-nearest-even (NaN kept quiet); same rule as the oracle.
 __device__ __forceinline__ uint32_t f2bf_bits(float f) {
   uint32_t u = __float_as_uint(f);
@@ -136,6 +163,15 @@ __device__ __forceinline__ void st_stream_bf16x8(uint16_t* p, const float (&r)[8
   for (int k = 0; k < 4; ++k) w[k] = f2bf_bits(r[2 * k]) | (f2bf_bits(r[2 * k + 1]) << 16);
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w[0]),
                "r"(w[1]), "r"(w[2]), "r"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ void st_stream_bf16x16(uint16_t* p, const float (&r)[16]) {
+  uint32_t w[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = f2bf_bits(r[2 * k]) | (f2bf_bits(r[2 * k + 1]) << 16);
+  asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
+               "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+               "r"(w[7])
                : "memory");
 }
 __device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }

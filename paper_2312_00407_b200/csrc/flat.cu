@@ -10,6 +10,7 @@
 // arithmetic is the reference's operation order, no fused multiply-add, IEEE
 // division and square root -- bit-identical to oracle/mco_oracle.c.
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -22,8 +23,9 @@ namespace {
 using namespace upd;
 constexpr int kThreads = 256;
 
-template <int KIND, typename T, typename GT, bool MIXED, int U>
-__global__ void __launch_bounds__(kThreads)
+// MINB > 1 caps registers so MINB CTAs fit per SM (Adan streams 11 buffers).
+template <int KIND, typename T, typename GT, bool MIXED, int U, int MINB = 1>
+__global__ void __launch_bounds__(kThreads, MINB)
     flat_step_kernel(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
                      T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
                      uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
@@ -112,11 +114,18 @@ __device__ __forceinline__ T lomo_factor(double lr, double scale, const double* 
 }
 
 template <typename PT, typename GT>
+constexpr int lomo_width() {
+  if constexpr (std::is_same<PT, double>::value) return 4;
+  if constexpr (std::is_same<PT, uint16_t>::value && std::is_same<GT, uint16_t>::value) return 16;
+  return 8;
+}
+
+template <typename PT, typename GT>
 __global__ void __launch_bounds__(kThreads)
     lomo_kernel(PT* __restrict__ p, const GT* __restrict__ g, uint64_t nvec, uint64_t n,
                 double lr, double scale, const double* __restrict__ sumsq, double clip) {
   using T = typename std::conditional<std::is_same<PT, double>::value, double, float>::type;
-  constexpr int W = std::is_same<PT, double>::value ? 4 : 8;
+  constexpr int W = lomo_width<PT, GT>();
   const T f = lomo_factor<T>(lr, scale, sumsq, clip);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -127,11 +136,16 @@ __global__ void __launch_bounds__(kThreads)
     for (int u = 0; u < U; ++u) {
       const uint64_t vi = base + (uint64_t)u * stride;
       if (vi < nvec) {
-        if constexpr (std::is_same<PT, uint16_t>::value)
-          ld_stream_bf16x8(p + vi * W, pv[u]);
-        else
-          ld_stream(p + vi * W, pv[u]);
-        load_grad(g + vi * W, gv[u]);
+        if constexpr (W == 16) {  // bf16 params and grads: one 256-bit access each
+          ld_stream_bf16x16(p + vi * W, pv[u]);
+          ld_stream_ro_bf16x16(g + vi * W, gv[u]);
+        } else {
+          if constexpr (std::is_same<PT, uint16_t>::value)
+            ld_stream_bf16x8(p + vi * W, pv[u]);
+          else
+            ld_stream(p + vi * W, pv[u]);
+          load_grad(g + vi * W, gv[u]);
+        }
       }
     }
 #pragma unroll
@@ -140,7 +154,9 @@ __global__ void __launch_bounds__(kThreads)
       if (vi < nvec) {
 #pragma unroll
         for (int j = 0; j < W; ++j) pv[u][j] = pv[u][j] - f * gv[u][j];
-        if constexpr (std::is_same<PT, uint16_t>::value)
+        if constexpr (W == 16)
+          st_stream_bf16x16(p + vi * W, pv[u]);
+        else if constexpr (std::is_same<PT, uint16_t>::value)
           st_stream_bf16x8(p + vi * W, pv[u]);
         else
           st_stream(p + vi * W, pv[u]);
@@ -163,19 +179,27 @@ __global__ void __launch_bounds__(kThreads)
 constexpr int kSumsqMaxBlocks = 1024;
 
 template <typename XT>
+constexpr int sumsq_width() {
+  return std::is_same<XT, double>::value ? 4 : (std::is_same<XT, uint16_t>::value ? 16 : 8);
+}
+
+template <typename XT>
 __global__ void __launch_bounds__(kThreads)
     sumsq_kernel(const XT* __restrict__ x, uint64_t nvec, uint64_t n, double* __restrict__ out,
                  int accumulate, double* __restrict__ partials, unsigned* __restrict__ counter) {
   __shared__ double scratch[32];
   __shared__ bool is_last;
-  constexpr int W = std::is_same<XT, double>::value ? 4 : 8;
+  constexpr int W = sumsq_width<XT>();
   using LT = typename std::conditional<std::is_same<XT, double>::value, double, float>::type;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   double acc = 0.0;
   for (uint64_t vi = tid; vi < nvec; vi += stride) {
     LT v[W];
-    load_grad(x + vi * W, v);
+    if constexpr (W == 16)
+      ld_stream_ro_bf16x16(x + vi * W, v);
+    else
+      load_grad(x + vi * W, v);
 #pragma unroll
     for (int j = 0; j < W; ++j) acc += (double)v[j] * (double)v[j];
   }
@@ -270,6 +294,13 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   constexpr int W = Vec<T>::W;
   constexpr int U = (KIND == K_ADAN) ? 1 : 2;
   auto kern = flat_step_kernel<KIND, T, GT, MIXED, U>;
+  if constexpr (KIND == K_ADAN && sizeof(T) == 4) {
+    static const int minb = [] {
+      const char* e = getenv("MCO_ADAN_MINB");  // tuning knob
+      return e ? atoi(e) : 1;
+    }();
+    if (minb == 4) kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4>;
+  }
   bool vec = aligned(a.p, 32) && aligned(a.g, sizeof(GT) * W);
   for (int i = 0; i < 4; ++i) vec = vec && aligned(a.s[i], 32);
   if (MIXED) vec = vec && aligned(a.p_out_bf16, 16);
@@ -312,7 +343,7 @@ void dispatch_dtypes(const FlatArgs& a, const StepConsts<float>& kf, const StepC
 template <typename PT, typename GT>
 void run_lomo(void* p, const void* g, uint64_t n, double lr, double scale, const double* sumsq,
               double clip, cudaStream_t st) {
-  constexpr int W = std::is_same<PT, double>::value ? 4 : 8;
+  constexpr int W = lomo_width<PT, GT>();
   auto kern = lomo_kernel<PT, GT>;
   const bool vec = aligned(p, sizeof(PT) * W) && aligned(g, sizeof(GT) * W);
   const uint64_t nvec = vec ? n / W : 0;
@@ -325,7 +356,7 @@ void run_lomo(void* p, const void* g, uint64_t n, double lr, double scale, const
 template <typename XT>
 void run_sumsq(const void* x, uint64_t n, double* out, int accumulate, double* partials,
                unsigned* counter, int dev, cudaStream_t st) {
-  constexpr int W = std::is_same<XT, double>::value ? 4 : 8;
+  constexpr int W = sumsq_width<XT>();
   auto kern = sumsq_kernel<XT>;
   const bool vec = aligned(x, sizeof(XT) * W);
   const uint64_t nvec = vec ? n / W : 0;
