@@ -105,11 +105,11 @@ float orc_bf16_to_f32(uint16_t h) {
   return f;
 }
 
-/* Round-to-nearest-even; NaN stays NaN (quiet). */
+/* Round-to-nearest-even; any NaN -> canonical 0x7fff (the cvt.rn.bf16 rule). */
 uint16_t orc_f32_to_bf16(float f) {
   uint32_t u;
   memcpy(&u, &f, 4);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)((u >> 16) | 0x40u);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return (uint16_t)0x7fffu;
   u += 0x7fffu + ((u >> 16) & 1u);
   return (uint16_t)(u >> 16);
 }

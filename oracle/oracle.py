@@ -192,11 +192,11 @@ def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
 
 
 def f32_to_bf16(x: np.ndarray) -> np.ndarray:
-    """RNE, NaN-preserving (same rule as orc_f32_to_bf16 / the kernels)."""
+    """RNE, NaN -> 0x7fff (same rule as orc_f32_to_bf16 / cvt.rn.bf16 in the kernels)."""
     u = np.ascontiguousarray(x, np.float32).view(np.uint32).astype(np.uint64)
     nan = (u & 0x7FFFFFFF) > 0x7F800000
     r = ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
-    r[nan] = ((u[nan] >> 16) | 0x40).astype(np.uint16)
+    r[nan] = 0x7FFF
     return r
 
 

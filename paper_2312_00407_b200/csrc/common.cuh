@@ -150,17 +150,23 @@ __device__ __forceinline__ void ld_stream_ro_bf16x16(const uint16_t* p, float (&
   unpack_bf16x16(w, r);
 }
 
-// fp32 -> bf16 round-to-nearest-even (NaN kept quiet); same rule as the oracle.
+// fp32 -> bf16 round-to-nearest-even, NaN -> canonical 0x7fff: the hardware
+// cvt.rn.bf16x2.f32 (F2FP.BF16.F32.PACK_AB); same rule as the oracle.
 __device__ __forceinline__ uint32_t f2bf_bits(float f) {
-  uint32_t u = __float_as_uint(f);
-  if ((u & 0x7fffffffu) > 0x7f800000u) return (u >> 16) | 0x40u;
-  u += 0x7fffu + ((u >> 16) & 1u);
-  return u >> 16;
+  uint32_t r;
+  asm("{ .reg .b16 lo; cvt.rn.bf16.f32 lo, %1; mov.b32 %0, {lo, lo}; }" : "=r"(r) : "f"(f));
+  return r & 0xffffu;
+}
+// two floats -> packed bf16x2 (a in the low half), one instruction
+__device__ __forceinline__ uint32_t f2bf2_bits(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
 }
 __device__ __forceinline__ void st_stream_bf16x8(uint16_t* p, const float (&r)[8]) {
   uint32_t w[4];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) w[k] = f2bf_bits(r[2 * k]) | (f2bf_bits(r[2 * k + 1]) << 16);
+  for (int k = 0; k < 4; ++k) w[k] = f2bf2_bits(r[2 * k], r[2 * k + 1]);
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w[0]),
                "r"(w[1]), "r"(w[2]), "r"(w[3])
                : "memory");
@@ -168,7 +174,7 @@ __device__ __forceinline__ void st_stream_bf16x8(uint16_t* p, const float (&r)[8
 __device__ __forceinline__ void st_stream_bf16x16(uint16_t* p, const float (&r)[16]) {
   uint32_t w[8];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) w[k] = f2bf_bits(r[2 * k]) | (f2bf_bits(r[2 * k + 1]) << 16);
+  for (int k = 0; k < 8; ++k) w[k] = f2bf2_bits(r[2 * k], r[2 * k + 1]);
   asm volatile("st.global.L1::no_allocate.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
                "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
                "r"(w[7])

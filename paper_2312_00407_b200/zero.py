@@ -425,3 +425,30 @@ class RowShardedAdaLomo:
         if multi:
             dist.all_reduce(self.state.payload(1), op=dist.ReduceOp.SUM, group=self.group)
         self.state.phase(3, local_p, local_g, lr, stream)
+
+
+def reshard_state(states: list, total_len: int, new_world: int) -> list:
+    """Offline reshard of ZeRO optimizer state (the reference's gather_full_params +
+    load_state contract, parallel.cpp:820-935): `states[r]` is rank r's
+    extract_state() under ZeroPlan(total_len, len(states)); returns the
+    extract_state()-shaped dicts for ZeroPlan(total_len, new_world).  Buffers are
+    matched by name (m, v, n, h, g_prev); the step counter must agree."""
+    import torch
+
+    steps = {s["steps"] for s in states}
+    if len(steps) != 1:
+        raise optim.ContractError("reshard: ranks disagree on the step counter")
+    names = list(states[0]["buffers"])
+    full = {}
+    for name in names:
+        parts = [s["buffers"][name] for s in states]
+        full[name] = torch.cat([p.reshape(-1) for p in parts])
+        if full[name].numel() != total_len:
+            raise optim.ContractError(f"reshard: buffer '{name}' does not cover the set")
+    plan = ZeroPlan.make(total_len, new_world)
+    out = []
+    for r in range(new_world):
+        lo, hi = plan.owned_range(r)
+        out.append({"steps": states[0]["steps"],
+                    "buffers": {n: full[n][lo:hi].clone() for n in names}})
+    return out

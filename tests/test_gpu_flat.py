@@ -206,3 +206,17 @@ def test_sampled_parity_at_scale():
         assert bits_equal(tp[start:start + m].cpu().numpy(), p)
     del tp, tg
     torch.cuda.empty_cache()
+
+
+def test_state_bytes_match_device_memory():
+    """f3: state_bytes_runtime equals the device memory the optimizer allocates."""
+    n = 1 << 26
+    for kind, nbuf in ((Kind.ADAMW, 2), (Kind.LION, 1), (Kind.ADAN, 4), (Kind.SOPHIA, 2)):
+        torch.cuda.synchronize()
+        free0 = torch.cuda.mem_get_info()[0]
+        opt = optim.FlatOptimizer(cfg_for(kind), n)
+        torch.cuda.synchronize()
+        used = free0 - torch.cuda.mem_get_info()[0]
+        assert opt.state_bytes_runtime() == nbuf * n * 4
+        assert abs(used - opt.state_bytes_runtime()) <= 4 << 20 * nbuf  # allocation granularity
+        del opt
