@@ -274,7 +274,7 @@ struct mco_adalomo {
       if (s) cudaStreamDestroy(s);
     for (auto e : ev_in) cudaEventDestroy(e);
     for (auto e : ev_out) cudaEventDestroy(e);
-    void* ptrs[] = {plan.d_tiles, plan.d_tensors, plan.d_item_off, plan.d_col_off,
+    void* ptrs[] = {plan.d_tiles, plan.d_chunks, plan.d_chunk_sc, plan.d_tensors, plan.d_item_off, plan.d_col_off,
                     plan.d_payload, plan.d_state,
                     plan.d_colpart, plan.d_rowpart, plan.d_tile_sc, plan.d_tens_sc,
                     plan.d_fa,    plan.d_fb,      plan.d_glob};
@@ -686,6 +686,8 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
       MCO_CUDA_CHECK(cudaMemset(*p, 0, std::max<size_t>(count, 1) * esz));
     };
     alloc(&pl.d_tiles, pl.h_tiles.size(), sizeof(Tile));
+    alloc(&pl.d_chunks, pl.h_chunks.size(), sizeof(Chunk));
+    alloc(&pl.d_chunk_sc, pl.h_chunks.size(), sizeof(double));
     alloc(&pl.d_tensors, pl.h_tensors.size(), sizeof(TensorInfo));
     alloc(&pl.d_item_off, pl.h_item_off.size(), sizeof(int64_t));
     alloc(&pl.d_col_off, pl.h_col_off.size(), sizeof(int64_t));
@@ -700,6 +702,8 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
     alloc(&pl.d_glob, 4, sizeof(double));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_tiles, pl.h_tiles.data(), pl.h_tiles.size() * sizeof(Tile),
                               cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(pl.d_chunks, pl.h_chunks.data(),
+                              pl.h_chunks.size() * sizeof(Chunk), cudaMemcpyHostToDevice));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_tensors, pl.h_tensors.data(),
                               pl.h_tensors.size() * sizeof(TensorInfo), cudaMemcpyHostToDevice));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_col_off, pl.h_col_off.data(),

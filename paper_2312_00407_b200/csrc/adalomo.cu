@@ -50,6 +50,8 @@ struct Ctx {
   double* pay;        // stats payload: 3 per tensor (gsq, psq, vrs) | column sums
   double* pay_usq;    // usq payload: 1 per tensor
   int64_t ntens;      // total tensors (payload layout)
+  const Chunk* chunks;
+  double* chunk_sc;   // per-chunk sum u^2
 };
 
 enum { TS_GSQ = 0, TS_PSQ, TS_VRS, TS_CORR, TS_LRT, TS_ROWMEAN, TS_USQ, TS_F, kTensScalars };
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
   for (int k = t0 + warp; k < t1; k += 32) {
     const TensorInfo T = c.tensors[k];
     double us = 0;
-    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += c.tile_sc[i * 4 + 3];
+    for (int64_t i = T.chunk_begin + lane; i < T.chunk_end; i += 32) us += c.chunk_sc[i];
     us = warp_sum(us);
     if (lane == 0) c.pay_usq[k] = T.weight * us;
   }
@@ -378,52 +380,78 @@ __device__ __forceinline__ float u_fact(float g, float s, float a, float b, floa
 }
 
 // ============================ K4: sum u^2 ============================================
+// Flat chunks: each thread takes 8-wide vectors (C % 8 == 0 on the vector path, so a
+// vector never straddles rows), kU vectors in flight, row = e / C and col = e % C in
+// 32-bit arithmetic (tensor numel < 2^31), a_row and b[col..col+7] from L1/L2.
+constexpr int kU = 4;
+
+template <bool VEC, typename GT>
+__device__ __forceinline__ void chunk_vec_load(const GT* g, int64_t e, int64_t e1, float (&v)[VW]) {
+  if constexpr (VEC) {
+    load8<GT>(g + e, v);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VW; ++j) v[j] = (e + j < e1) ? ld1(g + e + j) : 0.f;
+  }
+}
+
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads)
-    k4_usq(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double b2, double eps) {
+    k4_usq(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double b2, double eps) {
   __shared__ double scratch[32];
   const float sf = (float)c.glob[0], epsf = (float)eps;
-  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-    const Tile tl = c.tiles[tile0 + ti];
-    const TensorInfo T = c.tensors[tl.tensor];
+  for (int64_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
+    const Chunk ch = c.chunks[chunk0 + ci];
+    const TensorInfo T = c.tensors[ch.tensor];
     const GT* g = gptr<GT>(P, T);
     double usq = 0.0;
     if (T.factored) {
-      const int TC = T.tc, TR = kThreads / T.tc;
-      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
-      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
-      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
-      if (valid > 0) {
-        float bv[VW];
+      const uint32_t C = (uint32_t)T.cols;
+      const float* fa = c.fa + T.fa_off;
+      const float* fb = c.fb + T.fb_off;
+      for (int64_t base = ch.e0 + (int64_t)threadIdx.x * VW; base < ch.e1;
+           base += (int64_t)kThreads * VW * kU) {
+        float gv[kU][VW];
 #pragma unroll
-        for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
-        for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB2 * TR) {
-          float gv[kRB2][VW];
+        for (int u = 0; u < kU; ++u) {
+          const int64_t e = base + (int64_t)u * kThreads * VW;
+          if (e < ch.e1) chunk_vec_load<VEC, GT>(g, e, ch.e1, gv[u]);
+        }
+        float su = 0.f;
 #pragma unroll
-          for (int b = 0; b < kRB2; ++b) {
-            const int64_t r = r0 + (int64_t)b * TR;
-            if (r < tl.r1) load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
-          }
-#pragma unroll
-          for (int b = 0; b < kRB2; ++b) {
-            const int64_t r = r0 + (int64_t)b * TR;
-            if (r < tl.r1) {
-              const float a = c.fa[T.fa_off + r];
-              float su = 0.f;
+        for (int u = 0; u < kU; ++u) {
+          const int64_t e = base + (int64_t)u * kThreads * VW;
+          if (e < ch.e1) {
+            if constexpr (VEC) {
+              const uint32_t row = (uint32_t)e / C, col = (uint32_t)e - row * C;
+              const float a = fa[row];
+              const float4 b0 = *reinterpret_cast<const float4*>(fb + col);
+              const float4 b1 = *reinterpret_cast<const float4*>(fb + col + 4);
+              const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
               for (int j = 0; j < VW; ++j) {
-                const float u = u_fact(gv[b][j], sf, a, bv[j], epsf);
-                su += j < valid ? u * u : 0.f;
+                const float x = u_fact(gv[u][j], sf, a, bv[j], epsf);
+                su += x * x;
               }
-              usq += (double)su;
+            } else {
+#pragma unroll
+              for (int j = 0; j < VW; ++j) {
+                const int64_t ej = e + j;
+                if (ej < ch.e1) {
+                  const uint32_t row = (uint32_t)ej / C, col = (uint32_t)ej - row * C;
+                  const float x = u_fact(gv[u][j], sf, fa[row], fb[col], epsf);
+                  su += x * x;
+                }
+              }
             }
           }
         }
+        usq += (double)su;
       }
     } else {  // optim.cpp:262-267 with fp64 state
       const double s = c.glob[0];
-      const double corr = c.tens_sc[tl.tensor * kTensScalars + TS_CORR];
-      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+      const double corr = c.tens_sc[ch.tensor * kTensScalars + TS_CORR];
+      for (int64_t e = ch.e0 + threadIdx.x; e < ch.e1; e += kThreads) {
         const double gs = s * (double)ld1(g + e);
         double& v = c.state[T.vfull_off + e];
         v = b2 * v + (1 - b2) * gs * gs;
@@ -432,7 +460,7 @@ __global__ void __launch_bounds__(kThreads)
       }
     }
     const double b = block_sum(usq, scratch);
-    if (threadIdx.x == 0) c.tile_sc[(tile0 + ti) * 4 + 3] = b;
+    if (threadIdx.x == 0) c.chunk_sc[chunk0 + ci] = b;
   }
 }
 
@@ -452,52 +480,68 @@ __global__ void __launch_bounds__(1024)
 // ============================ K6: update ==============================================
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads)
-    k6_update(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
+    k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps) {
   const float sf = (float)c.glob[0], epsf = (float)eps;
-  // reverse tile order: the tail of K4's gradient reads is still L2-resident
-  for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
-    const int64_t ti = ntiles - 1 - k;
-    const Tile tl = c.tiles[tile0 + ti];
-    const TensorInfo T = c.tensors[tl.tensor];
+  // reverse chunk order: the tail of K4's gradient reads is still L2-resident
+  for (int64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
+    const int64_t ci = nchunks - 1 - k;
+    const Chunk ch = c.chunks[chunk0 + ci];
+    const TensorInfo T = c.tensors[ch.tensor];
     const GT* g = gptr<GT>(P, T);
     float* p = pptr(P, T);
-    const double f = c.tens_sc[tl.tensor * kTensScalars + TS_F];
+    const double f = c.tens_sc[ch.tensor * kTensScalars + TS_F];
     if (T.factored) {
       const float ff = (float)f;
-      const int TC = T.tc, TR = kThreads / T.tc;
-      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
-      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
-      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
-      if (valid <= 0) continue;
-      float bv[VW];
+      const uint32_t C = (uint32_t)T.cols;
+      const float* fa = c.fa + T.fa_off;
+      const float* fb = c.fb + T.fb_off;
+      constexpr int U6 = 2;
+      for (int64_t base = ch.e0 + (int64_t)threadIdx.x * VW; base < ch.e1;
+           base += (int64_t)kThreads * VW * U6) {
+        float gv[U6][VW], pv[U6][VW];
 #pragma unroll
-      for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
-      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB * TR) {
-        float gv[kRB][VW], pv[kRB][VW];
+        for (int u = 0; u < U6; ++u) {
+          const int64_t e = base + (int64_t)u * kThreads * VW;
+          if (e < ch.e1) {
+            chunk_vec_load<VEC, GT>(g, e, ch.e1, gv[u]);
+            if constexpr (VEC) {
+              ld_stream(p + e, pv[u]);
+            } else {
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
-          const int64_t r = r0 + (int64_t)b * TR;
-          if (r < tl.r1) {
-            load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
-            load_p<VEC>(p + r * T.cols + col, pv[b], valid);
+              for (int j = 0; j < VW; ++j) pv[u][j] = (e + j < ch.e1) ? p[e + j] : 0.f;
+            }
           }
         }
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
-          const int64_t r = r0 + (int64_t)b * TR;
-          if (r < tl.r1) {
-            const float a = c.fa[T.fa_off + r];
+        for (int u = 0; u < U6; ++u) {
+          const int64_t e = base + (int64_t)u * kThreads * VW;
+          if (e < ch.e1) {
+            if constexpr (VEC) {
+              const uint32_t row = (uint32_t)e / C, col = (uint32_t)e - row * C;
+              const float a = fa[row];
+              const float4 b0 = *reinterpret_cast<const float4*>(fb + col);
+              const float4 b1 = *reinterpret_cast<const float4*>(fb + col + 4);
+              const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-            for (int j = 0; j < VW; ++j)
-              pv[b][j] = pv[b][j] - ff * u_fact(gv[b][j], sf, a, bv[j], epsf);
-            store_p<VEC>(p + r * T.cols + col, pv[b], valid);
+              for (int j = 0; j < VW; ++j) pv[u][j] = pv[u][j] - ff * u_fact(gv[u][j], sf, a, bv[j], epsf);
+              st_stream(p + e, pv[u]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < VW; ++j) {
+                const int64_t ej = e + j;
+                if (ej < ch.e1) {
+                  const uint32_t row = (uint32_t)ej / C, col = (uint32_t)ej - row * C;
+                  p[ej] = pv[u][j] - ff * u_fact(gv[u][j], sf, fa[row], fb[col], epsf);
+                }
+              }
+            }
           }
         }
       }
     } else {
       const double s = c.glob[0];
-      const double corr = c.tens_sc[tl.tensor * kTensScalars + TS_CORR];
-      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+      const double corr = c.tens_sc[ch.tensor * kTensScalars + TS_CORR];
+      for (int64_t e = ch.e0 + threadIdx.x; e < ch.e1; e += kThreads) {
         const double gs = s * (double)ld1(g + e);
         const double u = gs / sqrt(c.state[T.vfull_off + e] / corr + eps);
         p[e] = (float)((double)p[e] - f * u);
@@ -519,11 +563,14 @@ template <bool VEC, typename GT>
 void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaStream_t st) {
   Ctx c{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
         pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
-        pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size()};
+        pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
+        pl.d_chunks,  pl.d_chunk_sc};
   Ptrs P{(float*)call.p, call.g, call.single};
   const int dev = current_device();
   const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
   const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
+  const int64_t chunk0 = pl.h_tensors[call.t0].chunk_begin;
+  const int64_t nchunks = pl.h_tensors[call.t1 - 1].chunk_end - chunk0;
   const auto& cfg = pl.cfg;
   const int64_t sms = device_info(dev).sms;
 
@@ -547,7 +594,8 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
       launch_check("adalomo k3_moments");
     }
     auto kk4 = k4_usq<VEC, GT>;
-    kk4<<<grid_for(kk4, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.beta2, cfg.eps);
+    kk4<<<grid_for(kk4, nchunks, dev), kThreads, 0, st>>>(c, P, chunk0, nchunks, cfg.beta2,
+                                                          cfg.eps);
     launch_check("adalomo k4_usq");
     kr_usq<<<1, 1024, 0, st>>>(c, call.t0, call.t1);
     launch_check("adalomo kr_usq");
@@ -555,7 +603,7 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
     k5_damp<<<1, 1024, 0, st>>>(c, call.t0, call.t1, cfg.adalomo_clip);
     launch_check("adalomo k5_damp");
     auto kk6 = k6_update<VEC, GT>;
-    kk6<<<grid_for(kk6, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.eps);
+    kk6<<<grid_for(kk6, nchunks, dev), kThreads, 0, st>>>(c, P, chunk0, nchunks, cfg.eps);
     launch_check("adalomo k6_update");
   }
 }
@@ -608,6 +656,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
                         int sms) {
   pl.h_tensors.clear();
   pl.h_tiles.clear();
+  pl.h_chunks.clear();
   pl.h_item_off.assign(1, 0);
   pl.h_col_off.assign(1, 0);
   int64_t elem = 0, state = 0, colpart = 0, rowpart = 0, fa = 0, fb = 0;
@@ -646,7 +695,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
       T.fa_off = fa;
       fa += T.rows;
       T.fb_off = fb;
-      fb += T.cols;
+      fb += (T.cols + 7) / 8 * 8;  // 32 B aligned per tensor (float4 loads in K4 / K6)
       for (int64_t rb = 0; rb < T.nrb; ++rb)
         for (int cb = 0; cb < T.kc; ++cb) {
           Tile tl{};
@@ -684,6 +733,10 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
       pl.h_col_off.push_back(pl.h_col_off.back());
     }
     T.tile_end = (int64_t)pl.h_tiles.size();
+    T.chunk_begin = (int64_t)pl.h_chunks.size();
+    for (int64_t e0 = 0; e0 < numel; e0 += kChunkElems)
+      pl.h_chunks.push_back(Chunk{(int32_t)k, 0, e0, std::min(numel, e0 + kChunkElems)});
+    T.chunk_end = (int64_t)pl.h_chunks.size();
     T.t = 0;
     T.rows_global = T.rows;
     T.numel_global = T.numel;

@@ -20,6 +20,14 @@ struct Tile {
   int64_t r0, r1, c0, c1;  // 1-D tensors: [r0, r1) is the element range
 };
 
+// Work unit of the two streaming passes after the statistics (K4, K6): a flat
+// element range of one tensor; row / column recovered per 8-wide vector.
+struct Chunk {
+  int32_t tensor, pad;
+  int64_t e0, e1;
+};
+constexpr int64_t kChunkElems = 1 << 16;
+
 struct TensorInfo {
   int64_t numel, rows, cols;
   int32_t factored, tc;  // tc: column lanes per row group (32/64/128)
@@ -29,6 +37,7 @@ struct TensorInfo {
   int64_t vrow_off, vcol_off, vfull_off;  // fp64 state offsets
   int64_t colpart_off, rowpart_off, fa_off, fb_off;
   int64_t tile_begin, tile_end;
+  int64_t chunk_begin, chunk_end;
   int64_t t;  // per-entry step counter (optim.hpp:93), advanced on the device
   // row-split sharding: statistics normalise by the global shape; the payload
   // contribution is scaled by `weight` (0 on ranks holding a duplicate replica)
@@ -41,12 +50,15 @@ struct AdaLomoPlan {
   int device = 0;
   std::vector<TensorInfo> h_tensors;
   std::vector<Tile> h_tiles;
+  std::vector<Chunk> h_chunks;
   std::vector<int64_t> h_item_off;  // per tensor prefix of (rows + cols) for factored
   std::vector<int64_t> h_col_off;   // per tensor prefix of cols for factored
   int64_t state_len = 0, colpart_len = 0, rowpart_len = 0, fa_len = 0, fb_len = 0;
   int64_t stats_len = 0, usq_len = 0;  // payload: [3 per tensor | column sums] + [usq]
   // device
   Tile* d_tiles = nullptr;
+  Chunk* d_chunks = nullptr;
+  double* d_chunk_sc = nullptr;  // per-chunk sum u^2
   TensorInfo* d_tensors = nullptr;
   int64_t* d_item_off = nullptr;
   int64_t* d_col_off = nullptr;

@@ -218,5 +218,5 @@ def test_state_bytes_match_device_memory():
         torch.cuda.synchronize()
         used = free0 - torch.cuda.mem_get_info()[0]
         assert opt.state_bytes_runtime() == nbuf * n * 4
-        assert abs(used - opt.state_bytes_runtime()) <= 4 << 20 * nbuf  # allocation granularity
+        assert abs(used - opt.state_bytes_runtime()) <= (4 << 20) * nbuf  # allocation granularity
         del opt
