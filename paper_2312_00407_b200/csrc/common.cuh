@@ -74,6 +74,22 @@ __device__ __forceinline__ void st_stream(float* p, const float (&r)[8]) {
       "f"(r[1]), "f"(r[2]), "f"(r[3]), "f"(r[4]), "f"(r[5]), "f"(r[6]), "f"(r[7])
       : "memory");
 }
+// 128-bit variants (L2 eviction hints need 256-bit accesses on sm_100a)
+__device__ __forceinline__ void ld_stream(const float* p, float (&r)[4]) {
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld_stream_ro(const float* p, float (&r)[4]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void st_stream(float* p, const float (&r)[4]) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(r[0]),
+               "f"(r[1]), "f"(r[2]), "f"(r[3])
+               : "memory");
+}
 // Keep-in-L2 variants (AdaLomo re-reads gradients across passes).
 __device__ __forceinline__ void ld_keep_ro(const float* p, float (&r)[8]) {
   asm volatile(

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <string>
 #include <unordered_map>
 
 #include "kernels.h"
@@ -24,13 +25,15 @@ using namespace upd;
 constexpr int kThreads = 256;
 
 // MINB > 1 caps registers so MINB CTAs fit per SM (Adan streams 11 buffers).
-template <int KIND, typename T, typename GT, bool MIXED, int U, int MINB = 1>
+// WV: elements per vector access (8 f32 = 256-bit, 4 f32 = 128-bit, 4 f64 = 256-bit).
+template <int KIND, typename T, typename GT, bool MIXED, int U, int MINB = 1,
+          int WV = Vec<T>::W>
 __global__ void __launch_bounds__(kThreads, MINB)
     flat_step_kernel(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
                      T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
                      uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
                      const StepConsts<T> k) {
-  constexpr int W = Vec<T>::W;
+  constexpr int W = WV;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = tid; base < nvec; base += stride * U) {
@@ -75,7 +78,15 @@ __global__ void __launch_bounds__(kThreads, MINB)
           st_stream(s2 + e, c[u]);
           st_stream(s3 + e, d[u]);
         }
-        if constexpr (MIXED) st_stream_bf16x8(pout + e, pv[u]);
+        if constexpr (MIXED) {
+          if constexpr (W == 8) {
+            st_stream_bf16x8(pout + e, pv[u]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < W; j += 2)
+              *reinterpret_cast<uint32_t*>(pout + e + j) = f2bf2_bits(pv[u][j], pv[u][j + 1]);
+          }
+        }
       }
     }
   }
@@ -291,19 +302,31 @@ inline bool aligned(const void* ptr, size_t bytes) {
 
 template <int KIND, typename T, typename GT, bool MIXED>
 void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
-  constexpr int W = Vec<T>::W;
   constexpr int U = (KIND == K_ADAN) ? 1 : 2;
+  int W = Vec<T>::W;
   auto kern = flat_step_kernel<KIND, T, GT, MIXED, U>;
-  if constexpr (KIND == K_ADAN && sizeof(T) == 4) {
-    static const int minb = [] {
-      const char* e = getenv("MCO_ADAN_MINB");  // tuning knob
-      return e ? atoi(e) : 1;
+  if constexpr (sizeof(T) == 4) {
+    // tuning knob MCO_FLAT_VARIANT: "w4m4" = 128-bit accesses with
+    // 4 CTAs/SM, "w8m4" = 256-bit with 4 CTAs/SM, default 256-bit occupancy-driven
+    static const int variant = [] {
+      const char* e = getenv("MCO_FLAT_VARIANT");
+      if (!e) return 0;
+      const std::string s(e);
+      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : 0;
     }();
-    if (minb == 4) kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4>;
+    if (variant == 1) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
+      W = 4;
+    } else if (variant == 2) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 8>;
+    } else if (variant == 3) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 1, 4>;
+      W = 4;
+    }
   }
-  bool vec = aligned(a.p, 32) && aligned(a.g, sizeof(GT) * W);
-  for (int i = 0; i < 4; ++i) vec = vec && aligned(a.s[i], 32);
-  if (MIXED) vec = vec && aligned(a.p_out_bf16, 16);
+  bool vec = aligned(a.p, sizeof(T) * W) && aligned(a.g, sizeof(GT) * W);
+  for (int i = 0; i < 4; ++i) vec = vec && aligned(a.s[i], sizeof(T) * W);
+  if (MIXED) vec = vec && aligned(a.p_out_bf16, 2 * W);
   const uint64_t nvec = vec ? a.n / W : 0;
   const uint64_t items = nvec ? (nvec + U - 1) / U : a.n;
   const int dev = current_device();

@@ -66,6 +66,14 @@ __device__ __forceinline__ void load_grad(const uint16_t* g, float (&r)[8]) {
   ld_stream_ro_bf16x8(g, r);
 }
 __device__ __forceinline__ void load_grad(const double* g, double (&r)[4]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ void load_grad(const float* g, float (&r)[4]) { ld_stream_ro(g, r); }
+__device__ __forceinline__ void load_grad(const uint16_t* g, float (&r)[4]) {
+  const uint2 w = *reinterpret_cast<const uint2*>(g);
+  r[0] = __uint_as_float(w.x << 16);
+  r[1] = __uint_as_float(w.x & 0xffff0000u);
+  r[2] = __uint_as_float(w.y << 16);
+  r[3] = __uint_as_float(w.y & 0xffff0000u);
+}
 __device__ __forceinline__ float load_grad1(const float* g) { return *g; }
 __device__ __forceinline__ float load_grad1(const uint16_t* g) { return bf2f(*g); }
 __device__ __forceinline__ double load_grad1(const double* g) { return *g; }
