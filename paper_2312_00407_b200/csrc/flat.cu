@@ -113,6 +113,94 @@ __global__ void __launch_bounds__(kThreads, MINB)
   }
 }
 
+// Software-pipelined variant: the next vector's loads are issued before the
+// current vector's arithmetic (static ping-pong buffers, no local memory).
+template <int KIND, typename T, typename GT>
+struct PfBuf {
+  static constexpr int W = Vec<T>::W;
+  T p[W], g[W], a[W], b[W], c[W], d[W];
+  __device__ __forceinline__ void load(const T* pp, const GT* gg, const T* s0, const T* s1,
+                                       const T* s2, const T* s3, uint64_t e, bool first) {
+    ld_stream(pp + e, p);
+    load_grad(gg + e, g);
+    ld_stream(s0 + e, a);
+    if constexpr (reads_s1(KIND)) ld_stream(s1 + e, b);
+    if constexpr (KIND == K_ADAN) {
+      ld_stream(s2 + e, c);
+      if (!first) ld_stream(s3 + e, d);
+    }
+  }
+  __device__ __forceinline__ void run_store(T* pp, T* s0, T* s1, T* s2, T* s3, uint16_t* pout,
+                                            uint64_t e, const StepConsts<T>& k, bool mixed) {
+#pragma unroll
+    for (int j = 0; j < W; ++j) {
+      if constexpr (KIND != K_ADAN) c[j] = d[j] = T(0);
+      if constexpr (KIND == K_ADAN) {
+        if (k.first) d[j] = T(0);
+      }
+      if constexpr (!reads_s1(KIND)) b[j] = T(0);
+      update<KIND, T>(p[j], g[j], a[j], b[j], c[j], d[j], k);
+    }
+    st_stream(pp + e, p);
+    st_stream(s0 + e, a);
+    if constexpr (KIND == K_ADAMW || KIND == K_ADAN) st_stream(s1 + e, b);
+    if constexpr (KIND == K_SOPHIA) {
+      if (k.refresh) st_stream(s1 + e, b);
+    }
+    if constexpr (KIND == K_ADAN) {
+      st_stream(s2 + e, c);
+      st_stream(s3 + e, d);
+    }
+    if constexpr (sizeof(T) == 4) {
+      if (mixed) st_stream_bf16x8(pout + e, p);
+    }
+  }
+};
+
+template <int KIND, typename T, typename GT, bool MIXED>
+__global__ void __launch_bounds__(kThreads)
+    flat_step_kernel_pf(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
+                        T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
+                        uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
+                        const StepConsts<T> k) {
+  constexpr int W = Vec<T>::W;
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  PfBuf<KIND, T, GT> A, B;
+  uint64_t vi = tid;
+  if (vi < nvec) A.load(p, g, s0, s1, s2, s3, vi * W, k.first);
+  while (vi < nvec) {
+    const uint64_t v1 = vi + stride;
+    if (v1 < nvec) B.load(p, g, s0, s1, s2, s3, v1 * W, k.first);
+    A.run_store(p, s0, s1, s2, s3, pout, vi * W, k, MIXED);
+    if (v1 >= nvec) break;
+    const uint64_t v2 = v1 + stride;
+    if (v2 < nvec) A.load(p, g, s0, s1, s2, s3, v2 * W, k.first);
+    B.run_store(p, s0, s1, s2, s3, pout, v1 * W, k, MIXED);
+    vi = v2;
+  }
+  for (uint64_t e = nvec * W + tid; e < n; e += stride) {
+    T pp = p[e], gg = (T)load_grad1(g + e), aa = s0[e], bb = T(0), cc = T(0), dd = T(0);
+    if constexpr (reads_s1(KIND)) bb = s1[e];
+    if constexpr (KIND == K_ADAN) {
+      cc = s2[e];
+      if (!k.first) dd = s3[e];
+    }
+    update<KIND, T>(pp, gg, aa, bb, cc, dd, k);
+    p[e] = pp;
+    s0[e] = aa;
+    if constexpr (KIND == K_ADAMW || KIND == K_ADAN) s1[e] = bb;
+    if constexpr (KIND == K_SOPHIA) {
+      if (k.refresh) s1[e] = bb;
+    }
+    if constexpr (KIND == K_ADAN) {
+      s2[e] = cc;
+      s3[e] = dd;
+    }
+    if constexpr (MIXED) pout[e] = (uint16_t)f2bf_bits((float)pp);
+  }
+}
+
 // ---- LOMO ---------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ T lomo_factor(double lr, double scale, const double* sumsq,
@@ -312,7 +400,7 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       const char* e = getenv("MCO_FLAT_VARIANT");
       if (!e) return 0;
       const std::string s(e);
-      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : 0;
+      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : s == "pf" ? 4 : 0;
     }();
     if (variant == 1) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
@@ -322,6 +410,8 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
     } else if (variant == 3) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, U, 1, 4>;
       W = 4;
+    } else if (variant == 4) {
+      kern = flat_step_kernel_pf<KIND, T, GT, MIXED>;
     }
   }
   bool vec = aligned(a.p, sizeof(T) * W) && aligned(a.g, sizeof(GT) * W);
