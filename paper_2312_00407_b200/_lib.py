@@ -11,7 +11,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "_build", "libmco.so")
+LIB_PATH = os.environ.get("MCO_LIB_PATH") or os.path.join(HERE, "_build", "libmco.so")
 HEADER = os.path.join(ROOT, "include", "mco.h")
 
 MCO_OK, MCO_CONFIG, MCO_DATA, MCO_CONTRACT, MCO_PROTOCOL, MCO_IO, MCO_CUDA = 0, 2, 3, 4, 5, 6, 7

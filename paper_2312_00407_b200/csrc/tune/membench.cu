@@ -3,6 +3,7 @@
 // the highest HBM throughput?  Prints one line per configuration.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o membench membench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 #include <vector>
 
@@ -76,18 +77,31 @@ void run(const char* name, float* const* dbufs, uint64_t n, int sms) {
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   const uint64_t n = 1ull << 30;  // 4 GiB per buffer
   std::vector<float*> bufs(7);
+  float** dbufs;
+  cudaMalloc(&dbufs, sizeof(float*) * 7);
+  if (argc > 1) {  // staggered sub-buffers of one allocation: stagger bytes = argv[1]
+    const uint64_t stg = strtoull(argv[1], nullptr, 10);
+    char* big;
+    cudaMalloc(&big, 7 * (n * 4 + stg) + 4096);
+    cudaMemset(big, 0, 7 * (n * 4 + stg));
+    for (int i = 0; i < 7; ++i) bufs[i] = (float*)(big + i * (n * 4 + stg));
+    cudaMemcpy(dbufs, bufs.data(), sizeof(float*) * 7, cudaMemcpyHostToDevice);
+    printf("stagger %llu bytes\n", (unsigned long long)stg);
+    run<6, 5, 1>("adan6r5w", dbufs, n, sms);
+    run<4, 3, 1>("adamw4r3w", dbufs, n, sms);
+    return 0;
+  }
   for (auto& p : bufs) {
     cudaMalloc(&p, n * 4);
     cudaMemset(p, 0, n * 4);
   }
-  float** dbufs;
-  cudaMalloc(&dbufs, sizeof(float*) * 7);
   cudaMemcpy(dbufs, bufs.data(), sizeof(float*) * 7, cudaMemcpyHostToDevice);
+  run<6, 5, 1>("adan6r5w", dbufs, n, sms);
   run<1, 1, 1>("copy", dbufs, n, sms);
   run<1, 1, 2>("copy", dbufs, n, sms);
   run<1, 1, 4>("copy", dbufs, n, sms);
