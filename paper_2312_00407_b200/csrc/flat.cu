@@ -391,8 +391,12 @@ inline bool aligned(const void* ptr, size_t bytes) {
 template <int KIND, typename T, typename GT, bool MIXED>
 void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   constexpr int U = (KIND == K_ADAN) ? 1 : 2;
+  // 3 resident CTAs (768 threads) per SM: registers capped at 80 (ncu r01: Adan at
+  // 84 registers fell to 2 CTAs/SM and 0.88 of the HBM copy bandwidth)
+  constexpr int MINB = (sizeof(T) == 4 && (KIND == K_ADAN || KIND == K_LION)) ? 3 : 1;
   int W = Vec<T>::W;
-  auto kern = flat_step_kernel<KIND, T, GT, MIXED, U>;
+  int u_eff = U;
+  auto kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB>;
   if constexpr (sizeof(T) == 4) {
     // tuning knob MCO_FLAT_VARIANT: "w4m4" = 128-bit accesses with
     // 4 CTAs/SM, "w8m4" = 256-bit with 4 CTAs/SM, default 256-bit occupancy-driven
@@ -400,7 +404,8 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       const char* e = getenv("MCO_FLAT_VARIANT");
       if (!e) return 0;
       const std::string s(e);
-      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : s == "pf" ? 4 : 0;
+      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : s == "pf" ? 4 :
+             s == "u1m3" ? 5 : s == "u2m3" ? 6 : 0;
     }();
     if (variant == 1) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
@@ -412,13 +417,19 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       W = 4;
     } else if (variant == 4) {
       kern = flat_step_kernel_pf<KIND, T, GT, MIXED>;
+    } else if (variant == 5) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, 1, 3>;
+      u_eff = 1;
+    } else if (variant == 6) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, 2, 3>;
+      u_eff = 2;
     }
   }
   bool vec = aligned(a.p, sizeof(T) * W) && aligned(a.g, sizeof(GT) * W);
   for (int i = 0; i < 4; ++i) vec = vec && aligned(a.s[i], sizeof(T) * W);
   if (MIXED) vec = vec && aligned(a.p_out_bf16, 2 * W);
   const uint64_t nvec = vec ? a.n / W : 0;
-  const uint64_t items = nvec ? (nvec + U - 1) / U : a.n;
+  const uint64_t items = nvec ? (nvec + u_eff - 1) / u_eff : a.n;
   const int dev = current_device();
   const int grid = grid_for(kern, std::max<uint64_t>(items, 1), dev);
   kern<<<grid, kThreads, 0, st>>>((T*)a.p, (const GT*)a.g, (T*)a.s[0], (T*)a.s[1], (T*)a.s[2],
