@@ -36,6 +36,14 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kRB = 2;   // K1 / K6 tiles: rows per thread per loop iteration (loads in flight)
+#ifndef MCO_K1_MINB
+#define MCO_K1_MINB 3
+#endif
+#ifndef MCO_K4_MINB
+#define MCO_K4_MINB 3
+#endif
+constexpr int kMinCtasK1 = MCO_K1_MINB;  // resident CTAs per SM (register cap)
+constexpr int kMinCtasK4 = MCO_K4_MINB;
 
 struct Ctx {
   const Tile* tiles;
@@ -123,7 +131,7 @@ __device__ __forceinline__ float* pptr(const Ptrs& P, const TensorInfo& T) {
 
 // ============================ K1: statistics =====================================
 template <bool VEC, typename GT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kMinCtasK1)
     k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles) {
   __shared__ float colbuf[kThreads * VW];
   __shared__ float rowbuf[kMaxTileRows * 4];
@@ -397,7 +405,7 @@ __device__ __forceinline__ void chunk_vec_load(const GT* g, int64_t e, int64_t e
 }
 
 template <bool VEC, typename GT>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kMinCtasK4)
     k4_usq(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double b2, double eps) {
   __shared__ double scratch[32];
   const float sf = (float)c.glob[0], epsf = (float)eps;
