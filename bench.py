@@ -115,8 +115,10 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 
 def cpu_sample_shapes():
-    from paper_2312_00407_b200.registry import LLAMA_7B
+    from paper_2312_00407_b200.registry import CONFIG1, LLAMA_7B
 
+    if os.environ.get("MCO_CPU_SAMPLE") == "tiny":  # CPU test of the bench contract
+        return CONFIG1.shapes()[1:10]
     return LLAMA_7B.shapes()[1:10]  # one decoder layer: 9 tensors, 202,383,360 params
 
 
@@ -149,7 +151,7 @@ def run_cpu_reference(warmup: int, steps: int):
         log(f"[cpu-ref] {k}: {sec * 1e3:.1f} ms/step, {n / sec / 1e9:.3f} Gparam/s "
             f"({threads} threads)")
     value = len(KINDS) * n / total
-    sample = (f"one LLaMA-7B decoder layer (9 tensors, {n} fp64 params) per optimizer, "
+    sample = (f"one decoder layer of the registry (9 tensors, {n} fp64 params) per optimizer, "
               f"{warmup} warm-up + {steps} timed steps, one FlatOptimizer per thread over "
               "disjoint slices (stored-state kinds) / tensors across threads (LOMO, AdaLomo)")
     return value, threads, sample, per, total / max(steps, 1)
