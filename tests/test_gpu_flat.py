@@ -220,3 +220,13 @@ def test_state_bytes_match_device_memory():
         assert opt.state_bytes_runtime() == nbuf * n * 4
         assert abs(used - opt.state_bytes_runtime()) <= (4 << 20) * nbuf  # allocation granularity
         del opt
+
+
+def test_empty_step_advances_counter_like_the_reference():
+    # optim.cpp:100-112: empty spans pass the length check, ++t, no element loop
+    opt = optim.FlatOptimizer(cfg_for(Kind.ADAN), 0)
+    e = torch.empty(0, device="cuda")
+    opt.step(e, e, 1e-3)
+    assert opt.steps_taken() == 1
+    optim.lomo_apply(e, e, 1e-3)
+    assert optim.sumsq(e).item() == 0.0
