@@ -1,0 +1,60 @@
+"""Randomised parity sweep (fixed seed): random optimizer kind, length, element
+offset (alignment), gradient dtype, hyper-parameters and step count -- the fp32
+kernels must stay bit-exact with the restatement for every draw."""
+import numpy as np
+import pytest
+
+import oracle as O
+from paper_2312_00407_b200 import optim
+from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+rng = np.random.default_rng(20260)
+CASES = []
+for i in range(40):
+    CASES.append(dict(kind=int(rng.integers(0, 4)), n=int(rng.choice([1, 7, 8, 9, 63, 4096,
+                                                                       12345, 100003])),
+                      off=int(rng.integers(0, 9)), bf16=bool(rng.random() < 0.3),
+                      mixed=bool(rng.random() < 0.3), lr=float(10 ** rng.uniform(-5, -1)),
+                      wd=float(rng.choice([0.0, 0.01, 0.1])), b1=float(rng.uniform(0.5, 0.99)),
+                      b2=float(rng.uniform(0.9, 0.9999)), b3=float(rng.uniform(0.9, 0.999)),
+                      k=int(rng.integers(1, 5)), steps=int(rng.integers(1, 5)), seed=i))
+
+
+@pytest.mark.parametrize("c", CASES, ids=[f"case{i}" for i in range(len(CASES))])
+def test_random_case_bit_exact(c):
+    cfg = OptimizerConfig.defaults_for(Kind(c["kind"]))
+    cfg.weight_decay, cfg.beta1, cfg.beta2, cfg.beta3 = c["wd"], c["b1"], c["b2"], c["b3"]
+    cfg.update_interval = c["k"]
+    n, off = c["n"], c["off"]
+    pbig = O.synth(n + off, c["seed"], 0, 0, 0, 0, -6, 0, False)
+    tp = torch.from_numpy(pbig.copy()).cuda()
+    p = pbig[off:].copy()
+    opt, orc = optim.FlatOptimizer(cfg, n), O.OracleFlat(cfg, n, np.float32)
+    out = torch.empty(n, dtype=torch.bfloat16, device="cuda") if c["mixed"] else None
+    for t in range(1, c["steps"] + 1):
+        if c["bf16"]:
+            gb = O.synth(n + off, c["seed"], 1, 0, t, 0, -7, 10, False, "bf16")
+            tg = torch.from_numpy(gb.view(np.int16)).cuda().view(torch.bfloat16)[off:]
+            g = O.bf16_to_f32(gb[off:])
+        else:
+            gbig = O.synth(n + off, c["seed"], 1, 0, t, 0, -7, 10, False)
+            tg = torch.from_numpy(gbig).cuda()[off:]
+            g = gbig[off:].copy()
+        if out is not None:
+            opt.step_mixed(tp[off:], tg, out, c["lr"])
+        else:
+            opt.step(tp[off:], tg, c["lr"])
+        orc.step(p, np.ascontiguousarray(g), c["lr"])
+    torch.cuda.synchronize()
+    got = tp.cpu().numpy()
+    assert np.array_equal(got[off:].view(np.uint32), p.view(np.uint32))
+    assert np.array_equal(got[:off].view(np.uint32), pbig[:off].view(np.uint32))
+    for name, buf in opt.buffers():
+        assert np.array_equal(buf.cpu().numpy().view(np.uint32),
+                              orc.state[name].view(np.uint32)), name
+    if out is not None:
+        assert np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16),
+                              O.f32_to_bf16(p))
