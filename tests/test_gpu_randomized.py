@@ -58,3 +58,55 @@ def test_random_case_bit_exact(c):
     if out is not None:
         assert np.array_equal(out.view(torch.int16).cpu().numpy().view(np.uint16),
                               O.f32_to_bf16(p))
+
+
+ADA_CASES = []
+for i in range(12):
+    shapes = []
+    for _ in range(int(rng.integers(1, 6))):
+        if rng.random() < 0.25:
+            shapes.append((int(rng.integers(1, 3000)),))
+        else:
+            shapes.append((int(rng.integers(1, 300)), int(rng.choice([1, 3, 8, 17, 256, 1000,
+                                                                      1032, 2100]))))
+    ADA_CASES.append(dict(shapes=shapes, clip=float(rng.choice([0.0, 1e-3, 1e3])),
+                          bf16=bool(rng.random() < 0.3), lr=float(10 ** rng.uniform(-4, -2)),
+                          seed=100 + i))
+
+
+@pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("c", ADA_CASES, ids=[f"ada{i}" for i in range(len(ADA_CASES))])
+def test_random_adalomo_within_tolerance(c):
+    shapes = c["shapes"]
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    if c["clip"] > 0:
+        cfg.clip_threshold = c["clip"]
+    ps = O.registry_params(shapes, c["seed"], np.float64)
+    p0 = [x.copy() for x in ps]
+    st, o = optim.AdaLomoState(cfg, shapes), O.OracleAdaLomo(cfg, shapes)
+    tp = torch.from_numpy(np.concatenate(ps).astype(np.float32)).cuda()
+    for t in range(1, 3):
+        gs = O.registry_grads(shapes, c["seed"], t, np.float32)
+        gflat = np.concatenate(gs)
+        if c["bf16"]:
+            gb = O.f32_to_bf16(gflat)
+            tg = torch.from_numpy(gb.view(np.int16)).cuda().view(torch.bfloat16)
+            gflat = O.bf16_to_f32(gb)
+        else:
+            tg = torch.from_numpy(gflat).cuda()
+        st.apply_all(tp, tg, c["lr"])
+        g64 = gflat.astype(np.float64)
+        scale = 1.0
+        if c["clip"] > 0:
+            scale = O.orc.orc_clip_scale(O.orc.orc_sumsq_f64(O._ptr(g64), g64.size), c["clip"])
+        offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+        for k in range(len(shapes)):
+            o.apply(k, ps[k], g64[offs[k]:offs[k + 1]].copy(), c["lr"], scale)
+    torch.cuda.synchronize()
+    got = tp.cpu().numpy().astype(np.float64)
+    offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+    for k in range(len(shapes)):
+        want = ps[k]
+        rms = max(float(np.sqrt(np.mean(p0[k] ** 2))), 1e-30)
+        err = np.max(np.abs(got[offs[k]:offs[k + 1]] - want) / np.maximum(np.abs(want), rms))
+        assert err <= 1e-5, (k, shapes[k], err)
