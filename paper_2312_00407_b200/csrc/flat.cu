@@ -15,6 +15,7 @@
 #include <string>
 #include <unordered_map>
 
+#include "flat_tma.h"
 #include "kernels.h"
 #include "update.cuh"
 
@@ -405,7 +406,7 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       if (!e) return 0;
       const std::string s(e);
       return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : s == "pf" ? 4 :
-             s == "u1m3" ? 5 : s == "u2m3" ? 6 : 0;
+             s == "u1m3" ? 5 : s == "u2m3" ? 6 : s == "tma" ? 7 : 0;
     }();
     if (variant == 1) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
@@ -423,6 +424,9 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
     } else if (variant == 6) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, 2, 3>;
       u_eff = 2;
+    } else if (variant == 7 && flat_tma_eligible(a)) {
+      launch_flat_tma(a, k, st);
+      return;
     }
   }
   bool vec = aligned(a.p, sizeof(T) * W) && aligned(a.g, sizeof(GT) * W);
