@@ -157,6 +157,24 @@ def run_cpu_reference(warmup: int, steps: int):
     return value, threads, sample, per, total / max(steps, 1)
 
 
+def run_cpu_single_thread():
+    """The reference on ONE host thread (T = nproc and T = 1), on a
+    smaller sample: the first q-projection matrix of the 7B registry."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    shapes = cpu_sample_shapes()[1:2]
+    n = sum(int(__import__("math").prod(s)) for s in shapes)
+    per, total = {}, 0.0
+    for k in KINDS:
+        sec = O.ref_bench(make_cfg(k), shapes, 1, 1, 1)
+        per[k] = {"ms": round(sec * 1e3, 2), "params_per_s": n / sec}
+        total += sec
+    return {"value": len(KINDS) * n / total, "unit": "params/s", "cores": 1,
+            "sample": f"one {shapes[0][0]}x{shapes[0][1]} matrix ({n} fp64 params) per "
+                      "optimizer, 1 warm-up + 1 timed step", "per_optimizer": per}
+
+
 # ---------------------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------------------
@@ -260,13 +278,19 @@ def bench_ours(args, rank, world, local_rank):
         l0 = optim.launch_count()
         if kind == kinds[0]:
             clocks.start()
+        # per-step events (Sophia: refresh steps write h, SURVEY 8(d) reports them apart)
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+        t0 = st.opt.steps_taken() if kind in ("adamw", "lion", "adan", "sophia") else 0
         e0.record(stream)
-        for _ in range(args.steps):
+        evs[0].record(stream)
+        for i in range(args.steps):
             st.step()
+            evs[i + 1].record(stream)
         e1.record(stream)
         torch.cuda.synchronize()
         launches += optim.launch_count() - l0
         ms = e0.elapsed_time(e1) / args.steps
+        step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
         if world > 1:
             t = torch.tensor([ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -278,6 +302,17 @@ def bench_ours(args, rank, world, local_rank):
                      "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
                      "params_per_launch": st.n,
                      "launches_per_step": (optim.launch_count() - l0) / max(args.steps, 1)}
+        if kind == "sophia":
+            k = st.cfg.update_interval
+            ref = [m for i, m in enumerate(step_ms) if (t0 + i) % k == 0]  # t-1 = t0+i
+            non = [m for i, m in enumerate(step_ms) if (t0 + i) % k != 0]
+            for name, xs, b in (("refresh", ref, 28), ("non_refresh", non, 24)):
+                if xs:
+                    m = sum(xs) / len(xs)
+                    per[kind][name] = {"steps": len(xs), "ms": round(m, 4),
+                                       "bytes_per_param": b,
+                                       "frac_of_measured_hbm": round(
+                                           b * st.n / (m * 1e-3) / 1e9 / hbm_peak, 4)}
         total_ms += ms
         log(f"[rank {rank}] {kind}: {ms:.3f} ms/step, {P / ms / 1e6:.1f} Gparam/s (all GPUs), "
             f"{gbs:.0f} GB/s/GPU = {gbs / hbm_peak:.3f} of {peak_src} HBM")
@@ -361,6 +396,39 @@ def load_traffic(kind, params_per_launch):
         return None
 
 
+def pcie_ceiling(hp, dev):
+    """Pinned-host copy bandwidth on this box (GB/s): H2D, D2H, and both at once
+    (two streams) -- the roofline of the host-buffer path."""
+    import torch
+
+    n = min(hp.numel(), 1 << 28)  # 1 GiB
+    d = torch.empty(n, device=dev)
+    d2 = torch.empty(n, device=dev)
+    h2 = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def bw(fn, nbytes, it=4):
+        fn()
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        for _ in range(it):
+            fn()
+        torch.cuda.synchronize()
+        return nbytes * it / (time.perf_counter() - t) / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(hp[:n], non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    out = {"h2d_gbs": bw(lambda: d.copy_(hp[:n], non_blocking=True), 4 * n),
+           "d2h_gbs": bw(lambda: h2.copy_(d, non_blocking=True), 4 * n),
+           "both_gbs": bw(both, 8 * n)}
+    del d, d2, h2
+    return {k: round(v, 1) for k, v in out.items()}
+
+
 def bench_e2e(args, res):
     """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p)."""
     import psutil
@@ -384,6 +452,8 @@ def bench_e2e(args, res):
     hg = torch.empty(n, dtype=torch.float32, pin_memory=True)
     hp.copy_(res["p"][:n].cpu())
     hg.copy_(res["g"][:n].cpu())
+    pcie = pcie_ceiling(hp, res["p"].device)
+    log(f"[e2e] PCIe ceiling (pinned, GB/s): {pcie}")
     steps = max(1, min(args.steps, args.e2e_steps))
     tot_s, h2d, d2h = 0.0, 0, 0
     per = {}
@@ -418,8 +488,14 @@ def bench_e2e(args, res):
         h2d += 2 * n * 4
         d2h += n * 4
         log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {n / dt / 1e9:.2f} Gparam/s")
+    # the copies bound the step: max(H2D bytes / H2D BW, D2H / D2H BW, all / both-ways BW)
+    bound_s = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
+                  (h2d + d2h) / (pcie["both_gbs"] * 1e9))
     return {"value": len(per) * n / tot_s, "unit": "params/s", "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "params": n, "per_optimizer": per,
+            "roofline": {"bound": "pcie", "achieved": round((h2d + d2h) / tot_s / 1e9, 1),
+                         "unit": "GB/s", "peak": pcie, "peak_source": "measured in this run",
+                         "frac": round(bound_s / tot_s, 4)},
             "path": "C-ABI host-span calls on pinned host buffers: mco_flat_step_host, "
                     "mco_lomo_apply_host, mco_adalomo_apply_all_host (H2D p+g, update, D2H p "
                     "pipelined per chunk / per tensor)"}
@@ -495,6 +571,7 @@ def main():
             v, threads, sample, per, _ = run_cpu_reference(1, args.cpu_steps)
             cpu = {"value": v, "unit": "params/s", "cores": threads, "kind": "reference",
                    "sample": sample, "per_optimizer": per}
+            cpu["single_thread"] = run_cpu_single_thread()
         except Exception as ex:
             log(f"[cpu_baseline] failed: {ex!r}")
     if rank == 0:

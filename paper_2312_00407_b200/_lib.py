@@ -103,6 +103,8 @@ _SIGS = {
                             _i, _i, _p]),
     "mco_sync": (_i, [_p]),
     "mco_device_count": (_i, [C.POINTER(_i)]),
+    "mco_set_flat_variant": (_i, [C.c_char_p]),
+    "mco_flat_variant": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

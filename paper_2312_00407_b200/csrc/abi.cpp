@@ -962,6 +962,12 @@ mco_status mco_sync(void* stream) {
   return guard([&] { MCO_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream)); });
 }
 
+mco_status mco_set_flat_variant(const char* name) {
+  return guard([&] { set_flat_variant(name ? name : ""); });
+}
+
+const char* mco_flat_variant(void) { return flat_variant_name(); }
+
 mco_status mco_device_count(int* out) {
   return guard([&] {
     *out = 0;

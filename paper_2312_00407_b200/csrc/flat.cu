@@ -10,6 +10,7 @@
 // arithmetic is the reference's operation order, no fused multiply-add, IEEE
 // division and square root -- bit-identical to oracle/mco_oracle.c.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -363,6 +364,31 @@ __global__ void synth_kernel(void* dst, int dtype, uint64_t n, uint64_t key, int
   }
 }
 
+// ---- tuning knob: flat-kernel variant ----------------------------------------
+// mco_set_flat_variant(name) or MCO_FLAT_VARIANT (read at first use).  "" / "ldg" is
+// the default 256-bit LDG kernel; the others are the measured alternatives kept for
+// A/B runs on new hardware.
+const char* const kVariantNames[] = {"ldg", "w4m4", "w8m4", "w4m1", "pf", "u1m3", "u2m3", "tma"};
+std::atomic<int> g_variant{-1};
+
+int parse_flat_variant(const char* name) {
+  const std::string s(name ? name : "");
+  if (s.empty()) return 0;
+  for (int i = 0; i < (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0])); ++i)
+    if (s == kVariantNames[i]) return i;
+  return -1;
+}
+
+int flat_variant() {
+  int v = g_variant.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char* e = getenv("MCO_FLAT_VARIANT");
+    v = e ? std::max(parse_flat_variant(e), 0) : 0;
+    g_variant.store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
 // ---- launch configuration --------------------------------------------------------
 template <typename K>
 int grid_for(K kernel, uint64_t work_items, int device) {
@@ -401,13 +427,7 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   if constexpr (sizeof(T) == 4) {
     // tuning knob MCO_FLAT_VARIANT: "w4m4" = 128-bit accesses with
     // 4 CTAs/SM, "w8m4" = 256-bit with 4 CTAs/SM, default 256-bit occupancy-driven
-    static const int variant = [] {
-      const char* e = getenv("MCO_FLAT_VARIANT");
-      if (!e) return 0;
-      const std::string s(e);
-      return s == "w4m4" ? 1 : s == "w8m4" ? 2 : s == "w4m1" ? 3 : s == "pf" ? 4 :
-             s == "u1m3" ? 5 : s == "u2m3" ? 6 : s == "tma" ? 7 : 0;
-    }();
+    const int variant = flat_variant();
     if (variant == 1) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
       W = 4;
@@ -555,5 +575,13 @@ void launch_synth(void* dst, int dtype, uint64_t n, uint64_t key, int64_t cols, 
                                                       zero_log2, rowcol);
   launch_check("synth_kernel");
 }
+
+void set_flat_variant(const char* name) {
+  const int v = parse_flat_variant(name);
+  if (v < 0) throw Error(MCO_CONFIG, std::string("unknown flat-kernel variant '") + name + "'");
+  g_variant.store(v, std::memory_order_relaxed);
+}
+
+const char* flat_variant_name() { return kVariantNames[flat_variant()]; }
 
 }  // namespace mco

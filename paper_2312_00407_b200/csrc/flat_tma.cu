@@ -7,9 +7,10 @@
 //   (mbarrier complete_tx)                      ld.shared, update, st.shared,
 //                                               fence.proxy.async; arrive done[s]
 //   wait done[s]; cp.async.bulk smem->global
-//   for every written stream; once the store
-//   has read smem, refill stage s with tile
-//   i + STAGES
+//   for every written stream; then refill the
+//   PREVIOUS tile's stage (its store has had a
+//   tile-time to read smem) with tile
+//   i - 1 + STAGES
 //
 // One CTA per SM; STAGES-1 tiles of every input stream are in flight per SM
 // (Adan: 3 x 48 KB) independent of register pressure, which is what limits the
@@ -81,8 +82,8 @@ __device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ void bulk_wait_read_all() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+__device__ __forceinline__ void bulk_wait_read_1() {
+  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() {
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -155,9 +156,12 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
         }
         if constexpr (MIXED) bulk_s2g(pout + e, obuf + (size_t)s * kTile, kTile * 2);
         bulk_commit();
-        if (i + NS < mine) {
-          bulk_wait_read_all();  // the stage's smem has been read out by the store
-          issue(i + NS);
+        // refill the PREVIOUS tile's stage: its store group (all but the one just
+        // committed) has had a tile-time to drain out of smem, so the wait is short and
+        // the producer never stalls on the store it has just issued
+        if (i >= 1 && i - 1 + NS < mine) {
+          bulk_wait_read_1();
+          issue(i - 1 + NS);
         }
       }
       bulk_wait_all();

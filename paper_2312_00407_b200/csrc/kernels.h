@@ -28,6 +28,11 @@ struct FlatArgs {
 void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
                       const StepConsts<double>& kd, cudaStream_t st);
 
+// Flat-kernel variant (tuning knob; "ldg" default, "tma", ...).  Throws CONFIG on an
+// unknown name.
+void set_flat_variant(const char* name);
+const char* flat_variant_name();
+
 // LOMO p -= f*g with f = lr*scale (host) or derived from a device Σg² (clip).
 void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
                  double scale, const double* dev_sumsq, double clip, cudaStream_t st);

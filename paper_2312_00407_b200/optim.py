@@ -500,6 +500,15 @@ def synth_fill(t, seed: int, role: int, tensor: int, step: int, cols: int = 0,
                               int(zero_log2), int(rowcol), _stream(stream)))
 
 
+def set_flat_variant(name: str) -> None:
+    """Select the stored-state kernels' data-movement variant ("ldg" default, "tma")."""
+    _check(lib.mco_set_flat_variant(name.encode()))
+
+
+def flat_variant() -> str:
+    return lib.mco_flat_variant().decode()
+
+
 def launch_count() -> int:
     """Kernel launches issued by libmco in this process."""
     return int(lib.mco_launch_count())

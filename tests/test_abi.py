@@ -52,3 +52,15 @@ def test_config_struct_layout_matches_header():
 
 def test_no_gpu_reports_zero_devices_or_real_count():
     assert optim.device_count() >= 0
+
+
+def test_flat_variant_knob_host_side():
+    from paper_2312_00407_b200 import optim
+
+    prev = optim.flat_variant()
+    with pytest.raises(optim.ConfigError, match="unknown flat-kernel variant 'nope'"):
+        optim.set_flat_variant("nope")
+    assert optim.flat_variant() == prev
+    optim.set_flat_variant("tma")
+    assert optim.flat_variant() == "tma"
+    optim.set_flat_variant(prev)

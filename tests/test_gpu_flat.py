@@ -230,3 +230,40 @@ def test_empty_step_advances_counter_like_the_reference():
     assert opt.steps_taken() == 1
     optim.lomo_apply(e, e, 1e-3)
     assert optim.sumsq(e).item() == 0.0
+
+
+@pytest.fixture
+def flat_variant():
+    """Switch the stored-state kernels' data-movement variant for one test."""
+    prev = optim.flat_variant()
+    yield optim.set_flat_variant
+    optim.set_flat_variant(prev)
+
+
+@pytest.mark.parametrize("variant", ["tma", "pf", "w4m4"])
+@pytest.mark.parametrize("kind", FLAT)
+@pytest.mark.parametrize("n", [2048, 3 * 2048 + 77, (1 << 20) + 5])
+def test_kernel_variants_bit_exact(flat_variant, variant, kind, n):
+    """Every data-movement variant (TMA bulk-copy pipeline included) produces the
+    restatement's bits: tail elements, Adan's t == 1, Sophia refresh / non-refresh,
+    mixed bf16 replica output."""
+    flat_variant(variant)
+    assert optim.flat_variant() == variant
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=3)
+    p = O.synth(n, 77, 0, 3, 0, 0, -6, 0, False)
+    tp, tpo = dev(p), torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    opt = optim.FlatOptimizer(cfg, n)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    for t in range(1, 6):
+        g = O.synth(n, 77, 1, 3, t, 0, -7, 10, False)
+        if t == 5:
+            opt.step_mixed(tp, dev(g), tpo, 1e-3)
+        else:
+            opt.step(tp, dev(g), 1e-3)
+        orc.step(p, g, 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    assert bits_equal(tpo.view(torch.int16).cpu().numpy().view(np.uint16), O.f32_to_bf16(p))
+    for name, t in opt.buffers():
+        assert bits_equal(t.cpu().numpy(), orc.state[name]), name
+
