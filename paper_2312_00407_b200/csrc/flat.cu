@@ -28,8 +28,15 @@ constexpr int kThreads = 256;
 
 // MINB > 1 caps registers so MINB CTAs fit per SM (Adan streams 11 buffers).
 // WV: elements per vector access (8 f32 = 256-bit, 4 f32 = 128-bit, 4 f64 = 256-bit).
+__device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ptr), "r"(bytes) : "memory");
+}
+
+// PFD > 0: each warp bulk-prefetches (cp.async.bulk.prefetch.L2) the 1 KB segments of
+// every input stream it will load PFD grid-stride iterations later, so the LDGs of
+// that iteration hit L2 (more bytes in flight than the register file holds).
 template <int KIND, typename T, typename GT, bool MIXED, int U, int MINB = 1,
-          int WV = Vec<T>::W>
+          int WV = Vec<T>::W, int PFD = 0>
 __global__ void __launch_bounds__(kThreads, MINB)
     flat_step_kernel(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
                      T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
@@ -39,6 +46,21 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t base = tid; base < nvec; base += stride * U) {
+    if constexpr (PFD > 0) {
+      constexpr int NIN = KIND == K_ADAN ? 6 : (reads_s1(KIND) ? 4 : 3);
+      const int lane = threadIdx.x & 31;
+      const int j = lane % NIN, u = lane / NIN;
+      const uint64_t w0 = base - lane + (uint64_t)PFD * stride * U + (uint64_t)u * stride;
+      if (u < U && w0 + 32 <= nvec && !(KIND == K_ADAN && j == 5 && k.first)) {
+        const uint64_t e = w0 * W;
+        if (j == 1) {
+          prefetch_l2(g + e, 32 * W * sizeof(GT));
+        } else {
+          const T* src = j == 0 ? p : j == 2 ? s0 : j == 3 ? s1 : j == 4 ? s2 : s3;
+          prefetch_l2(src + e, 32 * W * sizeof(T));
+        }
+      }
+    }
     T pv[U][W], gv[U][W], a[U][W], b[U][W], c[U][W], d[U][W];
     // issue every load of the U vectors before any arithmetic
 #pragma unroll
@@ -368,7 +390,8 @@ __global__ void synth_kernel(void* dst, int dtype, uint64_t n, uint64_t key, int
 // mco_set_flat_variant(name) or MCO_FLAT_VARIANT (read at first use).  "" / "ldg" is
 // the default 256-bit LDG kernel; the others are the measured alternatives kept for
 // A/B runs on new hardware.
-const char* const kVariantNames[] = {"ldg", "w4m4", "w8m4", "w4m1", "pf", "u1m3", "u2m3", "tma"};
+const char* const kVariantNames[] = {"ldg",  "w4m4", "w8m4",  "w4m1",  "pf",
+                                     "u1m3", "u2m3", "tma",   "l2pf1", "l2pf2", "l2pf4"};
 std::atomic<int> g_variant{-1};
 
 int parse_flat_variant(const char* name) {
@@ -444,6 +467,12 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
     } else if (variant == 6) {
       kern = flat_step_kernel<KIND, T, GT, MIXED, 2, 3>;
       u_eff = 2;
+    } else if (variant == 8) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 1>;
+    } else if (variant == 9) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 2>;
+    } else if (variant == 10) {
+      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 4>;
     } else if (variant == 7 && flat_tma_eligible(a)) {
       launch_flat_tma(a, k, st);
       return;
