@@ -326,7 +326,9 @@ def bench_ours(args, rank, world, local_rank):
     # dominant kernel = the optimizer with the largest share of the step
     dom = max(per, key=lambda k: per[k]["ms"])
     npl = per[dom]["params_per_launch"]
-    roofline = {"bound": "hbm", "kernel": f"{dom} update (flat_step_kernel)" if dom not in (
+    kname = ("flat_tma_kernel: cp.async.bulk + mbarrier pipeline"
+             if optim.flat_variant() == "tma" else f"flat_step_kernel, variant {optim.flat_variant()}")
+    roofline = {"bound": "hbm", "kernel": f"{dom} update ({kname})" if dom not in (
         "lomo", "adalomo") else dom, "achieved": per[dom]["achieved_gbs_per_gpu"],
         "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
         "frac": round(per[dom]["achieved_gbs_per_gpu"] / hbm_peak, 4),

@@ -239,11 +239,13 @@ mco_status mco_synth_fill(void* dst, int dtype, uint64_t n, uint64_t seed, uint3
 /* ---- misc -------------------------------------------------------------------- */
 mco_status mco_sync(void* stream);                 /* cudaStreamSynchronize + error check */
 mco_status mco_device_count(int* out);
-/* Tuning knob (no reference counterpart): data-movement variant of the stored-state
- * kernels, process-wide.  "ldg" (default: 256-bit LDG/STG, persistent grid-stride) or
- * "tma" (cp.async.bulk + mbarrier pipeline); other names are the measured alternatives
- * listed in DESIGN.md.  Results are bit-identical across variants.  Initial value from
- * the MCO_FLAT_VARIANT environment variable.  CONFIG on an unknown name. */
+/* Tuning knob (no reference counterpart): data-movement variant of the fp32
+ * stored-state kernels, process-wide.  "tma" (default: cp.async.bulk + mbarrier
+ * producer/consumer pipeline when the call is eligible -- fp32 params / grads / state,
+ * 16 B aligned, >= one tile -- else "ldg") or "ldg" (256-bit LDG/STG, persistent
+ * grid-stride); other names are the measured alternatives listed in DESIGN.md.
+ * Results are bit-identical across variants.  Initial value from the
+ * MCO_FLAT_VARIANT environment variable.  CONFIG on an unknown name. */
 mco_status mco_set_flat_variant(const char* name);
 const char* mco_flat_variant(void);
 /* Kernel launches issued by this library on the calling process (counter). */

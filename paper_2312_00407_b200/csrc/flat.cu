@@ -386,18 +386,25 @@ __global__ void synth_kernel(void* dst, int dtype, uint64_t n, uint64_t key, int
   }
 }
 
-// ---- tuning knob: flat-kernel variant ----------------------------------------
-// mco_set_flat_variant(name) or MCO_FLAT_VARIANT (read at first use).  "" / "ldg" is
-// the default 256-bit LDG kernel; the others are the measured alternatives kept for
-// A/B runs on new hardware.
-const char* const kVariantNames[] = {"ldg",  "w4m4", "w8m4",  "w4m1",  "pf",
-                                     "u1m3", "u2m3", "tma",   "l2pf1", "l2pf2", "l2pf4"};
+// ---- data-movement variant of the fp32 stored-state kernels -------------------------
+// mco_set_flat_variant(name) or MCO_FLAT_VARIANT (read at first use).  Default "tma":
+// the cp.async.bulk / mbarrier pipeline (flat_tma.cu) when the call is eligible (fp32
+// params / grads / state, 16 B aligned, >= one tile), else the LDG kernel.  The rest
+// are the measured alternatives kept for A/B runs; every variant
+// produces the same bits.
+enum Variant {
+  V_TMA, V_LDG, V_W4M4, V_W8M4, V_W4M1, V_PF, V_U1M3, V_U2M3, V_L2PF1, V_L2PF2, V_L2PF4,
+  V_TMA_S3, V_TMA_S5, V_TMA24, V_TMA8, V_COUNT
+};
+const char* const kVariantNames[V_COUNT] = {
+    "tma",   "ldg",   "w4m4",  "w8m4",   "w4m1",   "pf",    "u1m3", "u2m3",
+    "l2pf1", "l2pf2", "l2pf4", "tma_s3", "tma_s5", "tma24", "tma8"};
 std::atomic<int> g_variant{-1};
 
 int parse_flat_variant(const char* name) {
   const std::string s(name ? name : "");
-  if (s.empty()) return 0;
-  for (int i = 0; i < (int)(sizeof(kVariantNames) / sizeof(kVariantNames[0])); ++i)
+  if (s.empty()) return V_TMA;
+  for (int i = 0; i < V_COUNT; ++i)
     if (s == kVariantNames[i]) return i;
   return -1;
 }
@@ -448,33 +455,27 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   int u_eff = U;
   auto kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB>;
   if constexpr (sizeof(T) == 4) {
-    // tuning knob MCO_FLAT_VARIANT: "w4m4" = 128-bit accesses with
-    // 4 CTAs/SM, "w8m4" = 256-bit with 4 CTAs/SM, default 256-bit occupancy-driven
     const int variant = flat_variant();
-    if (variant == 1) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>;
-      W = 4;
-    } else if (variant == 2) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 8>;
-    } else if (variant == 3) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, 1, 4>;
-      W = 4;
-    } else if (variant == 4) {
-      kern = flat_step_kernel_pf<KIND, T, GT, MIXED>;
-    } else if (variant == 5) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, 1, 3>;
-      u_eff = 1;
-    } else if (variant == 6) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, 2, 3>;
-      u_eff = 2;
-    } else if (variant == 8) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 1>;
-    } else if (variant == 9) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 2>;
-    } else if (variant == 10) {
-      kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 4>;
-    } else if (variant == 7 && flat_tma_eligible(a)) {
-      launch_flat_tma(a, k, st);
+    int tma_cfg = -1;  // flat_tma.h configurations
+    switch (variant) {
+      case V_TMA: tma_cfg = 0; break;
+      case V_TMA_S3: tma_cfg = 1; break;
+      case V_TMA_S5: tma_cfg = 2; break;
+      case V_TMA24: tma_cfg = 3; break;
+      case V_TMA8: tma_cfg = 4; break;
+      case V_W4M4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>; W = 4; break;
+      case V_W8M4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 8>; break;
+      case V_W4M1: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 1, 4>; W = 4; break;
+      case V_PF: kern = flat_step_kernel_pf<KIND, T, GT, MIXED>; break;
+      case V_U1M3: kern = flat_step_kernel<KIND, T, GT, MIXED, 1, 3>; u_eff = 1; break;
+      case V_U2M3: kern = flat_step_kernel<KIND, T, GT, MIXED, 2, 3>; u_eff = 2; break;
+      case V_L2PF1: kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 1>; break;
+      case V_L2PF2: kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 2>; break;
+      case V_L2PF4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 4>; break;
+      default: break;  // V_LDG
+    }
+    if (tma_cfg >= 0 && flat_tma_eligible(a, tma_cfg)) {
+      launch_flat_tma(a, k, st, tma_cfg);
       return;
     }
   }

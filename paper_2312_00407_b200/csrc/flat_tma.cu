@@ -2,8 +2,8 @@
 // Adan / Sophia, fp32).  Same arithmetic (update.cuh) and therefore the same bits
 // as flat_step_kernel; only the data movement differs:
 //
-//   producer warp (one elected lane)          consumer warps (256 threads)
-//   cp.async.bulk global->smem, per stream  ->  wait full[s]; 8 elements / thread:
+//   producer warp (one elected lane)          consumer warps (512 threads)
+//   cp.async.bulk global->smem, per stream  ->  wait full[s]; 4 elements / thread:
 //   (mbarrier complete_tx)                      ld.shared, update, st.shared,
 //                                               fence.proxy.async; arrive done[s]
 //   wait done[s]; cp.async.bulk smem->global
@@ -16,6 +16,7 @@
 // (Adan: 3 x 48 KB) independent of register pressure, which is what limits the
 // LDG version of the 11-stream Adan kernel to 3 CTAs/SM.
 #include <algorithm>
+#include <atomic>
 
 #include "flat_tma.h"
 #include "update.cuh"
@@ -24,25 +25,36 @@ namespace mco {
 namespace {
 
 using namespace upd;
-constexpr int kTile = 2048;  // elements per stream per stage (8 KB of fp32)
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = kConsumerWarps * 32;
-constexpr int kSmemBudget = 200 * 1024;
+// Configuration: CW consumer warps (each thread updates one float4 per stream per
+// stage, so a tile is CW*128 elements) and NS pipeline stages (capped by shared
+// memory).  Default 16 warps (4 per scheduler: at 8 warps ncu showed the consumers'
+// fp32 div / sqrt chains stalled on 'wait' + 'branch_resolving') and 4 stages
+// (measured: fewer starve the loads, more lose bandwidth for AdamW / Sophia).
+template <int CW_, int NS_>
+struct TmaCfg {
+  static constexpr int CW = CW_;
+  static constexpr int kConsumers = CW * 32;
+  static constexpr int kTile = CW * 32 * 4;  // elements per stream per stage
+  static constexpr int kStages = NS_;
+};
+constexpr int kSmemMax = 220 * 1024;
 
 template <int KIND>
 constexpr int n_in() {  // p, g, s0 [, s1 [, s2, s3]]
   return KIND == K_ADAN ? 6 : (KIND == K_LION ? 3 : 4);
 }
-template <int KIND, bool MIXED>
-constexpr int stages() {
-  constexpr int per = n_in<KIND>() * kTile * 4 + (MIXED ? kTile * 2 : 0);
-  constexpr int s = kSmemBudget / per;
-  return s > 8 ? 8 : s;
+template <class C, int KIND, bool MIXED>
+constexpr int stage_bytes() {
+  return n_in<KIND>() * C::kTile * 4 + (MIXED ? C::kTile * 2 : 0);
 }
-template <int KIND, bool MIXED>
+template <class C, int KIND, bool MIXED>
+constexpr int stages() {
+  constexpr int cap = kSmemMax / stage_bytes<C, KIND, MIXED>();
+  return C::kStages < cap ? C::kStages : cap;
+}
+template <class C, int KIND, bool MIXED>
 constexpr int smem_bytes() {
-  return stages<KIND, MIXED>() * (n_in<KIND>() * kTile * 4 + (MIXED ? kTile * 2 : 0)) +
-         2 * stages<KIND, MIXED>() * 8;
+  return stages<C, KIND, MIXED>() * stage_bytes<C, KIND, MIXED>() + 2 * stages<C, KIND, MIXED>() * 8;
 }
 
 __device__ __forceinline__ uint32_t sa(const void* p) {
@@ -92,21 +104,22 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-__device__ __forceinline__ void lds8(const float* s, float (&r)[8]) {
-  const float4 x = reinterpret_cast<const float4*>(s)[0], y = reinterpret_cast<const float4*>(s)[1];
-  r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w, r[4] = y.x, r[5] = y.y, r[6] = y.z, r[7] = y.w;
+// consecutive threads read consecutive 16 B: conflict-free LDS.128 / STS.128
+__device__ __forceinline__ void lds4(const float* s, float (&r)[4]) {
+  const float4 x = *reinterpret_cast<const float4*>(s);
+  r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w;
 }
-__device__ __forceinline__ void sts8(float* s, const float (&r)[8]) {
-  reinterpret_cast<float4*>(s)[0] = make_float4(r[0], r[1], r[2], r[3]);
-  reinterpret_cast<float4*>(s)[1] = make_float4(r[4], r[5], r[6], r[7]);
+__device__ __forceinline__ void sts4(float* s, const float (&r)[4]) {
+  *reinterpret_cast<float4*>(s) = make_float4(r[0], r[1], r[2], r[3]);
 }
 
-template <int KIND, bool MIXED>
-__global__ void __launch_bounds__(kConsumers + 32, 1)
+template <class C, int KIND, bool MIXED>
+__global__ void __launch_bounds__(C::kConsumers + 32, 1)
     flat_tma_kernel(float* p, const float* g, float* s0, float* s1, float* s2, float* s3,
                     uint16_t* pout, uint64_t ntiles, uint64_t n, const StepConsts<float> k) {
   constexpr int NIN = n_in<KIND>();
-  constexpr int NS = stages<KIND, MIXED>();
+  constexpr int NS = stages<C, KIND, MIXED>();
+  constexpr int kTile = C::kTile, kConsumers = C::kConsumers, kConsumerWarps = C::CW;
   extern __shared__ __align__(128) uint8_t smem[];
   float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kTile]
   uint16_t* obuf = reinterpret_cast<uint16_t*>(buf + NS * NIN * kTile);  // [NS][kTile]
@@ -167,22 +180,22 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
       bulk_wait_all();
     }
   } else {  // ---------------- consumers ----------------
-    const int c8 = threadIdx.x * 8;
+    const int c4 = threadIdx.x * 4;
     for (uint64_t i = 0; i < mine; ++i) {
       const int s = (int)(i % NS);
       mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
-      float* st = buf + (size_t)s * NIN * kTile + c8;
-      float pv[8], gv[8], a[8], b[8], c[8], d[8];
-      lds8(st, pv);
-      lds8(st + kTile, gv);
-      lds8(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) lds8(st + 3 * kTile, b);
+      float* st = buf + (size_t)s * NIN * kTile + c4;
+      float pv[4], gv[4], a[4], b[4], c[4], d[4];
+      lds4(st, pv);
+      lds4(st + kTile, gv);
+      lds4(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) lds4(st + 3 * kTile, b);
       if constexpr (KIND == K_ADAN) {
-        lds8(st + 4 * kTile, c);
-        if (!k.first) lds8(st + 5 * kTile, d);
+        lds4(st + 4 * kTile, c);
+        if (!k.first) lds4(st + 5 * kTile, d);
       }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
+      for (int j = 0; j < 4; ++j) {
         if constexpr (KIND == K_LION) b[j] = 0.f;
         if constexpr (KIND != K_ADAN) c[j] = d[j] = 0.f;
         if constexpr (KIND == K_ADAN) {
@@ -190,17 +203,17 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
         }
         update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
       }
-      sts8(st, pv);
-      sts8(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) sts8(st + 3 * kTile, b);
+      sts4(st, pv);
+      sts4(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) sts4(st + 3 * kTile, b);
       if constexpr (KIND == K_ADAN) {
-        sts8(st + 4 * kTile, c);
-        sts8(st + 5 * kTile, d);
+        sts4(st + 4 * kTile, c);
+        sts4(st + 5 * kTile, d);
       }
       if constexpr (MIXED) {
-        uint32_t* o = reinterpret_cast<uint32_t*>(obuf + (size_t)s * kTile + c8);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) o[j] = f2bf2_bits(pv[2 * j], pv[2 * j + 1]);
+        uint32_t* o = reinterpret_cast<uint32_t*>(obuf + (size_t)s * kTile + c4);
+        o[0] = f2bf2_bits(pv[0], pv[1]);
+        o[1] = f2bf2_bits(pv[2], pv[3]);
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk store
       mbar_arrive(&done[s]);
@@ -231,50 +244,79 @@ __global__ void __launch_bounds__(kConsumers + 32, 1)
   }
 }
 
-template <int KIND, bool MIXED>
+template <class C, int KIND, bool MIXED>
 void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  auto kern = flat_tma_kernel<KIND, MIXED>;
-  constexpr int smem = smem_bytes<KIND, MIXED>();
-  static bool attr = false;
-  if (!attr) {
+  auto kern = flat_tma_kernel<C, KIND, MIXED>;
+  constexpr int smem = smem_bytes<C, KIND, MIXED>();
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
+  if (!(attr_set.load() & (1ull << dev))) {
     MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    attr = true;
+    attr_set.fetch_or(1ull << dev);
   }
-  const uint64_t ntiles = a.n / kTile;
+  const uint64_t ntiles = a.n / C::kTile;
   const int grid = (int)std::max<uint64_t>(
-      1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(current_device()).sms));
-  kern<<<grid, kConsumers + 32, smem, st>>>((float*)a.p, (const float*)a.g, (float*)a.s[0],
-                                            (float*)a.s[1], (float*)a.s[2], (float*)a.s[3],
-                                            a.p_out_bf16, ntiles, a.n, k);
+      1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
+  kern<<<grid, C::kConsumers + 32, smem, st>>>((float*)a.p, (const float*)a.g, (float*)a.s[0],
+                                               (float*)a.s[1], (float*)a.s[2], (float*)a.s[3],
+                                               a.p_out_bf16, ntiles, a.n, k);
   launch_check("flat_tma_kernel");
 }
 
-template <int KIND>
+template <class C, int KIND>
 void dispatch(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
   if (a.p_out_bf16)
-    run<KIND, true>(a, k, st);
+    run<C, KIND, true>(a, k, st);
   else
-    run<KIND, false>(a, k, st);
+    run<C, KIND, false>(a, k, st);
+}
+
+template <class C>
+void launch_cfg(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
+  switch (a.kind) {
+    case MCO_ADAMW: dispatch<C, K_ADAMW>(a, k, st); break;
+    case MCO_LION: dispatch<C, K_LION>(a, k, st); break;
+    case MCO_ADAN: dispatch<C, K_ADAN>(a, k, st); break;
+    case MCO_SOPHIA: dispatch<C, K_SOPHIA>(a, k, st); break;
+    default: throw Error(MCO_CONTRACT, "flat_tma: unsupported kind");
+  }
 }
 
 }  // namespace
 
-bool flat_tma_eligible(const FlatArgs& a) {
+bool flat_tma_eligible(const FlatArgs& a, int cfg) {
   if (a.state_dtype != MCO_F32 || a.p_dtype != MCO_F32 || a.g_dtype != MCO_F32) return false;
   auto al = [](const void* q) { return q == nullptr || ((uintptr_t)q % 16) == 0; };
   bool ok = al(a.p) && al(a.g) && al(a.p_out_bf16);
   for (int i = 0; i < 4; ++i) ok = ok && al(a.s[i]);
-  return ok && a.n >= (uint64_t)kTile;
+  return ok && a.n >= (uint64_t)tma_tile(cfg);
 }
 
-void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  switch (a.kind) {
-    case MCO_ADAMW: dispatch<K_ADAMW>(a, k, st); break;
-    case MCO_LION: dispatch<K_LION>(a, k, st); break;
-    case MCO_ADAN: dispatch<K_ADAN>(a, k, st); break;
-    case MCO_SOPHIA: dispatch<K_SOPHIA>(a, k, st); break;
-    default: throw Error(MCO_CONTRACT, "flat_tma: unsupported kind");
+#define MCO_TMA_CONFIGS(X) \
+  X(0, 16, 4)                  \
+  X(1, 16, 3)                  \
+  X(2, 16, 5)                  \
+  X(3, 24, 4)                  \
+  X(4, 8, 4)
+
+int tma_tile(int cfg) {
+  switch (cfg) {
+#define X(id, cw, ns) \
+  case id: return TmaCfg<cw, ns>::kTile;
+    MCO_TMA_CONFIGS(X)
+#undef X
   }
+  throw Error(MCO_CONFIG, "flat_tma: unknown configuration");
+}
+
+void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st, int cfg) {
+  switch (cfg) {
+#define X(id, cw, ns) \
+  case id: launch_cfg<TmaCfg<cw, ns>>(a, k, st); return;
+    MCO_TMA_CONFIGS(X)
+#undef X
+  }
+  throw Error(MCO_CONFIG, "flat_tma: unknown configuration");
 }
 
 }  // namespace mco

@@ -5,8 +5,11 @@
 
 namespace mco {
 
-// fp32 state / params / grads, 16 B aligned buffers, at least one 2048-element tile.
-bool flat_tma_eligible(const FlatArgs& a);
-void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st);
+// cfg (consumer warps, stages): 0 = (16, 4) default, 1 = (16, 3), 2 = (16, 5),
+// 3 = (24, 4), 4 = (8, 4).  A tile is 128 elements per consumer warp.
+int tma_tile(int cfg);
+// fp32 state / params / grads, 16 B aligned buffers, at least one tile.
+bool flat_tma_eligible(const FlatArgs& a, int cfg);
+void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st, int cfg);
 
 }  // namespace mco

@@ -501,7 +501,7 @@ def synth_fill(t, seed: int, role: int, tensor: int, step: int, cols: int = 0,
 
 
 def set_flat_variant(name: str) -> None:
-    """Select the stored-state kernels' data-movement variant ("ldg" default, "tma")."""
+    """Select the stored-state kernels' data-movement variant ("tma" default, "ldg")."""
     _check(lib.mco_set_flat_variant(name.encode()))
 
 

@@ -10,11 +10,14 @@ import collections
 import csv
 import json
 import os
+import re
 import sys
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-9, "nsecond": 1e-9,
         "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3}
-KIND_OF = [("flat_step_kernel<0,", "adamw"), ("flat_step_kernel<1,", "lion"),
+KIND_OF = [("flat_tma_kernel<0,", "adamw"), ("flat_tma_kernel<1,", "lion"),
+           ("flat_tma_kernel<2,", "adan"), ("flat_tma_kernel<3,", "sophia"),
+           ("flat_step_kernel<0,", "adamw"), ("flat_step_kernel<1,", "lion"),
            ("flat_step_kernel<2,", "adan"), ("flat_step_kernel<3,", "sophia"),
            ("lomo_kernel", "lomo"), ("k1_stats", "adalomo"), ("k2_scalars", "adalomo"),
            ("k3_moments", "adalomo"), ("k4_usq", "adalomo"), ("k5_damp", "adalomo"),
@@ -52,8 +55,11 @@ def main(path, nparams):
         gbs = a["last_bytes"] / a["last_t"] / 1e9 if a["last_t"] else 0
         print(f"| `{name[:70]}` | {a['n']} | {a['t'] * 1e3:.2f} | {a['t'] / total_t:.1%} | "
               f"{bpp:.3f} | {gbs:.0f} |")
+        # flat_tma_kernel<TmaCfg<CW,NS>,KIND,MIXED> -> flat_tma_kernel<KIND,
+        key = re.sub(r"flat_tma_kernel<.*?TmaCfg<\d+,\d+>,", "flat_tma_kernel<",
+                     name.replace(" ", ""))
         for pat, kind in KIND_OF:
-            if pat in name.replace(" ", ""):
+            if pat in key:
                 traffic[kind] += bpp
     out = {k: {"dram_bytes_per_param": round(v, 4), "source": os.path.basename(path)}
            for k, v in traffic.items()}

@@ -61,6 +61,6 @@ def test_flat_variant_knob_host_side():
     with pytest.raises(optim.ConfigError, match="unknown flat-kernel variant 'nope'"):
         optim.set_flat_variant("nope")
     assert optim.flat_variant() == prev
-    optim.set_flat_variant("tma")
-    assert optim.flat_variant() == "tma"
+    optim.set_flat_variant("ldg")
+    assert optim.flat_variant() == "ldg"
     optim.set_flat_variant(prev)

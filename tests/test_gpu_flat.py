@@ -240,9 +240,9 @@ def flat_variant():
     optim.set_flat_variant(prev)
 
 
-@pytest.mark.parametrize("variant", ["tma", "pf", "w4m4", "l2pf2"])
+@pytest.mark.parametrize("variant", ["ldg", "tma", "tma_s3", "tma24", "tma8", "pf", "w4m4", "l2pf2"])
 @pytest.mark.parametrize("kind", FLAT)
-@pytest.mark.parametrize("n", [2048, 3 * 2048 + 77, (1 << 20) + 5])
+@pytest.mark.parametrize("n", [2048, 3 * 3072 + 77, (1 << 20) + 5])
 def test_kernel_variants_bit_exact(flat_variant, variant, kind, n):
     """Every data-movement variant (TMA bulk-copy pipeline included) produces the
     restatement's bits: tail elements, Adan's t == 1, Sophia refresh / non-refresh,
