@@ -31,7 +31,9 @@ constexpr int64_t kChunkElems = 1 << 16;
 struct TensorInfo {
   int64_t numel, rows, cols;
   int32_t factored, tc;  // tc: column lanes per row group (32/64/128)
-  int32_t kc, pad0;      // column blocks
+  int32_t kc;            // column blocks
+  uint32_t div_m;        // row = umulhi(e, div_m) >> div_s  (e / cols, e < 2^31; cols > 1)
+  int32_t div_s, pad0;
   int64_t nrb;           // row blocks
   int64_t elem_off;      // offset in the registry-order flat buffer
   int64_t vrow_off, vcol_off, vfull_off;  // fp64 state offsets
