@@ -382,10 +382,13 @@ __global__ void __launch_bounds__(kThreads)
 // u for a factored element: u = (s*g) / sqrt(a_i*b_j + eps)   (optim.cpp:256-259),
 // evaluated as (s*g) * rsqrt(.) -- MUFU.RSQ, <= 2 ulp -- instead of an IEEE sqrt and
 // an IEEE division: K4 reads 4 B/element and would otherwise be issue-bound.
-// K4 and K6 evaluate the identical expression, so both see the same u.
+// K4 and K6 evaluate the identical expression, so both see the same u.  a*b + eps is
+// one fused multiply-add (explicit: the library is built with --fmad=false so that the
+// stored-state kernels keep the reference's operation order; AdaLomo is compared
+// within the fp32 tolerance of the fp64 reference).
 __device__ __forceinline__ float u_fact(float g, float s, float a, float b, float eps) {
   const float gs = s * g;
-  return gs * rsqrtf(a * b + eps);
+  return gs * rsqrtf(__fmaf_rn(a, b, eps));
 }
 
 // row / col of element e of a factored tensor: e / C by multiply-high with the
@@ -450,7 +453,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
 #pragma unroll
               for (int j = 0; j < VW; ++j) {
                 const float x = u_fact(gv[u][j], sf, a, bv[j], epsf);
-                su += x * x;
+                su = __fmaf_rn(x, x, su);
               }
             } else {
 #pragma unroll
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
                   uint32_t row, col;
                   row_col((uint32_t)ej, T, C, row, col);
                   const float x = u_fact(gv[u][j], sf, fa[row], fb[col], epsf);
-                  su += x * x;
+                  su = __fmaf_rn(x, x, su);
                 }
               }
             }
