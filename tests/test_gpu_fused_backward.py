@@ -62,27 +62,80 @@ def test_lomo_clip_matches_manually_clipped_sgd():  # test_optim.cpp:259-284
 
 
 def test_fused_steps_bound_live_gradients():  # test_optim.cpp:286-316
+    """At every gradient-ready event only that parameter's gradient is alive: the fused
+    hook drops each gradient right after its update, so the live gradient elements
+    never exceed the largest tensor (the reference's RuntimeStats peak check)."""
     m = tiny_model(3)
     params = list(m.parameters())
-    live, peak = [0], [0]
+    largest = max(p.numel() for p in params)
+    peak = [0]
 
-    def track(p):
-        live[0] += p.grad.numel()
-        peak[0] = max(peak[0], live[0])
+    def track(_p):  # registered first: runs before the fused hook of the same tensor
+        peak[0] = max(peak[0], sum(q.grad.numel() for q in params if q.grad is not None))
 
     hs = [p.register_post_accumulate_grad_hook(track) for p in params]
-    fused.lomo_fused_backward_step(params, lambda: toy_loss(m), 0.01)
-    for h in hs:
-        h.remove()
-    # hooks run in registration order per parameter: the fused hook drops the
-    # gradient right after the update, so live gradients never exceed the largest
-    largest = max(p.numel() for p in params)
-    assert all(p.grad is None for p in params)
-    st = optim.AdaLomoState(OptimizerConfig.defaults_for(Kind.ADALOMO),
-                            [tuple(p.shape) for p in params])
-    fused.adalomo_fused_step(params, lambda: toy_loss(m), 0.01, st)
-    assert all(p.grad is None for p in params)
-    assert largest > 0 and peak[0] <= sum(p.numel() for p in params)
+    try:
+        fused.lomo_fused_backward_step(params, lambda: toy_loss(m), 0.01)
+        fused.lomo_fused_backward_step(params, lambda: toy_loss(m), 0.01, clip_norm=0.5)
+        assert all(p.grad is None for p in params)
+        st = optim.AdaLomoState(OptimizerConfig.defaults_for(Kind.ADALOMO),
+                                [tuple(p.shape) for p in params])
+        fused.adalomo_fused_step(params, lambda: toy_loss(m), 0.01, st)
+        assert all(p.grad is None for p in params)
+    finally:
+        for h in hs:
+            h.remove()
+    assert 0 < peak[0] <= largest < sum(p.numel() for p in params)
+
+
+class LoraLinear(torch.nn.Module):
+    """y = x W^T + (x A^T) B^T * (alpha / r): frozen base W, trainable adapters A, B."""
+
+    def __init__(self, base, r, seed):
+        super().__init__()
+        g = torch.Generator().manual_seed(seed)
+        self.base = base
+        self.base.weight.requires_grad_(False)
+        if self.base.bias is not None:
+            self.base.bias.requires_grad_(False)
+        self.A = torch.nn.Parameter(torch.randn(r, base.in_features, generator=g) * 0.1)
+        self.B = torch.nn.Parameter(torch.randn(base.out_features, r, generator=g) * 0.1)
+        self.scale = 2.0 / r
+
+    def forward(self, x):
+        return self.base(x) + (x @ self.A.t()) @ self.B.t() * self.scale
+
+
+def lora_model(seed, r=2):
+    m = tiny_model(seed).cpu()
+    m[0].weight.requires_grad_(False)
+    m[1] = LoraLinear(m[1], r, seed + 1)
+    m[3] = LoraLinear(m[3], r, seed + 2)
+    return m.cuda()
+
+
+def test_lomo_updates_adapters_only():  # test_lora.cpp:122-150
+    m = lora_model(31)
+    base = [p.detach().clone() for p in m.parameters() if not p.requires_grad]
+    trainable = [p for p in m.parameters() if p.requires_grad]
+    assert len(trainable) == 4 and base
+    before = [p.detach().clone() for p in trainable]
+    for _ in range(3):
+        fused.lomo_fused_backward_step(trainable, lambda: toy_loss(m), 0.1)
+    after = [p for p in m.parameters() if not p.requires_grad]
+    assert all(torch.equal(x, y) for x, y in zip(after, base))  # bit-identical base
+    assert sum(float((p.detach() - q).abs().sum()) for p, q in zip(trainable, before)) > 0
+
+
+def test_state_scales_with_trainable_count():  # test_lora.cpp:152-163
+    m = lora_model(31, r=2)
+    trainable = sum(p.numel() for p in m.parameters() if p.requires_grad)
+    total = sum(p.numel() for p in m.parameters())
+    cfg = OptimizerConfig.defaults_for(Kind.ADAMW)
+    assert optim.FlatOptimizer(cfg, trainable, state_dtype="f64").state_bytes_runtime() == \
+        2 * trainable * 8
+    assert optim.FlatOptimizer(cfg, trainable).state_bytes_runtime() == 2 * trainable * 4
+    assert trainable < total / 2
 
 
 def test_adalomo_fused_equals_stored_gradient_apply_all():
