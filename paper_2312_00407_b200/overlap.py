@@ -33,7 +33,7 @@ from __future__ import annotations
 from typing import Callable, Optional, Sequence
 
 from . import optim
-from .zero import ZeroPlan, _dist
+from .zero import ZeroPlan, _dist, check_agreement
 
 
 class OverlappedZeroOptimizer:
@@ -77,6 +77,9 @@ class OverlappedZeroOptimizer:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        check_agreement("OverlappedZeroOptimizer",
+                        dict(shapes=[tuple(p.shape) for p in self.params],
+                             bucket_elems=bucket_elems, kind=int(cfg.kind)), group)
         self.plan = ZeroPlan.make(P, self.world, 2)
         self.lo, self.hi = self.plan.owned_range(self.rank)
 

@@ -33,6 +33,27 @@ def _dist():
     return dist
 
 
+def check_agreement(what: str, fields: dict, group=None) -> None:
+    """Every rank must build its sharded optimizer from the same plan (total length,
+    kind, shapes ...).  One all_gather_object at construction; on a mismatch EVERY
+    rank raises ProtocolError naming the disagreeing ranks -- instead of hanging in
+    (or silently mis-pairing) the per-step collectives.  The reference aborts a
+    collective whose members disagree on the length (comm.cpp:160-167) and re-raises
+    worker failures with a [rank r] prefix (comm.cpp:337-360)."""
+    dist = _dist()
+    if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        return
+    world = dist.get_world_size(group)
+    mine = tuple(sorted((k, repr(v)) for k, v in fields.items()))
+    allf = [None] * world
+    dist.all_gather_object(allf, mine, group=group)
+    bad = [r for r in range(world) if allf[r] != allf[0]]
+    if bad:
+        diff = {r: dict(allf[r]) for r in [0] + bad}
+        raise optim.ProtocolError(
+            f"[rank {dist.get_rank(group)}] {what}: ranks {bad} disagree with rank 0: {diff}")
+
+
 class ZeroPlan:
     """parallel.hpp:22-29 / parallel.cpp:20-38 (computed by the C-ABI, mco_zero_plan)."""
 
@@ -111,6 +132,8 @@ class ZeroShardedOptimizer:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        check_agreement("ZeroShardedOptimizer", dict(total_len=total_len, stage=stage,
+                                                     kind=int(cfg.kind), mixed=mixed), group)
         self.plan = ZeroPlan.make(total_len, self.world, stage)
         self.lo, self.hi = self.plan.owned_range(self.rank)
         self.mixed = mixed
@@ -250,6 +273,8 @@ class PeerBuffers:
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.device = device
         self.total_len = total_len
+        check_agreement("PeerBuffers", dict(total_len=total_len, param_dtype=str(param_dtype),
+                                            grad_dtype=str(grad_dtype)), group)
         self._pbuf = _PeerBuffer(total_len, param_dtype or torch.float32, device)
         self._gbuf = _PeerBuffer(total_len, grad_dtype or torch.float32, device)
         self.params, self.grads = self._pbuf.tensor(), self._gbuf.tensor()
@@ -381,6 +406,9 @@ class RowShardedAdaLomo:
             rank = dist.get_rank(group) if dist.is_initialized() else 0
         self.world, self.rank = world, rank
         self.global_shapes = [tuple(s) for s in shapes]
+        if dist.is_initialized() and self.world > 1:
+            check_agreement("RowShardedAdaLomo", dict(shapes=self.global_shapes,
+                                                      kind=int(cfg.kind)), group)
         self.local_shapes, self.pieces, self._shard = [], [], []
         goff = 0
         for s in self.global_shapes:

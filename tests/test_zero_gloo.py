@@ -192,3 +192,40 @@ def test_sharded_lomo_clip_uses_global_norm(world2):
         lp, s, (lo, hi) = world2[rank]["lomo"]
         assert s == pytest.approx(total, rel=1e-13)  # every rank sees the global sum
         np.testing.assert_allclose(lp, pf[lo:hi] - (0.1 * scale) * g[lo:hi], rtol=1e-13)
+
+
+def _mismatch_worker(rank, world, port, out_q):
+    import sys
+
+    for p in (ROOT, os.path.join(ROOT, "oracle")):
+        sys.path.insert(0, p)
+    from paper_2312_00407_b200 import optim, zero
+    from paper_2312_00407_b200.optim import OptimizerConfig
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = OptimizerConfig.defaults_for(0)
+        try:  # rank 1 was handed a different flat length: every rank must fail fast
+            zero.ZeroShardedOptimizer(cfg, 1000 + rank, local_step=lambda *a: None)
+            out_q.put((rank, "no error"))
+        except optim.ProtocolError as e:
+            out_q.put((rank, str(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_plan_mismatch_fails_fast_on_every_rank():
+    """comm.cpp:160-167 length-mismatch abort + comm.cpp:337-360 rank attribution."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mismatch_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert res[r].startswith(f"[rank {r}] ZeroShardedOptimizer: ranks [1] disagree"), res[r]
+        assert "1000" in res[r] and "1001" in res[r]
