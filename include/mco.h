@@ -230,6 +230,30 @@ mco_status mco_adalomo_buffer(mco_adalomo* h, int tensor_index, int which, void*
 mco_status mco_zero_plan(uint64_t total_len, int dp_size, int stage, uint64_t* part_sizes,
                          uint64_t* offsets);
 
+/* ---- native sharder over NCCL (parallel.cpp:656-666, comm.cpp:193-246) -------
+ * NCCL is resolved at run time: the libnccl.so.2 already loaded in the process
+ * (e.g. torch's) is reused, else $MCO_NCCL_LIB, else the system libnccl.so.2;
+ * failure -> MCO_IO.  NCCL errors -> MCO_PROTOCOL with NCCL's message. */
+typedef struct mco_comm mco_comm;
+/* 128-byte ncclUniqueId, created on one rank and shipped to the others by the caller. */
+mco_status mco_comm_unique_id(void* id_out_128);
+mco_status mco_comm_create(const void* id_128, int nranks, int rank, int device,
+                           mco_comm** out);
+mco_status mco_comm_destroy(mco_comm* c);
+/* ncclCommGetAsyncError: MCO_PROTOCOL if the communicator has failed. */
+mco_status mco_comm_check(mco_comm* c);
+/* In-place SUM all-reduce (LOMO global sum of squares, AdaLomo statistic payloads). */
+mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n, void* stream);
+/* Stage-2 ZeRO step of ParallelWorker::train_step, stream-ordered:
+ * reduce-scatter(SUM) of flat_grads over ZeroPlan(total_len, nranks) parts ->
+ * FlatOptimizer step of this rank's part of flat_params (h owns exactly that part:
+ * MCO_CONTRACT otherwise) -> all-gather of flat_params in place.  Equal parts use
+ * ncclReduceScatter / ncclAllGather; P mod N != 0 uses per-part ncclReduce /
+ * ncclBroadcast (the reference's uneven ownership, parallel.cpp:25-32). */
+mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param_dtype,
+                          const void* flat_grads, int grad_dtype, uint64_t total_len,
+                          double lr, void* stream);
+
 /* ---- synthetic inputs ------------------------------------------ */
 /* Counter-based, stateless generator; values exact in fp32 (bf16 grid for BF16). */
 mco_status mco_synth_fill(void* dst, int dtype, uint64_t n, uint64_t seed, uint32_t role,

@@ -22,6 +22,7 @@
 // Like the reference, instances are not thread-safe; use one per device/thread.
 #pragma once
 
+#include <array>
 #include <cstdint>
 #include <cstring>
 #include <optional>
@@ -347,6 +348,41 @@ struct ZeroPlan {  // parallel.hpp:22-29
     return {offsets[static_cast<size_t>(dp_index)], offsets[static_cast<size_t>(dp_index) + 1]};
   }
 };
+
+// The sharder's NCCL communicator (libmco's mco_comm; the CommHub group of
+// comm.hpp:77-135).  NCCL is loaded at run time by libmco (no link dependency).
+class NcclComm {
+ public:
+  using Id = std::array<char, 128>;
+  static Id unique_id() {  // on one rank; ship the bytes to the others
+    Id id{};
+    mco_throw(mco_comm_unique_id(id.data()));
+    return id;
+  }
+  NcclComm(const Id& id, int nranks, int rank, int device = 0) {
+    mco_throw(mco_comm_create(id.data(), nranks, rank, device, &h_));
+  }
+  ~NcclComm() {
+    if (h_) mco_comm_destroy(h_);
+  }
+  NcclComm(const NcclComm&) = delete;
+  NcclComm& operator=(const NcclComm&) = delete;
+  mco_comm* handle() const { return h_; }
+  void check() const { mco_throw(mco_comm_check(h_)); }
+
+ private:
+  mco_comm* h_ = nullptr;
+};
+
+// Stage-2 ZeRO step of ParallelWorker::train_step (parallel.cpp:656-666) on device
+// flat buffers: reduce-scatter(SUM) -> step of the owned ZeroPlan part -> all-gather.
+// `opt` must own exactly this rank's part (ZeroPlan::make(total_len, nranks)).
+inline void shard_step(optim::FlatOptimizer& opt, const NcclComm& comm, float* flat_params,
+                       const float* flat_grads, size_t total_len, double lr,
+                       void* stream = nullptr) {
+  mco_throw(mco_shard_step(opt.handle(), comm.handle(), flat_params, MCO_F32, flat_grads,
+                           MCO_F32, total_len, lr, stream));
+}
 }  // namespace parallel
 
 }  // namespace minicollie

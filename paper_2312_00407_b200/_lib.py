@@ -104,6 +104,12 @@ _SIGS = {
     "mco_sync": (_i, [_p]),
     "mco_device_count": (_i, [C.POINTER(_i)]),
     "mco_set_flat_variant": (_i, [C.c_char_p]),
+    "mco_comm_unique_id": (_i, [_p]),
+    "mco_comm_create": (_i, [_p, _i, _i, _i, C.POINTER(_p)]),
+    "mco_comm_destroy": (_i, [_p]),
+    "mco_comm_check": (_i, [_p]),
+    "mco_comm_allreduce_sum": (_i, [_p, _p, _i, _u64, _p]),
+    "mco_shard_step": (_i, [_p, _p, _p, _i, _p, _i, _u64, _d, _p]),
     "mco_flat_variant": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():

@@ -27,6 +27,7 @@ thread_local std::string g_err;
 }  // namespace
 
 void note_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void set_last_error(const std::string& m) { g_err = m; }
 
 const DeviceInfo& device_info(int device) {
   static std::mutex mu;

@@ -1,0 +1,282 @@
+// Native ZeRO sharder over NCCL (SURVEY 8(b) "mco_shard_step", 8(e)): the stage-2
+// branch of ParallelWorker::train_step (parallel.cpp:656-666) as one C-ABI call,
+//
+//   owned_grads = reduce_scatter(flat_grads, SUM, ZeroPlan parts)   parallel.cpp:657-658
+//   FlatOptimizer::step(params[owned], owned_grads, lr)             parallel.cpp:660
+//   params      = all_gather(params[owned])                         parallel.cpp:661-663
+//
+// stream-ordered on the caller's stream, so a C / C++ host (the reference's own
+// parallel engine) gets the sharded step without torch.  Equal ZeroPlan parts use
+// ncclReduceScatter / ncclAllGather (in place); unequal parts (P mod N != 0: the first
+// P mod N ranks own one more element, parallel.cpp:25-32) use one ncclReduce and one
+// ncclBroadcast per part inside a group, which keeps the reference's ownership.
+//
+// NCCL is resolved at run time (dlopen): the libnccl.so.2 already mapped into the
+// process (torch's build) is reused, never a second copy; otherwise MCO_NCCL_LIB, then
+// the system libnccl.so.2.  libmco.so has no link-time NCCL dependency.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "mco.h"
+
+namespace mco {
+void set_last_error(const std::string& m);  // abi.cpp
+
+namespace {
+
+struct NcclApi {
+  void* so = nullptr;
+  std::string from;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*comm_get_async_error)(ncclComm_t, ncclResult_t*) = nullptr;
+  const char* (*get_error_string)(ncclResult_t) = nullptr;
+  ncclResult_t (*reduce_scatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                 ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int,
+                         ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                             ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*group_start)() = nullptr;
+  ncclResult_t (*group_end)() = nullptr;
+};
+
+template <class F>
+void sym(void* so, const char* name, F& out) {
+  out = reinterpret_cast<F>(dlsym(so, name));
+  if (!out) throw Error(MCO_IO, std::string("NCCL: missing symbol ") + name);
+}
+
+const NcclApi& nccl() {
+  static std::mutex mu;
+  static NcclApi api;
+  std::lock_guard<std::mutex> lock(mu);
+  if (api.so) return api;
+  void* so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // the process's own NCCL
+  std::string from = "already loaded";
+  if (!so) {
+    if (const char* env = getenv("MCO_NCCL_LIB")) {
+      so = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+      from = env;
+    }
+  }
+  if (!so) {
+    so = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    from = "libnccl.so.2";
+  }
+  if (!so) throw Error(MCO_IO, std::string("NCCL: cannot load libnccl.so.2: ") + dlerror());
+  NcclApi a;
+  a.so = so;
+  a.from = from;
+  sym(so, "ncclGetUniqueId", a.get_unique_id);
+  sym(so, "ncclCommInitRank", a.comm_init_rank);
+  sym(so, "ncclCommDestroy", a.comm_destroy);
+  sym(so, "ncclCommGetAsyncError", a.comm_get_async_error);
+  sym(so, "ncclGetErrorString", a.get_error_string);
+  sym(so, "ncclReduceScatter", a.reduce_scatter);
+  sym(so, "ncclAllGather", a.all_gather);
+  sym(so, "ncclReduce", a.reduce);
+  sym(so, "ncclBroadcast", a.broadcast);
+  sym(so, "ncclAllReduce", a.all_reduce);
+  sym(so, "ncclGroupStart", a.group_start);
+  sym(so, "ncclGroupEnd", a.group_end);
+  api = a;
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw Error(MCO_PROTOCOL, std::string(what) + ": " + nccl().get_error_string(r));
+}
+#define MCO_NCCL_CHECK(x) nccl_check((x), #x)
+
+ncclDataType_t nccl_type(int dt) {
+  switch (dt) {
+    case MCO_F32: return ncclFloat32;
+    case MCO_BF16: return ncclBfloat16;
+    case MCO_F64: return ncclFloat64;
+  }
+  throw Error(MCO_CONTRACT, "NCCL: unsupported dtype " + std::to_string(dt));
+}
+
+size_t dt_size(int dt) { return dt == MCO_F64 ? 8 : dt == MCO_BF16 ? 2 : 4; }
+
+template <class F>
+mco_status guarded(F&& f) {
+  try {
+    f();
+    return MCO_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.status;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return MCO_CUDA;
+  }
+}
+
+struct DevSwitch {
+  int prev = -1;
+  explicit DevSwitch(int d) {
+    MCO_CUDA_CHECK(cudaGetDevice(&prev));
+    if (prev != d) MCO_CUDA_CHECK(cudaSetDevice(d));
+  }
+  ~DevSwitch() {
+    int cur = -1;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+}  // namespace mco
+
+using namespace mco;
+
+struct mco_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+  void* scratch = nullptr;  // reduced owned gradient (ZeroPlan part of this rank)
+  size_t scratch_bytes = 0;
+  ~mco_comm() {
+    if (scratch) cudaFree(scratch);
+    if (comm) nccl().comm_destroy(comm);
+  }
+};
+
+extern "C" {
+
+mco_status mco_comm_unique_id(void* id_out) {
+  return guarded([&] {
+    if (!id_out) throw Error(MCO_CONTRACT, "comm unique id: null output");
+    ncclUniqueId id;
+    MCO_NCCL_CHECK(nccl().get_unique_id(&id));
+    std::memcpy(id_out, &id, sizeof(id));
+  });
+}
+
+mco_status mco_comm_create(const void* id, int nranks, int rank, int device, mco_comm** out) {
+  return guarded([&] {
+    if (!id || !out) throw Error(MCO_CONTRACT, "comm create: null argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      throw Error(MCO_CONFIG, "comm create: rank " + std::to_string(rank) + " of " +
+                                  std::to_string(nranks));
+    DevSwitch ds(device);
+    ncclUniqueId uid;
+    std::memcpy(&uid, id, sizeof(uid));
+    auto* c = new mco_comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    const ncclResult_t r = nccl().comm_init_rank(&c->comm, nranks, uid, rank);
+    if (r != ncclSuccess) {
+      c->comm = nullptr;
+      delete c;
+      nccl_check(r, "ncclCommInitRank");
+    }
+    *out = c;
+  });
+}
+
+mco_status mco_comm_destroy(mco_comm* c) {
+  return guarded([&] {
+    if (!c) return;
+    DevSwitch ds(c->device);
+    delete c;
+  });
+}
+
+mco_status mco_comm_check(mco_comm* c) {
+  return guarded([&] {
+    ncclResult_t r = ncclSuccess;
+    MCO_NCCL_CHECK(nccl().comm_get_async_error(c->comm, &r));
+    nccl_check(r, "NCCL asynchronous error");
+  });
+}
+
+mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n, void* stream) {
+  return guarded([&] {
+    DevSwitch ds(c->device);
+    MCO_NCCL_CHECK(nccl().all_reduce(buf, buf, n, nccl_type(dtype), ncclSum, c->comm,
+                                     (cudaStream_t)stream));
+  });
+}
+
+mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param_dtype,
+                          const void* flat_grads, int grad_dtype, uint64_t total_len, double lr,
+                          void* stream) {
+  // argument checks come first, before any collective (every rank fails the same way)
+  return guarded([&] {
+    if (!h || !c || !flat_params || !flat_grads)
+      throw Error(MCO_CONTRACT, "shard step: null argument");
+    const int N = c->nranks, me = c->rank;
+    std::vector<uint64_t> parts(N), offs(N + 1);
+    const mco_status zs = mco_zero_plan(total_len, N, 2, parts.data(), offs.data());
+    if (zs != MCO_OK) throw Error(zs, "shard step: zero plan");
+    uint64_t nbuf = 0;
+    int idx = 0;
+    mco_status bs = mco_flat_num_buffers(h, &idx);
+    if (bs != MCO_OK) throw Error(bs, "shard step: handle");
+    // the handle's owned length must be this rank's ZeroPlan part (parallel.cpp:330)
+    const char* nm = nullptr;
+    void* ptr = nullptr;
+    int sdt = 0;
+    bs = mco_flat_buffer(h, 0, &nm, &ptr, &nbuf, &sdt);
+    if (bs != MCO_OK) throw Error(bs, "shard step: handle");
+    if (nbuf != parts[me])
+      throw Error(MCO_CONTRACT, "shard step: optimizer owns " + std::to_string(nbuf) +
+                                    " elements but ZeroPlan gives rank " + std::to_string(me) +
+                                    " " + std::to_string(parts[me]));
+    const ncclDataType_t gt = nccl_type(grad_dtype), pt = nccl_type(param_dtype);
+    const size_t gs = dt_size(grad_dtype), ps = dt_size(param_dtype);
+    DevSwitch ds(c->device);
+    const size_t need = std::max<size_t>(parts[me] * gs, 256);
+    if (c->scratch_bytes < need) {
+      if (c->scratch) MCO_CUDA_CHECK(cudaFree(c->scratch));
+      c->scratch = nullptr;
+      MCO_CUDA_CHECK(cudaMalloc(&c->scratch, need));
+      c->scratch_bytes = need;
+    }
+    auto s = (cudaStream_t)stream;
+    const char* algo = getenv("MCO_SHARD_ALGO");  // "p2p": force the per-part path (tests)
+    const bool even = total_len % (uint64_t)N == 0 && !(algo && std::string(algo) == "p2p");
+    const auto& api = nccl();
+    if (even) {
+      MCO_NCCL_CHECK(api.reduce_scatter(flat_grads, c->scratch, parts[me], gt, ncclSum, c->comm, s));
+    } else {
+      MCO_NCCL_CHECK(api.group_start());
+      for (int r = 0; r < N; ++r)
+        MCO_NCCL_CHECK(api.reduce((const char*)flat_grads + offs[r] * gs, c->scratch, parts[r], gt,
+                                  ncclSum, r, c->comm, s));
+      MCO_NCCL_CHECK(api.group_end());
+    }
+    char* mine = (char*)flat_params + offs[me] * ps;
+    const mco_status st = mco_flat_step(h, mine, param_dtype, parts[me], c->scratch, grad_dtype, parts[me], lr,
+                       stream);
+    if (st != MCO_OK) throw Error(st, mco_last_error());
+    if (even) {
+      MCO_NCCL_CHECK(api.all_gather(mine, flat_params, parts[me], pt, c->comm, s));
+    } else {
+      MCO_NCCL_CHECK(api.group_start());
+      for (int r = 0; r < N; ++r) {
+        char* part = (char*)flat_params + offs[r] * ps;
+        MCO_NCCL_CHECK(api.broadcast(part, part, parts[r], pt, r, c->comm, s));
+      }
+      MCO_NCCL_CHECK(api.group_end());
+    }
+  });
+}
+
+}  // extern "C"

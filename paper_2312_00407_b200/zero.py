@@ -480,3 +480,80 @@ def reshard_state(states: list, total_len: int, new_world: int) -> list:
         out.append({"steps": states[0]["steps"],
                     "buffers": {n: full[n][lo:hi].clone() for n in names}})
     return out
+
+
+class NcclComm:
+    """The C-ABI's own NCCL communicator (mco_comm): ncclUniqueId from rank 0, shipped
+    over the torch.distributed group (any backend), ncclCommInitRank on every rank.
+    Lets the sharded step run as one stream-ordered C call (mco_shard_step)."""
+
+    def __init__(self, group=None, device: int = 0):
+        import ctypes as C
+
+        from ._lib import lib
+
+        dist = _dist()
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            optim._check(lib.mco_comm_unique_id(uid))
+        if self.world > 1:
+            box = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(box, src=src, group=group)
+            C.memmove(uid, box[0], 128)
+        h = C.c_void_p()
+        optim._check(lib.mco_comm_create(uid, self.world, self.rank, device, C.byref(h)))
+        self._h = h
+
+    def allreduce_sum(self, t, stream=None) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_comm_allreduce_sum(self._h, t.data_ptr(), optim._dtype_code(t),
+                                                t.numel(), optim._stream(stream)))
+
+    def check(self) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_comm_check(self._h))
+
+    def __del__(self):
+        from ._lib import lib
+
+        h = getattr(self, "_h", None)
+        if h:
+            lib.mco_comm_destroy(h)
+            self._h = None
+
+
+class NativeZeroOptimizer:
+    """Stage-2 ZeRO step as one C-ABI call (mco_shard_step): NCCL reduce-scatter of the
+    flat gradient -> the sm_100a FlatOptimizer on the ZeroPlan-owned slice -> NCCL
+    all-gather of the flat parameters, stream-ordered, no torch collectives.  Same
+    ownership and state as ZeroShardedOptimizer (parallel.cpp:656-666)."""
+
+    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, comm: NcclComm,
+                 device: int = 0):
+        self.comm = comm
+        self.total_len = int(total_len)
+        self.plan = ZeroPlan.make(self.total_len, comm.world, 2)
+        self.lo, self.hi = self.plan.owned_range(comm.rank)
+        self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=device)
+
+    def step(self, flat_params, flat_grads, lr: float, stream=None) -> None:
+        from ._lib import lib
+
+        optim._dev(flat_params, "shard step params")
+        optim._dev(flat_grads, "shard step grads")
+        if flat_params.numel() != self.total_len or flat_grads.numel() != self.total_len:
+            raise optim.ContractError(
+                f"shard step: flat buffers of {flat_params.numel()} / {flat_grads.numel()} "
+                f"elements for a plan of {self.total_len}")
+        optim._check(lib.mco_shard_step(self.opt._h, self.comm._h, flat_params.data_ptr(),
+                                         optim._dtype_code(flat_params), flat_grads.data_ptr(),
+                                         optim._dtype_code(flat_grads), self.total_len,
+                                         float(lr), optim._stream(stream)))
+
+    def owned_range(self) -> tuple[int, int]:
+        return self.lo, self.hi

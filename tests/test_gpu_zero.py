@@ -282,3 +282,52 @@ def test_peer_sharded_two_processes_ipc_one_gpu(kind):
         else:  # the clip norm is summed in a different order than the oracle's
             np.testing.assert_allclose(res[r], want, rtol=0, atol=1e-7)
     assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("algo", ["even", "p2p"])
+@pytest.mark.parametrize("kind", [Kind.ADAMW, Kind.ADAN])
+def test_native_nccl_shard_step_world1(monkeypatch, algo, kind):
+    """mco_shard_step through the library's own NCCL communicator (one rank: the
+    collectives are identities) == the plain FlatOptimizer step, bit for bit, on both
+    the reduce-scatter / all-gather path and the per-part reduce / broadcast path."""
+    if algo == "p2p":
+        monkeypatch.setenv("MCO_SHARD_ALGO", "p2p")
+    n = 100003
+    cfg = OptimizerConfig.defaults_for(kind)
+    cfg.weight_decay = 0.01
+    comm = zero.NcclComm()
+    nz = zero.NativeZeroOptimizer(cfg, n, comm)
+    ref = optim.FlatOptimizer(cfg, n)
+    p0 = O.synth(n, 5, 0, 0, 0, 0, -6, 0, False)
+    a, b = torch.from_numpy(p0.copy()).cuda(), torch.from_numpy(p0.copy()).cuda()
+    for t in (1, 2, 3):
+        g = torch.from_numpy(O.synth(n, 5, 1, 0, t, 0, -7, 10, False)).cuda()
+        g_keep = g.clone()
+        nz.step(a, g, 1e-3)
+        ref.step(b, g_keep, 1e-3)
+        torch.cuda.synchronize()
+        assert torch.equal(g, g_keep)  # const gradients: reduced into the comm's scratch
+    assert torch.equal(a, b)
+    for (n1, x), (n2, y) in zip(nz.opt.buffers(), ref.buffers()):
+        assert n1 == n2 and torch.equal(x, y)
+    comm.check()
+    t = torch.arange(10, dtype=torch.float64, device="cuda")
+    comm.allreduce_sum(t)
+    torch.cuda.synchronize()
+    assert torch.equal(t, torch.arange(10, dtype=torch.float64, device="cuda"))
+
+
+def test_native_shard_step_contract_errors():
+    comm = zero.NcclComm()
+    nz = zero.NativeZeroOptimizer(OptimizerConfig.defaults_for(Kind.ADAMW), 1000, comm)
+    with pytest.raises(optim.ContractError):
+        nz.step(torch.zeros(999, device="cuda"), torch.zeros(999, device="cuda"), 1e-3)
+    from paper_2312_00407_b200 import _lib
+    import ctypes as C
+
+    bad = optim.FlatOptimizer(OptimizerConfig.defaults_for(Kind.ADAMW), 10)
+    p = torch.zeros(1000, device="cuda")
+    st = _lib.lib.mco_shard_step(bad._h, comm._h, p.data_ptr(), 0, p.data_ptr(), 0, 1000,
+                                 C.c_double(1e-3), None)
+    assert st == _lib.MCO_CONTRACT
+    assert "ZeroPlan gives rank 0 1000" in _lib.lib.mco_last_error().decode()
