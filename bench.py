@@ -343,7 +343,52 @@ def bench_ours(args, rank, world, local_rank):
         gc.collect()
         torch.cuda.empty_cache()
         out["collectives"] = bench_peer_step(args, P, rank, world, dev)
+        gc.collect()
+        torch.cuda.empty_cache()
+        import torch.distributed as dist
+
+        if dist.get_backend() == "nccl":  # NCCL refuses two ranks on one device (gloo tests)
+            try:
+                out["collectives"]["nccl_baseline"] = bench_nccl_step(args, P, rank, world, dev)
+            except Exception as ex:  # report, never fake
+                out["collectives"]["nccl_baseline"] = {"unavailable": repr(ex)[:200]}
     return out
+
+
+def bench_nccl_step(args, P, rank, world, dev):
+    """The same AdamW ZeRO step with NCCL collectives around the kernel
+    (mco_shard_step: ncclReduceScatter -> owned-slice step -> ncclAllGather), the
+    library-collective baseline the fused peer-memory kernel is measured against."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_00407_b200 import optim, registry, zero
+
+    cfg = make_cfg("adamw")
+    comm = zero.NcclComm(device=dev.index)
+    nz = zero.NativeZeroOptimizer(cfg, P, comm, device=dev.index)
+    p = torch.empty(P, device=dev)
+    g = torch.empty(P, device=dev)
+    optim.synth_fill(p, registry.SEED, 0, 0xFFFC, 0, 0, -6)
+    optim.synth_fill(g, registry.SEED, 1, 0xFFFC, 1, 0, -7, 10)
+    for _ in range(args.warmup):
+        nz.step(p, g, cfg.lr)
+    torch.cuda.synchronize()
+    dist.barrier()
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        nz.step(p, g, cfg.lr)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    comm.check()
+    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = ms.item()
+    log(f"[rank {rank}] NCCL RS + adamw + AG (mco_shard_step): {ms:.2f} ms/step")
+    return {"path": "mco_shard_step: ncclReduceScatter + flat_tma_kernel + ncclAllGather",
+            "ms": ms, "params_per_s": P / (ms * 1e-3)}
 
 
 def bench_peer_step(args, P, rank, world, dev):
