@@ -122,6 +122,17 @@ def cpu_sample_shapes():
     return LLAMA_7B.shapes()[1:10]  # one decoder layer: 9 tensors, 202,383,360 params
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def host_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -587,7 +598,8 @@ def main():
                 "ms_per_step": sec_step * 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads,
-                                 "kind": "reference", "sample": sample},
+                                 "kind": "reference", "cpu_model": cpu_model(),
+                                 "sample": sample},
                 "e2e": {"value": value, "unit": "params/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0},
                 "per_optimizer": per}
@@ -617,7 +629,7 @@ def main():
         try:
             v, threads, sample, per, _ = run_cpu_reference(1, args.cpu_steps)
             cpu = {"value": v, "unit": "params/s", "cores": threads, "kind": "reference",
-                   "sample": sample, "per_optimizer": per}
+                   "cpu_model": cpu_model(), "sample": sample, "per_optimizer": per}
             cpu["single_thread"] = run_cpu_single_thread()
         except Exception as ex:
             log(f"[cpu_baseline] failed: {ex!r}")
