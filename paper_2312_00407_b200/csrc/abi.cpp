@@ -188,13 +188,17 @@ void* sumsq_ws(cudaStream_t st) {
   return p;
 }
 
-// Host-span staging: [H2D a, H2D b] -> kernel -> D2H a, chunk by chunk on two
-// streams, so both PCIe directions and the kernels overlap.  One staging set
+// Host-span staging: [H2D a, H2D b] -> kernel -> D2H a, chunk by chunk on
+// kHostStages streams, so both PCIe directions and the kernels overlap.  One staging set
 // per device (host-span calls are synchronous; the mutex serialises them).
+#ifndef MCO_HOST_STAGES
+#define MCO_HOST_STAGES 3
+#endif
+constexpr int kHostStages = MCO_HOST_STAGES;  // chunk k+S reuses chunk k's buffers
 struct HostStage {
   std::mutex mu;
-  cudaStream_t st[2] = {nullptr, nullptr};
-  void* buf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  cudaStream_t st[kHostStages] = {};
+  void* buf[kHostStages][2] = {};
   uint64_t chunk_bytes = 0;
 };
 
@@ -206,7 +210,7 @@ HostStage& host_stage(int dev) {
   if (!s) {
     s = new HostStage;
     s->chunk_bytes = 8ull << 24;  // 16 Mi elements of <= 8 bytes
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kHostStages; ++i) {
       MCO_CUDA_CHECK(cudaStreamCreateWithFlags(&s->st[i], cudaStreamNonBlocking));
       MCO_CUDA_CHECK(cudaMalloc(&s->buf[i][0], s->chunk_bytes));
       MCO_CUDA_CHECK(cudaMalloc(&s->buf[i][1], s->chunk_bytes));
@@ -223,7 +227,7 @@ void host_pipeline(int dev, void* a, size_t as, const void* b, size_t bs, uint64
   std::lock_guard<std::mutex> lock(hs.mu);
   const uint64_t C = hs.chunk_bytes / 8;
   int k = 0;
-  for (uint64_t off = 0; off < n; off += C, k ^= 1) {
+  for (uint64_t off = 0; off < n; off += C, k = (k + 1) % kHostStages) {
     const uint64_t m = std::min(C, n - off);
     cudaStream_t st = hs.st[k];
     MCO_CUDA_CHECK(cudaMemcpyAsync(hs.buf[k][0], (const char*)a + off * as, m * as,
@@ -236,8 +240,7 @@ void host_pipeline(int dev, void* a, size_t as, const void* b, size_t bs, uint64
       MCO_CUDA_CHECK(cudaMemcpyAsync((char*)a + off * as, hs.buf[k][0], m * as,
                                      cudaMemcpyDeviceToHost, st));
   }
-  MCO_CUDA_CHECK(cudaStreamSynchronize(hs.st[0]));
-  MCO_CUDA_CHECK(cudaStreamSynchronize(hs.st[1]));
+  for (int i = 0; i < kHostStages; ++i) MCO_CUDA_CHECK(cudaStreamSynchronize(hs.st[i]));
 }
 
 }  // namespace
