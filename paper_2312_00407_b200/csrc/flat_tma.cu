@@ -30,12 +30,16 @@ using namespace upd;
 // memory).  Default 16 warps (4 per scheduler: at 8 warps ncu showed the consumers'
 // fp32 div / sqrt chains stalled on 'wait' + 'branch_resolving') and 4 stages
 // (measured: fewer starve the loads, more lose bandwidth for AdamW / Sophia).
-template <int CW_, int NS_>
+// EPT: elements per consumer thread per stream and stage (4: float4, 2: float2);
+// HINT: bulk copies carry an L2 evict-first cache policy (streams are touched once).
+template <int CW_, int NS_, int EPT_ = 4, bool HINT_ = false>
 struct TmaCfg {
   static constexpr int CW = CW_;
   static constexpr int kConsumers = CW * 32;
-  static constexpr int kTile = CW * 32 * 4;  // elements per stream per stage
+  static constexpr int kEPT = EPT_;
+  static constexpr int kTile = CW * 32 * EPT_;  // elements per stream per stage
   static constexpr int kStages = NS_;
+  static constexpr bool kHint = HINT_;
 };
 constexpr int kSmemMax = 220 * 1024;
 
@@ -78,18 +82,38 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-          "r"(sa(dst)),
-      "l"(src), "r"(bytes), "r"(sa(bar))
-      : "memory");
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-               "r"(sa(src)), "r"(bytes)
-               : "memory");
+template <bool HINT>
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  if constexpr (HINT)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1], %2, [%3], %4;" ::"r"(sa(dst)),
+        "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];" ::"r"(sa(dst)),
+        "l"(src), "r"(bytes), "r"(sa(bar))
+        : "memory");
+}
+template <bool HINT>
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t pol) {
+  if constexpr (HINT)
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                 ::"l"(dst), "r"(sa(src)), "r"(bytes), "l"(pol)
+                 : "memory");
+  else
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(sa(src)), "r"(bytes)
+                 : "memory");
 }
 __device__ __forceinline__ void bulk_commit() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -104,13 +128,23 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-// consecutive threads read consecutive 16 B: conflict-free LDS.128 / STS.128
-__device__ __forceinline__ void lds4(const float* s, float (&r)[4]) {
-  const float4 x = *reinterpret_cast<const float4*>(s);
-  r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w;
+// consecutive threads read consecutive 16 B (8 B): conflict-free LDS.128 / LDS.64
+template <int E>
+__device__ __forceinline__ void lds(const float* s, float (&r)[E]) {
+  if constexpr (E == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(s);
+    r[0] = x.x, r[1] = x.y, r[2] = x.z, r[3] = x.w;
+  } else {
+    const float2 x = *reinterpret_cast<const float2*>(s);
+    r[0] = x.x, r[1] = x.y;
+  }
 }
-__device__ __forceinline__ void sts4(float* s, const float (&r)[4]) {
-  *reinterpret_cast<float4*>(s) = make_float4(r[0], r[1], r[2], r[3]);
+template <int E>
+__device__ __forceinline__ void sts(float* s, const float (&r)[E]) {
+  if constexpr (E == 4)
+    *reinterpret_cast<float4*>(s) = make_float4(r[0], r[1], r[2], r[3]);
+  else
+    *reinterpret_cast<float2*>(s) = make_float2(r[0], r[1]);
 }
 
 template <class C, int KIND, bool MIXED>
@@ -142,6 +176,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
 
   if (warp == kConsumerWarps) {  // ---------------- producer ----------------
     if (lane == 0) {
+      const uint64_t pol = C::kHint ? evict_first_policy() : 0;
       const bool skip_gp = (KIND == K_ADAN) && k.first;  // g_prev unused at t == 1
       const int nload = skip_gp ? NIN - 1 : NIN;
       auto issue = [&](uint64_t i) {
@@ -149,7 +184,8 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
         mbar_expect_tx(&full[s], (uint32_t)(nload * kTile * 4));
         for (int j = 0; j < nload; ++j)
-          bulk_g2s(buf + ((size_t)s * NIN + j) * kTile, src[j] + e, kTile * 4, &full[s]);
+          bulk_g2s<C::kHint>(buf + ((size_t)s * NIN + j) * kTile, src[j] + e, kTile * 4, &full[s],
+                              pol);
       };
       for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
       for (uint64_t i = 0; i < mine; ++i) {
@@ -157,17 +193,17 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
         float* st = buf + (size_t)s * NIN * kTile;
-        bulk_s2g(p + e, st, kTile * 4);
-        bulk_s2g(s0 + e, st + 2 * kTile, kTile * 4);
-        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) bulk_s2g(s1 + e, st + 3 * kTile, kTile * 4);
+        bulk_s2g<C::kHint>(p + e, st, kTile * 4, pol);
+        bulk_s2g<C::kHint>(s0 + e, st + 2 * kTile, kTile * 4, pol);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) bulk_s2g<C::kHint>(s1 + e, st + 3 * kTile, kTile * 4, pol);
         if constexpr (KIND == K_SOPHIA) {
-          if (k.refresh) bulk_s2g(s1 + e, st + 3 * kTile, kTile * 4);
+          if (k.refresh) bulk_s2g<C::kHint>(s1 + e, st + 3 * kTile, kTile * 4, pol);
         }
         if constexpr (KIND == K_ADAN) {
-          bulk_s2g(s2 + e, st + 4 * kTile, kTile * 4);
-          bulk_s2g(s3 + e, st + 5 * kTile, kTile * 4);
+          bulk_s2g<C::kHint>(s2 + e, st + 4 * kTile, kTile * 4, pol);
+          bulk_s2g<C::kHint>(s3 + e, st + 5 * kTile, kTile * 4, pol);
         }
-        if constexpr (MIXED) bulk_s2g(pout + e, obuf + (size_t)s * kTile, kTile * 2);
+        if constexpr (MIXED) bulk_s2g<C::kHint>(pout + e, obuf + (size_t)s * kTile, kTile * 2, pol);
         bulk_commit();
         // refill the PREVIOUS tile's stage: its store group (all but the one just
         // committed) has had a tile-time to drain out of smem, so the wait is short and
@@ -180,22 +216,23 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
       bulk_wait_all();
     }
   } else {  // ---------------- consumers ----------------
-    const int c4 = threadIdx.x * 4;
+    constexpr int E = C::kEPT;
+    const int c0 = threadIdx.x * E;
     for (uint64_t i = 0; i < mine; ++i) {
       const int s = (int)(i % NS);
       mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
-      float* st = buf + (size_t)s * NIN * kTile + c4;
-      float pv[4], gv[4], a[4], b[4], c[4], d[4];
-      lds4(st, pv);
-      lds4(st + kTile, gv);
-      lds4(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) lds4(st + 3 * kTile, b);
+      float* st = buf + (size_t)s * NIN * kTile + c0;
+      float pv[E], gv[E], a[E], b[E], c[E], d[E];
+      lds<E>(st, pv);
+      lds<E>(st + kTile, gv);
+      lds<E>(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) lds<E>(st + 3 * kTile, b);
       if constexpr (KIND == K_ADAN) {
-        lds4(st + 4 * kTile, c);
-        if (!k.first) lds4(st + 5 * kTile, d);
+        lds<E>(st + 4 * kTile, c);
+        if (!k.first) lds<E>(st + 5 * kTile, d);
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+      for (int j = 0; j < E; ++j) {
         if constexpr (KIND == K_LION) b[j] = 0.f;
         if constexpr (KIND != K_ADAN) c[j] = d[j] = 0.f;
         if constexpr (KIND == K_ADAN) {
@@ -203,17 +240,17 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         }
         update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
       }
-      sts4(st, pv);
-      sts4(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) sts4(st + 3 * kTile, b);
+      sts<E>(st, pv);
+      sts<E>(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) sts<E>(st + 3 * kTile, b);
       if constexpr (KIND == K_ADAN) {
-        sts4(st + 4 * kTile, c);
-        sts4(st + 5 * kTile, d);
+        sts<E>(st + 4 * kTile, c);
+        sts<E>(st + 5 * kTile, d);
       }
       if constexpr (MIXED) {
-        uint32_t* o = reinterpret_cast<uint32_t*>(obuf + (size_t)s * kTile + c4);
-        o[0] = f2bf2_bits(pv[0], pv[1]);
-        o[1] = f2bf2_bits(pv[2], pv[3]);
+        uint32_t* o = reinterpret_cast<uint32_t*>(obuf + (size_t)s * kTile + c0);
+#pragma unroll
+        for (int j = 0; j < E / 2; ++j) o[j] = f2bf2_bits(pv[2 * j], pv[2 * j + 1]);
       }
       fence_proxy_async();  // generic-proxy smem writes -> visible to the bulk store
       mbar_arrive(&done[s]);
@@ -292,17 +329,21 @@ bool flat_tma_eligible(const FlatArgs& a, int cfg) {
   return ok && a.n >= (uint64_t)tma_tile(cfg);
 }
 
-#define MCO_TMA_CONFIGS(X) \
-  X(0, 16, 4)                  \
-  X(1, 16, 3)                  \
-  X(2, 16, 5)                  \
-  X(3, 24, 4)                  \
-  X(4, 8, 4)
+#define MCO_UNPAREN(...) __VA_ARGS__
+#define MCO_TMA_CONFIGS(X)        \
+  X(0, (TmaCfg<16, 4>))             \
+  X(1, (TmaCfg<16, 3>))             \
+  X(2, (TmaCfg<16, 5>))             \
+  X(3, (TmaCfg<24, 4>))             \
+  X(4, (TmaCfg<8, 4>))              \
+  X(5, (TmaCfg<16, 8, 2>))          \
+  X(6, (TmaCfg<16, 4, 4, true>))    \
+  X(7, (TmaCfg<24, 6, 2>))
 
 int tma_tile(int cfg) {
   switch (cfg) {
-#define X(id, cw, ns) \
-  case id: return TmaCfg<cw, ns>::kTile;
+#define X(id, cfg) \
+  case id: return MCO_UNPAREN cfg::kTile;
     MCO_TMA_CONFIGS(X)
 #undef X
   }
@@ -311,8 +352,8 @@ int tma_tile(int cfg) {
 
 void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st, int cfg) {
   switch (cfg) {
-#define X(id, cw, ns) \
-  case id: launch_cfg<TmaCfg<cw, ns>>(a, k, st); return;
+#define X(id, cfg) \
+  case id: launch_cfg<MCO_UNPAREN cfg>(a, k, st); return;
     MCO_TMA_CONFIGS(X)
 #undef X
   }

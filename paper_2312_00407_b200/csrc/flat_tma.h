@@ -5,8 +5,9 @@
 
 namespace mco {
 
-// cfg (consumer warps, stages): 0 = (16, 4) default, 1 = (16, 3), 2 = (16, 5),
-// 3 = (24, 4), 4 = (8, 4).  A tile is 128 elements per consumer warp.
+// cfg (consumer warps, stages[, elements per thread, L2 hint]): 0 = (16, 4) default,
+// 1 = (16, 3), 2 = (16, 5), 3 = (24, 4), 4 = (8, 4), 5 = (16, 8, 2), 6 = (16, 4, 4,
+// evict-first), 7 = (24, 6, 2).  A tile is 32 * EPT elements per consumer warp.
 int tma_tile(int cfg);
 // fp32 state / params / grads, 16 B aligned buffers, at least one tile.
 bool flat_tma_eligible(const FlatArgs& a, int cfg);
