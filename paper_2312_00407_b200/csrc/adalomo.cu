@@ -34,6 +34,35 @@
 namespace mco {
 namespace {
 
+// ---- Programmatic Dependent Launch --------------------------------------------------
+// Every AdaLomo kernel is launched with programmatic stream serialization and starts
+// with griddepcontrol.wait: its launch and CTA rasterisation overlap the tail of the
+// previous kernel in the stream, while no CTA touches memory before that kernel has
+// completed and flushed (so stream-order semantics are unchanged).  The per-tensor
+// hook form runs 8 dependent launches per tensor, where the launch gaps dominate.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#ifndef MCO_ADALOMO_PDL
+#define MCO_ADALOMO_PDL 1
+#endif
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = MCO_ADALOMO_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MCO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
+
 constexpr int kThreads = 256;
 constexpr int kRB = 2;   // K1 / K6 tiles: rows per thread per loop iteration (loads in flight)
 #ifndef MCO_K1_MINB
@@ -133,6 +162,7 @@ __device__ __forceinline__ float* pptr(const Ptrs& P, const TensorInfo& T) {
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads, kMinCtasK1)
     k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles) {
+  pdl_wait();
   __shared__ float colbuf[kThreads * VW];
   __shared__ float rowbuf[kMaxTileRows * 4];
   __shared__ double scratch[32];
@@ -238,6 +268,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK1)
 __global__ void __launch_bounds__(kThreads)
     kr_stats(Ctx c, int t0, int t1, const int64_t* __restrict__ col_off, int64_t ncols,
              int ncolblk) {
+  pdl_wait();
   if ((int)blockIdx.x < ncolblk) {
     const int64_t gi = col_off[t0] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (gi >= col_off[t0] + ncols) return;
@@ -278,6 +309,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
+  pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = t0 + warp; k < t1; k += 32) {
     const TensorInfo T = c.tensors[k];
@@ -295,6 +327,7 @@ __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
 __global__ void __launch_bounds__(1024)
     k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
                const double* ext_sumsq) {
+  pdl_wait();
   __shared__ double red[32];
   // per-tensor sums arrive (already all-reduced across ranks when sharded) in the payload
   for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
@@ -345,6 +378,7 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(kThreads)
     k3_moments(Ctx c, int t0, int t1, const int64_t* __restrict__ item_off, int64_t item0,
                int64_t nitems, double b2) {
+  pdl_wait();
   const double s = c.glob[0], s2 = s * s;
   for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nitems;
        it += (int64_t)gridDim.x * blockDim.x) {
@@ -419,6 +453,7 @@ __device__ __forceinline__ void chunk_vec_load(const GT* g, int64_t e, int64_t e
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads, kMinCtasK4)
     k4_usq(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double b2, double eps) {
+  pdl_wait();
   __shared__ double scratch[32];
   const float sf = (float)c.glob[0], epsf = (float)eps;
   for (int64_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
@@ -490,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
 // ============================ K5: damping ==============================================
 __global__ void __launch_bounds__(1024)
     k5_damp(Ctx c, int t0, int t1, double adalomo_clip) {
+  pdl_wait();
   for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
     const TensorInfo T = c.tensors[k];
     const double us = c.pay_usq[k];
@@ -504,6 +540,7 @@ __global__ void __launch_bounds__(1024)
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads)
     k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps) {
+  pdl_wait();
   const float sf = (float)c.glob[0], epsf = (float)eps;
   // reverse chunk order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
@@ -579,6 +616,7 @@ __global__ void __launch_bounds__(kThreads)
 template <bool VEC, typename GT>
 __global__ void __launch_bounds__(kThreads)
     k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
+  pdl_wait();
   const float sf = (float)c.glob[0], epsf = (float)eps;
   // reverse tile order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
@@ -658,31 +696,32 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
 
   if (phase == 1) {  // pass 1 over {g, p} + reduction of the tile partials into the payload
     auto kk1 = k1_stats<VEC, GT>;
-    kk1<<<grid_for(kk1, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles);
+    launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles);
     launch_check("adalomo k1_stats");
     const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
     const int ncolblk = (int)((ncols + kThreads - 1) / kThreads);
-    kr_stats<<<ncolblk + 1, kThreads, 0, st>>>(c, call.t0, call.t1, pl.d_col_off, ncols, ncolblk);
+    launch_pdl(kr_stats, ncolblk + 1, kThreads, st, c, call.t0, call.t1,
+               (const int64_t*)pl.d_col_off, ncols, ncolblk);
     launch_check("adalomo kr_stats");
   } else if (phase == 2) {  // scalars, moments, pass 2 over {g}
-    k2_scalars<<<1, 1024, 0, st>>>(c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
-                                   cfg.clip_threshold, call.ext_sumsq);
+    launch_pdl(k2_scalars, 1, 1024, st, c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
+               cfg.clip_threshold, call.ext_sumsq);
     launch_check("adalomo k2_scalars");
     const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
     if (nitems > 0) {
       const int64_t blocks = std::min<int64_t>((nitems + kThreads - 1) / kThreads, sms * 8);
-      k3_moments<<<(unsigned)blocks, kThreads, 0, st>>>(
-          c, call.t0, call.t1, pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
+      launch_pdl(k3_moments, (unsigned)blocks, kThreads, st, c, call.t0, call.t1,
+                 (const int64_t*)pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
       launch_check("adalomo k3_moments");
     }
     auto kk4 = k4_usq<VEC, GT>;
-    kk4<<<grid_for(kk4, nchunks, dev), kThreads, 0, st>>>(c, P, chunk0, nchunks, cfg.beta2,
-                                                          cfg.eps);
+    launch_pdl(kk4, grid_for(kk4, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.beta2,
+               cfg.eps);
     launch_check("adalomo k4_usq");
-    kr_usq<<<1, 1024, 0, st>>>(c, call.t0, call.t1);
+    launch_pdl(kr_usq, 1, 1024, st, c, call.t0, call.t1);
     launch_check("adalomo kr_usq");
   } else {  // damping + pass 3 over {g, p -> p}
-    k5_damp<<<1, 1024, 0, st>>>(c, call.t0, call.t1, cfg.adalomo_clip);
+    launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip);
     launch_check("adalomo k5_damp");
     static const bool k6_tiles = [] {
       // tuning knob MCO_ADALOMO_K6 = "tiles" (default; measured 2.4% faster: the
@@ -692,10 +731,10 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
     }();
     if (k6_tiles) {
       auto kk6 = k6_update_tiles<VEC, GT>;
-      kk6<<<grid_for(kk6, ntiles, dev), kThreads, 0, st>>>(c, P, tile0, ntiles, cfg.eps);
+      launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps);
     } else {
       auto kk6 = k6_update<VEC, GT>;
-      kk6<<<grid_for(kk6, nchunks, dev), kThreads, 0, st>>>(c, P, chunk0, nchunks, cfg.eps);
+      launch_pdl(kk6, grid_for(kk6, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.eps);
     }
     launch_check("adalomo k6_update");
   }

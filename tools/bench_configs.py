@@ -57,7 +57,7 @@ def main():
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     W, K = 2, 5
-    which = sys.argv[1:] or ["c3", "c4", "c5"]
+    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks"]
 
     if "c3" in which:
         m = registry.LLAMA_13B
@@ -108,6 +108,52 @@ def main():
              {"passes": "sum of squares (2 B/param) + clipped update (6 B/param)"})
         ms = timed(lambda: optim.lomo_apply(p, g, 1e-2, 1.0), W, K)
         line("c5 lomo bf16 no clip, rank shard of llama2-70b at N=8", n, ms, 6)
+        del p, g
+        gc.collect()
+        torch.cuda.empty_cache()
+
+    if "hooks" in which:
+        hooks_7b(W, K)
+
+
+def hooks_7b(W, K):
+    """The per-tensor (backward-hook) forms of LOMO and AdaLomo over
+    the 7B set, one call per tensor in reverse registry order as backward produces
+    them, against the multi-tensor flat forms: the per-call overhead of the hook path."""
+    import torch
+
+    from paper_2312_00407_b200 import optim, registry
+    from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+    m = registry.LLAMA_7B
+    shapes, n = m.shapes(), m.param_count()
+    p = torch.empty(n, device="cuda")
+    g = torch.empty(n, device="cuda")
+    registry.fill_params(p, shapes)
+    registry.fill_grads(g, shapes, 1)
+    offs = [0]
+    for s in shapes:
+        offs.append(offs[-1] + int(torch.tensor(s).prod()))
+    views = [(p[offs[k]:offs[k + 1]], g[offs[k]:offs[k + 1]]) for k in range(len(shapes))]
+    order = list(reversed(range(len(shapes))))
+
+    def lomo_hooks():
+        for k in order:
+            optim.lomo_apply(views[k][0], views[k][1], 1e-2, 1.0)
+
+    ms = timed(lomo_hooks, W, K)
+    line("hook-form lomo, llama-7b (291 calls)", n, ms, 12, {"calls": len(shapes)})
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    st = optim.AdaLomoState(cfg, shapes)
+
+    def ada_hooks():
+        for k in order:
+            st.apply(k, views[k][0], views[k][1], 5e-4)
+
+    ms = timed(ada_hooks, W, K)
+    line("hook-form adalomo, llama-7b (291 calls)", n, ms, 24, {"calls": len(shapes)})
+    ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
+    line("multi-tensor adalomo, llama-7b (1 call)", n, ms, 24)
 
 
 if __name__ == "__main__":
