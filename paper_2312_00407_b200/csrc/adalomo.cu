@@ -34,33 +34,9 @@
 namespace mco {
 namespace {
 
-// ---- Programmatic Dependent Launch --------------------------------------------------
-// Every AdaLomo kernel is launched with programmatic stream serialization and starts
-// with griddepcontrol.wait: its launch and CTA rasterisation overlap the tail of the
-// previous kernel in the stream, while no CTA touches memory before that kernel has
-// completed and flushed (so stream-order semantics are unchanged).  The per-tensor
-// hook form runs 8 dependent launches per tensor, where the launch gaps dominate.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-#ifndef MCO_ADALOMO_PDL
-#define MCO_ADALOMO_PDL 1
-#endif
-
-template <typename... KArgs, typename... Args>
-void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
-                Args... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = MCO_ADALOMO_PDL;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  MCO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
-}
+// Programmatic Dependent Launch (common.cuh): every AdaLomo kernel starts with
+// pdl_wait() and is launched with launch_pdl.  The per-tensor hook form runs 8
+// dependent launches per tensor, where the launch gaps dominate.
 
 
 constexpr int kThreads = 256;

@@ -31,6 +31,34 @@ inline void launch_check(const char* what) {
   cuda_check(cudaGetLastError(), what);
 }
 
+// ---- Programmatic Dependent Launch ------------------------------------------------
+// Kernels of dependent chains (AdaLomo's passes, LOMO's sum of squares -> update, the
+// per-tensor hook forms) are launched with programmatic stream serialization and
+// start with griddepcontrol.wait: the launch and CTA rasterisation overlap the tail of
+// the previous kernel in the stream, while no CTA touches memory before that kernel
+// has completed and flushed, so stream-order semantics are unchanged.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+#ifndef MCO_PDL
+#define MCO_PDL 1
+#endif
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = MCO_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+}
+
 struct DeviceInfo {
   int sms = 148;
   int l2_bytes = 0;

@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(kThreads)
                 double lr, double scale, const double* __restrict__ sumsq, double clip) {
   using T = typename std::conditional<std::is_same<PT, double>::value, double, float>::type;
   constexpr int W = lomo_width<PT, GT>();
+  pdl_wait();
   const T f = lomo_factor<T>(lr, scale, sumsq, clip);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -313,6 +314,7 @@ __global__ void __launch_bounds__(kThreads)
   __shared__ double scratch[32];
   __shared__ bool is_last;
   constexpr int W = sumsq_width<XT>();
+  pdl_wait();
   using LT = typename std::conditional<std::is_same<XT, double>::value, double, float>::type;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -531,7 +533,7 @@ void run_lomo(void* p, const void* g, uint64_t n, double lr, double scale, const
   const uint64_t nvec = vec ? n / W : 0;
   const uint64_t items = nvec ? (nvec + 1) / 2 : n;
   const int grid = grid_for(kern, std::max<uint64_t>(items, 1), current_device());
-  kern<<<grid, kThreads, 0, st>>>((PT*)p, (const GT*)g, nvec, n, lr, scale, sumsq, clip);
+  launch_pdl(kern, grid, kThreads, st, (PT*)p, (const GT*)g, nvec, n, lr, scale, sumsq, clip);
   launch_check("lomo_kernel");
 }
 
@@ -544,7 +546,7 @@ void run_sumsq(const void* x, uint64_t n, double* out, int accumulate, double* p
   const uint64_t nvec = vec ? n / W : 0;
   int grid = grid_for(kern, std::max<uint64_t>(nvec ? nvec : n, 1), dev);
   grid = std::min(grid, kSumsqMaxBlocks);
-  kern<<<grid, kThreads, 0, st>>>((const XT*)x, nvec, n, out, accumulate, partials, counter);
+  launch_pdl(kern, grid, kThreads, st, (const XT*)x, nvec, n, out, accumulate, partials, counter);
   launch_check("sumsq_kernel");
 }
 
