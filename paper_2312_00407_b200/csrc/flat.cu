@@ -226,15 +226,6 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // ---- LOMO ---------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ T lomo_factor(double lr, double scale, const double* sumsq,
-                                         double clip) {
-  if (sumsq) {  // optim.cpp:302-303
-    const double norm = sqrt(*sumsq);
-    scale = (norm > clip && norm > 0) ? clip / norm : 1.0;
-  }
-  return (T)(lr * scale);  // optim.cpp:188  f = lr * scale
-}
 
 template <typename PT, typename GT>
 constexpr int lomo_width() {
@@ -567,6 +558,15 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
 void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
                  double scale, const double* dev_sumsq, double clip, cudaStream_t st) {
   if (n == 0) return;
+  const int variant = flat_variant();
+  // LOMO's 16 KB (fp32) stages want 8 in flight (measured: 4 -> 0.95, 8 -> 1.02 of the
+  // copy bandwidth); "tma_s3" / "tma_s5" select 4 / 12 for A/B runs
+  if ((variant == V_TMA || variant == V_TMA_S3 || variant == V_TMA_S5) &&
+      lomo_tma_eligible(p, p_dtype, g, g_dtype, n)) {
+    launch_lomo_tma(p, p_dtype, g, n, lr, scale, dev_sumsq, clip, st,
+                    variant == V_TMA_S3 ? 4 : variant == V_TMA_S5 ? 12 : 8);
+    return;
+  }
   if (p_dtype == MCO_F32 && g_dtype == MCO_F32)
     run_lomo<float, float>(p, g, n, lr, scale, dev_sumsq, clip, st);
   else if (p_dtype == MCO_F32 && g_dtype == MCO_BF16)

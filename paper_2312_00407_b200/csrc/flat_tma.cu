@@ -281,6 +281,137 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
   }
 }
 
+// ---- LOMO on the same pipeline -----------------------------------------------------
+// p -= f * g (optim.cpp:185-190): two input streams of one element type (fp32, or bf16
+// parameters with bf16 gradients -- fp32 arithmetic, RNE store, as lomo_kernel), p
+// stored back.  Each consumer thread moves 16 B per stream per stage.
+constexpr int kLomoWarps = 16;
+constexpr int kLomoConsumers = kLomoWarps * 32;
+
+template <typename ET>
+constexpr int lomo_tile() {
+  return kLomoConsumers * (16 / (int)sizeof(ET));
+}
+
+template <typename ET, int NS>
+__global__ void __launch_bounds__(kLomoConsumers + 32, 1)
+    lomo_tma_kernel(ET* p, const ET* g, uint64_t ntiles, uint64_t n, double lr, double scale,
+                    const double* sumsq, double clip) {
+  constexpr int EPT = 16 / (int)sizeof(ET);
+  constexpr int kTile = lomo_tile<ET>();
+  constexpr uint32_t kBytes = kTile * sizeof(ET);
+  extern __shared__ __align__(128) uint8_t smem[];
+  ET* buf = reinterpret_cast<ET*>(smem);  // [NS][2][kTile]
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * 2 * kTile);
+  uint64_t* done = full + NS;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kLomoConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();  // the clip's sum of squares comes from the previous kernel
+  const uint64_t mine =
+      ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (warp == kLomoWarps) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      auto issue = [&](uint64_t i) {
+        const int s = (int)(i % NS);
+        const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
+        mbar_expect_tx(&full[s], 2 * kBytes);
+        bulk_g2s<false>(buf + (size_t)s * 2 * kTile, p + e, kBytes, &full[s], 0);
+        bulk_g2s<false>(buf + ((size_t)s * 2 + 1) * kTile, g + e, kBytes, &full[s], 0);
+      };
+      for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
+      for (uint64_t i = 0; i < mine; ++i) {
+        const int s = (int)(i % NS);
+        mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
+        const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
+        bulk_s2g<false>(p + e, buf + (size_t)s * 2 * kTile, kBytes, 0);
+        bulk_commit();
+        if (i >= 1 && i - 1 + NS < mine) {  // refill the previous tile's stage
+          bulk_wait_read_1();
+          issue(i - 1 + NS);
+        }
+      }
+      bulk_wait_all();
+    }
+  } else {  // ---------------- consumers ----------------
+    const float f = lomo_factor<float>(lr, scale, sumsq, clip);
+    const int c0 = threadIdx.x * EPT;
+    for (uint64_t i = 0; i < mine; ++i) {
+      const int s = (int)(i % NS);
+      mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+      ET* sp = buf + (size_t)s * 2 * kTile + c0;
+      const ET* sg = sp + kTile;
+      if constexpr (sizeof(ET) == 4) {
+        float4 pv = *reinterpret_cast<const float4*>(sp);
+        const float4 gv = *reinterpret_cast<const float4*>(sg);
+        pv.x = pv.x - f * gv.x;
+        pv.y = pv.y - f * gv.y;
+        pv.z = pv.z - f * gv.z;
+        pv.w = pv.w - f * gv.w;
+        *reinterpret_cast<float4*>(sp) = pv;
+      } else {
+        uint4 pw = *reinterpret_cast<const uint4*>(sp);
+        const uint4 gw = *reinterpret_cast<const uint4*>(sg);
+        uint32_t* pa = &pw.x;
+        const uint32_t* ga = &gw.x;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float lo = __uint_as_float(pa[k] << 16) - f * __uint_as_float(ga[k] << 16);
+          const float hi = __uint_as_float(pa[k] & 0xffff0000u) -
+                           f * __uint_as_float(ga[k] & 0xffff0000u);
+          pa[k] = f2bf2_bits(lo, hi);
+        }
+        *reinterpret_cast<uint4*>(sp) = pw;
+      }
+      fence_proxy_async();
+      mbar_arrive(&done[s]);
+    }
+    if (blockIdx.x == 0) {  // tail (< one tile)
+      for (uint64_t e = ntiles * kTile + threadIdx.x; e < n; e += kLomoConsumers) {
+        if constexpr (sizeof(ET) == 4)
+          p[e] = p[e] - f * g[e];
+        else
+          p[e] = (ET)f2bf_bits(bf2f(p[e]) - f * bf2f(g[e]));
+      }
+    }
+  }
+}
+
+template <typename ET, int NS>
+void run_lomo_tma(void* p, const void* g, uint64_t n, double lr, double scale,
+                  const double* sumsq, double clip, cudaStream_t st) {
+  auto kern = lomo_tma_kernel<ET, NS>;
+  constexpr int smem = NS * 2 * lomo_tile<ET>() * (int)sizeof(ET) + 2 * NS * 8;
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr_set{0};
+  if (!(attr_set.load() & (1ull << dev))) {
+    MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set.fetch_or(1ull << dev);
+  }
+  const uint64_t ntiles = n / lomo_tile<ET>();
+  const int grid = (int)std::max<uint64_t>(
+      1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kLomoConsumers + 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = MCO_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MCO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (ET*)p, (const ET*)g, ntiles, n, lr, scale,
+                                    sumsq, clip));
+  launch_check("lomo_tma_kernel");
+}
+
 template <class C, int KIND, bool MIXED>
 void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
   auto kern = flat_tma_kernel<C, KIND, MIXED>;
@@ -358,6 +489,30 @@ void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t
 #undef X
   }
   throw Error(MCO_CONFIG, "flat_tma: unknown configuration");
+}
+
+bool lomo_tma_eligible(const void* p, int p_dtype, const void* g, int g_dtype, uint64_t n) {
+  if (p_dtype != g_dtype || (p_dtype != MCO_F32 && p_dtype != MCO_BF16)) return false;
+  if (((uintptr_t)p % 16) || ((uintptr_t)g % 16)) return false;
+  return n >= (uint64_t)(p_dtype == MCO_F32 ? lomo_tile<float>() : lomo_tile<uint16_t>());
+}
+
+void launch_lomo_tma(void* p, int p_dtype, const void* g, uint64_t n, double lr, double scale,
+                     const double* sumsq, double clip, cudaStream_t st, int stages) {
+  const bool f32 = p_dtype == MCO_F32;
+  switch (stages) {
+    case 4:
+      f32 ? run_lomo_tma<float, 4>(p, g, n, lr, scale, sumsq, clip, st)
+          : run_lomo_tma<uint16_t, 4>(p, g, n, lr, scale, sumsq, clip, st);
+      break;
+    case 12:
+      f32 ? run_lomo_tma<float, 12>(p, g, n, lr, scale, sumsq, clip, st)
+          : run_lomo_tma<uint16_t, 12>(p, g, n, lr, scale, sumsq, clip, st);
+      break;
+    default:
+      f32 ? run_lomo_tma<float, 8>(p, g, n, lr, scale, sumsq, clip, st)
+          : run_lomo_tma<uint16_t, 8>(p, g, n, lr, scale, sumsq, clip, st);
+  }
 }
 
 }  // namespace mco

@@ -13,4 +13,9 @@ int tma_tile(int cfg);
 bool flat_tma_eligible(const FlatArgs& a, int cfg);
 void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st, int cfg);
 
+// LOMO p -= f*g on the TMA pipeline: fp32/fp32 or bf16/bf16, 16 B aligned, >= one tile.
+bool lomo_tma_eligible(const void* p, int p_dtype, const void* g, int g_dtype, uint64_t n);
+void launch_lomo_tma(void* p, int p_dtype, const void* g, uint64_t n, double lr, double scale,
+                     const double* sumsq, double clip, cudaStream_t st, int stages);
+
 }  // namespace mco

@@ -49,6 +49,18 @@ __device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
   }
 }
 
+// LOMO step factor f = lr * scale (optim.cpp:188); with a device sum of squares the
+// scale is the global-norm clip rule (optim.cpp:291-303).
+template <typename T>
+__device__ __forceinline__ T lomo_factor(double lr, double scale, const double* sumsq,
+                                         double clip) {
+  if (sumsq) {  // optim.cpp:302-303
+    const double norm = sqrt(*sumsq);
+    scale = (norm > clip && norm > 0) ? clip / norm : 1.0;
+  }
+  return (T)(lr * scale);  // optim.cpp:188  f = lr * scale
+}
+
 // ---- vector load helpers by element type -----------------------------------
 template <typename T>
 struct Vec;

@@ -89,6 +89,44 @@ def test_lomo_clip_matches_reference_two_pass(clip):
                                atol=4 * np.finfo(np.float64).eps * np.abs(want).max())
 
 
+@pytest.mark.parametrize("variant", ["ldg", "tma", "tma_s3", "tma_s5"])
+@pytest.mark.parametrize("n", [4096 + 3, 3 * 8192 + 17, (1 << 20) + 5])
+def test_lomo_variants_bit_exact(variant, n):
+    """The TMA LOMO pipeline (default) and the LDG kernel give the restatement's bits,
+    fp32 and bf16, with and without the device-side clip scale."""
+    prev = optim.flat_variant()
+    optim.set_flat_variant(variant)
+    try:
+        for clip in (None, 0.01):
+            p32 = O.synth(n, 6, 0, 0, 0, 0, -6, 0, False)
+            g32 = O.synth(n, 6, 1, 0, 1, 0, -7, 10, False)
+            t, tg = dev(p32), dev(g32)
+            scale = 0.75
+            if clip is None:
+                optim.lomo_apply(t, tg, 1e-2, scale)
+            else:
+                s = optim.sumsq(tg)
+                optim.lomo_apply_clipped(t, tg, 1e-2, s, clip)
+                scale = O.orc.orc_clip_scale(float(s.item()), clip)
+            O.orc.orc_lomo_f32(O._ptr(p32), O._ptr(g32), n, 1e-2, scale)
+            assert bits_equal(t.cpu().numpy(), p32)
+
+            pb = O.synth(n, 6, 0, 0, 0, 0, -6, 0, False, "bf16")
+            gb = O.synth(n, 6, 1, 0, 1, 0, -7, 10, False, "bf16")
+            tb, tgb = dev(pb).view(torch.bfloat16), dev(gb).view(torch.bfloat16)
+            scale = 1.0
+            if clip is None:
+                optim.lomo_apply(tb, tgb, 1e-2, scale)
+            else:
+                s = optim.sumsq(tgb)
+                optim.lomo_apply_clipped(tb, tgb, 1e-2, s, clip)
+                scale = O.orc.orc_clip_scale(float(s.item()), clip)
+            O.orc.orc_lomo_bf16(O._ptr(pb), O._ptr(gb), n, 1e-2, scale)
+            assert bits_equal(tb.view(torch.int16).cpu().numpy(), pb.view(np.int16))
+    finally:
+        optim.set_flat_variant(prev)
+
+
 def test_lomo_lr_zero_is_noop():  # test_optim.cpp:248-257
     p = O.synth(1000, 1, 0, 0, 0, 0, -6, 0, False)
     t = dev(p)
