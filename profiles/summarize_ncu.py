@@ -19,7 +19,7 @@ KIND_OF = [("flat_tma_kernel<0,", "adamw"), ("flat_tma_kernel<1,", "lion"),
            ("flat_tma_kernel<2,", "adan"), ("flat_tma_kernel<3,", "sophia"),
            ("flat_step_kernel<0,", "adamw"), ("flat_step_kernel<1,", "lion"),
            ("flat_step_kernel<2,", "adan"), ("flat_step_kernel<3,", "sophia"),
-           ("lomo_kernel", "lomo"), ("k1_stats", "adalomo"), ("k2_scalars", "adalomo"),
+           ("lomo_kernel", "lomo"), ("lomo_tma_kernel", "lomo"), ("k1_stats", "adalomo"), ("k2_scalars", "adalomo"),
            ("k3_moments", "adalomo"), ("k4_usq", "adalomo"), ("k5_damp", "adalomo"),
            ("k6_update", "adalomo")]
 
@@ -56,7 +56,7 @@ def main(path, nparams):
         print(f"| `{name[:70]}` | {a['n']} | {a['t'] * 1e3:.2f} | {a['t'] / total_t:.1%} | "
               f"{bpp:.3f} | {gbs:.0f} |")
         # flat_tma_kernel<TmaCfg<CW,NS>,KIND,MIXED> -> flat_tma_kernel<KIND,
-        key = re.sub(r"flat_tma_kernel<.*?TmaCfg<\d+,\d+>,", "flat_tma_kernel<",
+        key = re.sub(r"flat_tma_kernel<.*?TmaCfg<[\d,]+>,", "flat_tma_kernel<",
                      name.replace(" ", ""))
         for pat, kind in KIND_OF:
             if pat in key:
