@@ -7,9 +7,15 @@ gradient is complete (the reference's Tape::add_post_grad_hook, tensor.cpp:215-2
 then the gradient is dropped -- so at most one parameter gradient is alive at a
 time plus whatever autograd holds, which is LOMO's memory property
 (test_optim.cpp:286-316).  The update itself is the sm_100a kernel behind the C-ABI
-(lomo_apply / lomo_apply_clipped / AdaLomoState.apply); with a process group the
-hook first all-reduces (SUM) the gradient, as the reference's fused DP path does
-(parallel.cpp:585-599).
+(lomo_apply / lomo_apply_clipped / AdaLomoState.apply).
+
+With a process group the gradient is SUM-all-reduced first, as the reference's fused
+DP path does (parallel.cpp:585-599): one all-reduce per parameter (the reference's
+behaviour), or -- with ``bucket_elems`` -- gradients are packed into one reusable flat
+bucket and all-reduced together, then every packed parameter is updated from its
+view of the reduced bucket (a bucketed DP all-reduce instead of one
+per parameter, parallel.cpp:591).  Live gradient memory stays bounded by the bucket
+plus one tensor.
 """
 from __future__ import annotations
 
@@ -18,27 +24,106 @@ from typing import Callable, Optional, Sequence
 from . import optim
 
 
+class _CudaOps:
+    sumsq = staticmethod(optim.sumsq)
+    lomo_apply = staticmethod(optim.lomo_apply)
+    lomo_apply_clipped = staticmethod(optim.lomo_apply_clipped)
+
+
 def _hooks(params, fn):
     handles = [p.register_post_accumulate_grad_hook(fn) for p in params]
     return handles
 
 
-def _dp_reduce(p, group):
+def _world(group) -> int:
     if group is None:
-        return
+        return 1
     import torch.distributed as dist
 
-    if dist.get_world_size(group) > 1:
-        dist.all_reduce(p.grad, op=dist.ReduceOp.SUM, group=group)
+    return dist.get_world_size(group)
+
+
+class _GradPath:
+    """Delivers each parameter's (DP-reduced) gradient to ``fn(p, grad)``.
+
+    Unbucketed: all_reduce(p.grad) per parameter (parallel.cpp:591), then fn.
+    Bucketed: p.grad is copied into a flat bucket and dropped; when the next gradient
+    would not fit (or at flush), the bucket is all-reduced once and fn runs for every
+    packed parameter on its view.  A gradient larger than the bucket is reduced alone.
+    """
+
+    def __init__(self, fn: Callable, group, bucket_elems: Optional[int]):
+        self.fn, self.group = fn, group
+        self.bucket_elems = bucket_elems or None
+        self.world = _world(group)
+        self.buf = None
+        self.items: list = []
+        self.used = 0
+
+    def _allreduce(self, t) -> None:
+        if self.world == 1:
+            return
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def add(self, p) -> None:
+        import torch
+
+        if self.bucket_elems is None:
+            self._allreduce(p.grad)
+            self.fn(p, p.grad)
+            p.grad = None
+            return
+        n = p.grad.numel()
+        if n > self.bucket_elems:  # oversize: reduce alone, keep the order of updates
+            self.flush()
+            self._allreduce(p.grad)
+            self.fn(p, p.grad)
+            p.grad = None
+            return
+        if self.buf is None or self.buf.dtype != p.grad.dtype or self.buf.device != p.grad.device:
+            self.flush()
+            self.buf = torch.empty(self.bucket_elems, dtype=p.grad.dtype, device=p.grad.device)
+        if self.used + n > self.bucket_elems:
+            self.flush()
+        self.buf[self.used:self.used + n].copy_(p.grad.reshape(-1))
+        self.items.append((p, self.used, n))
+        self.used += n
+        p.grad = None
+
+    def flush(self) -> None:
+        if not self.items:
+            return
+        self._allreduce(self.buf[:self.used])
+        for p, off, n in self.items:
+            self.fn(p, self.buf[off:off + n].view_as(p))
+        self.items, self.used = [], 0
+
+
+def _run_backward(params, grad_fn, loss_fn, group, bucket_elems, want_loss):
+    path = _GradPath(grad_fn, group, bucket_elems)
+    hs = _hooks(params, lambda p: path.add(p))
+    try:
+        loss = loss_fn()
+        value = loss.detach() if want_loss else None
+        loss.backward()
+        path.flush()
+    finally:
+        for h in hs:
+            h.remove()
+    return value
 
 
 def lomo_fused_backward_step(params: Sequence, loss_fn: Callable, lr: float,
-                             clip_norm: Optional[float] = None, group=None):
+                             clip_norm: Optional[float] = None, group=None,
+                             bucket_elems: Optional[int] = None, ops=_CudaOps):
     """optim.cpp:284-318.  With clip_norm: pass 1 accumulates the global sum of
-    squares of every gradient on the device (deterministic kernel) and drops each
-    gradient at once; pass 2 re-runs forward + backward and applies
+    squares of every (reduced) gradient on the device (deterministic kernel) and drops
+    each gradient at once; pass 2 re-runs forward + backward and applies
     p -= lr * scale * g per parameter with scale = clip/||g|| iff ||g|| > clip.
-    Returns the loss value of the update pass."""
+    Returns the loss value of the update pass.  ``ops`` is the kernel set (CUDA by
+    default; the CPU tests inject the oracle)."""
     import torch
 
     params = list(params)
@@ -46,40 +131,24 @@ def lomo_fused_backward_step(params: Sequence, loss_fn: Callable, lr: float,
     if clip_norm is not None:
         norm2 = torch.zeros((), dtype=torch.float64, device=params[0].device)
 
-        def acc(p):
-            _dp_reduce(p, group)
-            optim.sumsq(p.grad, out=norm2, accumulate=True)
-            p.grad = None
+        def acc(p, g):
+            ops.sumsq(g, out=norm2, accumulate=True)
 
-        hs = _hooks(params, acc)
-        try:
-            loss_fn().backward()
-        finally:
-            for h in hs:
-                h.remove()
+        _run_backward(params, acc, loss_fn, group, bucket_elems, False)
 
-    def upd(p):
-        _dp_reduce(p, group)
+    def upd(p, g):
         with torch.no_grad():
             if norm2 is None:
-                optim.lomo_apply(p.data, p.grad, lr, 1.0)
+                ops.lomo_apply(p.data, g, lr, 1.0)
             else:
-                optim.lomo_apply_clipped(p.data, p.grad, lr, norm2, clip_norm)
-        p.grad = None
+                ops.lomo_apply_clipped(p.data, g, lr, norm2, clip_norm)
 
-    hs = _hooks(params, upd)
-    try:
-        loss = loss_fn()
-        value = loss.detach()
-        loss.backward()
-    finally:
-        for h in hs:
-            h.remove()
-    return value
+    return _run_backward(params, upd, loss_fn, group, bucket_elems, True)
 
 
 def adalomo_fused_step(params: Sequence, loss_fn: Callable, lr: float,
-                       state: "optim.AdaLomoState", group=None):
+                       state: "optim.AdaLomoState", group=None,
+                       bucket_elems: Optional[int] = None):
     """optim.cpp:320-335: AdaLomoState::apply per parameter inside backward.
     `state` was created with the parameters' shapes in the same order."""
     import torch
@@ -87,18 +156,8 @@ def adalomo_fused_step(params: Sequence, loss_fn: Callable, lr: float,
     params = list(params)
     index = {id(p): k for k, p in enumerate(params)}
 
-    def upd(p):
-        _dp_reduce(p, group)
+    def upd(p, g):
         with torch.no_grad():
-            state.apply(index[id(p)], p.data, p.grad, lr)
-        p.grad = None
+            state.apply(index[id(p)], p.data, g.contiguous(), lr)
 
-    hs = _hooks(params, upd)
-    try:
-        loss = loss_fn()
-        value = loss.detach()
-        loss.backward()
-    finally:
-        for h in hs:
-            h.remove()
-    return value
+    return _run_backward(params, upd, loss_fn, group, bucket_elems, True)

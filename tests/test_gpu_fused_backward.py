@@ -152,3 +152,26 @@ def test_adalomo_fused_equals_stored_gradient_apply_all():
                 sb.apply(k, p.data, p.grad, 0.01)
     for x, y in zip(a.parameters(), b.parameters()):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("bucket", [None, 300, 1 << 20])
+def test_bucketed_gradient_path_same_result(bucket):
+    """Gradients packed into a flat bucket (the bucketed DP all-reduce path of f1) give
+    the same bits as the per-parameter path; live gradients stay within the bucket."""
+    a, b = tiny_model(8), tiny_model(8)
+    for _ in range(3):
+        fused.lomo_fused_backward_step(list(a.parameters()), lambda: toy_loss(a), 0.05,
+                                       clip_norm=0.3)
+        fused.lomo_fused_backward_step(list(b.parameters()), lambda: toy_loss(b), 0.05,
+                                       clip_norm=0.3, bucket_elems=bucket)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+    shapes = [tuple(p.shape) for p in a.parameters()]
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    sa, sb = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    fused.adalomo_fused_step(list(a.parameters()), lambda: toy_loss(a), 0.01, sa)
+    fused.adalomo_fused_step(list(b.parameters()), lambda: toy_loss(b), 0.01, sb,
+                             bucket_elems=bucket)
+    for x, y in zip(a.parameters(), b.parameters()):
+        assert torch.equal(x, y)
+        assert x.grad is None and y.grad is None
