@@ -245,26 +245,44 @@ __global__ void __launch_bounds__(kThreads)
     kr_stats(Ctx c, int t0, int t1, const int64_t* __restrict__ col_off, int64_t ncols,
              int ncolblk) {
   pdl_wait();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((int)blockIdx.x < ncolblk) {
-    const int64_t gi = col_off[t0] + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= col_off[t0] + ncols) return;
-    int lo = t0, hi = t1 - 1;  // largest k with col_off[k] <= gi
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (col_off[mid] <= gi)
-        lo = mid;
-      else
-        hi = mid - 1;
-    }
-    const TensorInfo T = c.tensors[lo];
-    const int64_t j = gi - col_off[lo];
+    // 32 columns per CTA (one per lane, coalesced rows of the partials); the 8 warps
+    // take row blocks warp, warp+8, ... and are combined in warp order: a fixed order,
+    // with 8x the loads in flight of one thread walking all row blocks (the single-
+    // tensor hook form launches only C/32 CTAs here)
+    __shared__ double part[kThreads / 32][32];
+    const int64_t gi = col_off[t0] + (int64_t)blockIdx.x * 32 + lane;
+    const bool valid = gi < col_off[t0] + ncols;
     double acc = 0.0;
-    for (int64_t rb = 0; rb < T.nrb; ++rb)
-      acc += (double)c.colpart[T.colpart_off + rb * T.cols + j];
-    c.pay[3 * c.ntens + T.fb_off + j] = T.weight * acc;
+    int64_t slot = -1;
+    double w = 0.0;
+    if (valid) {
+      int lo = t0, hi = t1 - 1;  // largest k with col_off[k] <= gi
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (col_off[mid] <= gi)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      const TensorInfo& T = c.tensors[lo];
+      const int64_t j = gi - col_off[lo];
+      const float* src = c.colpart + T.colpart_off + j;
+      const int64_t nrb = T.nrb, C = T.cols;
+      for (int64_t rb = warp; rb < nrb; rb += nw) acc += (double)src[rb * C];
+      slot = 3 * c.ntens + T.fb_off + j;
+      w = T.weight;
+    }
+    part[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && valid) {
+      double sum = 0.0;
+      for (int q = 0; q < nw; ++q) sum += part[q][lane];
+      c.pay[slot] = w * sum;
+    }
     return;
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = t0 + warp; k < t1; k += nw) {
     const TensorInfo T = c.tensors[k];
     double ps = 0, gs = 0, vr = 0;
@@ -675,7 +693,7 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
     launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles);
     launch_check("adalomo k1_stats");
     const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
-    const int ncolblk = (int)((ncols + kThreads - 1) / kThreads);
+    const int ncolblk = (int)((ncols + 31) / 32);
     launch_pdl(kr_stats, ncolblk + 1, kThreads, st, c, call.t0, call.t1,
                (const int64_t*)pl.d_col_off, ncols, ncolblk);
     launch_check("adalomo kr_stats");
