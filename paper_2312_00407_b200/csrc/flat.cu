@@ -4,11 +4,15 @@
 //
 // One pass per step: every param / grad / state element is read once and
 // written at most once (HBM roofline: SURVEY.md 8(d) bytes per param).
-// Persistent grid-stride CTAs (SMs x resident CTAs), 256-bit LDG/STG
-// (ld.global.v8.f32 -> LDG.E.256), L1 no-allocate + L2 evict-first for the
+// Dispatch (launch_flat_step / launch_lomo): fp32 calls go to the warp-specialised
+// cp.async.bulk pipeline of flat_tma.cu (the default "tma" variant); everything
+// else -- bf16 gradients, f64 state, unaligned ZeRO shard edges, the "ldg" variant --
+// runs the kernels here: persistent grid-stride CTAs (SMs x resident CTAs), 256-bit
+// LDG/STG (ld.global.v8.f32 -> LDG.E.256), L1 no-allocate + L2 evict-first for the
 // streams, U vectors in flight per thread.  Compiled with --fmad=false: the
 // arithmetic is the reference's operation order, no fused multiply-add, IEEE
-// division and square root -- bit-identical to oracle/mco_oracle.c.
+// division and square root -- bit-identical to oracle/mco_oracle.c, whichever
+// variant moves the data.
 #include <algorithm>
 #include <atomic>
 #include <cstdlib>
