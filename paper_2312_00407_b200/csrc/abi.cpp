@@ -17,6 +17,7 @@
 #include "adalomo.h"
 #include "kernels.h"
 #include "mco.h"
+#include "abi_util.h"
 #include "peer.h"
 
 namespace mco {
@@ -48,36 +49,6 @@ int current_device() {
 }
 
 namespace {
-
-template <class F>
-mco_status guard(F&& f) {
-  try {
-    f();
-    return MCO_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.status;
-  } catch (const std::bad_alloc&) {
-    g_err = "host allocation failed";
-    return MCO_CUDA;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return MCO_CUDA;
-  }
-}
-
-// RAII current-device switch.
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    MCO_CUDA_CHECK(cudaGetDevice(&prev));
-    if (prev != dev) MCO_CUDA_CHECK(cudaSetDevice(dev));
-  }
-  ~DeviceGuard() {
-    int cur = -1;
-    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
-  }
-};
 
 // optim.cpp:17-28
 const char* kind_cstr(int kind) {

@@ -24,12 +24,11 @@
 #include <string>
 #include <vector>
 
+#include "abi_util.h"
 #include "common.cuh"
 #include "mco.h"
 
 namespace mco {
-void set_last_error(const std::string& m);  // abi.cpp
-
 namespace {
 
 struct NcclApi {
@@ -114,31 +113,6 @@ ncclDataType_t nccl_type(int dt) {
 
 size_t dt_size(int dt) { return dt == MCO_F64 ? 8 : dt == MCO_BF16 ? 2 : 4; }
 
-template <class F>
-mco_status guarded(F&& f) {
-  try {
-    f();
-    return MCO_OK;
-  } catch (const Error& e) {
-    set_last_error(e.what());
-    return e.status;
-  } catch (const std::exception& e) {
-    set_last_error(e.what());
-    return MCO_CUDA;
-  }
-}
-
-struct DevSwitch {
-  int prev = -1;
-  explicit DevSwitch(int d) {
-    MCO_CUDA_CHECK(cudaGetDevice(&prev));
-    if (prev != d) MCO_CUDA_CHECK(cudaSetDevice(d));
-  }
-  ~DevSwitch() {
-    int cur = -1;
-    if (cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
-  }
-};
 
 }  // namespace
 }  // namespace mco
@@ -159,7 +133,7 @@ struct mco_comm {
 extern "C" {
 
 mco_status mco_comm_unique_id(void* id_out) {
-  return guarded([&] {
+  return guard([&] {
     if (!id_out) throw Error(MCO_CONTRACT, "comm unique id: null output");
     ncclUniqueId id;
     MCO_NCCL_CHECK(nccl().get_unique_id(&id));
@@ -168,12 +142,12 @@ mco_status mco_comm_unique_id(void* id_out) {
 }
 
 mco_status mco_comm_create(const void* id, int nranks, int rank, int device, mco_comm** out) {
-  return guarded([&] {
+  return guard([&] {
     if (!id || !out) throw Error(MCO_CONTRACT, "comm create: null argument");
     if (nranks < 1 || rank < 0 || rank >= nranks)
       throw Error(MCO_CONFIG, "comm create: rank " + std::to_string(rank) + " of " +
                                   std::to_string(nranks));
-    DevSwitch ds(device);
+    DeviceGuard ds(device);
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
     auto* c = new mco_comm;
@@ -191,15 +165,15 @@ mco_status mco_comm_create(const void* id, int nranks, int rank, int device, mco
 }
 
 mco_status mco_comm_destroy(mco_comm* c) {
-  return guarded([&] {
+  return guard([&] {
     if (!c) return;
-    DevSwitch ds(c->device);
+    DeviceGuard ds(c->device);
     delete c;
   });
 }
 
 mco_status mco_comm_check(mco_comm* c) {
-  return guarded([&] {
+  return guard([&] {
     ncclResult_t r = ncclSuccess;
     MCO_NCCL_CHECK(nccl().comm_get_async_error(c->comm, &r));
     nccl_check(r, "NCCL asynchronous error");
@@ -207,8 +181,8 @@ mco_status mco_comm_check(mco_comm* c) {
 }
 
 mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n, void* stream) {
-  return guarded([&] {
-    DevSwitch ds(c->device);
+  return guard([&] {
+    DeviceGuard ds(c->device);
     MCO_NCCL_CHECK(nccl().all_reduce(buf, buf, n, nccl_type(dtype), ncclSum, c->comm,
                                      (cudaStream_t)stream));
   });
@@ -218,7 +192,7 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
                           const void* flat_grads, int grad_dtype, uint64_t total_len, double lr,
                           void* stream) {
   // argument checks come first, before any collective (every rank fails the same way)
-  return guarded([&] {
+  return guard([&] {
     if (!h || !c || !flat_params || !flat_grads)
       throw Error(MCO_CONTRACT, "shard step: null argument");
     const int N = c->nranks, me = c->rank;
@@ -241,7 +215,7 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
                                     " " + std::to_string(parts[me]));
     const ncclDataType_t gt = nccl_type(grad_dtype), pt = nccl_type(param_dtype);
     const size_t gs = dt_size(grad_dtype), ps = dt_size(param_dtype);
-    DevSwitch ds(c->device);
+    DeviceGuard ds(c->device);
     const size_t need = std::max<size_t>(parts[me] * gs, 256);
     if (c->scratch_bytes < need) {
       if (c->scratch) MCO_CUDA_CHECK(cudaFree(c->scratch));
