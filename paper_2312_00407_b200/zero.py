@@ -135,7 +135,11 @@ class ZeroShardedOptimizer:
         check_agreement("ZeroShardedOptimizer", dict(total_len=total_len, stage=stage,
                                                      kind=int(cfg.kind), mixed=mixed), group)
         self.plan = ZeroPlan.make(total_len, self.world, stage)
-        self.lo, self.hi = self.plan.owned_range(self.rank)
+        self.stage = stage
+        self.total_len = total_len
+        # the optimizer owns the ZeroPlan part for stage >= 1, everything at stage 0
+        # (parallel.cpp:330)
+        self.lo, self.hi = self.plan.owned_range(self.rank) if stage >= 1 else (0, total_len)
         self.mixed = mixed
         self.master = None
         if mixed:
@@ -150,8 +154,31 @@ class ZeroShardedOptimizer:
             self.opt = None
 
     def step(self, flat_params, flat_grads, lr: float) -> None:
-        g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group)
-        p_owned = flat_params[self.lo:self.hi]
+        """The ZeRO branches of ParallelWorker::train_step (parallel.cpp:637-672):
+          stage 0: all-reduce(SUM) grads, step the whole vector on every rank;
+          stage 1: all-reduce(SUM) grads, step the owned slice, all-gather params;
+          stage 2: reduce-scatter(SUM) grads, step the owned slice, all-gather params;
+          stage 3: reduce-scatter(SUM) grads, step the owned shard -- flat_params IS
+                   this rank's shard (hi - lo elements), nothing is gathered.
+        Stages 0 and 1 reduce flat_grads in place (as the reference reduces its
+        flattened copy); stages 2 and 3 leave it untouched."""
+        if self.stage == 3:
+            if flat_params.numel() != self.hi - self.lo:
+                raise optim.ContractError(
+                    f"zero stage 3: params hold {flat_params.numel()} elements, the owned "
+                    f"shard is {self.hi - self.lo}")
+        elif flat_params.numel() != self.total_len or flat_grads.numel() != self.total_len:
+            raise optim.ContractError(
+                f"zero step: flat buffers of {flat_params.numel()} / {flat_grads.numel()} "
+                f"elements for a plan of {self.total_len}")
+        if self.stage <= 1:
+            if self.world > 1:
+                dist = _dist()
+                dist.all_reduce(flat_grads, op=dist.ReduceOp.SUM, group=self.group)
+            g_owned = flat_grads[self.lo:self.hi]
+        else:
+            g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group)
+        p_owned = flat_params if self.stage == 3 else flat_params[self.lo:self.hi]
         if self._local is not None:
             self._local(self.master if self.mixed else p_owned, g_owned, lr,
                         p_owned if self.mixed else None)
@@ -159,7 +186,8 @@ class ZeroShardedOptimizer:
             self.opt.step_mixed(self.master, g_owned.contiguous(), p_owned, lr)
         else:
             self.opt.step(p_owned, g_owned.contiguous(), lr)
-        all_gather_owned(flat_params, self.plan, self.rank, self.group)
+        if self.stage in (1, 2):
+            all_gather_owned(flat_params, self.plan, self.rank, self.group)
 
     def owned_range(self) -> tuple[int, int]:
         return self.lo, self.hi

@@ -62,6 +62,26 @@ def _worker(rank, world, port, out_q):
                 opt.step(params, torch.from_numpy(_grad(P, rank, t)), 1e-3)
             out[(P, kind)] = (params.numpy().copy(), (lo, hi), dict(orc.state))
 
+        # the other ZeRO stages of parallel.cpp:637-672 on the first case
+        P, kind = CASES[world][0]
+        for stage in (0, 1, 3):
+            cfg = OptimizerConfig.defaults_for(kind)
+            cfg.weight_decay = 0.01
+            plan = zero.ZeroPlan.make(P, world, stage)
+            lo, hi = plan.owned_range(rank) if stage >= 1 else (0, P)
+            orc = O.OracleFlat(cfg, hi - lo, np.float64)
+
+            def local_s(p_owned, g_owned, lr, p_out, orc=orc):
+                orc.step(p_owned.numpy(), np.ascontiguousarray(g_owned.numpy()), lr)
+
+            full = torch.from_numpy(O.synth(P, 3, 0, 0, 0, 0, -6, 0, False, np.float64))
+            params = full[lo:hi].clone() if stage == 3 else full
+            opt = zero.ZeroShardedOptimizer(cfg, P, stage=stage, local_step=local_s)
+            assert opt.owned_range() == (lo, hi)
+            for t in range(1, STEPS + 1):
+                opt.step(params, torch.from_numpy(_grad(P, rank, t)), 1e-3)
+            out[("stage", stage)] = (params.numpy().copy(), (lo, hi))
+
         if world == 2:
             # mixed precision: bf16 replicated params, fp32 master + state per shard
             P = 1000
@@ -161,6 +181,26 @@ def _check(res, world):
         assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
         if (world, P) == (3, 10):
             assert [b - a for a, b in ranges] == [4, 3, 3]  # ZeroPlan, trailing smaller
+
+
+def _check_stages(res, world):
+    P, kind = CASES[world][0]
+    want, _ = _serial(P, world, kind)
+    for rank in range(world):
+        for stage in (0, 1, 3):
+            got, (lo, hi) = res[rank][("stage", stage)]
+            ref = want[lo:hi] if stage == 3 else want
+            if world == 2:
+                assert np.array_equal(got, ref), stage
+            else:
+                np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-18)
+
+
+def test_zero_stages_0_1_3_equal_serial(world2, world3):
+    """parallel.cpp:637-672: AR + full step (0), AR + owned step + AG (1), RS + owned
+    step on the stage-3 shard (3) -- the same trajectory as stage 2 and serial."""
+    _check_stages(world2, 2)
+    _check_stages(world3, 3)
 
 
 def test_sharded_step_equals_serial_world2(world2):
