@@ -302,8 +302,7 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-__global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
-  pdl_wait();
+__device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int k = t0 + warp; k < t1; k += 32) {
     const TensorInfo T = c.tensors[k];
@@ -312,6 +311,11 @@ __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
     us = warp_sum(us);
     if (lane == 0) c.pay_usq[k] = T.weight * us;
   }
+}
+
+__global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
+  pdl_wait();
+  usq_payload(c, t0, t1);
 }
 
 // ============================ K2: per-tensor scalars ===============================
@@ -518,8 +522,12 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
 
 // ============================ K5: damping ==============================================
 __global__ void __launch_bounds__(1024)
-    k5_damp(Ctx c, int t0, int t1, double adalomo_clip) {
+    k5_damp(Ctx c, int t0, int t1, double adalomo_clip, int with_usq) {
   pdl_wait();
+  if (with_usq) {  // unsharded call: KR2's reduction here, one launch less per tensor
+    usq_payload(c, t0, t1);
+    __syncthreads();
+  }
   for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
     const TensorInfo T = c.tensors[k];
     const double us = c.pay_usq[k];
@@ -712,10 +720,12 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
     launch_pdl(kk4, grid_for(kk4, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.beta2,
                cfg.eps);
     launch_check("adalomo k4_usq");
-    launch_pdl(kr_usq, 1, 1024, st, c, call.t0, call.t1);
-    launch_check("adalomo kr_usq");
+    if (!call.fuse_usq) {
+      launch_pdl(kr_usq, 1, 1024, st, c, call.t0, call.t1);
+      launch_check("adalomo kr_usq");
+    }
   } else {  // damping + pass 3 over {g, p -> p}
-    launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip);
+    launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip, call.fuse_usq);
     launch_check("adalomo k5_damp");
     static const bool k6_tiles = [] {
       // tuning knob MCO_ADALOMO_K6 = "tiles" (default; measured 2.4% faster: the
@@ -766,7 +776,9 @@ void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int ph
 }
 
 void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
-  for (int phase = 1; phase <= 3; ++phase) launch_adalomo_phase(pl, call, phase, st);
+  AdaLomoCall c = call;
+  c.fuse_usq = 1;  // no all-reduce between the phases
+  for (int phase = 1; phase <= 3; ++phase) launch_adalomo_phase(pl, c, phase, st);
 }
 
 }  // namespace mco

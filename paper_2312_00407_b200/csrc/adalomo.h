@@ -84,6 +84,7 @@ struct AdaLomoCall {
   double lr;
   int use_clip;
   const double* ext_sumsq;  // device global sum g^2 (hook form), or null
+  int fuse_usq;  // phases run back to back: the usq payload is reduced inside K5
 };
 
 // Build the host tile plan for `shapes` (registry order) on a device with `sms` SMs.
