@@ -24,6 +24,8 @@
 // All reductions are fixed-order (no float atomics): results are
 // bit-reproducible run to run.
 #include <algorithm>
+#include <mutex>
+#include <unordered_map>
 #include <cmath>
 #include <cstdlib>
 #include <string>
@@ -674,11 +676,26 @@ __global__ void __launch_bounds__(kThreads)
 
 template <typename K>
 int grid_for(K kernel, int64_t ntiles, int device) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> cache;  // kernel -> resident CTAs per SM
   int per_sm = 0;
-  MCO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
-  per_sm = std::max(per_sm, 1);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find((const void*)kernel);
+    if (it == cache.end()) {
+      MCO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
+      per_sm = std::max(per_sm, 1);
+      cache[(const void*)kernel] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
   const int64_t full = (int64_t)device_info(device).sms * per_sm;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(full, ntiles));
+  // balanced rounds: every CTA takes the same number of items, so the last round is
+  // not a partial wave at a fraction of the bandwidth (the per-tensor hook form:
+  // 512 tiles of a 4096^2 matrix on 444 resident CTAs -> 256 CTAs x 2 tiles)
+  const int64_t rounds = (std::max<int64_t>(ntiles, 1) + full - 1) / full;
+  return (int)std::max<int64_t>(1, (ntiles + rounds - 1) / rounds);
 }
 
 template <bool VEC, typename GT>
@@ -807,6 +824,16 @@ void set_fast_div(TensorInfo& T) {
 // row blocks of h <= 128 rows; h is halved (down to 8) until one tensor alone
 // yields >= 2 tiles per SM, so the per-tensor hook form also fills the GPU.
 // Column partials cost ceil(R/h)*C floats per tensor (written once, read once).
+// Element range per CTA for a 1-D (unfactored) tensor: its passes are fp64 element
+// loops (v_full EMA, sqrt, divide), latency-bound per thread, so a norm vector of
+// 4096 elements is spread over ~2 CTAs per SM (>= 256 elements each) instead of one
+// 64 Ki chunk on one CTA (ncu: K4 16 us, K6 21 us for a single 4096-vector).
+int64_t vector_chunk(int64_t numel, int sms) {
+  int64_t c = (numel + 2LL * sms - 1) / (2LL * sms);
+  c = (c + 255) / 256 * 256;
+  return std::min<int64_t>(std::max<int64_t>(c, 256), 1 << 16);
+}
+
 void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>& shapes,
                         int sms) {
   pl.h_tensors.clear();
@@ -878,7 +905,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
       T.vfull_off = state;
       state += numel;
       T.colpart_off = T.rowpart_off = T.fa_off = T.fb_off = -1;
-      const int64_t chunk = 1 << 16;
+      const int64_t chunk = vector_chunk(numel, sms);
       for (int64_t e0 = 0; e0 < numel || (numel == 0 && e0 == 0); e0 += chunk) {
         Tile tl{};
         tl.tensor = (int32_t)k;
@@ -892,8 +919,9 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
     }
     T.tile_end = (int64_t)pl.h_tiles.size();
     T.chunk_begin = (int64_t)pl.h_chunks.size();
-    for (int64_t e0 = 0; e0 < numel; e0 += kChunkElems)
-      pl.h_chunks.push_back(Chunk{(int32_t)k, 0, e0, std::min(numel, e0 + kChunkElems)});
+    const int64_t chunk = T.factored ? kChunkElems : vector_chunk(numel, sms);
+    for (int64_t e0 = 0; e0 < numel; e0 += chunk)
+      pl.h_chunks.push_back(Chunk{(int32_t)k, 0, e0, std::min(numel, e0 + chunk)});
     T.chunk_end = (int64_t)pl.h_chunks.size();
     T.t = 0;
     T.rows_global = T.rows;
