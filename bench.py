@@ -216,16 +216,16 @@ class Stepper:
         self.rs = None
         self.n = p.numel()
         if kind in ("adamw", "lion", "adan", "sophia"):
-            self.opt = optim.FlatOptimizer(self.cfg, p.numel())
+            self.opt = optim.FlatOptimizer(self.cfg, p.numel(), device=p.device.index)
         elif kind == "adalomo" and world > 1:
-            self.rs = zero.RowShardedAdaLomo(self.cfg, shapes)
+            self.rs = zero.RowShardedAdaLomo(self.cfg, shapes, device=p.device.index)
             self.n = self.rs.local_numel
             self.lp = torch.empty(self.n, device=p.device)
             self.lg = torch.empty(self.n, device=p.device)
             optim.synth_fill(self.lp, registry.SEED, 0, 0xFFFE, 0, 0, -6)
             optim.synth_fill(self.lg, registry.SEED, 1, 0xFFFE, 1, 0, -7, 10)
         elif kind == "adalomo":
-            self.opt = optim.AdaLomoState(self.cfg, shapes)
+            self.opt = optim.AdaLomoState(self.cfg, shapes, device=p.device.index)
         else:
             self.opt = None
 

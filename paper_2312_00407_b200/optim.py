@@ -205,6 +205,16 @@ def _dev(t, what: str):
     return t
 
 
+def _device(device: Optional[int]) -> int:
+    """Explicit device index, or the calling thread's current CUDA device (one process
+    per GPU: rank r works on cuda:r after torch.cuda.set_device)."""
+    if device is not None:
+        return int(device)
+    torch = _torch()
+    # no CUDA device: 0 (host-side argument checks still run; device work fails loudly)
+    return int(torch.cuda.current_device()) if torch.cuda.is_available() else 0
+
+
 def _stream(stream) -> int:
     if stream is None:
         return _torch().cuda.current_stream().cuda_stream
@@ -223,9 +233,9 @@ class _CudaArray:
             "version": 3, "strides": None, "stream": None}
 
 
-def _as_tensor(ptr: int, n: int, dtype: int, owner):
+def _as_tensor(ptr: int, n: int, dtype: int, owner, device: int):
     torch = _torch()
-    return torch.as_tensor(_CudaArray(ptr, n, dtype, owner), device="cuda")
+    return torch.as_tensor(_CudaArray(ptr, n, dtype, owner), device=f"cuda:{device}")
 
 
 # ---- FlatOptimizer ----------------------------------------------------------------------
@@ -237,13 +247,14 @@ class FlatOptimizer:
     state_dtype: "f32" (product path) or "f64" (bit-exact parity mode).
     """
 
-    def __init__(self, cfg: OptimizerConfig, owned_len: int, device: int = 0,
+    def __init__(self, cfg: OptimizerConfig, owned_len: int, device: Optional[int] = None,
                  state_dtype: str = "f32"):
         self._cfg = cfg
         self._n = int(owned_len)
         self._sd = {"f32": MCO_F32, "f64": MCO_F64}[state_dtype]
         h = C.c_void_p()
-        _check(lib.mco_flat_create(C.byref(cfg._to_c()), self._n, device, self._sd,
+        self.device = _device(device)
+        _check(lib.mco_flat_create(C.byref(cfg._to_c()), self._n, self.device, self._sd,
                                    C.byref(h)))
         self._h = h
 
@@ -304,7 +315,8 @@ class FlatOptimizer:
             name, ptr, ln, dt = C.c_char_p(), C.c_void_p(), C.c_uint64(), C.c_int()
             _check(lib.mco_flat_buffer(self._h, i, C.byref(name), C.byref(ptr), C.byref(ln),
                                        C.byref(dt)))
-            out.append((name.value.decode(), _as_tensor(ptr.value, ln.value, dt.value, self)))
+            out.append((name.value.decode(),
+                        _as_tensor(ptr.value, ln.value, dt.value, self, self.device)))
         return out
 
     def config(self) -> OptimizerConfig:
@@ -394,15 +406,17 @@ def lomo_step(params, grads, lr: float, clip: Optional[float] = None, stream=Non
 class AdaLomoState:
     """optim.hpp:76-96.  `shapes` in registry order; 2-D -> factored."""
 
-    def __init__(self, cfg: OptimizerConfig, shapes: Sequence[Sequence[int]], device: int = 0):
+    def __init__(self, cfg: OptimizerConfig, shapes: Sequence[Sequence[int]],
+                 device: Optional[int] = None):
         self._cfg = cfg
         self.shapes = [tuple(int(d) for d in s) for s in shapes]
         self.numels = [int(np.prod(s)) if len(s) else 1 for s in self.shapes]
         self.offsets = np.concatenate([[0], np.cumsum(self.numels)]).astype(np.int64)
         nd, dims = _shape_arrays(self.shapes)
         h = C.c_void_p()
-        _check(lib.mco_adalomo_create(C.byref(cfg._to_c()), len(self.shapes), nd, dims, device,
-                                      C.byref(h)))
+        self.device = _device(device)
+        _check(lib.mco_adalomo_create(C.byref(cfg._to_c()), len(self.shapes), nd, dims,
+                                      self.device, C.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -462,7 +476,7 @@ class AdaLomoState:
         """fp64 device view of the statistics (0) or sum-u^2 (1) payload."""
         ptr, ln = C.c_void_p(), C.c_uint64()
         _check(lib.mco_adalomo_payload(self._h, int(which), C.byref(ptr), C.byref(ln)))
-        return _as_tensor(ptr.value, ln.value, MCO_F64, self)
+        return _as_tensor(ptr.value, ln.value, MCO_F64, self, self.device)
 
     def steps(self, index: int) -> int:
         t = C.c_int64()
@@ -476,7 +490,7 @@ class AdaLomoState:
         _check(lib.mco_adalomo_buffer(self._h, int(index), w, C.byref(ptr), C.byref(ln)))
         if not ptr.value:
             return None
-        return _as_tensor(ptr.value, ln.value, MCO_F64, self)
+        return _as_tensor(ptr.value, ln.value, MCO_F64, self, self.device)
 
 
 # ---- misc ---------------------------------------------------------------------------------

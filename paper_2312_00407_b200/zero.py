@@ -148,7 +148,7 @@ class ZeroShardedOptimizer:
             self.master = master_init[self.lo:self.hi].float().clone()
         self._local = local_step
         if local_step is None:
-            dev = device if device is not None else 0
+            dev = optim._device(device)
             self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=dev)
         else:
             self.opt = None
@@ -253,8 +253,8 @@ class _PeerBuffer:
 
         code = optim.MCO_F32 if self.esize == 4 else optim.MCO_BF16
         if code == optim.MCO_F32:
-            return optim._as_tensor(self.ptr, self.numel, optim.MCO_F32, self)
-        raw = torch.as_tensor(_U16View(self.ptr, self.numel, self), device="cuda")
+            return optim._as_tensor(self.ptr, self.numel, optim.MCO_F32, self, self.device)
+        raw = torch.as_tensor(_U16View(self.ptr, self.numel, self), device=f"cuda:{self.device}")
         return raw.view(torch.bfloat16)
 
     def handle(self) -> bytes:
@@ -288,7 +288,7 @@ class PeerBuffers:
     On one device with several processes (tests) the same IPC path is used."""
 
     def __init__(self, total_len: int, group=None, param_dtype=None, grad_dtype=None,
-                 device: int = 0):
+                 device: Optional[int] = None):
         import ctypes as C
 
         import torch
@@ -299,7 +299,7 @@ class PeerBuffers:
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
         self.rank = dist.get_rank(group) if dist.is_initialized() else 0
-        self.device = device
+        self.device = device = optim._device(device)
         self.total_len = total_len
         check_agreement("PeerBuffers", dict(total_len=total_len, param_dtype=str(param_dtype),
                                             grad_dtype=str(grad_dtype)), group)
@@ -363,7 +363,7 @@ class PeerShardedOptimizer:
     """
 
     def __init__(self, cfg: optim.OptimizerConfig, total_len: int, group=None,
-                 param_dtype=None, grad_dtype=None, master_init=None, device: int = 0,
+                 param_dtype=None, grad_dtype=None, master_init=None, device: Optional[int] = None,
                  buffers: Optional[PeerBuffers] = None):
         self.cfg = cfg
         self.buf = buffers or PeerBuffers(total_len, group, param_dtype, grad_dtype, device)
@@ -425,7 +425,7 @@ class RowShardedAdaLomo:
     everywhere.  The reference's own TP variant computes stats per local shard
     (parallel.cpp:334, 593-594) and is NOT serial AdaLomo; this is."""
 
-    def __init__(self, cfg: optim.OptimizerConfig, shapes, group=None, device: int = 0,
+    def __init__(self, cfg: optim.OptimizerConfig, shapes, group=None, device: Optional[int] = None,
                  rank: Optional[int] = None, world: Optional[int] = None):
         dist = _dist()
         self.group = group
@@ -515,7 +515,7 @@ class NcclComm:
     over the torch.distributed group (any backend), ncclCommInitRank on every rank.
     Lets the sharded step run as one stream-ordered C call (mco_shard_step)."""
 
-    def __init__(self, group=None, device: int = 0):
+    def __init__(self, group=None, device: Optional[int] = None):
         import ctypes as C
 
         from ._lib import lib
@@ -532,7 +532,8 @@ class NcclComm:
             dist.broadcast_object_list(box, src=src, group=group)
             C.memmove(uid, box[0], 128)
         h = C.c_void_p()
-        optim._check(lib.mco_comm_create(uid, self.world, self.rank, device, C.byref(h)))
+        optim._check(lib.mco_comm_create(uid, self.world, self.rank, optim._device(device),
+                                         C.byref(h)))
         self._h = h
 
     def allreduce_sum(self, t, stream=None) -> None:
@@ -562,7 +563,7 @@ class NativeZeroOptimizer:
     ownership and state as ZeroShardedOptimizer (parallel.cpp:656-666)."""
 
     def __init__(self, cfg: optim.OptimizerConfig, total_len: int, comm: NcclComm,
-                 device: int = 0):
+                 device: Optional[int] = None):
         self.comm = comm
         self.total_len = int(total_len)
         self.plan = ZeroPlan.make(self.total_len, comm.world, 2)
