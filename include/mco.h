@@ -193,7 +193,8 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
 mco_status mco_adalomo_destroy(mco_adalomo* h);
 /* AdaLomoState::apply(Tensor& param, lr) -- the per-tensor hook form.
  * dev_grad_sumsq: optional device Σg² over ALL tensors (global grad-norm
- * clip with cfg.clip_threshold); NULL = no clip.  dtypes F32/F32, F32/BF16. */
+ * clip with cfg.clip_threshold); NULL = no clip.  dtypes (param/grad) F32/F32,
+ * F32/BF16, BF16/BF16 (bf16 parameters: fp32 arithmetic, RNE store). */
 mco_status mco_adalomo_apply(mco_adalomo* h, int tensor_index, void* param, int param_dtype,
                              const void* grad, int grad_dtype, double lr,
                              const double* dev_grad_sumsq, void* stream);

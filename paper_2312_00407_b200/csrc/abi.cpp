@@ -699,8 +699,11 @@ mco_status mco_adalomo_destroy(mco_adalomo* h) {
 
 namespace {
 void check_ada_dtypes(int pdt, int gdt) {
-  if (pdt != MCO_F32 || (gdt != MCO_F32 && gdt != MCO_BF16))
-    throw Error(MCO_CONTRACT, "adalomo: params must be f32 and grads f32 or bf16");
+  const bool ok = (pdt == MCO_F32 && (gdt == MCO_F32 || gdt == MCO_BF16)) ||
+                  (pdt == MCO_BF16 && gdt == MCO_BF16);
+  if (!ok)
+    throw Error(MCO_CONTRACT,
+                "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
 }
 }  // namespace
 
@@ -716,6 +719,7 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, cons
     c.t0 = idx;
     c.t1 = idx + 1;
     c.p = param;
+    c.p_dtype = pdt;
     c.g = grad;
     c.g_dtype = gdt;
     c.single = 1;
@@ -736,6 +740,7 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
     c.t0 = 0;
     c.t1 = (int)h->plan.h_tensors.size();
     c.p = flat_p;
+    c.p_dtype = pdt;
     c.g = flat_g;
     c.g_dtype = gdt;
     c.single = 0;
@@ -760,7 +765,7 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
     const int nt = (int)pl.h_tensors.size();
     const uint64_t total = nt ? (uint64_t)(pl.h_tensors.back().elem_off +
                                            pl.h_tensors.back().numel) : 0;
-    const size_t gs = dtype_size(gdt);
+    const size_t gs = dtype_size(gdt), ps = dtype_size(pdt);
     if (!h->hp) {
       MCO_CUDA_CHECK(cudaMalloc(&h->hp, std::max<uint64_t>(total, 1) * 4));
       MCO_CUDA_CHECK(cudaMalloc(&h->hg, std::max<uint64_t>(total, 1) * 4));
@@ -774,10 +779,11 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
     }
     cudaStream_t up = h->hst[0], comp = h->hst[1], down = h->hst[2];
     AdaLomoCall c{};
+    c.p_dtype = pdt;
     c.g_dtype = gdt;
     c.lr = lr;
     if (pl.cfg.has_clip_threshold) {
-      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hp, p, total * 4, cudaMemcpyHostToDevice, up));
+      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hp, p, total * ps, cudaMemcpyHostToDevice, up));
       MCO_CUDA_CHECK(cudaMemcpyAsync(h->hg, g, total * gs, cudaMemcpyHostToDevice, up));
       MCO_CUDA_CHECK(cudaStreamSynchronize(up));
       c.t0 = 0;
@@ -788,14 +794,15 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
       c.use_clip = 1;
       launch_adalomo(pl, c, comp);
       MCO_CUDA_CHECK(cudaStreamSynchronize(comp));
-      MCO_CUDA_CHECK(cudaMemcpyAsync(p, h->hp, total * 4, cudaMemcpyDeviceToHost, down));
+      MCO_CUDA_CHECK(cudaMemcpyAsync(p, h->hp, total * ps, cudaMemcpyDeviceToHost, down));
     } else {
       for (int k = 0; k < nt; ++k) {
         const TensorInfo& T = pl.h_tensors[k];
         const uint64_t off = (uint64_t)T.elem_off, n = (uint64_t)T.numel;
-        float* dp = h->hp + off;
+        char* dp = (char*)h->hp + off * ps;
         char* dgp = (char*)h->hg + off * gs;
-        MCO_CUDA_CHECK(cudaMemcpyAsync(dp, (const float*)p + off, n * 4, cudaMemcpyHostToDevice, up));
+        MCO_CUDA_CHECK(cudaMemcpyAsync(dp, (const char*)p + off * ps, n * ps,
+                                       cudaMemcpyHostToDevice, up));
         MCO_CUDA_CHECK(cudaMemcpyAsync(dgp, (const char*)g + off * gs, n * gs,
                                        cudaMemcpyHostToDevice, up));
         MCO_CUDA_CHECK(cudaEventRecord(h->ev_in[k], up));
@@ -809,7 +816,8 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
         launch_adalomo(pl, c, comp);
         MCO_CUDA_CHECK(cudaEventRecord(h->ev_out[k], comp));
         MCO_CUDA_CHECK(cudaStreamWaitEvent(down, h->ev_out[k], 0));
-        MCO_CUDA_CHECK(cudaMemcpyAsync((float*)p + off, dp, n * 4, cudaMemcpyDeviceToHost, down));
+        MCO_CUDA_CHECK(cudaMemcpyAsync((char*)p + off * ps, dp, n * ps, cudaMemcpyDeviceToHost,
+                                       down));
       }
     }
     for (auto st : h->hst) MCO_CUDA_CHECK(cudaStreamSynchronize(st));
@@ -854,6 +862,7 @@ mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_p, int pdt,
     c.t0 = 0;
     c.t1 = (int)h->plan.h_tensors.size();
     c.p = flat_p;
+    c.p_dtype = pdt;
     c.g = flat_g;
     c.g_dtype = gdt;
     c.single = 0;

@@ -43,6 +43,12 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kRB = 2;   // K1 / K6 tiles: rows per thread per loop iteration (loads in flight)
+// bf16 parameters and gradients move half the bytes per row: twice the rows in flight
+// (ncu, bf16 at kRB: K1 / K6 stalled on long_scoreboard at ~30 % issue, 0.5 of copy BW)
+template <typename GT, typename PT>
+constexpr int rows_in_flight() {
+  return (sizeof(GT) == 2 && sizeof(PT) == 2) ? 2 * kRB : kRB;
+}
 #ifndef MCO_K1_MINB
 #define MCO_K1_MINB 3
 #endif
@@ -99,32 +105,98 @@ __device__ __forceinline__ void load_vec(const GT* g, float (&r)[VW], int valid)
 #pragma unroll
   for (int j = 0; j < VW; ++j) r[j] = j < valid ? ld1(g + j) : 0.f;
 }
-template <bool VEC>
-__device__ __forceinline__ void load_p(const float* p, float (&r)[VW], int valid) {
+// Parameters: fp32, or bf16 storage (fp32 arithmetic, RNE store -- the fp32 result
+// rounded once, as LOMO's bf16 path).
+__device__ __forceinline__ float ldp1(const float* p) { return *p; }
+__device__ __forceinline__ float ldp1(const uint16_t* p) { return bf2f(*p); }
+__device__ __forceinline__ void stp1(float* p, float v) { *p = v; }
+__device__ __forceinline__ void stp1(uint16_t* p, float v) { *p = (uint16_t)f2bf_bits(v); }
+
+template <bool VEC, typename PT>
+__device__ __forceinline__ void load_p(const PT* p, float (&r)[VW], int valid) {
   if constexpr (VEC) {
     if (valid == VW) {
-      ld_stream(p, r);
+      if constexpr (sizeof(PT) == 4)
+        ld_stream(p, r);
+      else
+        ld_stream_bf16x8(p, r);
       return;
     }
   }
 #pragma unroll
-  for (int j = 0; j < VW; ++j) r[j] = j < valid ? p[j] : 0.f;
+  for (int j = 0; j < VW; ++j) r[j] = j < valid ? ldp1(p + j) : 0.f;
 }
-template <bool VEC>
-__device__ __forceinline__ void store_p(float* p, const float (&r)[VW], int valid) {
+template <bool VEC, typename PT>
+__device__ __forceinline__ void store_p(PT* p, const float (&r)[VW], int valid) {
   if constexpr (VEC) {
     if (valid == VW) {
-      st_stream(p, r);
+      if constexpr (sizeof(PT) == 4)
+        st_stream(p, r);
+      else
+        st_stream_bf16x8(p, r);
       return;
     }
   }
 #pragma unroll
   for (int j = 0; j < VW; ++j)
-    if (j < valid) p[j] = r[j];
+    if (j < valid) stp1(p + j, r[j]);
 }
 
+// One lane's 8-column chunk of one row, held in load form until it is consumed: fp32
+// as 8 floats, bf16 as the 4 raw 32-bit words (half the registers), so the bf16 tile
+// kernels can keep twice the rows in flight (rows_in_flight) without spilling.
+template <bool VEC, typename T, bool RO>
+struct RowVec {
+  float v[VW];
+  __device__ __forceinline__ void load(const T* src, int valid) {
+    if constexpr (RO)
+      load_vec<VEC, T>(src, v, valid);
+    else
+      load_p<VEC, T>(src, v, valid);
+  }
+  __device__ __forceinline__ void get(float (&r)[VW]) const {
+#pragma unroll
+    for (int j = 0; j < VW; ++j) r[j] = v[j];
+  }
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int j = 0; j < VW; ++j) v[j] = 0.f;
+  }
+};
+template <bool VEC, bool RO>
+struct RowVec<VEC, uint16_t, RO> {
+  uint32_t w[4];
+  __device__ __forceinline__ void load(const uint16_t* src, int valid) {
+    if (VEC && valid == VW) {
+      if constexpr (RO)
+        asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "l"(src));
+      else
+        asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                     : "l"(src));
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t lo = 2 * k < valid ? src[2 * k] : 0u;
+      const uint32_t hi = 2 * k + 1 < valid ? src[2 * k + 1] : 0u;
+      w[k] = lo | (hi << 16);
+    }
+  }
+  __device__ __forceinline__ void get(float (&r)[VW]) const {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      r[2 * k] = __uint_as_float(w[k] << 16);
+      r[2 * k + 1] = __uint_as_float(w[k] & 0xffff0000u);
+    }
+  }
+  __device__ __forceinline__ void zero() { w[0] = w[1] = w[2] = w[3] = 0u; }
+};
+
 struct Ptrs {
-  float* p;
+  void* p;
   const void* g;
   int single;  // 1: p / g point at the call's only tensor
 };
@@ -132,12 +204,13 @@ template <typename GT>
 __device__ __forceinline__ const GT* gptr(const Ptrs& P, const TensorInfo& T) {
   return (const GT*)P.g + (P.single ? 0 : T.elem_off);
 }
-__device__ __forceinline__ float* pptr(const Ptrs& P, const TensorInfo& T) {
-  return P.p + (P.single ? 0 : T.elem_off);
+template <typename PT>
+__device__ __forceinline__ PT* pptr(const Ptrs& P, const TensorInfo& T) {
+  return (PT*)P.p + (P.single ? 0 : T.elem_off);
 }
 
 // ============================ K1: statistics =====================================
-template <bool VEC, typename GT>
+template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads, kMinCtasK1)
     k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles) {
   pdl_wait();
@@ -148,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK1)
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
     const GT* g = gptr<GT>(P, T);
-    const float* p = pptr(P, T);
+    const PT* p = pptr<PT>(P, T);
     double psq = 0.0, gsq = 0.0;
     if (T.factored) {
       const int TC = T.tc, TR = kThreads / T.tc;
@@ -161,29 +234,34 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK1)
 #pragma unroll
       for (int j = 0; j < VW; ++j) cacc[j] = 0.f;
       // RB rows per iteration: all their loads are in flight before any math
-      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB * TR) {
-        float gv[kRB][VW], pv[kRB][VW];
+      constexpr int RB = rows_in_flight<GT, PT>();
+      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
+        RowVec<VEC, GT, true> gr[RB];
+        RowVec<VEC, PT, false> pr[RB];
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
+        for (int b = 0; b < RB; ++b) {
           const int64_t r = r0 + (int64_t)b * TR;
           if (valid > 0 && r < tl.r1) {
-            load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
-            load_p<VEC>(p + r * T.cols + col, pv[b], valid);
+            gr[b].load(g + r * T.cols + col, valid);
+            pr[b].load(p + r * T.cols + col, valid);
           } else {
-#pragma unroll
-            for (int j = 0; j < VW; ++j) gv[b][j] = pv[b][j] = 0.f;
+            gr[b].zero();
+            pr[b].zero();
           }
         }
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
+        for (int b = 0; b < RB; ++b) {
           const int64_t r = r0 + (int64_t)b * TR;
+          float gv[VW], pv[VW];
+          gr[b].get(gv);
+          pr[b].get(pv);
           float sg = 0.f, sp = 0.f;
 #pragma unroll
           for (int j = 0; j < VW; ++j) {
-            const float g2 = gv[b][j] * gv[b][j];
+            const float g2 = gv[j] * gv[j];
             cacc[j] += g2;
             sg += g2;
-            sp += pv[b][j] * pv[b][j];
+            sp += pv[j] * pv[j];
           }
           psq += (double)sp;
           sg = warp_sum(sg);  // a warp never straddles two rows (TC >= 32)
@@ -222,7 +300,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK1)
       __syncthreads();  // colbuf / rowbuf reuse by the next tile
     } else {
       for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
-        const double gv = (double)ld1(g + e), pv = (double)p[e];
+        const double gv = (double)ld1(g + e), pv = (double)ldp1(p + e);
         gsq += gv * gv;
         psq += pv * pv;
       }
@@ -541,7 +619,7 @@ __global__ void __launch_bounds__(1024)
 }
 
 // ============================ K6: update ==============================================
-template <bool VEC, typename GT>
+template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads)
     k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps) {
   pdl_wait();
@@ -552,7 +630,7 @@ __global__ void __launch_bounds__(kThreads)
     const Chunk ch = c.chunks[chunk0 + ci];
     const TensorInfo T = c.tensors[ch.tensor];
     const GT* g = gptr<GT>(P, T);
-    float* p = pptr(P, T);
+    PT* p = pptr<PT>(P, T);
     const double f = c.tens_sc[ch.tensor * kTensScalars + TS_F];
     if (T.factored) {
       const float ff = (float)f;
@@ -568,12 +646,7 @@ __global__ void __launch_bounds__(kThreads)
           const int64_t e = base + (int64_t)u * kThreads * VW;
           if (e < ch.e1) {
             chunk_vec_load<VEC, GT>(g, e, ch.e1, gv[u]);
-            if constexpr (VEC) {
-              ld_stream(p + e, pv[u]);
-            } else {
-#pragma unroll
-              for (int j = 0; j < VW; ++j) pv[u][j] = (e + j < ch.e1) ? p[e + j] : 0.f;
-            }
+            load_p<VEC, PT>(p + e, pv[u], (int)std::min<int64_t>(VW, ch.e1 - e));
           }
         }
 #pragma unroll
@@ -589,7 +662,7 @@ __global__ void __launch_bounds__(kThreads)
               const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
               for (int j = 0; j < VW; ++j) pv[u][j] = pv[u][j] - ff * u_fact(gv[u][j], sf, a, bv[j], epsf);
-              st_stream(p + e, pv[u]);
+              store_p<VEC, PT>(p + e, pv[u], VW);
             } else {
 #pragma unroll
               for (int j = 0; j < VW; ++j) {
@@ -597,7 +670,7 @@ __global__ void __launch_bounds__(kThreads)
                 if (ej < ch.e1) {
                   uint32_t row, col;
                   row_col((uint32_t)ej, T, C, row, col);
-                  p[ej] = pv[u][j] - ff * u_fact(gv[u][j], sf, fa[row], fb[col], epsf);
+                  stp1(p + ej, pv[u][j] - ff * u_fact(gv[u][j], sf, fa[row], fb[col], epsf));
                 }
               }
             }
@@ -610,14 +683,14 @@ __global__ void __launch_bounds__(kThreads)
       for (int64_t e = ch.e0 + threadIdx.x; e < ch.e1; e += kThreads) {
         const double gs = s * (double)ld1(g + e);
         const double u = gs / sqrt(c.state[T.vfull_off + e] / corr + eps);
-        p[e] = (float)((double)p[e] - f * u);
+        stp1(p + e, (float)((double)ldp1(p + e) - f * u));
       }
     }
   }
 }
 
 // K6 over the statistics tiles (alternative traversal; identical arithmetic and result)
-template <bool VEC, typename GT>
+template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads)
     k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
   pdl_wait();
@@ -628,7 +701,7 @@ __global__ void __launch_bounds__(kThreads)
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
     const GT* g = gptr<GT>(P, T);
-    float* p = pptr(P, T);
+    PT* p = pptr<PT>(P, T);
     const double f = c.tens_sc[tl.tensor * kTensScalars + TS_F];
     if (T.factored) {
       const float ff = (float)f;
@@ -640,25 +713,29 @@ __global__ void __launch_bounds__(kThreads)
       float bv[VW];
 #pragma unroll
       for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
-      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)kRB * TR) {
-        float gv[kRB][VW], pv[kRB][VW];
+      constexpr int RB = rows_in_flight<GT, PT>();
+      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
+        RowVec<VEC, GT, true> gr[RB];
+        RowVec<VEC, PT, false> pr[RB];
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
+        for (int b = 0; b < RB; ++b) {
           const int64_t r = r0 + (int64_t)b * TR;
           if (r < tl.r1) {
-            load_vec<VEC, GT>(g + r * T.cols + col, gv[b], valid);
-            load_p<VEC>(p + r * T.cols + col, pv[b], valid);
+            gr[b].load(g + r * T.cols + col, valid);
+            pr[b].load(p + r * T.cols + col, valid);
           }
         }
 #pragma unroll
-        for (int b = 0; b < kRB; ++b) {
+        for (int b = 0; b < RB; ++b) {
           const int64_t r = r0 + (int64_t)b * TR;
           if (r < tl.r1) {
             const float a = c.fa[T.fa_off + r];
+            float gv[VW], pv[VW];
+            gr[b].get(gv);
+            pr[b].get(pv);
 #pragma unroll
-            for (int j = 0; j < VW; ++j)
-              pv[b][j] = pv[b][j] - ff * u_fact(gv[b][j], sf, a, bv[j], epsf);
-            store_p<VEC>(p + r * T.cols + col, pv[b], valid);
+            for (int j = 0; j < VW; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
+            store_p<VEC, PT>(p + r * T.cols + col, pv, valid);
           }
         }
       }
@@ -668,7 +745,7 @@ __global__ void __launch_bounds__(kThreads)
       for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
         const double gs = s * (double)ld1(g + e);
         const double u = gs / sqrt(c.state[T.vfull_off + e] / corr + eps);
-        p[e] = (float)((double)p[e] - f * u);
+        stp1(p + e, (float)((double)ldp1(p + e) - f * u));
       }
     }
   }
@@ -698,13 +775,13 @@ int grid_for(K kernel, int64_t ntiles, int device) {
   return (int)std::max<int64_t>(1, (ntiles + rounds - 1) / rounds);
 }
 
-template <bool VEC, typename GT>
+template <bool VEC, typename GT, typename PT>
 void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaStream_t st) {
   Ctx c{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
         pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
         pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
         pl.d_chunks,  pl.d_chunk_sc};
-  Ptrs P{(float*)call.p, call.g, call.single};
+  Ptrs P{call.p, call.g, call.single};
   const int dev = current_device();
   const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
   const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
@@ -714,7 +791,7 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
   const int64_t sms = device_info(dev).sms;
 
   if (phase == 1) {  // pass 1 over {g, p} + reduction of the tile partials into the payload
-    auto kk1 = k1_stats<VEC, GT>;
+    auto kk1 = k1_stats<VEC, GT, PT>;
     launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles);
     launch_check("adalomo k1_stats");
     const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
@@ -751,10 +828,10 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
       return !(e && std::string(e) == "chunks");
     }();
     if (k6_tiles) {
-      auto kk6 = k6_update_tiles<VEC, GT>;
+      auto kk6 = k6_update_tiles<VEC, GT, PT>;
       launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps);
     } else {
-      auto kk6 = k6_update<VEC, GT>;
+      auto kk6 = k6_update<VEC, GT, PT>;
       launch_pdl(kk6, grid_for(kk6, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.eps);
     }
     launch_check("adalomo k6_update");
@@ -766,29 +843,30 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
 void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase,
                           cudaStream_t st) {
   if (call.t1 <= call.t0) return;
-  // 256-bit path: every factored tensor in the call has C % 8 == 0 and 32 B
-  // (f32) / 16 B (bf16) aligned rows.
+  // vector path: every factored tensor in the call has C % 8 == 0 and rows aligned to
+  // 8 elements of their type (32 B f32, 16 B bf16) for both params and grads.
   const size_t gsz = call.g_dtype == MCO_BF16 ? 2 : 4;
+  const size_t psz = call.p_dtype == MCO_BF16 ? 2 : 4;
   bool vec = true;
   for (int k = call.t0; k < call.t1 && vec; ++k) {
     const TensorInfo& T = pl.h_tensors[k];
     if (!T.factored) continue;
     const int64_t off = call.single ? 0 : T.elem_off;
-    vec = (T.cols % 8 == 0) && (((uintptr_t)call.p + off * 4) % 32 == 0) &&
+    vec = (T.cols % 8 == 0) && (((uintptr_t)call.p + off * psz) % (8 * psz) == 0) &&
           (((uintptr_t)call.g + off * gsz) % (8 * gsz) == 0);
   }
-  if (call.g_dtype == MCO_F32) {
-    if (vec)
-      run_phase<true, float>(pl, call, phase, st);
-    else
-      run_phase<false, float>(pl, call, phase, st);
-  } else if (call.g_dtype == MCO_BF16) {
-    if (vec)
-      run_phase<true, uint16_t>(pl, call, phase, st);
-    else
-      run_phase<false, uint16_t>(pl, call, phase, st);
+  // (params, grads): (f32, f32), (f32, bf16), (bf16, bf16)
+  if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_F32) {
+    vec ? run_phase<true, float, float>(pl, call, phase, st)
+        : run_phase<false, float, float>(pl, call, phase, st);
+  } else if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_BF16) {
+    vec ? run_phase<true, uint16_t, float>(pl, call, phase, st)
+        : run_phase<false, uint16_t, float>(pl, call, phase, st);
+  } else if (call.p_dtype == MCO_BF16 && call.g_dtype == MCO_BF16) {
+    vec ? run_phase<true, uint16_t, uint16_t>(pl, call, phase, st)
+        : run_phase<false, uint16_t, uint16_t>(pl, call, phase, st);
   } else {
-    throw Error(MCO_CONTRACT, "adalomo: grads must be f32 or bf16");
+    throw Error(MCO_CONTRACT, "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
   }
 }
 

@@ -78,6 +78,7 @@ struct AdaLomoPlan {
 struct AdaLomoCall {
   int t0, t1;  // tensor range [t0, t1)
   void* p;
+  int p_dtype;  // MCO_F32 or MCO_BF16 (bf16 storage: fp32 arithmetic, RNE store)
   const void* g;
   int g_dtype;
   int single;

@@ -277,6 +277,48 @@ def test_adalomo_bf16_grads_and_determinism():
     assert np.all(np.isfinite(outs[0]))
 
 
+@pytest.mark.parametrize("clip", [None, 0.5])
+def test_adalomo_bf16_params_round_the_f32_result(clip):
+    """bf16 parameter storage (C5-style memory; fp32 arithmetic, RNE store): one step
+    gives exactly RNE_bf16 of the fp32-parameter step on the same (bf16-valued) inputs,
+    multi-tensor and hook forms; shapes include 1-D tensors and a column count that is
+    not a multiple of 8 (scalar path)."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    if clip is not None:
+        cfg.clip_threshold = clip
+    shapes = registry.CONFIG1.shapes()[:10] + [(37, 29), (5,)]
+    n = sum(int(np.prod(s)) for s in shapes)
+    g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    p32 = torch.empty(n, device="cuda")
+    registry.fill_grads(g, shapes, 1)
+    registry.fill_params(p32, shapes)
+    p32 = p32.to(torch.bfloat16).float()  # bf16-representable starting point
+    pb = p32.to(torch.bfloat16)
+    qa, qb = p32.clone(), pb.clone()  # the hook form starts from the same point
+    sa, sb = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    sa.apply_all(p32, g, 1e-3)
+    sb.apply_all(pb, g, 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(p32.to(torch.bfloat16).view(torch.int16), pb.view(torch.int16))
+    assert not torch.equal(pb.float(), p32)  # a real rounding happened somewhere
+    if clip is None:  # hook form, one tensor at a time
+        offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+        ha, hb = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+        for k in reversed(range(len(shapes))):
+            a, b = int(offs[k]), int(offs[k + 1])
+            ha.apply(k, qa[a:b], g[a:b], 1e-3)
+            hb.apply(k, qb[a:b], g[a:b], 1e-3)
+        torch.cuda.synchronize()
+        assert torch.equal(qa.to(torch.bfloat16).view(torch.int16), qb.view(torch.int16))
+
+
+def test_adalomo_rejects_bf16_params_with_f32_grads():
+    st = optim.AdaLomoState(OptimizerConfig.defaults_for(Kind.ADALOMO), [(8, 8)])
+    with pytest.raises(optim.ContractError, match="bf16 / bf16"):
+        st.apply_all(torch.zeros(64, dtype=torch.bfloat16, device="cuda"),
+                     torch.zeros(64, device="cuda"), 1e-3)
+
+
 @needs_ref
 def test_adalomo_config1_registry_vs_reference():
     """All 75 tensors of configuration 1 (10.5M params) through apply_all, 2 steps."""

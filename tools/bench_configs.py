@@ -57,7 +57,7 @@ def main():
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     W, K = 2, 5
-    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks"]
+    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks", "bf16"]
 
     if "c3" in which:
         m = registry.LLAMA_13B
@@ -114,6 +114,31 @@ def main():
 
     if "hooks" in which:
         hooks_7b(W, K)
+
+    if "bf16" in which:  # AdaLomo on bf16 parameters and gradients (12 B/param)
+        m = registry.LLAMA_7B
+        shapes, n = m.shapes(), m.param_count()
+        p = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+        tmp = torch.empty(n // 4 + 1, device="cuda")
+        off = 0  # fp32 synthetic values, rounded to bf16, a slice at a time
+        for k, s_ in enumerate(shapes):
+            cnt = int(torch.tensor(s_).prod())
+            for a in range(0, cnt, tmp.numel()):
+                b = min(cnt, a + tmp.numel())
+                t = tmp[:b - a]
+                if len(s_) == 2:
+                    optim.synth_fill(t, registry.SEED, 0, k, 0, 0, -6)
+                else:
+                    t.fill_(1.0)
+                p[off + a:off + b].copy_(t)
+            off += cnt
+        registry.fill_grads(g, shapes, 1)
+        del tmp
+        cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+        st = optim.AdaLomoState(cfg, shapes)
+        ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
+        line("adalomo bf16 params + bf16 grads, llama-7b", n, ms, 12)
 
 
 def hooks_7b(W, K):
