@@ -115,7 +115,9 @@ class OverlappedZeroOptimizer:
                 for r, a, b in ps:
                     if r == self.rank:
                         self._opt[(a, b)] = optim.FlatOptimizer(cfg, b - a, device=dev.index)
-        self._side = torch.cuda.Stream(dev) if dev.type == "cuda" else None
+        # high-priority side stream: bucket updates are scheduled ahead of queued backward
+        # CTAs, so they overlap instead of waiting for a gap in the compute stream
+        self._side = torch.cuda.Stream(dev, priority=-1) if dev.type == "cuda" else None
         self._ready = [0] * len(self.buckets)
         self._next = 0
         self._lr = None
