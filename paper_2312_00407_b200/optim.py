@@ -254,6 +254,7 @@ class FlatOptimizer:
         self._sd = {"f32": MCO_F32, "f64": MCO_F64}[state_dtype]
         h = C.c_void_p()
         self.device = _device(device)
+        self._destroy = lib.mco_flat_destroy  # kept: module globals vanish at shutdown
         _check(lib.mco_flat_create(C.byref(cfg._to_c()), self._n, self.device, self._sd,
                                    C.byref(h)))
         self._h = h
@@ -261,7 +262,7 @@ class FlatOptimizer:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib.mco_flat_destroy(h)
+            self._destroy(h)
             self._h = None
 
     def step(self, params, grads, lr: float, stream=None) -> None:
@@ -415,6 +416,7 @@ class AdaLomoState:
         nd, dims = _shape_arrays(self.shapes)
         h = C.c_void_p()
         self.device = _device(device)
+        self._destroy = lib.mco_adalomo_destroy
         _check(lib.mco_adalomo_create(C.byref(cfg._to_c()), len(self.shapes), nd, dims,
                                       self.device, C.byref(h)))
         self._h = h
@@ -422,7 +424,7 @@ class AdaLomoState:
     def __del__(self):
         h = getattr(self, "_h", None)
         if h:
-            lib.mco_adalomo_destroy(h)
+            self._destroy(h)
             self._h = None
 
     def apply(self, index: int, param, grad, lr: float, grad_sumsq=None, stream=None) -> None:

@@ -244,6 +244,7 @@ class _PeerBuffer:
 
         self.numel, self.dtype, self.device = numel, dtype, device
         self.esize = {"float32": 4, "bfloat16": 2}[str(dtype).split(".")[-1]]
+        self._free = lib.mco_peer_free  # kept: module globals vanish at shutdown
         p = C.c_void_p()
         optim._check(lib.mco_peer_alloc(numel * self.esize, device, C.byref(p)))
         self.ptr = p.value
@@ -267,10 +268,8 @@ class _PeerBuffer:
         return bytes(buf)
 
     def __del__(self):
-        from ._lib import lib
-
         if getattr(self, "ptr", None):
-            lib.mco_peer_free(self.ptr)
+            self._free(self.ptr)
             self.ptr = None
 
 
@@ -313,6 +312,7 @@ class PeerBuffers:
         else:
             allh = [mine]
         self._opened = []
+        self._close = lib.mco_peer_close
         self.pptrs, self.gptrs = [], []
         for r, (ph, gh) in enumerate(allh):
             if r == self.rank:
@@ -343,10 +343,9 @@ class PeerBuffers:
             dist.barrier(group=self.group)
 
     def __del__(self):
-        from ._lib import lib
-
+        close = getattr(self, "_close", None)
         for p in getattr(self, "_opened", []):
-            lib.mco_peer_close(p)
+            close(p)
 
 
 class PeerShardedOptimizer:
@@ -532,6 +531,7 @@ class NcclComm:
             dist.broadcast_object_list(box, src=src, group=group)
             C.memmove(uid, box[0], 128)
         h = C.c_void_p()
+        self._destroy = lib.mco_comm_destroy
         optim._check(lib.mco_comm_create(uid, self.world, self.rank, optim._device(device),
                                          C.byref(h)))
         self._h = h
@@ -548,11 +548,9 @@ class NcclComm:
         optim._check(lib.mco_comm_check(self._h))
 
     def __del__(self):
-        from ._lib import lib
-
         h = getattr(self, "_h", None)
         if h:
-            lib.mco_comm_destroy(h)
+            self._destroy(h)
             self._h = None
 
 
