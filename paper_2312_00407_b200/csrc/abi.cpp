@@ -110,6 +110,22 @@ void validate(const mco_config& c) {
 
 // Per-step scalars (optim.cpp:116-117, 138-141, 159): double on the host, one
 // rounding to the kernel's type.  Identical rule in oracle/mco_oracle.c.
+// sqrt_plus_eps (update.cuh): the largest x with RN(sqrt(RN(x / c)) + eps) == eps
+// guaranteed, (ulp(eps)/4)^2 * c rounded down; fp32 only (0 = no shortcut).
+template <typename T>
+T sqrt_eps_threshold(T eps, T c) {
+  if constexpr (sizeof(T) == 4) {
+    if (!(eps > 0) || !std::isnormal(eps) || !(c > 0)) return 0;
+    const double q = ((double)std::nextafter(eps, INFINITY) - (double)eps) / 4.0;
+    const double thr = q * q * (double)c;
+    float f = (float)thr;
+    if ((double)f > thr) f = std::nextafter(f, 0.0f);
+    return f;
+  } else {
+    return 0;
+  }
+}
+
 template <typename T>
 StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
   StepConsts<T> k{};
@@ -128,6 +144,7 @@ StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
   k.lrwd = (T)(lr * c.weight_decay);
   k.den = (T)(1.0 + lr * c.weight_decay);
   k.rho = (T)c.sophia_rho;
+  k.sthr = sqrt_eps_threshold<T>(k.eps, c.kind == MCO_ADAN ? k.c3 : k.c2);
   k.first = t == 1 ? 1 : 0;
   k.refresh = ((t - 1) % c.update_interval) == 0 ? 1 : 0;
   return k;

@@ -74,6 +74,7 @@ template <typename T>
 struct StepConsts {
   T b1, b2, b3, omb1, omb2, omb3;  // beta_k and (1 - beta_k)
   T c1, c2, c3;                    // 1 - beta_k^t
+  T sthr;                          // sqrt_plus_eps threshold (AdamW: c2, Adan: c3; 0 = off)
   T lr, eps, wd, lrwd, den, rho;   // den = 1 + lr*wd (Adan), lrwd = lr*wd (Sophia)
   int first;                       // Adan: t == 1
   int refresh;                     // Sophia: (t-1) % k == 0

@@ -12,6 +12,20 @@ enum { K_ADAMW = 0, K_LION = 1, K_ADAN = 2, K_SOPHIA = 3 };
 __device__ __forceinline__ float dsqrt(float x) { return sqrtf(x); }
 __device__ __forceinline__ double dsqrt(double x) { return sqrt(x); }
 
+// sqrt(x / c) + eps, bit-identical to the plain expression, without the IEEE slow paths
+// of div.rn / sqrt.rn on tiny x (an EMA of squared gradients below ~1e-19 is
+// subnormal: AdamW / Adan ran 2x slower).  thr (host, make_consts) = (ulp(eps)/4)^2 * c,
+// so x < thr gives RN(sqrt(RN(x / c))) <= ulp(eps)/4 and the sum rounds back to eps;
+// a normal stand-in keeps the unselected division and square root on the fast path.
+__device__ __forceinline__ float sqrt_plus_eps(float x, float c, float eps, float thr) {
+  const bool tiny = x < thr;
+  const float r = dsqrt((tiny ? c : x) / c) + eps;
+  return tiny ? eps : r;
+}
+__device__ __forceinline__ double sqrt_plus_eps(double x, double c, double eps, double) {
+  return dsqrt(x / c) + eps;
+}
+
 // The per-element update, operation for operation as optim.cpp.
 template <int KIND, typename T>
 __device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
@@ -20,8 +34,7 @@ __device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
     a = k.b1 * a + k.omb1 * g;
     b = k.b2 * b + k.omb2 * g * g;
     const T mhat = a / k.c1;
-    const T vhat = b / k.c2;
-    p = p - k.lr * (mhat / (dsqrt(vhat) + k.eps) + k.wd * p);
+    p = p - k.lr * (mhat / sqrt_plus_eps(b, k.c2, k.eps, k.sthr) + k.wd * p);
   } else if constexpr (KIND == K_LION) {  // optim.cpp:129-134; a = m
     const T u = k.b1 * a + k.omb1 * g;
     const T s = u > T(0) ? T(1) : (u < T(0) ? T(-1) : T(0));  // sign(0) = 0
@@ -35,8 +48,7 @@ __device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
     c = k.b3 * c + k.omb3 * nu * nu;
     const T mhat = a / k.c1;
     const T vhat = b / k.c2;
-    const T nhat = c / k.c3;
-    p = (p - k.lr * (mhat + k.b2 * vhat) / (dsqrt(nhat) + k.eps)) / k.den;
+    p = (p - k.lr * (mhat + k.b2 * vhat) / sqrt_plus_eps(c, k.c3, k.eps, k.sthr)) / k.den;
     d = g;
   } else {  // K_SOPHIA, optim.cpp:160-166; a = m, b = h
     a = k.b1 * a + k.omb1 * g;

@@ -267,3 +267,27 @@ def test_kernel_variants_bit_exact(flat_variant, variant, kind, n):
     for name, t in opt.buffers():
         assert bits_equal(t.cpu().numpy(), orc.state[name]), name
 
+
+
+@pytest.mark.parametrize("variant", ["tma", "ldg"])
+@pytest.mark.parametrize("kind", FLAT)
+@pytest.mark.parametrize("g_log2", [-66, -100, -130])
+def test_tiny_gradients_bit_exact(flat_variant, variant, kind, g_log2):
+    """Gradients of 2^-66 .. 2^-130 (squares and EMAs subnormal, g itself subnormal at
+    the end): the subnormal-safe sqrt(x/c) + eps keeps the restatement's bits while
+    avoiding the IEEE slow paths."""
+    flat_variant(variant)
+    n = (1 << 20) + 5
+    cfg = cfg_for(kind, weight_decay=0.01)
+    p = O.synth(n, 31, 0, 4, 0, 0, -6, 0, False)
+    tp = dev(p)
+    opt = optim.FlatOptimizer(cfg, n)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    for t in range(1, 4):
+        g = O.synth(n, 31, 1, 4, t, 0, g_log2, 10, False)
+        opt.step(tp, dev(g), 1e-3)
+        orc.step(p, g, 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    for name, t in opt.buffers():
+        assert bits_equal(t.cpu().numpy(), orc.state[name]), name
