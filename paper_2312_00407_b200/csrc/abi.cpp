@@ -244,9 +244,12 @@ struct mco_flat {
   int state_dtype = MCO_F32;
   int64_t t = 0;
   void* slot[4] = {nullptr, nullptr, nullptr, nullptr};  // kernel slots s0..s3
+  void* base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (8 elements slack)
+  int phase = 0;         // slot = base + phase elements (matches the params' phase mod 8)
+  bool exposed = false;  // buffers() handed out: the layout is frozen
   std::vector<std::pair<const char*, void*>> named;       // buffers() order
   ~mco_flat() {
-    for (void* p : slot)
+    for (void* p : base)
       if (p) cudaFree(p);
   }
 };
@@ -368,10 +371,13 @@ mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device
         nslots = 4; break;
       case MCO_SOPHIA: names[0] = "m"; names[1] = "h"; nslots = 2; break;
     }
-    const size_t bytes = std::max<uint64_t>(owned_len, 1) * dtype_size(state_dtype);
+    // 8 elements of slack: the state is shifted to the parameters' alignment phase at
+    // the first step (align_state_to), so shard views at odd offsets stay vectorised
+    const size_t bytes = (std::max<uint64_t>(owned_len, 1) + 8) * dtype_size(state_dtype);
     for (int i = 0; i < nslots; ++i) {
-      MCO_CUDA_CHECK(cudaMalloc(&h->slot[i], bytes));
-      MCO_CUDA_CHECK(cudaMemset(h->slot[i], 0, bytes));
+      MCO_CUDA_CHECK(cudaMalloc(&h->base[i], bytes));
+      MCO_CUDA_CHECK(cudaMemset(h->base[i], 0, bytes));
+      h->slot[i] = h->base[i];
       h->named.emplace_back(names[i], h->slot[i]);
     }
     *out = h.release();
@@ -394,6 +400,23 @@ void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
   if (np > h->n)
     throw Error(MCO_CONTRACT, "optimizer step: " + std::to_string(np) +
                                   " elements exceed the owned state of " + std::to_string(h->n));
+}
+
+// Before the first step (state still all zero, never handed out) the state buffers are
+// shifted within their slack so that state[i] has the same address phase (mod 8
+// elements) as params[i]: the launch can then peel a short head and run the rest
+// aligned (flat.cu, launch_flat_step).
+void align_state_to(mco_flat* h, const void* params) {
+  if (h->exposed || h->t != 0 || !params) return;
+  const size_t es = dtype_size(h->state_dtype);
+  const uintptr_t u = (uintptr_t)params;
+  if (u % es) return;
+  const int want = (int)((u / es) % 8);
+  if (want == h->phase) return;
+  h->phase = want;
+  for (int i = 0; i < 4; ++i)
+    if (h->base[i]) h->slot[i] = (char*)h->base[i] + (size_t)want * es;
+  for (size_t i = 0; i < h->named.size(); ++i) h->named[i].second = h->slot[i];
 }
 
 void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
@@ -431,6 +454,7 @@ mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const 
     check_lengths(h, np, ng);
     check_dtypes(h, pdt, gdt);
     DeviceGuard dg(h->device);
+    align_state_to(h, params);
     ++h->t;  // optim.cpp:104
     flat_launch(h, params, pdt, grads, gdt, nullptr, np, 0, lr, (cudaStream_t)stream);
   });
@@ -444,6 +468,7 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
     if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
     if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
     DeviceGuard dg(h->device);
+    align_state_to(h, master);
     ++h->t;
     flat_launch(h, master, MCO_F32, grads, gdt, pout, n, 0, lr, (cudaStream_t)stream);
   });
@@ -485,6 +510,7 @@ mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, ui
   return guard([&] {
     if (i < 0 || i >= (int)h->named.size())
       throw Error(MCO_CONTRACT, "buffers(): index out of range");
+    h->exposed = true;  // callers may keep the pointer: no more relayout
     *name = h->named[i].first;
     *ptr = h->named[i].second;
     *len = h->n;

@@ -15,6 +15,7 @@
 // variant moves the data.
 #include <algorithm>
 #include <atomic>
+#include <initializer_list>
 #include <cstdlib>
 #include <mutex>
 #include <string>
@@ -545,11 +546,34 @@ void run_sumsq(const void* x, uint64_t n, double* out, int accumulate, double* p
   launch_check("sumsq_kernel");
 }
 
-}  // namespace
+size_t dtype_bytes(int dt) { return dt == MCO_F64 ? 8 : dt == MCO_BF16 ? 2 : 4; }
 
-void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
-                      const StepConsts<double>& kd, cudaStream_t st) {
-  if (a.n == 0) return;
+// Element phase shared by every stream of a launch: (address / element size) mod 8,
+// or -1 when the streams disagree (or one is not element-aligned).  With a common
+// nonzero phase -- a ZeRO shard at an odd element offset, with its state laid out to
+// match (abi.cpp) -- the first 8 - phase elements go to a small launch of their own and
+// the rest starts 32 B-aligned on the vector / TMA paths (else every element of the
+// shard took the scalar path: 2-2.6x slower).
+int common_phase(std::initializer_list<std::pair<const void*, size_t>> ptrs) {
+  int ph = -1;
+  for (const auto& [ptr, es] : ptrs) {
+    if (!ptr) continue;
+    const uintptr_t u = (uintptr_t)ptr;
+    if (u % es) return -1;
+    const int q = (int)((u / es) % 8);
+    if (ph >= 0 && q != ph) return -1;
+    ph = q;
+  }
+  return ph < 0 ? 0 : ph;
+}
+
+template <typename T>
+T* advance(T* ptr, uint64_t elems, size_t es) {
+  return ptr ? (T*)((char*)ptr + elems * es) : nullptr;
+}
+
+void launch_flat_one(const FlatArgs& a, const StepConsts<float>& kf,
+                     const StepConsts<double>& kd, cudaStream_t st) {
   switch (a.kind) {
     case MCO_ADAMW: dispatch_dtypes<K_ADAMW>(a, kf, kd, st); break;
     case MCO_LION: dispatch_dtypes<K_LION>(a, kf, kd, st); break;
@@ -559,9 +583,53 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
   }
 }
 
+void launch_lomo_one(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
+                     double scale, const double* dev_sumsq, double clip, cudaStream_t st);
+
+}  // namespace
+
+void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
+                      const StepConsts<double>& kd, cudaStream_t st) {
+  if (a.n == 0) return;
+  const size_t ps = dtype_bytes(a.p_dtype), gs = dtype_bytes(a.g_dtype),
+               ss = dtype_bytes(a.state_dtype);
+  const int ph = common_phase({{a.p, ps}, {a.g, gs}, {a.s[0], ss}, {a.s[1], ss},
+                               {a.s[2], ss}, {a.s[3], ss}, {a.p_out_bf16, 2}});
+  if (ph <= 0 || a.n <= (uint64_t)(8 - ph)) {
+    launch_flat_one(a, kf, kd, st);
+    return;
+  }
+  const uint64_t head = 8 - ph;
+  FlatArgs h = a, b = a;
+  h.n = head;
+  b.n = a.n - head;
+  b.p = advance(a.p, head, ps);
+  b.g = advance(a.g, head, gs);
+  for (int i = 0; i < 4; ++i) b.s[i] = advance(a.s[i], head, ss);
+  b.p_out_bf16 = advance(a.p_out_bf16, head, 2);
+  launch_flat_one(h, kf, kd, st);
+  launch_flat_one(b, kf, kd, st);
+}
+
 void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
                  double scale, const double* dev_sumsq, double clip, cudaStream_t st) {
   if (n == 0) return;
+  const size_t ps = dtype_bytes(p_dtype), gs = dtype_bytes(g_dtype);
+  const int ph = common_phase({{p, ps}, {g, gs}});
+  if (ph <= 0 || n <= (uint64_t)(8 - ph)) {
+    launch_lomo_one(p, p_dtype, g, g_dtype, n, lr, scale, dev_sumsq, clip, st);
+    return;
+  }
+  const uint64_t head = 8 - ph;
+  launch_lomo_one(p, p_dtype, g, g_dtype, head, lr, scale, dev_sumsq, clip, st);
+  launch_lomo_one(advance(p, head, ps), p_dtype, advance(g, head, gs), g_dtype, n - head, lr,
+                  scale, dev_sumsq, clip, st);
+}
+
+namespace {
+
+void launch_lomo_one(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
+                     double scale, const double* dev_sumsq, double clip, cudaStream_t st) {
   const int variant = flat_variant();
   // LOMO's 16 KB (fp32) stages want 8 in flight (measured: 4 -> 0.95, 8 -> 1.02 of the
   // copy bandwidth); "tma_s3" / "tma_s5" select 4 / 12 for A/B runs
@@ -582,6 +650,8 @@ void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, d
   else
     throw Error(MCO_CONTRACT, "lomo_apply: unsupported param/grad dtype pair");
 }
+
+}  // namespace
 
 size_t sumsq_ws_bytes() { return kSumsqMaxBlocks * sizeof(double) + 256; }
 

@@ -216,7 +216,11 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
     const ncclDataType_t gt = nccl_type(grad_dtype), pt = nccl_type(param_dtype);
     const size_t gs = dt_size(grad_dtype), ps = dt_size(param_dtype);
     DeviceGuard ds(c->device);
-    const size_t need = std::max<size_t>(parts[me] * gs, 256);
+    // reduced gradient in the owned parameter slice's alignment phase (mod 8 elements):
+    // the update then vectorises after a short head (flat.cu launch_flat_step)
+    char* mine = (char*)flat_params + offs[me] * ps;
+    const size_t phase = ((uintptr_t)mine % ps) ? 0 : ((uintptr_t)mine / ps) % 8;
+    const size_t need = (parts[me] + 8) * gs + 256;
     if (c->scratch_bytes < need) {
       if (c->scratch) MCO_CUDA_CHECK(cudaFree(c->scratch));
       c->scratch = nullptr;
@@ -224,21 +228,21 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
       c->scratch_bytes = need;
     }
     auto s = (cudaStream_t)stream;
+    char* gdst = (char*)c->scratch + phase * gs;
     const char* algo = getenv("MCO_SHARD_ALGO");  // "p2p": force the per-part path (tests)
     const bool even = total_len % (uint64_t)N == 0 && !(algo && std::string(algo) == "p2p");
     const auto& api = nccl();
     if (even) {
-      MCO_NCCL_CHECK(api.reduce_scatter(flat_grads, c->scratch, parts[me], gt, ncclSum, c->comm, s));
+      MCO_NCCL_CHECK(api.reduce_scatter(flat_grads, gdst, parts[me], gt, ncclSum, c->comm, s));
     } else {
       MCO_NCCL_CHECK(api.group_start());
       for (int r = 0; r < N; ++r)
-        MCO_NCCL_CHECK(api.reduce((const char*)flat_grads + offs[r] * gs, c->scratch, parts[r], gt,
+        MCO_NCCL_CHECK(api.reduce((const char*)flat_grads + offs[r] * gs, gdst, parts[r], gt,
                                   ncclSum, r, c->comm, s));
       MCO_NCCL_CHECK(api.group_end());
     }
-    char* mine = (char*)flat_params + offs[me] * ps;
-    const mco_status st = mco_flat_step(h, mine, param_dtype, parts[me], c->scratch, grad_dtype, parts[me], lr,
-                       stream);
+    const mco_status st = mco_flat_step(h, mine, param_dtype, parts[me], gdst, grad_dtype,
+                                        parts[me], lr, stream);
     if (st != MCO_OK) throw Error(st, mco_last_error());
     if (even) {
       MCO_NCCL_CHECK(api.all_gather(mine, flat_params, parts[me], pt, c->comm, s));

@@ -73,23 +73,39 @@ class ZeroPlan:
         return len(set(self.part_sizes)) <= 1
 
 
-def reduce_scatter_owned(flat, plan: ZeroPlan, rank: int, group=None):
-    """SUM-reduce `flat` and return this rank's owned slice (comm.cpp:219-246 semantics)."""
+def phased_empty(n: int, dtype, device, phase: int):
+    """An n-element buffer whose first element sits `phase` elements past a 32 B
+    boundary (mod 8 elements): gradients reduced for a shard view at an odd offset share
+    its alignment phase, so the update kernel peels a short head and vectorises the rest
+    (flat.cu launch_flat_step) instead of running every element on the scalar path."""
     import torch
 
+    buf = torch.empty(n + 8, dtype=dtype, device=device)
+    shift = (phase - (buf.data_ptr() // buf.element_size())) % 8
+    return buf[shift:shift + n]
+
+
+def elem_phase(t) -> int:
+    return (t.data_ptr() // t.element_size()) % 8
+
+
+def reduce_scatter_owned(flat, plan: ZeroPlan, rank: int, group=None, phase: int = 0):
+    """SUM-reduce `flat` and return this rank's owned slice (comm.cpp:219-246 semantics),
+    in a buffer of the given alignment phase."""
     dist = _dist()
     lo, hi = plan.owned_range(rank)
     world = len(plan.part_sizes)
     if world == 1:
         return flat[lo:hi]
     if plan.even:
-        out = torch.empty(hi - lo, dtype=flat.dtype, device=flat.device)
+        out = phased_empty(hi - lo, flat.dtype, flat.device, phase)
         dist.reduce_scatter_tensor(out, flat, op=dist.ReduceOp.SUM, group=group)
         return out
     out = None
     for r in range(world):
         a, b = plan.owned_range(r)
-        part = flat[a:b].clone()
+        part = phased_empty(b - a, flat.dtype, flat.device, phase if r == rank else 0)
+        part.copy_(flat[a:b])
         dist.reduce(part, dst=dist.get_global_rank(group, r) if group else r,
                     op=dist.ReduceOp.SUM, group=group)
         if r == rank:
@@ -176,9 +192,19 @@ class ZeroShardedOptimizer:
                 dist = _dist()
                 dist.all_reduce(flat_grads, op=dist.ReduceOp.SUM, group=self.group)
             g_owned = flat_grads[self.lo:self.hi]
-        else:
-            g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group)
         p_owned = flat_params if self.stage == 3 else flat_params[self.lo:self.hi]
+        if (self.mixed and self.master.is_cuda and self._local is None
+                and elem_phase(self.master) != elem_phase(p_owned)):
+            # the fp32 master moves to the bf16 replica slice's alignment phase (once,
+            # before the state takes the master's phase at the first step)
+            m = phased_empty(self.master.numel(), self.master.dtype, self.master.device,
+                             elem_phase(p_owned))
+            m.copy_(self.master)
+            self.master = m
+        if self.stage >= 2:
+            ref = self.master if self.mixed else p_owned
+            g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group,
+                                           phase=elem_phase(ref) if ref.is_cuda else 0)
         if self._local is not None:
             self._local(self.master if self.mixed else p_owned, g_owned, lr,
                         p_owned if self.mixed else None)

@@ -52,8 +52,9 @@ def test_f32_bit_exact_vs_restatement(kind, n):
 
 
 @pytest.mark.parametrize("kind", FLAT)
-def test_unaligned_views_take_scalar_path_bit_exact(kind):
-    """ZeRO shard edges: params / grads at odd element offsets."""
+def test_unaligned_views_bit_exact(kind):
+    """ZeRO shard edges: params / grads at odd element offsets (the state takes their
+    alignment phase at the first step; a short head is peeled, the rest vectorised)."""
     n, off = 10007, 3
     cfg = cfg_for(kind, weight_decay=0.01)
     pbig = O.synth(n + off, 7, 0, 2, 0, 0, -6, 0, False)
@@ -291,3 +292,55 @@ def test_tiny_gradients_bit_exact(flat_variant, variant, kind, g_log2):
     assert bits_equal(tp.cpu().numpy(), p)
     for name, t in opt.buffers():
         assert bits_equal(t.cpu().numpy(), orc.state[name]), name
+
+
+@pytest.mark.parametrize("variant", ["tma", "ldg"])
+@pytest.mark.parametrize("kind", FLAT)
+def test_phase_peeling_cases_bit_exact(flat_variant, variant, kind):
+    """Views at every phase 1..7, mismatched param / grad phases (scalar path), state
+    handed out before the first step (layout frozen), the mixed step with a bf16 replica
+    at an odd offset, and LOMO on views: all give the restatement's bits."""
+    flat_variant(variant)
+    n = 3 * 4096 + 11
+    cfg = cfg_for(kind, weight_decay=0.01)
+    P = O.synth(n + 16, 8, 0, 5, 0, 0, -6, 0, False)
+    G = O.synth(n + 16, 8, 1, 5, 1, 0, -7, 10, False)
+    tP, tG = dev(P), dev(G)
+    for po, go, expose in [(ph, ph, False) for ph in range(1, 8)] + [(3, 5, False), (2, 2, True)]:
+        p = P[po:po + n].copy()
+        tp = tP.clone()[po:po + n]
+        opt = optim.FlatOptimizer(cfg, n)
+        if expose:
+            _ = opt.buffers()
+        orc = O.OracleFlat(cfg, n, np.float32)
+        for t in (1, 2):
+            opt.step(tp, tG[go:go + n], 1e-3)
+            orc.step(p, G[go:go + n].copy(), 1e-3)
+        torch.cuda.synchronize()
+        assert bits_equal(tp.cpu().numpy(), p), (po, go, expose)
+        for name, buf in opt.buffers():
+            assert bits_equal(buf.cpu().numpy(), orc.state[name]), (po, go, name)
+    # mixed step: fp32 master (aligned) + bf16 replica slice at offset 3: phases differ
+    master = O.synth(n, 9, 0, 5, 0, 0, -6, 0, False)
+    tm = dev(master)
+    rep = torch.empty(n + 8, dtype=torch.bfloat16, device="cuda")[3:3 + n]
+    opt = optim.FlatOptimizer(cfg, n)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    opt.step_mixed(tm, tG[:n], rep, 1e-3)
+    orc.step(master, G[:n].copy(), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tm.cpu().numpy(), master)
+    assert bits_equal(rep.view(torch.int16).cpu().numpy().view(np.uint16), O.f32_to_bf16(master))
+
+
+@pytest.mark.parametrize("off", [1, 5])
+def test_lomo_views_bit_exact(off):
+    n = 50000
+    P = O.synth(n + 8, 4, 0, 0, 0, 0, -6, 0, False)
+    G = O.synth(n + 8, 4, 1, 0, 1, 0, -7, 10, False)
+    tp = dev(P)[off:off + n]
+    optim.lomo_apply(tp, dev(G)[off:off + n], 1e-2, 0.5)
+    p = P[off:off + n].copy()
+    O.orc.orc_lomo_f32(O._ptr(p), O._ptr(G[off:off + n].copy()), n, 1e-2, 0.5)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
