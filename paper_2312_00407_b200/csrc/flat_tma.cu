@@ -147,9 +147,27 @@ __device__ __forceinline__ void sts(float* s, const float (&r)[E]) {
     *reinterpret_cast<float2*>(s) = make_float2(r[0], r[1]);
 }
 
-template <class C, int KIND, bool MIXED>
+// Gradient tile of a stage (stream slot 1), fp32 or bf16 (bf16 fills half the slot).
+template <int E>
+__device__ __forceinline__ void lds_grad(const float* slot, int c0, float (&r)[E]) {
+  lds<E>(slot + c0, r);
+}
+template <int E>
+__device__ __forceinline__ void lds_grad_bf16(const float* slot, int c0, float (&r)[E]) {
+  const uint16_t* h = reinterpret_cast<const uint16_t*>(slot) + c0;
+  if constexpr (E == 4) {
+    const uint2 w = *reinterpret_cast<const uint2*>(h);
+    r[0] = __uint_as_float(w.x << 16), r[1] = __uint_as_float(w.x & 0xffff0000u);
+    r[2] = __uint_as_float(w.y << 16), r[3] = __uint_as_float(w.y & 0xffff0000u);
+  } else {
+    const uint32_t w = *reinterpret_cast<const uint32_t*>(h);
+    r[0] = __uint_as_float(w << 16), r[1] = __uint_as_float(w & 0xffff0000u);
+  }
+}
+
+template <class C, int KIND, bool MIXED, typename GT>
 __global__ void __launch_bounds__(C::kConsumers + 32, 1)
-    flat_tma_kernel(float* p, const float* g, float* s0, float* s1, float* s2, float* s3,
+    flat_tma_kernel(float* p, const GT* g, float* s0, float* s1, float* s2, float* s3,
                     uint16_t* pout, uint64_t ntiles, uint64_t n, const StepConsts<float> k) {
   constexpr int NIN = n_in<KIND>();
   constexpr int NS = stages<C, KIND, MIXED>();
@@ -169,8 +187,9 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
   }
   __syncthreads();
 
-  // stream j of a stage: 0 p, 1 g, 2 s0, 3 s1, 4 s2, 5 s3
-  const float* src[6] = {p, g, s0, s1, s2, s3};
+  // stream j of a stage: 0 p, 1 g, 2 s0, 3 s1, 4 s2, 5 s3 (slot of kTile floats each;
+  // a bf16 gradient tile uses the first half of its slot)
+  const float* src[6] = {p, nullptr, s0, s1, s2, s3};
   const uint64_t mine =
       ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
 
@@ -182,10 +201,15 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
       auto issue = [&](uint64_t i) {
         const int s = (int)(i % NS);
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
-        mbar_expect_tx(&full[s], (uint32_t)(nload * kTile * 4));
-        for (int j = 0; j < nload; ++j)
-          bulk_g2s<C::kHint>(buf + ((size_t)s * NIN + j) * kTile, src[j] + e, kTile * 4, &full[s],
-                              pol);
+        constexpr uint32_t gbytes = kTile * sizeof(GT);
+        mbar_expect_tx(&full[s], (uint32_t)((nload - 1) * kTile * 4) + gbytes);
+        for (int j = 0; j < nload; ++j) {
+          float* dst = buf + ((size_t)s * NIN + j) * kTile;
+          if (j == 1)
+            bulk_g2s<C::kHint>(dst, g + e, gbytes, &full[s], pol);
+          else
+            bulk_g2s<C::kHint>(dst, src[j] + e, kTile * 4, &full[s], pol);
+        }
       };
       for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
       for (uint64_t i = 0; i < mine; ++i) {
@@ -224,7 +248,10 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
       float* st = buf + (size_t)s * NIN * kTile + c0;
       float pv[E], gv[E], a[E], b[E], c[E], d[E];
       lds<E>(st, pv);
-      lds<E>(st + kTile, gv);
+      if constexpr (sizeof(GT) == 4)
+        lds<E>(st + kTile, gv);
+      else
+        lds_grad_bf16<E>(buf + (size_t)s * NIN * kTile + kTile, c0, gv);
       lds<E>(st + 2 * kTile, a);
       if constexpr (KIND != K_LION) lds<E>(st + 3 * kTile, b);
       if constexpr (KIND == K_ADAN) {
@@ -258,7 +285,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     // tail (< one tile): plain loads / stores by the consumer threads of CTA 0
     if (blockIdx.x == 0) {
       for (uint64_t e = ntiles * kTile + threadIdx.x; e < n; e += kConsumers) {
-        float pp = p[e], gg = g[e], aa = s0[e], bb = 0.f, cc = 0.f, dd = 0.f;
+        float pp = p[e], gg = load_grad1(g + e), aa = s0[e], bb = 0.f, cc = 0.f, dd = 0.f;
         if constexpr (KIND != K_LION) bb = s1[e];
         if constexpr (KIND == K_ADAN) {
           cc = s2[e];
@@ -412,9 +439,9 @@ void run_lomo_tma(void* p, const void* g, uint64_t n, double lr, double scale,
   launch_check("lomo_tma_kernel");
 }
 
-template <class C, int KIND, bool MIXED>
+template <class C, int KIND, bool MIXED, typename GT>
 void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  auto kern = flat_tma_kernel<C, KIND, MIXED>;
+  auto kern = flat_tma_kernel<C, KIND, MIXED, GT>;
   constexpr int smem = smem_bytes<C, KIND, MIXED>();
   const int dev = current_device();
   static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
@@ -425,7 +452,7 @@ void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
   const uint64_t ntiles = a.n / C::kTile;
   const int grid = (int)std::max<uint64_t>(
       1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
-  kern<<<grid, C::kConsumers + 32, smem, st>>>((float*)a.p, (const float*)a.g, (float*)a.s[0],
+  kern<<<grid, C::kConsumers + 32, smem, st>>>((float*)a.p, (const GT*)a.g, (float*)a.s[0],
                                                (float*)a.s[1], (float*)a.s[2], (float*)a.s[3],
                                                a.p_out_bf16, ntiles, a.n, k);
   launch_check("flat_tma_kernel");
@@ -433,10 +460,17 @@ void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
 
 template <class C, int KIND>
 void dispatch(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  if (a.p_out_bf16)
-    run<C, KIND, true>(a, k, st);
-  else
-    run<C, KIND, false>(a, k, st);
+  if (a.g_dtype == MCO_BF16) {
+    if (a.p_out_bf16)
+      run<C, KIND, true, uint16_t>(a, k, st);
+    else
+      run<C, KIND, false, uint16_t>(a, k, st);
+  } else {
+    if (a.p_out_bf16)
+      run<C, KIND, true, float>(a, k, st);
+    else
+      run<C, KIND, false, float>(a, k, st);
+  }
 }
 
 template <class C>
@@ -453,7 +487,8 @@ void launch_cfg(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) 
 }  // namespace
 
 bool flat_tma_eligible(const FlatArgs& a, int cfg) {
-  if (a.state_dtype != MCO_F32 || a.p_dtype != MCO_F32 || a.g_dtype != MCO_F32) return false;
+  if (a.state_dtype != MCO_F32 || a.p_dtype != MCO_F32) return false;
+  if (a.g_dtype != MCO_F32 && a.g_dtype != MCO_BF16) return false;
   auto al = [](const void* q) { return q == nullptr || ((uintptr_t)q % 16) == 0; };
   bool ok = al(a.p) && al(a.g) && al(a.p_out_bf16);
   for (int i = 0; i < 4; ++i) ok = ok && al(a.s[i]);

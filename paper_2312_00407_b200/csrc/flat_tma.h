@@ -9,7 +9,7 @@ namespace mco {
 // 1 = (16, 3), 2 = (16, 5), 3 = (24, 4), 4 = (8, 4), 5 = (16, 8, 2), 6 = (16, 4, 4,
 // evict-first), 7 = (24, 6, 2).  A tile is 32 * EPT elements per consumer warp.
 int tma_tile(int cfg);
-// fp32 state / params / grads, 16 B aligned buffers, at least one tile.
+// fp32 state / params, fp32 or bf16 grads, 16 B aligned buffers, at least one tile.
 bool flat_tma_eligible(const FlatArgs& a, int cfg);
 void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st, int cfg);
 

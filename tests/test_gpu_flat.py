@@ -344,3 +344,30 @@ def test_lomo_views_bit_exact(off):
     O.orc.orc_lomo_f32(O._ptr(p), O._ptr(G[off:off + n].copy()), n, 1e-2, 0.5)
     torch.cuda.synchronize()
     assert bits_equal(tp.cpu().numpy(), p)
+
+
+@pytest.mark.parametrize("variant", ["tma", "ldg"])
+@pytest.mark.parametrize("kind", FLAT)
+def test_bf16_grads_both_paths_bit_exact(flat_variant, variant, kind):
+    """bf16 gradients with fp32 state on the TMA pipeline (bf16 gradient tiles) and on
+    the LDG kernel, plain and mixed (bf16 replica out), tail included."""
+    flat_variant(variant)
+    n = 5 * 2048 + 37
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=2)
+    p = O.synth(n, 13, 0, 6, 0, 0, -6, 0, False)
+    tp, tpo = dev(p), torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    opt = optim.FlatOptimizer(cfg, n)
+    orc = O.OracleFlat(cfg, n, np.float32)
+    for t in range(1, 5):
+        gb = O.synth(n, 13, 1, 6, t, 0, -7, 10, False, "bf16")
+        tg = dev(gb).view(torch.bfloat16)
+        if t % 2:
+            opt.step(tp, tg, 1e-3)
+        else:
+            opt.step_mixed(tp, tg, tpo, 1e-3)
+        orc.step(p, O.bf16_to_f32(gb), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    assert bits_equal(tpo.view(torch.int16).cpu().numpy().view(np.uint16), O.f32_to_bf16(p))
+    for name, t in opt.buffers():
+        assert bits_equal(t.cpu().numpy(), orc.state[name]), name
