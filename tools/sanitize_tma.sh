@@ -4,7 +4,7 @@
 for tool in memcheck racecheck synccheck; do
   echo "## $tool: flat_tma_kernel (variant tests, every kind, tails, mixed output)"
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_flat.py -q -x \
-      -k "variants and tma and not tma_ and not tma24 and not tma8 and not 1048581" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
+      -k "(variants or bf16_grads_both or phase_peeling or tiny_gradients) and tma and not tma_ and not tma24 and not tma8 and not 1048581" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
   echo "## $tool: lomo_tma_kernel (fp32 / bf16, device clip)"
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_fused.py -q -x \
       -k "lomo_variants and tma and not tma_ and not 1048581" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
