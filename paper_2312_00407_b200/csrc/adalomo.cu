@@ -821,12 +821,15 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
   } else {  // damping + pass 3 over {g, p -> p}
     launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip, call.fuse_usq);
     launch_check("adalomo k5_damp");
-    static const bool k6_tiles = [] {
-      // tuning knob MCO_ADALOMO_K6 = "tiles" (default; measured 2.4% faster: the
-      // per-thread b_j and a_i loads amortise over a tile) or "chunks"
+    // K6 traversal: tiles for multi-tensor calls (the per-thread b_j and a_i loads
+    // amortise over a tile: 24.6 vs 25.4 ms on 7B), flat chunks for the one-tensor hook
+    // form (finer work items for one tensor: 32.4 vs 33.9 ms over the 7B tensors);
+    // MCO_ADALOMO_K6 = "tiles" / "chunks" forces one
+    static const int k6_force = [] {
       const char* e = getenv("MCO_ADALOMO_K6");
-      return !(e && std::string(e) == "chunks");
+      return !e ? 0 : std::string(e) == "chunks" ? 2 : std::string(e) == "tiles" ? 1 : 0;
     }();
+    const bool k6_tiles = k6_force ? k6_force == 1 : !call.single;
     if (k6_tiles) {
       auto kk6 = k6_update_tiles<VEC, GT, PT>;
       launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps);
