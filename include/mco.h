@@ -198,6 +198,13 @@ mco_status mco_adalomo_destroy(mco_adalomo* h);
 mco_status mco_adalomo_apply(mco_adalomo* h, int tensor_index, void* param, int param_dtype,
                              const void* grad, int grad_dtype, double lr,
                              const double* dev_grad_sumsq, void* stream);
+/* List form of the hook: tensors t0..t1-1 (consecutive registry indices) at separate
+ * device pointers params[i] / grads[i] -- a bucket of backward-completed gradients
+ * applied with one launch chain per 64 tensors instead of one per tensor.  Same
+ * result as t1 - t0 mco_adalomo_apply calls. */
+mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* params,
+                                  int param_dtype, const void* const* grads, int grad_dtype,
+                                  double lr, const double* dev_grad_sumsq, void* stream);
 /* Multi-tensor form: every tensor at once over registry-order flat buffers
  * (tensor k at element offset sum_{j<k} numel_j).  If cfg.has_clip_threshold
  * the global grad norm over the whole set is computed in the same pass and

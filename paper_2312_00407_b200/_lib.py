@@ -92,6 +92,8 @@ _SIGS = {
     "mco_adalomo_destroy": (_i, [_p]),
     "mco_adalomo_apply": (_i, [_p, _i, _p, _i, _p, _i, _d, _p, _p]),
     "mco_adalomo_apply_all": (_i, [_p, _p, _i, _p, _i, _d, _p]),
+    "mco_adalomo_apply_list": (_i, [_p, _i, _i, C.POINTER(_p), _i, C.POINTER(_p), _i, _d, _p,
+                                    _p]),
     "mco_adalomo_state_bytes": (_i, [_p, C.POINTER(_u64)]),
     "mco_adalomo_set_shard": (_i, [_p, _i, _i64, _d]),
     "mco_adalomo_phase": (_i, [_p, _i, _p, _i, _p, _i, _d, _p]),

@@ -774,6 +774,42 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, cons
   });
 }
 
+// List form of the hook: tensors t0..t1-1 at separate device pointers, one launch chain
+// per kMaxTab tensors (AdaLomo's statistics are per tensor, so the split is exact).
+mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* params,
+                                  int pdt, const void* const* grads, int gdt, double lr,
+                                  const double* dev_grad_sumsq, void* stream) {
+  return guard([&] {
+    const int nt = (int)h->plan.h_tensors.size();
+    if (t0 < 0 || t1 > nt || t0 > t1)
+      throw Error(MCO_CONTRACT, "adalomo: tensor range [" + std::to_string(t0) + ", " +
+                                    std::to_string(t1) + ") outside 0.." + std::to_string(nt));
+    check_ada_dtypes(pdt, gdt);
+    for (int k = t0; k < t1; ++k)
+      if (!params[k - t0] || !grads[k - t0])
+        throw Error(MCO_CONTRACT, "adalomo: null tensor pointer for index " + std::to_string(k));
+    DeviceGuard dg(h->plan.device);
+    for (int a = t0; a < t1; a += kMaxTab) {
+      const int b = std::min(t1, a + kMaxTab);
+      AdaLomoCall c{};
+      c.t0 = a;
+      c.t1 = b;
+      c.p_dtype = pdt;
+      c.g_dtype = gdt;
+      c.lr = lr;
+      c.use_clip = (dev_grad_sumsq != nullptr && h->plan.cfg.has_clip_threshold) ? 1 : 0;
+      c.ext_sumsq = dev_grad_sumsq;
+      c.ntab = b - a;
+      for (int k = a; k < b; ++k) {
+        c.ptab[k - a] = params[k - t0];
+        c.gtab[k - a] = grads[k - t0];
+      }
+      launch_adalomo(h->plan, c, (cudaStream_t)stream);
+    }
+    for (int k = t0; k < t1; ++k) h->plan.h_tensors[k].t += 1;
+  });
+}
+
 mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const void* flat_g,
                                  int gdt, double lr, void* stream) {
   return guard([&] {

@@ -199,13 +199,19 @@ struct Ptrs {
   void* p;
   const void* g;
   int single;  // 1: p / g point at the call's only tensor
+  int ntab;    // > 0: tensor t0 + i at ptab[i] / gtab[i] (list form)
+  int t0;
+  void* ptab[kMaxTab];
+  const void* gtab[kMaxTab];
 };
 template <typename GT>
-__device__ __forceinline__ const GT* gptr(const Ptrs& P, const TensorInfo& T) {
+__device__ __forceinline__ const GT* gptr(const Ptrs& P, const TensorInfo& T, int k) {
+  if (P.ntab) return (const GT*)P.gtab[k - P.t0];
   return (const GT*)P.g + (P.single ? 0 : T.elem_off);
 }
 template <typename PT>
-__device__ __forceinline__ PT* pptr(const Ptrs& P, const TensorInfo& T) {
+__device__ __forceinline__ PT* pptr(const Ptrs& P, const TensorInfo& T, int k) {
+  if (P.ntab) return (PT*)P.ptab[k - P.t0];
   return (PT*)P.p + (P.single ? 0 : T.elem_off);
 }
 
@@ -220,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK1)
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
-    const GT* g = gptr<GT>(P, T);
-    const PT* p = pptr<PT>(P, T);
+    const GT* g = gptr<GT>(P, T, tl.tensor);
+    const PT* p = pptr<PT>(P, T, tl.tensor);
     double psq = 0.0, gsq = 0.0;
     if (T.factored) {
       const int TC = T.tc, TR = kThreads / T.tc;
@@ -537,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
   for (int64_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
     const Chunk ch = c.chunks[chunk0 + ci];
     const TensorInfo T = c.tensors[ch.tensor];
-    const GT* g = gptr<GT>(P, T);
+    const GT* g = gptr<GT>(P, T, ch.tensor);
     double usq = 0.0;
     if (T.factored) {
       const uint32_t C = (uint32_t)T.cols;
@@ -629,8 +635,8 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t ci = nchunks - 1 - k;
     const Chunk ch = c.chunks[chunk0 + ci];
     const TensorInfo T = c.tensors[ch.tensor];
-    const GT* g = gptr<GT>(P, T);
-    PT* p = pptr<PT>(P, T);
+    const GT* g = gptr<GT>(P, T, ch.tensor);
+    PT* p = pptr<PT>(P, T, ch.tensor);
     const double f = c.tens_sc[ch.tensor * kTensScalars + TS_F];
     if (T.factored) {
       const float ff = (float)f;
@@ -700,8 +706,8 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t ti = ntiles - 1 - k;
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
-    const GT* g = gptr<GT>(P, T);
-    PT* p = pptr<PT>(P, T);
+    const GT* g = gptr<GT>(P, T, tl.tensor);
+    PT* p = pptr<PT>(P, T, tl.tensor);
     const double f = c.tens_sc[tl.tensor * kTensScalars + TS_F];
     if (T.factored) {
       const float ff = (float)f;
@@ -781,7 +787,16 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
         pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
         pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
         pl.d_chunks,  pl.d_chunk_sc};
-  Ptrs P{call.p, call.g, call.single};
+  Ptrs P{};
+  P.p = call.p;
+  P.g = call.g;
+  P.single = call.single;
+  P.ntab = call.ntab;
+  P.t0 = call.t0;
+  for (int i = 0; i < call.ntab; ++i) {
+    P.ptab[i] = call.ptab[i];
+    P.gtab[i] = call.gtab[i];
+  }
   const int dev = current_device();
   const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
   const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
@@ -854,9 +869,11 @@ void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int ph
   for (int k = call.t0; k < call.t1 && vec; ++k) {
     const TensorInfo& T = pl.h_tensors[k];
     if (!T.factored) continue;
-    const int64_t off = call.single ? 0 : T.elem_off;
-    vec = (T.cols % 8 == 0) && (((uintptr_t)call.p + off * psz) % (8 * psz) == 0) &&
-          (((uintptr_t)call.g + off * gsz) % (8 * gsz) == 0);
+    const int64_t off = call.single || call.ntab ? 0 : T.elem_off;
+    const uintptr_t pb = (uintptr_t)(call.ntab ? call.ptab[k - call.t0] : call.p);
+    const uintptr_t gb = (uintptr_t)(call.ntab ? call.gtab[k - call.t0] : call.g);
+    vec = (T.cols % 8 == 0) && ((pb + off * psz) % (8 * psz) == 0) &&
+          ((gb + off * gsz) % (8 * gsz) == 0);
   }
   // (params, grads): (f32, f32), (f32, bf16), (bf16, bf16)
   if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_F32) {

@@ -75,6 +75,8 @@ struct AdaLomoPlan {
   double* d_glob = nullptr;
 };
 
+constexpr int kMaxTab = 64;  // tensors per list call (pointer table in the kernel params)
+
 struct AdaLomoCall {
   int t0, t1;  // tensor range [t0, t1)
   void* p;
@@ -86,6 +88,11 @@ struct AdaLomoCall {
   int use_clip;
   const double* ext_sumsq;  // device global sum g^2 (hook form), or null
   int fuse_usq;  // phases run back to back: the usq payload is reduced inside K5
+  // list form: tensor t0 + i lives at ptab[i] / gtab[i] (separate allocations, the
+  // per-parameter tensors of a model); ntab = 0 -> flat buffers / single tensor
+  int ntab;
+  void* ptab[kMaxTab];
+  const void* gtab[kMaxTab];
 };
 
 // Build the host tile plan for `shapes` (registry order) on a device with `sms` SMs.

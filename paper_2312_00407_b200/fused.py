@@ -52,8 +52,9 @@ class _GradPath:
     packed parameter on its view.  A gradient larger than the bucket is reduced alone.
     """
 
-    def __init__(self, fn: Callable, group, bucket_elems: Optional[int]):
-        self.fn, self.group = fn, group
+    def __init__(self, fn: Callable, group, bucket_elems: Optional[int],
+                 group_fn: Optional[Callable] = None):
+        self.fn, self.group, self.group_fn = fn, group, group_fn
         self.bucket_elems = bucket_elems or None
         self.world = _world(group)
         self.buf = None
@@ -96,13 +97,17 @@ class _GradPath:
         if not self.items:
             return
         self._allreduce(self.buf[:self.used])
-        for p, off, n in self.items:
-            self.fn(p, self.buf[off:off + n].view_as(p))
+        views = [(p, self.buf[off:off + n].view_as(p)) for p, off, n in self.items]
+        if self.group_fn is not None:
+            self.group_fn(views)  # the whole bucket in one call (AdaLomo list form)
+        else:
+            for p, g in views:
+                self.fn(p, g)
         self.items, self.used = [], 0
 
 
-def _run_backward(params, grad_fn, loss_fn, group, bucket_elems, want_loss):
-    path = _GradPath(grad_fn, group, bucket_elems)
+def _run_backward(params, grad_fn, loss_fn, group, bucket_elems, want_loss, group_fn=None):
+    path = _GradPath(grad_fn, group, bucket_elems, group_fn)
     hs = _hooks(params, lambda p: path.add(p))
     try:
         loss = loss_fn()
@@ -160,4 +165,19 @@ def adalomo_fused_step(params: Sequence, loss_fn: Callable, lr: float,
         with torch.no_grad():
             state.apply(index[id(p)], p.data, g.contiguous(), lr)
 
-    return _run_backward(params, upd, loss_fn, group, bucket_elems, True)
+    def upd_bucket(views):
+        # runs of consecutive registry indices -> one list call each (mco_adalomo_apply_list)
+        views = sorted(views, key=lambda pg: index[id(pg[0])])
+        run = [views[0]]
+        for pg in views[1:] + [None]:
+            if pg is not None and index[id(pg[0])] == index[id(run[-1][0])] + 1:
+                run.append(pg)
+                continue
+            with torch.no_grad():
+                state.apply_list(index[id(run[0][0])], [p.data for p, _ in run],
+                                 [g.contiguous() for _, g in run], lr)
+            if pg is not None:
+                run = [pg]
+
+    return _run_backward(params, upd, loss_fn, group, bucket_elems, True,
+                         group_fn=upd_bucket if bucket_elems else None)

@@ -438,6 +438,29 @@ class AdaLomoState:
             _dtype_code(grad), float(lr),
             grad_sumsq.data_ptr() if grad_sumsq is not None else None, _stream(stream)))
 
+    def apply_list(self, first: int, params, grads, lr: float, grad_sumsq=None,
+                   stream=None) -> None:
+        """Hook form for consecutive tensors first, first+1, ...: params[i] / grads[i]
+        are tensor first+i (separate CUDA tensors).  == len(params) apply() calls."""
+        params, grads = list(params), list(grads)
+        n = len(params)
+        if n != len(grads):
+            raise ContractError("adalomo apply_list: params / grads length mismatch")
+        if n == 0:
+            return
+        for i, (p, g) in enumerate(zip(params, grads)):
+            _dev(p, "adalomo param")
+            _dev(g, "adalomo grad")
+            k = first + i
+            if not (0 <= k < len(self.shapes)) or p.numel() != self.numels[k]:
+                raise ContractError(f"adalomo: unknown parameter '{k}'")
+        pt = (C.c_void_p * n)(*[p.data_ptr() for p in params])
+        gt = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
+        _check(lib.mco_adalomo_apply_list(
+            self._h, int(first), int(first) + n, pt, _dtype_code(params[0]), gt,
+            _dtype_code(grads[0]), float(lr),
+            grad_sumsq.data_ptr() if grad_sumsq is not None else None, _stream(stream)))
+
     def apply_all(self, flat_params, flat_grads, lr: float, stream=None) -> None:
         """Every tensor in one multi-tensor pass over registry-order flat buffers;
         global grad-norm clip when cfg.clip_threshold is set.  numpy (host) arrays:

@@ -385,3 +385,23 @@ def test_adalomo_host_path_equals_device_path(clip):
     torch.cuda.synchronize()
     assert bits_equal(hp, tp.cpu().numpy())
     assert a.steps(0) == 2
+
+
+def test_adalomo_list_form_equals_per_tensor():
+    """mco_adalomo_apply_list (pointer table, > 64 tensors split in chunks) == one
+    apply per tensor, bit for bit; misaligned / odd tensors included."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = registry.CONFIG1.shapes() + [(7, 13), (3,)]  # 77 tensors: two list chunks
+    a = optim.AdaLomoState(cfg, shapes)
+    b = optim.AdaLomoState(cfg, shapes)
+    ps = [torch.randn(s, device="cuda") * 0.02 for s in shapes]
+    qs = [p.clone() for p in ps]
+    for t in range(2):
+        gs = [torch.randn(s, device="cuda") * 1e-3 for s in shapes]
+        for k in range(len(shapes)):
+            a.apply(k, ps[k], gs[k], 1e-3)
+        b.apply_list(0, qs, gs, 1e-3)
+    torch.cuda.synchronize()
+    for k in range(len(shapes)):
+        assert torch.equal(ps[k], qs[k]), k
+    assert [b.steps(k) for k in range(len(shapes))] == [2] * len(shapes)

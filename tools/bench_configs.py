@@ -177,6 +177,17 @@ def hooks_7b(W, K):
 
     ms = timed(ada_hooks, W, K)
     line("hook-form adalomo, llama-7b (291 calls)", n, ms, 24, {"calls": len(shapes)})
+    bucket = 32  # the bucketed hook path: consecutive tensors in one list call
+
+    def ada_buckets():
+        for hi in range(len(shapes), 0, -bucket):
+            lo = max(0, hi - bucket)
+            st.apply_list(lo, [views[k][0] for k in range(lo, hi)],
+                          [views[k][1] for k in range(lo, hi)], 5e-4)
+
+    ms = timed(ada_buckets, W, K)
+    line(f"hook-form adalomo, buckets of {bucket} tensors (list form), llama-7b", n, ms, 24,
+         {"calls": (len(shapes) + bucket - 1) // bucket})
     ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
     line("multi-tensor adalomo, llama-7b (1 call)", n, ms, 24)
 
