@@ -24,6 +24,7 @@
 // All reductions are fixed-order (no float atomics): results are
 // bit-reproducible run to run.
 #include <algorithm>
+#include <cfloat>
 #include <mutex>
 #include <unordered_map>
 #include <cmath>
@@ -504,9 +505,20 @@ __global__ void __launch_bounds__(kThreads)
 // one fused multiply-add (explicit: the library is built with --fmad=false so that the
 // stored-state kernels keep the reference's operation order; AdaLomo is compared
 // within the fp32 tolerance of the fp64 reference).
+// rsqrt.approx.ftz: the flush-to-zero form is one MUFU.RSQ, the default form wraps it in
+// a subnormal check and two scaling multiplies (3 more instructions per element in the
+// issue-bound K4).  Its argument a*b + eps is never subnormal -- eps is clamped to
+// FLT_MIN (ada_eps) and a, b >= 0 -- so both forms give the same bits.
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ada_eps(double eps) { return fmaxf((float)eps, FLT_MIN); }
+
 __device__ __forceinline__ float u_fact(float g, float s, float a, float b, float eps) {
   const float gs = s * g;
-  return gs * rsqrtf(__fmaf_rn(a, b, eps));
+  return gs * rsqrt_ftz(__fmaf_rn(a, b, eps));
 }
 
 // row / col of element e of a factored tensor: e / C by multiply-high with the
@@ -539,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, kMinCtasK4)
     k4_usq(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double b2, double eps) {
   pdl_wait();
   __shared__ double scratch[32];
-  const float sf = (float)c.glob[0], epsf = (float)eps;
+  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   for (int64_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
     const Chunk ch = c.chunks[chunk0 + ci];
     const TensorInfo T = c.tensors[ch.tensor];
@@ -629,7 +641,7 @@ template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads)
     k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps) {
   pdl_wait();
-  const float sf = (float)c.glob[0], epsf = (float)eps;
+  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   // reverse chunk order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
     const int64_t ci = nchunks - 1 - k;
@@ -700,7 +712,7 @@ template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads)
     k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
   pdl_wait();
-  const float sf = (float)c.glob[0], epsf = (float)eps;
+  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   // reverse tile order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
     const int64_t ti = ntiles - 1 - k;
