@@ -977,7 +977,12 @@ mco_status mco_adalomo_get_steps(const mco_adalomo* h, int idx, int64_t* t) {
   return guard([&] {
     if (idx < 0 || idx >= (int)h->plan.h_tensors.size())
       throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
-    *t = h->plan.h_tensors[idx].t;
+    // the device counter is the truth (K2 advances it): steps replayed from a captured
+    // CUDA graph count too, which a host mirror would miss
+    DeviceGuard dg(h->plan.device);
+    MCO_CUDA_CHECK(cudaDeviceSynchronize());
+    const TensorInfo* dT = reinterpret_cast<const TensorInfo*>(h->plan.d_tensors) + idx;
+    MCO_CUDA_CHECK(cudaMemcpy(t, &dT->t, sizeof(int64_t), cudaMemcpyDeviceToHost));
   });
 }
 

@@ -405,3 +405,32 @@ def test_adalomo_list_form_equals_per_tensor():
     for k in range(len(shapes)):
         assert torch.equal(ps[k], qs[k]), k
     assert [b.steps(k) for k in range(len(shapes))] == [2] * len(shapes)
+
+
+def test_adalomo_and_lomo_replay_from_a_cuda_graph():
+    """AdaLomo's chain (step counter, scalars and clip scale on the device, PDL launches)
+    and LOMO capture into a CUDA graph: three replays == three eager steps, bit for bit,
+    and the step counter counts the replays."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = registry.CONFIG1.shapes()[:12]
+    n = sum(int(np.prod(s)) for s in shapes)
+    p = torch.empty(n, device="cuda")
+    g = torch.empty(n, device="cuda")
+    registry.fill_params(p, shapes)
+    registry.fill_grads(g, shapes, 1)
+    pe, pg = p.clone(), p.clone()
+    qe, qg = p.clone(), p.clone()
+    se, sg = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    for _ in range(3):
+        se.apply_all(pe, g, 1e-3)
+        optim.lomo_apply(qe, g, 1e-3, 0.5)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sg.apply_all(pg, g, 1e-3)
+        optim.lomo_apply(qg, g, 1e-3, 0.5)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(pe, pg)
+    assert torch.equal(qe, qg)
+    assert [sg.steps(k) for k in range(len(shapes))] == [3] * len(shapes)
