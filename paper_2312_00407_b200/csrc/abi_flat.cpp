@@ -1,0 +1,347 @@
+// C-ABI: FlatOptimizer (optim.cpp:74-181), LOMO (optim.cpp:185-190, 291-303) and the
+// ZeRO step fused with its collectives over peer memory (parallel.cpp:656-666).
+#include "abi_internal.h"
+
+using namespace mco;
+
+extern "C" {
+
+// ---- FlatOptimizer ---------------------------------------------------------------
+// optim.cpp:74-98
+mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device,
+                           int state_dtype, mco_flat** out) {
+  return guard([&] {
+    *out = nullptr;
+    if (fused(cfg->kind))
+      throw Error(MCO_CONTRACT, "FlatOptimizer: " + kind_str(cfg->kind) +
+                                    " is a fused optimizer and keeps no flat state");
+    kind_str(cfg->kind);
+    if (state_dtype != MCO_F32 && state_dtype != MCO_F64)
+      throw Error(MCO_CONTRACT, "FlatOptimizer: state dtype must be f32 or f64");
+    DeviceGuard dg(device);
+    auto h = std::make_unique<mco_flat>();
+    h->cfg = *cfg;
+    h->n = owned_len;
+    h->device = device;
+    h->state_dtype = state_dtype;
+    // slots s0..s3 and the reference's buffers() names / order (optim.cpp:173-181)
+    const char* names[4] = {nullptr, nullptr, nullptr, nullptr};
+    int nslots = 0;
+    switch (cfg->kind) {
+      case MCO_ADAMW: names[0] = "m"; names[1] = "v"; nslots = 2; break;
+      case MCO_LION: names[0] = "m"; nslots = 1; break;
+      case MCO_ADAN: names[0] = "m"; names[1] = "v"; names[2] = "n"; names[3] = "g_prev";
+        nslots = 4; break;
+      case MCO_SOPHIA: names[0] = "m"; names[1] = "h"; nslots = 2; break;
+    }
+    // 8 elements of slack: the state is shifted to the parameters' alignment phase at
+    // the first step (align_state_to), so shard views at odd offsets stay vectorised
+    const size_t bytes = (std::max<uint64_t>(owned_len, 1) + 8) * dtype_size(state_dtype);
+    for (int i = 0; i < nslots; ++i) {
+      MCO_CUDA_CHECK(cudaMalloc(&h->base[i], bytes));
+      MCO_CUDA_CHECK(cudaMemset(h->base[i], 0, bytes));
+      h->slot[i] = h->base[i];
+      h->named.emplace_back(names[i], h->slot[i]);
+    }
+    *out = h.release();
+  });
+}
+
+mco_status mco_flat_destroy(mco_flat* h) {
+  return guard([&] {
+    if (!h) return;
+    DeviceGuard dg(h->device);
+    delete h;
+  });
+}
+
+namespace {
+void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
+  if (np != ng)  // optim.cpp:101-103
+    throw Error(MCO_CONTRACT, "optimizer step: params/grads length mismatch: " +
+                                  std::to_string(np) + " vs " + std::to_string(ng));
+  if (np > h->n)
+    throw Error(MCO_CONTRACT, "optimizer step: " + std::to_string(np) +
+                                  " elements exceed the owned state of " + std::to_string(h->n));
+}
+
+// Before the first step (state still all zero, never handed out) the state buffers are
+// shifted within their slack so that state[i] has the same address phase (mod 8
+// elements) as params[i]: the launch can then peel a short head and run the rest
+// aligned (flat.cu, launch_flat_step).
+void align_state_to(mco_flat* h, const void* params) {
+  if (h->exposed || h->t != 0 || !params) return;
+  const size_t es = dtype_size(h->state_dtype);
+  const uintptr_t u = (uintptr_t)params;
+  if (u % es) return;
+  const int want = (int)((u / es) % 8);
+  if (want == h->phase) return;
+  h->phase = want;
+  for (int i = 0; i < 4; ++i)
+    if (h->base[i]) h->slot[i] = (char*)h->base[i] + (size_t)want * es;
+  for (size_t i = 0; i < h->named.size(); ++i) h->named[i].second = h->slot[i];
+}
+
+void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
+                 uint64_t n, uint64_t state_off, double lr, cudaStream_t st) {
+  FlatArgs a{};
+  a.kind = h->cfg.kind;
+  a.state_dtype = h->state_dtype;
+  a.p = p;
+  a.p_dtype = pdt;
+  a.g = g;
+  a.g_dtype = gdt;
+  const size_t es = dtype_size(h->state_dtype);
+  for (int i = 0; i < 4; ++i) a.s[i] = h->slot[i] ? (char*)h->slot[i] + state_off * es : nullptr;
+  a.p_out_bf16 = pout;
+  a.n = n;
+  const auto kf = make_consts<float>(h->cfg, h->t, lr);
+  const auto kd = make_consts<double>(h->cfg, h->t, lr);
+  launch_flat_step(a, kf, kd, st);
+}
+
+void check_dtypes(const mco_flat* h, int pdt, int gdt) {
+  if (h->state_dtype == MCO_F64) {
+    if (pdt != MCO_F64 || gdt != MCO_F64)
+      throw Error(MCO_CONTRACT, "optimizer step: f64 state takes f64 params and grads");
+  } else if (pdt != MCO_F32 || (gdt != MCO_F32 && gdt != MCO_BF16)) {
+    throw Error(MCO_CONTRACT, "optimizer step: f32 state takes f32 params and f32/bf16 grads");
+  }
+}
+}  // namespace
+
+// optim.cpp:100-112
+mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
+                         int gdt, uint64_t ng, double lr, void* stream) {
+  return guard([&] {
+    check_lengths(h, np, ng);
+    check_dtypes(h, pdt, gdt);
+    DeviceGuard dg(h->device);
+    align_state_to(h, params);
+    ++h->t;  // optim.cpp:104
+    flat_launch(h, params, pdt, grads, gdt, nullptr, np, 0, lr, (cudaStream_t)stream);
+  });
+}
+
+mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, int gdt,
+                               uint16_t* pout, uint64_t n, double lr, void* stream) {
+  return guard([&] {
+    check_lengths(h, n, n);
+    check_dtypes(h, MCO_F32, gdt);
+    if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
+    if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
+    DeviceGuard dg(h->device);
+    align_state_to(h, master);
+    ++h->t;
+    flat_launch(h, master, MCO_F32, grads, gdt, pout, n, 0, lr, (cudaStream_t)stream);
+  });
+}
+
+// Host-span overload: pipelined H2D(p,g) -> step -> D2H(p) over chunks on two
+// streams, so PCIe traffic in both directions overlaps the kernels.
+mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
+                              int gdt, uint64_t ng, double lr) {
+  return guard([&] {
+    check_lengths(h, np, ng);
+    check_dtypes(h, pdt, gdt);
+    DeviceGuard dg(h->device);
+    ++h->t;
+    host_pipeline(h->device, params, dtype_size(pdt), grads, dtype_size(gdt), np, true,
+                  [&](void* dp, void* dg_, uint64_t off, uint64_t m, cudaStream_t st) {
+                    flat_launch(h, dp, pdt, dg_, gdt, nullptr, m, off, lr, st);
+                  });
+  });
+}
+
+mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t) {
+  return guard([&] { *t = h->t; });
+}
+mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
+  return guard([&] { h->t = t; });
+}
+mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out) {
+  return guard([&] { *out = h->named.size() * h->n * dtype_size(h->state_dtype); });
+}
+mco_status mco_flat_config(const mco_flat* h, mco_config* out) {
+  return guard([&] { *out = h->cfg; });
+}
+mco_status mco_flat_num_buffers(const mco_flat* h, int* out) {
+  return guard([&] { *out = (int)h->named.size(); });
+}
+mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, uint64_t* len,
+                           int* dtype) {
+  return guard([&] {
+    if (i < 0 || i >= (int)h->named.size())
+      throw Error(MCO_CONTRACT, "buffers(): index out of range");
+    h->exposed = true;  // callers may keep the pointer: no more relayout
+    *name = h->named[i].first;
+    *ptr = h->named[i].second;
+    *len = h->n;
+    *dtype = h->state_dtype;
+  });
+}
+
+// ---- ZeRO step fused with RS / AG over peer memory (peer.cu) ------------------------
+mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int grad_dtype,
+                               void* const* param_bufs, int param_dtype, int npeers,
+                               float* master, uint64_t offset, uint64_t n, double lr,
+                               void* stream) {
+  return guard([&] {
+    check_lengths(h, n, n);
+    if (h->state_dtype != MCO_F32)
+      throw Error(MCO_CONTRACT, "peer step: f32 optimizer state required");
+    if (!master) throw Error(MCO_CONTRACT, "peer step: master is null");
+    if (npeers < 1 || npeers > kMaxPeers)
+      throw Error(MCO_CONTRACT, "peer step: npeers must be 1.." + std::to_string(kMaxPeers));
+    PeerPtrs pp{};
+    pp.n = npeers;
+    for (int r = 0; r < npeers; ++r) {
+      if (!grad_bufs[r] || !param_bufs[r])
+        throw Error(MCO_CONTRACT, "peer step: null peer buffer");
+      pp.g[r] = grad_bufs[r];
+      pp.p[r] = param_bufs[r];
+    }
+    DeviceGuard dg(h->device);
+    ++h->t;
+    const auto kf = make_consts<float>(h->cfg, h->t, lr);
+    launch_peer_step(h->cfg.kind, pp, grad_dtype, param_dtype, master, h->slot, offset, n, kf,
+                     (cudaStream_t)stream);
+  });
+}
+
+namespace {
+PeerPtrs make_peers(const void* const* grad_bufs, void* const* param_bufs, int npeers) {
+  if (npeers < 1 || npeers > kMaxPeers)
+    throw Error(MCO_CONTRACT, "peer step: npeers must be 1.." + std::to_string(kMaxPeers));
+  PeerPtrs pp{};
+  pp.n = npeers;
+  for (int r = 0; r < npeers; ++r) {
+    if (!grad_bufs[r] || (param_bufs && !param_bufs[r]))
+      throw Error(MCO_CONTRACT, "peer step: null peer buffer");
+    pp.g[r] = grad_bufs[r];
+    pp.p[r] = param_bufs ? param_bufs[r] : nullptr;
+  }
+  return pp;
+}
+}  // namespace
+
+// (sum over ranks of g_r)^2 summed over this rank's owned range, into *dev_out.
+mco_status mco_sumsq_peers(const void* const* grad_bufs, int grad_dtype, int npeers,
+                           uint64_t offset, uint64_t n, double* dev_out, void* stream) {
+  return guard([&] {
+    const PeerPtrs pp = make_peers(grad_bufs, nullptr, npeers);
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_peer_sumsq(pp, grad_dtype, offset, n, dev_out, sumsq_ws(st), st);
+  });
+}
+
+// LOMO fused with its collectives: p = p - f * sum_r g_r over the owned range,
+// written into every rank's replica; f = lr*scale, or from the all-reduced
+// dev_sumsq and clip (optim.cpp:302-303) when dev_sumsq is not null.
+mco_status mco_lomo_apply_peers(const void* const* grad_bufs, int grad_dtype,
+                                void* const* param_bufs, int param_dtype, int npeers,
+                                float* master, uint64_t offset, uint64_t n, double lr,
+                                double scale, const double* dev_sumsq, double clip,
+                                void* stream) {
+  return guard([&] {
+    const PeerPtrs pp = make_peers(grad_bufs, param_bufs, npeers);
+    launch_peer_lomo(pp, grad_dtype, param_dtype, master, offset, n, lr, scale, dev_sumsq, clip,
+                     (cudaStream_t)stream);
+  });
+}
+
+// Symmetric buffers for the peer step: allocation + CUDA IPC export / import.
+mco_status mco_peer_alloc(uint64_t bytes, int device, void** out) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    MCO_CUDA_CHECK(cudaMalloc(out, std::max<uint64_t>(bytes, 1)));
+  });
+}
+mco_status mco_peer_free(void* p) {
+  return guard([&] { MCO_CUDA_CHECK(cudaFree(p)); });
+}
+mco_status mco_peer_export(void* p, void* handle_out) {
+  return guard([&] {
+    cudaIpcMemHandle_t h;
+    MCO_CUDA_CHECK(cudaIpcGetMemHandle(&h, p));
+    static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+    std::memcpy(handle_out, &h, sizeof(h));
+  });
+}
+mco_status mco_peer_import(const void* handle, int device, void** out) {
+  return guard([&] {
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    MCO_CUDA_CHECK(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  });
+}
+mco_status mco_peer_close(void* p) {
+  return guard([&] { MCO_CUDA_CHECK(cudaIpcCloseMemHandle(p)); });
+}
+
+// ---- LOMO -------------------------------------------------------------------------
+mco_status mco_lomo_apply(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                          double scale, void* stream) {
+  return guard([&] { launch_lomo(p, pdt, g, gdt, n, lr, scale, nullptr, 0.0, (cudaStream_t)stream); });
+}
+
+mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                                  const double* dev_sumsq, double clip, void* stream) {
+  return guard([&] {
+    if (!dev_sumsq) throw Error(MCO_CONTRACT, "lomo clip: device sum of squares is null");
+    launch_lomo(p, pdt, g, gdt, n, lr, 1.0, dev_sumsq, clip, (cudaStream_t)stream);
+  });
+}
+
+// lomo_apply on host spans (the reference's Tensor data is host memory).
+// clip >= 0: two passes over the gradient -- sum of squares, then the update.
+mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
+                               double scale, double clip) {
+  return guard([&] {
+    const int dev = current_device();
+    const double* dnorm = nullptr;
+    double* acc = nullptr;
+    if (clip >= 0) {
+      MCO_CUDA_CHECK(cudaMalloc(&acc, sizeof(double)));
+      MCO_CUDA_CHECK(cudaMemset(acc, 0, sizeof(double)));
+      HostStage& hs = host_stage(dev);
+      host_pipeline(dev, const_cast<void*>(g), dtype_size(gdt), nullptr, 0, n, false,
+                    [&](void* dg_, void*, uint64_t, uint64_t m, cudaStream_t st) {
+                      // one accumulator, chunks strictly ordered through stream 0
+                      if (st != hs.st[0]) {
+                        cudaEvent_t ev;
+                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                        MCO_CUDA_CHECK(cudaEventRecord(ev, hs.st[0]));
+                        MCO_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                      }
+                      launch_sumsq(dg_, gdt, m, acc, 1, sumsq_ws(st), st);
+                      if (st != hs.st[0]) {
+                        cudaEvent_t ev;
+                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                        MCO_CUDA_CHECK(cudaEventRecord(ev, st));
+                        MCO_CUDA_CHECK(cudaStreamWaitEvent(hs.st[0], ev, 0));
+                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                      }
+                    });
+      dnorm = acc;
+    }
+    host_pipeline(dev, p, dtype_size(pdt), g, dtype_size(gdt), n, true,
+                  [&](void* dp, void* dg_, uint64_t, uint64_t m, cudaStream_t st) {
+                    launch_lomo(dp, pdt, dg_, gdt, m, lr, scale, dnorm, clip, st);
+                  });
+    if (acc) cudaFree(acc);
+  });
+}
+
+mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* out, int accumulate,
+                     void* stream) {
+  return guard([&] {
+    dtype_size(dtype);
+    cudaStream_t st = (cudaStream_t)stream;
+    launch_sumsq(x, dtype, n, out, accumulate, sumsq_ws(st), st);
+  });
+}
+
+}  // extern "C"
