@@ -123,6 +123,16 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int param_dtype, uint64
 
 mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t);  /* steps_taken()     */
 mco_status mco_flat_set_steps(mco_flat* h, int64_t t);          /* set_steps_taken() */
+/* Graph mode (beyond the reference: CUDA-graph capture of the step).  The step counter
+ * moves to the device: the kernels of mco_flat_step / mco_flat_step_mixed derive the
+ * step's scalars from it and advance it, so a step captured into a CUDA graph replays
+ * as the next step, bit-identical to eager steps (no extra launch per step).  dev_lr: optional device
+ * double read at every step (a schedule updates it between replays); null = the lr
+ * argument of each call (baked into a captured graph).  Host-span and peer steps are
+ * refused in graph mode.  get/set_steps synchronise the device.  Calling enable again
+ * only changes dev_lr; disable brings t back to the host. */
+mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr);
+mco_status mco_flat_graph_disable(mco_flat* h);
 mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out); /* state_bytes_runtime() */
 mco_status mco_flat_config(const mco_flat* h, mco_config* out);   /* config()          */
 /* buffers(): names in the reference's fixed order m, v, n, h, g_prev (optim.cpp:173-181). */

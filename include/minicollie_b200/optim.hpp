@@ -223,6 +223,9 @@ class FlatOptimizer {  // optim.hpp:40-64
     return t;
   }
   void set_steps_taken(int64_t t) { mco_throw(mco_flat_set_steps(h_, t)); }
+  // CUDA-graph mode (mco_flat_graph_enable): dev_lr = optional device double
+  void enable_graph(const double* dev_lr = nullptr) { mco_throw(mco_flat_graph_enable(h_, dev_lr)); }
+  void disable_graph() { mco_throw(mco_flat_graph_disable(h_)); }
   uint64_t state_bytes_runtime() const {
     uint64_t b = 0;
     mco_throw(mco_flat_state_bytes(h_, &b));

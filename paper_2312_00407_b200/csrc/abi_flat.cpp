@@ -70,7 +70,7 @@ void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
 // elements) as params[i]: the launch can then peel a short head and run the rest
 // aligned (flat.cu, launch_flat_step).
 void align_state_to(mco_flat* h, const void* params) {
-  if (h->exposed || h->t != 0 || !params) return;
+  if (h->exposed || h->stepped || h->t != 0 || !params) return;
   const size_t es = dtype_size(h->state_dtype);
   const uintptr_t u = (uintptr_t)params;
   if (u % es) return;
@@ -97,7 +97,32 @@ void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t
   a.n = n;
   const auto kf = make_consts<float>(h->cfg, h->t, lr);
   const auto kd = make_consts<double>(h->cfg, h->t, lr);
+  if (h->gdev) {  // graph mode: the kernels read t and advance it (common.cuh)
+    a.gs.d = h->gdev;
+    a.gs.rows = h->state_dtype == MCO_F64 ? (const void*)h->grow_d : (const void*)h->grow_f;
+    a.gs.nrows = h->grows;
+    a.gs.lr = h->glr;
+    a.gs.lr_host = lr;
+    a.gs.wd = h->cfg.weight_decay;
+    a.gs.interval = h->cfg.update_interval;
+    a.gs.bump = 1;
+  }
   launch_flat_step(a, kf, kd, st);
+  h->stepped = true;
+}
+
+void no_graph(const mco_flat* h, const char* what) {
+  if (h->gdev)
+    throw Error(MCO_CONTRACT, std::string(what) + ": not available in graph mode "
+                              "(mco_flat_graph_disable first)");
+}
+
+// Device step counter <-> host (graph mode); the device may still be running steps.
+int64_t graph_steps(const mco_flat* h) {
+  int64_t t = 0;
+  MCO_CUDA_CHECK(cudaDeviceSynchronize());
+  MCO_CUDA_CHECK(cudaMemcpy(&t, &h->gdev->t, sizeof(t), cudaMemcpyDeviceToHost));
+  return t;
 }
 
 void check_dtypes(const mco_flat* h, int pdt, int gdt) {
@@ -118,7 +143,7 @@ mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const 
     check_dtypes(h, pdt, gdt);
     DeviceGuard dg(h->device);
     align_state_to(h, params);
-    ++h->t;  // optim.cpp:104
+    if (!h->gdev) ++h->t;  // optim.cpp:104 (graph mode: on the device)
     flat_launch(h, params, pdt, grads, gdt, nullptr, np, 0, lr, (cudaStream_t)stream);
   });
 }
@@ -132,7 +157,7 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
     if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
     DeviceGuard dg(h->device);
     align_state_to(h, master);
-    ++h->t;
+    if (!h->gdev) ++h->t;
     flat_launch(h, master, MCO_F32, grads, gdt, pout, n, 0, lr, (cudaStream_t)stream);
   });
 }
@@ -144,6 +169,7 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, c
   return guard([&] {
     check_lengths(h, np, ng);
     check_dtypes(h, pdt, gdt);
+    no_graph(h, "host-span step");
     DeviceGuard dg(h->device);
     ++h->t;
     host_pipeline(h->device, params, dtype_size(pdt), grads, dtype_size(gdt), np, true,
@@ -154,10 +180,78 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, c
 }
 
 mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t) {
-  return guard([&] { *t = h->t; });
+  return guard([&] {
+    if (h->gdev) {
+      DeviceGuard dg(h->device);
+      *t = graph_steps(h);
+    } else {
+      *t = h->t;
+    }
+  });
 }
 mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
-  return guard([&] { h->t = t; });
+  return guard([&] {
+    h->t = t;
+    if (h->gdev) {
+      DeviceGuard dg(h->device);
+      MCO_CUDA_CHECK(cudaDeviceSynchronize());
+      MCO_CUDA_CHECK(cudaMemcpy(&h->gdev->t, &t, sizeof(t), cudaMemcpyHostToDevice));
+    }
+  });
+}
+
+// Graph mode: the step counter moves to the device; the step kernels derive the step's
+// scalars from it and the step's last launch advances it (common.cuh step_consts /
+// graph_bump), so a step captured into a CUDA graph replays as the next step -- bit-identical to eager steps (the t-dependent scalars are the
+// host's own, tabulated up to the step where every 1 - beta_k^t has rounded to 1.0).
+mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr) {
+  return guard([&] {
+    DeviceGuard dg(h->device);
+    if (h->gdev) {  // already on: only the lr source changes
+      h->glr = dev_lr;
+      return;
+    }
+    constexpr int64_t kMaxRows = int64_t(1) << 25;
+    std::vector<GraphRow<float>> rf(1);
+    std::vector<GraphRow<double>> rd(1);
+    for (int64_t t = 1;; ++t) {
+      const auto f = make_consts<float>(h->cfg, t, 0.0);
+      const auto d = make_consts<double>(h->cfg, t, 0.0);
+      rf.push_back({f.c1, f.c2, f.c3, f.sthr});
+      rd.push_back({d.c1, d.c2, d.c3, d.sthr});
+      if (d.c1 == 1.0 && d.c2 == 1.0 && d.c3 == 1.0) break;  // 1 - beta^t is 1.0 from here on
+      if (t + 1 >= kMaxRows)
+        throw Error(MCO_CONFIG, "graph mode: betas too close to 1 (1 - beta^t still below "
+                                "1.0 after 2^25 steps)");
+    }
+    rf[0] = rf[1];
+    rd[0] = rd[1];
+    mco_flat g;  // allocation holder: released into h on success
+    MCO_CUDA_CHECK(cudaMalloc(&g.gdev, sizeof(FlatGraphDev)));
+    MCO_CUDA_CHECK(cudaMalloc(&g.grow_f, rf.size() * sizeof(GraphRow<float>)));
+    MCO_CUDA_CHECK(cudaMalloc(&g.grow_d, rd.size() * sizeof(GraphRow<double>)));
+    MCO_CUDA_CHECK(cudaDeviceSynchronize());
+    FlatGraphDev init{};
+    init.t = h->t;
+    MCO_CUDA_CHECK(cudaMemcpy(g.gdev, &init, sizeof(init), cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(g.grow_f, rf.data(), rf.size() * sizeof(GraphRow<float>),
+                              cudaMemcpyHostToDevice));
+    MCO_CUDA_CHECK(cudaMemcpy(g.grow_d, rd.data(), rd.size() * sizeof(GraphRow<double>),
+                              cudaMemcpyHostToDevice));
+    h->gdev = g.gdev, h->grow_f = g.grow_f, h->grow_d = g.grow_d;
+    h->grows = (int64_t)rf.size();
+    h->glr = dev_lr;
+    g.gdev = nullptr, g.grow_f = nullptr, g.grow_d = nullptr;
+  });
+}
+
+mco_status mco_flat_graph_disable(mco_flat* h) {
+  return guard([&] {
+    if (!h->gdev) return;
+    DeviceGuard dg(h->device);
+    h->t = graph_steps(h);
+    h->free_graph();
+  });
 }
 mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out) {
   return guard([&] { *out = h->named.size() * h->n * dtype_size(h->state_dtype); });
@@ -201,6 +295,7 @@ mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int gr
       pp.g[r] = grad_bufs[r];
       pp.p[r] = param_bufs[r];
     }
+    no_graph(h, "peer step");
     DeviceGuard dg(h->device);
     ++h->t;
     const auto kf = make_consts<float>(h->cfg, h->t, lr);

@@ -126,8 +126,21 @@ struct mco_flat {
   void* base[4] = {nullptr, nullptr, nullptr, nullptr};  // allocations (8 elements slack)
   int phase = 0;         // slot = base + phase elements (matches the params' phase mod 8)
   bool exposed = false;  // buffers() handed out: the layout is frozen
+  bool stepped = false;  // a step was launched (graph mode leaves t on the device)
   std::vector<std::pair<const char*, void*>> named;       // buffers() order
+  // graph mode (mco_flat_graph_enable): device step counter + scalar rows
+  mco::FlatGraphDev* gdev = nullptr;
+  mco::GraphRow<float>* grow_f = nullptr;
+  mco::GraphRow<double>* grow_d = nullptr;
+  int64_t grows = 0;
+  const double* glr = nullptr;  // device lr (null: the lr argument of each call)
+  void free_graph() {
+    for (void* p : {(void*)gdev, (void*)grow_f, (void*)grow_d})
+      if (p) cudaFree(p);
+    gdev = nullptr, grow_f = nullptr, grow_d = nullptr, grows = 0, glr = nullptr;
+  }
   ~mco_flat() {
+    free_graph();
     for (void* p : base)
       if (p) cudaFree(p);
   }

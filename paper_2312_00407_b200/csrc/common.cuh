@@ -80,6 +80,71 @@ struct StepConsts {
   int refresh;                     // Sophia: (t-1) % k == 0
 };
 
+// ---- graph mode (mco_flat_graph_enable) --------------------------------------------
+// The step counter lives on the device and DEV kernels derive the step scalars from it,
+// so a step captured into a CUDA graph replays as the next step.  rows[t] holds the
+// t-dependent scalars (1 - beta_k^t, the sqrt_plus_eps threshold) computed on the host
+// exactly as make_consts does; past the last row they are constant (every 1 - beta_k^t
+// has rounded to 1.0).  Thread 0 of each CTA is the CTA's only reader of t; the launch
+// with bump = 1 (the step's last) advances t in its last CTA to finish (graph_bump).
+struct FlatGraphDev {
+  int64_t t;      // steps taken
+  unsigned done;  // CTAs of the bumping launch that have finished
+};
+template <typename T>
+struct GraphRow {
+  T c1, c2, c3, sthr;
+};
+struct GraphStep {
+  FlatGraphDev* d = nullptr;  // null: eager (the by-value scalars)
+  const void* rows = nullptr;  // GraphRow<state type>[nrows]
+  int64_t nrows = 0;
+  const double* lr = nullptr;  // device lr (null: lr_host)
+  double lr_host = 0, wd = 0;
+  int64_t interval = 1;        // Sophia's update_interval
+  int bump = 0;
+};
+
+template <bool DEV, typename T>
+__device__ __forceinline__ StepConsts<T> step_consts(const StepConsts<T>& kv,
+                                                     const GraphStep& gs) {
+  if constexpr (!DEV) {
+    return kv;
+  } else {
+    __shared__ int64_t t_sh;
+    if (threadIdx.x == 0) t_sh = gs.d->t;
+    __syncthreads();
+    const int64_t t = t_sh + 1;
+    const auto& r = static_cast<const GraphRow<T>*>(gs.rows)[t < gs.nrows ? t : gs.nrows - 1];
+    const double lr = gs.lr ? *gs.lr : gs.lr_host;
+    const double lw = lr * gs.wd;  // make_consts, same double arithmetic (--fmad=false)
+    StepConsts<T> k = kv;
+    k.c1 = r.c1, k.c2 = r.c2, k.c3 = r.c3, k.sthr = r.sthr;
+    k.lr = (T)lr;
+    k.lrwd = (T)lw;
+    k.den = (T)(1.0 + lw);
+    k.first = t == 1 ? 1 : 0;
+    k.refresh = ((t - 1) % gs.interval) == 0 ? 1 : 0;
+    return k;
+  }
+}
+
+// End of a DEV kernel, thread 0 (after its CTA's read of t): the last CTA of the
+// bumping launch advances t; every CTA has read it by then.
+template <bool DEV>
+__device__ __forceinline__ void graph_bump(const GraphStep& gs) {
+  if constexpr (DEV) {
+    if (gs.bump && threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&gs.d->done, 1u) == gridDim.x - 1) {
+        gs.d->done = 0;
+        gs.d->t += 1;
+        __threadfence();
+      }
+    }
+  }
+}
+
 // ---- 256-bit global memory access (LDG.E.256 / STG.E.256 on sm_100a) ----------
 // Streaming data larger than L2 is read once: no L1 allocation, evict-first in L2.
 __device__ __forceinline__ void ld_stream(const float* p, float (&r)[8]) {

@@ -40,13 +40,16 @@ __device__ __forceinline__ void prefetch_l2(const void* ptr, uint32_t bytes) {
 // PFD > 0: each warp bulk-prefetches (cp.async.bulk.prefetch.L2) the 1 KB segments of
 // every input stream it will load PFD grid-stride iterations later, so the LDGs of
 // that iteration hit L2 (more bytes in flight than the register file holds).
+// DEV: graph mode -- the step scalars are derived from the device step counter
+// (common.cuh step_consts / graph_bump) instead of the by-value kv.
 template <int KIND, typename T, typename GT, bool MIXED, int U, int MINB = 1,
-          int WV = Vec<T>::W, int PFD = 0>
+          int WV = Vec<T>::W, int PFD = 0, bool DEV = false>
 __global__ void __launch_bounds__(kThreads, MINB)
     flat_step_kernel(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
                      T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
                      uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
-                     const StepConsts<T> k) {
+                     const StepConsts<T> kv, const GraphStep gs) {
+  const StepConsts<T> k = step_consts<DEV>(kv, gs);
   constexpr int W = WV;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -140,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
     }
     if constexpr (MIXED) pout[e] = (uint16_t)f2bf_bits((float)pp);
   }
+  graph_bump<DEV>(gs);
 }
 
 // Software-pipelined variant: the next vector's loads are issued before the
@@ -191,7 +195,7 @@ __global__ void __launch_bounds__(kThreads)
     flat_step_kernel_pf(T* __restrict__ p, const GT* __restrict__ g, T* __restrict__ s0,
                         T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
                         uint16_t* __restrict__ pout, uint64_t nvec, uint64_t n,
-                        const StepConsts<T> k) {
+                        const StepConsts<T> k, const GraphStep) {
   constexpr int W = Vec<T>::W;
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -453,8 +457,10 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   int W = Vec<T>::W;
   int u_eff = U;
   auto kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB>;
+  const bool dev_step = a.gs.d != nullptr;
+  if (dev_step) kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, Vec<T>::W, 0, true>;
   if constexpr (sizeof(T) == 4) {
-    const int variant = flat_variant();
+    const int variant = dev_step ? (flat_variant() == V_LDG ? V_LDG : V_TMA) : flat_variant();
     int tma_cfg = -1;  // flat_tma.h configurations
     switch (variant) {
       case V_TMA: tma_cfg = 0; break;
@@ -489,7 +495,7 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   const int dev = current_device();
   const int grid = grid_for(kern, std::max<uint64_t>(items, 1), dev);
   kern<<<grid, kThreads, 0, st>>>((T*)a.p, (const GT*)a.g, (T*)a.s[0], (T*)a.s[1], (T*)a.s[2],
-                                  (T*)a.s[3], a.p_out_bf16, nvec, a.n, k);
+                                  (T*)a.s[3], a.p_out_bf16, nvec, a.n, k, a.gs);
   launch_check("flat_step_kernel");
 }
 
@@ -590,7 +596,10 @@ void launch_lomo_one(void* p, int p_dtype, const void* g, int g_dtype, uint64_t 
 
 void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
                       const StepConsts<double>& kd, cudaStream_t st) {
-  if (a.n == 0) return;
+  if (a.n == 0) {
+    if (a.gs.d) launch_flat_graph_bump(a.gs.d, st);
+    return;
+  }
   const size_t ps = dtype_bytes(a.p_dtype), gs = dtype_bytes(a.g_dtype),
                ss = dtype_bytes(a.state_dtype);
   const int ph = common_phase({{a.p, ps}, {a.g, gs}, {a.s[0], ss}, {a.s[1], ss},
@@ -601,6 +610,7 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
   }
   const uint64_t head = 8 - ph;
   FlatArgs h = a, b = a;
+  h.gs.bump = 0;  // graph mode: the body launch advances the step
   h.n = head;
   b.n = a.n - head;
   b.p = advance(a.p, head, ps);
@@ -609,6 +619,15 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
   b.p_out_bf16 = advance(a.p_out_bf16, head, 2);
   launch_flat_one(h, kf, kd, st);
   launch_flat_one(b, kf, kd, st);
+}
+
+namespace {
+__global__ void flat_graph_bump(FlatGraphDev* d) { d->t += 1; }
+}  // namespace
+
+void launch_flat_graph_bump(FlatGraphDev* d, cudaStream_t st) {
+  flat_graph_bump<<<1, 1, 0, st>>>(d);
+  launch_check("flat_graph_bump");
 }
 
 void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,

@@ -17,6 +17,7 @@
 // LDG version of the 11-stream Adan kernel to 3 CTAs/SM.
 #include <algorithm>
 #include <atomic>
+#include <type_traits>
 
 #include "flat_tma.h"
 #include "update.cuh"
@@ -165,10 +166,12 @@ __device__ __forceinline__ void lds_grad_bf16(const float* slot, int c0, float (
   }
 }
 
-template <class C, int KIND, bool MIXED, typename GT>
+template <class C, int KIND, bool MIXED, typename GT, bool DEV = false>
 __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     flat_tma_kernel(float* p, const GT* g, float* s0, float* s1, float* s2, float* s3,
-                    uint16_t* pout, uint64_t ntiles, uint64_t n, const StepConsts<float> k) {
+                    uint16_t* pout, uint64_t ntiles, uint64_t n, const StepConsts<float> kv,
+                    const GraphStep gs) {
+  const StepConsts<float> k = step_consts<DEV>(kv, gs);  // DEV: graph mode (common.cuh)
   constexpr int NIN = n_in<KIND>();
   constexpr int NS = stages<C, KIND, MIXED>();
   constexpr int kTile = C::kTile, kConsumers = C::kConsumers, kConsumerWarps = C::CW;
@@ -305,6 +308,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         if constexpr (MIXED) pout[e] = (uint16_t)f2bf_bits(pp);
       }
     }
+    graph_bump<DEV>(gs);  // thread 0 is a consumer
   }
 }
 
@@ -439,9 +443,9 @@ void run_lomo_tma(void* p, const void* g, uint64_t n, double lr, double scale,
   launch_check("lomo_tma_kernel");
 }
 
-template <class C, int KIND, bool MIXED, typename GT>
-void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  auto kern = flat_tma_kernel<C, KIND, MIXED, GT>;
+template <class C, int KIND, bool MIXED, typename GT, bool DEV>
+void run_kern(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
+  auto kern = flat_tma_kernel<C, KIND, MIXED, GT, DEV>;
   constexpr int smem = smem_bytes<C, KIND, MIXED>();
   const int dev = current_device();
   static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
@@ -454,8 +458,18 @@ void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
       1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
   kern<<<grid, C::kConsumers + 32, smem, st>>>((float*)a.p, (const GT*)a.g, (float*)a.s[0],
                                                (float*)a.s[1], (float*)a.s[2], (float*)a.s[3],
-                                               a.p_out_bf16, ntiles, a.n, k);
+                                               a.p_out_bf16, ntiles, a.n, k, a.gs);
   launch_check("flat_tma_kernel");
+}
+
+// graph mode (a.dk set) is instantiated for the default configuration only
+template <class C, int KIND, bool MIXED, typename GT>
+void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
+  if constexpr (std::is_same_v<C, TmaCfg<16, 4>>) {
+    if (a.gs.d) return run_kern<C, KIND, MIXED, GT, true>(a, k, st);
+  }
+  if (a.gs.d) throw Error(MCO_CONFIG, "flat_tma: graph mode runs the default configuration");
+  run_kern<C, KIND, MIXED, GT, false>(a, k, st);
 }
 
 template <class C, int KIND>

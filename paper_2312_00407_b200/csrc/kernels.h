@@ -21,12 +21,18 @@ struct FlatArgs {
   void* s[4];
   uint16_t* p_out_bf16;  // mixed step only
   uint64_t n;
+  // graph mode (common.cuh): the step scalars come from the device step counter;
+  // gs.d null = the by-value scalars of launch_flat_step
+  GraphStep gs;
 };
 
 // Launch one fused read-grad / update-state / write-param pass.
 // `kd` / `kf` carry the per-step scalars (only the one matching state_dtype is used).
 void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
                       const StepConsts<double>& kd, cudaStream_t st);
+
+// Graph mode: a step with no elements still counts (t += 1 on the device).
+void launch_flat_graph_bump(FlatGraphDev* d, cudaStream_t st);
 
 // Flat-kernel variant (tuning knob; "ldg" default, "tma", ...).  Throws CONFIG on an
 // unknown name.

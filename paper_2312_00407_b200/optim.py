@@ -302,6 +302,24 @@ class FlatOptimizer:
     def set_steps_taken(self, t: int) -> None:
         _check(lib.mco_flat_set_steps(self._h, int(t)))
 
+    def enable_graph(self, lr=None) -> None:
+        """CUDA-graph mode (mco_flat_graph_enable): the step counter and the step
+        scalars move to the device, so ``step`` can be captured into a
+        torch.cuda.CUDAGraph and each replay is the next step (bit-identical to eager).
+        ``lr``: optional 0-dim float64 CUDA tensor read at every step (update it between
+        replays for a schedule); None = the lr passed to each captured call."""
+        ptr = None
+        if lr is not None:
+            if lr.dtype != _torch().float64 or lr.numel() != 1 or not lr.is_cuda:
+                raise ContractError("enable_graph: lr must be a 1-element float64 CUDA tensor")
+            self._graph_lr = lr  # keep it alive while the library reads it
+            ptr = lr.data_ptr()
+        _check(lib.mco_flat_graph_enable(self._h, ptr))
+
+    def disable_graph(self) -> None:
+        _check(lib.mco_flat_graph_disable(self._h))
+        self._graph_lr = None
+
     def state_bytes_runtime(self) -> int:
         out = C.c_uint64()
         _check(lib.mco_flat_state_bytes(self._h, C.byref(out)))
