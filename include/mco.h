@@ -121,6 +121,14 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
 mco_status mco_flat_step_host(mco_flat* h, void* params, int param_dtype, uint64_t n_params,
                               const void* grads, int grad_dtype, uint64_t n_grads, double lr);
 
+/* List form (beyond the reference's flat spans): `count` parameter tensors and their
+ * gradients at separate device pointers (lens[i] elements each, registry order) over
+ * the handle's flat state -- tensor i's state is the slice at the sum of the preceding
+ * lengths, so results and state equal mco_flat_step over the concatenation bit for bit,
+ * without flattening.  sum(lens) <= owned_len.  One launch per 40 tensors. */
+mco_status mco_flat_step_list(mco_flat* h, int count, void* const* params, int param_dtype,
+                              const void* const* grads, int grad_dtype, const uint64_t* lens,
+                              double lr, void* stream);
 mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t);  /* steps_taken()     */
 mco_status mco_flat_set_steps(mco_flat* h, int64_t t);          /* set_steps_taken() */
 /* Graph mode (beyond the reference: CUDA-graph capture of the step).  The step counter

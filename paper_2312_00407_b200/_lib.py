@@ -69,6 +69,8 @@ _SIGS = {
     "mco_flat_get_steps": (_i, [_p, C.POINTER(_i64)]),
     "mco_flat_set_steps": (_i, [_p, _i64]),
     "mco_flat_graph_enable": (_i, [_p, _p]),
+    "mco_flat_step_list": (_i, [_p, _i, C.POINTER(_p), _i, C.POINTER(_p), _i,
+                                C.POINTER(_u64), _d, _p]),
     "mco_flat_graph_disable": (_i, [_p]),
     "mco_flat_state_bytes": (_i, [_p, C.POINTER(_u64)]),
     "mco_flat_config": (_i, [_p, _cfgp]),

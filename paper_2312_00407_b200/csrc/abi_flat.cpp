@@ -82,6 +82,21 @@ void align_state_to(mco_flat* h, const void* params) {
   for (size_t i = 0; i < h->named.size(); ++i) h->named[i].second = h->slot[i];
 }
 
+// Graph mode: the kernels read t and advance it (common.cuh); eager: empty.
+GraphStep graph_step(const mco_flat* h, double lr) {
+  GraphStep gs{};
+  if (!h->gdev) return gs;
+  gs.d = h->gdev;
+  gs.rows = h->state_dtype == MCO_F64 ? (const void*)h->grow_d : (const void*)h->grow_f;
+  gs.nrows = h->grows;
+  gs.lr = h->glr;
+  gs.lr_host = lr;
+  gs.wd = h->cfg.weight_decay;
+  gs.interval = h->cfg.update_interval;
+  gs.bump = 1;
+  return gs;
+}
+
 void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
                  uint64_t n, uint64_t state_off, double lr, cudaStream_t st) {
   FlatArgs a{};
@@ -97,16 +112,7 @@ void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t
   a.n = n;
   const auto kf = make_consts<float>(h->cfg, h->t, lr);
   const auto kd = make_consts<double>(h->cfg, h->t, lr);
-  if (h->gdev) {  // graph mode: the kernels read t and advance it (common.cuh)
-    a.gs.d = h->gdev;
-    a.gs.rows = h->state_dtype == MCO_F64 ? (const void*)h->grow_d : (const void*)h->grow_f;
-    a.gs.nrows = h->grows;
-    a.gs.lr = h->glr;
-    a.gs.lr_host = lr;
-    a.gs.wd = h->cfg.weight_decay;
-    a.gs.interval = h->cfg.update_interval;
-    a.gs.bump = 1;
-  }
+  a.gs = graph_step(h, lr);
   launch_flat_step(a, kf, kd, st);
   h->stepped = true;
 }
@@ -159,6 +165,49 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
     align_state_to(h, master);
     if (!h->gdev) ++h->t;
     flat_launch(h, master, MCO_F32, grads, gdt, pout, n, 0, lr, (cudaStream_t)stream);
+  });
+}
+
+// List form (beyond the reference's flat spans): the model's parameter tensors and their
+// gradients at separate device pointers, stepped in one launch per kListMax tensors
+// over the handle's flat state -- tensor i's state is the slice the flattened vector
+// would give it (registry order), so the result and the state equal a flat step over
+// the concatenation bit for bit, without the flatten / scatter copies
+// (parallel.cpp:468-494).
+mco_status mco_flat_step_list(mco_flat* h, int count, void* const* params, int pdt,
+                              const void* const* grads, int gdt, const uint64_t* lens,
+                              double lr, void* stream) {
+  return guard([&] {
+    if (count < 0 || (count > 0 && (!params || !grads || !lens)))
+      throw Error(MCO_CONTRACT, "step list: null table");
+    uint64_t total = 0;
+    for (int i = 0; i < count; ++i) {
+      if (lens[i] && (!params[i] || !grads[i]))
+        throw Error(MCO_CONTRACT, "step list: null tensor " + std::to_string(i));
+      total += lens[i];
+    }
+    if (total > h->n)
+      throw Error(MCO_CONTRACT, "step list: " + std::to_string(total) +
+                                    " elements exceed the owned state of " + std::to_string(h->n));
+    check_dtypes(h, pdt, gdt);
+    DeviceGuard dg(h->device);
+    if (count > 0) align_state_to(h, params[0]);
+    if (!h->gdev) ++h->t;
+    FlatListArgs a{};
+    a.kind = h->cfg.kind;
+    a.state_dtype = h->state_dtype;
+    a.p_dtype = pdt;
+    a.g_dtype = gdt;
+    a.count = count;
+    a.p = params;
+    a.g = grads;
+    a.len = lens;
+    for (int i = 0; i < 4; ++i) a.s[i] = h->slot[i];
+    const auto kf = make_consts<float>(h->cfg, h->t, lr);
+    const auto kd = make_consts<double>(h->cfg, h->t, lr);
+    a.gs = graph_step(h, lr);
+    launch_flat_step_list(a, kf, kd, (cudaStream_t)stream);
+    h->stepped = true;
   });
 }
 

@@ -31,6 +31,33 @@ struct FlatArgs {
 void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
                       const StepConsts<double>& kd, cudaStream_t st);
 
+// List form: separate parameter / gradient tensors over the flat state (tensor i's state
+// at the sum of the preceding lengths).  One launch per kListMax tensors.
+constexpr int kListMax = 40;
+struct FlatList {  // one launch (kernel parameter)
+  int n;
+  uint64_t vbeg[kListMax + 1];      // prefix sums: vector-path vectors
+  uint64_t ebeg[kListMax + 1];      // prefix sums: scalar-path elements
+  uint64_t first_scalar[kListMax];  // first element on the scalar path
+  void* p[kListMax];
+  const void* g[kListMax];
+  uint64_t soff[kListMax];          // state offset (elements)
+};
+struct FlatListArgs {
+  int kind;
+  int state_dtype;
+  int p_dtype;
+  int g_dtype;
+  int count;
+  void* const* p;
+  const void* const* g;
+  const uint64_t* len;
+  void* s[4];  // state slots at the list's first element
+  GraphStep gs;
+};
+void launch_flat_step_list(const FlatListArgs& a, const StepConsts<float>& kf,
+                           const StepConsts<double>& kd, cudaStream_t st);
+
 // Graph mode: a step with no elements still counts (t += 1 on the device).
 void launch_flat_graph_bump(FlatGraphDev* d, cudaStream_t st);
 

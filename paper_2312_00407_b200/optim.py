@@ -281,6 +281,36 @@ class FlatOptimizer:
                                  params.numel(), grads.data_ptr(), _dtype_code(grads),
                                  grads.numel(), float(lr), _stream(stream)))
 
+    def step_list(self, params, grads, lr: float, stream=None) -> None:
+        """List form (mco_flat_step_list): params[i] / grads[i] are separate contiguous
+        CUDA tensors (e.g. a model's parameters and their .grad) in registry order; the
+        state is the flat slice the flattened vector would give each tensor, so this
+        equals step() over the concatenation bit for bit, without flattening."""
+        params, grads = list(params), list(grads)
+        n = len(params)
+        if n != len(grads):
+            raise ContractError("step_list: params / grads length mismatch")
+        for i, (p, g) in enumerate(zip(params, grads)):
+            _dev(p, "step_list param")
+            _dev(g, "step_list grad")
+            if p.numel() != g.numel():
+                raise ContractError(f"step_list: tensor {i}: {p.numel()} params vs "
+                                    f"{g.numel()} grads")
+            if not (p.is_contiguous() and g.is_contiguous()):
+                raise ContractError(f"step_list: tensor {i} is not contiguous")
+        if n == 0:
+            pd = gd = MCO_F32 if self._sd == MCO_F32 else MCO_F64
+        else:
+            pd, gd = _dtype_code(params[0]), _dtype_code(grads[0])
+            if any(_dtype_code(p) != pd for p in params) or any(
+                    _dtype_code(g) != gd for g in grads):
+                raise ContractError("step_list: mixed dtypes in one list")
+        pt = (C.c_void_p * max(n, 1))(*[p.data_ptr() for p in params])
+        gt = (C.c_void_p * max(n, 1))(*[g.data_ptr() for g in grads])
+        lt = (C.c_uint64 * max(n, 1))(*[p.numel() for p in params])
+        _check(lib.mco_flat_step_list(self._h, n, pt, pd, gt, gd, lt, float(lr),
+                                      _stream(stream)))
+
     def step_mixed(self, master, grads, param_out, lr: float, stream=None) -> None:
         """fp32 master step that also writes the bf16 parameter copy."""
         _dev(master, "master")

@@ -4,7 +4,8 @@
 (1) one AdamW step over a large flat slice: the graph-mode kernel (step scalars read
     from the device) must run at the eager kernel's speed;
 (2) per-tensor optimizers (one FlatOptimizer per parameter tensor of a small model):
-    eager = one host call + launch per tensor; graph = one replay of all of them.
+    eager = one host call + launch per tensor; graph = one replay of all of them;
+    list = one FlatOptimizer over all tensors (mco_flat_step_list), eager and replayed.
 Prints one JSON line."""
 import json
 import os
@@ -80,10 +81,19 @@ def main():
             o.enable_graph(lr_t)
         graph = capture(lambda: [o.step(x, y, 0.0) for o, x, y in zip(opts, ps, gs)])
         ms_g = timed(graph.replay)
+        del opts, graph
+        # list form: one optimizer over the flat state, the tensors stepped in place
+        lo = optim.FlatOptimizer(cfg, sum(x.numel() for x in ps))
+        ms_l = timed(lambda: lo.step_list(ps, gs, 1e-4))
+        lo.enable_graph(lr_t)
+        graph = capture(lambda: lo.step_list(ps, gs, 0.0))
+        ms_lg = timed(graph.replay)
         out[name] = {"tensors": len(shapes), "params": sum(x.numel() for x in ps),
                      "eager_ms": round(ms_e, 3), "graph_ms": round(ms_g, 3),
-                     "speedup": round(ms_e / ms_g, 3)}
-        del ps, gs, opts, graph
+                     "speedup": round(ms_e / ms_g, 3), "list_ms": round(ms_l, 3),
+                     "list_graph_ms": round(ms_lg, 3),
+                     "list_gbps": round(28 * sum(x.numel() for x in ps) / ms_l / 1e6, 1)}
+        del ps, gs, lo, graph
     print(json.dumps(out))
 
 
