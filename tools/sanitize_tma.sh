@@ -8,6 +8,9 @@ for tool in memcheck racecheck synccheck; do
   echo "## $tool: lomo_tma_kernel (fp32 / bf16, device clip)"
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_fused.py -q -x \
       -k "lomo_variants and tma and not tma_ and not 1048581" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
+  echo "## $tool: graph mode (device step counter, last-CTA bump) and list form"
+  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_graph.py tests/test_gpu_flat_list.py -q -x \
+      -k "not 10000000 and not f64" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
   echo "## $tool: AdaLomo (PDL chain; hook and multi-tensor forms)"
   timeout 900 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_fused.py -q -x \
       -k "adalomo and not reference" 2>&1 | grep -E "passed|failed|SUMMARY|rror|azard" | head -8
