@@ -279,6 +279,15 @@ mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n,
 mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param_dtype,
                           const void* flat_grads, int grad_dtype, uint64_t total_len,
                           double lr, void* stream);
+/* Mixed-precision stage 2 (beyond the reference's fp64): the handle
+ * (fp32 state) and master_owned (fp32, this rank's ZeroPlan part) cover the owned part;
+ * flat_params_bf16 are the bf16 replicas.  RS(grads) -> mco_flat_step_mixed(master,
+ * g, replica slice) -> all-gather of the bf16 replicas.  For the vector path, allocate
+ * master_owned with the element phase (address / elem size mod 8) of the replica
+ * slice it writes. */
+mco_status mco_shard_step_mixed(mco_flat* h, mco_comm* c, float* master_owned,
+                                uint16_t* flat_params_bf16, const void* flat_grads,
+                                int grad_dtype, uint64_t total_len, double lr, void* stream);
 
 /* ---- synthetic inputs ------------------------------------------ */
 /* Counter-based, stateless generator; values exact in fp32 (bf16 grid for BF16). */

@@ -386,6 +386,14 @@ inline void shard_step(optim::FlatOptimizer& opt, const NcclComm& comm, float* f
   mco_throw(mco_shard_step(opt.handle(), comm.handle(), flat_params, MCO_F32, flat_grads,
                            MCO_F32, total_len, lr, stream));
 }
+// Mixed precision: fp32 master of the owned part, bf16 replicas (mco_shard_step_mixed).
+inline void shard_step_mixed(optim::FlatOptimizer& opt, const NcclComm& comm,
+                             float* master_owned, uint16_t* flat_params_bf16,
+                             const float* flat_grads, size_t total_len, double lr,
+                             void* stream = nullptr) {
+  mco_throw(mco_shard_step_mixed(opt.handle(), comm.handle(), master_owned, flat_params_bf16,
+                                 flat_grads, MCO_F32, total_len, lr, stream));
+}
 }  // namespace parallel
 
 }  // namespace minicollie

@@ -116,6 +116,7 @@ _SIGS = {
     "mco_comm_check": (_i, [_p]),
     "mco_comm_allreduce_sum": (_i, [_p, _p, _i, _u64, _p]),
     "mco_shard_step": (_i, [_p, _p, _p, _i, _p, _i, _u64, _d, _p]),
+    "mco_shard_step_mixed": (_i, [_p, _p, _p, _p, _p, _i, _u64, _d, _p]),
     "mco_flat_variant": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():

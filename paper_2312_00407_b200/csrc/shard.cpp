@@ -188,72 +188,113 @@ mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n,
   });
 }
 
+}  // extern "C"
+
+namespace {
+// RS (or grouped reduce) of flat_grads into a scratch slice whose element phase (mod 8)
+// matches `phase_ref` -> step(gdst, owned_len) -> AG (or grouped broadcast) of ag_buf,
+// whose element type is ag_dtype.  Argument checks come first, before any collective
+// (every rank fails the same way).
+template <class StepFn>
+void shard_run(mco_flat* h, mco_comm* c, const void* flat_grads, int grad_dtype,
+               uint64_t total_len, void* ag_buf, int ag_dtype, const void* phase_ref,
+               size_t phase_es, void* stream, StepFn step) {
+  if (!h || !c || !flat_grads || !ag_buf) throw Error(MCO_CONTRACT, "shard step: null argument");
+  const int N = c->nranks, me = c->rank;
+  std::vector<uint64_t> parts(N), offs(N + 1);
+  const mco_status zs = mco_zero_plan(total_len, N, 2, parts.data(), offs.data());
+  if (zs != MCO_OK) throw Error(zs, "shard step: zero plan");
+  uint64_t nbuf = 0;
+  const char* nm = nullptr;
+  void* ptr = nullptr;
+  int sdt = 0;
+  mco_status bs = mco_flat_buffer(h, 0, &nm, &ptr, &nbuf, &sdt);
+  if (bs != MCO_OK) throw Error(bs, "shard step: handle");
+  // the handle's owned length must be this rank's ZeroPlan part (parallel.cpp:330)
+  if (nbuf != parts[me])
+    throw Error(MCO_CONTRACT, "shard step: optimizer owns " + std::to_string(nbuf) +
+                                  " elements but ZeroPlan gives rank " + std::to_string(me) +
+                                  " " + std::to_string(parts[me]));
+  const ncclDataType_t gt = nccl_type(grad_dtype), at = nccl_type(ag_dtype);
+  const size_t gs = dt_size(grad_dtype), as = dt_size(ag_dtype);
+  DeviceGuard ds(c->device);
+  // reduced gradient in the stepped slice's alignment phase (mod 8 elements): the update
+  // then vectorises after a short head (flat.cu launch_flat_step)
+  const uintptr_t u = (uintptr_t)phase_ref;
+  const size_t phase = (u % phase_es) ? 0 : (u / phase_es) % 8;
+  const size_t need = (parts[me] + 8) * gs + 256;
+  if (c->scratch_bytes < need) {
+    if (c->scratch) MCO_CUDA_CHECK(cudaFree(c->scratch));
+    c->scratch = nullptr;
+    MCO_CUDA_CHECK(cudaMalloc(&c->scratch, need));
+    c->scratch_bytes = need;
+  }
+  auto s = (cudaStream_t)stream;
+  char* gdst = (char*)c->scratch + phase * gs;
+  const char* algo = getenv("MCO_SHARD_ALGO");  // "p2p": force the per-part path (tests)
+  const bool even = total_len % (uint64_t)N == 0 && !(algo && std::string(algo) == "p2p");
+  const auto& api = nccl();
+  if (even) {
+    MCO_NCCL_CHECK(api.reduce_scatter(flat_grads, gdst, parts[me], gt, ncclSum, c->comm, s));
+  } else {
+    MCO_NCCL_CHECK(api.group_start());
+    for (int r = 0; r < N; ++r)
+      MCO_NCCL_CHECK(api.reduce((const char*)flat_grads + offs[r] * gs, gdst, parts[r], gt,
+                                ncclSum, r, c->comm, s));
+    MCO_NCCL_CHECK(api.group_end());
+  }
+  step(gdst, parts[me], (char*)ag_buf + offs[me] * as);
+  if (even) {
+    MCO_NCCL_CHECK(api.all_gather((char*)ag_buf + offs[me] * as, ag_buf, parts[me], at,
+                                  c->comm, s));
+  } else {
+    MCO_NCCL_CHECK(api.group_start());
+    for (int r = 0; r < N; ++r) {
+      char* part = (char*)ag_buf + offs[r] * as;
+      MCO_NCCL_CHECK(api.broadcast(part, part, parts[r], at, r, c->comm, s));
+    }
+    MCO_NCCL_CHECK(api.group_end());
+  }
+}
+}  // namespace
+
+extern "C" {
+
 mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param_dtype,
                           const void* flat_grads, int grad_dtype, uint64_t total_len, double lr,
                           void* stream) {
-  // argument checks come first, before any collective (every rank fails the same way)
   return guard([&] {
-    if (!h || !c || !flat_params || !flat_grads)
-      throw Error(MCO_CONTRACT, "shard step: null argument");
-    const int N = c->nranks, me = c->rank;
-    std::vector<uint64_t> parts(N), offs(N + 1);
-    const mco_status zs = mco_zero_plan(total_len, N, 2, parts.data(), offs.data());
-    if (zs != MCO_OK) throw Error(zs, "shard step: zero plan");
-    uint64_t nbuf = 0;
-    int idx = 0;
-    mco_status bs = mco_flat_num_buffers(h, &idx);
-    if (bs != MCO_OK) throw Error(bs, "shard step: handle");
-    // the handle's owned length must be this rank's ZeroPlan part (parallel.cpp:330)
-    const char* nm = nullptr;
-    void* ptr = nullptr;
-    int sdt = 0;
-    bs = mco_flat_buffer(h, 0, &nm, &ptr, &nbuf, &sdt);
-    if (bs != MCO_OK) throw Error(bs, "shard step: handle");
-    if (nbuf != parts[me])
-      throw Error(MCO_CONTRACT, "shard step: optimizer owns " + std::to_string(nbuf) +
-                                    " elements but ZeroPlan gives rank " + std::to_string(me) +
-                                    " " + std::to_string(parts[me]));
-    const ncclDataType_t gt = nccl_type(grad_dtype), pt = nccl_type(param_dtype);
-    const size_t gs = dt_size(grad_dtype), ps = dt_size(param_dtype);
-    DeviceGuard ds(c->device);
-    // reduced gradient in the owned parameter slice's alignment phase (mod 8 elements):
-    // the update then vectorises after a short head (flat.cu launch_flat_step)
-    char* mine = (char*)flat_params + offs[me] * ps;
-    const size_t phase = ((uintptr_t)mine % ps) ? 0 : ((uintptr_t)mine / ps) % 8;
-    const size_t need = (parts[me] + 8) * gs + 256;
-    if (c->scratch_bytes < need) {
-      if (c->scratch) MCO_CUDA_CHECK(cudaFree(c->scratch));
-      c->scratch = nullptr;
-      MCO_CUDA_CHECK(cudaMalloc(&c->scratch, need));
-      c->scratch_bytes = need;
-    }
-    auto s = (cudaStream_t)stream;
-    char* gdst = (char*)c->scratch + phase * gs;
-    const char* algo = getenv("MCO_SHARD_ALGO");  // "p2p": force the per-part path (tests)
-    const bool even = total_len % (uint64_t)N == 0 && !(algo && std::string(algo) == "p2p");
-    const auto& api = nccl();
-    if (even) {
-      MCO_NCCL_CHECK(api.reduce_scatter(flat_grads, gdst, parts[me], gt, ncclSum, c->comm, s));
-    } else {
-      MCO_NCCL_CHECK(api.group_start());
-      for (int r = 0; r < N; ++r)
-        MCO_NCCL_CHECK(api.reduce((const char*)flat_grads + offs[r] * gs, gdst, parts[r], gt,
-                                  ncclSum, r, c->comm, s));
-      MCO_NCCL_CHECK(api.group_end());
-    }
-    const mco_status st = mco_flat_step(h, mine, param_dtype, parts[me], gdst, grad_dtype,
-                                        parts[me], lr, stream);
-    if (st != MCO_OK) throw Error(st, mco_last_error());
-    if (even) {
-      MCO_NCCL_CHECK(api.all_gather(mine, flat_params, parts[me], pt, c->comm, s));
-    } else {
-      MCO_NCCL_CHECK(api.group_start());
-      for (int r = 0; r < N; ++r) {
-        char* part = (char*)flat_params + offs[r] * ps;
-        MCO_NCCL_CHECK(api.broadcast(part, part, parts[r], pt, r, c->comm, s));
-      }
-      MCO_NCCL_CHECK(api.group_end());
-    }
+    if (!c) throw Error(MCO_CONTRACT, "shard step: null argument");
+    const size_t ps = dt_size(param_dtype);
+    std::vector<uint64_t> parts(c->nranks), offs(c->nranks + 1);
+    if (mco_zero_plan(total_len, c->nranks, 2, parts.data(), offs.data()) != MCO_OK)
+      throw Error(MCO_CONFIG, "shard step: zero plan");
+    const char* mine = (const char*)flat_params + offs[c->rank] * ps;
+    shard_run(h, c, flat_grads, grad_dtype, total_len, flat_params, param_dtype, mine, ps,
+              stream, [&](void* g, uint64_t n, void* p_owned) {
+                const mco_status st =
+                    mco_flat_step(h, p_owned, param_dtype, n, g, grad_dtype, n, lr, stream);
+                if (st != MCO_OK) throw Error(st, mco_last_error());
+              });
+  });
+}
+
+// Mixed-precision stage 2: fp32 master + state for the owned part,
+// bf16 replicas.  RS(grads) -> mco_flat_step_mixed(master, g, bf16 replica slice) ->
+// AG of the bf16 replicas (2 B/param on the wire instead of 4).
+mco_status mco_shard_step_mixed(mco_flat* h, mco_comm* c, float* master_owned,
+                                uint16_t* flat_params_bf16, const void* flat_grads,
+                                int grad_dtype, uint64_t total_len, double lr, void* stream) {
+  return guard([&] {
+    if (!master_owned) throw Error(MCO_CONTRACT, "shard step: null master");
+    shard_run(h, c, flat_grads, grad_dtype, total_len, flat_params_bf16, MCO_BF16,
+              master_owned, sizeof(float), stream,
+              [&](void* g, uint64_t n, void* replica_owned) {
+                const mco_status st = mco_flat_step_mixed(h, master_owned, g, grad_dtype,
+                                                          (uint16_t*)replica_owned, n, lr,
+                                                          stream);
+                if (st != MCO_OK) throw Error(st, mco_last_error());
+              });
   });
 }
 

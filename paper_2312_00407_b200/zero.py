@@ -587,12 +587,23 @@ class NativeZeroOptimizer:
     ownership and state as ZeroShardedOptimizer (parallel.cpp:656-666)."""
 
     def __init__(self, cfg: optim.OptimizerConfig, total_len: int, comm: NcclComm,
-                 device: Optional[int] = None):
+                 device: Optional[int] = None, mixed: bool = False, master_init=None):
+        """mixed: bf16 replicas with an fp32 master of the owned part
+        (mco_shard_step_mixed); master_init = the fp32 initial parameters (full vector
+        or the owned slice)."""
         self.comm = comm
         self.total_len = int(total_len)
         self.plan = ZeroPlan.make(self.total_len, comm.world, 2)
         self.lo, self.hi = self.plan.owned_range(comm.rank)
         self.opt = optim.FlatOptimizer(cfg, self.hi - self.lo, device=device)
+        self.mixed = mixed
+        self.master = None
+        if mixed:
+            if master_init is None:
+                raise optim.ContractError("mixed sharding needs the fp32 master init")
+            src = master_init if master_init.numel() == self.hi - self.lo else \
+                master_init[self.lo:self.hi]
+            self._master_src = src.float()
 
     def step(self, flat_params, flat_grads, lr: float, stream=None) -> None:
         from ._lib import lib
@@ -603,6 +614,20 @@ class NativeZeroOptimizer:
             raise optim.ContractError(
                 f"shard step: flat buffers of {flat_params.numel()} / {flat_grads.numel()} "
                 f"elements for a plan of {self.total_len}")
+        if self.mixed:
+            if flat_params.dtype.itemsize != 2:
+                raise optim.ContractError("mixed shard step: bf16 replicas expected")
+            if self.master is None:  # the replica slice's phase, so the step vectorises
+                self.master = phased_empty(self.hi - self.lo, self._master_src.dtype,
+                                           flat_params.device,
+                                           elem_phase(flat_params[self.lo:self.hi]))
+                self.master.copy_(self._master_src)
+                self._master_src = None
+            optim._check(lib.mco_shard_step_mixed(
+                self.opt._h, self.comm._h, self.master.data_ptr(), flat_params.data_ptr(),
+                flat_grads.data_ptr(), optim._dtype_code(flat_grads), self.total_len,
+                float(lr), optim._stream(stream)))
+            return
         optim._check(lib.mco_shard_step(self.opt._h, self.comm._h, flat_params.data_ptr(),
                                          optim._dtype_code(flat_params), flat_grads.data_ptr(),
                                          optim._dtype_code(flat_grads), self.total_len,

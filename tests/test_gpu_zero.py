@@ -317,6 +317,37 @@ def test_native_nccl_shard_step_world1(monkeypatch, algo, kind):
     assert torch.equal(t, torch.arange(10, dtype=torch.float64, device="cuda"))
 
 
+@pytest.mark.parametrize("algo", ["rs_ag", "p2p"])
+@pytest.mark.parametrize("gdt", [torch.float32, torch.bfloat16], ids=["f32g", "bf16g"])
+def test_native_nccl_shard_step_mixed_world1(monkeypatch, algo, gdt):
+    """mco_shard_step_mixed (fp32 master + state, bf16 replicas, bf16 all-gather) with
+    one rank == FlatOptimizer.step_mixed on the whole vector, master and replicas bit for
+    bit; the master follows the replica slice's alignment phase."""
+    if algo == "p2p":
+        monkeypatch.setenv("MCO_SHARD_ALGO", "p2p")
+    n = 100003
+    cfg = OptimizerConfig.defaults_for(Kind.ADAN)
+    cfg.weight_decay = 0.01
+    p0 = torch.from_numpy(O.synth(n, 9, 0, 0, 0, 0, -6, 0, False)).cuda()
+    comm = zero.NcclComm()
+    nz = zero.NativeZeroOptimizer(cfg, n, comm, mixed=True, master_init=p0)
+    ref = optim.FlatOptimizer(cfg, n)
+    rep_buf = torch.empty(n + 3, dtype=torch.bfloat16, device="cuda")
+    rep = rep_buf[3:]  # replicas at an odd phase: the master must follow it
+    rep.copy_(p0.bfloat16())
+    master = p0.clone()
+    rep_ref = rep.clone()
+    for t in (1, 2, 3):
+        g = torch.from_numpy(O.synth(n, 9, 1, 0, t, 0, -7, 10, False)).cuda().to(gdt)
+        nz.step(rep, g, 1e-3)
+        ref.step_mixed(master, g, rep_ref, 1e-3)
+    torch.cuda.synchronize()
+    assert zero.elem_phase(nz.master) == zero.elem_phase(rep)
+    assert torch.equal(nz.master, master)
+    assert torch.equal(rep, rep_ref)
+    comm.check()
+
+
 def test_native_shard_step_contract_errors():
     comm = zero.NcclComm()
     nz = zero.NativeZeroOptimizer(OptimizerConfig.defaults_for(Kind.ADAMW), 1000, comm)

@@ -6,7 +6,8 @@ order is the rank order (peer-memory kernel; any two-rank sum), within one fp32
 rounding of the sum otherwise (NCCL's reduction order).
 
 Paths: zero.ZeroShardedOptimizer (torch.distributed RS / AG), zero.NativeZeroOptimizer
-(mco_shard_step over the library's NCCL communicator), zero.PeerShardedOptimizer (one
+(mco_shard_step over the library's NCCL communicator; mco_shard_step_mixed with bf16
+replicas), zero.PeerShardedOptimizer (one
 kernel over NVLink peer memory), zero.RowShardedAdaLomo (two statistic all-reduces),
 and bench.py under torchrun with NCCL."""
 import json
@@ -75,6 +76,13 @@ def _worker(rank, world, port, q):
         comm.check()
         out["native"] = p.cpu().numpy()
 
+        nm = zero.NativeZeroOptimizer(cfg, P, comm, mixed=True, master_init=p0)
+        rep = p0.bfloat16()
+        for t in range(1, STEPS + 1):
+            nm.step(rep, torch.from_numpy(_grad(rank, t)).cuda(), 1e-3)
+        torch.cuda.synchronize()
+        out["native_mixed"] = rep.float().cpu().numpy()
+
         ps = zero.PeerShardedOptimizer(cfg, P)
         ps.params.copy_(p0)
         for t in range(1, STEPS + 1):
@@ -124,9 +132,11 @@ def _serial():
 
 
 @needs_multi
-@pytest.mark.parametrize("path", ["zero", "native", "peer"])
+@pytest.mark.parametrize("path", ["zero", "native", "peer", "native_mixed"])
 def test_sharded_paths_equal_serial(results, path):
     want = _serial()
+    if path == "native_mixed":  # bf16 replicas of the fp32 master (RNE)
+        want = torch.from_numpy(want).bfloat16().float().numpy()
     for r in range(WORLD):
         got = results[r][path]
         assert np.array_equal(got, results[0][path])  # replicas agree bit for bit
