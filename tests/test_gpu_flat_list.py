@@ -121,3 +121,35 @@ def test_list_contract_errors():
         opt.step_list([a], [], 1e-3)
     opt.step_list([], [], 1e-3)  # an empty list still counts as a step
     assert opt.steps_taken() == 1
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_list_randomised_sweep(seed):
+    """Random kinds, dtype modes, tensor counts (1-90: up to three launches), sizes
+    (odd, tiny, vector-sized, empty) and step counts: list == flat, bit for bit."""
+    import random
+
+    rnd = random.Random(seed)
+    kind = rnd.choice(KINDS)
+    mode = rnd.choice(["f32", "bf16g", "f64"])
+    cfg = _cfg(kind)
+    cfg.weight_decay = rnd.choice([0.0, 0.01, 0.1])
+    pdt = torch.float64 if mode == "f64" else torch.float32
+    gdt = torch.bfloat16 if mode == "bf16g" else pdt
+    sd = "f64" if mode == "f64" else "f32"
+    sizes = [rnd.choice([0, 1, 3, 8, 17, 256, 1000, 4096, 8200, 40000])
+             for _ in range(rnd.randint(1, 90))]
+    steps = rnd.randint(1, 4)
+    ps, gs = _tensors(sizes, pdt, gdt, seed=seed, steps=steps)
+    total = sum(sizes)
+    flat = optim.FlatOptimizer(cfg, max(total, 1), state_dtype=sd)
+    lst = optim.FlatOptimizer(cfg, max(total, 1), state_dtype=sd)
+    flat_p = torch.cat([p.reshape(-1) for p in ps])
+    for t, g in enumerate(gs):
+        lr = rnd.choice([1e-4, 1e-3, 3e-2])
+        flat.step(flat_p, torch.cat([x.reshape(-1) for x in g]), lr)
+        lst.step_list(ps, g, lr)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([p.reshape(-1) for p in ps]), flat_p)
+    for (na, a), (nb, b) in zip(flat.buffers(), lst.buffers()):
+        assert na == nb and torch.equal(a[:total], b[:total]), na
