@@ -216,6 +216,20 @@ class FlatOptimizer {  // optim.hpp:40-64
             void* stream = nullptr) {
     mco_throw(mco_flat_step(h_, dev_params, MCO_F64, n, dev_grads, MCO_F64, n, lr, stream));
   }
+  // List form (mco_flat_step_list): a model's tensors in registry order over the flat
+  // state -- == step() over their concatenation, without flattening.
+  void step(std::span<DeviceTensor> tensors, double lr, void* stream = nullptr) {
+    std::vector<void*> p;
+    std::vector<const void*> g;
+    std::vector<uint64_t> len;
+    for (auto& t : tensors) {
+      p.push_back(t.data);
+      g.push_back(t.grad);
+      len.push_back(static_cast<uint64_t>(t.numel()));
+    }
+    mco_throw(mco_flat_step_list(h_, static_cast<int>(tensors.size()), p.data(), MCO_F32,
+                                 g.data(), MCO_F32, len.data(), lr, stream));
+  }
 
   int64_t steps_taken() const {
     int64_t t = 0;
