@@ -23,13 +23,16 @@
 
 #include "flat_tma.h"
 #include "kernels.h"
+#include "launch.cuh"
 #include "update.cuh"
 
 namespace mco {
 namespace {
 
 using namespace upd;
-constexpr int kThreads = 256;
+using flatk::aligned;
+using flatk::grid_for;
+using flatk::kThreads;
 
 // MINB > 1 caps registers so MINB CTAs fit per SM (Adan streams 11 buffers).
 // WV: elements per vector access (8 f32 = 256-bit, 4 f32 = 128-bit, 4 f64 = 256-bit).
@@ -142,111 +145,6 @@ __global__ void __launch_bounds__(kThreads, MINB)
       s3[e] = dd;
     }
     if constexpr (MIXED) pout[e] = (uint16_t)f2bf_bits((float)pp);
-  }
-  graph_bump<DEV>(gs);
-}
-
-// ---- list form (mco_flat_step_list) --------------------------------------------------
-// Separate parameter / gradient tensors over the handle's flat state: tensor i's state
-// is elements [soff_i, soff_i + n_i) -- the layout of the flattened vector, so the state
-// equals a flat step over the concatenation bit for bit.  The launch's vectors (of the
-// tensors whose streams are all W-aligned) and scalar elements (tails, unaligned
-// tensors) are two virtual index spaces; a thread finds its tensor by binary search over
-// the prefix sums (shared memory).
-__device__ __forceinline__ int list_find(const uint64_t* b, int n, uint64_t v) {
-  int lo = 0, hi = n - 1;  // largest i with b[i] <= v (skips empty ranges)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (b[mid] <= v) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
-
-template <int KIND, typename T, typename GT, int U, int MINB, bool DEV>
-__global__ void __launch_bounds__(kThreads, MINB)
-    flat_list_kernel(const __grid_constant__ FlatList L, T* __restrict__ s0,
-                     T* __restrict__ s1, T* __restrict__ s2, T* __restrict__ s3,
-                     const StepConsts<T> kv, const GraphStep gs) {
-  const StepConsts<T> k = step_consts<DEV>(kv, gs);
-  constexpr int W = Vec<T>::W;
-  __shared__ uint64_t vb[kListMax + 1], eb[kListMax + 1];
-  for (int i = threadIdx.x; i <= L.n; i += blockDim.x) vb[i] = L.vbeg[i], eb[i] = L.ebeg[i];
-  __syncthreads();
-  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  const uint64_t nv = vb[L.n];
-  for (uint64_t base = tid; base < nv; base += stride * U) {
-    T pv[U][W], gv[U][W], a[U][W], b[U][W], c[U][W], d[U][W];
-    T* pp[U];
-    uint64_t so[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t vi = base + (uint64_t)u * stride;
-      if (vi < nv) {
-        const int i = list_find(vb, L.n, vi);
-        const uint64_t e = (vi - vb[i]) * W;
-        pp[u] = static_cast<T*>(L.p[i]) + e;
-        so[u] = L.soff[i] + e;
-        ld_stream(pp[u], pv[u]);
-        load_grad(static_cast<const GT*>(L.g[i]) + e, gv[u]);
-        ld_stream(s0 + so[u], a[u]);
-        if constexpr (reads_s1(KIND)) ld_stream(s1 + so[u], b[u]);
-        if constexpr (KIND == K_ADAN) {
-          ld_stream(s2 + so[u], c[u]);
-          if (!k.first) ld_stream(s3 + so[u], d[u]);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint64_t vi = base + (uint64_t)u * stride;
-      if (vi < nv) {
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          if constexpr (KIND != K_ADAN) c[u][j] = d[u][j] = T(0);
-          if constexpr (KIND == K_ADAN) {
-            if (k.first) d[u][j] = T(0);
-          }
-          if constexpr (!reads_s1(KIND)) b[u][j] = T(0);
-          update<KIND, T>(pv[u][j], gv[u][j], a[u][j], b[u][j], c[u][j], d[u][j], k);
-        }
-        st_stream(pp[u], pv[u]);
-        st_stream(s0 + so[u], a[u]);
-        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) st_stream(s1 + so[u], b[u]);
-        if constexpr (KIND == K_SOPHIA) {
-          if (k.refresh) st_stream(s1 + so[u], b[u]);
-        }
-        if constexpr (KIND == K_ADAN) {
-          st_stream(s2 + so[u], c[u]);
-          st_stream(s3 + so[u], d[u]);
-        }
-      }
-    }
-  }
-  const uint64_t ne = eb[L.n];
-  for (uint64_t x = tid; x < ne; x += stride) {
-    const int i = list_find(eb, L.n, x);
-    const uint64_t e = L.first_scalar[i] + (x - eb[i]), o = L.soff[i] + e;
-    T* p = static_cast<T*>(L.p[i]);
-    T pp = p[e], gg = (T)load_grad1(static_cast<const GT*>(L.g[i]) + e), aa = s0[o],
-      bb = T(0), cc = T(0), dd = T(0);
-    if constexpr (reads_s1(KIND)) bb = s1[o];
-    if constexpr (KIND == K_ADAN) {
-      cc = s2[o];
-      if (!k.first) dd = s3[o];
-    }
-    update<KIND, T>(pp, gg, aa, bb, cc, dd, k);
-    p[e] = pp;
-    s0[o] = aa;
-    if constexpr (KIND == K_ADAMW || KIND == K_ADAN) s1[o] = bb;
-    if constexpr (KIND == K_SOPHIA) {
-      if (k.refresh) s1[o] = bb;
-    }
-    if constexpr (KIND == K_ADAN) {
-      s2[o] = cc;
-      s3[o] = dd;
-    }
   }
   graph_bump<DEV>(gs);
 }
@@ -527,31 +425,6 @@ int flat_variant() {
   return v;
 }
 
-// ---- launch configuration --------------------------------------------------------
-template <typename K>
-int grid_for(K kernel, uint64_t work_items, int device) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, int> cache;  // kernel -> resident CTAs per SM
-  int per_sm = 0;
-  {
-    std::lock_guard<std::mutex> lock(mu);
-    auto it = cache.find((const void*)kernel);
-    if (it == cache.end()) {
-      MCO_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0));
-      per_sm = std::max(per_sm, 1);
-      cache[(const void*)kernel] = per_sm;
-    } else {
-      per_sm = it->second;
-    }
-  }
-  const uint64_t full = (uint64_t)device_info(device).sms * (uint64_t)per_sm;
-  const uint64_t need = (work_items + kThreads - 1) / kThreads;
-  return (int)std::max<uint64_t>(1, std::min(full, need));
-}
-
-inline bool aligned(const void* ptr, size_t bytes) {
-  return ptr == nullptr || ((uintptr_t)ptr % bytes) == 0;
-}
 
 template <int KIND, typename T, typename GT, bool MIXED>
 void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
@@ -694,80 +567,6 @@ void launch_flat_one(const FlatArgs& a, const StepConsts<float>& kf,
   }
 }
 
-template <int KIND, typename T, typename GT>
-void run_list(const FlatList& L, const FlatListArgs& a, const StepConsts<T>& k,
-              const GraphStep& gs, cudaStream_t st) {
-  constexpr int U = (KIND == K_ADAN) ? 1 : 2;
-  constexpr int MINB = (sizeof(T) == 4 && (KIND == K_ADAN || KIND == K_LION)) ? 3 : 1;
-  auto kern = gs.d ? flat_list_kernel<KIND, T, GT, U, MINB, true>
-                   : flat_list_kernel<KIND, T, GT, U, MINB, false>;
-  const uint64_t nv = L.vbeg[L.n], ne = L.ebeg[L.n];
-  const uint64_t items = std::max<uint64_t>(std::max((nv + U - 1) / U, ne), 1);
-  const int grid = grid_for(kern, items, current_device());
-  kern<<<grid, kThreads, 0, st>>>(L, (T*)a.s[0], (T*)a.s[1], (T*)a.s[2], (T*)a.s[3], k, gs);
-  launch_check("flat_list_kernel");
-}
-
-template <int KIND, typename T, typename GT>
-void list_chunks(const FlatListArgs& a, const StepConsts<T>& k, cudaStream_t st) {
-  constexpr int W = Vec<T>::W;
-  uint64_t soff = 0;
-  int launches = 0, last = -1;
-  for (int i = 0; i < a.count; ++i)
-    if (a.len[i]) last = i;
-  if (last < 0) {  // nothing to update: the step still counts
-    if (a.gs.d) launch_flat_graph_bump(a.gs.d, st);
-    return;
-  }
-  FlatList L{};
-  auto flush = [&](bool final_chunk) {
-    if (L.n == 0) return;
-    GraphStep gs = a.gs;
-    gs.bump = final_chunk ? 1 : 0;  // graph mode: the step's last launch advances t
-    run_list<KIND, T, GT>(L, a, k, gs, st);
-    ++launches;
-    L = FlatList{};
-  };
-  for (int i = 0; i < a.count; ++i) {
-    const uint64_t n = a.len[i];
-    if (n) {
-      bool vec = aligned(a.p[i], sizeof(T) * W) && aligned(a.g[i], sizeof(GT) * W);
-      for (int j = 0; j < 4; ++j)
-        vec = vec && aligned(a.s[j] ? (const char*)a.s[j] + soff * sizeof(T) : nullptr,
-                             sizeof(T) * W);
-      const uint64_t nvec = vec ? n / W : 0;
-      const int t = L.n++;
-      L.p[t] = a.p[i];
-      L.g[t] = a.g[i];
-      L.soff[t] = soff;
-      L.first_scalar[t] = nvec * W;
-      L.vbeg[t + 1] = L.vbeg[t] + nvec;
-      L.ebeg[t + 1] = L.ebeg[t] + (n - nvec * W);
-      if (L.n == kListMax) flush(i == last);
-    }
-    soff += n;
-  }
-  flush(true);
-}
-
-template <int KIND>
-void list_dtypes(const FlatListArgs& a, const StepConsts<float>& kf,
-                 const StepConsts<double>& kd, cudaStream_t st) {
-  if (a.state_dtype == MCO_F64) {
-    if (a.p_dtype != MCO_F64 || a.g_dtype != MCO_F64)
-      throw Error(MCO_CONTRACT, "flat step list: f64 state takes f64 params and grads");
-    list_chunks<KIND, double, double>(a, kd, st);
-  } else if (a.p_dtype != MCO_F32) {
-    throw Error(MCO_CONTRACT, "flat step list: f32 state takes f32 params");
-  } else if (a.g_dtype == MCO_F32) {
-    list_chunks<KIND, float, float>(a, kf, st);
-  } else if (a.g_dtype == MCO_BF16) {
-    list_chunks<KIND, float, uint16_t>(a, kf, st);
-  } else {
-    throw Error(MCO_CONTRACT, "flat step list: f32 state takes f32 or bf16 grads");
-  }
-}
-
 void launch_lomo_one(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, double lr,
                      double scale, const double* dev_sumsq, double clip, cudaStream_t st);
 
@@ -798,17 +597,6 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
   b.p_out_bf16 = advance(a.p_out_bf16, head, 2);
   launch_flat_one(h, kf, kd, st);
   launch_flat_one(b, kf, kd, st);
-}
-
-void launch_flat_step_list(const FlatListArgs& a, const StepConsts<float>& kf,
-                           const StepConsts<double>& kd, cudaStream_t st) {
-  switch (a.kind) {
-    case MCO_ADAMW: list_dtypes<K_ADAMW>(a, kf, kd, st); break;
-    case MCO_LION: list_dtypes<K_LION>(a, kf, kd, st); break;
-    case MCO_ADAN: list_dtypes<K_ADAN>(a, kf, kd, st); break;
-    case MCO_SOPHIA: list_dtypes<K_SOPHIA>(a, kf, kd, st); break;
-    default: throw Error(MCO_CONTRACT, "FlatOptimizer: fused kind");
-  }
 }
 
 namespace {
