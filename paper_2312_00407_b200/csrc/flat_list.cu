@@ -125,7 +125,11 @@ template <int KIND, typename T, typename GT>
 void run_list(const FlatList& L, const FlatListArgs& a, const StepConsts<T>& k,
               const GraphStep& gs, cudaStream_t st) {
   constexpr int U = (KIND == K_ADAN) ? 1 : 2;
-  constexpr int MINB = (sizeof(T) == 4 && (KIND == K_ADAN || KIND == K_LION)) ? 3 : 1;
+#ifndef MCO_LIST_MINB
+#define MCO_LIST_MINB 1
+#endif
+  constexpr int MINB =
+      (sizeof(T) == 4 && (KIND == K_ADAN || KIND == K_LION)) ? 3 : MCO_LIST_MINB;
   auto kern = gs.d ? flat_list_kernel<KIND, T, GT, U, MINB, true>
                    : flat_list_kernel<KIND, T, GT, U, MINB, false>;
   const uint64_t nv = L.vbeg[L.n], ne = L.ebeg[L.n];
