@@ -368,7 +368,11 @@ def bench_ours(args, rank, world, local_rank):
         out["p"] = out["g"] = None
         gc.collect()
         torch.cuda.empty_cache()
-        out["collectives"] = bench_peer_step(args, P, rank, world, dev)
+        try:  # the headline line must not depend on the collective benchmarks
+            out["collectives"] = bench_peer_step(args, P, rank, world, dev)
+        except Exception as ex:  # report, never fake
+            log(f"[rank {rank}] peer-memory step unavailable: {ex!r}")
+            out["collectives"] = {"unavailable": repr(ex)[:200]}
         gc.collect()
         torch.cuda.empty_cache()
         import torch.distributed as dist
