@@ -141,6 +141,17 @@ __device__ __forceinline__ StepConsts<T> step_consts(const StepConsts<T>& kv,
   }
 }
 
+// List forms: largest i in [0, n) with b[i] <= v (prefix sums; skips empty ranges).
+__device__ __forceinline__ int list_find(const uint64_t* b, int n, uint64_t v) {
+  int lo = 0, hi = n - 1;  // largest i with b[i] <= v (skips empty ranges)
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (b[mid] <= v) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
 // End of a DEV kernel, thread 0 (after its CTA's read of t): the last CTA of the
 // bumping launch advances t; every CTA has read it by then.
 template <bool DEV>

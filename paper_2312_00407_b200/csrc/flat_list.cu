@@ -3,7 +3,10 @@
 // arithmetic as the flat kernels (update.cuh, --fmad=false): bit-identical to a flat
 // step over the concatenation.
 #include <algorithm>
+#include <cstring>
+#include <type_traits>
 
+#include "flat_tma.h"
 #include "kernels.h"
 #include "launch.cuh"
 #include "update.cuh"
@@ -23,15 +26,6 @@ using flatk::kThreads;
 // tensors whose streams are all W-aligned) and scalar elements (tails, unaligned
 // tensors) are two virtual index spaces; a thread finds its tensor by binary search over
 // the prefix sums (shared memory).
-__device__ __forceinline__ int list_find(const uint64_t* b, int n, uint64_t v) {
-  int lo = 0, hi = n - 1;  // largest i with b[i] <= v (skips empty ranges)
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (b[mid] <= v) lo = mid;
-    else hi = mid - 1;
-  }
-  return lo;
-}
 
 template <int KIND, typename T, typename GT, int U, int MINB, bool DEV>
 __global__ void __launch_bounds__(kThreads, MINB)
@@ -139,11 +133,18 @@ void run_list(const FlatList& L, const FlatListArgs& a, const StepConsts<T>& k,
   launch_check("flat_list_kernel");
 }
 
+// tma: fp32 state and parameters on the cp.async.bulk pipeline (flat_tma.cu), the
+// default variant -- tiles of list_tma_tile() elements per 16 B-aligned tensor; else
+// the LDG kernel above (W-element vectors per W-aligned tensor).
 template <int KIND, typename T, typename GT>
 void list_chunks(const FlatListArgs& a, const StepConsts<T>& k, cudaStream_t st) {
   constexpr int W = Vec<T>::W;
+  bool tma = false;
+  if constexpr (std::is_same_v<T, float>) tma = std::strcmp(flat_variant_name(), "tma") == 0;
+  const uint64_t unit = tma ? (uint64_t)list_tma_tile() : (uint64_t)W;  // elements per item
+  const size_t align = tma ? 16 : sizeof(T) * W;
   uint64_t soff = 0;
-  int launches = 0, last = -1;
+  int last = -1;
   for (int i = 0; i < a.count; ++i)
     if (a.len[i]) last = i;
   if (last < 0) {  // nothing to update: the step still counts
@@ -155,25 +156,31 @@ void list_chunks(const FlatListArgs& a, const StepConsts<T>& k, cudaStream_t st)
     if (L.n == 0) return;
     GraphStep gs = a.gs;
     gs.bump = final_chunk ? 1 : 0;  // graph mode: the step's last launch advances t
+    if constexpr (std::is_same_v<T, float>) {
+      if (tma) {
+        float* sl[4] = {(float*)a.s[0], (float*)a.s[1], (float*)a.s[2], (float*)a.s[3]};
+        launch_list_tma(a.kind, a.g_dtype, L, sl, k, gs, st);
+        L = FlatList{};
+        return;
+      }
+    }
     run_list<KIND, T, GT>(L, a, k, gs, st);
-    ++launches;
     L = FlatList{};
   };
   for (int i = 0; i < a.count; ++i) {
     const uint64_t n = a.len[i];
     if (n) {
-      bool vec = aligned(a.p[i], sizeof(T) * W) && aligned(a.g[i], sizeof(GT) * W);
+      bool vec = aligned(a.p[i], align) && aligned(a.g[i], tma ? 16 : sizeof(GT) * W);
       for (int j = 0; j < 4; ++j)
-        vec = vec && aligned(a.s[j] ? (const char*)a.s[j] + soff * sizeof(T) : nullptr,
-                             sizeof(T) * W);
-      const uint64_t nvec = vec ? n / W : 0;
+        vec = vec && aligned(a.s[j] ? (const char*)a.s[j] + soff * sizeof(T) : nullptr, align);
+      const uint64_t items = vec ? n / unit : 0;
       const int t = L.n++;
       L.p[t] = a.p[i];
       L.g[t] = a.g[i];
       L.soff[t] = soff;
-      L.first_scalar[t] = nvec * W;
-      L.vbeg[t + 1] = L.vbeg[t] + nvec;
-      L.ebeg[t + 1] = L.ebeg[t] + (n - nvec * W);
+      L.first_scalar[t] = items * unit;
+      L.vbeg[t + 1] = L.vbeg[t] + items;
+      L.ebeg[t + 1] = L.ebeg[t] + (n - items * unit);
       if (L.n == kListMax) flush(i == last);
     }
     soff += n;

@@ -498,6 +498,206 @@ void launch_cfg(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) 
   }
 }
 
+// ---- list form on the pipeline (mco_flat_step_list, kernels.h FlatList) -------------
+// FlatList.vbeg holds tile prefix sums here: tile t belongs to tensor list_find(t) and
+// starts at element (t - vbeg[i]) * kTile of it; the producer resolves every tile's
+// addresses (p_i, g_i, state + soff_i), the consumers run exactly the flat kernel's
+// update.  Scalar elements (tensor tails, tensors not 16 B aligned) are spread over the
+// consumer threads of every CTA afterwards.
+template <class C, int KIND, typename GT, bool DEV>
+__global__ void __launch_bounds__(C::kConsumers + 32, 1)
+    list_tma_kernel(const __grid_constant__ FlatList L, float* s0, float* s1, float* s2,
+                    float* s3, const StepConsts<float> kv, const GraphStep gs) {
+  const StepConsts<float> k = step_consts<DEV>(kv, gs);
+  constexpr int NIN = n_in<KIND>();
+  constexpr int NS = stages<C, KIND, false>();
+  constexpr int kTile = C::kTile, kConsumers = C::kConsumers, kConsumerWarps = C::CW;
+  extern __shared__ __align__(128) uint8_t smem[];
+  float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kTile]
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * NIN * kTile);
+  uint64_t* done = full + NS;
+  __shared__ uint64_t tb[kListMax + 1], eb[kListMax + 1];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i <= L.n; i += blockDim.x) tb[i] = L.vbeg[i], eb[i] = L.ebeg[i];
+  __syncthreads();
+  const uint64_t ntiles = tb[L.n];
+  const uint64_t mine =
+      ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+
+  if (warp == kConsumerWarps) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const bool skip_gp = (KIND == K_ADAN) && k.first;  // g_prev unused at t == 1
+      const int nload = skip_gp ? NIN - 1 : NIN;
+      auto where = [&](uint64_t i, float*& p, const GT*& g, uint64_t& so) {
+        const uint64_t t = blockIdx.x + i * gridDim.x;
+        const int q = list_find(tb, L.n, t);
+        const uint64_t e = (t - tb[q]) * (uint64_t)kTile;
+        p = static_cast<float*>(L.p[q]) + e;
+        g = static_cast<const GT*>(L.g[q]) + e;
+        so = L.soff[q] + e;
+      };
+      auto issue = [&](uint64_t i) {
+        const int s = (int)(i % NS);
+        float* p;
+        const GT* g;
+        uint64_t so;
+        where(i, p, g, so);
+        const float* src[6] = {p, nullptr, s0 + so, s1 + so, s2 + so, s3 + so};
+        constexpr uint32_t gbytes = kTile * sizeof(GT);
+        mbar_expect_tx(&full[s], (uint32_t)((nload - 1) * kTile * 4) + gbytes);
+        for (int j = 0; j < nload; ++j) {
+          float* dst = buf + ((size_t)s * NIN + j) * kTile;
+          if (j == 1)
+            bulk_g2s<false>(dst, g, gbytes, &full[s], 0);
+          else
+            bulk_g2s<false>(dst, src[j], kTile * 4, &full[s], 0);
+        }
+      };
+      for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
+      for (uint64_t i = 0; i < mine; ++i) {
+        const int s = (int)(i % NS);
+        mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
+        float* p;
+        const GT* g;
+        uint64_t so;
+        where(i, p, g, so);
+        float* st = buf + (size_t)s * NIN * kTile;
+        bulk_s2g<false>(p, st, kTile * 4, 0);
+        bulk_s2g<false>(s0 + so, st + 2 * kTile, kTile * 4, 0);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN)
+          bulk_s2g<false>(s1 + so, st + 3 * kTile, kTile * 4, 0);
+        if constexpr (KIND == K_SOPHIA) {
+          if (k.refresh) bulk_s2g<false>(s1 + so, st + 3 * kTile, kTile * 4, 0);
+        }
+        if constexpr (KIND == K_ADAN) {
+          bulk_s2g<false>(s2 + so, st + 4 * kTile, kTile * 4, 0);
+          bulk_s2g<false>(s3 + so, st + 5 * kTile, kTile * 4, 0);
+        }
+        bulk_commit();
+        if (i >= 1 && i - 1 + NS < mine) {  // refill the previous tile's stage (flat kernel)
+          bulk_wait_read_1();
+          issue(i - 1 + NS);
+        }
+      }
+      bulk_wait_all();
+    }
+  } else {  // ---------------- consumers ----------------
+    constexpr int E = C::kEPT;
+    const int c0 = threadIdx.x * E;
+    for (uint64_t i = 0; i < mine; ++i) {
+      const int s = (int)(i % NS);
+      mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+      float* st = buf + (size_t)s * NIN * kTile + c0;
+      float pv[E], gv[E], a[E], b[E], c[E], d[E];
+      lds<E>(st, pv);
+      if constexpr (sizeof(GT) == 4)
+        lds<E>(st + kTile, gv);
+      else
+        lds_grad_bf16<E>(buf + (size_t)s * NIN * kTile + kTile, c0, gv);
+      lds<E>(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) lds<E>(st + 3 * kTile, b);
+      if constexpr (KIND == K_ADAN) {
+        lds<E>(st + 4 * kTile, c);
+        if (!k.first) lds<E>(st + 5 * kTile, d);
+      }
+#pragma unroll
+      for (int j = 0; j < E; ++j) {
+        if constexpr (KIND == K_LION) b[j] = 0.f;
+        if constexpr (KIND != K_ADAN) c[j] = d[j] = 0.f;
+        if constexpr (KIND == K_ADAN) {
+          if (k.first) d[j] = 0.f;
+        }
+        update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
+      }
+      sts<E>(st, pv);
+      sts<E>(st + 2 * kTile, a);
+      if constexpr (KIND != K_LION) sts<E>(st + 3 * kTile, b);
+      if constexpr (KIND == K_ADAN) {
+        sts<E>(st + 4 * kTile, c);
+        sts<E>(st + 5 * kTile, d);
+      }
+      fence_proxy_async();
+      mbar_arrive(&done[s]);
+    }
+    // scalar elements: consumers of every CTA
+    const uint64_t ne = eb[L.n];
+    for (uint64_t x = (uint64_t)blockIdx.x * kConsumers + threadIdx.x; x < ne;
+         x += (uint64_t)gridDim.x * kConsumers) {
+      const int q = list_find(eb, L.n, x);
+      const uint64_t e = L.first_scalar[q] + (x - eb[q]), o = L.soff[q] + e;
+      float* p = static_cast<float*>(L.p[q]);
+      float pp = p[e], gg = load_grad1(static_cast<const GT*>(L.g[q]) + e), aa = s0[o],
+            bb = 0.f, cc = 0.f, dd = 0.f;
+      if constexpr (KIND != K_LION) bb = s1[o];
+      if constexpr (KIND == K_ADAN) {
+        cc = s2[o];
+        if (!k.first) dd = s3[o];
+      }
+      update<KIND, float>(pp, gg, aa, bb, cc, dd, k);
+      p[e] = pp;
+      s0[o] = aa;
+      if constexpr (KIND == K_ADAMW || KIND == K_ADAN) s1[o] = bb;
+      if constexpr (KIND == K_SOPHIA) {
+        if (k.refresh) s1[o] = bb;
+      }
+      if constexpr (KIND == K_ADAN) {
+        s2[o] = cc;
+        s3[o] = dd;
+      }
+    }
+    graph_bump<DEV>(gs);  // thread 0 is a consumer
+  }
+}
+
+using ListCfg = TmaCfg<16, 4>;
+
+template <int KIND, typename GT, bool DEV>
+void run_list_tma(const FlatList& L, float* const* s, const StepConsts<float>& k,
+                  const GraphStep& gs, cudaStream_t st) {
+  using C = ListCfg;
+  auto kern = list_tma_kernel<C, KIND, GT, DEV>;
+  constexpr int smem = smem_bytes<C, KIND, false>();
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr_set{0};
+  if (!(attr_set.load() & (1ull << dev))) {
+    MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set.fetch_or(1ull << dev);
+  }
+  const uint64_t nt = L.vbeg[L.n], ne = L.ebeg[L.n];
+  const uint64_t want = std::max<uint64_t>({nt, (ne + C::kConsumers - 1) / C::kConsumers, 1});
+  const int grid = (int)std::min<uint64_t>(want, (uint64_t)device_info(dev).sms);
+  kern<<<grid, C::kConsumers + 32, smem, st>>>(L, s[0], s[1], s[2], s[3], k, gs);
+  launch_check("list_tma_kernel");
+}
+
+template <int KIND, typename GT>
+void list_tma_dev(const FlatList& L, float* const* s, const StepConsts<float>& k,
+                  const GraphStep& gs, cudaStream_t st) {
+  if (gs.d)
+    run_list_tma<KIND, GT, true>(L, s, k, gs, st);
+  else
+    run_list_tma<KIND, GT, false>(L, s, k, gs, st);
+}
+
+template <typename GT>
+void list_tma_kind(int kind, const FlatList& L, float* const* s, const StepConsts<float>& k,
+                   const GraphStep& gs, cudaStream_t st) {
+  switch (kind) {
+    case MCO_ADAMW: list_tma_dev<K_ADAMW, GT>(L, s, k, gs, st); break;
+    case MCO_LION: list_tma_dev<K_LION, GT>(L, s, k, gs, st); break;
+    case MCO_ADAN: list_tma_dev<K_ADAN, GT>(L, s, k, gs, st); break;
+    case MCO_SOPHIA: list_tma_dev<K_SOPHIA, GT>(L, s, k, gs, st); break;
+    default: throw Error(MCO_CONTRACT, "list_tma: unsupported kind");
+  }
+}
+
 }  // namespace
 
 bool flat_tma_eligible(const FlatArgs& a, int cfg) {
@@ -562,6 +762,16 @@ void launch_lomo_tma(void* p, int p_dtype, const void* g, uint64_t n, double lr,
       f32 ? run_lomo_tma<float, 8>(p, g, n, lr, scale, sumsq, clip, st)
           : run_lomo_tma<uint16_t, 8>(p, g, n, lr, scale, sumsq, clip, st);
   }
+}
+
+int list_tma_tile() { return ListCfg::kTile; }
+
+void launch_list_tma(int kind, int g_dtype, const FlatList& L, float* const* s,
+                     const StepConsts<float>& k, const GraphStep& gs, cudaStream_t st) {
+  if (g_dtype == MCO_BF16)
+    list_tma_kind<uint16_t>(kind, L, s, k, gs, st);
+  else
+    list_tma_kind<float>(kind, L, s, k, gs, st);
 }
 
 }  // namespace mco

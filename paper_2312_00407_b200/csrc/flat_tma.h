@@ -18,4 +18,10 @@ bool lomo_tma_eligible(const void* p, int p_dtype, const void* g, int g_dtype, u
 void launch_lomo_tma(void* p, int p_dtype, const void* g, uint64_t n, double lr, double scale,
                      const double* sumsq, double clip, cudaStream_t st, int stages);
 
+// List form on the pipeline (flat_list.cu): L.vbeg = tile prefix sums (list_tma_tile()
+// elements per tile; tensors 16 B aligned in p, g and state), L.ebeg = scalar elements.
+int list_tma_tile();
+void launch_list_tma(int kind, int g_dtype, const FlatList& L, float* const* s,
+                     const StepConsts<float>& k, const GraphStep& gs, cudaStream_t st);
+
 }  // namespace mco
