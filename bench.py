@@ -363,6 +363,13 @@ def bench_ours(args, rank, world, local_rank):
     out = dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
                launches=launches, clocks=clocks.summary(), P=P, owned=owned,
                shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
+    out["dev"] = dev
+    if world > 1 and not args.no_e2e:
+        try:  # every rank takes part (max-over-ranks time); failures are reported
+            out["e2e"] = bench_e2e(args, out, rank, world)
+        except Exception as ex:
+            log(f"[rank {rank}] e2e failed: {ex!r}")
+            out["e2e"] = None
     if world > 1 and not args.no_collectives:
         del p, g
         out["p"] = out["g"] = None
@@ -506,42 +513,79 @@ def pcie_ceiling(hp, dev):
     return {k: round(v, 1) for k, v in out.items()}
 
 
-def bench_e2e(args, res):
-    """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p)."""
+def bench_e2e(args, res, rank=0, world=1):
+    """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p).  N > 1: every rank
+    runs its own part (the ZeroPlan slice for the flat kinds and LOMO, every N-th tensor
+    for AdaLomo) through the same host-span calls over its own PCIe link; per-kind time =
+    max over ranks; bytes are whole-job."""
+    import math
+
     import psutil
     import torch
 
-    from paper_2312_00407_b200 import optim, registry
+    from paper_2312_00407_b200 import optim
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        import torch.distributed as dist
+
+        t = torch.tensor([x], dtype=torch.float64, device=res["dev"])
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
 
     P = res["owned"]
-    need = 2 * P * 4 * 1.3
-    avail = psutil.virtual_memory().available
-    n = P if need < avail * 0.6 else int(avail * 0.6 / (2 * 4 * 1.3)) // 1024 * 1024
-    shapes = res["shapes"]
-    if n < P:  # whole tensors prefix that fits
+    shapes = res["shapes"] if world == 1 else res["shapes"][rank::world]
+    n_ada = sum(int(math.prod(s)) for s in shapes)
+    need = 2 * max(P, n_ada) * 4 * 1.3
+    avail = psutil.virtual_memory().available / world
+    fits = need < avail * 0.6
+    n = P
+    if world == 1 and not fits:  # whole tensors prefix that fits
+        cap = int(avail * 0.6 / (2 * 4 * 1.3)) // 1024 * 1024
         acc, k = 0, 0
-        while k < len(shapes) and acc + int(__import__("math").prod(shapes[k])) <= n:
-            acc += int(__import__("math").prod(shapes[k]))
+        while k < len(shapes) and acc + int(math.prod(shapes[k])) <= cap:
+            acc += int(math.prod(shapes[k]))
             k += 1
         shapes, n = shapes[:k], acc
-    log(f"[e2e] host buffers: {n} params ({'full set' if n == P else 'prefix'}), pinned")
-    hp = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    hg = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    hp.copy_(res["p"][:n].cpu())
-    hg.copy_(res["g"][:n].cpu())
+        n_ada = n
+    ok = 1.0 if (world == 1 or fits) else 0.0
+    if world > 1:  # every rank takes the same branch (collectives follow)
+        ok = -max_over_ranks(-ok)
+    if ok < 1.0:
+        raise RuntimeError(f"e2e: host memory for {max(P, n_ada)} params per rank unavailable "
+                           f"on some rank (this rank: {avail / 1e9:.1f} GB available share)")
+    log(f"[e2e] rank {rank}: host buffers {n} params ({'full part' if n == P else 'prefix'}), "
+        f"AdaLomo {len(shapes)} tensors / {n_ada} params, pinned")
+    m = max(n, n_ada)
+    hp = torch.empty(m, dtype=torch.float32, pin_memory=True)
+    hg = torch.empty(m, dtype=torch.float32, pin_memory=True)
+    src_p, src_g = res["p"][:n].cpu(), res["g"][:n].cpu()
+    for a in range(0, m, n):  # the part's values, repeated when AdaLomo's subset is larger
+        b = min(m, a + n)
+        hp[a:b].copy_(src_p[:b - a])
+        hg[a:b].copy_(src_g[:b - a])
+    del src_p, src_g
     pcie = pcie_ceiling(hp, res["p"].device)
-    log(f"[e2e] PCIe ceiling (pinned, GB/s): {pcie}")
+    log(f"[e2e] rank {rank}: PCIe ceiling (pinned, GB/s): {pcie}")
     steps = max(1, min(args.steps, args.e2e_steps))
-    tot_s, h2d, d2h = 0.0, 0, 0
+    tot_s, h2d, d2h, h2d_me, d2h_me = 0.0, 0, 0, 0, 0
     per = {}
     opt = ada = one = None
     for kind in res["kinds"]:
         cfg = make_cfg(kind)
         opt = ada = one = None  # free the previous optimizer's device state first
         gc.collect()
-        hpn, hgn = hp.numpy(), hg.numpy()
+        k_n = n_ada if kind == "adalomo" else n
+        hpn, hgn = hp[:k_n].numpy(), hg[:k_n].numpy()
         if kind in ("adamw", "lion", "adan", "sophia"):
-            opt = optim.FlatOptimizer(cfg, n)
+            opt = optim.FlatOptimizer(cfg, k_n)
 
             def one():
                 opt.step(hpn, hgn, cfg.lr)  # mco_flat_step_host: pipelined H2D/step/D2H
@@ -555,27 +599,38 @@ def bench_e2e(args, res):
                 optim.lomo_apply(hpn, hgn, cfg.lr, 1.0)  # mco_lomo_apply_host
         one()
         torch.cuda.synchronize()
+        barrier()
         t0 = time.perf_counter()
         for _ in range(steps):
             one()
         torch.cuda.synchronize()
-        dt = (time.perf_counter() - t0) / steps
-        per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": n / dt}
+        dt = max_over_ranks((time.perf_counter() - t0) / steps)
+        total = res["P"] if world > 1 else k_n  # params of the whole job this step
+        per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": total / dt}
         tot_s += dt
-        h2d += 2 * n * 4
-        d2h += n * 4
-        log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {n / dt / 1e9:.2f} Gparam/s")
+        h2d += 2 * total * 4
+        d2h += total * 4
+        h2d_me += 2 * k_n * 4
+        d2h_me += k_n * 4
+        if rank == 0:
+            log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {total / dt / 1e9:.2f} Gparam/s")
     # the copies bound the step: max(H2D bytes / H2D BW, D2H / D2H BW, all / both-ways BW)
-    bound_s = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
-                  (h2d + d2h) / (pcie["both_gbs"] * 1e9))
-    return {"value": len(per) * n / tot_s, "unit": "params/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "params": n, "per_optimizer": per,
+    # over this rank's own link (every rank has one)
+    bound_s = max(h2d_me / (pcie["h2d_gbs"] * 1e9), d2h_me / (pcie["d2h_gbs"] * 1e9),
+                  (h2d_me + d2h_me) / (pcie["both_gbs"] * 1e9))
+    total_params = res["P"] if world > 1 else n
+    return {"value": len(per) * total_params / tot_s, "unit": "params/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "params": total_params,
+            "per_optimizer": per,
             "roofline": {"bound": "pcie", "achieved": round((h2d + d2h) / tot_s / 1e9, 1),
-                         "unit": "GB/s", "peak": pcie, "peak_source": "measured in this run",
+                         "unit": "GB/s", "peak": pcie,
+                         "peak_source": "measured in this run" + (" (rank 0's link)"
+                                                                 if world > 1 else ""),
                          "frac": round(bound_s / tot_s, 4)},
             "path": "C-ABI host-span calls on pinned host buffers: mco_flat_step_host, "
                     "mco_lomo_apply_host, mco_adalomo_apply_all_host (H2D p+g, update, D2H p "
-                    "pipelined per chunk / per tensor)"}
+                    "pipelined per chunk / per tensor)" + (
+                        f"; each of {world} ranks over its own part" if world > 1 else "")}
 
 
 def main():
@@ -640,7 +695,7 @@ def main():
         local_rank = local_rank % max(torch.cuda.device_count(), 1)
     res = bench_ours(args, rank, world, local_rank)
     config["params"] = res["P"]
-    e2e = None
+    e2e = res.get("e2e")
     cpu = None
     if rank == 0 and world == 1 and not args.no_e2e:
         try:
