@@ -79,7 +79,10 @@ def _worker(rank, world, port, out_q):
                                                clip_norm=clip, group=dist.group.WORLD,
                                                bucket_elems=bucket, ops=CpuOps)
             assert all(p.grad is None for p in net.parameters())
-            res[(clip, bucket)] = torch.cat([p.detach().reshape(-1) for p in net.parameters()])
+            res[(clip, bucket)] = torch.cat(
+                [p.detach().reshape(-1) for p in net.parameters()]).numpy().copy()
+        # numpy, not tensors: a tensor in a Queue is passed by file descriptor, which
+        # races with this process's exit
         out_q.put((rank, res))
     finally:
         dist.destroy_process_group()
@@ -117,6 +120,7 @@ def test_fused_lomo_dp_per_parameter_and_bucketed_equal_serial():
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
+    res = {r: {k: torch.from_numpy(v) for k, v in d.items()} for r, d in res.items()}
     for clip, bucket in CASES:
         want = _serial(2, clip)
         for r in range(2):
