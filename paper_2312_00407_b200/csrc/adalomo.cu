@@ -608,8 +608,8 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
               const float4 b1 = *reinterpret_cast<const float4*>(fb + col + 4);
               const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-              for (int j = 0; j < VW; ++j) {
-                const float x = u_fact(gv[u][j], sf, a, bv[j], epsf);
+              for (int j = 0; j < VW; ++j) {  // s is applied once per chunk (s^2 below)
+                const float x = gv[u][j] * rsqrt_ftz(__fmaf_rn(a, bv[j], epsf));
                 su = __fmaf_rn(x, x, su);
               }
             } else {
@@ -619,7 +619,7 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
                 if (ej < ch.e1) {
                   uint32_t row, col;
                   row_col((uint32_t)ej, T, C, row, col);
-                  const float x = u_fact(gv[u][j], sf, fa[row], fb[col], epsf);
+                  const float x = gv[u][j] * rsqrt_ftz(__fmaf_rn(fa[row], fb[col], epsf));
                   su = __fmaf_rn(x, x, su);
                 }
               }
@@ -628,6 +628,8 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
         }
         usq += (double)su;
       }
+      usq *= (double)sf * (double)sf;  // sum (s g r)^2 = s^2 sum (g r)^2: one multiply less
+                                       // per element (K4 is issue-bound on bf16 data)
     } else {  // optim.cpp:262-267 with fp64 state
       const double s = c.glob[0];
       const double corr = c.tens_sc[ch.tensor * kTensScalars + TS_CORR];
