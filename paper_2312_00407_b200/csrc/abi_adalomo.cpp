@@ -79,6 +79,7 @@ void check_ada_dtypes(int pdt, int gdt) {
 mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, const void* grad,
                              int gdt, double lr, const double* dev_grad_sumsq, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply: null handle");
     if (idx < 0 || idx >= (int)h->plan.h_tensors.size())  // optim.cpp:212
       throw Error(MCO_CONTRACT, "adalomo: unknown parameter '" + std::to_string(idx) + "'");
     check_ada_dtypes(pdt, gdt);
@@ -105,6 +106,7 @@ mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* p
                                   int pdt, const void* const* grads, int gdt, double lr,
                                   const double* dev_grad_sumsq, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply_list: null handle");
     const int nt = (int)h->plan.h_tensors.size();
     if (t0 < 0 || t1 > nt || t0 > t1)
       throw Error(MCO_CONTRACT, "adalomo: tensor range [" + std::to_string(t0) + ", " +
@@ -138,6 +140,7 @@ mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* p
 mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const void* flat_g,
                                  int gdt, double lr, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply_all: null handle");
     check_ada_dtypes(pdt, gdt);
     DeviceGuard dg(h->plan.device);
     AdaLomoCall c{};
@@ -163,6 +166,7 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
 mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const void* g, int gdt,
                                       double lr) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply_all_host: null handle");
     check_ada_dtypes(pdt, gdt);
     auto& pl = h->plan;
     DeviceGuard dg(pl.device);
@@ -236,6 +240,7 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
 // one rank for a replica, 0 elsewhere).
 mco_status mco_adalomo_set_shard(mco_adalomo* h, int idx, int64_t global_rows, double weight) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_set_shard: null handle");
     auto& pl = h->plan;
     if (idx < 0 || idx >= (int)pl.h_tensors.size())
       throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
@@ -259,6 +264,7 @@ mco_status mco_adalomo_set_shard(mco_adalomo* h, int idx, int64_t global_rows, d
 mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_p, int pdt,
                              const void* flat_g, int gdt, double lr, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_phase: null handle");
     check_ada_dtypes(pdt, gdt);
     if (phase < 1 || phase > 3) throw Error(MCO_CONTRACT, "adalomo: phase must be 1, 2 or 3");
     DeviceGuard dg(h->plan.device);
@@ -281,6 +287,7 @@ mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_p, int pdt,
 // which 0: stats payload (3 per tensor + column sums), 1: sum u^2 payload.
 mco_status mco_adalomo_payload(mco_adalomo* h, int which, double** dev_ptr, uint64_t* len) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_payload: null handle");
     if (which == 0) {
       *dev_ptr = h->plan.d_payload;
       *len = (uint64_t)h->plan.stats_len;
@@ -295,11 +302,15 @@ mco_status mco_adalomo_payload(mco_adalomo* h, int which, double** dev_ptr, uint
 
 // optim.cpp:277-282 (fp64 state, as the reference)
 mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out) {
-  return guard([&] { *out = (uint64_t)h->plan.state_len * sizeof(double); });
+  return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_state_bytes: null handle");
+    *out = (uint64_t)h->plan.state_len * sizeof(double);
+  });
 }
 
 mco_status mco_adalomo_get_steps(const mco_adalomo* h, int idx, int64_t* t) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_get_steps: null handle");
     if (idx < 0 || idx >= (int)h->plan.h_tensors.size())
       throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
     // the device counter is the truth (K2 advances it): steps replayed from a captured
@@ -313,6 +324,7 @@ mco_status mco_adalomo_get_steps(const mco_adalomo* h, int idx, int64_t* t) {
 
 mco_status mco_adalomo_buffer(mco_adalomo* h, int idx, int which, void** ptr, uint64_t* len) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_buffer: null handle");
     if (idx < 0 || idx >= (int)h->plan.h_tensors.size())
       throw Error(MCO_CONTRACT, "adalomo: tensor index out of range");
     const TensorInfo& T = h->plan.h_tensors[idx];

@@ -145,6 +145,7 @@ void check_dtypes(const mco_flat* h, int pdt, int gdt) {
 mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
                          int gdt, uint64_t ng, double lr, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_step: null handle");
     check_lengths(h, np, ng);
     check_dtypes(h, pdt, gdt);
     DeviceGuard dg(h->device);
@@ -157,6 +158,7 @@ mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const 
 mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, int gdt,
                                uint16_t* pout, uint64_t n, double lr, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_mixed: null handle");
     check_lengths(h, n, n);
     check_dtypes(h, MCO_F32, gdt);
     if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
@@ -178,6 +180,7 @@ mco_status mco_flat_step_list(mco_flat* h, int count, void* const* params, int p
                               const void* const* grads, int gdt, const uint64_t* lens,
                               double lr, void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_list: null handle");
     if (count < 0 || (count > 0 && (!params || !grads || !lens)))
       throw Error(MCO_CONTRACT, "step list: null table");
     uint64_t total = 0;
@@ -216,6 +219,7 @@ mco_status mco_flat_step_list(mco_flat* h, int count, void* const* params, int p
 mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
                               int gdt, uint64_t ng, double lr) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_host: null handle");
     check_lengths(h, np, ng);
     check_dtypes(h, pdt, gdt);
     no_graph(h, "host-span step");
@@ -230,6 +234,7 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, c
 
 mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_get_steps: null handle");
     if (h->gdev) {
       DeviceGuard dg(h->device);
       *t = graph_steps(h);
@@ -240,6 +245,7 @@ mco_status mco_flat_get_steps(const mco_flat* h, int64_t* t) {
 }
 mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_set_steps: null handle");
     h->t = t;
     if (h->gdev) {
       DeviceGuard dg(h->device);
@@ -255,6 +261,7 @@ mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
 // host's own, tabulated up to the step where every 1 - beta_k^t has rounded to 1.0).
 mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_graph_enable: null handle");
     DeviceGuard dg(h->device);
     if (h->gdev) {  // already on: only the lr source changes
       h->glr = dev_lr;
@@ -296,6 +303,7 @@ mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr) {
 
 mco_status mco_flat_graph_disable(mco_flat* h) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_graph_disable: null handle");
     if (!h->gdev) return;
     DeviceGuard dg(h->device);
     h->t = graph_steps(h);
@@ -303,17 +311,27 @@ mco_status mco_flat_graph_disable(mco_flat* h) {
   });
 }
 mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out) {
-  return guard([&] { *out = h->named.size() * h->n * dtype_size(h->state_dtype); });
+  return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_state_bytes: null handle");
+    *out = h->named.size() * h->n * dtype_size(h->state_dtype);
+  });
 }
 mco_status mco_flat_config(const mco_flat* h, mco_config* out) {
-  return guard([&] { *out = h->cfg; });
+  return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_config: null handle");
+    *out = h->cfg;
+  });
 }
 mco_status mco_flat_num_buffers(const mco_flat* h, int* out) {
-  return guard([&] { *out = (int)h->named.size(); });
+  return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_num_buffers: null handle");
+    *out = (int)h->named.size();
+  });
 }
 mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, uint64_t* len,
                            int* dtype) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_buffer: null handle");
     if (i < 0 || i >= (int)h->named.size())
       throw Error(MCO_CONTRACT, "buffers(): index out of range");
     h->exposed = true;  // callers may keep the pointer: no more relayout
@@ -330,6 +348,7 @@ mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int gr
                                float* master, uint64_t offset, uint64_t n, double lr,
                                void* stream) {
   return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_peers: null handle");
     check_lengths(h, n, n);
     if (h->state_dtype != MCO_F32)
       throw Error(MCO_CONTRACT, "peer step: f32 optimizer state required");

@@ -174,6 +174,7 @@ mco_status mco_comm_destroy(mco_comm* c) {
 
 mco_status mco_comm_check(mco_comm* c) {
   return guard([&] {
+    if (!c) throw Error(MCO_CONTRACT, "mco_comm_check: null handle");
     ncclResult_t r = ncclSuccess;
     MCO_NCCL_CHECK(nccl().comm_get_async_error(c->comm, &r));
     nccl_check(r, "NCCL asynchronous error");
@@ -182,6 +183,7 @@ mco_status mco_comm_check(mco_comm* c) {
 
 mco_status mco_comm_allreduce_sum(mco_comm* c, void* buf, int dtype, uint64_t n, void* stream) {
   return guard([&] {
+    if (!c) throw Error(MCO_CONTRACT, "mco_comm_allreduce_sum: null handle");
     DeviceGuard ds(c->device);
     MCO_NCCL_CHECK(nccl().all_reduce(buf, buf, n, nccl_type(dtype), ncclSum, c->comm,
                                      (cudaStream_t)stream));
@@ -264,6 +266,7 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
                           const void* flat_grads, int grad_dtype, uint64_t total_len, double lr,
                           void* stream) {
   return guard([&] {
+    if (!h || !c) throw Error(MCO_CONTRACT, "mco_shard_step: null handle");
     if (!c) throw Error(MCO_CONTRACT, "shard step: null argument");
     const size_t ps = dt_size(param_dtype);
     std::vector<uint64_t> parts(c->nranks), offs(c->nranks + 1);
@@ -286,6 +289,7 @@ mco_status mco_shard_step_mixed(mco_flat* h, mco_comm* c, float* master_owned,
                                 uint16_t* flat_params_bf16, const void* flat_grads,
                                 int grad_dtype, uint64_t total_len, double lr, void* stream) {
   return guard([&] {
+    if (!h || !c) throw Error(MCO_CONTRACT, "mco_shard_step_mixed: null handle");
     if (!master_owned) throw Error(MCO_CONTRACT, "shard step: null master");
     shard_run(h, c, flat_grads, grad_dtype, total_len, flat_params_bf16, MCO_BF16,
               master_owned, sizeof(float), stream,

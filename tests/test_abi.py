@@ -64,3 +64,35 @@ def test_flat_variant_knob_host_side():
     optim.set_flat_variant("ldg")
     assert optim.flat_variant() == "ldg"
     optim.set_flat_variant(prev)
+
+
+def test_null_handles_are_contract_errors():
+    """Every entry point taking a handle (mco_flat / mco_adalomo / mco_comm) returns
+    MCO_CONTRACT with a message for a NULL handle, before touching the device."""
+    import re
+
+    header = open(_lib.HEADER_PATH).read() if hasattr(_lib, "HEADER_PATH") else None
+    if header is None:
+        import os
+
+        header = open(os.path.join(os.path.dirname(os.path.dirname(_lib.__file__)), "include",
+                                   "mco.h")).read()
+    decls = re.findall(r"mco_status (mco_\w+)\(([^;]*?)\);", header, re.S)
+    checked = 0
+    for name, args in decls:
+        first = args.split(",")[0]
+        if not re.search(r"mco_(flat|adalomo|comm)\s*\*", first) or name.endswith("destroy"):
+            continue
+        fn = getattr(_lib.lib, name)
+        argv = []
+        for t in fn.argtypes:
+            if t in (C.c_double, C.c_float):
+                argv.append(0.0)
+            elif t in (C.c_int, C.c_int64, C.c_uint64, C.c_uint32):
+                argv.append(0)
+            else:
+                argv.append(None)
+        assert fn(*argv) == _lib.MCO_CONTRACT, name
+        assert "null handle" in _lib.lib.mco_last_error().decode(), name
+        checked += 1
+    assert checked >= 25
