@@ -56,6 +56,11 @@ mco_status mco_flat_destroy(mco_flat* h) {
 }
 
 namespace {
+// n > 0 elements behind a null pointer would fault on the device: a contract error
+void check_data(uint64_t n, const void* a, const void* b, const char* what) {
+  if (n && (!a || !b)) throw Error(MCO_CONTRACT, std::string(what) + ": null data pointer");
+}
+
 void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
   if (np != ng)  // optim.cpp:101-103
     throw Error(MCO_CONTRACT, "optimizer step: params/grads length mismatch: " +
@@ -147,6 +152,7 @@ mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const 
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_flat_step: null handle");
     check_lengths(h, np, ng);
+    check_data(np, params, grads, "optimizer step");
     check_dtypes(h, pdt, gdt);
     DeviceGuard dg(h->device);
     align_state_to(h, params);
@@ -160,6 +166,7 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_mixed: null handle");
     check_lengths(h, n, n);
+    check_data(n, master, grads, "mixed step");
     check_dtypes(h, MCO_F32, gdt);
     if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
     if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
@@ -221,6 +228,7 @@ mco_status mco_flat_step_host(mco_flat* h, void* params, int pdt, uint64_t np, c
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_flat_step_host: null handle");
     check_lengths(h, np, ng);
+    check_data(np, params, grads, "optimizer step");
     check_dtypes(h, pdt, gdt);
     no_graph(h, "host-span step");
     DeviceGuard dg(h->device);
@@ -446,13 +454,17 @@ mco_status mco_peer_close(void* p) {
 // ---- LOMO -------------------------------------------------------------------------
 mco_status mco_lomo_apply(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                           double scale, void* stream) {
-  return guard([&] { launch_lomo(p, pdt, g, gdt, n, lr, scale, nullptr, 0.0, (cudaStream_t)stream); });
+  return guard([&] {
+    check_data(n, p, g, "lomo_apply");
+    launch_lomo(p, pdt, g, gdt, n, lr, scale, nullptr, 0.0, (cudaStream_t)stream);
+  });
 }
 
 mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                                   const double* dev_sumsq, double clip, void* stream) {
   return guard([&] {
     if (!dev_sumsq) throw Error(MCO_CONTRACT, "lomo clip: device sum of squares is null");
+    check_data(n, p, g, "lomo_apply_clipped");
     launch_lomo(p, pdt, g, gdt, n, lr, 1.0, dev_sumsq, clip, (cudaStream_t)stream);
   });
 }
@@ -462,6 +474,7 @@ mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint
 mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                                double scale, double clip) {
   return guard([&] {
+    check_data(n, p, g, "lomo_apply_host");
     const int dev = current_device();
     const double* dnorm = nullptr;
     double* acc = nullptr;
@@ -502,6 +515,8 @@ mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* out, int accu
                      void* stream) {
   return guard([&] {
     dtype_size(dtype);
+    check_data(n, x, x, "sumsq");
+    if (!out) throw Error(MCO_CONTRACT, "sumsq: null output");
     cudaStream_t st = (cudaStream_t)stream;
     launch_sumsq(x, dtype, n, out, accumulate, sumsq_ws(st), st);
   });

@@ -96,3 +96,15 @@ def test_null_handles_are_contract_errors():
         assert "null handle" in _lib.lib.mco_last_error().decode(), name
         checked += 1
     assert checked >= 25
+
+
+def test_null_data_pointers_are_contract_errors():
+    """n > 0 elements behind a NULL pointer is refused on the host (it would fault on
+    the device and poison the context)."""
+    L = _lib.lib
+    assert L.mco_lomo_apply(None, _lib.MCO_F32, None, _lib.MCO_F32, 8, 1e-3, 1.0,
+                            None) == _lib.MCO_CONTRACT
+    assert "null data pointer" in L.mco_last_error().decode()
+    assert L.mco_lomo_apply_host(None, _lib.MCO_F32, None, _lib.MCO_F32, 8, 1e-3, 1.0,
+                                 -1.0) == _lib.MCO_CONTRACT
+    assert L.mco_sumsq(None, _lib.MCO_F32, 8, None, 0, None) == _lib.MCO_CONTRACT
