@@ -83,6 +83,7 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, cons
     if (idx < 0 || idx >= (int)h->plan.h_tensors.size())  // optim.cpp:212
       throw Error(MCO_CONTRACT, "adalomo: unknown parameter '" + std::to_string(idx) + "'");
     check_ada_dtypes(pdt, gdt);
+    if (!param || !grad) throw Error(MCO_CONTRACT, "adalomo: null data pointer");
     DeviceGuard dg(h->plan.device);
     AdaLomoCall c{};
     c.t0 = idx;
@@ -112,6 +113,7 @@ mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* p
       throw Error(MCO_CONTRACT, "adalomo: tensor range [" + std::to_string(t0) + ", " +
                                     std::to_string(t1) + ") outside 0.." + std::to_string(nt));
     check_ada_dtypes(pdt, gdt);
+    if (t1 > t0 && (!params || !grads)) throw Error(MCO_CONTRACT, "adalomo: null table");
     for (int k = t0; k < t1; ++k)
       if (!params[k - t0] || !grads[k - t0])
         throw Error(MCO_CONTRACT, "adalomo: null tensor pointer for index " + std::to_string(k));
@@ -142,6 +144,7 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply_all: null handle");
     check_ada_dtypes(pdt, gdt);
+    if (!flat_p || !flat_g) throw Error(MCO_CONTRACT, "adalomo: null data pointer");
     DeviceGuard dg(h->plan.device);
     AdaLomoCall c{};
     c.t0 = 0;
@@ -168,6 +171,7 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_apply_all_host: null handle");
     check_ada_dtypes(pdt, gdt);
+    if (!p || !g) throw Error(MCO_CONTRACT, "adalomo: null data pointer");
     auto& pl = h->plan;
     DeviceGuard dg(pl.device);
     const int nt = (int)pl.h_tensors.size();
