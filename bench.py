@@ -672,7 +672,8 @@ def main():
         config["params"] = LLAMA_7B.param_count()
         line = {"impl": "reference", "metric": metric, "value": value, "unit": "params/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": sec_step * 1e3, "higher_is_better": True, "scaling": "weak",
+                "ms_per_step": sec_step * 1e3, "higher_is_better": True,
+                "scaling": "strong" if world > 1 else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": value, "unit": "params/s", "cores": threads,
                                  "kind": "reference", "cpu_model": cpu_model(),
