@@ -1,6 +1,9 @@
 """Randomised parity sweep (fixed seed): random optimizer kind, length, element
-offset (alignment), gradient dtype, hyper-parameters and step count -- the fp32
-kernels must stay bit-exact with the restatement for every draw."""
+offset (alignment), gradient dtype, hyper-parameters, step count and graph mode -- the
+fp32 kernels must stay bit-exact with the restatement for every draw.
+MCO_RANDOM_CASES=N widens the stored-state sweep (default 40)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -12,15 +15,17 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 rng = np.random.default_rng(20260)
+grng = np.random.default_rng(7)  # graph-mode draws (keeps the other draws unchanged)
 CASES = []
-for i in range(40):
+for i in range(int(os.environ.get("MCO_RANDOM_CASES", "40"))):
     CASES.append(dict(kind=int(rng.integers(0, 4)), n=int(rng.choice([1, 7, 8, 9, 63, 4096,
                                                                        12345, 100003])),
                       off=int(rng.integers(0, 9)), bf16=bool(rng.random() < 0.3),
                       mixed=bool(rng.random() < 0.3), lr=float(10 ** rng.uniform(-5, -1)),
                       wd=float(rng.choice([0.0, 0.01, 0.1])), b1=float(rng.uniform(0.5, 0.99)),
                       b2=float(rng.uniform(0.9, 0.9999)), b3=float(rng.uniform(0.9, 0.999)),
-                      k=int(rng.integers(1, 5)), steps=int(rng.integers(1, 5)), seed=i))
+                      k=int(rng.integers(1, 5)), steps=int(rng.integers(1, 5)), seed=i,
+                      graph=bool(grng.random() < 0.3)))
 
 
 @pytest.mark.parametrize("c", CASES, ids=[f"case{i}" for i in range(len(CASES))])
@@ -33,6 +38,8 @@ def test_random_case_bit_exact(c):
     tp = torch.from_numpy(pbig.copy()).cuda()
     p = pbig[off:].copy()
     opt, orc = optim.FlatOptimizer(cfg, n), O.OracleFlat(cfg, n, np.float32)
+    if c["graph"]:  # device step counter + tabulated scalars (mco_flat_graph_enable)
+        opt.enable_graph()
     out = torch.empty(n, dtype=torch.bfloat16, device="cuda") if c["mixed"] else None
     for t in range(1, c["steps"] + 1):
         if c["bf16"]:
