@@ -3,6 +3,8 @@ over the flat state.  Bar: bit-identical to FlatOptimizer::step (optim.cpp:100-1
 over the concatenated vector -- parameters and every state buffer -- for every kind and
 dtype mode, with odd / empty / unaligned tensors, more tensors than one launch carries,
 and in graph mode."""
+import os
+
 import pytest
 
 from paper_2312_00407_b200 import optim
@@ -123,10 +125,11 @@ def test_list_contract_errors():
     assert opt.steps_taken() == 1
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("MCO_LIST_CASES", "12"))))
 def test_list_randomised_sweep(seed):
     """Random kinds, dtype modes, tensor counts (1-90: up to three launches), sizes
-    (odd, tiny, vector-sized, empty) and step counts: list == flat, bit for bit."""
+    (odd, tiny, vector-sized, empty), step counts and graph mode: list == flat, bit for
+    bit.  MCO_LIST_CASES=N widens the sweep (default 12)."""
     import random
 
     rnd = random.Random(seed)
@@ -144,6 +147,8 @@ def test_list_randomised_sweep(seed):
     total = sum(sizes)
     flat = optim.FlatOptimizer(cfg, max(total, 1), state_dtype=sd)
     lst = optim.FlatOptimizer(cfg, max(total, 1), state_dtype=sd)
+    if rnd.random() < 0.3:
+        lst.enable_graph()  # eager calls on the device step counter
     flat_p = torch.cat([p.reshape(-1) for p in ps])
     for t, g in enumerate(gs):
         lr = rnd.choice([1e-4, 1e-3, 3e-2])
