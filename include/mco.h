@@ -187,6 +187,14 @@ mco_status mco_lomo_apply(void* params, int param_dtype, const void* grads, int 
                           uint64_t n, double lr, double scale, void* stream);
 /* Same, with the clip scale computed on the device from a device Σg²
  * (optim.cpp:302-303: scale = clip/‖g‖ iff ‖g‖ > clip and ‖g‖ > 0). */
+/* LOMO list form: `count` tensors at separate device pointers (lens[i] elements each) in
+ * one launch per 40 tensors; each tensor's update equals mco_lomo_apply's bit for bit.
+ * dev_sumsq (nullable): device global sum of squares -> clip scale as
+ * mco_lomo_apply_clipped (then `scale` is ignored). */
+mco_status mco_lomo_apply_list(int count, void* const* params, int param_dtype,
+                               const void* const* grads, int grad_dtype, const uint64_t* lens,
+                               double lr, double scale, const double* dev_sumsq, double clip,
+                               void* stream);
 mco_status mco_lomo_apply_clipped(void* params, int param_dtype, const void* grads,
                                   int grad_dtype, uint64_t n, double lr, const double* dev_sumsq,
                                   double clip, void* stream);

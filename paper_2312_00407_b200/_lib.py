@@ -89,6 +89,8 @@ _SIGS = {
     "mco_peer_close": (_i, [_p]),
     "mco_lomo_apply": (_i, [_p, _i, _p, _i, _u64, _d, _d, _p]),
     "mco_lomo_apply_clipped": (_i, [_p, _i, _p, _i, _u64, _d, _p, _d, _p]),
+    "mco_lomo_apply_list": (_i, [_i, C.POINTER(_p), _i, C.POINTER(_p), _i, C.POINTER(_u64),
+                                 _d, _d, _p, _d, _p]),
     "mco_sumsq": (_i, [_p, _i, _u64, _p, _i, _p]),
     "mco_lomo_apply_host": (_i, [_p, _i, _p, _i, _u64, _d, _d, _d]),
     "mco_adalomo_apply_all_host": (_i, [_p, _p, _i, _p, _i, _d]),

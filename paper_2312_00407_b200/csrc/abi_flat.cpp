@@ -460,6 +460,23 @@ mco_status mco_lomo_apply(void* p, int pdt, const void* g, int gdt, uint64_t n, 
   });
 }
 
+// LOMO list form: `count` tensors at separate device pointers in one launch per 40
+// tensors -- each tensor's update is lomo_apply's, bit for bit (optim.cpp:185-190);
+// dev_sumsq != null applies the global-norm clip rule (optim.cpp:291-303).
+mco_status mco_lomo_apply_list(int count, void* const* params, int pdt,
+                               const void* const* grads, int gdt, const uint64_t* lens,
+                               double lr, double scale, const double* dev_sumsq, double clip,
+                               void* stream) {
+  return guard([&] {
+    if (count < 0 || (count > 0 && (!params || !grads || !lens)))
+      throw Error(MCO_CONTRACT, "lomo_apply_list: null table");
+    for (int i = 0; i < count; ++i)
+      check_data(lens[i], params[i], grads[i], "lomo_apply_list");
+    launch_lomo_list(count, params, pdt, grads, gdt, lens, lr, scale, dev_sumsq, clip,
+                     (cudaStream_t)stream);
+  });
+}
+
 mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                                   const double* dev_sumsq, double clip, void* stream) {
   return guard([&] {

@@ -239,12 +239,6 @@ __global__ void __launch_bounds__(kThreads)
 
 // ---- LOMO ---------------------------------------------------------------------
 
-template <typename PT, typename GT>
-constexpr int lomo_width() {
-  if constexpr (std::is_same<PT, double>::value) return 4;
-  if constexpr (std::is_same<PT, uint16_t>::value && std::is_same<GT, uint16_t>::value) return 16;
-  return 8;
-}
 
 template <typename PT, typename GT>
 __global__ void __launch_bounds__(kThreads)

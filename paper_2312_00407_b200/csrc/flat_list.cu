@@ -206,6 +206,93 @@ void list_dtypes(const FlatListArgs& a, const StepConsts<float>& kf,
   }
 }
 
+// ---- LOMO list form (mco_lomo_apply_list) -------------------------------------------
+// p_i -= f * g_i over separate tensors in one launch per kListMax tensors: lomo_kernel's
+// loads, arithmetic and stores per W-element vector (vbeg: vectors), scalar tails.
+template <typename PT, typename GT>
+__global__ void __launch_bounds__(kThreads)
+    lomo_list_kernel(const __grid_constant__ FlatList L, double lr, double scale,
+                     const double* __restrict__ sumsq, double clip) {
+  using T = typename std::conditional<std::is_same<PT, double>::value, double, float>::type;
+  constexpr int W = lomo_width<PT, GT>();
+  __shared__ uint64_t vb[kListMax + 1], eb[kListMax + 1];
+  pdl_wait();
+  for (int i = threadIdx.x; i <= L.n; i += blockDim.x) vb[i] = L.vbeg[i], eb[i] = L.ebeg[i];
+  __syncthreads();
+  const T f = lomo_factor<T>(lr, scale, sumsq, clip);
+  const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t nv = vb[L.n];
+  for (uint64_t vi = tid; vi < nv; vi += stride) {
+    const int i = list_find(vb, L.n, vi);
+    const uint64_t e = (vi - vb[i]) * W;
+    PT* p = static_cast<PT*>(L.p[i]) + e;
+    const GT* g = static_cast<const GT*>(L.g[i]) + e;
+    T pv[W], gv[W];
+    if constexpr (W == 16) {
+      ld_stream_bf16x16(p, pv);
+      ld_stream_ro_bf16x16(g, gv);
+    } else {
+      if constexpr (std::is_same<PT, uint16_t>::value)
+        ld_stream_bf16x8(p, pv);
+      else
+        ld_stream(p, pv);
+      load_grad(g, gv);
+    }
+#pragma unroll
+    for (int j = 0; j < W; ++j) pv[j] = pv[j] - f * gv[j];
+    if constexpr (W == 16)
+      st_stream_bf16x16(p, pv);
+    else if constexpr (std::is_same<PT, uint16_t>::value)
+      st_stream_bf16x8(p, pv);
+    else
+      st_stream(p, pv);
+  }
+  const uint64_t ne = eb[L.n];
+  for (uint64_t x = tid; x < ne; x += stride) {
+    const int i = list_find(eb, L.n, x);
+    const uint64_t e = L.first_scalar[i] + (x - eb[i]);
+    PT* p = static_cast<PT*>(L.p[i]);
+    const GT* g = static_cast<const GT*>(L.g[i]);
+    if constexpr (std::is_same<PT, uint16_t>::value)
+      p[e] = (uint16_t)f2bf_bits(bf2f(p[e]) - f * load_grad1(g + e));
+    else
+      p[e] = p[e] - f * (T)load_grad1(g + e);
+  }
+}
+
+template <typename PT, typename GT>
+void lomo_list_chunks(int count, void* const* ps, const void* const* gs, const uint64_t* len,
+                      double lr, double scale, const double* sumsq, double clip,
+                      cudaStream_t st) {
+  constexpr int W = lomo_width<PT, GT>();
+  auto kern = lomo_list_kernel<PT, GT>;
+  FlatList L{};
+  auto flush = [&] {
+    if (L.n == 0) return;
+    const uint64_t items = std::max<uint64_t>(std::max(L.vbeg[L.n], L.ebeg[L.n]), 1);
+    const int grid = grid_for(kern, items, current_device());
+    launch_pdl(kern, grid, kThreads, st, L, lr, scale, sumsq, clip);
+    launch_check("lomo_list_kernel");
+    L = FlatList{};
+  };
+  for (int i = 0; i < count; ++i) {
+    const uint64_t n = len[i];
+    if (!n) continue;
+    const bool vec = aligned(ps[i], sizeof(PT) * W) && aligned(gs[i], sizeof(GT) * W);
+    const uint64_t nvec = vec ? n / W : 0;
+    const int t = L.n++;
+    L.p[t] = ps[i];
+    L.g[t] = gs[i];
+    L.soff[t] = 0;
+    L.first_scalar[t] = nvec * W;
+    L.vbeg[t + 1] = L.vbeg[t] + nvec;
+    L.ebeg[t + 1] = L.ebeg[t] + (n - nvec * W);
+    if (L.n == kListMax) flush();
+  }
+  flush();
+}
+
 }  // namespace
 
 void launch_flat_step_list(const FlatListArgs& a, const StepConsts<float>& kf,
@@ -217,6 +304,21 @@ void launch_flat_step_list(const FlatListArgs& a, const StepConsts<float>& kf,
     case MCO_SOPHIA: list_dtypes<K_SOPHIA>(a, kf, kd, st); break;
     default: throw Error(MCO_CONTRACT, "FlatOptimizer: fused kind");
   }
+}
+
+void launch_lomo_list(int count, void* const* p, int p_dtype, const void* const* g, int g_dtype,
+                      const uint64_t* len, double lr, double scale, const double* dev_sumsq,
+                      double clip, cudaStream_t st) {
+  if (p_dtype == MCO_F32 && g_dtype == MCO_F32)
+    lomo_list_chunks<float, float>(count, p, g, len, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_F32 && g_dtype == MCO_BF16)
+    lomo_list_chunks<float, uint16_t>(count, p, g, len, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_BF16 && g_dtype == MCO_BF16)
+    lomo_list_chunks<uint16_t, uint16_t>(count, p, g, len, lr, scale, dev_sumsq, clip, st);
+  else if (p_dtype == MCO_F64 && g_dtype == MCO_F64)
+    lomo_list_chunks<double, double>(count, p, g, len, lr, scale, dev_sumsq, clip, st);
+  else
+    throw Error(MCO_CONTRACT, "lomo_apply_list: unsupported param/grad dtype pair");
 }
 
 }  // namespace mco

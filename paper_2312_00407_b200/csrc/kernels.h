@@ -55,6 +55,11 @@ struct FlatListArgs {
   void* s[4];  // state slots at the list's first element
   GraphStep gs;
 };
+// LOMO over separate tensors (FlatList vbeg = vectors, no state), one launch per
+// kListMax tensors; dev_sumsq != null: the global-norm clip scale from the device sum.
+void launch_lomo_list(int count, void* const* p, int p_dtype, const void* const* g, int g_dtype,
+                      const uint64_t* len, double lr, double scale, const double* dev_sumsq,
+                      double clip, cudaStream_t st);
 void launch_flat_step_list(const FlatListArgs& a, const StepConsts<float>& kf,
                            const StepConsts<double>& kd, cudaStream_t st);
 

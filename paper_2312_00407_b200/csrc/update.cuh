@@ -2,6 +2,8 @@
 // peer-memory ZeRO kernel (peer.cu).  Operation order = optim.cpp:114-167.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace mco {
@@ -101,6 +103,14 @@ __device__ __forceinline__ void load_grad(const uint16_t* g, float (&r)[4]) {
 __device__ __forceinline__ float load_grad1(const float* g) { return *g; }
 __device__ __forceinline__ float load_grad1(const uint16_t* g) { return bf2f(*g); }
 __device__ __forceinline__ double load_grad1(const double* g) { return *g; }
+
+// LOMO elements per 256-bit access: f64 4, bf16 params + bf16 grads 16, else 8.
+template <typename PT, typename GT>
+constexpr int lomo_width() {
+  if constexpr (std::is_same<PT, double>::value) return 4;
+  if constexpr (std::is_same<PT, uint16_t>::value && std::is_same<GT, uint16_t>::value) return 16;
+  return 8;
+}
 
 constexpr bool reads_s1(int k) { return k == K_ADAMW || k == K_ADAN || k == K_SOPHIA; }
 

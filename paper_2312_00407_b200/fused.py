@@ -28,6 +28,7 @@ class _CudaOps:
     sumsq = staticmethod(optim.sumsq)
     lomo_apply = staticmethod(optim.lomo_apply)
     lomo_apply_clipped = staticmethod(optim.lomo_apply_clipped)
+    lomo_apply_list = staticmethod(optim.lomo_apply_list)
 
 
 def _hooks(params, fn):
@@ -99,7 +100,7 @@ class _GradPath:
         self._allreduce(self.buf[:self.used])
         views = [(p, self.buf[off:off + n].view_as(p)) for p, off, n in self.items]
         if self.group_fn is not None:
-            self.group_fn(views)  # the whole bucket in one call (AdaLomo list form)
+            self.group_fn(views)  # the whole bucket in one call (list forms)
         else:
             for p, g in views:
                 self.fn(p, g)
@@ -148,7 +149,13 @@ def lomo_fused_backward_step(params: Sequence, loss_fn: Callable, lr: float,
             else:
                 ops.lomo_apply_clipped(p.data, g, lr, norm2, clip_norm)
 
-    return _run_backward(params, upd, loss_fn, group, bucket_elems, True)
+    def upd_bucket(views):  # the whole bucket in one launch (mco_lomo_apply_list)
+        with torch.no_grad():
+            ops.lomo_apply_list([p.data for p, _ in views], [g for _, g in views], lr, 1.0,
+                                norm2, clip_norm if norm2 is not None else None)
+
+    group_fn = upd_bucket if bucket_elems and hasattr(ops, "lomo_apply_list") else None
+    return _run_backward(params, upd, loss_fn, group, bucket_elems, True, group_fn=group_fn)
 
 
 def adalomo_fused_step(params: Sequence, loss_fn: Callable, lr: float,

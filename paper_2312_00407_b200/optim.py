@@ -418,6 +418,38 @@ def lomo_apply_clipped(param, grad, lr: float, grad_sumsq, clip: float, stream=N
                                       grad_sumsq.data_ptr(), float(clip), _stream(stream)))
 
 
+def lomo_apply_list(params, grads, lr: float, scale: float = 1.0, grad_sumsq=None,
+                    clip: Optional[float] = None, stream=None) -> None:
+    """lomo_apply over separate CUDA tensors in one launch per 40 tensors
+    (mco_lomo_apply_list), each tensor's update bit-identical to lomo_apply's; with
+    grad_sumsq (float64 CUDA scalar) and clip: the global-norm clip rule as
+    lomo_apply_clipped."""
+    params, grads = list(params), list(grads)
+    n = len(params)
+    if n != len(grads):
+        raise ContractError("lomo_apply_list: params / grads length mismatch")
+    if n == 0:
+        return
+    for i, (p, g) in enumerate(zip(params, grads)):
+        _dev(p, "lomo param")
+        _dev(g, "lomo grad")
+        if p.numel() != g.numel():
+            raise ContractError(f"lomo_apply_list: tensor {i}: param/grad length mismatch")
+        if not (p.is_contiguous() and g.is_contiguous()):
+            raise ContractError(f"lomo_apply_list: tensor {i} is not contiguous")
+    pd, gd = _dtype_code(params[0]), _dtype_code(grads[0])
+    if any(_dtype_code(p) != pd for p in params) or any(_dtype_code(g) != gd for g in grads):
+        raise ContractError("lomo_apply_list: mixed dtypes in one list")
+    if (grad_sumsq is None) != (clip is None):
+        raise ContractError("lomo_apply_list: grad_sumsq and clip go together")
+    pt = (C.c_void_p * n)(*[p.data_ptr() for p in params])
+    gt = (C.c_void_p * n)(*[g.data_ptr() for g in grads])
+    lt = (C.c_uint64 * n)(*[p.numel() for p in params])
+    _check(lib.mco_lomo_apply_list(n, pt, pd, gt, gd, lt, float(lr), float(scale),
+                                   grad_sumsq.data_ptr() if grad_sumsq is not None else None,
+                                   float(clip) if clip is not None else 0.0, _stream(stream)))
+
+
 def sumsq(x, out=None, accumulate: bool = False, stream=None):
     """Deterministic sum of squares into a float64 CUDA scalar (optim.cpp:294-300)."""
     torch = _torch()

@@ -434,3 +434,35 @@ def test_adalomo_and_lomo_replay_from_a_cuda_graph():
     assert torch.equal(pe, pg)
     assert torch.equal(qe, qg)
     assert [sg.steps(k) for k in range(len(shapes))] == [3] * len(shapes)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16", "f32_bf16g", "f64"])
+@pytest.mark.parametrize("clip", [None, 0.5])
+def test_lomo_apply_list_equals_per_tensor(dt, clip):
+    """mco_lomo_apply_list (one launch per 40 tensors, odd / tiny / empty / unaligned
+    tensors) == lomo_apply / lomo_apply_clipped per tensor, bit for bit."""
+    pdt = {"f32": torch.float32, "bf16": torch.bfloat16, "f32_bf16g": torch.float32,
+           "f64": torch.float64}[dt]
+    gdt = torch.bfloat16 if dt in ("bf16", "f32_bf16g") else pdt
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    sizes = [4096, 7, 0, 1000, 65536, 3, 12288, 1] * 6  # 48 tensors: two launches
+    base = [torch.randn(n + 1, generator=gen, device="cuda", dtype=torch.float32) for n in sizes]
+    # every third tensor starts one element in: unaligned views take the scalar path
+    ps = [(b[1:] if k % 3 == 2 else b[:-1]).to(pdt) for k, b in enumerate(base)]
+    ps = [p if p.is_contiguous() else p.contiguous() for p in ps]
+    gs = [(torch.randn(n, generator=gen, device="cuda") * 0.1).to(gdt) for n in sizes]
+    qs = [p.clone() for p in ps]
+    norm2 = None
+    if clip is not None:
+        norm2 = torch.zeros((), dtype=torch.float64, device="cuda")
+        for g in gs:
+            optim.sumsq(g, out=norm2, accumulate=True)
+    optim.lomo_apply_list(ps, gs, 1e-2, 1.0, norm2, clip)
+    for q, g in zip(qs, gs):
+        if clip is None:
+            optim.lomo_apply(q, g, 1e-2, 1.0)
+        else:
+            optim.lomo_apply_clipped(q, g, 1e-2, norm2, clip)
+    torch.cuda.synchronize()
+    for p, q in zip(ps, qs):
+        assert torch.equal(p, q)
