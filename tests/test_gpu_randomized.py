@@ -1,7 +1,8 @@
 """Randomised parity sweep (fixed seed): random optimizer kind, length, element
 offset (alignment), gradient dtype, hyper-parameters, step count and graph mode -- the
 fp32 kernels must stay bit-exact with the restatement for every draw.
-MCO_RANDOM_CASES=N widens the stored-state sweep (default 40)."""
+MCO_RANDOM_CASES=N / MCO_RANDOM_ADA_CASES=N widen the stored-state / AdaLomo sweeps
+(defaults 40 / 12)."""
 import os
 
 import numpy as np
@@ -68,7 +69,7 @@ def test_random_case_bit_exact(c):
 
 
 ADA_CASES = []
-for i in range(12):
+for i in range(int(os.environ.get("MCO_RANDOM_ADA_CASES", "12"))):
     shapes = []
     for _ in range(int(rng.integers(1, 6))):
         if rng.random() < 0.25:
