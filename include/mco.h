@@ -5,7 +5,8 @@
  * namespace minicollie::optim (/root/reference/proj/core/include/minicollie/optim.hpp).
  * Every entry point below names the reference interface it replaces.
  * Plain C types only: device buffers are `void*` device pointers, streams are
- * `void*` holding a cudaStream_t (NULL = legacy default stream).
+ * `void*` holding a cudaStream_t (NULL = legacy default stream).  A `device`
+ * argument < 0 means the calling thread's current CUDA device.
  *
  * Error model (errors.hpp:8-32): each call returns an mco_status; the message
  * of the last failure on the calling thread is mco_last_error() and equals the
@@ -217,9 +218,16 @@ typedef struct mco_adalomo mco_adalomo;
 mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* ndims,
                               const int64_t* dims, int device, mco_adalomo** out);
 mco_status mco_adalomo_destroy(mco_adalomo* h);
+/* Opt-in global grad-norm clip of the gradients before the AdaLomo update (BASELINE
+ * C3; no reference counterpart -- the reference's AdaLomoState ignores
+ * cfg.clip_threshold, which only LOMO reads, optim.hpp:28, optim.cpp:288-304).  The
+ * LOMO rule (optim.cpp:302-303): g *= clip/||g|| iff ||g|| > clip and ||g|| > 0, with
+ * ||g|| over every tensor of the call (multi-tensor / phase / host forms) or from the
+ * caller's device sum of squares (hook forms).  enable = 0: off (the default). */
+mco_status mco_adalomo_set_grad_clip(mco_adalomo* h, int enable, double clip);
 /* AdaLomoState::apply(Tensor& param, lr) -- the per-tensor hook form.
- * dev_grad_sumsq: optional device Σg² over ALL tensors (global grad-norm
- * clip with cfg.clip_threshold); NULL = no clip.  dtypes (param/grad) F32/F32,
+ * dev_grad_sumsq: optional device Σg² over ALL tensors (global grad-norm clip; needs
+ * mco_adalomo_set_grad_clip, else MCO_CONTRACT); NULL = no clip.  dtypes (param/grad) F32/F32,
  * F32/BF16, BF16/BF16 (bf16 parameters: fp32 arithmetic, RNE store). */
 mco_status mco_adalomo_apply(mco_adalomo* h, int tensor_index, void* param, int param_dtype,
                              const void* grad, int grad_dtype, double lr,
@@ -232,14 +240,14 @@ mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* p
                                   int param_dtype, const void* const* grads, int grad_dtype,
                                   double lr, const double* dev_grad_sumsq, void* stream);
 /* Multi-tensor form: every tensor at once over registry-order flat buffers
- * (tensor k at element offset sum_{j<k} numel_j).  If cfg.has_clip_threshold
+ * (tensor k at element offset sum_{j<k} numel_j).  With mco_adalomo_set_grad_clip
  * the global grad norm over the whole set is computed in the same pass and
  * applied (clip fused into pass 1). */
 mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_params, int param_dtype,
                                  const void* flat_grads, int grad_dtype, double lr,
                                  void* stream);
 /* apply_all over HOST arrays: per-tensor H2D -> apply -> D2H pipeline on three
- * streams (whole-set upload first when cfg.has_clip_threshold).  Synchronous. */
+ * streams (whole-set upload first with the grad-norm clip on).  Synchronous. */
 mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* flat_params, int param_dtype,
                                       const void* flat_grads, int grad_dtype, double lr);
 mco_status mco_adalomo_state_bytes(const mco_adalomo* h, uint64_t* out); /* fp64 accounting */

@@ -162,6 +162,10 @@ struct OptimizerConfig {  // optim.hpp:20-35
 // spans (the drop-in default); kF32 is the HBM-roofline product path.
 enum class Precision { kF64, kF32 };
 
+// Device argument default: the calling thread's current CUDA device (resolved inside the
+// C-ABI), so a rank that called cudaSetDevice(r) gets its state on GPU r.
+constexpr int kCurrentDevice = -1;
+
 struct DeviceBuffer {
   void* ptr = nullptr;
   uint64_t len = 0;
@@ -170,7 +174,7 @@ struct DeviceBuffer {
 
 class FlatOptimizer {  // optim.hpp:40-64
  public:
-  FlatOptimizer(const OptimizerConfig& cfg, size_t owned_len, int device = 0,
+  FlatOptimizer(const OptimizerConfig& cfg, size_t owned_len, int device = kCurrentDevice,
                 Precision precision = Precision::kF64)
       : cfg_(cfg), precision_(precision) {
     const mco_config c = cfg.to_c();
@@ -275,7 +279,7 @@ inline void lomo_apply(DeviceTensor& param, double lr, double scale, void* strea
 class AdaLomoState {  // optim.hpp:76-96
  public:
   AdaLomoState(const OptimizerConfig& cfg, const std::vector<DeviceTensor>& params,
-               int device = 0)
+               int device = kCurrentDevice)
       : cfg_(cfg) {
     std::vector<int> nd;
     std::vector<int64_t> dims;
@@ -304,6 +308,11 @@ class AdaLomoState {  // optim.hpp:76-96
         return;
       }
     throw ContractError("adalomo: unknown parameter '" + param.name + "'");
+  }
+  // Opt-in global grad-norm clip (beyond the reference, whose AdaLomoState ignores
+  // cfg.clip_threshold): mco_adalomo_set_grad_clip.
+  void set_grad_clip(std::optional<double> clip) {
+    mco_throw(mco_adalomo_set_grad_clip(h_, clip.has_value() ? 1 : 0, clip.value_or(0.0)));
   }
   // Every registered tensor at once over registry-order flat device buffers.
   void apply_all(float* flat_params, const float* flat_grads, double lr, void* stream = nullptr) {
@@ -376,7 +385,7 @@ class NcclComm {
     mco_throw(mco_comm_unique_id(id.data()));
     return id;
   }
-  NcclComm(const Id& id, int nranks, int rank, int device = 0) {
+  NcclComm(const Id& id, int nranks, int rank, int device = optim::kCurrentDevice) {
     mco_throw(mco_comm_create(id.data(), nranks, rank, device, &h_));
   }
   ~NcclComm() {

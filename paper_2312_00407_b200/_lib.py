@@ -102,6 +102,7 @@ _SIGS = {
                                     _p]),
     "mco_adalomo_state_bytes": (_i, [_p, C.POINTER(_u64)]),
     "mco_adalomo_set_shard": (_i, [_p, _i, _i64, _d]),
+    "mco_adalomo_set_grad_clip": (_i, [_p, _i, _d]),
     "mco_adalomo_phase": (_i, [_p, _i, _p, _i, _p, _i, _d, _p]),
     "mco_adalomo_payload": (_i, [_p, _i, C.POINTER(_p), C.POINTER(_u64)]),
     "mco_adalomo_get_steps": (_i, [_p, _i, C.POINTER(_i64)]),

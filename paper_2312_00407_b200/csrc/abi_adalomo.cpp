@@ -12,6 +12,7 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
                               const int64_t* dims, int device, mco_adalomo** out) {
   return guard([&] {
     *out = nullptr;
+    device = resolve_device(device);
     DeviceGuard dg(device);
     auto h = std::make_unique<mco_adalomo>();
     auto& pl = h->plan;
@@ -73,7 +74,29 @@ void check_ada_dtypes(int pdt, int gdt) {
     throw Error(MCO_CONTRACT,
                 "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
 }
+
+// Hook forms clip with a caller-supplied global Σg² only when the handle opted in.
+int hook_clip(const AdaLomoPlan& pl, const double* dev_grad_sumsq) {
+  if (!dev_grad_sumsq) return 0;
+  if (!pl.grad_clip_on)
+    throw Error(MCO_CONTRACT, "adalomo: a gradient sum of squares was passed but the "
+                              "grad-norm clip is off (mco_adalomo_set_grad_clip)");
+  return 1;
+}
 }  // namespace
+
+// Opt-in global grad-norm clip for AdaLomo (BASELINE C3; no reference counterpart: the
+// reference's AdaLomoState::apply ignores cfg.clip_threshold, optim.cpp:215-275, which
+// only LOMO reads, optim.cpp:288-304).  enable = 0 turns it off.
+mco_status mco_adalomo_set_grad_clip(mco_adalomo* h, int enable, double clip) {
+  return guard([&] {
+    if (!h) throw Error(MCO_CONTRACT, "mco_adalomo_set_grad_clip: null handle");
+    if (enable && !(clip >= 0))  // the LOMO rule accepts any threshold >= 0
+      throw Error(MCO_CONFIG, "adalomo: grad-norm clip threshold must be >= 0");
+    h->plan.grad_clip_on = enable ? 1 : 0;
+    h->plan.grad_clip = enable ? clip : 0.0;
+  });
+}
 
 // optim.cpp:215-275 (hook form: one tensor)
 mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, const void* grad,
@@ -94,7 +117,7 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, cons
     c.g_dtype = gdt;
     c.single = 1;
     c.lr = lr;
-    c.use_clip = (dev_grad_sumsq != nullptr && h->plan.cfg.has_clip_threshold) ? 1 : 0;
+    c.use_clip = hook_clip(h->plan, dev_grad_sumsq);
     c.ext_sumsq = dev_grad_sumsq;
     launch_adalomo(h->plan, c, (cudaStream_t)stream);
     h->plan.h_tensors[idx].t += 1;
@@ -126,7 +149,7 @@ mco_status mco_adalomo_apply_list(mco_adalomo* h, int t0, int t1, void* const* p
       c.p_dtype = pdt;
       c.g_dtype = gdt;
       c.lr = lr;
-      c.use_clip = (dev_grad_sumsq != nullptr && h->plan.cfg.has_clip_threshold) ? 1 : 0;
+      c.use_clip = hook_clip(h->plan, dev_grad_sumsq);
       c.ext_sumsq = dev_grad_sumsq;
       c.ntab = b - a;
       for (int k = a; k < b; ++k) {
@@ -155,7 +178,7 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
     c.g_dtype = gdt;
     c.single = 0;
     c.lr = lr;
-    c.use_clip = h->plan.cfg.has_clip_threshold ? 1 : 0;
+    c.use_clip = h->plan.grad_clip_on;
     c.ext_sumsq = nullptr;
     launch_adalomo(h->plan, c, (cudaStream_t)stream);
     for (auto& T : h->plan.h_tensors) T.t += 1;
@@ -194,7 +217,7 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
     c.p_dtype = pdt;
     c.g_dtype = gdt;
     c.lr = lr;
-    if (pl.cfg.has_clip_threshold) {
+    if (pl.grad_clip_on) {
       MCO_CUDA_CHECK(cudaMemcpyAsync(h->hp, p, total * ps, cudaMemcpyHostToDevice, up));
       MCO_CUDA_CHECK(cudaMemcpyAsync(h->hg, g, total * gs, cudaMemcpyHostToDevice, up));
       MCO_CUDA_CHECK(cudaStreamSynchronize(up));
@@ -281,7 +304,7 @@ mco_status mco_adalomo_phase(mco_adalomo* h, int phase, void* flat_p, int pdt,
     c.g_dtype = gdt;
     c.single = 0;
     c.lr = lr;
-    c.use_clip = h->plan.cfg.has_clip_threshold ? 1 : 0;
+    c.use_clip = h->plan.grad_clip_on;
     launch_adalomo_phase(h->plan, c, phase, (cudaStream_t)stream);
     if (phase == 3)
       for (auto& T : h->plan.h_tensors) T.t += 1;

@@ -16,8 +16,13 @@ mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device
       throw Error(MCO_CONTRACT, "FlatOptimizer: " + kind_str(cfg->kind) +
                                     " is a fused optimizer and keeps no flat state");
     kind_str(cfg->kind);
+    // the reference's Sophia evaluates (t - 1) % update_interval every step
+    // (optim.cpp:161): an interval < 1 would divide by zero there and on the device here
+    if (cfg->kind == MCO_SOPHIA && cfg->update_interval < 1)
+      throw Error(MCO_CONFIG, "optimizer: update_interval must be >= 1");
     if (state_dtype != MCO_F32 && state_dtype != MCO_F64)
       throw Error(MCO_CONTRACT, "FlatOptimizer: state dtype must be f32 or f64");
+    device = resolve_device(device);
     DeviceGuard dg(device);
     auto h = std::make_unique<mco_flat>();
     h->cfg = *cfg;

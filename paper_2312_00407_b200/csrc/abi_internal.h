@@ -68,7 +68,10 @@ StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
   k.rho = (T)c.sophia_rho;
   k.sthr = sqrt_eps_threshold<T>(k.eps, c.kind == MCO_ADAN ? k.c3 : k.c2);
   k.first = t == 1 ? 1 : 0;
-  k.refresh = ((t - 1) % c.update_interval) == 0 ? 1 : 0;
+  // only Sophia reads the refresh flag (optim.cpp:161); interval < 1 is refused for it at
+  // create, every other kind ignores the field as the reference does
+  k.refresh = (c.kind == MCO_SOPHIA && c.update_interval >= 1 &&
+               ((t - 1) % c.update_interval) == 0) ? 1 : 0;
   return k;
 }
 

@@ -32,6 +32,14 @@ mco_status guard(F&& f) {
   }
 }
 
+// device < 0 means the calling thread's current CUDA device (mco.h "device" arguments).
+inline int resolve_device(int dev) {
+  if (dev >= 0) return dev;
+  int cur = 0;
+  MCO_CUDA_CHECK(cudaGetDevice(&cur));
+  return cur;
+}
+
 // RAII current-device switch.
 struct DeviceGuard {
   int prev = -1;

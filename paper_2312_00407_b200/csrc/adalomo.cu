@@ -856,7 +856,7 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
     launch_check("adalomo kr_stats");
   } else if (phase == 2) {  // scalars, moments, pass 2 over {g}
     launch_pdl(k2_scalars, 1, 1024, st, c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
-               cfg.clip_threshold, call.ext_sumsq);
+               pl.grad_clip, call.ext_sumsq);
     launch_check("adalomo k2_scalars");
     const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
     if (nitems > 0) {

@@ -50,6 +50,11 @@ struct TensorInfo {
 struct AdaLomoPlan {
   mco_config cfg{};
   int device = 0;
+  // global grad-norm clip of the gradients before the AdaLomo update (BASELINE C3, beyond
+  // the reference: its AdaLomoState ignores clip_threshold, which is LOMO's,
+  // optim.hpp:28).  Opt-in through mco_adalomo_set_grad_clip only.
+  int grad_clip_on = 0;
+  double grad_clip = 0.0;
   std::vector<TensorInfo> h_tensors;
   std::vector<Tile> h_tiles;
   std::vector<Chunk> h_chunks;

@@ -136,7 +136,7 @@ __device__ __forceinline__ StepConsts<T> step_consts(const StepConsts<T>& kv,
     k.lrwd = (T)lw;
     k.den = (T)(1.0 + lw);
     k.first = t == 1 ? 1 : 0;
-    k.refresh = ((t - 1) % gs.interval) == 0 ? 1 : 0;
+    k.refresh = (gs.interval >= 1 && ((t - 1) % gs.interval) == 0) ? 1 : 0;
     return k;
   }
 }

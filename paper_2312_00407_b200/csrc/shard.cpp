@@ -24,9 +24,7 @@
 #include <string>
 #include <vector>
 
-#include "abi_util.h"
-#include "common.cuh"
-#include "mco.h"
+#include "abi_internal.h"
 
 namespace mco {
 namespace {
@@ -147,6 +145,7 @@ mco_status mco_comm_create(const void* id, int nranks, int rank, int device, mco
     if (nranks < 1 || rank < 0 || rank >= nranks)
       throw Error(MCO_CONFIG, "comm create: rank " + std::to_string(rank) + " of " +
                                   std::to_string(nranks));
+    device = resolve_device(device);
     DeviceGuard ds(device);
     ncclUniqueId uid;
     std::memcpy(&uid, id, sizeof(uid));
@@ -206,12 +205,10 @@ void shard_run(mco_flat* h, mco_comm* c, const void* flat_grads, int grad_dtype,
   std::vector<uint64_t> parts(N), offs(N + 1);
   const mco_status zs = mco_zero_plan(total_len, N, 2, parts.data(), offs.data());
   if (zs != MCO_OK) throw Error(zs, "shard step: zero plan");
-  uint64_t nbuf = 0;
-  const char* nm = nullptr;
-  void* ptr = nullptr;
-  int sdt = 0;
-  mco_status bs = mco_flat_buffer(h, 0, &nm, &ptr, &nbuf, &sdt);
-  if (bs != MCO_OK) throw Error(bs, "shard step: handle");
+  // the owned length straight from the handle: the public mco_flat_buffer() would mark
+  // the state exposed and freeze its layout before the first step re-phases it to the
+  // parameters' alignment (abi_flat.cpp align_state_to)
+  const uint64_t nbuf = h->n;
   // the handle's owned length must be this rank's ZeroPlan part (parallel.cpp:330)
   if (nbuf != parts[me])
     throw Error(MCO_CONTRACT, "shard step: optimizer owns " + std::to_string(nbuf) +

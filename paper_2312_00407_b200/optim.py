@@ -488,8 +488,12 @@ class AdaLomoState:
     """optim.hpp:76-96.  `shapes` in registry order; 2-D -> factored."""
 
     def __init__(self, cfg: OptimizerConfig, shapes: Sequence[Sequence[int]],
-                 device: Optional[int] = None):
+                 device: Optional[int] = None, grad_clip: Optional[float] = None):
+        """grad_clip: opt-in global grad-norm clip of the gradients (BASELINE C3; the
+        reference's AdaLomoState ignores cfg.clip_threshold, which is LOMO's field,
+        optim.hpp:28) -- the LOMO rule, optim.cpp:302-303, applied to g first."""
         self._cfg = cfg
+        self.grad_clip = grad_clip
         self.shapes = [tuple(int(d) for d in s) for s in shapes]
         self.numels = [int(np.prod(s)) if len(s) else 1 for s in self.shapes]
         self.offsets = np.concatenate([[0], np.cumsum(self.numels)]).astype(np.int64)
@@ -500,6 +504,8 @@ class AdaLomoState:
         _check(lib.mco_adalomo_create(C.byref(cfg._to_c()), len(self.shapes), nd, dims,
                                       self.device, C.byref(h)))
         self._h = h
+        if grad_clip is not None:
+            _check(lib.mco_adalomo_set_grad_clip(h, 1, float(grad_clip)))
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -543,7 +549,7 @@ class AdaLomoState:
 
     def apply_all(self, flat_params, flat_grads, lr: float, stream=None) -> None:
         """Every tensor in one multi-tensor pass over registry-order flat buffers;
-        global grad-norm clip when cfg.clip_threshold is set.  numpy (host) arrays:
+        global grad-norm clip when the state was built with grad_clip.  numpy (host) arrays:
         per-tensor H2D / apply / D2H pipeline (mco_adalomo_apply_all_host)."""
         if isinstance(flat_params, np.ndarray):
             if flat_params.size != int(self.offsets[-1]) or flat_grads.size != flat_params.size:

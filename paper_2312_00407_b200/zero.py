@@ -451,7 +451,11 @@ class RowShardedAdaLomo:
     (parallel.cpp:334, 593-594) and is NOT serial AdaLomo; this is."""
 
     def __init__(self, cfg: optim.OptimizerConfig, shapes, group=None, device: Optional[int] = None,
-                 rank: Optional[int] = None, world: Optional[int] = None):
+                 rank: Optional[int] = None, world: Optional[int] = None,
+                 grad_clip: Optional[float] = None):
+        """grad_clip: the global grad-norm clip over the whole (all-rank) gradient
+        (C3; the LOMO rule, optim.cpp:302-303, on the concatenated gradient): the
+        per-rank Σg² rides in the first all-reduce payload."""
         dist = _dist()
         self.group = group
         if world is None:  # explicit rank/world: single-process (virtual-rank) use
@@ -461,7 +465,8 @@ class RowShardedAdaLomo:
         self.global_shapes = [tuple(s) for s in shapes]
         if dist.is_initialized() and self.world > 1:
             check_agreement("RowShardedAdaLomo", dict(shapes=self.global_shapes,
-                                                      kind=int(cfg.kind)), group)
+                                                      kind=int(cfg.kind), grad_clip=grad_clip),
+                            group)
         self.local_shapes, self.pieces, self._shard = [], [], []
         goff = 0
         for s in self.global_shapes:
@@ -479,7 +484,8 @@ class RowShardedAdaLomo:
                 self.pieces.append((goff, n))
                 self._shard.append((s[0] if s else 1, 1.0 if self.rank == 0 else 0.0))
             goff += n
-        self.state = optim.AdaLomoState(cfg, self.local_shapes, device=device)
+        self.state = optim.AdaLomoState(cfg, self.local_shapes, device=device,
+                                        grad_clip=grad_clip)
         for k, (rows, w) in enumerate(self._shard):
             self.state.set_shard(k, rows, w)
         self.local_numel = int(self.state.offsets[-1])

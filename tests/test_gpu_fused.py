@@ -208,10 +208,9 @@ def test_adalomo_global_clip_matches_composed_oracle(clip):
     oracle: the reference's clip rule, optim.cpp:302-303, scaling g, then the
     reference AdaLomoState::apply)."""
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-    cfg.clip_threshold = clip
     ps, gs = ada_inputs(SHAPES, 2)
     p0 = [p.copy() for p in ps]
-    st = optim.AdaLomoState(cfg, SHAPES)
+    st = optim.AdaLomoState(cfg, SHAPES, grad_clip=clip)
     o = O.OracleAdaLomo(cfg, SHAPES)
     flat_p = dev(np.concatenate(ps).astype(np.float32))
     for t in range(2):
@@ -231,9 +230,9 @@ def test_adalomo_global_clip_matches_composed_oracle(clip):
 
 def test_adalomo_hook_form_with_device_norm_equals_all_form_clip():
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-    cfg.clip_threshold = 1e-3
     ps, gs = ada_inputs(SHAPES, 1)
-    a, b = optim.AdaLomoState(cfg, SHAPES), optim.AdaLomoState(cfg, SHAPES)
+    a, b = (optim.AdaLomoState(cfg, SHAPES, grad_clip=1e-3),
+            optim.AdaLomoState(cfg, SHAPES, grad_clip=1e-3))
     fp = np.concatenate(ps).astype(np.float32)
     g = dev(np.concatenate(gs[0]).astype(np.float32))
     pa, pb = dev(fp), dev(fp)
@@ -284,8 +283,6 @@ def test_adalomo_bf16_params_round_the_f32_result(clip):
     multi-tensor and hook forms; shapes include 1-D tensors and a column count that is
     not a multiple of 8 (scalar path)."""
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-    if clip is not None:
-        cfg.clip_threshold = clip
     shapes = registry.CONFIG1.shapes()[:10] + [(37, 29), (5,)]
     n = sum(int(np.prod(s)) for s in shapes)
     g = torch.empty(n, dtype=torch.bfloat16, device="cuda")
@@ -295,7 +292,8 @@ def test_adalomo_bf16_params_round_the_f32_result(clip):
     p32 = p32.to(torch.bfloat16).float()  # bf16-representable starting point
     pb = p32.to(torch.bfloat16)
     qa, qb = p32.clone(), pb.clone()  # the hook form starts from the same point
-    sa, sb = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    sa, sb = (optim.AdaLomoState(cfg, shapes, grad_clip=clip),
+              optim.AdaLomoState(cfg, shapes, grad_clip=clip))
     sa.apply_all(p32, g, 1e-3)
     sb.apply_all(pb, g, 1e-3)
     torch.cuda.synchronize()
@@ -310,6 +308,27 @@ def test_adalomo_bf16_params_round_the_f32_result(clip):
             hb.apply(k, qb[a:b], g[a:b], 1e-3)
         torch.cuda.synchronize()
         assert torch.equal(qa.to(torch.bfloat16).view(torch.int16), qb.view(torch.int16))
+
+
+def test_adalomo_ignores_lomo_clip_threshold_like_the_reference():
+    """cfg.clip_threshold is LOMO's field (optim.hpp:28); the reference's AdaLomoState
+    never reads it (optim.cpp:215-275), so every AdaLomo form gives the same result with
+    or without it; the global clip is the explicit grad_clip opt-in."""
+    ps, gs = ada_inputs(SHAPES, 1)
+    fp = np.concatenate(ps).astype(np.float32)
+    g = dev(np.concatenate(gs[0]).astype(np.float32))
+    outs = []
+    for clip in (None, 1e-6):
+        cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+        cfg.clip_threshold = clip
+        st, tp = optim.AdaLomoState(cfg, SHAPES), dev(fp)
+        st.apply_all(tp, g, 1e-2)
+        outs.append(tp.cpu().numpy())
+    assert bits_equal(outs[0], outs[1])
+    st = optim.AdaLomoState(OptimizerConfig.defaults_for(Kind.ADALOMO), SHAPES)
+    with pytest.raises(optim.ContractError, match="grad-norm clip is off"):
+        st.apply(0, dev(fp)[:int(st.offsets[1])], g[:int(st.offsets[1])], 1e-2,
+                 grad_sumsq=optim.sumsq(g))
 
 
 def test_adalomo_rejects_bf16_params_with_f32_grads():
@@ -368,9 +387,9 @@ def test_lomo_host_path_equals_device_path():
 @pytest.mark.parametrize("clip", [None, 1e-3])
 def test_adalomo_host_path_equals_device_path(clip):
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-    cfg.clip_threshold = clip
     ps, gs = ada_inputs(SHAPES, 2)
-    a, b = optim.AdaLomoState(cfg, SHAPES), optim.AdaLomoState(cfg, SHAPES)
+    a, b = (optim.AdaLomoState(cfg, SHAPES, grad_clip=clip),
+            optim.AdaLomoState(cfg, SHAPES, grad_clip=clip))
     hp = np.concatenate(ps).astype(np.float32)
     tp = dev(hp)
     for t in range(2):

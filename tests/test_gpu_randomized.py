@@ -87,11 +87,10 @@ for i in range(int(os.environ.get("MCO_RANDOM_ADA_CASES", "12"))):
 def test_random_adalomo_within_tolerance(c):
     shapes = c["shapes"]
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-    if c["clip"] > 0:
-        cfg.clip_threshold = c["clip"]
+    clip = c["clip"] if c["clip"] > 0 else None
     ps = O.registry_params(shapes, c["seed"], np.float64)
     p0 = [x.copy() for x in ps]
-    st, o = optim.AdaLomoState(cfg, shapes), O.OracleAdaLomo(cfg, shapes)
+    st, o = optim.AdaLomoState(cfg, shapes, grad_clip=clip), O.OracleAdaLomo(cfg, shapes)
     tp = torch.from_numpy(np.concatenate(ps).astype(np.float32)).cuda()
     for t in range(1, 3):
         gs = O.registry_grads(shapes, c["seed"], t, np.float32)

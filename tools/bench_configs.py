@@ -67,8 +67,8 @@ def main():
         registry.fill_params(p, shapes)
         registry.fill_grads(g, shapes, 1)
         cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
-        cfg.lr, cfg.clip_threshold = 5e-4, 1.0
-        st = optim.AdaLomoState(cfg, shapes)
+        cfg.lr = 5e-4
+        st = optim.AdaLomoState(cfg, shapes, grad_clip=1.0)
         ms = timed(lambda: st.apply_all(p, g, cfg.lr), W, K)
         line("c3 adalomo+clip llama-13b 1xB200", n, ms, 24,
              {"tensors": len(shapes), "state_floats": st.state_bytes_runtime() // 8})
