@@ -3,31 +3,47 @@
 
 Workload (BASELINE.json configs[1]): all six optimizers -- AdamW, Lion, Adan,
 Sophia, LOMO, AdaLomo -- each updating a LLaMA-7B-shaped synthetic parameter set
-(291 tensors, 6,738,415,616 fp32 params, registry order) once per step.  One
-"step" = one update of the whole set by each of the six optimizers in turn;
-value = 6 * P * K / (device time of the K timed steps).  Inputs are synthetic
-(counter-based generator), fp32, resident in HBM, and 27 GB per buffer (> L2),
-so no L2 flush is needed between iterations.
+(291 tensors, 6,738,415,616 fp32 params, registry order) once per step.  LOMO and
+AdaLomo include the global gradient-norm clipping pass (north_star; clip = 1.0):
+LOMO = deterministic Σg² pass + clipped update (16 B/param), AdaLomo = clip fused
+into its first pass (24 B/param).  One "step" = one update of the whole set by each
+of the six optimizers in turn; value = 6 * P * K / (device time of the K timed
+steps).  Inputs are synthetic (counter-based generator), fp32, resident in HBM,
+27 GB per buffer (> L2), so no L2 flush is needed between iterations.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-N > 1 (torchrun, one process per GPU): ZeRO partition of the same set
-(ZeroPlan, parallel.cpp:20-34) -- each rank updates its owned shard; the
-gradient reduce-scatter / parameter all-gather are timed separately
-(`collectives`), value = P * 6 * K / max-over-ranks time ("strong").
+--gpus N > 1 without a torchrun environment re-launches itself under
+torch.distributed.run with N local ranks (one process per GPU, NCCL); under torchrun
+WORLD_SIZE must equal N.  At N > 1 each optimizer runs the WHOLE data-parallel step
+of the reference's stage-2 branch (parallel.cpp:656-666) on the same 7B set
+(strong scaling): every rank holds its local gradients for all P params,
+    stored-state kinds  reduce-scatter(SUM, fp32 grads) -> fused update of the
+                        ZeroPlan-owned slice -> all-gather(fp32 params)
+    LOMO + clip         reduce-scatter -> Σg² of the owned slice -> all-reduce(1 fp64)
+                        -> clipped update -> all-gather
+    AdaLomo + clip      row-split: reduce-scatter (rank-major layout) -> pass 1 ->
+                        all-reduce(column sums, Σg², Σp², Σv_row) -> pass 2 ->
+                        all-reduce(Σu²) -> pass 3 -> all-gather
+value = 6 * P / Σ max-over-ranks step time.  Beside it: the shard-local update time
+(the same kernels without the collectives), the NVLink bytes per rank, and the
+measured NCCL bus bandwidth they are bounded by.
 
-e2e: the same metric through the C-ABI with HOST (pinned) buffers -- per step
-H2D params+grads, the update, D2H params (mco_flat_step_host pipelines it for
-the four stored-state kinds).  cpu_baseline / --impl reference: the
-reference's own minicollie::optim (oracle/_ref, compiled from its sources)
-timed on this host's cores on a bounded sample (one 7B decoder layer).
+e2e: the same metric through the public API with HOST (pinned) buffers -- per step
+H2D params+grads, the update, D2H params (C-ABI host-span calls).  cpu_baseline /
+--impl reference: the reference's own minicollie::optim (oracle/_ref, compiled from
+its sources, driven through oracle/oracle.py only -- no product code) on this host's
+cores on a bounded registry-order sample (5 decoder layers of the 7B set: 45 tensors,
+1.01e9 params, fewer layers when host RAM is short).
 """
 from __future__ import annotations
 
 import argparse
 import gc
 import json
+import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -37,13 +53,18 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 KINDS = ["adamw", "lion", "adan", "sophia", "lomo", "adalomo"]
-# Algorithmic (dependency-forced) HBM bytes per parameter, fp32.
-BYTES_PER_PARAM = {"adamw": 28, "lion": 20, "adan": 44, "sophia": 24, "lomo": 12,
+STORED = ("adamw", "lion", "adan", "sophia")
+CLIP = 1.0  # LOMO / AdaLomo global grad-norm clip threshold (optim.cpp:291-303)
+# Algorithmic (dependency-forced) HBM bytes per parameter, fp32:
+# LOMO with its clip pass 16 (Σg² pass reads g; update reads p, g, writes p),
+# AdaLomo with the clip fused into pass 1 24.
+BYTES_PER_PARAM = {"adamw": 28, "lion": 20, "adan": 44, "sophia": 24, "lomo": 16,
                    "adalomo": 24}
 # Paper Table 4 hyper-parameters for throughput runs; Sophia: defaults.
 HPARAMS = {"adamw": dict(lr=1e-5, weight_decay=1e-2), "lion": dict(lr=3e-6, weight_decay=3e-2),
            "adan": dict(lr=5e-5, weight_decay=2e-2), "sophia": dict(lr=1e-4),
            "lomo": dict(lr=1e-2), "adalomo": dict(lr=5e-4)}
+NVLINK_NOMINAL_GBS = 900.0  # NVLink 5, per direction per GPU
 
 
 def log(*a):
@@ -111,15 +132,37 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------------------
-# reference arm / CPU baseline: the reference's own code on the host cores
+# reference arm / CPU baseline: the reference's own code on the host cores.  Only
+# oracle/ is imported here (the compiled reference + its kind parser and defaults).
 # ---------------------------------------------------------------------------------------
 
-def cpu_sample_shapes():
-    from paper_2312_00407_b200.registry import CONFIG1, LLAMA_7B
+def _oracle():
+    p = os.path.join(ROOT, "oracle")
+    if p not in sys.path:
+        sys.path.insert(0, p)
+    import oracle as O
 
-    if os.environ.get("MCO_CPU_SAMPLE") == "tiny":  # CPU test of the bench contract
-        return CONFIG1.shapes()[1:10]
-    return LLAMA_7B.shapes()[1:10]  # one decoder layer: 9 tensors, 202,383,360 params
+    if O.ref is None:
+        raise RuntimeError("oracle/_ref/libmco_ref.so missing (run __graft_entry__.build())")
+    return O
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def host_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for ln in f:
+                if ln.startswith("MemAvailable:"):
+                    return int(ln.split()[1]) * 1024
+    except Exception:
+        pass
+    return 16 << 30
 
 
 def cpu_model() -> str:
@@ -133,57 +176,57 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def host_threads() -> int:
-    try:
-        return len(os.sched_getaffinity(0))
-    except Exception:
-        return os.cpu_count() or 1
+def cpu_sample_shapes(O):
+    """Registry-order run of whole decoder layers of the 7B set (tensors 1..9L): the
+    reference spreads LOMO / AdaLomo over tensors, so the sample holds more tensors
+    than host threads; 5 layers = 45 tensors, 1,011,916,800 params (a
+    1e9-param 7B sample), fewer layers if the host cannot hold Adan's 48 B/param fp64
+    working set in half its free RAM."""
+    if os.environ.get("MCO_CPU_SAMPLE") == "tiny":  # CPU test of the bench contract
+        return O.llama_shapes(256, 688, 8, 8192)[1:19], 2
+    per_layer = 4 * 4096 * 4096 + 3 * 4096 * 11008 + 2 * 4096
+    layers = int(max(1, min(5, host_available_bytes() * 0.5 // (48 * per_layer))))
+    return O.llama_shapes(4096, 11008, 32, 32000)[1:1 + 9 * layers], layers
 
 
 def run_cpu_reference(warmup: int, steps: int):
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-    from paper_2312_00407_b200.optim import OptimizerConfig, parse_kind
-
-    if O.ref is None:
-        raise RuntimeError("oracle/_ref/libmco_ref.so missing (run __graft_entry__.build())")
-    shapes = cpu_sample_shapes()
-    n = sum(int(__import__("math").prod(s)) for s in shapes)
+    O = _oracle()
+    shapes, layers = cpu_sample_shapes(O)
+    n = sum(math.prod(s) for s in shapes)
     threads = host_threads()
-    per = {}
-    total = 0.0
+    per, total = {}, 0.0
     for k in KINDS:
-        cfg = OptimizerConfig.defaults_for(parse_kind(k))
-        for a, v in HPARAMS[k].items():
-            setattr(cfg, a, v)
-        sec = O.ref_bench(cfg, shapes, threads, warmup, steps)
-        per[k] = {"ms": sec * 1e3, "params_per_s": n / sec}
+        cfg = O.ref_config(k, **HPARAMS[k])
+        clip = CLIP if k in ("lomo", "adalomo") else None
+        sec = O.ref_bench(cfg, shapes, threads, warmup, steps, clip=clip)
+        per[k] = {"ms": round(sec * 1e3, 2), "params_per_s": n / sec}
         total += sec
         log(f"[cpu-ref] {k}: {sec * 1e3:.1f} ms/step, {n / sec / 1e9:.3f} Gparam/s "
             f"({threads} threads)")
     value = len(KINDS) * n / total
-    sample = (f"one decoder layer of the registry (9 tensors, {n} fp64 params) per optimizer, "
-              f"{warmup} warm-up + {steps} timed steps, one FlatOptimizer per thread over "
-              "disjoint slices (stored-state kinds) / tensors across threads (LOMO, AdaLomo)")
-    return value, threads, sample, per, total / max(steps, 1)
+    sample = (f"{layers} registry-order decoder layers of the 7B set ({len(shapes)} tensors, "
+              f"{n} fp64 params) per optimizer, {warmup} warm-up + {steps} timed steps; "
+              "stored-state kinds: one FlatOptimizer per thread over disjoint slices; "
+              "LOMO / AdaLomo: tensors spread largest-first over the threads, with the "
+              f"global grad-norm clip pass (clip {CLIP})")
+    return value, threads, sample, per, total / max(steps, 1), n
 
 
 def run_cpu_single_thread():
-    """The reference on ONE host thread (T = nproc and T = 1), on a
-    smaller sample: the first q-projection matrix of the 7B registry."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import oracle as O
-
-    shapes = cpu_sample_shapes()[1:2]
-    n = sum(int(__import__("math").prod(s)) for s in shapes)
+    """The reference on ONE host thread (T = nproc and T = 1): the first
+    q-projection matrix of the 7B registry."""
+    O = _oracle()
+    shapes = [(4096, 4096)]
+    n = 4096 * 4096
     per, total = {}, 0.0
     for k in KINDS:
-        sec = O.ref_bench(make_cfg(k), shapes, 1, 1, 1)
+        clip = CLIP if k in ("lomo", "adalomo") else None
+        sec = O.ref_bench(O.ref_config(k, **HPARAMS[k]), shapes, 1, 1, 1, clip=clip)
         per[k] = {"ms": round(sec * 1e3, 2), "params_per_s": n / sec}
         total += sec
     return {"value": len(KINDS) * n / total, "unit": "params/s", "cores": 1,
-            "sample": f"one {shapes[0][0]}x{shapes[0][1]} matrix ({n} fp64 params) per "
-                      "optimizer, 1 warm-up + 1 timed step", "per_optimizer": per}
+            "sample": f"one 4096x4096 matrix ({n} fp64 params) per optimizer, 1 warm-up + "
+                      "1 timed step", "per_optimizer": per}
 
 
 # ---------------------------------------------------------------------------------------
@@ -200,53 +243,131 @@ def make_cfg(kind: str):
 
 
 class Stepper:
-    """One optimizer over (a shard of) the flat registry buffers, via the public API.
-    N > 1: stored-state kinds and LOMO update this rank's ZeroPlan slice (gradients
-    already reduced); AdaLomo runs row-split (zero.RowShardedAdaLomo) on its local
-    row slices with its two statistic all-reduces inside the step."""
+    """One optimizer over the flat registry buffers through the public API.
 
-    def __init__(self, kind, shapes, p, g, world=1):
-        import torch
+    world == 1: the whole set on this GPU.  world > 1: the whole data-parallel step
+    (module docstring), and `local()` = the same update kernels on this rank's part
+    without the collectives (the shard-local figure)."""
 
-        from paper_2312_00407_b200 import optim, registry, zero
+    def __init__(self, kind, shapes, P, bp, bg, world, rank, comm=None):
+        from paper_2312_00407_b200 import optim, zero
 
-        self.kind, self.p, self.g = kind, p, g
+        self.kind, self.world, self.rank = kind, world, rank
         self.cfg = make_cfg(kind)
         self.lr = self.cfg.lr
-        self.rs = None
-        self.n = p.numel()
-        if kind in ("adamw", "lion", "adan", "sophia"):
-            self.opt = optim.FlatOptimizer(self.cfg, p.numel(), device=p.device.index)
-        elif kind == "adalomo" and world > 1:
-            self.rs = zero.RowShardedAdaLomo(self.cfg, shapes, device=p.device.index)
-            self.n = self.rs.local_numel
-            self.lp = torch.empty(self.n, device=p.device)
-            self.lg = torch.empty(self.n, device=p.device)
-            optim.synth_fill(self.lp, registry.SEED, 0, 0xFFFE, 0, 0, -6)
-            optim.synth_fill(self.lg, registry.SEED, 1, 0xFFFE, 1, 0, -7, 10)
-        elif kind == "adalomo":
-            self.opt = optim.AdaLomoState(self.cfg, shapes, device=p.device.index)
+        self.P = P
+        self.p, self.g = bp[:P], bg[:P]
+        self.n_local = P
+        dev = bp.device.index
+        if world == 1:
+            if kind in STORED:
+                self.opt = optim.FlatOptimizer(self.cfg, P, device=dev)
+                self._step = lambda: self.opt.step(self.p, self.g, self.lr)
+            elif kind == "lomo":
+                self._norm = None
+
+                def lomo():
+                    self._norm = optim.lomo_step(self.p, self.g, self.lr, clip=CLIP)
+                self._step = lomo
+            else:
+                self.opt = optim.AdaLomoState(self.cfg, shapes, device=dev, grad_clip=CLIP)
+                self._step = lambda: self.opt.apply_all(self.p, self.g, self.lr)
+            self.local = self._step
+            return
+        plan = zero.ZeroPlan.make(P, world, 2)
+        lo, hi = plan.owned_range(rank)
+        self.n_local = hi - lo
+        if kind in STORED:
+            if comm is not None:  # NCCL: the C-ABI sharded step (mco_shard_step)
+                self.opt = zero.NativeZeroOptimizer(self.cfg, P, comm, device=dev)
+                flat = self.opt.opt
+            else:  # gloo (several ranks on one GPU in the tests): torch.distributed
+                self.opt = zero.ZeroShardedOptimizer(self.cfg, P, device=dev)
+                flat = self.opt.opt
+            self._step = lambda: self.opt.step(self.p, self.g, self.lr)
+            po, go = self.p[lo:hi], self.g[lo:hi]
+            self.local = lambda: flat.step(po, go, self.lr)
+        elif kind == "lomo":
+            self.opt = zero.ZeroShardedLomo(P, CLIP)
+            self._step = lambda: self.opt.step(self.p, self.g, self.lr)
+            po, go = self.p[lo:hi], self.g[lo:hi]
+            self.local = lambda: zero.sharded_lomo_step(po, go, self.lr, CLIP)
         else:
-            self.opt = None
+            self.rs = zero.RowShardedAdaLomo(self.cfg, shapes, device=dev, grad_clip=CLIP)
+            L = world * self.rs.chunk
+            if L > bp.numel():
+                raise RuntimeError(f"rank-major AdaLomo buffers need {L} elements")
+            self.p, self.g = bp[:L], bg[:L]
+            self.n_local = self.rs.local_numel
+            c = self.rs.chunk
+            lp = self.p[rank * c:rank * c + self.n_local]
+            lg = self.g[rank * c:rank * c + self.n_local]
+            self._step = lambda: self.rs.step_dp(self.p, self.g, self.lr)
+            self.local = lambda: self.rs.step(lp, lg, self.lr)
 
     def step(self):
-        from paper_2312_00407_b200 import optim
+        self._step()
 
-        if self.kind == "lomo":
-            optim.lomo_apply(self.p, self.g, self.lr, 1.0)
-        elif self.rs is not None:
-            self.rs.step(self.lp, self.lg, self.lr)
-        elif self.kind == "adalomo":
-            self.opt.apply_all(self.p, self.g, self.lr)
-        else:
-            self.opt.step(self.p, self.g, self.lr)
+    def steps_taken(self):
+        o = getattr(self, "opt", None)
+        o = getattr(o, "opt", o)  # the sharded wrappers keep a FlatOptimizer in .opt
+        return o.steps_taken() if hasattr(o, "steps_taken") else 0
+
+
+def nvlink_bytes_per_rank(kind, P, world, rs_chunk=None, payload=0):
+    """Bytes each rank sends (= receives) per step over NVLink in the ring collectives:
+    reduce-scatter + all-gather of fp32 move (N-1)/N of the buffer each; the scalar /
+    payload all-reduces move 2 (N-1)/N of theirs."""
+    f = (world - 1) / world
+    if kind == "adalomo":
+        L = world * rs_chunk
+        return int(f * L * 4 * 2 + 2 * f * payload * 8)
+    return int(f * P * 4 * 2 + (2 * f * 8 if kind == "lomo" else 0))
+
+
+def nccl_busbw(dev, world, nbytes=1 << 30):
+    """Measured all-gather bus bandwidth (GB/s per rank and direction) over this job's
+    NCCL communicator: (N-1)/N * bytes / time, best of 3."""
+    import torch
+    import torch.distributed as dist
+
+    n = nbytes // 4 // world * world
+    out = torch.empty(n, device=dev)
+    inp = out[:n // world].clone()
+    best = 0.0
+    for _ in range(4):
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dist.all_gather_into_tensor(out, inp)
+        e1.record()
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        best = max(best, (world - 1) / world * n * 4 / t.item() / 1e9)
+    del out, inp
+    return round(best, 1)
+
+
+def timed_block(fn, steps, stream, per_step=False):
+    import torch
+
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    evs[0].record(stream)
+    for i in range(steps):
+        fn()
+        evs[i + 1].record(stream)
+    torch.cuda.synchronize()
+    ms = evs[0].elapsed_time(evs[-1]) / steps
+    return (ms, [evs[i].elapsed_time(evs[i + 1]) for i in range(steps)]) if per_step else ms
 
 
 def bench_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_2312_00407_b200 import optim, registry
+    from paper_2312_00407_b200 import optim, registry, zero
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
@@ -257,77 +378,92 @@ def bench_ours(args, rank, world, local_rank):
     P = model.param_count()
     kinds = args.optimizers.split(",")
     hbm_peak, peak_src = measured_peaks()
+    backend = dist.get_backend() if world > 1 else None
+    log(f"[rank {rank}] model {model.name} P={P} world={world} kinds={kinds}")
 
-    # ZeRO partition of the flat registry (N=1: the whole set)
-    parts, offs = optim.zero_plan(P, world, 1)
-    owned = parts[rank]
-    log(f"[rank {rank}] model {model.name} P={P} owned={owned} kinds={kinds}")
-
-    p = torch.empty(owned, dtype=torch.float32, device=dev)
-    g = torch.empty(owned, dtype=torch.float32, device=dev)
-    if world == 1:
-        registry.fill_params(p, shapes)
-        registry.fill_grads(g, shapes, 1)
-    else:
-        optim.synth_fill(p, registry.SEED, 0, 0xFFFF, 0, 0, -6)
-        optim.synth_fill(g, registry.SEED, 1, 0xFFFF, 1, 0, -7, 10)
+    # one pair of flat buffers for every kind (rank-major AdaLomo needs a little more)
+    cap = P
+    if world > 1 and "adalomo" in kinds:
+        probe = zero.RowShardedAdaLomo.chunk_len(shapes, world)
+        cap = max(P, world * probe)
+    bp = torch.empty(cap, dtype=torch.float32, device=dev)
+    bg = torch.empty(cap, dtype=torch.float32, device=dev)
+    registry.fill_params(bp[:P], shapes)
+    registry.fill_grads(bg[:P], shapes, 1)
+    if cap > P:
+        bp[P:].zero_()
+        bg[P:].zero_()
     torch.cuda.synchronize()
+    comm = None
+    busbw = None
+    if world > 1:
+        if backend == "nccl":
+            comm = zero.NcclComm(device=local_rank)
+            busbw = nccl_busbw(dev, world)
+            log(f"[rank {rank}] NCCL all-gather bus bandwidth {busbw} GB/s")
 
     stream = torch.cuda.current_stream()
-    per = {}
-    total_ms = 0.0
-    launches = 0
+    per, total_ms, launches = {}, 0.0, 0
     clocks = ClockSampler(local_rank)
     for kind in kinds:
-        st = Stepper(kind, shapes, p, g, world)
+        st = Stepper(kind, shapes, P, bp, bg, world, rank, comm)
         for _ in range(args.warmup):
             st.step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         l0 = optim.launch_count()
         if kind == kinds[0]:
             clocks.start()
-        # per-step events (Sophia: refresh steps write h, SURVEY 8(d) reports them apart)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-        t0 = st.opt.steps_taken() if kind in ("adamw", "lion", "adan", "sophia") else 0
-        e0.record(stream)
-        evs[0].record(stream)
-        for i in range(args.steps):
-            st.step()
-            evs[i + 1].record(stream)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        t0 = st.steps_taken()
+        ms, step_ms = timed_block(st.step, args.steps, stream, per_step=True)
         launches_kind = optim.launch_count() - l0
         launches += launches_kind
-        ms = e0.elapsed_time(e1) / args.steps
-        step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-        # the median of repeated K-step blocks, reported next to the one
-        # contract-timed block above (which alone defines ms / value)
-        rep_ms = [ms]
-        for _ in range(max(args.repeats, 1) - 1):
-            r0, r1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            r0.record(stream)
-            for _ in range(args.steps):
-                st.step()
-            r1.record(stream)
-            torch.cuda.synchronize()
-            rep_ms.append(r0.elapsed_time(r1) / args.steps)
+        rep_ms = [ms] + [timed_block(st.step, args.steps, stream)
+                         for _ in range(max(args.repeats, 1) - 1)]
+        local_ms = None
         if world > 1:
-            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            torch.cuda.synchronize()
+            dist.barrier()
+            local_ms = timed_block(st.local, args.steps, stream)
+            t = torch.tensor([ms, local_ms], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            ms = t.item()
+            ms, local_ms = t.tolist()
         bpp = BYTES_PER_PARAM[kind]
-        gbs = bpp * st.n / (ms * 1e-3) / 1e9  # per GPU (this rank's launch)
-        per[kind] = {"ms": round(ms, 4), "params_per_s": P / (ms * 1e-3),
-                     "bytes_per_param": bpp, "achieved_gbs_per_gpu": round(gbs, 1),
-                     "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
-                     "params_per_launch": st.n,
-                     "launches_per_step": args.steps and (launches_kind / args.steps),
-                     "repeats": len(rep_ms), "ms_median_of_repeats":
-                         round(sorted(rep_ms)[len(rep_ms) // 2], 4),
-                     "ms_min_max_of_repeats": [round(min(rep_ms), 4), round(max(rep_ms), 4)]}
+        gbs = bpp * st.n_local / (ms * 1e-3) / 1e9  # per GPU (this rank's update bytes)
+        e = {"ms": round(ms, 4), "params_per_s": P / (ms * 1e-3), "bytes_per_param": bpp,
+             "achieved_gbs_per_gpu": round(gbs, 1),
+             "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
+             "params_per_launch": st.n_local,
+             "launches_per_step": args.steps and (launches_kind / args.steps),
+             "repeats": len(rep_ms),
+             "ms_median_of_repeats": round(sorted(rep_ms)[len(rep_ms) // 2], 4),
+             "ms_min_max_of_repeats": [round(min(rep_ms), 4), round(max(rep_ms), 4)]}
+        if kind in ("lomo", "adalomo"):
+            e["clip"] = CLIP
+        if world > 1:
+            lgbs = bpp * st.n_local / (local_ms * 1e-3) / 1e9
+            payload = 0
+            if kind == "adalomo":
+                payload = sum(t.numel() for t in (st.rs.state.payload(0), st.rs.state.payload(1)))
+            nvb = nvlink_bytes_per_rank(kind, P, world, getattr(getattr(st, "rs", None),
+                                                                "chunk", None), payload)
+            e["shard_local"] = {
+                "ms": round(local_ms, 4), "params_per_s": P / (local_ms * 1e-3),
+                "frac_of_measured_hbm": round(lgbs / hbm_peak, 4),
+                "what": "the same update kernels on this rank's part, no gradient "
+                        "reduce-scatter / parameter all-gather (max over ranks)"}
+            e["nvlink"] = {"bytes_per_rank_per_direction": nvb,
+                           "gb_per_s": round(nvb / (ms * 1e-3) / 1e9, 1),
+                           "frac_of_nominal": round(nvb / (ms * 1e-3) / 1e9
+                                                    / NVLINK_NOMINAL_GBS, 4)}
+            if busbw:
+                e["nvlink"]["frac_of_measured_busbw"] = round(
+                    nvb / (ms * 1e-3) / 1e9 / busbw, 4)
+            # the step cannot beat max(collective bytes / bus bw, update bytes / HBM)
+            if busbw:
+                e["roofline_ms"] = round(max(nvb / (busbw * 1e9), bpp * st.n_local
+                                             / (hbm_peak * 1e9)) * 1e3, 3)
         if kind == "sophia":
             k = st.cfg.update_interval
             ref = [m for i, m in enumerate(step_ms) if (t0 + i) % k == 0]  # t-1 = t0+i
@@ -335,137 +471,52 @@ def bench_ours(args, rank, world, local_rank):
             for name, xs, b in (("refresh", ref, 28), ("non_refresh", non, 24)):
                 if xs:
                     m = sum(xs) / len(xs)
-                    per[kind][name] = {"steps": len(xs), "ms": round(m, 4),
-                                       "bytes_per_param": b,
-                                       "frac_of_measured_hbm": round(
-                                           b * st.n / (m * 1e-3) / 1e9 / hbm_peak, 4)}
+                    e[name] = {"steps": len(xs), "ms": round(m, 4), "bytes_per_param": b,
+                               "frac_of_measured_hbm": round(
+                                   b * st.n_local / (m * 1e-3) / 1e9 / hbm_peak, 4)}
+        per[kind] = e
         total_ms += ms
         log(f"[rank {rank}] {kind}: {ms:.3f} ms/step, {P / ms / 1e6:.1f} Gparam/s (all GPUs), "
-            f"{gbs:.0f} GB/s/GPU = {gbs / hbm_peak:.3f} of {peak_src} HBM")
+            f"{gbs:.0f} GB/s/GPU = {gbs / hbm_peak:.3f} of {peak_src} HBM"
+            + (f"; shard-local {local_ms:.3f} ms" if local_ms else ""))
         del st
         gc.collect()
         torch.cuda.synchronize()
     clocks.stop()
-    nk = len(per)
-    value = nk * P / (total_ms * 1e-3)
+    value = len(per) * P / (total_ms * 1e-3)
 
-    # dominant kernel = the optimizer with the largest share of the step
-    dom = max(per, key=lambda k: per[k]["ms"])
+    # dominant kernel = the optimizer with the largest share of the step (N = 1)
+    dom = max(per, key=lambda k: per[k]["ms"] if world == 1 else
+              per[k]["shard_local"]["ms"])
+    src = per[dom] if world == 1 else per[dom]["shard_local"]
     npl = per[dom]["params_per_launch"]
-    kname = ("flat_tma_kernel: cp.async.bulk + mbarrier pipeline"
-             if optim.flat_variant() == "tma" else f"flat_step_kernel, variant {optim.flat_variant()}")
-    roofline = {"bound": "hbm", "kernel": f"{dom} update ({kname})" if dom not in (
-        "lomo", "adalomo") else dom, "achieved": per[dom]["achieved_gbs_per_gpu"],
-        "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-        "frac": round(per[dom]["achieved_gbs_per_gpu"] / hbm_peak, 4),
-        "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": npl,
-        "traffic": load_traffic(dom, npl)}
+    achieved = BYTES_PER_PARAM[dom] * npl / (src["ms"] * 1e-3) / 1e9
+    kname = {"lomo": "sumsq_kernel + lomo_tma_kernel (clip)",
+             "adalomo": "k1_stats .. k6_update (clip fused into pass 1)"}.get(
+        dom, "flat_tma_kernel: cp.async.bulk + mbarrier pipeline"
+        if optim.flat_variant() == "tma" else f"flat_step_kernel, variant {optim.flat_variant()}")
+    roofline = {"bound": "hbm", "kernel": f"{dom} update ({kname})",
+                "achieved": round(achieved, 1), "peak": hbm_peak, "peak_source": peak_src,
+                "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                "algorithmic_bytes_per_param": BYTES_PER_PARAM[dom], "params_per_launch": npl,
+                "traffic": load_traffic(dom, npl)}
+    if world > 1:
+        roofline["note"] = ("dominant shard-local update kernel; the whole step at N > 1 is "
+                            "bounded by the collectives (per_optimizer.*.nvlink)")
     out = dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
-               launches=launches, clocks=clocks.summary(), P=P, owned=owned,
-               shapes=shapes, kinds=[k for k in kinds if k in per], p=p, g=g)
-    out["dev"] = dev
+               launches=launches, clocks=clocks.summary(), P=P, owned=P, shapes=shapes,
+               kinds=[k for k in kinds if k in per], p=bp[:P], g=bg[:P], dev=dev,
+               busbw=busbw)
+    if world > 1:
+        out["lo"], hi = zero.ZeroPlan.make(P, world, 2).owned_range(rank)
+        out["owned"] = hi - out["lo"]
     if world > 1 and not args.no_e2e:
         try:  # every rank takes part (max-over-ranks time); failures are reported
             out["e2e"] = bench_e2e(args, out, rank, world)
         except Exception as ex:
             log(f"[rank {rank}] e2e failed: {ex!r}")
             out["e2e"] = None
-    if world > 1 and not args.no_collectives:
-        del p, g
-        out["p"] = out["g"] = None
-        gc.collect()
-        torch.cuda.empty_cache()
-        try:  # the headline line must not depend on the collective benchmarks
-            out["collectives"] = bench_peer_step(args, P, rank, world, dev)
-        except Exception as ex:  # report, never fake
-            log(f"[rank {rank}] peer-memory step unavailable: {ex!r}")
-            out["collectives"] = {"unavailable": repr(ex)[:200]}
-        gc.collect()
-        torch.cuda.empty_cache()
-        import torch.distributed as dist
-
-        if dist.get_backend() == "nccl":  # NCCL refuses two ranks on one device (gloo tests)
-            try:
-                out["collectives"]["nccl_baseline"] = bench_nccl_step(args, P, rank, world, dev)
-            except Exception as ex:  # report, never fake
-                out["collectives"]["nccl_baseline"] = {"unavailable": repr(ex)[:200]}
     return out
-
-
-def bench_nccl_step(args, P, rank, world, dev):
-    """The same AdamW ZeRO step with NCCL collectives around the kernel
-    (mco_shard_step: ncclReduceScatter -> owned-slice step -> ncclAllGather), the
-    library-collective baseline the fused peer-memory kernel is measured against."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2312_00407_b200 import optim, registry, zero
-
-    cfg = make_cfg("adamw")
-    comm = zero.NcclComm(device=dev.index)
-    nz = zero.NativeZeroOptimizer(cfg, P, comm, device=dev.index)
-    p = torch.empty(P, device=dev)
-    g = torch.empty(P, device=dev)
-    optim.synth_fill(p, registry.SEED, 0, 0xFFFC, 0, 0, -6)
-    optim.synth_fill(g, registry.SEED, 1, 0xFFFC, 1, 0, -7, 10)
-    for _ in range(args.warmup):
-        nz.step(p, g, cfg.lr)
-    torch.cuda.synchronize()
-    dist.barrier()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        nz.step(p, g, cfg.lr)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    comm.check()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = ms.item()
-    log(f"[rank {rank}] NCCL RS + adamw + AG (mco_shard_step): {ms:.2f} ms/step")
-    return {"path": "mco_shard_step: ncclReduceScatter + flat_tma_kernel + ncclAllGather",
-            "ms": ms, "params_per_s": P / (ms * 1e-3)}
-
-
-def bench_peer_step(args, P, rank, world, dev):
-    """ZeRO step fused with its collectives (csrc/peer.cu): AdamW over the whole 7B
-    set, grads summed from every rank's buffer over NVLink, params stored into every
-    replica.  Roofline = max(HBM bytes / HBM BW, NVLink bytes / 770 GB/s)."""
-    import torch
-    import torch.distributed as dist
-
-    from paper_2312_00407_b200 import optim, registry, zero
-
-    cfg = make_cfg("adamw")
-    ps = zero.PeerShardedOptimizer(cfg, P, device=dev.index)
-    optim.synth_fill(ps.params, registry.SEED, 0, 0xFFFD, 0, 0, -6)
-    optim.synth_fill(ps.grads, registry.SEED, 1, 0xFFFD, 1, 0, -7, 10)
-    torch.cuda.synchronize()
-    for _ in range(args.warmup):
-        ps.step(cfg.lr)
-    torch.cuda.synchronize()
-    dist.barrier()
-    stream = torch.cuda.current_stream()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        ps.step(cfg.lr)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1) / args.steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
-    ms = ms.item()
-    owned = ps.hi - ps.lo
-    nvl = owned * (world - 1) * 4 / 1e9  # GB in (grads) and out (params) per rank
-    hbm = owned * (28 + 4 * world) / 1e9  # local state + master + grads + replica traffic
-    bound_ms = max(nvl / 770.0, hbm / measured_peaks()[0]) * 1e3
-    log(f"[rank {rank}] fused RS+adamw+AG: {ms:.2f} ms/step, NVLink {nvl:.1f} GB/dir/rank, "
-        f"roofline {bound_ms:.2f} ms")
-    return {"kernel": "peer_step_kernel (adamw, RS + update + AG over NVLink)", "ms": ms,
-            "params_per_s": P / (ms * 1e-3), "nvlink_gb_per_direction_per_rank": round(nvl, 2),
-            "roofline_ms": round(bound_ms, 3), "frac": round(bound_ms / ms, 4),
-            "nvlink_peak_gbs": 770.0}
 
 
 def load_traffic(kind, params_per_launch):
@@ -514,13 +565,10 @@ def pcie_ceiling(hp, dev):
 
 
 def bench_e2e(args, res, rank=0, world=1):
-    """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p).  N > 1: every rank
-    runs its own part (the ZeroPlan slice for the flat kinds and LOMO, every N-th tensor
-    for AdaLomo) through the same host-span calls over its own PCIe link; per-kind time =
-    max over ranks; bytes are whole-job."""
-    import math
-
-    import psutil
+    """Host-buffer end-to-end: per step H2D(p, g) + update + D2H(p) through the C-ABI
+    host-span calls (LOMO / AdaLomo with their clip).  N > 1: every rank runs its own
+    part (the ZeroPlan slice for the flat kinds and LOMO, every N-th tensor for AdaLomo)
+    over its own PCIe link; per-kind time = max over ranks; bytes are whole-job."""
     import torch
 
     from paper_2312_00407_b200 import optim
@@ -542,16 +590,16 @@ def bench_e2e(args, res, rank=0, world=1):
 
     P = res["owned"]
     shapes = res["shapes"] if world == 1 else res["shapes"][rank::world]
-    n_ada = sum(int(math.prod(s)) for s in shapes)
+    n_ada = sum(math.prod(s) for s in shapes)
     need = 2 * max(P, n_ada) * 4 * 1.3
-    avail = psutil.virtual_memory().available / world
+    avail = host_available_bytes() / world
     fits = need < avail * 0.6
     n = P
     if world == 1 and not fits:  # whole tensors prefix that fits
         cap = int(avail * 0.6 / (2 * 4 * 1.3)) // 1024 * 1024
         acc, k = 0, 0
-        while k < len(shapes) and acc + int(math.prod(shapes[k])) <= cap:
-            acc += int(math.prod(shapes[k]))
+        while k < len(shapes) and acc + math.prod(shapes[k]) <= cap:
+            acc += math.prod(shapes[k])
             k += 1
         shapes, n = shapes[:k], acc
         n_ada = n
@@ -566,7 +614,8 @@ def bench_e2e(args, res, rank=0, world=1):
     m = max(n, n_ada)
     hp = torch.empty(m, dtype=torch.float32, pin_memory=True)
     hg = torch.empty(m, dtype=torch.float32, pin_memory=True)
-    src_p, src_g = res["p"][:n].cpu(), res["g"][:n].cpu()
+    lo = res.get("lo", 0)
+    src_p, src_g = res["p"][lo:lo + n].cpu(), res["g"][lo:lo + n].cpu()
     for a in range(0, m, n):  # the part's values, repeated when AdaLomo's subset is larger
         b = min(m, a + n)
         hp[a:b].copy_(src_p[:b - a])
@@ -584,19 +633,19 @@ def bench_e2e(args, res, rank=0, world=1):
         gc.collect()
         k_n = n_ada if kind == "adalomo" else n
         hpn, hgn = hp[:k_n].numpy(), hg[:k_n].numpy()
-        if kind in ("adamw", "lion", "adan", "sophia"):
+        if kind in STORED:
             opt = optim.FlatOptimizer(cfg, k_n)
 
             def one():
                 opt.step(hpn, hgn, cfg.lr)  # mco_flat_step_host: pipelined H2D/step/D2H
         elif kind == "adalomo":
-            ada = optim.AdaLomoState(cfg, shapes)
+            ada = optim.AdaLomoState(cfg, shapes, grad_clip=CLIP)
 
             def one():
-                ada.apply_all(hpn, hgn, cfg.lr)  # per-tensor H2D / apply / D2H pipeline
+                ada.apply_all(hpn, hgn, cfg.lr)  # whole-set upload (clip), apply, download
         else:
             def one():
-                optim.lomo_apply(hpn, hgn, cfg.lr, 1.0)  # mco_lomo_apply_host
+                optim.lomo_step(hpn, hgn, cfg.lr, clip=CLIP)  # mco_lomo_apply_host, 2 passes
         one()
         torch.cuda.synchronize()
         barrier()
@@ -628,9 +677,27 @@ def bench_e2e(args, res, rank=0, world=1):
                                                                  if world > 1 else ""),
                          "frac": round(bound_s / tot_s, 4)},
             "path": "C-ABI host-span calls on pinned host buffers: mco_flat_step_host, "
-                    "mco_lomo_apply_host, mco_adalomo_apply_all_host (H2D p+g, update, D2H p "
-                    "pipelined per chunk / per tensor)" + (
+                    "mco_lomo_apply_host (with the clip pass), mco_adalomo_apply_all_host "
+                    "(with the clip; H2D p+g, update, D2H p)" + (
                         f"; each of {world} ranks over its own part" if world > 1 else "")}
+
+
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(n: int) -> int:
+    """`python bench.py --gpus N` outside torchrun: run this script under
+    torch.distributed.run with N local ranks (rank 0 prints the line)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr", "127.0.0.1",
+           "--master-port", str(free_port()), os.path.abspath(__file__), *sys.argv[1:]]
+    log(f"[bench] --gpus {n}: launching {n} ranks: {' '.join(cmd[1:6])} ...")
+    return subprocess.run(cmd).returncode
 
 
 def main():
@@ -646,30 +713,42 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-collectives", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--repeats", type=int, default=5,
                     help="K-step blocks per optimizer for the reported median (the first "
                          "block alone is the contract-timed value)")
     args = ap.parse_args()
 
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    env_world = os.environ.get("WORLD_SIZE")
+    if env_world is None and args.gpus > 1:
+        sys.exit(relaunch(args.gpus))
+    world = int(env_world or 1)
+    if world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch one rank per "
+              "GPU (torchrun --nproc-per-node N ... --gpus N)", file=sys.stderr)
+        sys.exit(2)
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))
     metric = "params updated/sec (all six optimizers, LLaMA-7B-shaped set)"
-    config = {"workload": "configs[1]: AdamW/Lion/Adan/Sophia/LOMO/AdaLomo each updating a "
-                          "LLaMA-7B-shaped synthetic set (291 tensors, 6,738,415,616 params)",
+    config = {"workload": "configs[1]: AdamW/Lion/Adan/Sophia/LOMO+clip/AdaLomo+clip each "
+                          "updating a LLaMA-7B-shaped synthetic set (291 tensors, "
+                          "6,738,415,616 params)" + (
+                              "; N > 1: the whole data-parallel step (gradient "
+                              "reduce-scatter, update, parameter all-gather) per optimizer"
+                              if world > 1 else ""),
               "model_shape": args.model, "params": None, "dtype_storage": "fp32 p/g/state",
+              "grad_norm_clip": CLIP,
               "l2": "inputs larger than L2 (27 GB per buffer); no flush needed",
-              "parallelism": f"zero{world}" if world > 1 else "single GPU"}
+              "parallelism": f"dp{world} (ZeRO stage 2)" if world > 1 else "single GPU"}
 
     if args.impl == "reference":
         if rank != 0:
             return
-        value, threads, sample, per, sec_step = run_cpu_reference(args.warmup, args.steps)
-        from paper_2312_00407_b200.registry import LLAMA_7B
-
-        config["params"] = LLAMA_7B.param_count()
+        value, threads, sample, per, sec_step, n = run_cpu_reference(args.warmup, args.steps)
+        config["params"] = n
+        config["sample"] = sample
         line = {"impl": "reference", "metric": metric, "value": value, "unit": "params/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": sec_step * 1e3, "higher_is_better": True,
@@ -690,6 +769,10 @@ def main():
     if world > 1:
         backend = os.environ.get("MCO_BENCH_BACKEND", "nccl")  # gloo: test N ranks on 1 GPU
         if backend == "nccl":
+            if torch.cuda.device_count() < world:
+                print(f"bench.py: {world} ranks but {torch.cuda.device_count()} GPUs",
+                      file=sys.stderr)
+                sys.exit(2)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             dist.init_process_group(backend)
@@ -705,9 +788,10 @@ def main():
             log(f"[e2e] failed: {ex!r}")
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, threads, sample, per, _ = run_cpu_reference(1, args.cpu_steps)
+            v, threads, sample, per, _, n = run_cpu_reference(1, args.cpu_steps)
             cpu = {"value": v, "unit": "params/s", "cores": threads, "kind": "reference",
-                   "cpu_model": cpu_model(), "sample": sample, "per_optimizer": per}
+                   "cpu_model": cpu_model(), "sample": sample, "params": n,
+                   "per_optimizer": per}
             cpu["single_thread"] = run_cpu_single_thread()
         except Exception as ex:
             log(f"[cpu_baseline] failed: {ex!r}")
@@ -719,8 +803,10 @@ def main():
                 "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "per_optimizer": res["per"]}
-        if "collectives" in res:
-            line["collectives"] = res["collectives"]
+        if world > 1:
+            line["collectives"] = {"backend": dist.get_backend(),
+                                   "nccl_allgather_busbw_gbs": res["busbw"],
+                                   "nvlink_nominal_gbs": NVLINK_NOMINAL_GBS}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -35,6 +35,8 @@ class Config(C.Structure):
     @staticmethod
     def of(cfg) -> "Config":
         """From a paper_2312_00407_b200.optim.OptimizerConfig (or anything with its fields)."""
+        if isinstance(cfg, Config):
+            return cfg
         return Config(int(cfg.kind), cfg.lr, cfg.weight_decay, cfg.beta1, cfg.beta2, cfg.beta3,
                       cfg.eps, 1 if cfg.clip_threshold is not None else 0,
                       float(cfg.clip_threshold or 0.0), cfg.adalomo_clip, cfg.sophia_rho,
@@ -121,7 +123,7 @@ def _load_ref():
                                  C.POINTER(_u64)]),
         "ref_zero_plan": (_i, [C.c_size_t, _i, _i, C.POINTER(C.c_size_t),
                                C.POINTER(C.c_size_t)]),
-        "ref_bench": (_i, [_CP, _i, C.POINTER(_i), C.POINTER(_i64), _i, _i, _i, _u64, _D]),
+        "ref_bench": (_i, [_CP, _i, C.POINTER(_i), C.POINTER(_i64), _i, _i, _i, _u64, _d, _D]),
     }
     for n, (r, a) in sigs.items():
         f = getattr(lib, n)
@@ -323,12 +325,40 @@ def ref_lomo_fused(params: list, grads: list, lr: float, clip: float | None) -> 
     ref_check(ref.ref_lomo_fused_step(n, numels, ps, gs, lr, -1.0 if clip is None else clip))
 
 
-def ref_bench(cfg, shapes, threads: int, warmup: int, steps: int, seed: int = 2024) -> float:
-    """Seconds per step of the reference CPU path on `threads` host threads."""
+def ref_bench(cfg, shapes, threads: int, warmup: int, steps: int, seed: int = 2024,
+              clip=None) -> float:
+    """Seconds per step of the reference CPU path on `threads` host threads; clip (LOMO /
+    AdaLomo): the global grad-norm pass of optim.cpp:291-303 before the updates."""
     nd = (C.c_int * len(shapes))(*[len(s) for s in shapes])
     flat = [int(d) for s in shapes for d in s]
     dims = (C.c_int64 * max(len(flat), 1))(*flat)
     out = C.c_double()
     ref_check(ref.ref_bench(C.byref(Config.of(cfg)), len(shapes), nd, dims, threads, warmup,
-                            steps, seed, C.byref(out)))
+                            steps, seed, -1.0 if clip is None else float(clip), C.byref(out)))
     return out.value
+
+
+# ---- reference arm helpers (bench.py --impl reference / cpu_baseline): the reference's
+# own kind parser and defaults, no product code ------------------------------------------
+
+
+def ref_config(kind: str, **overrides) -> Config:
+    """OptimizerConfig::defaults_for(parse_kind(kind)) from the compiled reference
+    (optim.cpp:13-61), then the given field overrides."""
+    k = C.c_int()
+    ref_check(ref.ref_parse_kind(kind.encode(), C.byref(k)))
+    c = Config()
+    ref_check(ref.ref_defaults_for(k.value, C.byref(c)))
+    for a, v in overrides.items():
+        setattr(c, a, v)
+    return c
+
+
+def llama_shapes(hidden: int, inter: int, layers: int, vocab: int, kv=None) -> list:
+    """The reference registry order (model.cpp:353-370): tok_embedding, per layer
+    attn_norm, q, k, v, o, mlp_norm, gate, up, down; final_norm, lm_head."""
+    H, I, V, K = hidden, inter, vocab, kv or hidden
+    out = [(V, H)]
+    for _ in range(layers):
+        out += [(H,), (H, H), (K, H), (K, H), (H, H), (H,), (I, H), (I, H), (H, I)]
+    return out + [(H,), (V, H)]

@@ -283,12 +283,21 @@ int ref_zero_plan(size_t total, int dp, int stage, size_t* part_sizes, size_t* o
 
 // ---- CPU baseline timing (reference code on all host cores) ------------------------
 // Flat kinds: `threads` FlatOptimizers over disjoint slices of an n-element set.
-// Fused kinds: the registry tensors (shapes) spread round-robin over threads;
-// lomo_apply / AdaLomoState::apply per tensor.  Inputs are the synthetic
-// generator's values (params role 0, grads role 1).  Returns mean seconds per
-// step over `steps` timed steps after `warmup` untimed ones.
+// Fused kinds: the registry tensors (shapes) spread over threads largest-first onto the
+// least-loaded thread (LPT), so every thread gets work when there are more tensors than
+// threads; lomo_apply / AdaLomoState::apply per tensor.  clip >= 0 adds the global
+// gradient-norm pass of lomo_fused_backward_step (optim.cpp:291-303): every thread sums
+// g^2 over its tensors in the reference hook's order (`sum_sq += g * g`, optim.cpp:297),
+// the partials are combined in thread order, scale = clip / norm iff norm > clip and
+// norm > 0; LOMO then runs lomo_apply(t, lr, scale), AdaLomo scales the gradient by it
+// before AdaLomoState::apply (the composed oracle of SURVEY 8(c) "parity unpinned" 1).
+// The sum and the gradient scaling are the only arithmetic this file restates; every
+// update is the reference's.  Inputs are the synthetic generator's values (params
+// role 0, grads role 1).  Returns mean seconds per step over `steps` timed steps after
+// `warmup` untimed ones.
 int ref_bench(const ref_config* c, int ntensors, const int* ndims, const int64_t* dims,
-              int threads, int warmup, int steps, uint64_t seed, double* sec_per_step) {
+              int threads, int warmup, int steps, uint64_t seed, double clip,
+              double* sec_per_step) {
   return guard([&] {
     const OptimizerConfig cfg = to_cfg(*c);
     std::vector<Shape> shapes;
@@ -299,30 +308,53 @@ int ref_bench(const ref_config* c, int ntensors, const int* ndims, const int64_t
     }
     const int T = std::max(1, threads);
     std::barrier sync(T + 1);
+    std::barrier workers(T);
     std::atomic<int> failed{0};
     std::vector<std::thread> pool;
     const bool fused = is_fused(cfg.kind);
+    const bool clipped = fused && clip >= 0;
+    std::vector<double> partial(static_cast<size_t>(T), 0.0);
+    // LPT assignment of tensors to threads (fused kinds)
+    std::vector<int> owner(static_cast<size_t>(ntensors), 0);
+    {
+      std::vector<int> order(static_cast<size_t>(ntensors));
+      for (int k = 0; k < ntensors; ++k) order[static_cast<size_t>(k)] = k;
+      std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+        return shape_numel(shapes[static_cast<size_t>(a)]) >
+               shape_numel(shapes[static_cast<size_t>(b)]);
+      });
+      std::vector<int64_t> load(static_cast<size_t>(T), 0);
+      for (int k : order) {
+        const size_t w = static_cast<size_t>(std::min_element(load.begin(), load.end()) -
+                                             load.begin());
+        owner[static_cast<size_t>(k)] = static_cast<int>(w);
+        load[w] += shape_numel(shapes[static_cast<size_t>(k)]);
+      }
+    }
+    auto make_tensor = [&](int k) {
+      const Shape& s = shapes[static_cast<size_t>(k)];
+      const size_t n = static_cast<size_t>(shape_numel(s));
+      std::vector<double> pv(n), gv(n);
+      orc_synth_f64(pv.data(), n, orc_synth_key(seed, 0, static_cast<uint32_t>(k), 0),
+                    s.size() == 2 ? s[1] : 0, s.size() == 2 ? -6 : 0, 0, 0);
+      if (s.size() != 2) std::fill(pv.begin(), pv.end(), 1.0);
+      orc_synth_f64(gv.data(), n, orc_synth_key(seed, 1, static_cast<uint32_t>(k), 1),
+                    s.size() == 2 ? s[1] : 0, -7, 10, s.size() == 2);
+      Tensor t = Tensor::leaf(s, std::move(pv), true);
+      t.mark_param("t" + std::to_string(k));
+      t.grad() = std::move(gv);
+      return t;
+    };
     std::unique_ptr<AdaLomoState> ada;
     std::vector<Tensor> ada_params;
-    // Per-thread setup happens inside the thread (first-touch locality).
     std::vector<std::vector<Tensor>> owned(static_cast<size_t>(T));
     if (cfg.kind == Kind::kAdaLomo) {
-      // AdaLomoState keys entries on tensor identity; build every tensor up
-      // front so one state serves all threads (entries are disjoint per tensor).
+      // AdaLomoState keys entries on tensor identity; build every tensor up front so
+      // one state serves all threads (entries are disjoint per tensor).
       for (int k = 0; k < ntensors; ++k) {
-        const Shape& s = shapes[static_cast<size_t>(k)];
-        const size_t n = static_cast<size_t>(shape_numel(s));
-        std::vector<double> pv(n), gv(n);
-        orc_synth_f64(pv.data(), n, orc_synth_key(seed, 0, static_cast<uint32_t>(k), 0),
-                      s.size() == 2 ? s[1] : 0, s.size() == 2 ? -6 : 0, 0, 0);
-        if (s.size() != 2) std::fill(pv.begin(), pv.end(), 1.0);
-        orc_synth_f64(gv.data(), n, orc_synth_key(seed, 1, static_cast<uint32_t>(k), 1),
-                      s.size() == 2 ? s[1] : 0, -7, 10, s.size() == 2);
-        Tensor t = Tensor::leaf(s, std::move(pv), true);
-        t.mark_param("t" + std::to_string(k));
-        t.grad() = std::move(gv);
+        Tensor t = make_tensor(k);
         ada_params.push_back(t);
-        owned[static_cast<size_t>(k % T)].push_back(t);
+        owned[static_cast<size_t>(owner[static_cast<size_t>(k)])].push_back(t);
       }
       ada = std::make_unique<AdaLomoState>(cfg, ada_params);
     }
@@ -334,7 +366,7 @@ int ref_bench(const ref_config* c, int ntensors, const int* ndims, const int64_t
         try {
           std::unique_ptr<FlatOptimizer> opt;
           std::vector<double> p, g;
-          if (!fused) {
+          if (!fused) {  // per-thread setup inside the thread (first-touch locality)
             const uint64_t q = total / T, r = total % T;
             const uint64_t len = q + (static_cast<uint64_t>(w) < r ? 1 : 0);
             const uint64_t off = static_cast<uint64_t>(w) * q + std::min<uint64_t>(w, r);
@@ -344,30 +376,37 @@ int ref_bench(const ref_config* c, int ntensors, const int* ndims, const int64_t
             orc_synth_f64(g.data(), len, orc_synth_key(seed, 1, 0xffffu, 1) + off * 0x9E3779B97F4A7C15ULL, 0, -7, 10, 0);
             opt = std::make_unique<FlatOptimizer>(cfg, len);
           } else if (cfg.kind == Kind::kLomo) {
-            for (int k = w; k < ntensors; k += T) {
-              const Shape& s = shapes[static_cast<size_t>(k)];
-              const size_t n = static_cast<size_t>(shape_numel(s));
-              std::vector<double> pv(n), gv(n);
-              orc_synth_f64(pv.data(), n, orc_synth_key(seed, 0, static_cast<uint32_t>(k), 0), 0,
-                            -6, 0, 0);
-              orc_synth_f64(gv.data(), n, orc_synth_key(seed, 1, static_cast<uint32_t>(k), 1), 0,
-                            -7, 10, 0);
-              Tensor t = Tensor::leaf(s, std::move(pv), true);
-              t.mark_param("t" + std::to_string(k));
-              t.grad() = std::move(gv);
-              owned[static_cast<size_t>(w)].push_back(t);
-            }
+            for (int k = 0; k < ntensors; ++k)
+              if (owner[static_cast<size_t>(k)] == w)
+                owned[static_cast<size_t>(w)].push_back(make_tensor(k));
           }
+          auto& mine = owned[static_cast<size_t>(w)];
           for (int it = 0; it < warmup + steps; ++it) {
             sync.arrive_and_wait();  // start of step
             if (!fused) {
               opt->step(p, g, cfg.lr);
             } else {
-              for (Tensor& t : owned[static_cast<size_t>(w)]) {
-                if (cfg.kind == Kind::kLomo)
-                  lomo_apply(t, cfg.lr, 1.0);
-                else
+              double scale = 1.0;
+              if (clipped) {
+                double sum_sq = 0.0;
+                for (Tensor& t : mine)
+                  for (double x : t.grad()) sum_sq += x * x;
+                partial[static_cast<size_t>(w)] = sum_sq;
+                workers.arrive_and_wait();
+                double all = 0.0;
+                for (double x : partial) all += x;  // thread order
+                const double norm = std::sqrt(all);
+                if (norm > clip && norm > 0) scale = clip / norm;
+                workers.arrive_and_wait();  // partials read before the next step
+              }
+              for (Tensor& t : mine) {
+                if (cfg.kind == Kind::kLomo) {
+                  lomo_apply(t, cfg.lr, scale);
+                } else {
+                  if (scale != 1.0)
+                    for (double& x : t.grad()) x *= scale;
                   ada->apply(t, cfg.lr);
+                }
               }
             }
             sync.arrive_and_wait();  // end of step
@@ -377,6 +416,10 @@ int ref_bench(const ref_config* c, int ntensors, const int* ndims, const int64_t
           failed = 1;
           for (int it = 0; it < warmup + steps; ++it) {
             sync.arrive_and_wait();
+            if (clipped) {
+              workers.arrive_and_wait();
+              workers.arrive_and_wait();
+            }
             sync.arrive_and_wait();
           }
         }

@@ -89,6 +89,39 @@ def elem_phase(t) -> int:
     return (t.data_ptr() // t.element_size()) % 8
 
 
+def _gloo_cuda(t, group) -> bool:
+    return t.is_cuda and _dist().get_backend(group) == "gloo"
+
+
+def rs_tensor(out, inp, group=None) -> None:
+    """reduce_scatter_tensor(SUM).  gloo has no CUDA reduce-scatter (it is the backend of
+    the several-ranks-on-one-GPU tests): all-reduce a copy and keep this rank's chunk."""
+    dist = _dist()
+    if _gloo_cuda(inp, group):
+        tmp = inp.clone()
+        dist.all_reduce(tmp, op=dist.ReduceOp.SUM, group=group)
+        r, n = dist.get_rank(group), out.numel()
+        out.copy_(tmp[r * n:(r + 1) * n])
+        return
+    dist.reduce_scatter_tensor(out, inp, op=dist.ReduceOp.SUM, group=group)
+
+
+def ag_tensor(out, inp, group=None) -> None:
+    """all_gather_into_tensor; gloo + CUDA: an all-reduce of zeros around this rank's
+    chunk (x + 0 == x exactly)."""
+    dist = _dist()
+    if _gloo_cuda(inp, group):
+        import torch
+
+        r, n = dist.get_rank(group), inp.numel()
+        tmp = torch.zeros_like(out)
+        tmp[r * n:(r + 1) * n].copy_(inp)
+        dist.all_reduce(tmp, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(tmp)
+        return
+    dist.all_gather_into_tensor(out, inp, group=group)
+
+
 def reduce_scatter_owned(flat, plan: ZeroPlan, rank: int, group=None, phase: int = 0):
     """SUM-reduce `flat` and return this rank's owned slice (comm.cpp:219-246 semantics),
     in a buffer of the given alignment phase."""
@@ -99,15 +132,18 @@ def reduce_scatter_owned(flat, plan: ZeroPlan, rank: int, group=None, phase: int
         return flat[lo:hi]
     if plan.even:
         out = phased_empty(hi - lo, flat.dtype, flat.device, phase)
-        dist.reduce_scatter_tensor(out, flat, op=dist.ReduceOp.SUM, group=group)
+        rs_tensor(out, flat, group)
         return out
     out = None
     for r in range(world):
         a, b = plan.owned_range(r)
         part = phased_empty(b - a, flat.dtype, flat.device, phase if r == rank else 0)
         part.copy_(flat[a:b])
-        dist.reduce(part, dst=dist.get_global_rank(group, r) if group else r,
-                    op=dist.ReduceOp.SUM, group=group)
+        if _gloo_cuda(part, group):
+            dist.all_reduce(part, op=dist.ReduceOp.SUM, group=group)
+        else:
+            dist.reduce(part, dst=dist.get_global_rank(group, r) if group else r,
+                        op=dist.ReduceOp.SUM, group=group)
         if r == rank:
             out = part
     return out
@@ -121,7 +157,7 @@ def all_gather_owned(flat, plan: ZeroPlan, rank: int, group=None) -> None:
         return
     lo, hi = plan.owned_range(rank)
     if plan.even:
-        dist.all_gather_into_tensor(flat[:plan.offsets[-1]], flat[lo:hi].clone(), group=group)
+        ag_tensor(flat[:plan.offsets[-1]], flat[lo:hi].clone(), group)
         return
     for r in range(world):
         a, b = plan.owned_range(r)
@@ -512,6 +548,138 @@ class RowShardedAdaLomo:
         if multi:
             dist.all_reduce(self.state.payload(1), op=dist.ReduceOp.SUM, group=self.group)
         self.state.phase(3, local_p, local_g, lr, stream)
+
+    # ---- data-parallel form: gradients reduced and parameters gathered in the step ----
+    # Rank-major layout: chunk q (q = 0..world-1, `chunk` elements each, zero padded)
+    # holds rank q's local buffer (its row slices + every replicated 1-D tensor, in
+    # registry order).  A reduce-scatter(SUM) of each rank's local gradients in this
+    # layout hands rank r exactly the summed gradient of its rows and of the replicated
+    # tensors; an all-gather of the chunks rebuilds every rank's replica.
+
+    @staticmethod
+    def local_len_of(shapes, world: int, rank: int) -> int:
+        n = 0
+        for s in shapes:
+            if len(s) == 2:
+                _, offs = optim.zero_plan(s[0], world, 1)
+                n += (offs[rank + 1] - offs[rank]) * s[1]
+            else:
+                k = 1
+                for d in s:
+                    k *= d
+                n += k
+        return n
+
+    @staticmethod
+    def chunk_len(shapes, world: int) -> int:
+        """Rank-major chunk length: the largest rank's local buffer."""
+        return max(RowShardedAdaLomo.local_len_of(shapes, world, r) for r in range(world))
+
+    def local_len(self, rank: int) -> int:
+        return self.local_len_of(self.global_shapes, self.world, rank)
+
+    @property
+    def chunk(self) -> int:
+        if not hasattr(self, "_chunk"):
+            self._chunk = self.chunk_len(self.global_shapes, self.world)
+        return self._chunk
+
+    def pieces_of(self, rank: int):
+        """(global offset, length) of rank's local pieces, registry order."""
+        out, goff = [], 0
+        for s in self.global_shapes:
+            n = 1
+            for d in s:
+                n *= d
+            if len(s) == 2:
+                _, offs = optim.zero_plan(s[0], self.world, 1)
+                out.append((goff + offs[rank] * s[1], (offs[rank + 1] - offs[rank]) * s[1]))
+            else:
+                out.append((goff, n))
+            goff += n
+        return out
+
+    def to_rank_major(self, flat_global, out=None):
+        """Registry-order flat buffer -> rank-major (world x chunk)."""
+        import torch
+
+        c = self.chunk
+        if out is None:
+            out = torch.zeros(self.world * c, dtype=flat_global.dtype, device=flat_global.device)
+        for r in range(self.world):
+            off = r * c
+            for a, n in self.pieces_of(r):
+                out[off:off + n].copy_(flat_global[a:a + n])
+                off += n
+        return out
+
+    def from_rank_major(self, rm, flat_global) -> None:
+        """Rank-major -> registry order (replicated tensors taken from chunk 0)."""
+        c = self.chunk
+        for r in range(self.world):
+            off = r * c
+            for a, n in self.pieces_of(r):
+                flat_global[a:a + n].copy_(rm[off:off + n])
+                off += n
+
+    def step_dp(self, rm_params, rm_grads, lr: float, stream=None) -> None:
+        """One data-parallel AdaLomo step (C3 at N GPUs): reduce-scatter(SUM) of the
+        rank-major local gradients -> phase 1 -> all-reduce statistics payload (column
+        sums, Σg² for the clip, Σp², Σv_row) -> phase 2 -> all-reduce Σu² payload ->
+        phase 3 on this rank's rows -> all-gather of the rank-major parameters.  Equals
+        serial AdaLomo (optim.cpp:215-275, clip: optim.cpp:302-303) on the summed
+        gradient; the reference's TP variant (parallel.cpp:334, 593-594) does not."""
+        dist = _dist()
+        c, n = self.chunk, self.local_numel
+        if rm_params.numel() != self.world * c or rm_grads.numel() != self.world * c:
+            raise optim.ContractError(
+                f"row-sharded adalomo: rank-major buffers of {rm_params.numel()} / "
+                f"{rm_grads.numel()} elements, expected {self.world} x {c}")
+        lo = self.rank * c
+        local_p = rm_params[lo:lo + n]
+        if self.world > 1 and dist.is_initialized():
+            if not hasattr(self, "_gred") or self._gred.dtype != rm_grads.dtype:
+                self._gred = phased_empty(c, rm_grads.dtype, rm_grads.device,
+                                          elem_phase(local_p))
+            rs_tensor(self._gred, rm_grads, self.group)
+            local_g = self._gred[:n]
+        else:
+            local_g = rm_grads[lo:lo + n]
+        self.step(local_p, local_g, lr, stream)
+        if self.world > 1 and dist.is_initialized():
+            ag_tensor(rm_params, rm_params[lo:lo + c].clone(), self.group)
+
+
+class ZeroShardedLomo:
+    """LOMO (optionally with the global grad-norm clip, C5) as a data-parallel ZeRO
+    step: reduce-scatter(SUM) of the flat gradients over ZeroPlan parts -> local Σg² ->
+    all-reduce of one fp64 scalar -> clipped update of the owned slice -> all-gather of
+    the parameters (parallel.cpp:656-666 with LOMO in place of FlatOptimizer; the
+    reference forbids the clip in parallel runs, parallel.cpp:335-337, this applies the
+    serial rule, optim.cpp:291-303, to the summed gradient)."""
+
+    def __init__(self, total_len: int, clip: Optional[float] = None, group=None,
+                 ops=_CudaLomoOps):
+        dist = _dist()
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        check_agreement("ZeroShardedLomo", dict(total_len=total_len, clip=clip), group)
+        self.plan = ZeroPlan.make(total_len, self.world, 2)
+        self.lo, self.hi = self.plan.owned_range(self.rank)
+        self.total_len, self.clip, self.ops = total_len, clip, ops
+
+    def step(self, flat_params, flat_grads, lr: float, stream=None):
+        if flat_params.numel() != self.total_len or flat_grads.numel() != self.total_len:
+            raise optim.ContractError(
+                f"zero lomo step: flat buffers of {flat_params.numel()} / "
+                f"{flat_grads.numel()} elements for a plan of {self.total_len}")
+        p_owned = flat_params[self.lo:self.hi]
+        g_owned = reduce_scatter_owned(flat_grads, self.plan, self.rank, self.group,
+                                       phase=elem_phase(p_owned) if p_owned.is_cuda else 0)
+        s = sharded_lomo_step(p_owned, g_owned, lr, self.clip, self.group, stream, self.ops)
+        all_gather_owned(flat_params, self.plan, self.rank, self.group)
+        return s
 
 
 def reshard_state(states: list, total_len: int, new_world: int) -> list:
