@@ -249,7 +249,7 @@ class Stepper:
     (module docstring), and `local()` = the same update kernels on this rank's part
     without the collectives (the shard-local figure)."""
 
-    def __init__(self, kind, shapes, P, bp, bg, world, rank, comm=None):
+    def __init__(self, kind, shapes, P, bp, bg, world, rank, comm=None, bucket=0):
         from paper_2312_00407_b200 import optim, zero
 
         self.kind, self.world, self.rank = kind, world, rank
@@ -278,15 +278,17 @@ class Stepper:
         lo, hi = plan.owned_range(rank)
         self.n_local = hi - lo
         if kind in STORED:
-            if comm is not None:  # NCCL: the C-ABI sharded step (mco_shard_step)
-                self.opt = zero.NativeZeroOptimizer(self.cfg, P, comm, device=dev)
-                flat = self.opt.opt
+            if comm is not None:  # NCCL: the C-ABI bucketed, double-buffered step (mco_zb)
+                self.opt = zero.BucketedZeroOptimizer(self.cfg, P, comm, bucket_elems=bucket)
+                self._step = lambda: self.opt.step(self.p, self.g, self.lr)
+                self.local = lambda: self.opt.step_local(self.p, self.g, self.lr)
+                self.n_local = self.opt.owned
             else:  # gloo (several ranks on one GPU in the tests): torch.distributed
                 self.opt = zero.ZeroShardedOptimizer(self.cfg, P, device=dev)
                 flat = self.opt.opt
-            self._step = lambda: self.opt.step(self.p, self.g, self.lr)
-            po, go = self.p[lo:hi], self.g[lo:hi]
-            self.local = lambda: flat.step(po, go, self.lr)
+                self._step = lambda: self.opt.step(self.p, self.g, self.lr)
+                po, go = self.p[lo:hi], self.g[lo:hi]
+                self.local = lambda: flat.step(po, go, self.lr)
         elif kind == "lomo":
             self.opt = zero.ZeroShardedLomo(P, CLIP)
             self._step = lambda: self.opt.step(self.p, self.g, self.lr)
@@ -310,7 +312,8 @@ class Stepper:
 
     def steps_taken(self):
         o = getattr(self, "opt", None)
-        o = getattr(o, "opt", o)  # the sharded wrappers keep a FlatOptimizer in .opt
+        if o is not None and not hasattr(o, "steps_taken"):
+            o = getattr(o, "opt", None)  # ZeroShardedOptimizer keeps its FlatOptimizer in .opt
         return o.steps_taken() if hasattr(o, "steps_taken") else 0
 
 
@@ -406,7 +409,7 @@ def bench_ours(args, rank, world, local_rank):
     per, total_ms, launches = {}, 0.0, 0
     clocks = ClockSampler(local_rank)
     for kind in kinds:
-        st = Stepper(kind, shapes, P, bp, bg, world, rank, comm)
+        st = Stepper(kind, shapes, P, bp, bg, world, rank, comm, args.bucket_elems)
         for _ in range(args.warmup):
             st.step()
         torch.cuda.synchronize()
@@ -624,7 +627,7 @@ def bench_e2e(args, res, rank=0, world=1):
     pcie = pcie_ceiling(hp, res["p"].device)
     log(f"[e2e] rank {rank}: PCIe ceiling (pinned, GB/s): {pcie}")
     steps = max(1, min(args.steps, args.e2e_steps))
-    tot_s, h2d, d2h, h2d_me, d2h_me = 0.0, 0, 0, 0, 0
+    tot_s, h2d, d2h, h2d_me, d2h_me, bound_serial = 0.0, 0, 0, 0, 0, 0.0
     per = {}
     opt = ada = one = None
     for kind in res["kinds"]:
@@ -655,18 +658,26 @@ def bench_e2e(args, res, rank=0, world=1):
         torch.cuda.synchronize()
         dt = max_over_ranks((time.perf_counter() - t0) / steps)
         total = res["P"] if world > 1 else k_n  # params of the whole job this step
-        per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": total / dt}
+        # LOMO's clip pass streams g once more (mco_lomo_apply_host: Σg² pass, then the
+        # update pass over p and g); with a clip no parameter can leave before every
+        # gradient has arrived, so H2D and D2H do not overlap for LOMO / AdaLomo
+        hb = (3 if kind == "lomo" else 2) * 4
+        per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": total / dt,
+                     "h2d_bytes_per_param": hb, "d2h_bytes_per_param": 4}
         tot_s += dt
-        h2d += 2 * total * 4
+        h2d += hb * total
         d2h += total * 4
-        h2d_me += 2 * k_n * 4
-        d2h_me += k_n * 4
+        if kind in ("lomo", "adalomo"):
+            bound_serial += hb * k_n / (pcie["h2d_gbs"] * 1e9) + 4 * k_n / (pcie["d2h_gbs"] * 1e9)
+        else:
+            h2d_me += hb * k_n
+            d2h_me += k_n * 4
         if rank == 0:
             log(f"[e2e] {kind}: {dt * 1e3:.1f} ms/step, {total / dt / 1e9:.2f} Gparam/s")
     # the copies bound the step: max(H2D bytes / H2D BW, D2H / D2H BW, all / both-ways BW)
     # over this rank's own link (every rank has one)
     bound_s = max(h2d_me / (pcie["h2d_gbs"] * 1e9), d2h_me / (pcie["d2h_gbs"] * 1e9),
-                  (h2d_me + d2h_me) / (pcie["both_gbs"] * 1e9))
+                  (h2d_me + d2h_me) / (pcie["both_gbs"] * 1e9)) + bound_serial
     total_params = res["P"] if world > 1 else n
     return {"value": len(per) * total_params / tot_s, "unit": "params/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "params": total_params,
@@ -714,6 +725,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=1)
+    ap.add_argument("--bucket-elems", type=int, default=1 << 27,
+                    help="N > 1: bucket size of the bucketed stage-2 step (elements)")
     ap.add_argument("--repeats", type=int, default=5,
                     help="K-step blocks per optimizer for the reported median (the first "
                          "block alone is the contract-timed value)")

@@ -282,6 +282,18 @@ mco_status mco_comm_unique_id(void* id_out_128);
 mco_status mco_comm_create(const void* id_128, int nranks, int rank, int device,
                            mco_comm** out);
 mco_status mco_comm_destroy(mco_comm* c);
+/* Failure handling (comm.cpp:126-132 collective timeouts, comm.cpp:330-348 abort with
+ * the failing rank named): communicators are non-blocking with a deadline --
+ * timeout_s (<= 0: $MCO_NCCL_TIMEOUT_S, default 600 s).  An init that does not complete
+ * in time (a rank never joined), an NCCL error, or a mco_comm_wait whose collectives do
+ * not finish in time aborts the communicator (ncclCommAbort) and returns MCO_PROTOCOL
+ * with "[rank r of N] <what it waited for>"; later calls on it fail the same way. */
+mco_status mco_comm_create_timeout(const void* id_128, int nranks, int rank, int device,
+                                   double timeout_s, mco_comm** out);
+/* Host wait until `stream` (its collectives) completes, bounded by the deadline. */
+mco_status mco_comm_wait(mco_comm* c, void* stream);
+/* ncclCommAbort (idempotent); the handle still has to be destroyed. */
+mco_status mco_comm_abort(mco_comm* c);
 /* ncclCommGetAsyncError: MCO_PROTOCOL if the communicator has failed. */
 mco_status mco_comm_check(mco_comm* c);
 /* In-place SUM all-reduce (LOMO global sum of squares, AdaLomo statistic payloads). */
@@ -304,6 +316,64 @@ mco_status mco_shard_step(mco_flat* h, mco_comm* c, void* flat_params, int param
 mco_status mco_shard_step_mixed(mco_flat* h, mco_comm* c, float* master_owned,
                                 uint16_t* flat_params_bf16, const void* flat_grads,
                                 int grad_dtype, uint64_t total_len, double lr, void* stream);
+
+/* ---- bucketed, double-buffered stage-2 step (parallel.cpp:656-666) --
+ * The registry-order flat vector is cut into buckets of B elements (bucket_elems rounded
+ * up to a multiple of 8 N; 0 = one bucket); inside bucket k rank i owns piece i of
+ * ZeroPlan(len_k, N) (parallel.cpp:20-34 per bucket), so every rank updates its share of
+ * every bucket.  Per bucket, as its local gradient becomes ready: ncclReduceScatter(SUM)
+ * on the library's comm stream -> the fused update of this rank's piece on its update
+ * stream -> ncclAllGather of the bucket's replicas, issued after the NEXT bucket's
+ * reduce-scatter (which therefore overlaps this update).  No full-length gradient has to
+ * be resident: a caller can produce bucket k into the library's staging slot
+ * (mco_zb_grad_buffer, double-buffered) right before handing it in.  Results equal the
+ * whole-vector stage-2 step (elementwise update) and the serial FlatOptimizer on the
+ * rank-summed gradient.  replica_dtype F32 (params = replicas) or BF16 (fp32 master of
+ * the owned pieces + bf16 replicas: the C4 mixed layout).  State is fp32. */
+typedef struct mco_zb mco_zb;
+/* The bucket plan alone (host arithmetic): rounded bucket size, bucket count, and rank's
+ * piece of bucket k -- registry elements [bucket_off + off, bucket_off + off + n). */
+mco_status mco_zb_plan(uint64_t total_len, int nranks, uint64_t bucket_elems, int k, int rank,
+                       uint64_t* bucket_rounded, int* nbuckets, uint64_t* bucket_off,
+                       uint64_t* bucket_len, uint64_t* off, uint64_t* n);
+mco_status mco_zb_create(const mco_config* cfg, mco_comm* c, uint64_t total_len,
+                         uint64_t bucket_elems, int grad_dtype, int replica_dtype,
+                         mco_zb** out);
+mco_status mco_zb_destroy(mco_zb* z);
+/* Rounded bucket size, bucket count, owned elements, the state handle (buffers() names /
+ * steps over the owned pieces in bucket order; owned by z) and the fp32 master (BF16
+ * replicas; NULL otherwise). */
+mco_status mco_zb_info(const mco_zb* z, uint64_t* bucket_elems, int* nbuckets,
+                       uint64_t* owned, mco_flat** flat, float** master);
+/* Rank r's piece of bucket k: registry elements [bucket_off + off, bucket_off + off + n);
+ * state_off = its offset in this rank's state (UINT64_MAX for another rank). */
+mco_status mco_zb_piece(const mco_zb* z, int k, int rank, uint64_t* bucket_off,
+                        uint64_t* bucket_len, uint64_t* off, uint64_t* n, uint64_t* state_off);
+/* BF16 replicas: load the fp32 master of the owned pieces from a full registry-order
+ * buffer (F32, or BF16 widened exactly). */
+mco_status mco_zb_load_master(mco_zb* z, const void* full, int dtype, void* stream);
+/* One step: begin (++t, optim.cpp:104) -> grad_ready for every bucket exactly once, in
+ * the same order on every rank -> end (stream waits for the last all-gather). */
+mco_status mco_zb_begin(mco_zb* z, void* replicas, double lr, void* stream);
+/* Staging slot (k mod 2) for bucket k's local gradient; stream waits until it is free. */
+mco_status mco_zb_grad_buffer(mco_zb* z, int k, void** dev_ptr, uint64_t* len, void* stream);
+/* Bucket k's local gradient is complete on `stream`, at `grad` (len_k elements) or, when
+ * grad is NULL, in its staging slot. */
+mco_status mco_zb_grad_ready(mco_zb* z, int k, const void* grad, void* stream);
+mco_status mco_zb_end(mco_zb* z, void* stream);
+/* Ring mode (mco_zb_begin with replicas == NULL; BF16 replicas only, the stage-3 layout
+ * for sets whose full replicas do not fit, e.g. 65B Sophia at N = 8): bucket k is
+ * gathered into ring slot k mod 2; this returns it (len_k bf16 elements) and makes
+ * `stream` wait for its all-gather.  Valid until bucket k+2's update. */
+mco_status mco_zb_gathered(mco_zb* z, int k, void** dev_ptr, void* stream);
+/* The step's update kernels alone (each piece from this rank's own local gradient, no
+ * collectives): the shard-local cost the collectives add to (benchmarks). */
+mco_status mco_zb_step_local(mco_zb* z, void* replicas, const void* flat_grads, double lr,
+                             void* stream);
+/* Whole step from a full local gradient buffer (buckets in reverse registry order;
+ * replicas may be NULL in ring mode). */
+mco_status mco_zb_step(mco_zb* z, void* replicas, const void* flat_grads, double lr,
+                       void* stream);
 
 /* ---- synthetic inputs ------------------------------------------ */
 /* Counter-based, stateless generator; values exact in fp32 (bf16 grid for BF16). */

@@ -120,6 +120,25 @@ _SIGS = {
     "mco_comm_allreduce_sum": (_i, [_p, _p, _i, _u64, _p]),
     "mco_shard_step": (_i, [_p, _p, _p, _i, _p, _i, _u64, _d, _p]),
     "mco_shard_step_mixed": (_i, [_p, _p, _p, _p, _p, _i, _u64, _d, _p]),
+    "mco_comm_create_timeout": (_i, [_p, _i, _i, _i, _d, C.POINTER(_p)]),
+    "mco_comm_wait": (_i, [_p, _p]),
+    "mco_comm_abort": (_i, [_p]),
+    "mco_zb_create": (_i, [_p, _p, _u64, _u64, _i, _i, C.POINTER(_p)]),
+    "mco_zb_destroy": (_i, [_p]),
+    "mco_zb_info": (_i, [_p, C.POINTER(_u64), C.POINTER(_i), C.POINTER(_u64), C.POINTER(_p),
+                         C.POINTER(_p)]),
+    "mco_zb_piece": (_i, [_p, _i, _i, C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64),
+                          C.POINTER(_u64), C.POINTER(_u64)]),
+    "mco_zb_load_master": (_i, [_p, _p, _i, _p]),
+    "mco_zb_begin": (_i, [_p, _p, _d, _p]),
+    "mco_zb_grad_buffer": (_i, [_p, _i, C.POINTER(_p), C.POINTER(_u64), _p]),
+    "mco_zb_grad_ready": (_i, [_p, _i, _p, _p]),
+    "mco_zb_end": (_i, [_p, _p]),
+    "mco_zb_step": (_i, [_p, _p, _p, _d, _p]),
+    "mco_zb_gathered": (_i, [_p, _i, C.POINTER(_p), _p]),
+    "mco_zb_step_local": (_i, [_p, _p, _p, _d, _p]),
+    "mco_zb_plan": (_i, [_u64, _i, _u64, _i, _i, C.POINTER(_u64), C.POINTER(_i),
+                         C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64), C.POINTER(_u64)]),
     "mco_flat_variant": (C.c_char_p, []),
 }
 for _name, (_res, _args) in _SIGS.items():

@@ -151,6 +151,26 @@ void check_dtypes(const mco_flat* h, int pdt, int gdt) {
 }
 }  // namespace
 
+}  // extern "C"
+
+namespace mco {
+// Sharders (shard.cpp): one piece of a step -- params [0, n) against the state slice at
+// state_off, at the handle's current step counter (the caller advanced it once for the
+// whole step, optim.cpp:104).
+void flat_step_range(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
+                     uint64_t n, uint64_t state_off, double lr, cudaStream_t st) {
+  if (state_off + n > h->n)
+    throw Error(MCO_CONTRACT, "optimizer step: piece [" + std::to_string(state_off) + ", " +
+                                  std::to_string(state_off + n) + ") exceeds the owned state of " +
+                                  std::to_string(h->n));
+  check_dtypes(h, pdt, gdt);
+  if (pout && h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
+  flat_launch(h, p, pdt, g, gdt, pout, n, state_off, lr, st);
+}
+}  // namespace mco
+
+extern "C" {
+
 // optim.cpp:100-112
 mco_status mco_flat_step(mco_flat* h, void* params, int pdt, uint64_t np, const void* grads,
                          int gdt, uint64_t ng, double lr, void* stream) {

@@ -118,6 +118,13 @@ void host_pipeline(int dev, void* a, size_t as, const void* b, size_t bs, uint64
 
 }  // namespace mco
 
+struct mco_flat;
+namespace mco {
+// abi_flat.cpp: one piece of a step at the handle's current t (sharders, shard.cpp).
+void flat_step_range(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t* pout,
+                     uint64_t n, uint64_t state_off, double lr, cudaStream_t st);
+}  // namespace mco
+
 // ---- handles ---------------------------------------------------------------------
 struct mco_flat {
   mco_config cfg{};

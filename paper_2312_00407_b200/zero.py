@@ -712,29 +712,52 @@ def reshard_state(states: list, total_len: int, new_world: int) -> list:
 class NcclComm:
     """The C-ABI's own NCCL communicator (mco_comm): ncclUniqueId from rank 0, shipped
     over the torch.distributed group (any backend), ncclCommInitRank on every rank.
-    Lets the sharded step run as one stream-ordered C call (mco_shard_step)."""
+    Lets the sharded step run as one stream-ordered C call (mco_shard_step).
 
-    def __init__(self, group=None, device: Optional[int] = None):
+    timeout_s: the communicator's deadline (mco_comm_create_timeout; None = the
+    library default, $MCO_NCCL_TIMEOUT_S or 600 s).  world / rank / unique_id: build it
+    without a process group (the id must then be shared by the caller)."""
+
+    def __init__(self, group=None, device: Optional[int] = None,
+                 timeout_s: Optional[float] = None, world: Optional[int] = None,
+                 rank: Optional[int] = None, unique_id: Optional[bytes] = None):
         import ctypes as C
 
         from ._lib import lib
 
         dist = _dist()
-        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
-        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        explicit = world is not None
+        self.world = world if explicit else (
+            dist.get_world_size(group) if dist.is_initialized() else 1)
+        self.rank = rank if explicit else (dist.get_rank(group) if dist.is_initialized() else 0)
         uid = (C.c_char * 128)()
-        if self.rank == 0:
+        if unique_id is not None:
+            C.memmove(uid, unique_id, 128)
+        elif self.rank == 0:
             optim._check(lib.mco_comm_unique_id(uid))
-        if self.world > 1:
+        if self.world > 1 and not explicit:
             box = [bytes(uid)]
             src = dist.get_global_rank(group, 0) if group is not None else 0
             dist.broadcast_object_list(box, src=src, group=group)
             C.memmove(uid, box[0], 128)
         h = C.c_void_p()
         self._destroy = lib.mco_comm_destroy
-        optim._check(lib.mco_comm_create(uid, self.world, self.rank, optim._device(device),
-                                         C.byref(h)))
+        self.device = optim._device(device)
+        optim._check(lib.mco_comm_create_timeout(uid, self.world, self.rank, self.device,
+                                                 float(timeout_s or 0.0), C.byref(h)))
         self._h = h
+
+    def wait(self, stream=None) -> None:
+        """Host wait for the stream's collectives, bounded by the communicator's deadline
+        (ProtocolError naming this rank, communicator aborted, on expiry)."""
+        from ._lib import lib
+
+        optim._check(lib.mco_comm_wait(self._h, optim._stream(stream)))
+
+    def abort(self) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_comm_abort(self._h))
 
     def allreduce_sum(self, t, stream=None) -> None:
         from ._lib import lib
@@ -809,3 +832,212 @@ class NativeZeroOptimizer:
 
     def owned_range(self) -> tuple[int, int]:
         return self.lo, self.hi
+
+
+class BucketedZeroOptimizer:
+    """Bucketed, double-buffered stage-2 ZeRO step over the C-ABI's
+    NCCL communicator (mco_zb_*): per bucket of the registry-order flat vector,
+    reduce-scatter(SUM) of the bucket's local gradient on the library's comm stream ->
+    the fused update of this rank's piece (ZeroPlan within the bucket) -> all-gather of
+    the bucket's replicas, issued after the next bucket's reduce-scatter so that
+    reduce-scatter overlaps this update (parallel.cpp:656-666, bucketed).
+
+    `step(replicas, flat_grads, lr)`: the whole step from a full local gradient.
+    Streaming form (no full-length gradient resident): `begin(replicas, lr)`, then per
+    bucket `grad_buffer(k)` (a staging slot, double-buffered) -> fill -> `grad_ready(k)`,
+    then `end()`.  replica dtype fp32 (the replicas are the parameters) or bf16 (fp32
+    master of the owned pieces, `load_master`)."""
+
+    def __init__(self, cfg: optim.OptimizerConfig, total_len: int, comm: "NcclComm",
+                 bucket_elems: int = 0, grad_dtype=None, replica_dtype=None):
+        import ctypes as C
+
+        import torch
+
+        from ._lib import lib
+
+        self.comm, self.cfg = comm, cfg
+        self.total_len = int(total_len)
+        gd = optim.MCO_BF16 if grad_dtype == torch.bfloat16 else optim.MCO_F32
+        rd = optim.MCO_BF16 if replica_dtype == torch.bfloat16 else optim.MCO_F32
+        self.gdt, self.rdt = gd, rd
+        h = C.c_void_p()
+        self._destroy = lib.mco_zb_destroy
+        optim._check(lib.mco_zb_create(C.byref(cfg._to_c()), comm._h, self.total_len,
+                                       int(bucket_elems), gd, rd, C.byref(h)))
+        self._h = h
+        B, nb, own, fl, ms = C.c_uint64(), C.c_int(), C.c_uint64(), C.c_void_p(), C.c_void_p()
+        optim._check(lib.mco_zb_info(h, C.byref(B), C.byref(nb), C.byref(own), C.byref(fl),
+                                     C.byref(ms)))
+        self.bucket_elems, self.nbuckets, self.owned = B.value, nb.value, own.value
+        self._master_ptr = ms.value
+        self._fl = C.c_void_p(fl.value)  # the state handle (owned by the mco_zb)
+        self.device = comm_device(comm)
+
+    def _flat(self):
+        return self._fl
+
+    def pieces(self, rank: Optional[int] = None):
+        """[(registry offset, n, state offset)] of `rank`'s pieces in bucket order."""
+        import ctypes as C
+
+        from ._lib import lib
+
+        rank = self.comm.rank if rank is None else rank
+        out = []
+        for k in range(self.nbuckets):
+            bo, bl, o, n, so = (C.c_uint64() for _ in range(5))
+            optim._check(lib.mco_zb_piece(self._h, k, rank, C.byref(bo), C.byref(bl),
+                                          C.byref(o), C.byref(n), C.byref(so)))
+            out.append((bo.value + o.value, n.value,
+                        so.value if rank == self.comm.rank else None))
+        return out
+
+    def master(self):
+        if not self._master_ptr:
+            return None
+        return optim._as_tensor(self._master_ptr, self.owned, optim.MCO_F32, self,
+                                self.device)
+
+    def load_master(self, full, stream=None) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_zb_load_master(self._h, full.data_ptr(), optim._dtype_code(full),
+                                            optim._stream(stream)))
+
+    def step(self, replicas, flat_grads, lr: float, stream=None) -> None:
+        from ._lib import lib
+
+        optim._dev(replicas, "zb replicas")
+        optim._dev(flat_grads, "zb grads")
+        if replicas.numel() != self.total_len or flat_grads.numel() != self.total_len:
+            raise optim.ContractError(
+                f"bucketed shard step: flat buffers of {replicas.numel()} / "
+                f"{flat_grads.numel()} elements for a plan of {self.total_len}")
+        if optim._dtype_code(replicas) != self.rdt or optim._dtype_code(flat_grads) != self.gdt:
+            raise optim.ContractError("bucketed shard step: dtype differs from the plan")
+        optim._check(lib.mco_zb_step(self._h, replicas.data_ptr(), flat_grads.data_ptr(),
+                                     float(lr), optim._stream(stream)))
+
+    def step_local(self, replicas, flat_grads, lr: float, stream=None) -> None:
+        """The same update kernels without the collectives (shard-local cost)."""
+        from ._lib import lib
+
+        optim._check(lib.mco_zb_step_local(self._h, replicas.data_ptr(), flat_grads.data_ptr(),
+                                           float(lr), optim._stream(stream)))
+
+    def begin(self, replicas, lr: float, stream=None) -> None:
+        """replicas=None: ring mode (bf16 replicas only) -- no full replica is resident,
+        bucket k is gathered into a two-slot ring (`gathered(k)`)."""
+        from ._lib import lib
+
+        if replicas is not None:
+            optim._dev(replicas, "zb replicas")
+        optim._check(lib.mco_zb_begin(self._h, replicas.data_ptr() if replicas is not None
+                                      else None, float(lr), optim._stream(stream)))
+
+    def gathered(self, k: int, stream=None):
+        """Ring mode: bucket k's gathered bf16 parameters (valid until bucket k+2's
+        update); the stream waits for its all-gather."""
+        import ctypes as C
+
+        import torch
+
+        from ._lib import lib
+
+        ptr = C.c_void_p()
+        optim._check(lib.mco_zb_gathered(self._h, int(k), C.byref(ptr), optim._stream(stream)))
+        n = min(self.bucket_elems, self.total_len - k * self.bucket_elems)
+        raw = torch.as_tensor(_U16View(ptr.value, n, self), device=f"cuda:{self.device}")
+        return raw.view(torch.bfloat16)
+
+    @staticmethod
+    def footprint(kind: int, total_len: int, world: int, bucket_elems: int,
+                  replica_dtype_bytes: int = 4, ring: bool = False,
+                  grad_dtype_bytes: int = 4) -> dict:
+        """Device bytes one rank holds for the bucketed step (the largest rank): fp32
+        state of its pieces (kinds' slot counts, optim.cpp:74-98), the fp32 master
+        (bf16 replicas), the replicas (or the two ring slots), two gradient staging
+        buckets and two reduced pieces."""
+        slots = {0: 2, 1: 1, 2: 4, 3: 2}[int(kind)]
+        unit = 8 * world
+        B = min(bucket_elems or total_len, total_len)
+        B = (B + unit - 1) // unit * unit
+        nb = (total_len + B - 1) // B
+        own = 0
+        for k in range(nb):
+            L = min(total_len, (k + 1) * B) - k * B
+            own += L // world + (1 if L % world else 0)
+        out = {"state": slots * own * 4,
+               "master": own * 4 if replica_dtype_bytes < 4 else 0,
+               "replicas": (2 * B if ring else total_len) * replica_dtype_bytes,
+               "staging": 2 * B * grad_dtype_bytes,
+               "reduced": 2 * (B // world + 8) * grad_dtype_bytes,
+               "owned": own, "bucket_elems": B}
+        out["total"] = sum(v for k, v in out.items() if k not in ("owned", "bucket_elems"))
+        return out
+
+    def grad_buffer(self, k: int, stream=None):
+        import ctypes as C
+
+        import torch
+
+        from ._lib import lib
+
+        ptr, n = C.c_void_p(), C.c_uint64()
+        optim._check(lib.mco_zb_grad_buffer(self._h, int(k), C.byref(ptr), C.byref(n),
+                                            optim._stream(stream)))
+        if self.gdt == optim.MCO_F32:
+            return optim._as_tensor(ptr.value, n.value, optim.MCO_F32, self, self.device)
+        raw = torch.as_tensor(_U16View(ptr.value, n.value, self),
+                              device=f"cuda:{self.device}")
+        return raw.view(torch.bfloat16)
+
+    def grad_ready(self, k: int, grad=None, stream=None) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_zb_grad_ready(self._h, int(k),
+                                           grad.data_ptr() if grad is not None else None,
+                                           optim._stream(stream)))
+
+    def end(self, stream=None) -> None:
+        from ._lib import lib
+
+        optim._check(lib.mco_zb_end(self._h, optim._stream(stream)))
+
+    def steps_taken(self) -> int:
+        import ctypes as C
+
+        from ._lib import lib
+
+        t = C.c_int64()
+        optim._check(lib.mco_flat_get_steps(self._flat(), C.byref(t)))
+        return t.value
+
+    def buffers(self):
+        """[(name, device view over this rank's pieces, bucket order)]."""
+        import ctypes as C
+
+        from ._lib import lib
+
+        nb = C.c_int()
+        optim._check(lib.mco_flat_num_buffers(self._flat(), C.byref(nb)))
+        out = []
+        for i in range(nb.value):
+            name, ptr, ln, dt = C.c_char_p(), C.c_void_p(), C.c_uint64(), C.c_int()
+            optim._check(lib.mco_flat_buffer(self._flat(), i, C.byref(name), C.byref(ptr),
+                                             C.byref(ln), C.byref(dt)))
+            out.append((name.value.decode(),
+                        optim._as_tensor(ptr.value, ln.value, dt.value, self, self.device)))
+        return out
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            self._destroy(h)
+            self._h = None
+
+
+def comm_device(comm) -> int:
+    dev = getattr(comm, "device", None)
+    return dev if dev is not None else optim._device(None)

@@ -35,9 +35,11 @@ def test_bench_two_ranks_one_line():
         assert e["nvlink"]["bytes_per_rank_per_direction"] >= P * 4, k  # RS + AG, fp32
         # value = 6 P / sum of the whole-step times
     total = sum(e["ms"] for e in d["per_optimizer"].values())
-    assert abs(d["value"] - 6 * P / (total * 1e-3)) / d["value"] < 1e-9
+    assert abs(d["value"] - 6 * P / (total * 1e-3)) / d["value"] < 1e-5  # ms are rounded to 4 decimals
     assert d["gpu_launches"] > 0 and d["collectives"]["backend"] == "gloo"
     # e2e over both ranks' host-span calls (max-over-ranks time, whole-job bytes)
     e = d["e2e"]
     assert e["value"] > 0 and set(e["per_optimizer"]) == kinds
-    assert e["h2d_bytes_per_step"] == 6 * 2 * 4 * e["params"] == 2 * e["d2h_bytes_per_step"]
+    # 8 B/param up (p, g) per optimizer, LOMO's clip pass streams g once more; 4 B down
+    assert e["h2d_bytes_per_step"] == (6 * 8 + 4) * e["params"]
+    assert e["d2h_bytes_per_step"] == 6 * 4 * e["params"]
