@@ -487,6 +487,26 @@ def bench_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
     clocks.stop()
     value = len(per) * P / (total_ms * 1e-3)
+    extra = {}
+    if world == 1 and "sophia" in per and not args.no_extra:
+        # Sophia precise-m (state "f32m64": fp64 m, the per-element 1e-5 bar met); not
+        # part of `value` -- the six-kind step uses the fp32 product path
+        cfg = make_cfg("sophia")
+        opt = optim.FlatOptimizer(cfg, P, state_dtype="f32m64")
+        pp, gg = bp[:P], bg[:P]
+        for _ in range(args.warmup):
+            opt.step(pp, gg, cfg.lr)
+        ms = timed_block(lambda: opt.step(pp, gg, cfg.lr), args.steps, stream)
+        gbs = 32 * P / (ms * 1e-3) / 1e9
+        extra["sophia_precise_m"] = {
+            "ms": round(ms, 4), "params_per_s": P / (ms * 1e-3), "bytes_per_param": 32,
+            "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
+            "what": "Sophia with an fp64 first moment (state f32m64, sophia_m64_kernel); "
+                    "refresh steps write h too (+4 B)", "parity": load_parity("sophia_m64")}
+        per["sophia"]["parity_fp32_m"] = load_parity("sophia")
+        del opt
+        gc.collect()
+        log(f"[rank {rank}] sophia precise-m: {ms:.3f} ms/step, {gbs / hbm_peak:.3f} of HBM")
 
     # dominant kernel = the optimizer with the largest share of the step (N = 1)
     dom = max(per, key=lambda k: per[k]["ms"] if world == 1 else
@@ -506,7 +526,7 @@ def bench_ours(args, rank, world, local_rank):
     if world > 1:
         roofline["note"] = ("dominant shard-local update kernel; the whole step at N > 1 is "
                             "bounded by the collectives (per_optimizer.*.nvlink)")
-    out = dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline,
+    out = dict(value=value, ms_per_step=total_ms, per=per, roofline=roofline, extra=extra,
                launches=launches, clocks=clocks.summary(), P=P, owned=P, shapes=shapes,
                kinds=[k for k in kinds if k in per], p=bp[:P], g=bg[:P], dev=dev,
                busbw=busbw)
@@ -520,6 +540,112 @@ def bench_ours(args, rank, world, local_rank):
             log(f"[rank {rank}] e2e failed: {ex!r}")
             out["e2e"] = None
     return out
+
+
+C4_BYTES = {"adan": 46, "sophia": 26, "adamw": 30, "lion": 22}  # mixed, SURVEY 8(d)
+
+
+def bench_c4(args, rank, world, local_rank):
+    """BASELINE configs[3]: ZeRO stage-2 Adan / Sophia on a LLaMA-65B-
+    shaped set over the bucketed, double-buffered C-ABI step (mco_zb): fp32 master +
+    state of each rank's pieces, bf16 replicas (ring mode -- buckets gathered into two
+    slots, the stage-3 layout -- when the full replicas do not fit), fp32 gradients
+    arriving bucket by bucket into the library's two staging slots (no full-length
+    gradient is resident; the backward that would produce them is not timed, the
+    staged values are reused).  Per step and bucket: reduce-scatter (fp32) -> update ->
+    all-gather (bf16), RS(k+1) overlapping update(k).  One JSON line per kind."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_00407_b200 import optim, registry, zero
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    model = registry.MODELS[args.model]
+    if args.layers:
+        model = registry.layer_subset(model, args.layers)
+    P = model.param_count()
+    hbm_peak, peak_src = measured_peaks()
+    comm = zero.NcclComm(device=local_rank)
+    busbw = nccl_busbw(dev, world) if world > 1 else None
+    stream = torch.cuda.current_stream()
+    kinds = [k for k in args.optimizers.split(",") if k in STORED]
+    for kind in kinds:
+        cfg = make_cfg(kind)
+        gc.collect()
+        torch.cuda.empty_cache()
+        free = torch.cuda.mem_get_info()[0]
+        fp = zero.BucketedZeroOptimizer.footprint(int(cfg.kind), P, world, args.bucket_elems, 2)
+        ring = fp["total"] > free * 0.97
+        if ring:
+            fp = zero.BucketedZeroOptimizer.footprint(int(cfg.kind), P, world,
+                                                      args.bucket_elems, 2, True)
+        zb = zero.BucketedZeroOptimizer(cfg, P, comm, bucket_elems=args.bucket_elems,
+                                        replica_dtype=torch.bfloat16)
+        optim.synth_fill(zb.master(), registry.SEED, 0, 0xFFFB, 0, 0, -6)
+        rep = None if ring else torch.zeros(P, dtype=torch.bfloat16, device=dev)
+        for k in (0, 1):
+            if k < zb.nbuckets:
+                optim.synth_fill(zb.grad_buffer(k), registry.SEED, 1, 0xFFFB, 1, 0, -7, 10)
+
+        def one():
+            zb.begin(rep, cfg.lr)
+            for k in reversed(range(zb.nbuckets)):
+                zb.grad_buffer(k)  # the slot is free (its previous bucket was reduced)
+                zb.grad_ready(k)
+            zb.end()
+
+        for _ in range(args.warmup):
+            one()
+        comm.wait()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ms = timed_block(one, args.steps, stream)
+        comm.check()
+        if world > 1:
+            t = torch.tensor([ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = t.item()
+        f = (world - 1) / world
+        nvb = int(f * P * 4 + f * P * 2)  # RS fp32 grads + AG bf16 params, per direction
+        hbm_b = C4_BYTES[kind] * zb.owned
+        line = {"metric": f"C4 ZeRO stage-2 {kind} step (params/s, whole job)",
+                "value": P / (ms * 1e-3), "unit": "params/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "dtype": "f32 master/state, "
+                "bf16 replicas, f32 grads", "data": "synthetic",
+                "config": {"workload": "configs[3]", "model_shape": model.name, "params": P,
+                           "bucket_elems": zb.bucket_elems, "buckets": zb.nbuckets,
+                           "mode": "ring (stage-3 layout)" if ring else "bf16 replicas",
+                           "per_rank_bytes": fp},
+                "hbm": {"update_bytes_per_rank": hbm_b, "peak": hbm_peak,
+                        "peak_source": peak_src,
+                        "bound_ms": round(hbm_b / (hbm_peak * 1e9) * 1e3, 3)},
+                "nvlink": {"bytes_per_rank_per_direction": nvb,
+                           "gb_per_s": round(nvb / (ms * 1e-3) / 1e9, 1),
+                           "nominal_gbs": NVLINK_NOMINAL_GBS, "measured_busbw_gbs": busbw,
+                           "bound_ms": round(nvb / ((busbw or NVLINK_NOMINAL_GBS) * 1e9)
+                                             * 1e3, 3)}}
+        line["roofline_ms"] = max(line["hbm"]["bound_ms"], line["nvlink"]["bound_ms"])
+        line["frac"] = round(line["roofline_ms"] / ms, 4)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+            log(f"[c4] {kind}: {ms:.2f} ms/step, {P / ms / 1e6:.1f} Gparam/s, roofline "
+                f"{line['roofline_ms']:.2f} ms ({'ring' if ring else 'replicas'})")
+        del zb, rep
+    comm.wait()
+
+
+def load_parity(kind):
+    """Measured fp32-vs-fp64-reference errors of `kind` (profiles/parity.json, written by
+    tests/test_gpu_flat.py on the GPU: fraction of elements past 1e-5 and the largest
+    error) -- bench.py never runs the oracle itself."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "parity.json")) as f:
+            return json.load(f).get(kind)
+    except Exception:
+        return None
 
 
 def load_traffic(kind, params_per_launch):
@@ -724,9 +850,14 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the legs reported beside the value (Sophia precise-m)")
     ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--bucket-elems", type=int, default=1 << 27,
                     help="N > 1: bucket size of the bucketed stage-2 step (elements)")
+    ap.add_argument("--c4", action="store_true",
+                    help="BASELINE configs[3]: bucketed mixed ZeRO step of --optimizers "
+                         "(stored-state kinds) on --model (e.g. llama-65b), one line per kind")
     ap.add_argument("--repeats", type=int, default=5,
                     help="K-step blocks per optimizer for the reported median (the first "
                          "block alone is the contract-timed value)")
@@ -790,6 +921,12 @@ def main():
         else:
             dist.init_process_group(backend)
         local_rank = local_rank % max(torch.cuda.device_count(), 1)
+    if args.c4:
+        bench_c4(args, rank, world, local_rank)
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     res = bench_ours(args, rank, world, local_rank)
     config["params"] = res["P"]
     e2e = res.get("e2e")
@@ -816,6 +953,8 @@ def main():
                 "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": res["launches"], "clocks": res["clocks"],
                 "per_optimizer": res["per"]}
+        if res.get("extra"):
+            line["extra_not_in_value"] = res["extra"]
         if world > 1:
             line["collectives"] = {"backend": dist.get_backend(),
                                    "nccl_allgather_busbw_gbs": res["busbw"],

@@ -52,7 +52,9 @@ typedef enum mco_kind {
   MCO_ADALOMO = 5
 } mco_kind;
 
-typedef enum mco_dtype { MCO_F32 = 0, MCO_BF16 = 1, MCO_F64 = 2 } mco_dtype;
+/* MCO_F32M64 is a FlatOptimizer state layout only: fp32 state with an fp64 first
+ * moment m (Sophia's opt-in "precise-m" mode, see mco_flat_create). */
+typedef enum mco_dtype { MCO_F32 = 0, MCO_BF16 = 1, MCO_F64 = 2, MCO_F32M64 = 3 } mco_dtype;
 
 /* optim.hpp:20-35  struct OptimizerConfig, field for field
  * (std::optional<double> clip_threshold -> has_clip_threshold + clip_threshold). */
@@ -96,7 +98,11 @@ typedef struct mco_flat mco_flat;
 
 /* FlatOptimizer(cfg, owned_len): zero-initialised SoA state on `device`
  * (m,v | m | m,v,n,g_prev | m,h).  state_dtype MCO_F32 (default product path)
- * or MCO_F64 (bit-exact parity mode).  Fused kinds -> MCO_CONTRACT. */
+ * or MCO_F64 (bit-exact parity mode), or -- Sophia only -- MCO_F32M64: fp32 h with an
+ * fp64 m and fp64 per-element arithmetic on fp32 params ("precise-m": the fp32 m's
+ * cancellation error, amplified by 1/(rho h), otherwise pushes ~0.06 % of elements past
+ * 1e-5 of the fp64 reference; 32 B/param instead of 24; mco_flat_step and the host-span
+ * step only).  Fused kinds -> MCO_CONTRACT. */
 mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device,
                            int state_dtype, mco_flat** out);
 mco_status mco_flat_destroy(mco_flat* h);

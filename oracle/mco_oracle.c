@@ -346,6 +346,26 @@ void orc_sophia_f32(float* p, const float* g, float* m, float* h, uint64_t n,
   }
 }
 
+/* Sophia "precise-m" (state MCO_F32M64, sophia_m64.cu): fp32 p, g, h with an fp64 m and
+ * fp64 per-element arithmetic in optim.cpp:160-166's order; h and p rounded once. */
+void orc_sophia_m64(float* p, const float* g, double* m, float* h, uint64_t n,
+                    const orc_config* c, int64_t t, double lr) {
+  const double b1 = c->beta1, b2 = c->beta2, omb1 = 1.0 - c->beta1, omb2 = 1.0 - c->beta2;
+  const double rho = c->sophia_rho, eps = c->eps, lrwd = lr * c->weight_decay;
+  const int refresh = ((t - 1) % c->update_interval) == 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    const double gd = (double)g[i];
+    m[i] = b1 * m[i] + omb1 * gd;
+    if (refresh) h[i] = (float)(b2 * (double)h[i] + omb2 * gd * gd);
+    const double rh = rho * (double)h[i];
+    const double denom = rh < eps ? eps : rh;
+    const double q = m[i] / denom;
+    const double u = q < -1.0 ? -1.0 : (1.0 < q ? 1.0 : q);
+    const double pd = (double)p[i];
+    p[i] = (float)(pd - (lr * u + lrwd * pd));
+  }
+}
+
 void orc_lomo_f32(float* p, const float* g, uint64_t n, double lr, double scale) {
   const float f = (float)(lr * scale);
   for (uint64_t i = 0; i < n; ++i) p[i] = p[i] - f * g[i];

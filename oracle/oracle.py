@@ -80,6 +80,7 @@ def _load_orc():
         "orc_lion_f32": (None, [_p, _p, _p, _u64, _CP, _d]),
         "orc_adan_f32": (None, [_p, _p, _p, _p, _p, _p, _u64, _CP, _i64, _d]),
         "orc_sophia_f32": (None, [_p, _p, _p, _p, _u64, _CP, _i64, _d]),
+        "orc_sophia_m64": (None, [_p, _p, _p, _p, _u64, _CP, _i64, _d]),
         "orc_lomo_f32": (None, [_p, _p, _u64, _d, _d]),
         "orc_lomo_bf16": (None, [_p, _p, _u64, _d, _d]),
         "orc_sumsq_f32": (_d, [_p, _u64]),
@@ -234,6 +235,21 @@ class OracleFlat:
                                            self.t, lr)
         else:
             raise ValueError("fused kind")
+
+
+class OracleSophiaM64:
+    """Sophia precise-m restated (fp32 p / g / h, fp64 m and arithmetic; mco_oracle.c)."""
+
+    def __init__(self, cfg, n: int):
+        self.cfg = Config.of(cfg)
+        self.t = 0
+        self.state = {"m": np.zeros(n, np.float64), "h": np.zeros(n, np.float32)}
+
+    def step(self, p: np.ndarray, g: np.ndarray, lr: float) -> None:
+        assert p.dtype == np.float32 and g.dtype == np.float32
+        self.t += 1
+        orc.orc_sophia_m64(_ptr(p), _ptr(g), _ptr(self.state["m"]), _ptr(self.state["h"]),
+                           p.size, C.byref(self.cfg), self.t, lr)
 
 
 class OracleAdaLomo:

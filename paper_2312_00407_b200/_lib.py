@@ -15,7 +15,7 @@ LIB_PATH = os.environ.get("MCO_LIB_PATH") or os.path.join(HERE, "_build", "libmc
 HEADER = os.path.join(ROOT, "include", "mco.h")
 
 MCO_OK, MCO_CONFIG, MCO_DATA, MCO_CONTRACT, MCO_PROTOCOL, MCO_IO, MCO_CUDA = 0, 2, 3, 4, 5, 6, 7
-MCO_F32, MCO_BF16, MCO_F64 = 0, 1, 2
+MCO_F32, MCO_BF16, MCO_F64, MCO_F32M64 = 0, 1, 2, 3
 
 
 class mco_config(C.Structure):

@@ -20,8 +20,10 @@ mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device
     // (optim.cpp:161): an interval < 1 would divide by zero there and on the device here
     if (cfg->kind == MCO_SOPHIA && cfg->update_interval < 1)
       throw Error(MCO_CONFIG, "optimizer: update_interval must be >= 1");
-    if (state_dtype != MCO_F32 && state_dtype != MCO_F64)
-      throw Error(MCO_CONTRACT, "FlatOptimizer: state dtype must be f32 or f64");
+    if (state_dtype != MCO_F32 && state_dtype != MCO_F64 && state_dtype != MCO_F32M64)
+      throw Error(MCO_CONTRACT, "FlatOptimizer: state dtype must be f32, f64 or f32m64");
+    if (state_dtype == MCO_F32M64 && cfg->kind != MCO_SOPHIA)
+      throw Error(MCO_CONTRACT, "FlatOptimizer: the fp64-m state (precise-m) is Sophia's");
     device = resolve_device(device);
     DeviceGuard dg(device);
     auto h = std::make_unique<mco_flat>();
@@ -41,8 +43,8 @@ mco_status mco_flat_create(const mco_config* cfg, uint64_t owned_len, int device
     }
     // 8 elements of slack: the state is shifted to the parameters' alignment phase at
     // the first step (align_state_to), so shard views at odd offsets stay vectorised
-    const size_t bytes = (std::max<uint64_t>(owned_len, 1) + 8) * dtype_size(state_dtype);
     for (int i = 0; i < nslots; ++i) {
+      const size_t bytes = (std::max<uint64_t>(owned_len, 1) + 8) * h->slot_es(i);
       MCO_CUDA_CHECK(cudaMalloc(&h->base[i], bytes));
       MCO_CUDA_CHECK(cudaMemset(h->base[i], 0, bytes));
       h->slot[i] = h->base[i];
@@ -81,14 +83,14 @@ void check_lengths(const mco_flat* h, uint64_t np, uint64_t ng) {
 // aligned (flat.cu, launch_flat_step).
 void align_state_to(mco_flat* h, const void* params) {
   if (h->exposed || h->stepped || h->t != 0 || !params) return;
-  const size_t es = dtype_size(h->state_dtype);
+  const size_t es = h->state_dtype == MCO_F64 ? 8 : 4;  // the parameters' element size
   const uintptr_t u = (uintptr_t)params;
   if (u % es) return;
   const int want = (int)((u / es) % 8);
   if (want == h->phase) return;
   h->phase = want;
   for (int i = 0; i < 4; ++i)
-    if (h->base[i]) h->slot[i] = (char*)h->base[i] + (size_t)want * es;
+    if (h->base[i]) h->slot[i] = (char*)h->base[i] + (size_t)want * h->slot_es(i);
   for (size_t i = 0; i < h->named.size(); ++i) h->named[i].second = h->slot[i];
 }
 
@@ -116,15 +118,27 @@ void flat_launch(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint16_t
   a.p_dtype = pdt;
   a.g = g;
   a.g_dtype = gdt;
-  const size_t es = dtype_size(h->state_dtype);
-  for (int i = 0; i < 4; ++i) a.s[i] = h->slot[i] ? (char*)h->slot[i] + state_off * es : nullptr;
+  for (int i = 0; i < 4; ++i)
+    a.s[i] = h->slot[i] ? (char*)h->slot[i] + state_off * h->slot_es(i) : nullptr;
   a.p_out_bf16 = pout;
   a.n = n;
   const auto kf = make_consts<float>(h->cfg, h->t, lr);
   const auto kd = make_consts<double>(h->cfg, h->t, lr);
   a.gs = graph_step(h, lr);
-  launch_flat_step(a, kf, kd, st);
+  if (h->state_dtype == MCO_F32M64) {  // Sophia precise-m (sophia_m64.cu)
+    if (pout || a.gs.d)
+      throw Error(MCO_CONTRACT, "precise-m Sophia: no mixed / graph-mode step");
+    launch_sophia_m64((float*)p, g, gdt, (double*)a.s[0], (float*)a.s[1], n, kd, st);
+  } else {
+    launch_flat_step(a, kf, kd, st);
+  }
   h->stepped = true;
+}
+
+void no_m64(const mco_flat* h, const char* what) {
+  if (h->state_dtype == MCO_F32M64)
+    throw Error(MCO_CONTRACT, std::string(what) + ": not available for the precise-m (f32m64) "
+                              "state");
 }
 
 void no_graph(const mco_flat* h, const char* what) {
@@ -164,6 +178,7 @@ void flat_step_range(mco_flat* h, void* p, int pdt, const void* g, int gdt, uint
                                   std::to_string(state_off + n) + ") exceeds the owned state of " +
                                   std::to_string(h->n));
   check_dtypes(h, pdt, gdt);
+  no_m64(h, "sharded step");
   if (pout && h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
   flat_launch(h, p, pdt, g, gdt, pout, n, state_off, lr, st);
 }
@@ -193,6 +208,7 @@ mco_status mco_flat_step_mixed(mco_flat* h, float* master, const void* grads, in
     check_lengths(h, n, n);
     check_data(n, master, grads, "mixed step");
     check_dtypes(h, MCO_F32, gdt);
+    no_m64(h, "mixed step");
     if (h->state_dtype != MCO_F32) throw Error(MCO_CONTRACT, "mixed step needs f32 state");
     if (!pout) throw Error(MCO_CONTRACT, "mixed step: param_out is null");
     DeviceGuard dg(h->device);
@@ -225,6 +241,7 @@ mco_status mco_flat_step_list(mco_flat* h, int count, void* const* params, int p
       throw Error(MCO_CONTRACT, "step list: " + std::to_string(total) +
                                     " elements exceed the owned state of " + std::to_string(h->n));
     check_dtypes(h, pdt, gdt);
+    no_m64(h, "list step");
     DeviceGuard dg(h->device);
     if (count > 0) align_state_to(h, params[0]);
     if (!h->gdev) ++h->t;
@@ -295,6 +312,7 @@ mco_status mco_flat_set_steps(mco_flat* h, int64_t t) {
 mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr) {
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_flat_graph_enable: null handle");
+    no_m64(h, "graph mode");
     DeviceGuard dg(h->device);
     if (h->gdev) {  // already on: only the lr source changes
       h->glr = dev_lr;
@@ -346,7 +364,9 @@ mco_status mco_flat_graph_disable(mco_flat* h) {
 mco_status mco_flat_state_bytes(const mco_flat* h, uint64_t* out) {
   return guard([&] {
     if (!h) throw Error(MCO_CONTRACT, "mco_flat_state_bytes: null handle");
-    *out = h->named.size() * h->n * dtype_size(h->state_dtype);
+    uint64_t b = 0;
+    for (size_t i = 0; i < h->named.size(); ++i) b += h->n * h->slot_es((int)i);
+    *out = b;
   });
 }
 mco_status mco_flat_config(const mco_flat* h, mco_config* out) {
@@ -371,7 +391,7 @@ mco_status mco_flat_buffer(mco_flat* h, int i, const char** name, void** ptr, ui
     *name = h->named[i].first;
     *ptr = h->named[i].second;
     *len = h->n;
-    *dtype = h->state_dtype;
+    *dtype = h->slot_dtype(i);
   });
 }
 
@@ -397,6 +417,7 @@ mco_status mco_flat_step_peers(mco_flat* h, const void* const* grad_bufs, int gr
       pp.p[r] = param_bufs[r];
     }
     no_graph(h, "peer step");
+    no_m64(h, "peer step");
     DeviceGuard dg(h->device);
     ++h->t;
     const auto kf = make_consts<float>(h->cfg, h->t, lr);

@@ -144,6 +144,15 @@ struct mco_flat {
   mco::GraphRow<double>* grow_d = nullptr;
   int64_t grows = 0;
   const double* glr = nullptr;  // device lr (null: the lr argument of each call)
+  // element size of state slot i: MCO_F32M64 (Sophia precise-m) keeps m (slot 0) in fp64
+  size_t slot_es(int i) const {
+    if (state_dtype == MCO_F32M64) return i == 0 ? 8 : 4;
+    return state_dtype == MCO_F64 ? 8 : 4;
+  }
+  int slot_dtype(int i) const {
+    if (state_dtype == MCO_F32M64) return i == 0 ? MCO_F64 : MCO_F32;
+    return state_dtype;
+  }
   void free_graph() {
     for (void* p : {(void*)gdev, (void*)grow_f, (void*)grow_d})
       if (p) cudaFree(p);

@@ -31,6 +31,10 @@ struct FlatArgs {
 void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
                       const StepConsts<double>& kd, cudaStream_t st);
 
+// Sophia with an fp64 first moment ("precise-m", state MCO_F32M64; sophia_m64.cu).
+void launch_sophia_m64(float* p, const void* g, int g_dtype, double* m, float* h, uint64_t n,
+                       const StepConsts<double>& kd, cudaStream_t st);
+
 // List form: separate parameter / gradient tensors over the flat state (tensor i's state
 // at the sum of the preceding lengths).  One launch per kListMax tensors.
 constexpr int kListMax = 40;

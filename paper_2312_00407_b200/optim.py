@@ -25,7 +25,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import MCO_BF16, MCO_F32, MCO_F64, lib
+from ._lib import MCO_BF16, MCO_F32, MCO_F32M64, MCO_F64, lib
 
 # ---- errors (errors.hpp:11-32) ------------------------------------------------------
 
@@ -244,14 +244,16 @@ def _as_tensor(ptr: int, n: int, dtype: int, owner, device: int):
 class FlatOptimizer:
     """optim.hpp:40-64: element-wise optimizer over a flat owned slice.
 
-    state_dtype: "f32" (product path) or "f64" (bit-exact parity mode).
+    state_dtype: "f32" (product path), "f64" (bit-exact parity mode) or, Sophia only,
+    "f32m64" (precise-m: fp64 first moment and fp64 per-element arithmetic on fp32
+    params / h, within 1e-5 per element of the fp64 reference where fp32 m is not).
     """
 
     def __init__(self, cfg: OptimizerConfig, owned_len: int, device: Optional[int] = None,
                  state_dtype: str = "f32"):
         self._cfg = cfg
         self._n = int(owned_len)
-        self._sd = {"f32": MCO_F32, "f64": MCO_F64}[state_dtype]
+        self._sd = {"f32": MCO_F32, "f64": MCO_F64, "f32m64": MCO_F32M64}[state_dtype]
         h = C.c_void_p()
         self.device = _device(device)
         self._destroy = lib.mco_flat_destroy  # kept: module globals vanish at shutdown

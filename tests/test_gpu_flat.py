@@ -109,22 +109,46 @@ def test_f64_mode_bit_exact_vs_compiled_reference(kind):
 
 
 @pytest.mark.skipif(O.ref is None, reason="oracle/_ref not built")
-@pytest.mark.parametrize("kind", FLAT)
+@pytest.mark.parametrize("kind", list(FLAT) + ["sophia_m64"])
 def test_f32_within_tolerance_of_reference(kind):
-    from test_oracle import fp32_vs_fp64_ok
+    """The product path vs the fp64 reference after 20 steps: p, Δp and every state
+    buffer within 1e-5 per element (tests/parity.py floors).  Sophia's fp32-m path is
+    held to its documented exceedance bound; its precise-m state ("f32m64") meets the
+    per-element bar and is bit-exact to its restatement."""
+    import parity
 
-    n, lr = 1 << 16, 1e-3
-    cfg = cfg_for(kind, weight_decay=0.01)
+    n, lr, steps = 1 << 16, 1e-3, 20
+    m64 = kind == "sophia_m64"
+    cfg = cfg_for(Kind.SOPHIA if m64 else kind, weight_decay=0.01)
     p64 = O.synth(n, 2024, 0, 1, 0, 0, -6, 0, False, np.float64)
     p0 = p64.copy()
-    tp = dev(p64.astype(np.float32))
-    opt, r = optim.FlatOptimizer(cfg, n), O.RefFlat(cfg, n)
-    for t in range(1, 21):
+    p32 = p64.astype(np.float32)
+    tp = dev(p32)
+    opt = optim.FlatOptimizer(cfg, n, state_dtype="f32m64" if m64 else "f32")
+    r = O.RefFlat(cfg, n)
+    o = O.OracleSophiaM64(cfg, n) if m64 else None
+    for t in range(1, steps + 1):
         g = O.synth(n, 2024, 1, 1, t, 0, -7, 10, False)
         opt.step(tp, dev(g), lr)
         r.step(p64, g.astype(np.float64), lr)
+        if o is not None:
+            o.step(p32, g, lr)
     torch.cuda.synchronize()
-    assert fp32_vs_fp64_ok(kind, tp.cpu().numpy(), p64, p0, lr)
+    got = tp.cpu().numpy()
+    state = {nm: t.cpu().numpy() for nm, t in opt.buffers()}
+    if m64:
+        assert bits_equal(got, p32)
+        assert bits_equal(state["m"], o.state["m"]) and bits_equal(state["h"], o.state["h"])
+        assert state["m"].dtype == np.float64
+    name = "sophia_m64" if m64 else Kind(kind).name.lower()
+    ex = parity.exceedance(got, p64, p0, lr)
+    ex.update(parity.flat_errors(got, p64, p0, lr, steps, state, r.buffers()))
+    ex["case"] = f"{n} elements, {steps} steps, lr {lr}, wd 0.01, vs the fp64 reference"
+    parity.record(name, ex)
+    if kind == Kind.SOPHIA:
+        assert ex["fraction"] <= 1e-3 and ex["max_abs_over_lr"] <= 0.02, ex
+        return
+    parity.assert_flat_within(got, p64, p0, lr, steps, state, r.buffers(), str(kind))
 
 
 @pytest.mark.parametrize("kind", FLAT)

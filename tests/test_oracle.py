@@ -290,26 +290,43 @@ def test_host_logic_matches_reference():
                                                   shapes)
 
 
-# ---- f32 restatement vs the f64 reference: the fp32 tolerance claim ------------------------
-
-def fp32_vs_fp64_ok(kind, got32, want64, p0, lr):
-    """The fp32 tolerance: per element
-    |got - want| <= 1e-5 * max(|want|, RMS(p0)).  Sophia's clamp(m / max(rho*h, eps))
-    amplifies the fp32 rounding of m by 1/(rho*h) (~1e7) in its unclamped band, so
-    for Sophia at most 0.1% of elements may exceed it, each by <= 0.02*lr."""
-    rms = float(np.sqrt(np.mean(np.asarray(p0, np.float64) ** 2)))
-    d = np.abs(got32.astype(np.float64) - want64)
-    err = d / np.maximum(np.abs(want64), rms)
-    if kind == Kind.SOPHIA:
-        return np.mean(err > 1e-5) <= 1e-3 and d.max() <= 0.02 * lr
-    return err.max() <= 1e-5
+# ---- f32 restatement vs the f64 reference: the fp32 tolerance claim (tests/parity.py) ----
 
 
 @needs_ref
-@pytest.mark.parametrize("kind", FLAT_KINDS)
+@pytest.mark.parametrize("kind", FLAT_KINDS + ["sophia_m64"])
 def test_f32_restatement_within_tolerance_of_reference(kind):
+    """p, Δp and every state buffer within 1e-5 of the fp64 reference per element
+    (tests/parity.py floors).  Sophia: the precise-m restatement (fp64 m); its fp32-m
+    path is the separate, documented claim below."""
+    import parity
+
+    if kind == Kind.SOPHIA:
+        pytest.skip("fp32-m Sophia: test_sophia_fp32_m_exceedance_is_bounded")
     n, steps, lr = 1 << 14, 20, 1e-3
-    cfg = cfg_for(kind, weight_decay=0.01)
+    m64 = kind == "sophia_m64"
+    cfg = cfg_for(Kind.SOPHIA if m64 else kind, weight_decay=0.01)
+    p64 = O.synth(n, 2024, 0, 1, 0, 0, -6, 0, False, np.float64)
+    p0, p32 = p64.copy(), p64.astype(np.float32)
+    r = O.RefFlat(cfg, n)
+    o = O.OracleSophiaM64(cfg, n) if m64 else O.OracleFlat(cfg, n, np.float32)
+    for t in range(1, steps + 1):
+        g32 = O.synth(n, 2024, 1, 1, t, 0, -7, 10, False, np.float32)
+        r.step(p64, g32.astype(np.float64), lr)
+        o.step(p32, g32, lr)
+    parity.assert_flat_within(p32, p64, p0, lr, steps, o.state, r.buffers(), str(kind))
+
+
+@needs_ref
+def test_sophia_fp32_m_exceedance_is_bounded():
+    """Sophia with fp32 m (the default product path): clamp(m / max(rho h, eps))
+    amplifies m's fp32 cancellation error by 1/(rho h) in the unclamped band, so a few
+    elements exceed the per-element bar -- measured 0.06 % of them, by <= 0.016 lr.  The
+    claim for this path is that bound; precise-m (state "f32m64") meets the bar."""
+    import parity
+
+    n, steps, lr = 1 << 16, 20, 1e-3
+    cfg = cfg_for(Kind.SOPHIA, weight_decay=0.01)
     p64 = O.synth(n, 2024, 0, 1, 0, 0, -6, 0, False, np.float64)
     p0, p32 = p64.copy(), p64.astype(np.float32)
     r, o = O.RefFlat(cfg, n), O.OracleFlat(cfg, n, np.float32)
@@ -317,7 +334,11 @@ def test_f32_restatement_within_tolerance_of_reference(kind):
         g32 = O.synth(n, 2024, 1, 1, t, 0, -7, 10, False, np.float32)
         r.step(p64, g32.astype(np.float64), lr)
         o.step(p32, g32, lr)
-    assert fp32_vs_fp64_ok(kind, p32, p64, p0, lr)
+    ex = parity.exceedance(p32, p64, p0, lr)
+    assert 0 < ex["fraction"] <= 1e-3 and ex["max_abs_over_lr"] <= 0.02, ex
+    # the state itself is within the bar: the drift is m / (rho h) amplification only
+    e = parity.flat_errors(p32, p64, p0, lr, steps, o.state, r.buffers())
+    assert e["m"] <= parity.TOL and e["h"] <= parity.TOL, e
 
 
 def test_synth_generator_exact_grid():
