@@ -10,8 +10,10 @@ for that quantity (measured margins in DESIGN.md section 4):
   state       floor = RMS(want) / 4 -- EMAs of sign-changing gradients (m, v of Adan)
               cancel, so near zero crossings only an absolute bar at the buffer's scale
               is attainable in fp32.
-  delta p     |Δgot - Δwant| <= 1e-5 max(|Δwant_i|, N lr), Δ = p_N - p_0 after N steps
-              (N lr bounds the total update with |u| <= 1; fp32 p keeps ~ulp(p) per step).
+  delta p     |Δgot - Δwant| <= 1e-5 max(|Δwant_i|, N lr, N 2^-24 |p0_i| / 1e-5),
+              Δ = p_N - p_0 after N steps: N lr bounds the total update (|u| <~ 1), and
+              fp32 storage rounds p by up to 2^-24 |p| per step, so an update smaller
+              than N 2^-24 |p0| / 1e-5 cannot be resolved to 1e-5 (norm weights = 1.0).
 """
 from __future__ import annotations
 
@@ -41,7 +43,8 @@ def state_err(got, want) -> np.ndarray:
 def dp_err(got, want, p0, lr, steps) -> np.ndarray:
     got, want, p0 = _f64(got), _f64(want), _f64(p0)
     dw = want - p0
-    return np.abs((got - p0) - dw) / np.maximum(np.abs(dw), steps * lr)
+    floor = np.maximum(steps * lr, steps * 2.0 ** -24 * np.abs(p0) / TOL)
+    return np.abs((got - p0) - dw) / np.maximum(np.abs(dw), floor)
 
 
 def flat_errors(got_p, want_p, p0, lr, steps, got_state=None, want_state=None) -> dict:
