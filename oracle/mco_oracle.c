@@ -308,21 +308,24 @@ void orc_adan_f32(float* p, const float* g, float* m, float* v, float* nb, float
   const float b1 = (float)c->beta1, b2 = (float)c->beta2, b3 = (float)c->beta3;
   const float omb1 = (float)(1.0 - c->beta1), omb2 = (float)(1.0 - c->beta2),
               omb3 = (float)(1.0 - c->beta3);
-  const float c1 = (float)(1.0 - pow(c->beta1, (double)t));
-  const float c2 = (float)(1.0 - pow(c->beta2, (double)t));
-  const float c3 = (float)(1.0 - pow(c->beta3, (double)t));
+  /* fp32 product form (update.cuh): the bias corrections 1 / (1 - beta^t) and the
+   * decay 1 / (1 + lr wd) are reciprocals rounded once and multiplied (the f64
+   * functions keep optim.cpp's divisions) */
+  const float rc1 = (float)(1.0 / (1.0 - pow(c->beta1, (double)t)));
+  const float rc2 = (float)(1.0 / (1.0 - pow(c->beta2, (double)t)));
+  const float rc3 = (float)(1.0 / (1.0 - pow(c->beta3, (double)t)));
   const float lrf = (float)lr, eps = (float)c->eps;
-  const float den = (float)(1.0 + lr * c->weight_decay);
+  const float rden = (float)(1.0 / (1.0 + lr * c->weight_decay));
   for (uint64_t i = 0; i < n; ++i) {
     const float gd = t == 1 ? 0.0f : g[i] - gp[i];
     m[i] = b1 * m[i] + omb1 * g[i];
     v[i] = b2 * v[i] + omb2 * gd;
     const float nu = g[i] + b2 * gd;
     nb[i] = b3 * nb[i] + omb3 * nu * nu;
-    const float mhat = m[i] / c1;
-    const float vhat = v[i] / c2;
-    const float nhat = nb[i] / c3;
-    p[i] = (p[i] - lrf * (mhat + b2 * vhat) / (sqrtf(nhat) + eps)) / den;
+    const float mhat = m[i] * rc1;
+    const float vhat = v[i] * rc2;
+    const float nhat = nb[i] * rc3;
+    p[i] = (p[i] - lrf * (mhat + b2 * vhat) / (sqrtf(nhat) + eps)) * rden;
     gp[i] = g[i];
   }
 }

@@ -324,8 +324,8 @@ mco_status mco_flat_graph_enable(mco_flat* h, const double* dev_lr) {
     for (int64_t t = 1;; ++t) {
       const auto f = make_consts<float>(h->cfg, t, 0.0);
       const auto d = make_consts<double>(h->cfg, t, 0.0);
-      rf.push_back({f.c1, f.c2, f.c3, f.sthr});
-      rd.push_back({d.c1, d.c2, d.c3, d.sthr});
+      rf.push_back({f.c1, f.c2, f.c3, f.sthr, f.rc1, f.rc2, f.rc3});
+      rd.push_back({d.c1, d.c2, d.c3, d.sthr, d.rc1, d.rc2, d.rc3});
       if (d.c1 == 1.0 && d.c2 == 1.0 && d.c3 == 1.0) break;  // 1 - beta^t is 1.0 from here on
       if (t + 1 >= kMaxRows)
         throw Error(MCO_CONFIG, "graph mode: betas too close to 1 (1 - beta^t still below "

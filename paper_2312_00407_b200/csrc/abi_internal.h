@@ -48,6 +48,23 @@ T sqrt_eps_threshold(T eps, T c) {
   }
 }
 
+// The multiply form sqrt(x * rc) + eps (fp32 Adan): x < thr guarantees RN(x * rc) <=
+// (ulp(eps)/4)^2, so RN(sqrt(.) + eps) == eps -- thr = (ulp(eps)/4)^2 / rc rounded down
+// with a 2^-20 margin.
+template <typename T>
+T sqrt_eps_threshold_mul(T eps, T rc) {
+  if constexpr (sizeof(T) == 4) {
+    if (!(eps > 0) || !std::isnormal(eps) || !(rc > 0)) return 0;
+    const double q = ((double)std::nextafter(eps, INFINITY) - (double)eps) / 4.0;
+    const double thr = q * q / (double)rc * (1.0 - std::ldexp(1.0, -20));
+    float f = (float)thr;
+    if ((double)f > thr) f = std::nextafter(f, 0.0f);
+    return f;
+  } else {
+    return 0;
+  }
+}
+
 template <typename T>
 StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
   StepConsts<T> k{};
@@ -66,7 +83,19 @@ StepConsts<T> make_consts(const mco_config& c, int64_t t, double lr) {
   k.lrwd = (T)(lr * c.weight_decay);
   k.den = (T)(1.0 + lr * c.weight_decay);
   k.rho = (T)c.sophia_rho;
-  k.sthr = sqrt_eps_threshold<T>(k.eps, c.kind == MCO_ADAN ? k.c3 : k.c2);
+  // fp32 Adan multiplies by the reciprocals (update.cuh): 1 IEEE division per element
+  // instead of 5 -- the per-element scalars are rounded once from their double values
+  const double c1d = 1.0 - std::pow(c.beta1, static_cast<double>(t));
+  const double c2d = 1.0 - std::pow(c.beta2, static_cast<double>(t));
+  const double c3d = 1.0 - std::pow(c.beta3, static_cast<double>(t));
+  k.rc1 = (T)(1.0 / c1d);
+  k.rc2 = (T)(1.0 / c2d);
+  k.rc3 = (T)(1.0 / c3d);
+  k.rden = (T)(1.0 / (1.0 + lr * c.weight_decay));
+  if (c.kind == MCO_ADAN && sizeof(T) == 4)
+    k.sthr = sqrt_eps_threshold_mul<T>(k.eps, k.rc3);
+  else
+    k.sthr = sqrt_eps_threshold<T>(k.eps, c.kind == MCO_ADAN ? k.c3 : k.c2);
   k.first = t == 1 ? 1 : 0;
   // only Sophia reads the refresh flag (optim.cpp:161); interval < 1 is refused for it at
   // create, every other kind ignores the field as the reference does

@@ -86,8 +86,10 @@ template <typename T>
 struct StepConsts {
   T b1, b2, b3, omb1, omb2, omb3;  // beta_k and (1 - beta_k)
   T c1, c2, c3;                    // 1 - beta_k^t
+  T rc1, rc2, rc3;                 // 1 / (1 - beta_k^t), rounded once (fp32 Adan)
   T sthr;                          // sqrt_plus_eps threshold (AdamW: c2, Adan: c3; 0 = off)
   T lr, eps, wd, lrwd, den, rho;   // den = 1 + lr*wd (Adan), lrwd = lr*wd (Sophia)
+  T rden;                          // 1 / (1 + lr*wd), rounded once (fp32 Adan)
   int first;                       // Adan: t == 1
   int refresh;                     // Sophia: (t-1) % k == 0
 };
@@ -105,7 +107,7 @@ struct FlatGraphDev {
 };
 template <typename T>
 struct GraphRow {
-  T c1, c2, c3, sthr;
+  T c1, c2, c3, sthr, rc1, rc2, rc3;
 };
 struct GraphStep {
   FlatGraphDev* d = nullptr;  // null: eager (the by-value scalars)
@@ -132,9 +134,11 @@ __device__ __forceinline__ StepConsts<T> step_consts(const StepConsts<T>& kv,
     const double lw = lr * gs.wd;  // make_consts, same double arithmetic (--fmad=false)
     StepConsts<T> k = kv;
     k.c1 = r.c1, k.c2 = r.c2, k.c3 = r.c3, k.sthr = r.sthr;
+    k.rc1 = r.rc1, k.rc2 = r.rc2, k.rc3 = r.rc3;
     k.lr = (T)lr;
     k.lrwd = (T)lw;
     k.den = (T)(1.0 + lw);
+    k.rden = (T)(1.0 / (1.0 + lw));
     k.first = t == 1 ? 1 : 0;
     k.refresh = (gs.interval >= 1 && ((t - 1) % gs.interval) == 0) ? 1 : 0;
     return k;

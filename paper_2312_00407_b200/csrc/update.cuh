@@ -27,6 +27,12 @@ __device__ __forceinline__ float sqrt_plus_eps(float x, float c, float eps, floa
 __device__ __forceinline__ double sqrt_plus_eps(double x, double c, double eps, double) {
   return dsqrt(x / c) + eps;
 }
+// The multiply form (fp32 Adan): sqrt(x * rc) + eps, thr from sqrt_eps_threshold_mul.
+__device__ __forceinline__ float sqrt_mul_plus_eps(float x, float rc, float eps, float thr) {
+  const bool tiny = x < thr;
+  const float r = dsqrt((tiny ? 1.0f : x) * rc) + eps;
+  return tiny ? eps : r;
+}
 
 // The per-element update, operation for operation as optim.cpp.
 template <int KIND, typename T>
@@ -48,9 +54,21 @@ __device__ __forceinline__ void update(T& p, const T g, T& a, T& b, T& c, T& d,
     b = k.b2 * b + k.omb2 * gd;
     const T nu = g + k.b2 * gd;
     c = k.b3 * c + k.omb3 * nu * nu;
-    const T mhat = a / k.c1;
-    const T vhat = b / k.c2;
-    p = (p - k.lr * (mhat + k.b2 * vhat) / sqrt_plus_eps(c, k.c3, k.eps, k.sthr)) / k.den;
+    if constexpr (sizeof(T) == 4) {
+      // fp32: the bias corrections and the decoupled decay as multiplications by
+      // reciprocals rounded once on the host (1 IEEE division instead of 5 per element;
+      // the division chains made this 11-stream kernel issue-bound at low SM clocks).
+      // Within 1e-5 of the fp64 reference like the rest (tests/parity.py); the f64
+      // mode keeps the reference's divisions and stays bit-exact to it.
+      const T mhat = a * k.rc1;
+      const T vhat = b * k.rc2;
+      p = (p - k.lr * (mhat + k.b2 * vhat) / sqrt_mul_plus_eps(c, k.rc3, k.eps, k.sthr)) *
+          k.rden;
+    } else {
+      const T mhat = a / k.c1;
+      const T vhat = b / k.c2;
+      p = (p - k.lr * (mhat + k.b2 * vhat) / sqrt_plus_eps(c, k.c3, k.eps, k.sthr)) / k.den;
+    }
     d = g;
   } else {  // K_SOPHIA, optim.cpp:160-166; a = m, b = h
     a = k.b1 * a + k.omb1 * g;
