@@ -30,12 +30,46 @@ __device__ __forceinline__ void ldg8(const float* g, float (&r)[8]) { ld_stream_
 __device__ __forceinline__ void ldg8(const uint16_t* g, float (&r)[8]) {
   ld_stream_ro_bf16x8(g, r);
 }
+__device__ __forceinline__ void ldp8(const float* p, float (&r)[8]) { ld_stream(p, r); }
+__device__ __forceinline__ void ldp8(const uint16_t* p, float (&r)[8]) { ld_stream_bf16x8(p, r); }
 __device__ __forceinline__ float ldg1(const float* g) { return *g; }
 __device__ __forceinline__ float ldg1(const uint16_t* g) { return bf2f(*g); }
 __device__ __forceinline__ void st8(float* p, const float (&r)[8]) { st_stream(p, r); }
 __device__ __forceinline__ void st8(uint16_t* p, const float (&r)[8]) { st_stream_bf16x8(p, r); }
 __device__ __forceinline__ void st1(float* p, float v) { *p = v; }
 __device__ __forceinline__ void st1(uint16_t* p, float v) { *p = (uint16_t)f2bf_bits(v); }
+
+// Sum over ranks of one 8-element gradient vector: every peer load is issued before the
+// first add (unrolled to kMaxPeers, predicated on the rank count), so the N-1 NVLink
+// round trips overlap instead of serialising; the adds then run in rank order (the
+// deterministic order of CommHub's reduce, comm.cpp:157-181), bit-identical to the loop.
+template <typename GT>
+__device__ __forceinline__ void rank_sum8(const PeerPtrs& pp, uint64_t ge, float (&g)[8]) {
+  float t[kMaxPeers][8];
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r)
+    if (r < pp.n) ldg8((const GT*)pp.g[r] + ge, t[r]);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) g[j] = t[0][j];
+#pragma unroll
+  for (int r = 1; r < kMaxPeers; ++r)
+    if (r < pp.n) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) g[j] = g[j] + t[r][j];
+    }
+}
+template <typename GT>
+__device__ __forceinline__ float rank_sum1(const PeerPtrs& pp, uint64_t ge) {
+  float t[kMaxPeers];
+#pragma unroll
+  for (int r = 0; r < kMaxPeers; ++r)
+    if (r < pp.n) t[r] = ldg1((const GT*)pp.g[r] + ge);
+  float g = t[0];
+#pragma unroll
+  for (int r = 1; r < kMaxPeers; ++r)
+    if (r < pp.n) g = g + t[r];
+  return g;
+}
 
 template <int KIND, typename GT, typename RT>
 __global__ void __launch_bounds__(kThreads)
@@ -46,13 +80,8 @@ __global__ void __launch_bounds__(kThreads)
   const int np = pp.n;
   for (uint64_t vi = tid; vi < nvec; vi += stride) {
     const uint64_t e = vi * 8, ge = off + e;
-    float g[8], t[8], pv[8], a[8], b[8], c[8], d[8];
-    ldg8((const GT*)pp.g[0] + ge, g);
-    for (int r = 1; r < np; ++r) {  // reduce-scatter part: peer loads in rank order
-      ldg8((const GT*)pp.g[r] + ge, t);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) g[j] = g[j] + t[j];
-    }
+    float g[8], pv[8], a[8], b[8], c[8], d[8];
+    rank_sum8<GT>(pp, ge, g);  // reduce-scatter part: peer loads, rank-order sum
     ld_stream(master + e, pv);
     ld_stream(s0 + e, a);
     if constexpr (KIND != K_LION) ld_stream(s1 + e, b);
@@ -79,12 +108,13 @@ __global__ void __launch_bounds__(kThreads)
       st_stream(s2 + e, c);
       st_stream(s3 + e, d);
     }
-    for (int r = 0; r < np; ++r) st8((RT*)pp.p[r] + ge, pv);  // all-gather part
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)  // all-gather part
+      if (r < np) st8((RT*)pp.p[r] + ge, pv);
   }
   for (uint64_t e = nvec * 8 + tid; e < n; e += stride) {
     const uint64_t ge = off + e;
-    float gg = ldg1((const GT*)pp.g[0] + ge);
-    for (int r = 1; r < np; ++r) gg = gg + ldg1((const GT*)pp.g[r] + ge);
+    const float gg = rank_sum1<GT>(pp, ge);
     float pp_ = master[e], aa = s0[e], bb = 0.f, cc = 0.f, dd = 0.f;
     if constexpr (KIND != K_LION) bb = s1[e];
     if constexpr (KIND == K_ADAN) {
@@ -121,8 +151,7 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   double acc = 0.0;
   for (uint64_t e = tid; e < n; e += stride) {
-    float g = ldg1((const GT*)pp.g[0] + off + e);
-    for (int r = 1; r < pp.n; ++r) g = g + ldg1((const GT*)pp.g[r] + off + e);
+    const float g = rank_sum1<GT>(pp, off + e);
     acc += (double)g * (double)g;
   }
   const double b = block_sum(acc, scratch);
@@ -146,7 +175,7 @@ __global__ void __launch_bounds__(kThreads)
 
 template <typename GT, typename RT>
 __global__ void __launch_bounds__(kThreads)
-    peer_lomo_kernel(PeerPtrs pp, float* master, uint64_t off, uint64_t n, double lr,
+    peer_lomo_kernel(PeerPtrs pp, float* master, uint64_t off, uint64_t nvec, uint64_t n, double lr,
                      double scale, const double* sumsq, double clip) {
   if (sumsq) {
     const double norm = sqrt(*sumsq);
@@ -155,9 +184,23 @@ __global__ void __launch_bounds__(kThreads)
   const float f = (float)(lr * scale);
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-  for (uint64_t e = tid; e < n; e += stride) {
-    float g = ldg1((const GT*)pp.g[0] + off + e);
-    for (int r = 1; r < pp.n; ++r) g = g + ldg1((const GT*)pp.g[r] + off + e);
+  for (uint64_t vi = tid; vi < nvec; vi += stride) {  // 8-element vectors
+    const uint64_t e = vi * 8, ge = off + e;
+    float g[8], p[8];
+    rank_sum8<GT>(pp, ge, g);
+    if (master)
+      ld_stream(master + e, p);
+    else
+      ldp8((const RT*)pp.p[0] + ge, p);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = p[j] - f * g[j];
+    if (master) st_stream(master + e, p);
+#pragma unroll
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (r < pp.n) st8((RT*)pp.p[r] + ge, p);
+  }
+  for (uint64_t e = nvec * 8 + tid; e < n; e += stride) {
+    const float g = rank_sum1<GT>(pp, off + e);
     const float p = (master ? master[e] : ldg1((const RT*)pp.p[0] + off + e)) - f * g;
     if (master) master[e] = p;
     for (int r = 0; r < pp.n; ++r) st1((RT*)pp.p[r] + off + e, p);
@@ -206,10 +249,17 @@ void launch_peer_lomo(const PeerPtrs& pp, int grad_dtype, int replica_dtype, flo
                       uint64_t off, uint64_t n, double lr, double scale, const double* sumsq,
                       double clip, cudaStream_t st) {
   if (n == 0) return;
-  const uint64_t blocks = std::min<uint64_t>((n + kThreads - 1) / kThreads,
-                                             (uint64_t)device_info(current_device()).sms * 8);
+  if (pp.n < 1 || pp.n > kMaxPeers)
+    throw Error(MCO_CONTRACT, "peer lomo: 1.." + std::to_string(kMaxPeers) + " ranks");
+  const size_t gsz = grad_dtype == MCO_BF16 ? 2 : 4, rsz = replica_dtype == MCO_BF16 ? 2 : 4;
+  bool vec = off % 8 == 0 && (master == nullptr || al(master, 32));
+  for (int r = 0; r < pp.n; ++r) vec = vec && al(pp.g[r], 8 * gsz) && al(pp.p[r], 8 * rsz);
+  const uint64_t nvec = vec ? n / 8 : 0;
+  const uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>(
+      ((nvec ? nvec : n) + kThreads - 1) / kThreads,
+      (uint64_t)device_info(current_device()).sms * 8));
   auto go = [&](auto kern) {
-    kern<<<(unsigned)blocks, kThreads, 0, st>>>(pp, master, off, n, lr, scale, sumsq, clip);
+    kern<<<(unsigned)blocks, kThreads, 0, st>>>(pp, master, off, nvec, n, lr, scale, sumsq, clip);
     launch_check("peer_lomo_kernel");
   };
   if (grad_dtype == MCO_F32 && replica_dtype == MCO_F32)

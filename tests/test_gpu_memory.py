@@ -23,13 +23,21 @@ GRAN = 4 << 20  # allocation granularity slack per buffer
 
 
 def used_by(fn):
+    """Bytes fn() keeps allocated: the library's cudaMalloc'd buffers from the driver's
+    free-memory delta, torch tensors from the caching allocator's allocated delta (a
+    torch tensor may be carved from a segment an earlier test left reserved, which the
+    driver delta would not see)."""
     gc.collect()
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     f0 = torch.cuda.mem_get_info()[0]
+    r0, a0 = torch.cuda.memory_reserved(), torch.cuda.memory_allocated()
     keep = fn()
     torch.cuda.synchronize()
-    return f0 - torch.cuda.mem_get_info()[0], keep
+    driver = f0 - torch.cuda.mem_get_info()[0]
+    torch_res = torch.cuda.memory_reserved() - r0
+    torch_alloc = torch.cuda.memory_allocated() - a0
+    return driver - torch_res + torch_alloc, keep
 
 
 def test_adalomo_state_bytes_match_device_memory():
