@@ -771,10 +771,10 @@ def bench_e2e(args, res, rank=0, world=1):
             ada = optim.AdaLomoState(cfg, shapes, grad_clip=CLIP)
 
             def one():
-                ada.apply_all(hpn, hgn, cfg.lr)  # whole-set upload (clip), apply, download
+                ada.apply_all(hpn, hgn, cfg.lr)  # g up + stats, then per tensor p up/update/down
         else:
             def one():
-                optim.lomo_step(hpn, hgn, cfg.lr, clip=CLIP)  # mco_lomo_apply_host, 2 passes
+                optim.lomo_step(hpn, hgn, cfg.lr, clip=CLIP)  # mco_lomo_apply_host: g resident
         one()
         torch.cuda.synchronize()
         barrier()
@@ -784,17 +784,23 @@ def bench_e2e(args, res, rank=0, world=1):
         torch.cuda.synchronize()
         dt = max_over_ranks((time.perf_counter() - t0) / steps)
         total = res["P"] if world > 1 else k_n  # params of the whole job this step
-        # LOMO's clip pass streams g once more (mco_lomo_apply_host: Σg² pass, then the
-        # update pass over p and g); with a clip no parameter can leave before every
-        # gradient has arrived, so H2D and D2H do not overlap for LOMO / AdaLomo
-        hb = (3 if kind == "lomo" else 2) * 4
+        # LOMO / AdaLomo with the clip: no parameter may move before every gradient has
+        # arrived, so the gradients go up first (resident on the device: 4 B/param), then
+        # the parameters go up and come back down overlapped (full duplex).  LOMO falls
+        # back to streaming g twice (12 B/param up) when the device has no room for it.
+        hb = 8
+        if kind == "lomo" and torch.cuda.mem_get_info()[0] < 4 * k_n + (2 << 30):
+            hb = 12
         per[kind] = {"ms": round(dt * 1e3, 2), "params_per_s": total / dt,
                      "h2d_bytes_per_param": hb, "d2h_bytes_per_param": 4}
         tot_s += dt
         h2d += hb * total
         d2h += total * 4
         if kind in ("lomo", "adalomo"):
-            bound_serial += hb * k_n / (pcie["h2d_gbs"] * 1e9) + 4 * k_n / (pcie["d2h_gbs"] * 1e9)
+            gb = (hb - 4) * k_n  # gradient upload(s) before any parameter is final
+            bound_serial += gb / (pcie["h2d_gbs"] * 1e9) + max(
+                4 * k_n / (pcie["h2d_gbs"] * 1e9), 4 * k_n / (pcie["d2h_gbs"] * 1e9),
+                8 * k_n / (pcie["both_gbs"] * 1e9))
         else:
             h2d_me += hb * k_n
             d2h_me += k_n * 4
@@ -814,8 +820,8 @@ def bench_e2e(args, res, rank=0, world=1):
                                                                  if world > 1 else ""),
                          "frac": round(bound_s / tot_s, 4)},
             "path": "C-ABI host-span calls on pinned host buffers: mco_flat_step_host, "
-                    "mco_lomo_apply_host (with the clip pass), mco_adalomo_apply_all_host "
-                    "(with the clip; H2D p+g, update, D2H p)" + (
+                    "mco_lomo_apply_host and mco_adalomo_apply_all_host (with the clip: "
+                    "H2D g + its statistics, then H2D p / update / D2H p overlapped)" + (
                         f"; each of {world} ranks over its own part" if world > 1 else "")}
 
 
@@ -913,6 +919,10 @@ def main():
     if world > 1:
         backend = os.environ.get("MCO_BENCH_BACKEND", "nccl")  # gloo: test N ranks on 1 GPU
         if backend == "nccl":
+            # NCCL's init log (rank / nRanks / NVLink / NVLS lines) stays on, on stderr,
+            # so the communicator actually created can be checked against --gpus
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,NVLS")
             if torch.cuda.device_count() < world:
                 print(f"bench.py: {world} ranks but {torch.cuda.device_count()} GPUs",
                       file=sys.stderr)

@@ -16,6 +16,10 @@
 #include <unordered_map>
 #include <vector>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "abi_internal.h"
 
 namespace mco {
@@ -130,6 +134,20 @@ void* sumsq_ws(cudaStream_t st) {
   MCO_CUDA_CHECK(cudaMemset(p, 0, sumsq_ws_bytes()));
   pool[key] = p;
   return p;
+}
+
+void host_trace(const char* what) {
+  static const bool on = [] {
+    const char* e = getenv("MCO_HOST_TRACE");
+    return e && atoi(e) != 0;
+  }();
+  if (!on) return;
+  thread_local std::chrono::steady_clock::time_point t0;
+  const auto now = std::chrono::steady_clock::now();
+  if (what)
+    fprintf(stderr, "[mco host] %s: %.1f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t0).count());
+  t0 = now;
 }
 
 HostStage& host_stage(int dev) {

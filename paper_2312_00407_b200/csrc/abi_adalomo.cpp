@@ -1,5 +1,7 @@
 // C-ABI: AdaLomoState (optim.cpp:192-282) -- hook, list, multi-tensor, host-span and
 // row-split (phase) forms.
+#include <cstdlib>
+
 #include "abi_internal.h"
 
 using namespace mco;
@@ -43,6 +45,9 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
     alloc(&pl.d_tens_sc, pl.h_tensors.size() * 8, sizeof(double));
     alloc(&pl.d_fa, pl.fa_len, sizeof(float));
     alloc(&pl.d_fb, pl.fb_len, sizeof(float));
+    alloc(&pl.d_fra, pl.fa_len, sizeof(float));
+    alloc(&pl.d_frb, pl.fb_len, sizeof(float));
+    alloc(&pl.d_mins, 2 * pl.h_tensors.size(), sizeof(unsigned));
     alloc(&pl.d_glob, 4, sizeof(double));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_tiles, pl.h_tiles.data(), pl.h_tiles.size() * sizeof(Tile),
                               cudaMemcpyHostToDevice));
@@ -73,6 +78,16 @@ void check_ada_dtypes(int pdt, int gdt) {
   if (!ok)
     throw Error(MCO_CONTRACT,
                 "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
+}
+
+// Consecutive hook-form calls overlap (the next tensor's K1 under the previous K6);
+// MCO_ADALOMO_HOOK_OVERLAP=0 turns it off (A/B knob).
+int hook_overlap() {
+  static const int on = [] {
+    const char* e = getenv("MCO_ADALOMO_HOOK_OVERLAP");
+    return e ? atoi(e) : 1;
+  }();
+  return on;
 }
 
 // Hook forms clip with a caller-supplied global Σg² only when the handle opted in.
@@ -119,8 +134,12 @@ mco_status mco_adalomo_apply(mco_adalomo* h, int idx, void* param, int pdt, cons
     c.lr = lr;
     c.use_clip = hook_clip(h->plan, dev_grad_sumsq);
     c.ext_sumsq = dev_grad_sumsq;
+    c.trigger = hook_overlap();
+    c.early = c.trigger && h->last_hook >= 0 && h->last_hook != idx && h->last_stream == stream;
     launch_adalomo(h->plan, c, (cudaStream_t)stream);
     h->plan.h_tensors[idx].t += 1;
+    h->last_hook = idx;
+    h->last_stream = stream;
   });
 }
 
@@ -188,7 +207,8 @@ mco_status mco_adalomo_apply_all(mco_adalomo* h, void* flat_p, int pdt, const vo
 // Host spans (the reference's Tensor data lives in host memory): per tensor,
 // H2D(p_k, g_k) -> hook-form apply(k) -> D2H(p_k) on three streams, so tensor
 // k+1's upload overlaps tensor k's update and tensor k-1's download.  With a
-// global clip every gradient must be seen first: upload all, apply_all, download.
+// global clip every gradient must be seen first: gradients up (with their statistics),
+// then per tensor parameters up -> update -> parameters down (below).
 mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const void* g, int gdt,
                                       double lr) {
   return guard([&] {
@@ -218,18 +238,53 @@ mco_status mco_adalomo_apply_all_host(mco_adalomo* h, void* p, int pdt, const vo
     c.g_dtype = gdt;
     c.lr = lr;
     if (pl.grad_clip_on) {
-      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hp, p, total * ps, cudaMemcpyHostToDevice, up));
-      MCO_CUDA_CHECK(cudaMemcpyAsync(h->hg, g, total * gs, cudaMemcpyHostToDevice, up));
-      MCO_CUDA_CHECK(cudaStreamSynchronize(up));
-      c.t0 = 0;
-      c.t1 = nt;
-      c.p = h->hp;
-      c.g = h->hg;
-      c.single = 0;
+      // The clip needs every gradient before any parameter moves, so the step streams in
+      // two halves.  A: the gradients go up tensor by tensor and each tensor's gradient
+      // statistics (K1 in its gradient-only mode) run as it lands; then the global sum of
+      // g^2.  B: per tensor, its parameters go up, sum p^2 (K1 parameter-only mode), the
+      // rest of the update, and the parameters come back down -- B's uploads share the
+      // link with its downloads (full duplex) instead of following them.  The statistics
+      // keep MODE 3's loops and order and the global sum K2's, so the result equals the
+      // device apply_all on the uploaded buffers bit for bit.
+      double* gsum = pl.d_glob + 2;
+      for (int k = 0; k < nt; ++k) {
+        const TensorInfo& T = pl.h_tensors[k];
+        const uint64_t off = (uint64_t)T.elem_off, n = (uint64_t)T.numel;
+        MCO_CUDA_CHECK(cudaMemcpyAsync((char*)h->hg + off * gs, (const char*)g + off * gs,
+                                       n * gs, cudaMemcpyHostToDevice, up));
+        MCO_CUDA_CHECK(cudaEventRecord(h->ev_in[k], up));
+        MCO_CUDA_CHECK(cudaStreamWaitEvent(comp, h->ev_in[k], 0));
+        c.t0 = k;
+        c.t1 = k + 1;
+        c.p = (char*)h->hp + off * ps;
+        c.g = (char*)h->hg + off * gs;
+        c.single = 1;
+        c.stats_mode = 1;
+        launch_adalomo_phase(pl, c, 1, comp);
+      }
+      launch_adalomo_gsumsq(pl, 0, nt, gsum, comp);
+      c.stats_mode = 2;
       c.use_clip = 1;
-      launch_adalomo(pl, c, comp);
-      MCO_CUDA_CHECK(cudaStreamSynchronize(comp));
-      MCO_CUDA_CHECK(cudaMemcpyAsync(p, h->hp, total * ps, cudaMemcpyDeviceToHost, down));
+      c.ext_sumsq = gsum;
+      c.fuse_usq = 1;
+      for (int k = 0; k < nt; ++k) {
+        const TensorInfo& T = pl.h_tensors[k];
+        const uint64_t off = (uint64_t)T.elem_off, n = (uint64_t)T.numel;
+        char* dp = (char*)h->hp + off * ps;
+        MCO_CUDA_CHECK(cudaMemcpyAsync(dp, (const char*)p + off * ps, n * ps,
+                                       cudaMemcpyHostToDevice, up));
+        MCO_CUDA_CHECK(cudaEventRecord(h->ev_in[k], up));
+        MCO_CUDA_CHECK(cudaStreamWaitEvent(comp, h->ev_in[k], 0));
+        c.t0 = k;
+        c.t1 = k + 1;
+        c.p = dp;
+        c.g = (char*)h->hg + off * gs;
+        for (int phase = 1; phase <= 3; ++phase) launch_adalomo_phase(pl, c, phase, comp);
+        MCO_CUDA_CHECK(cudaEventRecord(h->ev_out[k], comp));
+        MCO_CUDA_CHECK(cudaStreamWaitEvent(down, h->ev_out[k], 0));
+        MCO_CUDA_CHECK(cudaMemcpyAsync((char*)p + off * ps, dp, n * ps, cudaMemcpyDeviceToHost,
+                                       down));
+      }
     } else {
       for (int k = 0; k < nt; ++k) {
         const TensorInfo& T = pl.h_tensors[k];

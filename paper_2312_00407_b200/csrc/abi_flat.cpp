@@ -533,43 +533,90 @@ mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint
 }
 
 // lomo_apply on host spans (the reference's Tensor data is host memory).
-// clip >= 0: two passes over the gradient -- sum of squares, then the update.
+// clip >= 0: the norm needs every gradient before any parameter moves.  When the device
+// has room, the gradient goes up once into a resident buffer (its sum of squares chunk by
+// chunk as it lands), then the parameters stream up / update / down against it: 8 B/param
+// up instead of 12.  Otherwise two passes over the host gradient.  The chunking and the
+// accumulation order are the same either way (bit-identical norms).
 mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                                double scale, double clip) {
   return guard([&] {
     check_data(n, p, g, "lomo_apply_host");
     const int dev = current_device();
+    const size_t gsz = dtype_size(gdt), psz = dtype_size(pdt);
+    host_trace(nullptr);
     const double* dnorm = nullptr;
     double* acc = nullptr;
+    void* gres = nullptr;  // device-resident gradient (clip only)
     if (clip >= 0) {
       MCO_CUDA_CHECK(cudaMalloc(&acc, sizeof(double)));
       MCO_CUDA_CHECK(cudaMemset(acc, 0, sizeof(double)));
       HostStage& hs = host_stage(dev);
-      host_pipeline(dev, const_cast<void*>(g), dtype_size(gdt), nullptr, 0, n, false,
-                    [&](void* dg_, void*, uint64_t, uint64_t m, cudaStream_t st) {
-                      // one accumulator, chunks strictly ordered through stream 0
-                      if (st != hs.st[0]) {
-                        cudaEvent_t ev;
-                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                        MCO_CUDA_CHECK(cudaEventRecord(ev, hs.st[0]));
-                        MCO_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
-                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
-                      }
-                      launch_sumsq(dg_, gdt, m, acc, 1, sumsq_ws(st), st);
-                      if (st != hs.st[0]) {
-                        cudaEvent_t ev;
-                        MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                        MCO_CUDA_CHECK(cudaEventRecord(ev, st));
-                        MCO_CUDA_CHECK(cudaStreamWaitEvent(hs.st[0], ev, 0));
-                        MCO_CUDA_CHECK(cudaEventDestroy(ev));
-                      }
-                    });
+      size_t free_b = 0, total_b = 0;
+      MCO_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+      if (n * gsz + (2ull << 30) < free_b) {
+        if (cudaMalloc(&gres, n * gsz) != cudaSuccess) {
+          cudaGetLastError();  // out of memory: fall back to the two-pass form
+          gres = nullptr;
+        }
+      }
+      if (gres) {
+        std::lock_guard<std::mutex> lock(hs.mu);
+        const uint64_t C = hs.chunk_bytes / 8;
+        cudaStream_t up = hs.st[1], red = hs.st[0];
+        cudaEvent_t ev[2];
+        for (auto& e : ev) MCO_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        int k = 0;
+        for (uint64_t off = 0; off < n; off += C, k ^= 1) {
+          const uint64_t m = std::min(C, n - off);
+          char* dg_ = (char*)gres + off * gsz;
+          MCO_CUDA_CHECK(cudaMemcpyAsync(dg_, (const char*)g + off * gsz, m * gsz,
+                                         cudaMemcpyHostToDevice, up));
+          MCO_CUDA_CHECK(cudaEventRecord(ev[k], up));
+          MCO_CUDA_CHECK(cudaStreamWaitEvent(red, ev[k], 0));
+          launch_sumsq(dg_, gdt, m, acc, 1, sumsq_ws(red), red);  // chunk order, one stream
+        }
+        MCO_CUDA_CHECK(cudaStreamSynchronize(up));
+        MCO_CUDA_CHECK(cudaStreamSynchronize(red));
+        for (auto& e : ev) MCO_CUDA_CHECK(cudaEventDestroy(e));
+        host_trace("lomo_apply_host: gradient resident + sum of squares");
+      } else {
+        host_pipeline(dev, const_cast<void*>(g), gsz, nullptr, 0, n, false,
+                      [&](void* dg_, void*, uint64_t, uint64_t m, cudaStream_t st) {
+                        // one accumulator, chunks strictly ordered through stream 0
+                        if (st != hs.st[0]) {
+                          cudaEvent_t ev;
+                          MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                          MCO_CUDA_CHECK(cudaEventRecord(ev, hs.st[0]));
+                          MCO_CUDA_CHECK(cudaStreamWaitEvent(st, ev, 0));
+                          MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                        }
+                        launch_sumsq(dg_, gdt, m, acc, 1, sumsq_ws(st), st);
+                        if (st != hs.st[0]) {
+                          cudaEvent_t ev;
+                          MCO_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                          MCO_CUDA_CHECK(cudaEventRecord(ev, st));
+                          MCO_CUDA_CHECK(cudaStreamWaitEvent(hs.st[0], ev, 0));
+                          MCO_CUDA_CHECK(cudaEventDestroy(ev));
+                        }
+                      });
+      }
       dnorm = acc;
     }
-    host_pipeline(dev, p, dtype_size(pdt), g, dtype_size(gdt), n, true,
-                  [&](void* dp, void* dg_, uint64_t, uint64_t m, cudaStream_t st) {
-                    launch_lomo(dp, pdt, dg_, gdt, m, lr, scale, dnorm, clip, st);
-                  });
+    if (gres) {
+      host_pipeline(dev, p, psz, nullptr, 0, n, true,
+                    [&](void* dp, void*, uint64_t off, uint64_t m, cudaStream_t st) {
+                      launch_lomo(dp, pdt, (const char*)gres + off * gsz, gdt, m, lr, scale,
+                                  dnorm, clip, st);
+                    });
+    } else {
+      host_pipeline(dev, p, psz, g, gsz, n, true,
+                    [&](void* dp, void* dg_, uint64_t, uint64_t m, cudaStream_t st) {
+                      launch_lomo(dp, pdt, dg_, gdt, m, lr, scale, dnorm, clip, st);
+                    });
+    }
+    host_trace("lomo_apply_host: parameters up / update / down");
+    if (gres) cudaFree(gres);
     if (acc) cudaFree(acc);
   });
 }

@@ -121,6 +121,10 @@ struct HostStage {
 
 HostStage& host_stage(int dev);
 
+// MCO_HOST_TRACE=1: wall time of each stage of a host-span call on stderr (what = null
+// starts the clock).
+void host_trace(const char* what);
+
 // fn(dev_a, dev_b, offset, count, stream) runs the kernel(s) for one chunk.
 template <class F>
 void host_pipeline(int dev, void* a, size_t as, const void* b, size_t bs, uint64_t n,
@@ -202,6 +206,10 @@ struct mco_adalomo {
   void* hg = nullptr;
   cudaStream_t hst[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> ev_in, ev_out;
+  // last hook-form call (tensor, stream): the next one on the same stream for another
+  // tensor may start its K1 under the previous K6 (adalomo.h AdaLomoCall::early)
+  int last_hook = -1;
+  void* last_stream = nullptr;
   ~mco_adalomo() {
     if (hp) cudaFree(hp);
     if (hg) cudaFree(hg);
@@ -212,7 +220,8 @@ struct mco_adalomo {
     void* ptrs[] = {plan.d_tiles, plan.d_chunks, plan.d_chunk_sc, plan.d_tensors, plan.d_item_off, plan.d_col_off,
                     plan.d_payload, plan.d_state,
                     plan.d_colpart, plan.d_rowpart, plan.d_tile_sc, plan.d_tens_sc,
-                    plan.d_fa,    plan.d_fb,      plan.d_glob};
+                    plan.d_fa,    plan.d_fb,      plan.d_glob, plan.d_fra, plan.d_frb,
+                    plan.d_mins};
     for (void* p : ptrs)
       if (p) cudaFree(p);
   }

@@ -9,6 +9,8 @@
 //
 //   K1 stats   (tiles)   : per row sum g^2 (row partials), per column partial
 //                          sums over the tile's rows, sum p^2, sum v_row_old
+//   KR         (columns) : tile partials -> statistics payload (column sums, per tensor
+//                          sum g^2 / p^2 / v_row_old)
 //   K2 scalars (1 CTA)   : per tensor sum g^2, sum p^2 -> global clip scale s,
 //                          t += 1, corr, rms_theta, lr_t, row_mean (linearity)
 //   K3 moments (items)   : v_row / v_col EMAs (fp64 state) and the fp32
@@ -16,6 +18,9 @@
 //   K4 sum u^2 (tiles)   : u = s*g / sqrt(a_i*b_j + eps); 1-D tensors update v_full
 //   K5 damping (1 CTA)   : f = lr_t / max(1, rms_u / adalomo_clip)
 //   K6 update  (tiles)   : p -= f * u  (u recomputed bit-identically to K4)
+// Unsharded calls run K2 inside KR's scalar block and K5 in K4's last CTA (5 launches);
+// the row-split sharded phases all-reduce the payloads between KR and K2 and between
+// K4 and K5, so they launch all seven.
 //
 // Work unit = tile: rows [r0,r1) x columns [c0,c1) of one matrix (or an
 // element range of a 1-D tensor), one CTA per tile, persistent grid over the
@@ -24,6 +29,7 @@
 // All reductions are fixed-order (no float atomics): results are
 // bit-reproducible run to run.
 #include <algorithm>
+#include <atomic>
 #include <cfloat>
 #include <mutex>
 #include <unordered_map>
@@ -33,6 +39,7 @@
 #include <vector>
 
 #include "adalomo.h"
+#include "tma.cuh"
 
 namespace mco {
 namespace {
@@ -101,6 +108,9 @@ struct Ctx {
   int64_t ntens;      // total tensors (payload layout)
   const Chunk* chunks;
   double* chunk_sc;   // per-chunk sum u^2
+  float* fra;         // 1 / sqrt(a_i)  (separable form, see sep_ok)
+  float* frb;         // 1 / sqrt(b_j)
+  unsigned* mins;     // per tensor: min a_i, min b_j (fp32 bits; atomicMin)
 };
 
 enum { TS_GSQ = 0, TS_PSQ, TS_VRS, TS_CORR, TS_LRT, TS_ROWMEAN, TS_USQ, TS_F, kTensScalars };
@@ -172,14 +182,16 @@ __device__ __forceinline__ void store_p(PT* p, const float (&r)[VW], int valid) 
 // One lane's 8-column chunk of one row, held in load form until it is consumed: fp32
 // as 8 floats, bf16 as the 4 raw 32-bit words (half the registers), so the bf16 tile
 // kernels can keep twice the rows in flight (rows_in_flight) without spilling.
+// On the vector path (C % 8 == 0, so a lane's chunk is either whole or outside the tile)
+// a load is always a whole 8-element vector: callers load only lanes with valid > 0.
 template <bool VEC, typename T, bool RO>
 struct RowVec {
   float v[VW];
   __device__ __forceinline__ void load(const T* src, int valid) {
     if constexpr (RO)
-      load_vec<VEC, T>(src, v, valid);
+      load_vec<VEC, T>(src, v, VEC ? VW : valid);
     else
-      load_p<VEC, T>(src, v, valid);
+      load_p<VEC, T>(src, v, VEC ? VW : valid);
   }
   __device__ __forceinline__ void get(float (&r)[VW]) const {
 #pragma unroll
@@ -194,7 +206,7 @@ template <bool VEC, bool RO>
 struct RowVec<VEC, uint16_t, RO> {
   uint32_t w[4];
   __device__ __forceinline__ void load(const uint16_t* src, int valid) {
-    if (VEC && valid == VW) {
+    if constexpr (VEC) {
       if constexpr (RO)
         asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
@@ -243,10 +255,23 @@ __device__ __forceinline__ PT* pptr(const Ptrs& P, const TensorInfo& T, int k) {
 }
 
 // ============================ K1: statistics =====================================
-template <bool VEC, typename GT, typename PT>
+// MODE bit 1: gradient statistics (row sums, column partials, sum g^2, sum v_row_old);
+// bit 2: parameter statistics (sum p^2).  MODE 3 is the normal pass; the host-span
+// clipped form (mco_adalomo_apply_all_host) runs MODE 1 while the gradients stream in
+// and MODE 2 per tensor once its parameters have arrived -- same loops and accumulation
+// order, so the statistics are bit-identical to MODE 3's.
+constexpr int kStatsG = 1, kStatsP = 2, kStatsAll = 3;
+//
+// early (hook form, one tensor after another on one stream): the previous kernel is the
+// previous tensor's K6, which triggers its dependents as soon as it starts, and writes
+// only that tensor's parameters -- nothing this kernel reads.  So this pass starts
+// without waiting and fills the SMs K6's tail leaves idle; it waits before it exits, so
+// its own completion still implies K6's (every later kernel's pdl_wait stays transitive).
+template <bool VEC, typename GT, typename PT, int MODE>
 __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
-    k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles) {
-  pdl_wait();
+    k1_stats(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, int early) {
+  constexpr bool SG = MODE & kStatsG, SP = MODE & kStatsP;
+  if (!early) pdl_wait();
   __shared__ float colbuf[kThreads * VW];
   __shared__ float rowbuf[kMaxTileRows * 4];
   __shared__ double scratch[32];
@@ -268,42 +293,58 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
       for (int j = 0; j < VW; ++j) cacc[j] = 0.f;
       // RB rows per iteration: all their loads are in flight before any math
       constexpr int RB = rows_in_flight<GT, PT>();
+      const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
+      int64_t roff = (tl.r0 + tr) * T.cols + col;
       for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
         RowVec<VEC, GT, true> gr[RB];
         RowVec<VEC, PT, false> pr[RB];
 #pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          const int64_t r = r0 + (int64_t)b * TR;
-          if (valid > 0 && r < tl.r1) {
-            gr[b].load(g + r * T.cols + col, valid);
-            pr[b].load(p + r * T.cols + col, valid);
+        for (int b = 0; b < RB; ++b, roff += rstep) {
+          if (valid > 0 && r0 + (int64_t)b * TR < tl.r1) {
+            if constexpr (SG) gr[b].load(g + roff, valid);
+            if constexpr (SP) pr[b].load(p + roff, valid);
           } else {
             gr[b].zero();
             pr[b].zero();
           }
         }
+        float sg[RB];
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
-          const int64_t r = r0 + (int64_t)b * TR;
           float gv[VW], pv[VW];
-          gr[b].get(gv);
-          pr[b].get(pv);
-          float sg = 0.f, sp = 0.f;
+          if constexpr (SG) gr[b].get(gv);
+          if constexpr (SP) pr[b].get(pv);
+          float sp = 0.f;
+          sg[b] = 0.f;
 #pragma unroll
-          for (int j = 0; j < VW; ++j) {
-            const float g2 = gv[j] * gv[j];
-            cacc[j] += g2;
-            sg += g2;
-            sp += pv[j] * pv[j];
+          for (int j = 0; j < VW; ++j) {  // fused multiply-adds: K1 on bf16 data is issue-bound
+            if constexpr (SG) {
+              cacc[j] = __fmaf_rn(gv[j], gv[j], cacc[j]);
+              sg[b] = __fmaf_rn(gv[j], gv[j], sg[b]);
+            }
+            if constexpr (SP) sp = __fmaf_rn(pv[j], pv[j], sp);
           }
-          psq += (double)sp;
-          sg = warp_sum(sg);  // a warp never straddles two rows (TC >= 32)
-          if ((threadIdx.x & 31) == 0 && r < tl.r1) rowbuf[(r - tl.r0) * nwr + wrow] = sg;
+          if constexpr (SP) psq += (double)sp;
+        }
+        if constexpr (SG) {
+          // the RB rows' sums over the warp's 256 columns in one multi-value butterfly (a
+          // warp never straddles two rows: TC >= 32); lane group of row b writes it
+          const float tot = warp_sum_rows<RB>(sg);
+          const int lane = threadIdx.x & 31, b = warp_rows_index<RB>(lane);
+          const int64_t r = r0 + (int64_t)b * TR;
+          if ((lane & (32 / RB - 1)) == 0 && r < tl.r1) rowbuf[(r - tl.r0) * nwr + wrow] = tot;
         }
       }
+      if constexpr (!SG) {  // parameter statistics only
+        const double bps = block_sum(psq, scratch);
+        if (threadIdx.x == 0) c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
+        continue;
+      }
       // column partials: fixed-order sum over the TR row groups
+      if constexpr (SG) {
 #pragma unroll
-      for (int j = 0; j < VW; ++j) colbuf[(tr * TC + lane_c) * VW + j] = cacc[j];
+        for (int j = 0; j < VW; ++j) colbuf[(tr * TC + lane_c) * VW + j] = cacc[j];
+      }
       __syncthreads();
       const int64_t w = tl.c1 - tl.c0;
       for (int64_t q = threadIdx.x; q < w; q += kThreads) {
@@ -322,31 +363,44 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
         gsq += s;
         if (tl.cb == 0) vrs += c.state[T.vrow_off + tl.r0 + i];
       }
-      const double bps = block_sum(psq, scratch);
+      const double bps = SP ? block_sum(psq, scratch) : 0.0;
       const double bgs = block_sum(gsq, scratch);
       const double bvr = block_sum(vrs, scratch);
       if (threadIdx.x == 0) {
-        c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
+        if constexpr (SP) c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
         c.tile_sc[(tile0 + ti) * 4 + 1] = bgs;
         c.tile_sc[(tile0 + ti) * 4 + 2] = bvr;
       }
       __syncthreads();  // colbuf / rowbuf reuse by the next tile
     } else {
       for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
-        const double gv = (double)ld1(g + e), pv = (double)ldp1(p + e);
-        gsq += gv * gv;
-        psq += pv * pv;
+        if constexpr (SG) {
+          const double gv = (double)ld1(g + e);
+          gsq += gv * gv;
+        }
+        if constexpr (SP) {
+          const double pv = (double)ldp1(p + e);
+          psq += pv * pv;
+        }
       }
-      const double bps = block_sum(psq, scratch);
-      const double bgs = block_sum(gsq, scratch);
+      const double bps = SP ? block_sum(psq, scratch) : 0.0;
+      const double bgs = SG ? block_sum(gsq, scratch) : 0.0;
       if (threadIdx.x == 0) {
-        c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
-        c.tile_sc[(tile0 + ti) * 4 + 1] = bgs;
-        c.tile_sc[(tile0 + ti) * 4 + 2] = 0.0;
+        if constexpr (SP) c.tile_sc[(tile0 + ti) * 4 + 0] = bps;
+        if constexpr (SG) {
+          c.tile_sc[(tile0 + ti) * 4 + 1] = bgs;
+          c.tile_sc[(tile0 + ti) * 4 + 2] = 0.0;
+        }
       }
     }
   }
+  if (early) pdl_wait();
 }
+
+// K2's / K5's work, also run inside KR / K4 by unsharded (fused) calls
+__device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
+                        double clip, const double* ext_sumsq, double* red);
+__device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip);
 
 // ============================ KR: tile partials -> payload ===========================
 // Blocks [0, ncolblk): one thread per column of the factored tensors in [t0,t1):
@@ -356,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
 // already contributes), so an all-reduce of the payload yields global sums.
 __global__ void __launch_bounds__(kThreads)
     kr_stats(Ctx c, int t0, int t1, const int64_t* __restrict__ col_off, int64_t ncols,
-             int ncolblk) {
+             int ncolblk, int mode, int fuse2, double lr, double b2, int use_clip, double clip,
+             const double* ext_sumsq) {
   pdl_wait();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if ((int)blockIdx.x < ncolblk) {
@@ -408,19 +463,26 @@ __global__ void __launch_bounds__(kThreads)
     gs = warp_sum(gs);
     vr = warp_sum(vr);
     if (lane == 0) {
-      c.pay[k * 3 + 0] = T.weight * gs;
-      c.pay[k * 3 + 1] = T.weight * ps;
-      c.pay[k * 3 + 2] = T.weight * vr;
+      if (mode & kStatsG) {
+        c.pay[k * 3 + 0] = T.weight * gs;
+        c.pay[k * 3 + 2] = T.weight * vr;
+      }
+      if (mode & kStatsP) c.pay[k * 3 + 1] = T.weight * ps;
     }
+  }
+  if (fuse2) {  // unsharded call: nothing to all-reduce, K2's work follows in this block
+    __shared__ double red[32];
+    __syncthreads();
+    k2_body(c, t0, t1, lr, b2, use_clip, clip, ext_sumsq, red);
   }
 }
 
 __device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = t0 + warp; k < t1; k += 32) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int k = t0 + warp; k < t1; k += nw) {
     const TensorInfo T = c.tensors[k];
-    double us = 0;
-    for (int64_t i = T.chunk_begin + lane; i < T.chunk_end; i += 32) us += c.chunk_sc[i];
+    double us = 0;  // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
+    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += __ldcg(&c.tile_sc[i * 4 + 3]);
     us = warp_sum(us);
     if (lane == 0) c.pay_usq[k] = T.weight * us;
   }
@@ -431,15 +493,25 @@ __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
   usq_payload(c, t0, t1);
 }
 
-// ============================ K2: per-tensor scalars ===============================
-// One CTA of 1024 threads.  Warp w handles tensors w, w+32, ...; tile sums are
-// lane-strided + butterfly (fixed order).  Then the global sum of g^2 over the
-// call's tensors in tensor order, the clip scale, and the per-tensor scalars.
-__global__ void __launch_bounds__(1024)
-    k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
-               const double* ext_sumsq) {
+// Global sum of g^2 over tensors [t0, t1) from the payload, in K2's order (same
+// threads, strides and block reduction), so a clip scale computed from it equals the
+// one K2 derives over the same range bit for bit.
+__global__ void __launch_bounds__(kThreads) kg_sumsq(Ctx c, int t0, int t1, double* out) {
   pdl_wait();
   __shared__ double red[32];
+  double G = 0;
+  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) G += c.pay[k * 3 + 0];
+  G = block_sum(G, red);
+  if (threadIdx.x == 0) *out = G;
+}
+
+// ============================ K2: per-tensor scalars ===============================
+// One CTA of kThreads threads (k2_scalars, or KR's scalar block in fused calls).  Thread
+// i handles tensors i, i + kThreads, ...: the per-tensor sums, then the global sum of g^2
+// over the call's tensors (fixed order: block_sum), the clip scale and the per-tensor
+// scalars.
+__device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
+                        double clip, const double* ext_sumsq, double* red) {
   // per-tensor sums arrive (already all-reduced across ranks when sharded) in the payload
   for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
     c.tens_sc[k * kTensScalars + TS_GSQ] = c.pay[k * 3 + 0];
@@ -481,47 +553,97 @@ __global__ void __launch_bounds__(1024)
     c.tens_sc[k * kTensScalars + TS_CORR] = corr;
     c.tens_sc[k * kTensScalars + TS_LRT] = lr_t;
     c.tens_sc[k * kTensScalars + TS_ROWMEAN] = row_mean;
+    c.mins[2 * k] = c.mins[2 * k + 1] = 0x7f800000u;  // +inf: K3 lowers them
   }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k2_scalars(Ctx c, int t0, int t1, double lr, double b2, int use_clip, double clip,
+               const double* ext_sumsq) {
+  pdl_wait();
+  __shared__ double red[32];
+  k2_body(c, t0, t1, lr, b2, use_clip, clip, ext_sumsq, red);
 }
 
 // ============================ K3: moments ============================================
 // Item space: for each factored tensor in [t0,t1): rows then columns.
+//
+// Besides a_i and b_j, K3 writes their reciprocal square roots (from the fp64 values,
+// rounded once) and lowers the tensor's min a / min b (fp32 bits, atomicMin: a, b >= 0,
+// so the bit order is the value order -- deterministic), one atomic per warp and
+// (tensor, rows|cols) group.  K4 / K6 use them for the separable form of u (sep_ok).
 __global__ void __launch_bounds__(kThreads)
     k3_moments(Ctx c, int t0, int t1, const int64_t* __restrict__ item_off, int64_t item0,
                int64_t nitems, double b2) {
   pdl_wait();
   const double s = c.glob[0], s2 = s * s;
-  for (int64_t it = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; it < nitems;
-       it += (int64_t)gridDim.x * blockDim.x) {
-    // binary search the tensor owning this item
-    const int64_t gi = item0 + it;
-    int lo = t0, hi = t1 - 1;  // largest k with item_off[k] <= gi
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (item_off[mid] <= gi)
-        lo = mid;
-      else
-        hi = mid - 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // warp-uniform trip count (the min reduction below needs all 32 lanes)
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); base < nitems;
+       base += stride) {
+    const int64_t it = base + lane;
+    unsigned key = 0xffffffffu, bits = 0x7f800000u;
+    if (it < nitems) {
+      // binary search the tensor owning this item
+      const int64_t gi = item0 + it;
+      int lo = t0, hi = t1 - 1;  // largest k with item_off[k] <= gi
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (item_off[mid] <= gi)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      const TensorInfo T = c.tensors[lo];
+      const int64_t local = gi - item_off[lo];
+      const double corr = c.tens_sc[lo * kTensScalars + TS_CORR];
+      if (local < T.rows) {  // row i: optim.cpp:239-240
+        const int64_t i = local;
+        double acc = 0.0;
+        for (int k = 0; k < T.kc; ++k) acc += c.rowpart[T.rowpart_off + (int64_t)k * T.rows + i];
+        double& vr = c.state[T.vrow_off + i];
+        vr = b2 * vr + (1 - b2) * (s2 * acc / (double)T.cols);
+        const double a = vr / corr;
+        c.fa[T.fa_off + i] = (float)a;
+        c.fra[T.fa_off + i] = (float)(1.0 / sqrt(a));
+        key = 2u * (unsigned)lo;
+        bits = __float_as_uint((float)a);
+      } else {  // column j: optim.cpp:247-248
+        const int64_t j = local - T.rows;
+        const double acc = c.pay[3 * c.ntens + T.fb_off + j];  // all-reduced column sum
+        double& vc = c.state[T.vcol_off + j];
+        vc = b2 * vc + (1 - b2) * (s2 * acc / (double)T.rows_global);
+        const double rm = c.tens_sc[lo * kTensScalars + TS_ROWMEAN];
+        const double b = (vc / corr) / fmax(rm, 1e-300);
+        c.fb[T.fb_off + j] = (float)b;
+        c.frb[T.fb_off + j] = (float)(1.0 / sqrt(b));
+        key = 2u * (unsigned)lo + 1u;
+        bits = __float_as_uint((float)b);
+      }
     }
-    const TensorInfo T = c.tensors[lo];
-    const int64_t local = gi - item_off[lo];
-    const double corr = c.tens_sc[lo * kTensScalars + TS_CORR];
-    if (local < T.rows) {  // row i: optim.cpp:239-240
-      const int64_t i = local;
-      double acc = 0.0;
-      for (int k = 0; k < T.kc; ++k) acc += c.rowpart[T.rowpart_off + (int64_t)k * T.rows + i];
-      double& vr = c.state[T.vrow_off + i];
-      vr = b2 * vr + (1 - b2) * (s2 * acc / (double)T.cols);
-      c.fa[T.fa_off + i] = (float)(vr / corr);
-    } else {  // column j: optim.cpp:247-248
-      const int64_t j = local - T.rows;
-      const double acc = c.pay[3 * c.ntens + T.fb_off + j];  // all-reduced column sum
-      double& vc = c.state[T.vcol_off + j];
-      vc = b2 * vc + (1 - b2) * (s2 * acc / (double)T.rows_global);
-      const double rm = c.tens_sc[lo * kTensScalars + TS_ROWMEAN];
-      c.fb[T.fb_off + j] = (float)((vc / corr) / fmax(rm, 1e-300));
+    const unsigned k0 = __shfl_sync(0xffffffffu, key, 0);
+    if (__all_sync(0xffffffffu, key == k0 || key == 0xffffffffu)) {
+      const unsigned m = __reduce_min_sync(0xffffffffu, bits);
+      if (lane == 0 && k0 != 0xffffffffu) atomicMin(&c.mins[k0], m);
+    } else if (key != 0xffffffffu) {
+      atomicMin(&c.mins[key], bits);
     }
   }
+}
+
+// Separable form of u in K4: when eps <= 2^-26 a_i b_j for every element of the tensor,
+// eps moves a_i b_j + eps by < 2^-26 relative (u by < 2^-27), and
+//   sum u_ij^2 = s^2 sum_i (1/a_i) sum_j (g_ij / sqrt(b_j))^2
+// within fp32 rounding -- no per-element MUFU.RSQ (K4 reads 2-4 B per element and was
+// issue-bound on it, bf16 the most).  K6 keeps the per-element form (it is bound by
+// latency, not issue; u there and here agree to ~3e-7 relative, far inside the damping
+// factor's use).  min a, min b >= 2^-60 keeps every
+// product and the squares K4 sums far from fp32 underflow / overflow.  Otherwise (eps
+// not negligible, zero rows, vanishing gradients) the per-element form below runs.
+__device__ __forceinline__ bool sep_ok(const Ctx& c, int k, double eps) {
+  const float ma = __uint_as_float(c.mins[2 * k]), mb = __uint_as_float(c.mins[2 * k + 1]);
+  return ma >= 0x1p-60f && mb >= 0x1p-60f && (double)ma * (double)mb * 0x1p-26 >= eps;
 }
 
 // u for a factored element: u = (s*g) / sqrt(a_i*b_j + eps)   (optim.cpp:256-259),
@@ -557,11 +679,138 @@ __device__ __forceinline__ void row_col(uint32_t e, const TensorInfo& T, uint32_
 }
 
 // ============================ K4: sum u^2 ============================================
-// Flat chunks: each thread takes 8-wide vectors (C % 8 == 0 on the vector path, so a
-// vector never straddles rows), kU vectors in flight, row = e / C and col = e % C in
-// 32-bit arithmetic (tensor numel < 2^31), a_row and b[col..col+7] from L1/L2.
-constexpr int kU = 4;
+// Over the statistics tiles, like K1: each lane owns one 8-column chunk of the tile, so
+// b_j (or 1/sqrt(b_j)) sits in registers for the whole tile and a row costs one a_i
+// load -- no per-vector index arithmetic (the flat-chunk traversal spent ~14 address
+// instructions per 8 elements, with K4 issue-bound on bf16 data).  Rows in flight: one
+// stream only, so twice K1's.  The per-tile sums go to tile_sc[.][3].
+template <typename GT>
+constexpr int k4_rows() {
+  return sizeof(GT) == 2 ? 4 * kRB : 2 * kRB;
+}
 
+template <bool VEC, typename GT>
+__global__ void __launch_bounds__(kThreads, k4_minb<GT>())
+    k4_usq(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double b2, double eps, int t0, int t1,
+           int fuse5, double adalomo_clip) {
+  pdl_wait();
+  __shared__ double scratch[32];
+  __shared__ bool last;
+  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
+  for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const Tile tl = c.tiles[tile0 + ti];
+    const TensorInfo T = c.tensors[tl.tensor];
+    const GT* g = gptr<GT>(P, T, tl.tensor);
+    double usq = 0.0;
+    if (T.factored) {
+      const int TC = T.tc, TR = kThreads / T.tc;
+      const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
+      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
+      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      if (valid > 0) {
+        const bool sep = sep_ok(c, tl.tensor, eps);
+        const float* fa = (sep ? c.fra : c.fa) + T.fa_off;
+        float bv[VW];
+#pragma unroll
+        for (int j = 0; j < VW; ++j)
+          bv[j] = j < valid ? (sep ? c.frb : c.fb)[T.fb_off + col + j] : 0.f;
+        constexpr int RB = k4_rows<GT>();
+        const int64_t rstep = (int64_t)TR * T.cols;  // row pointers advance by adds
+        const GT* grow = g + (tl.r0 + tr) * T.cols + col;
+        for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
+          RowVec<VEC, GT, true> gr[RB];
+          const GT* gb = grow;
+#pragma unroll
+          for (int b = 0; b < RB; ++b, gb += rstep) {
+            if (r0 + (int64_t)b * TR < tl.r1)
+              gr[b].load(gb, valid);
+            else
+              gr[b].zero();
+          }
+          grow = gb;
+          float su = 0.f;
+#pragma unroll
+          for (int b = 0; b < RB; ++b) {
+            const int64_t r = r0 + (int64_t)b * TR;
+            if (r < tl.r1) {
+              const float a = fa[r];
+              float gv[VW];
+              gr[b].get(gv);
+              if (sep) {  // a = 1/sqrt(a_i), bv = 1/sqrt(b_j): ra^2 sum_j (g rb)^2
+                float rs = 0.f;
+#pragma unroll
+                for (int j = 0; j < VW; ++j) {
+                  const float x = gv[j] * bv[j];
+                  rs = __fmaf_rn(x, x, rs);
+                }
+                su = __fmaf_rn(a * a, rs, su);
+              } else {
+#pragma unroll
+                for (int j = 0; j < VW; ++j) {  // s is applied once per tile (s^2 below)
+                  const float x = gv[j] * rsqrt_ftz(__fmaf_rn(a, bv[j], epsf));
+                  su = __fmaf_rn(x, x, su);
+                }
+              }
+            }
+          }
+          usq += (double)su;
+        }
+      }
+      usq *= (double)sf * (double)sf;  // sum (s g r)^2 = s^2 sum (g r)^2
+    } else {  // optim.cpp:262-267 with fp64 state
+      const double s = c.glob[0];
+      const double corr = c.tens_sc[tl.tensor * kTensScalars + TS_CORR];
+      for (int64_t e = tl.r0 + threadIdx.x; e < tl.r1; e += kThreads) {
+        const double gs = s * (double)ld1(g + e);
+        double& v = c.state[T.vfull_off + e];
+        v = b2 * v + (1 - b2) * gs * gs;
+        const double u = gs / sqrt(v / corr + eps);
+        usq += u * u;
+      }
+    }
+    const double b = block_sum(usq, scratch);
+    if (threadIdx.x == 0) c.tile_sc[(tile0 + ti) * 4 + 3] = b;
+  }
+  if (fuse5) {  // unsharded call: the last CTA to finish does K5's reduction and damping
+    unsigned* ticket = reinterpret_cast<unsigned*>(c.glob + 3);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      usq_payload(c, t0, t1);
+      __syncthreads();
+      k5_body(c, t0, t1, adalomo_clip);
+      if (threadIdx.x == 0) *ticket = 0u;
+    }
+  }
+}
+
+// ============================ K5: damping ==============================================
+__device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip) {
+  for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
+    const TensorInfo T = c.tensors[k];
+    const double us = __ldcg(&c.pay_usq[k]);
+    const double rms_u = sqrt(us / (double)T.numel_global);
+    const double damp = fmax(1.0, rms_u / adalomo_clip);
+    c.tens_sc[k * kTensScalars + TS_USQ] = us;
+    c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
+  }
+}
+
+__global__ void __launch_bounds__(1024)
+    k5_damp(Ctx c, int t0, int t1, double adalomo_clip, int with_usq) {
+  pdl_wait();
+  if (with_usq) {  // unsharded call: KR2's reduction here, one launch less per tensor
+    usq_payload(c, t0, t1);
+    __syncthreads();
+  }
+  k5_body(c, t0, t1, adalomo_clip);
+}
+
+// ============================ K6: update ==============================================
 template <bool VEC, typename GT>
 __device__ __forceinline__ void chunk_vec_load(const GT* g, int64_t e, int64_t e1, float (&v)[VW]) {
   if constexpr (VEC) {
@@ -572,103 +821,11 @@ __device__ __forceinline__ void chunk_vec_load(const GT* g, int64_t e, int64_t e
   }
 }
 
-template <bool VEC, typename GT>
-__global__ void __launch_bounds__(kThreads, k4_minb<GT>())
-    k4_usq(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double b2, double eps) {
-  pdl_wait();
-  __shared__ double scratch[32];
-  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
-  for (int64_t ci = blockIdx.x; ci < nchunks; ci += gridDim.x) {
-    const Chunk ch = c.chunks[chunk0 + ci];
-    const TensorInfo T = c.tensors[ch.tensor];
-    const GT* g = gptr<GT>(P, T, ch.tensor);
-    double usq = 0.0;
-    if (T.factored) {
-      const uint32_t C = (uint32_t)T.cols;
-      const float* fa = c.fa + T.fa_off;
-      const float* fb = c.fb + T.fb_off;
-      for (int64_t base = ch.e0 + (int64_t)threadIdx.x * VW; base < ch.e1;
-           base += (int64_t)kThreads * VW * kU) {
-        float gv[kU][VW];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int64_t e = base + (int64_t)u * kThreads * VW;
-          if (e < ch.e1) chunk_vec_load<VEC, GT>(g, e, ch.e1, gv[u]);
-        }
-        float su = 0.f;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int64_t e = base + (int64_t)u * kThreads * VW;
-          if (e < ch.e1) {
-            if constexpr (VEC) {
-              uint32_t row, col;
-              row_col((uint32_t)e, T, C, row, col);
-              const float a = fa[row];
-              const float4 b0 = *reinterpret_cast<const float4*>(fb + col);
-              const float4 b1 = *reinterpret_cast<const float4*>(fb + col + 4);
-              const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-#pragma unroll
-              for (int j = 0; j < VW; ++j) {  // s is applied once per chunk (s^2 below)
-                const float x = gv[u][j] * rsqrt_ftz(__fmaf_rn(a, bv[j], epsf));
-                su = __fmaf_rn(x, x, su);
-              }
-            } else {
-#pragma unroll
-              for (int j = 0; j < VW; ++j) {
-                const int64_t ej = e + j;
-                if (ej < ch.e1) {
-                  uint32_t row, col;
-                  row_col((uint32_t)ej, T, C, row, col);
-                  const float x = gv[u][j] * rsqrt_ftz(__fmaf_rn(fa[row], fb[col], epsf));
-                  su = __fmaf_rn(x, x, su);
-                }
-              }
-            }
-          }
-        }
-        usq += (double)su;
-      }
-      usq *= (double)sf * (double)sf;  // sum (s g r)^2 = s^2 sum (g r)^2: one multiply less
-                                       // per element (K4 is issue-bound on bf16 data)
-    } else {  // optim.cpp:262-267 with fp64 state
-      const double s = c.glob[0];
-      const double corr = c.tens_sc[ch.tensor * kTensScalars + TS_CORR];
-      for (int64_t e = ch.e0 + threadIdx.x; e < ch.e1; e += kThreads) {
-        const double gs = s * (double)ld1(g + e);
-        double& v = c.state[T.vfull_off + e];
-        v = b2 * v + (1 - b2) * gs * gs;
-        const double u = gs / sqrt(v / corr + eps);
-        usq += u * u;
-      }
-    }
-    const double b = block_sum(usq, scratch);
-    if (threadIdx.x == 0) c.chunk_sc[chunk0 + ci] = b;
-  }
-}
-
-// ============================ K5: damping ==============================================
-__global__ void __launch_bounds__(1024)
-    k5_damp(Ctx c, int t0, int t1, double adalomo_clip, int with_usq) {
-  pdl_wait();
-  if (with_usq) {  // unsharded call: KR2's reduction here, one launch less per tensor
-    usq_payload(c, t0, t1);
-    __syncthreads();
-  }
-  for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
-    const TensorInfo T = c.tensors[k];
-    const double us = c.pay_usq[k];
-    const double rms_u = sqrt(us / (double)T.numel_global);
-    const double damp = fmax(1.0, rms_u / adalomo_clip);
-    c.tens_sc[k * kTensScalars + TS_USQ] = us;
-    c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
-  }
-}
-
-// ============================ K6: update ==============================================
 template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads)
-    k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps) {
+    k6_update(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps, int trigger) {
   pdl_wait();
+  if (trigger) pdl_trigger();  // the next tensor's K1 may start (see k1_stats)
   const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   // reverse chunk order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < nchunks; k += gridDim.x) {
@@ -735,11 +892,192 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// K6 on the cp.async.bulk pipeline (the chunk traversal's work, staged through shared
+// memory).  Items are 4096-element pieces of the call's chunks (16 per 64 Ki chunk; the
+// pieces past a short chunk's end are empty and skipped by producer and consumers alike),
+// round-robin over one CTA per SM.  One producer lane issues the bulk copies of a piece's
+// gradient and parameters into stage s (mbarrier complete_tx), 16 consumer warps update
+// the parameters in shared memory (8 elements per thread: row / column of the vector, a_i
+// and b_j from L1), and the producer writes the piece back with a bulk store, refilling
+// the previous piece's stage as in lomo_tma_kernel.  Bytes in flight per SM are set by
+// the stage count (6-8 pieces), not by registers: the register-resident tile K6 on bf16
+// data was latency-bound at 0.8 of the copy bandwidth.  Requires every tensor of the
+// call at a 16 B aligned start with a whole number of 16 B (host: k6_tma_ok).
+constexpr int kK6Piece = 4096;                // elements per piece
+constexpr int kK6Consumers = 512;             // 16 warps: one 8-element vector each
+constexpr int kK6PPC = (int)(kChunkElems / kK6Piece);
+template <typename GT, typename PT>
+constexpr int k6_stage_bytes() {
+  return kK6Piece * (int)(sizeof(GT) + sizeof(PT));
+}
+template <typename GT, typename PT>
+constexpr int k6_stages() {
+  return std::min(8, (200 * 1024) / k6_stage_bytes<GT, PT>());
+}
+template <typename GT, typename PT>
+constexpr int k6_smem() {
+  return k6_stages<GT, PT>() * k6_stage_bytes<GT, PT>() + 2 * k6_stages<GT, PT>() * 8;
+}
+
+__device__ __forceinline__ bool k6_piece(const Ctx& c, int64_t chunk0, int64_t k, Chunk& ch,
+                                         int64_t& e0, int64_t& e1) {
+  ch = c.chunks[chunk0 + k / kK6PPC];
+  e0 = ch.e0 + (k % kK6PPC) * (int64_t)kK6Piece;
+  e1 = std::min<int64_t>(ch.e1, e0 + kK6Piece);
+  return e0 < ch.e1;
+}
+
+template <typename GT, typename PT>
+__global__ void __launch_bounds__(kK6Consumers + 32, 1)
+    k6_tma(Ctx c, Ptrs P, int64_t chunk0, int64_t nchunks, double eps, int trigger) {
+  constexpr int NS = k6_stages<GT, PT>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * k6_stage_bytes<GT, PT>());
+  uint64_t* done = full + NS;
+  auto sp = [&](int s) { return reinterpret_cast<PT*>(smem + s * k6_stage_bytes<GT, PT>()); };
+  auto sg = [&](int s) {
+    return reinterpret_cast<GT*>(smem + s * k6_stage_bytes<GT, PT>() + kK6Piece * sizeof(PT));
+  };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kK6Consumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  pdl_wait();
+  if (trigger) pdl_trigger();
+  const int64_t nitems = nchunks * kK6PPC;
+  // next non-empty item of this CTA at or after k
+  auto next = [&](int64_t k) {
+    Chunk ch;
+    int64_t e0, e1;
+    while (k < nitems && !k6_piece(c, chunk0, k, ch, e0, e1)) k += gridDim.x;
+    return k;
+  };
+  if (warp == kK6Consumers / 32) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      auto issue = [&](int64_t k, int s) {
+        Chunk ch;
+        int64_t e0, e1;
+        k6_piece(c, chunk0, k, ch, e0, e1);
+        const TensorInfo& T = c.tensors[ch.tensor];
+        const uint32_t n = (uint32_t)(e1 - e0);
+        mbar_expect_tx(&full[s], n * (uint32_t)(sizeof(GT) + sizeof(PT)));
+        bulk_g2s<false>(sp(s), pptr<PT>(P, T, ch.tensor) + e0, n * (uint32_t)sizeof(PT), &full[s], 0);
+        bulk_g2s<false>(sg(s), gptr<GT>(P, T, ch.tensor) + e0, n * (uint32_t)sizeof(GT), &full[s], 0);
+      };
+      int64_t kf = next(blockIdx.x);
+      for (int i = 0; i < NS && kf < nitems; ++i, kf = next(kf + gridDim.x)) issue(kf, i);
+      int64_t i = 0;
+      for (int64_t kc = next(blockIdx.x); kc < nitems; kc = next(kc + gridDim.x), ++i) {
+        const int s = (int)(i % NS);
+        mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
+        Chunk ch;
+        int64_t e0, e1;
+        k6_piece(c, chunk0, kc, ch, e0, e1);
+        const TensorInfo& T = c.tensors[ch.tensor];
+        bulk_s2g<false>(pptr<PT>(P, T, ch.tensor) + e0, sp(s), (uint32_t)(e1 - e0) * sizeof(PT), 0);
+        bulk_commit();
+        if (i >= 1 && kf < nitems) {  // refill the previous piece's stage
+          bulk_wait_read_1();
+          issue(kf, (int)((i - 1) % NS));
+          kf = next(kf + gridDim.x);
+        }
+      }
+      bulk_wait_all();
+    }
+    return;
+  }
+  // ---------------- consumers ----------------
+  const float sf = (float)c.glob[0], epsf = ada_eps(eps);
+  int64_t i = 0;
+  for (int64_t k = next(blockIdx.x); k < nitems; k = next(k + gridDim.x), ++i) {
+    const int s = (int)(i % NS);
+    Chunk ch;
+    int64_t e0, e1;
+    k6_piece(c, chunk0, k, ch, e0, e1);
+    const TensorInfo& T = c.tensors[ch.tensor];
+    const double f = c.tens_sc[ch.tensor * kTensScalars + TS_F];
+    mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+    PT* ps = sp(s);
+    const GT* gs = sg(s);
+    const int n = (int)(e1 - e0);
+    if (T.factored) {  // n is a multiple of 8 (C % 8 == 0): whole vectors, one row each
+      const float ff = (float)f;
+      const uint32_t C = (uint32_t)T.cols;
+      for (int v = threadIdx.x; v * 8 < n; v += kK6Consumers) {
+        uint32_t row, col;
+        row_col((uint32_t)(e0 + v * 8), T, C, row, col);
+        const float a = c.fa[T.fa_off + row];
+        const float4 b0 = *reinterpret_cast<const float4*>(c.fb + T.fb_off + col);
+        const float4 b1 = *reinterpret_cast<const float4*>(c.fb + T.fb_off + col + 4);
+        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        float gv[8], pv[8];
+        if constexpr (sizeof(GT) == 2) {
+          const uint4 w = *reinterpret_cast<const uint4*>(gs + v * 8);
+          const uint32_t wa[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            gv[2 * q] = __uint_as_float(wa[q] << 16);
+            gv[2 * q + 1] = __uint_as_float(wa[q] & 0xffff0000u);
+          }
+        } else {
+          const float4 x0 = *reinterpret_cast<const float4*>(gs + v * 8);
+          const float4 x1 = *reinterpret_cast<const float4*>(gs + v * 8 + 4);
+          gv[0] = x0.x, gv[1] = x0.y, gv[2] = x0.z, gv[3] = x0.w;
+          gv[4] = x1.x, gv[5] = x1.y, gv[6] = x1.z, gv[7] = x1.w;
+        }
+        if constexpr (sizeof(PT) == 2) {
+          const uint4 w = *reinterpret_cast<const uint4*>(ps + v * 8);
+          const uint32_t wa[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            pv[2 * q] = __uint_as_float(wa[q] << 16);
+            pv[2 * q + 1] = __uint_as_float(wa[q] & 0xffff0000u);
+          }
+        } else {
+          const float4 x0 = *reinterpret_cast<const float4*>(ps + v * 8);
+          const float4 x1 = *reinterpret_cast<const float4*>(ps + v * 8 + 4);
+          pv[0] = x0.x, pv[1] = x0.y, pv[2] = x0.z, pv[3] = x0.w;
+          pv[4] = x1.x, pv[5] = x1.y, pv[6] = x1.z, pv[7] = x1.w;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
+        if constexpr (sizeof(PT) == 2) {
+          uint4 w;
+          w.x = f2bf2_bits(pv[0], pv[1]);
+          w.y = f2bf2_bits(pv[2], pv[3]);
+          w.z = f2bf2_bits(pv[4], pv[5]);
+          w.w = f2bf2_bits(pv[6], pv[7]);
+          *reinterpret_cast<uint4*>(ps + v * 8) = w;
+        } else {
+          *reinterpret_cast<float4*>(ps + v * 8) = make_float4(pv[0], pv[1], pv[2], pv[3]);
+          *reinterpret_cast<float4*>(ps + v * 8 + 4) = make_float4(pv[4], pv[5], pv[6], pv[7]);
+        }
+      }
+    } else {  // optim.cpp:262-274, fp64 state (elements of a 1-D tensor)
+      const double sd = c.glob[0];
+      const double corr = c.tens_sc[ch.tensor * kTensScalars + TS_CORR];
+      for (int q = threadIdx.x; q < n; q += kK6Consumers) {
+        const double gsd = sd * (double)ld1(gs + q);
+        const double u = gsd / sqrt(c.state[T.vfull_off + e0 + q] / corr + eps);
+        stp1(ps + q, (float)((double)ldp1(ps + q) - f * u));
+      }
+    }
+    fence_proxy_async();
+    mbar_arrive(&done[s]);
+  }
+}
+
 // K6 over the statistics tiles (alternative traversal; identical arithmetic and result)
 template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
-    k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps) {
+    k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps, int trigger) {
   pdl_wait();
+  if (trigger) pdl_trigger();
   const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   // reverse tile order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
@@ -760,19 +1098,22 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
 #pragma unroll
       for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
       constexpr int RB = rows_in_flight<GT, PT>();
+      const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
+      int64_t roff = (tl.r0 + tr) * T.cols + col;
       for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
         RowVec<VEC, GT, true> gr[RB];
         RowVec<VEC, PT, false> pr[RB];
+        int64_t o = roff;
 #pragma unroll
-        for (int b = 0; b < RB; ++b) {
-          const int64_t r = r0 + (int64_t)b * TR;
-          if (r < tl.r1) {
-            gr[b].load(g + r * T.cols + col, valid);
-            pr[b].load(p + r * T.cols + col, valid);
+        for (int b = 0; b < RB; ++b, o += rstep) {
+          if (r0 + (int64_t)b * TR < tl.r1) {
+            gr[b].load(g + o, valid);
+            pr[b].load(p + o, valid);
           }
         }
+        o = roff;
 #pragma unroll
-        for (int b = 0; b < RB; ++b) {
+        for (int b = 0; b < RB; ++b, o += rstep) {
           const int64_t r = r0 + (int64_t)b * TR;
           if (r < tl.r1) {
             const float a = c.fa[T.fa_off + r];
@@ -781,9 +1122,10 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
             pr[b].get(pv);
 #pragma unroll
             for (int j = 0; j < VW; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
-            store_p<VEC, PT>(p + r * T.cols + col, pv, valid);
+            store_p<VEC, PT>(p + o, pv, VEC ? VW : valid);
           }
         }
+        roff = o;
       }
     } else {
       const double s = c.glob[0];
@@ -821,12 +1163,25 @@ int grid_for(K kernel, int64_t ntiles, int device) {
   return (int)std::max<int64_t>(1, (ntiles + rounds - 1) / rounds);
 }
 
+// k6_tma: every tensor of the call starts 16 B aligned and spans a whole number of 16 B,
+// for parameters and gradients (bulk copies move 16 B units).
+bool k6_tma_ok(const AdaLomoPlan& pl, const AdaLomoCall& call, size_t gsz, size_t psz) {
+  for (int k = call.t0; k < call.t1; ++k) {
+    const TensorInfo& T = pl.h_tensors[k];
+    const int64_t off = call.single || call.ntab ? 0 : T.elem_off;
+    const uintptr_t pb = (uintptr_t)(call.ntab ? call.ptab[k - call.t0] : call.p) + off * psz;
+    const uintptr_t gb = (uintptr_t)(call.ntab ? call.gtab[k - call.t0] : call.g) + off * gsz;
+    if (pb % 16 || gb % 16 || (T.numel * psz) % 16 || (T.numel * gsz) % 16) return false;
+  }
+  return true;
+}
+
 template <bool VEC, typename GT, typename PT>
 void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaStream_t st) {
   Ctx c{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
         pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
         pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
-        pl.d_chunks,  pl.d_chunk_sc};
+        pl.d_chunks,  pl.d_chunk_sc, pl.d_fra,    pl.d_frb,     pl.d_mins};
   Ptrs P{};
   P.p = call.p;
   P.g = call.g;
@@ -846,18 +1201,31 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
   const int64_t sms = device_info(dev).sms;
 
   if (phase == 1) {  // pass 1 over {g, p} + reduction of the tile partials into the payload
-    auto kk1 = k1_stats<VEC, GT, PT>;
-    launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles);
+    const int mode = call.stats_mode ? call.stats_mode : kStatsAll;
+    auto go1 = [&](auto kk1) {
+      launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles,
+                 call.early);
+    };
+    if (mode == kStatsG)
+      go1(k1_stats<VEC, GT, PT, kStatsG>);
+    else if (mode == kStatsP)
+      go1(k1_stats<VEC, GT, PT, kStatsP>);
+    else
+      go1(k1_stats<VEC, GT, PT, kStatsAll>);
     launch_check("adalomo k1_stats");
     const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
-    const int ncolblk = (int)((ncols + 31) / 32);
+    const int ncolblk = (mode & kStatsG) ? (int)((ncols + 31) / 32) : 0;
+    // fused calls (no all-reduce between the phases): KR's scalar block does K2's work
     launch_pdl(kr_stats, ncolblk + 1, kThreads, st, c, call.t0, call.t1,
-               (const int64_t*)pl.d_col_off, ncols, ncolblk);
+               (const int64_t*)pl.d_col_off, ncols, ncolblk, mode, call.fuse_usq, call.lr,
+               cfg.beta2, call.use_clip, pl.grad_clip, call.ext_sumsq);
     launch_check("adalomo kr_stats");
   } else if (phase == 2) {  // scalars, moments, pass 2 over {g}
-    launch_pdl(k2_scalars, 1, 1024, st, c, call.t0, call.t1, call.lr, cfg.beta2, call.use_clip,
-               pl.grad_clip, call.ext_sumsq);
-    launch_check("adalomo k2_scalars");
+    if (!call.fuse_usq) {
+      launch_pdl(k2_scalars, 1, kThreads, st, c, call.t0, call.t1, call.lr, cfg.beta2,
+                 call.use_clip, pl.grad_clip, call.ext_sumsq);
+      launch_check("adalomo k2_scalars");
+    }
     const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
     if (nitems > 0) {
       const int64_t blocks = std::min<int64_t>((nitems + kThreads - 1) / kThreads, sms * 8);
@@ -866,31 +1234,55 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
       launch_check("adalomo k3_moments");
     }
     auto kk4 = k4_usq<VEC, GT>;
-    launch_pdl(kk4, grid_for(kk4, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.beta2,
-               cfg.eps);
+    // fused calls: K4's last CTA reduces sum u^2 and computes the damping (K5's work)
+    launch_pdl(kk4, grid_for(kk4, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.beta2,
+               cfg.eps, call.t0, call.t1, call.fuse_usq, cfg.adalomo_clip);
     launch_check("adalomo k4_usq");
     if (!call.fuse_usq) {
       launch_pdl(kr_usq, 1, 1024, st, c, call.t0, call.t1);
       launch_check("adalomo kr_usq");
     }
   } else {  // damping + pass 3 over {g, p -> p}
-    launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip, call.fuse_usq);
-    launch_check("adalomo k5_damp");
-    // K6 traversal: tiles for multi-tensor calls (the per-thread b_j and a_i loads
-    // amortise over a tile: 24.6 vs 25.4 ms on 7B), flat chunks for the one-tensor hook
-    // form (finer work items for one tensor: 32.4 vs 33.9 ms over the 7B tensors);
-    // MCO_ADALOMO_K6 = "tiles" / "chunks" forces one
+    if (!call.fuse_usq) {
+      launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip, 0);
+      launch_check("adalomo k5_damp");
+    }
+    // K6 traversal: the cp.async.bulk pipeline (k6_tma) whenever every tensor of the call
+    // is 16 B aligned and sized; else tiles for multi-tensor calls (the per-thread b_j and
+    // a_i loads amortise over a tile: 24.6 vs 25.4 ms on 7B) and flat chunks for the
+    // one-tensor hook form (finer work items for one tensor: 32.4 vs 33.9 ms over the 7B
+    // tensors).  MCO_ADALOMO_K6 = "tma" / "tiles" / "chunks" forces one (A/B knob).
     static const int k6_force = [] {
       const char* e = getenv("MCO_ADALOMO_K6");
-      return !e ? 0 : std::string(e) == "chunks" ? 2 : std::string(e) == "tiles" ? 1 : 0;
+      if (!e) return 0;
+      const std::string v(e);
+      return v == "tiles" ? 1 : v == "chunks" ? 2 : v == "tma" ? 3 : 0;
     }();
-    const bool k6_tiles = k6_force ? k6_force == 1 : !call.single;
-    if (k6_tiles) {
+    const bool tma_ok = VEC && k6_tma_ok(pl, call, sizeof(GT), sizeof(PT));
+    const int k6 = (k6_force == 3 || k6_force == 0) && tma_ok ? 3
+                   : k6_force == 1 || k6_force == 2          ? k6_force
+                   : call.single                             ? 2
+                                                             : 1;
+    if (k6 == 3) {
+      auto kk6 = k6_tma<GT, PT>;
+      constexpr int smem = k6_smem<GT, PT>();
+      static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
+      if (!(attr_set.load() & (1ull << dev))) {
+        MCO_CUDA_CHECK(cudaFuncSetAttribute(kk6, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_set.fetch_or(1ull << dev);
+      }
+      const int64_t nitems = nchunks * kK6PPC;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, nitems));
+      launch_pdl_smem(kk6, grid, kK6Consumers + 32, smem, st, c, P, chunk0, nchunks, cfg.eps,
+                      call.trigger);
+    } else if (k6 == 1) {
       auto kk6 = k6_update_tiles<VEC, GT, PT>;
-      launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps);
+      launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps,
+                 call.trigger);
     } else {
       auto kk6 = k6_update<VEC, GT, PT>;
-      launch_pdl(kk6, grid_for(kk6, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.eps);
+      launch_pdl(kk6, grid_for(kk6, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.eps,
+                 call.trigger);
     }
     launch_check("adalomo k6_update");
   }
@@ -928,6 +1320,13 @@ void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int ph
   } else {
     throw Error(MCO_CONTRACT, "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
   }
+}
+
+void launch_adalomo_gsumsq(const AdaLomoPlan& pl, int t0, int t1, double* out, cudaStream_t st) {
+  Ctx c{};
+  c.pay = pl.d_payload;
+  launch_pdl(kg_sumsq, 1, kThreads, st, c, t0, t1, out);
+  launch_check("adalomo kg_sumsq");
 }
 
 void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {

@@ -77,6 +77,9 @@ struct AdaLomoPlan {
   double* d_tens_sc = nullptr;
   float* d_fa = nullptr;
   float* d_fb = nullptr;
+  float* d_fra = nullptr;     // 1/sqrt(a_i), 1/sqrt(b_j): separable form of u
+  float* d_frb = nullptr;
+  unsigned* d_mins = nullptr;  // 2 per tensor: min a, min b (fp32 bits)
   double* d_glob = nullptr;
 };
 
@@ -92,7 +95,15 @@ struct AdaLomoCall {
   double lr;
   int use_clip;
   const double* ext_sumsq;  // device global sum g^2 (hook form), or null
-  int fuse_usq;  // phases run back to back: the usq payload is reduced inside K5
+  // phases run back to back (no all-reduce between them): KR's scalar block does K2's
+  // work and K4's last CTA K5's -- 5 launches per call instead of 7
+  int fuse_usq;
+  // phase 1 statistics: 0 / 3 all, 1 gradient statistics only, 2 sum p^2 only
+  int stats_mode;
+  // hook form, tensor after tensor on one stream: K6 triggers its dependents early and
+  // the next tensor's K1 starts without waiting (adalomo.cu k1_stats).  early may only be
+  // set when the previous kernel in the stream is a K6 of another tensor.
+  int trigger, early;
   // list form: tensor t0 + i lives at ptab[i] / gtab[i] (separate allocations, the
   // per-parameter tensors of a model); ntab = 0 -> flat buffers / single tensor
   int ntab;
@@ -108,5 +119,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
 void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase,
                           cudaStream_t st);
 void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st);
+// out = sum over tensors [t0, t1) of the payload's sum g^2, in K2's reduction order.
+void launch_adalomo_gsumsq(const AdaLomoPlan& pl, int t0, int t1, double* out, cudaStream_t st);
 
 }  // namespace mco

@@ -51,17 +51,23 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 
+// Explicit early trigger for one kernel (the hook-form K6, whose dependent is the next
+// tensor's K1 -- see adalomo.cu).
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 #ifndef MCO_PDL
 #define MCO_PDL 1
 #endif
 
 template <typename... KArgs, typename... Args>
-void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
-                Args... args) {
+void launch_pdl_smem(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                     cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -69,6 +75,11 @@ void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStrea
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   cuda_check(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...), "cudaLaunchKernelEx");
+}
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t st,
+                Args... args) {
+  launch_pdl_smem(kern, grid, block, 0, st, args...);
 }
 
 struct DeviceInfo {
@@ -325,6 +336,41 @@ __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
+}
+
+// Sums of N values (N = 1, 2, 4, 8) over the 32 lanes at once: the first log2 N
+// butterfly steps halve the values each lane carries (it keeps one half, its partner the
+// other), the remaining steps are a plain butterfly.  5 shuffles + (N-1) more instead of
+// 5 N.  Lane L ends with the sum for value index warp_rows_index<N>(L).  Fixed order:
+// deterministic.
+template <int N>
+__device__ __forceinline__ int warp_rows_index(int lane) {
+  int r = 0;
+#pragma unroll
+  for (int step = 0; (1 << step) < N; ++step) r = (r << 1) | ((lane >> (4 - step)) & 1);
+  return r;
+}
+template <int N>
+__device__ __forceinline__ float warp_sum_rows(const float (&v)[N]) {
+  const int lane = threadIdx.x & 31;
+  float w[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) w[i] = v[i];
+  int o = 16;
+#pragma unroll
+  for (int n = N; n > 1; n >>= 1, o >>= 1) {
+    const bool up = lane & o;
+    const int half = n >> 1;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? w[i] : w[i + half];
+      const float keep = up ? w[i + half] : w[i];
+      w[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (; o > 0; o >>= 1) w[0] += __shfl_xor_sync(0xffffffffu, w[0], o);
+  return w[0];
 }
 
 // Block sum in a fixed order (warp butterflies, then warp partials in warp

@@ -20,6 +20,7 @@
 #include <type_traits>
 
 #include "flat_tma.h"
+#include "tma.cuh"
 #include "update.cuh"
 
 namespace mco {
@@ -60,73 +61,6 @@ constexpr int stages() {
 template <class C, int KIND, bool MIXED>
 constexpr int smem_bytes() {
   return stages<C, KIND, MIXED>() * stage_bytes<C, KIND, MIXED>() + 2 * stages<C, KIND, MIXED>() * 8;
-}
-
-__device__ __forceinline__ uint32_t sa(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred P;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
-      " @!P bra WAIT_%=;\n}" ::"r"(sa(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-template <bool HINT>
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar, uint64_t pol) {
-  if constexpr (HINT)
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(sa(dst)),
-        "l"(src), "r"(bytes), "r"(sa(bar)), "l"(pol)
-        : "memory");
-  else
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
-        "[%3];" ::"r"(sa(dst)),
-        "l"(src), "r"(bytes), "r"(sa(bar))
-        : "memory");
-}
-template <bool HINT>
-__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t pol) {
-  if constexpr (HINT)
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
-                 ::"l"(dst), "r"(sa(src)), "r"(bytes), "l"(pol)
-                 : "memory");
-  else
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                 "r"(sa(src)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bulk_commit() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read_1() {
-  asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_all() {
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // consecutive threads read consecutive 16 B (8 B): conflict-free LDS.128 / LDS.64

@@ -2,7 +2,7 @@
 """Key metrics of an `ncu --set full` report (profiles/run_ncu_r02.sh step 2): time,
 DRAM bytes and achieved bandwidth against the measured copy peak, issue / warp
 activity, registers, and the top-3 warp stall reasons (cycles per issued instruction).
-usage: summarize_full_r02.py gpurun_out/prof_r02.ncu-rep [hbm_gbs] > profiles/ncu_full_r02.md"""
+usage: summarize_full_r02.py gpurun_out/prof_r02.ncu-rep|ncu_raw_r02.csv.gz [hbm_gbs] > profiles/ncu_full_r02.md"""
 import csv
 import io
 import re
@@ -11,8 +11,13 @@ import sys
 
 rep = sys.argv[1]
 peak = float(sys.argv[2]) if len(sys.argv) > 2 else 6540.5
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True, check=True).stdout
+if rep.endswith(".csv.gz"):  # the raw page exported on the box (run_ncu_r02.sh)
+    import gzip
+
+    raw = gzip.open(rep, "rt").read()
+else:
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True, check=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h, units, data = rows[0], rows[1], rows[2:]
 
@@ -27,7 +32,8 @@ def val(r, key, scale=1.0):
         return None
     u = units[h.index(key)]
     mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9,
-            "usecond": 1e-6, "msecond": 1e-3, "second": 1.0}.get(u, 1.0)
+            "usecond": 1e-6, "msecond": 1e-3, "second": 1.0, "ns": 1e-9, "us": 1e-6,
+            "ms": 1e-3, "s": 1.0}.get(u, 1.0)
     return x * mult * scale
 
 
@@ -51,5 +57,5 @@ for r in data:
     wa = val(r, "sm__warps_active.avg.pct_of_peak_sustained_active")
     regs = r[h.index("launch__registers_per_thread")] if "launch__registers_per_thread" in h else "-"
     grid = r[h.index("launch__grid_size")] if "launch__grid_size" in h else "-"
-    print(f"| `{name}` | {t * 1e3:.3f} ms | {(rd + wr) / 1e9:.3f} GB | {gbs:.0f} | "
+    print(f"| `{name}` | {t * 1e6:.1f} us | {(rd + wr) / 1e9:.3f} GB | {gbs:.0f} | "
           f"{gbs / peak:.3f} | {ia:.1f} | {wa:.1f} | {regs} | {grid} | {st} |")

@@ -19,7 +19,8 @@ KIND_OF = [("flat_tma_kernel<0,", "adamw"), ("flat_tma_kernel<1,", "lion"),
            ("flat_tma_kernel<2,", "adan"), ("flat_tma_kernel<3,", "sophia"),
            ("flat_step_kernel<0,", "adamw"), ("flat_step_kernel<1,", "lion"),
            ("flat_step_kernel<2,", "adan"), ("flat_step_kernel<3,", "sophia"),
-           ("lomo_kernel", "lomo"), ("lomo_tma_kernel", "lomo"), ("k1_stats", "adalomo"), ("k2_scalars", "adalomo"),
+           ("lomo_kernel", "lomo"), ("lomo_tma_kernel", "lomo"), ("sumsq_kernel", "lomo"),
+           ("k1_stats", "adalomo"), ("kr_stats", "adalomo"), ("k2_scalars", "adalomo"),
            ("k3_moments", "adalomo"), ("k4_usq", "adalomo"), ("k5_damp", "adalomo"),
            ("k6_update", "adalomo")]
 
