@@ -48,7 +48,7 @@ mco_status mco_adalomo_create(const mco_config* cfg, int ntensors, const int* nd
     alloc(&pl.d_fra, pl.fa_len, sizeof(float));
     alloc(&pl.d_frb, pl.fb_len, sizeof(float));
     alloc(&pl.d_mins, 2 * pl.h_tensors.size(), sizeof(unsigned));
-    alloc(&pl.d_glob, 4, sizeof(double));
+    alloc(&pl.d_glob, 6, sizeof(double));  // s, G, host-clip sum, K4 / KR tickets
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_tiles, pl.h_tiles.data(), pl.h_tiles.size() * sizeof(Tile),
                               cudaMemcpyHostToDevice));
     MCO_CUDA_CHECK(cudaMemcpy(pl.d_chunks, pl.h_chunks.data(),

@@ -36,7 +36,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <string>
+#include <type_traits>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "adalomo.h"
 #include "tma.cuh"
@@ -240,6 +243,11 @@ struct Ptrs {
   int single;  // 1: p / g point at the call's only tensor
   int ntab;    // > 0: tensor t0 + i at ptab[i] / gtab[i] (list form)
   int t0;
+  // calls mixing tensors that take the vector path with tensors that cannot (odd column
+  // counts, rows off the 8-element grid): 1 = this launch takes only the vector-path
+  // tensors, 2 = only the others, 0 = every tensor (the call is uniform)
+  int filt;
+  int psz, gsz;  // element bytes of the parameters / gradients
   void* ptab[kMaxTab];
   const void* gtab[kMaxTab];
 };
@@ -252,6 +260,23 @@ template <typename PT>
 __device__ __forceinline__ PT* pptr(const Ptrs& P, const TensorInfo& T, int k) {
   if (P.ntab) return (PT*)P.ptab[k - P.t0];
   return (PT*)P.p + (P.single ? 0 : T.elem_off);
+}
+
+// Vector-path eligibility of tensor k, as the host decides it (launch_adalomo_phase):
+// 1-D tensors run element loops on either path; a matrix needs C % 8 == 0 and its
+// parameter and gradient rows at 8-element-aligned addresses.  A mixed call launches
+// every tiled pass twice (VEC instance with filt 1, scalar instance with filt 2) and each
+// tile is taken by exactly one of them -- same tiles, same arithmetic, same order.
+__device__ __forceinline__ bool skip_tensor(const Ptrs& P, const TensorInfo& T, int k) {
+  if (!P.filt) return false;
+  bool v = true;
+  if (T.factored) {
+    const int64_t off = P.single ? 0 : T.elem_off;
+    const uintptr_t pb = P.ntab ? (uintptr_t)P.ptab[k - P.t0] : (uintptr_t)P.p + off * P.psz;
+    const uintptr_t gb = P.ntab ? (uintptr_t)P.gtab[k - P.t0] : (uintptr_t)P.g + off * P.gsz;
+    v = T.cols % 8 == 0 && pb % (8 * P.psz) == 0 && gb % (8 * P.gsz) == 0;
+  }
+  return v != (P.filt == 1);
 }
 
 // ============================ K1: statistics =====================================
@@ -278,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
+    if (skip_tensor(P, T, tl.tensor)) continue;
     const GT* g = gptr<GT>(P, T, tl.tensor);
     const PT* p = pptr<PT>(P, T, tl.tensor);
     double psq = 0.0, gsq = 0.0;
@@ -397,6 +423,27 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
   if (early) pdl_wait();
 }
 
+// One lane's (thread's) share of a strided fixed-order sum: x(i0) + x(i0 + stride) + ...
+// over [i0, end), added in that order, with the loads issued 8 at a time so their
+// latencies overlap (a one-tensor call reduces ~450 tile partials per tensor in one warp:
+// 14 dependent L2 round trips per lane before).  The padding adds +0.0, which leaves
+// every sum here (of squares / of non-negative statistics) bit-unchanged.
+template <typename F>
+__device__ __forceinline__ double strided_sum(int64_t i0, int64_t end, int64_t stride, F x) {
+  double acc = 0.0;
+  for (int64_t i = i0; i < end; i += 8 * stride) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = i + q * stride;
+      v[q] = j < end ? x(j) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc += v[q];
+  }
+  return acc;
+}
+
 // K2's / K5's work, also run inside KR / K4 by unsharded (fused) calls
 __device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
                         double clip, const double* ext_sumsq, double* red);
@@ -404,10 +451,32 @@ __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip);
 
 // ============================ KR: tile partials -> payload ===========================
 // Blocks [0, ncolblk): one thread per column of the factored tensors in [t0,t1):
-// fixed-order sum of the tile column partials.  Block ncolblk: one warp per
-// tensor, fixed-order sums of the tile scalars.  Everything is scaled by the
-// tensor's shard weight (1, or 0 on ranks that hold a replica another rank
-// already contributes), so an all-reduce of the payload yields global sums.
+// fixed-order sum of the tile column partials.  Blocks ncolblk + i: tensor t0 + i's
+// tile scalars (sum p^2, g^2, v_row_old), 256 thread-strided partials in a block_sum --
+// one block per tensor, so a one-tensor call (hook form) reduces its ~450 tiles with
+// 256 threads instead of one warp (KR 11.3 us -> see DESIGN.md), and every form of the
+// call sums a tensor in the same order.  Everything is scaled by the tensor's shard
+// weight (1, or 0 on ranks that hold a replica another rank already contributes), so an
+// all-reduce of the payload yields global sums.  fuse2 (no all-reduce between the
+// phases): the last tensor block to finish (ticket) runs K2's body for the call.
+__device__ __forceinline__ void tensor_stats(const Ctx& c, int k, int mode, double* red) {
+  const TensorInfo T = c.tensors[k];
+  const int64_t i0 = T.tile_begin + threadIdx.x;
+  double ps = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 0]; });
+  double gs = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 1]; });
+  double vr = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 2]; });
+  ps = block_sum(ps, red);
+  gs = block_sum(gs, red);
+  vr = block_sum(vr, red);
+  if (threadIdx.x == 0) {
+    if (mode & kStatsG) {
+      c.pay[k * 3 + 0] = T.weight * gs;
+      c.pay[k * 3 + 2] = T.weight * vr;
+    }
+    if (mode & kStatsP) c.pay[k * 3 + 1] = T.weight * ps;
+  }
+}
+
 __global__ void __launch_bounds__(kThreads)
     kr_stats(Ctx c, int t0, int t1, const int64_t* __restrict__ col_off, int64_t ncols,
              int ncolblk, int mode, int fuse2, double lr, double b2, int use_clip, double clip,
@@ -438,7 +507,7 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t j = gi - col_off[lo];
       const float* src = c.colpart + T.colpart_off + j;
       const int64_t nrb = T.nrb, C = T.cols;
-      for (int64_t rb = warp; rb < nrb; rb += nw) acc += (double)src[rb * C];
+      acc = strided_sum(warp, nrb, nw, [&](int64_t rb) { return (double)src[rb * C]; });
       slot = 3 * c.ntens + T.fb_off + j;
       w = T.weight;
     }
@@ -451,29 +520,21 @@ __global__ void __launch_bounds__(kThreads)
     }
     return;
   }
-  for (int k = t0 + warp; k < t1; k += nw) {
-    const TensorInfo T = c.tensors[k];
-    double ps = 0, gs = 0, vr = 0;
-    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) {
-      ps += c.tile_sc[i * 4 + 0];
-      gs += c.tile_sc[i * 4 + 1];
-      vr += c.tile_sc[i * 4 + 2];
+  __shared__ double red[32];
+  tensor_stats(c, t0 + (int)blockIdx.x - ncolblk, mode, red);
+  if (fuse2) {  // unsharded call: the last tensor block does K2's work
+    __shared__ bool last;
+    unsigned* ticket = reinterpret_cast<unsigned*>(c.glob + 4);
+    if (threadIdx.x == 0) {
+      __threadfence();
+      last = atomicAdd(ticket, 1u) == (unsigned)(t1 - t0) - 1;
     }
-    ps = warp_sum(ps);
-    gs = warp_sum(gs);
-    vr = warp_sum(vr);
-    if (lane == 0) {
-      if (mode & kStatsG) {
-        c.pay[k * 3 + 0] = T.weight * gs;
-        c.pay[k * 3 + 2] = T.weight * vr;
-      }
-      if (mode & kStatsP) c.pay[k * 3 + 1] = T.weight * ps;
-    }
-  }
-  if (fuse2) {  // unsharded call: nothing to all-reduce, K2's work follows in this block
-    __shared__ double red[32];
     __syncthreads();
-    k2_body(c, t0, t1, lr, b2, use_clip, clip, ext_sumsq, red);
+    if (last) {
+      __threadfence();
+      k2_body(c, t0, t1, lr, b2, use_clip, clip, ext_sumsq, red);
+      if (threadIdx.x == 0) *ticket = 0u;
+    }
   }
 }
 
@@ -481,8 +542,9 @@ __device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int k = t0 + warp; k < t1; k += nw) {
     const TensorInfo T = c.tensors[k];
-    double us = 0;  // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
-    for (int64_t i = T.tile_begin + lane; i < T.tile_end; i += 32) us += __ldcg(&c.tile_sc[i * 4 + 3]);
+    // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
+    double us = strided_sum(T.tile_begin + lane, T.tile_end, 32,
+                            [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); });
     us = warp_sum(us);
     if (lane == 0) c.pay_usq[k] = T.weight * us;
   }
@@ -513,10 +575,11 @@ __global__ void __launch_bounds__(kThreads) kg_sumsq(Ctx c, int t0, int t1, doub
 __device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
                         double clip, const double* ext_sumsq, double* red) {
   // per-tensor sums arrive (already all-reduced across ranks when sharded) in the payload
+  // (L2 reads: in fused calls other blocks of the same grid wrote them, kr_stats)
   for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
-    c.tens_sc[k * kTensScalars + TS_GSQ] = c.pay[k * 3 + 0];
-    c.tens_sc[k * kTensScalars + TS_PSQ] = c.pay[k * 3 + 1];
-    c.tens_sc[k * kTensScalars + TS_VRS] = c.pay[k * 3 + 2];
+    c.tens_sc[k * kTensScalars + TS_GSQ] = __ldcg(&c.pay[k * 3 + 0]);
+    c.tens_sc[k * kTensScalars + TS_PSQ] = __ldcg(&c.pay[k * 3 + 1]);
+    c.tens_sc[k * kTensScalars + TS_VRS] = __ldcg(&c.pay[k * 3 + 2]);
   }
   __syncthreads();
   double G = 0;
@@ -700,6 +763,7 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
+    if (skip_tensor(P, T, tl.tensor)) continue;
     const GT* g = gptr<GT>(P, T, tl.tensor);
     double usq = 0.0;
     if (T.factored) {
@@ -832,6 +896,7 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t ci = nchunks - 1 - k;
     const Chunk ch = c.chunks[chunk0 + ci];
     const TensorInfo T = c.tensors[ch.tensor];
+    if (skip_tensor(P, T, ch.tensor)) continue;
     const GT* g = gptr<GT>(P, T, ch.tensor);
     PT* p = pptr<PT>(P, T, ch.tensor);
     const double f = c.tens_sc[ch.tensor * kTensScalars + TS_F];
@@ -1084,6 +1149,7 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
     const int64_t ti = ntiles - 1 - k;
     const Tile tl = c.tiles[tile0 + ti];
     const TensorInfo T = c.tensors[tl.tensor];
+    if (skip_tensor(P, T, tl.tensor)) continue;
     const GT* g = gptr<GT>(P, T, tl.tensor);
     PT* p = pptr<PT>(P, T, tl.tensor);
     const double f = c.tens_sc[tl.tensor * kTensScalars + TS_F];
@@ -1139,6 +1205,150 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
   }
 }
 
+// ============================ one small 1-D tensor, one launch =======================
+// The hook form of a norm weight (LLaMA: 4096-8192 elements, 65 of the 7B set's 291
+// tensors) ran the 4-launch chain K1 -> KR(K2) -> K4(K5) -> K6 for ~20 KB of data.
+// One thread-block cluster (one CTA of 256 threads per plan tile, up to 8 CTAs; a CTA
+// takes tiles rank, rank + 8, ...) now runs the whole chain in one launch, with cluster
+// barriers where the chain had kernel boundaries and the tile sums gathered in CTA 0's
+// shared memory over DSMEM.  It reproduces the chain operation for operation -- each
+// tile's block_sum in a 256-thread CTA as K1 / K4 do, KR's tensor_stats and K2's body in
+// CTA 0 with 256 threads, usq_payload's lane-strided warp sum, K5's body -- so its bits
+// equal the multi-kernel path's, which every other form shares.  (A first version on
+// one 1024-thread CTA was issue-latency-bound on one SM: 22 us per call.)
+constexpr int kSmallTiles = 32, kSmallCluster = 8, kSmallPer = kSmallTiles / kSmallCluster;
+
+template <typename GT, typename PT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_small_vec(Ctx c, Ptrs P, int k, double lr, double b2, double eps, int use_clip,
+                double clip, const double* ext_sumsq, double adalomo_clip, int trigger) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  __shared__ double red[32];
+  __shared__ double sc[3][kSmallTiles];  // CTA 0: per tile sum p^2, sum g^2, sum u^2
+  __shared__ double bc[3];               // s, corr, f from CTA 0
+  pdl_wait();
+  if (trigger) pdl_trigger();  // the next tensor's K1 may start (see k1_stats)
+  const TensorInfo T = c.tensors[k];
+  const GT* g = gptr<GT>(P, T, k);
+  PT* p = pptr<PT>(P, T, k);
+  const int nt = (int)(T.tile_end - T.tile_begin);
+  double* sc0 = cl.map_shared_rank(&sc[0][0], 0);
+  // every load first: this thread's element of each of the CTA's tiles
+  float gv[kSmallPer], pv[kSmallPer];
+  double vv[kSmallPer];
+  int64_t ev[kSmallPer];
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    const int ti = rank + q * cs;
+    ev[q] = -1;
+    if (ti < nt) {
+      const Tile tl = c.tiles[T.tile_begin + ti];
+      const int64_t e = tl.r0 + threadIdx.x;
+      if (e < tl.r1) ev[q] = e;
+    }
+    gv[q] = ev[q] >= 0 ? ld1(g + ev[q]) : 0.f;
+    pv[q] = ev[q] >= 0 ? ldp1(p + ev[q]) : 0.f;
+    vv[q] = ev[q] >= 0 ? c.state[T.vfull_off + ev[q]] : 0.0;
+  }
+  // K1 (1-D branch): per tile sum p^2, sum g^2 -> CTA 0
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    const int ti = rank + q * cs;
+    if (ti >= nt) break;  // uniform in the CTA
+    double gsq = 0.0, psq = 0.0;
+    if (ev[q] >= 0) {
+      const double g1 = (double)gv[q], p1 = (double)pv[q];
+      gsq += g1 * g1;
+      psq += p1 * p1;
+    }
+    const double bps = block_sum(psq, red);
+    const double bgs = block_sum(gsq, red);
+    if (threadIdx.x == 0) {
+      sc0[ti] = bps;
+      sc0[kSmallTiles + ti] = bgs;
+    }
+  }
+  cl.sync();
+  if (rank == 0) {  // KR's tensor block + K2
+    double ps = strided_sum(threadIdx.x, nt, kThreads, [&](int64_t i) { return sc[0][i]; });
+    double gs = strided_sum(threadIdx.x, nt, kThreads, [&](int64_t i) { return sc[1][i]; });
+    double vr = strided_sum(threadIdx.x, nt, kThreads, [&](int64_t) { return 0.0; });
+    ps = block_sum(ps, red);
+    gs = block_sum(gs, red);
+    vr = block_sum(vr, red);
+    if (threadIdx.x == 0) {
+      c.pay[k * 3 + 0] = T.weight * gs;
+      c.pay[k * 3 + 2] = T.weight * vr;
+      c.pay[k * 3 + 1] = T.weight * ps;
+    }
+    __syncthreads();
+    k2_body(c, k, k + 1, lr, b2, use_clip, clip, ext_sumsq, red);
+    __syncthreads();
+    if (threadIdx.x < cs) {
+      double* dst = cl.map_shared_rank(&bc[0], (int)threadIdx.x);
+      dst[0] = c.glob[0];
+      dst[1] = c.tens_sc[k * kTensScalars + TS_CORR];
+    }
+  }
+  cl.sync();
+  const double s = bc[0], corr = bc[1];
+  // K4 (1-D branch): v_full EMA, per tile sum u^2 -> CTA 0
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    const int ti = rank + q * cs;
+    if (ti >= nt) break;
+    double usq = 0.0;
+    if (ev[q] >= 0) {
+      const double gs = s * (double)gv[q];
+      double v = vv[q];
+      v = b2 * v + (1 - b2) * gs * gs;
+      c.state[T.vfull_off + ev[q]] = v;
+      vv[q] = v;
+      const double u = gs / sqrt(v / corr + eps);
+      usq += u * u;
+    }
+    const double bu = block_sum(usq, red);
+    if (threadIdx.x == 0) sc0[2 * kSmallTiles + ti] = bu;
+  }
+  cl.sync();
+  if (rank == 0) {  // usq_payload + K5
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      double us = strided_sum(lane, nt, 32, [&](int64_t i) { return sc[2][i]; });
+      us = warp_sum(us);
+      if (lane == 0) c.pay_usq[k] = T.weight * us;
+    }
+    __syncthreads();
+    k5_body(c, k, k + 1, adalomo_clip);
+    __syncthreads();
+    if (threadIdx.x < cs)
+      cl.map_shared_rank(&bc[0], (int)threadIdx.x)[2] = c.tens_sc[k * kTensScalars + TS_F];
+  }
+  cl.sync();
+  const double f = bc[2];
+  // K6 (1-D branch)
+#pragma unroll
+  for (int q = 0; q < kSmallPer; ++q) {
+    if (ev[q] >= 0) {
+      const double gs = s * (double)gv[q];
+      const double u = gs / sqrt(vv[q] / corr + eps);
+      stp1(p + ev[q], (float)((double)pv[q] - f * u));
+    }
+  }
+}
+
+// The small path applies to a 1-D tensor whose plan tiles all hold <= 256 elements and
+// number <= kSmallTiles (vector_chunk gives 256-element tiles up to 2 * 256 * SMs).
+bool small_vec_ok(const AdaLomoPlan& pl, int k) {
+  const TensorInfo& T = pl.h_tensors[k];
+  if (T.factored || T.numel == 0 || T.tile_end - T.tile_begin > kSmallTiles) return false;
+  for (int64_t i = T.tile_begin; i < T.tile_end; ++i)
+    if (pl.h_tiles[i].r1 - pl.h_tiles[i].r0 > 256) return false;
+  return true;
+}
+
 template <typename K>
 int grid_for(K kernel, int64_t ntiles, int device) {
   static std::mutex mu;
@@ -1176,115 +1386,131 @@ bool k6_tma_ok(const AdaLomoPlan& pl, const AdaLomoCall& call, size_t gsz, size_
   return true;
 }
 
-template <bool VEC, typename GT, typename PT>
-void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaStream_t st) {
-  Ctx c{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
-        pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
-        pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
-        pl.d_chunks,  pl.d_chunk_sc, pl.d_fra,    pl.d_frb,     pl.d_mins};
-  Ptrs P{};
-  P.p = call.p;
-  P.g = call.g;
-  P.single = call.single;
-  P.ntab = call.ntab;
-  P.t0 = call.t0;
-  for (int i = 0; i < call.ntab; ++i) {
-    P.ptab[i] = call.ptab[i];
-    P.gtab[i] = call.gtab[i];
-  }
-  const int dev = current_device();
-  const int64_t tile0 = pl.h_tensors[call.t0].tile_begin;
-  const int64_t ntiles = pl.h_tensors[call.t1 - 1].tile_end - tile0;
-  const int64_t chunk0 = pl.h_tensors[call.t0].chunk_begin;
-  const int64_t nchunks = pl.h_tensors[call.t1 - 1].chunk_end - chunk0;
-  const auto& cfg = pl.cfg;
-  const int64_t sms = device_info(dev).sms;
+// Launch state shared by one phase's kernels.
+struct Launch {
+  Ctx c;
+  Ptrs P;
+  int dev;
+  int64_t tile0, ntiles, chunk0, nchunks, sms;
+};
 
-  if (phase == 1) {  // pass 1 over {g, p} + reduction of the tile partials into the payload
-    const int mode = call.stats_mode ? call.stats_mode : kStatsAll;
-    auto go1 = [&](auto kk1) {
-      launch_pdl(kk1, grid_for(kk1, ntiles, dev), kThreads, st, c, P, tile0, ntiles,
-                 call.early);
-    };
-    if (mode == kStatsG)
-      go1(k1_stats<VEC, GT, PT, kStatsG>);
-    else if (mode == kStatsP)
-      go1(k1_stats<VEC, GT, PT, kStatsP>);
-    else
-      go1(k1_stats<VEC, GT, PT, kStatsAll>);
-    launch_check("adalomo k1_stats");
-    const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
-    const int ncolblk = (mode & kStatsG) ? (int)((ncols + 31) / 32) : 0;
-    // fused calls (no all-reduce between the phases): KR's scalar block does K2's work
-    launch_pdl(kr_stats, ncolblk + 1, kThreads, st, c, call.t0, call.t1,
-               (const int64_t*)pl.d_col_off, ncols, ncolblk, mode, call.fuse_usq, call.lr,
-               cfg.beta2, call.use_clip, pl.grad_clip, call.ext_sumsq);
-    launch_check("adalomo kr_stats");
-  } else if (phase == 2) {  // scalars, moments, pass 2 over {g}
-    if (!call.fuse_usq) {
-      launch_pdl(k2_scalars, 1, kThreads, st, c, call.t0, call.t1, call.lr, cfg.beta2,
-                 call.use_clip, pl.grad_clip, call.ext_sumsq);
-      launch_check("adalomo k2_scalars");
+Launch make_launch(const AdaLomoPlan& pl, const AdaLomoCall& call) {
+  Launch L{};
+  L.c = Ctx{pl.d_tiles,   pl.d_tensors, pl.d_state, pl.d_colpart, pl.d_rowpart,
+            pl.d_tile_sc, pl.d_tens_sc, pl.d_fa,    pl.d_fb,      pl.d_glob,
+            pl.d_payload, pl.d_payload + pl.stats_len, (int64_t)pl.h_tensors.size(),
+            pl.d_chunks,  pl.d_chunk_sc, pl.d_fra,    pl.d_frb,     pl.d_mins};
+  L.P.p = call.p;
+  L.P.g = call.g;
+  L.P.single = call.single;
+  L.P.ntab = call.ntab;
+  L.P.t0 = call.t0;
+  L.P.filt = 0;
+  L.P.psz = call.p_dtype == MCO_BF16 ? 2 : 4;
+  L.P.gsz = call.g_dtype == MCO_BF16 ? 2 : 4;
+  for (int i = 0; i < call.ntab; ++i) {
+    L.P.ptab[i] = call.ptab[i];
+    L.P.gtab[i] = call.gtab[i];
+  }
+  L.dev = current_device();
+  L.tile0 = pl.h_tensors[call.t0].tile_begin;
+  L.ntiles = pl.h_tensors[call.t1 - 1].tile_end - L.tile0;
+  L.chunk0 = pl.h_tensors[call.t0].chunk_begin;
+  L.nchunks = pl.h_tensors[call.t1 - 1].chunk_end - L.chunk0;
+  L.sms = device_info(L.dev).sms;
+  return L;
+}
+
+// pass 1 over {g, p}
+template <bool VEC, typename GT, typename PT>
+void launch_k1(Launch L, const AdaLomoCall& call, int filt, cudaStream_t st) {
+  L.P.filt = filt;
+  const int mode = call.stats_mode ? call.stats_mode : kStatsAll;
+  auto go1 = [&](auto kk1) {
+    launch_pdl(kk1, grid_for(kk1, L.ntiles, L.dev), kThreads, st, L.c, L.P, L.tile0, L.ntiles,
+               call.early);
+  };
+  if (mode == kStatsG)
+    go1(k1_stats<VEC, GT, PT, kStatsG>);
+  else if (mode == kStatsP)
+    go1(k1_stats<VEC, GT, PT, kStatsP>);
+  else
+    go1(k1_stats<VEC, GT, PT, kStatsAll>);
+  launch_check("adalomo k1_stats");
+}
+
+// pass 2 over {g}; fuse5: K4's last CTA reduces sum u^2 and computes the damping
+template <bool VEC, typename GT, typename PT>
+void launch_k4(Launch L, const AdaLomoPlan& pl, const AdaLomoCall& call, int filt, int fuse5,
+               cudaStream_t st) {
+  L.P.filt = filt;
+  auto kk4 = k4_usq<VEC, GT>;
+  launch_pdl(kk4, grid_for(kk4, L.ntiles, L.dev), kThreads, st, L.c, L.P, L.tile0, L.ntiles,
+             pl.cfg.beta2, pl.cfg.eps, call.t0, call.t1, fuse5, pl.cfg.adalomo_clip);
+  launch_check("adalomo k4_usq");
+}
+
+// pass 3 over {g, p -> p}
+template <bool VEC, typename GT, typename PT>
+void launch_k6(Launch L, const AdaLomoPlan& pl, const AdaLomoCall& call, int filt,
+               cudaStream_t st) {
+  L.P.filt = filt;
+  // K6 traversal: tiles for multi-tensor calls (the per-thread b_j and a_i loads
+  // amortise over a tile) and flat chunks for the one-tensor hook form (finer work items
+  // for one tensor).  The cp.async.bulk pipeline (k6_tma, 16 B aligned / sized tensors
+  // only) measured slower on every form (same box, 7B: multi-tensor 27.5 vs 25.1 ms,
+  // bf16 18.8 vs 14.1, hook form 33.6 vs 31.2) and is opt-in.
+  // MCO_ADALOMO_K6 = "tma" / "tiles" / "chunks" forces one (A/B knob).
+  static const int k6_force = [] {
+    const char* e = getenv("MCO_ADALOMO_K6");
+    if (!e) return 0;
+    const std::string v(e);
+    return v == "tiles" ? 1 : v == "chunks" ? 2 : v == "tma" ? 3 : 0;
+  }();
+  const bool tma_ok = VEC && !filt && k6_tma_ok(pl, call, sizeof(GT), sizeof(PT));
+  const int k6 = k6_force == 3 && tma_ok               ? 3
+                 : k6_force == 1 || k6_force == 2      ? k6_force
+                 : call.single                         ? 2
+                                                       : 1;
+  const double eps = pl.cfg.eps;
+  if (k6 == 3) {
+    auto kk6 = k6_tma<GT, PT>;
+    constexpr int smem = k6_smem<GT, PT>();
+    static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
+    if (!(attr_set.load() & (1ull << L.dev))) {
+      MCO_CUDA_CHECK(cudaFuncSetAttribute(kk6, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      attr_set.fetch_or(1ull << L.dev);
     }
-    const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
-    if (nitems > 0) {
-      const int64_t blocks = std::min<int64_t>((nitems + kThreads - 1) / kThreads, sms * 8);
-      launch_pdl(k3_moments, (unsigned)blocks, kThreads, st, c, call.t0, call.t1,
-                 (const int64_t*)pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
-      launch_check("adalomo k3_moments");
-    }
-    auto kk4 = k4_usq<VEC, GT>;
-    // fused calls: K4's last CTA reduces sum u^2 and computes the damping (K5's work)
-    launch_pdl(kk4, grid_for(kk4, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.beta2,
-               cfg.eps, call.t0, call.t1, call.fuse_usq, cfg.adalomo_clip);
-    launch_check("adalomo k4_usq");
-    if (!call.fuse_usq) {
-      launch_pdl(kr_usq, 1, 1024, st, c, call.t0, call.t1);
-      launch_check("adalomo kr_usq");
-    }
-  } else {  // damping + pass 3 over {g, p -> p}
-    if (!call.fuse_usq) {
-      launch_pdl(k5_damp, 1, 1024, st, c, call.t0, call.t1, cfg.adalomo_clip, 0);
-      launch_check("adalomo k5_damp");
-    }
-    // K6 traversal: the cp.async.bulk pipeline (k6_tma) whenever every tensor of the call
-    // is 16 B aligned and sized; else tiles for multi-tensor calls (the per-thread b_j and
-    // a_i loads amortise over a tile: 24.6 vs 25.4 ms on 7B) and flat chunks for the
-    // one-tensor hook form (finer work items for one tensor: 32.4 vs 33.9 ms over the 7B
-    // tensors).  MCO_ADALOMO_K6 = "tma" / "tiles" / "chunks" forces one (A/B knob).
-    static const int k6_force = [] {
-      const char* e = getenv("MCO_ADALOMO_K6");
-      if (!e) return 0;
-      const std::string v(e);
-      return v == "tiles" ? 1 : v == "chunks" ? 2 : v == "tma" ? 3 : 0;
-    }();
-    const bool tma_ok = VEC && k6_tma_ok(pl, call, sizeof(GT), sizeof(PT));
-    const int k6 = (k6_force == 3 || k6_force == 0) && tma_ok ? 3
-                   : k6_force == 1 || k6_force == 2          ? k6_force
-                   : call.single                             ? 2
-                                                             : 1;
-    if (k6 == 3) {
-      auto kk6 = k6_tma<GT, PT>;
-      constexpr int smem = k6_smem<GT, PT>();
-      static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
-      if (!(attr_set.load() & (1ull << dev))) {
-        MCO_CUDA_CHECK(cudaFuncSetAttribute(kk6, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_set.fetch_or(1ull << dev);
-      }
-      const int64_t nitems = nchunks * kK6PPC;
-      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(sms, nitems));
-      launch_pdl_smem(kk6, grid, kK6Consumers + 32, smem, st, c, P, chunk0, nchunks, cfg.eps,
-                      call.trigger);
-    } else if (k6 == 1) {
-      auto kk6 = k6_update_tiles<VEC, GT, PT>;
-      launch_pdl(kk6, grid_for(kk6, ntiles, dev), kThreads, st, c, P, tile0, ntiles, cfg.eps,
-                 call.trigger);
-    } else {
-      auto kk6 = k6_update<VEC, GT, PT>;
-      launch_pdl(kk6, grid_for(kk6, nchunks, dev), kThreads, st, c, P, chunk0, nchunks, cfg.eps,
-                 call.trigger);
-    }
-    launch_check("adalomo k6_update");
+    const int64_t nitems = L.nchunks * kK6PPC;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(L.sms, nitems));
+    launch_pdl_smem(kk6, grid, kK6Consumers + 32, smem, st, L.c, L.P, L.chunk0, L.nchunks, eps,
+                    call.trigger);
+  } else if (k6 == 1) {
+    auto kk6 = k6_update_tiles<VEC, GT, PT>;
+    launch_pdl(kk6, grid_for(kk6, L.ntiles, L.dev), kThreads, st, L.c, L.P, L.tile0, L.ntiles,
+               eps, call.trigger);
+  } else {
+    auto kk6 = k6_update<VEC, GT, PT>;
+    launch_pdl(kk6, grid_for(kk6, L.nchunks, L.dev), kThreads, st, L.c, L.P, L.chunk0,
+               L.nchunks, eps, call.trigger);
+  }
+  launch_check("adalomo k6_update");
+}
+
+// f(vec_tag, gt_tag, pt_tag) for the call's dtype pair, VEC = vec
+template <typename F>
+void with_types(const AdaLomoCall& call, bool vec, F&& f) {
+  using T = std::true_type;
+  using N = std::false_type;
+  // (params, grads): (f32, f32), (f32, bf16), (bf16, bf16)
+  if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_F32) {
+    vec ? f(T{}, float{}, float{}) : f(N{}, float{}, float{});
+  } else if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_BF16) {
+    vec ? f(T{}, uint16_t{}, float{}) : f(N{}, uint16_t{}, float{});
+  } else if (call.p_dtype == MCO_BF16 && call.g_dtype == MCO_BF16) {
+    vec ? f(T{}, uint16_t{}, uint16_t{}) : f(N{}, uint16_t{}, uint16_t{});
+  } else {
+    throw Error(MCO_CONTRACT, "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
   }
 }
 
@@ -1293,34 +1519,86 @@ void run_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase, cudaSt
 void launch_adalomo_phase(const AdaLomoPlan& pl, const AdaLomoCall& call, int phase,
                           cudaStream_t st) {
   if (call.t1 <= call.t0) return;
-  // vector path: every factored tensor in the call has C % 8 == 0 and rows aligned to
-  // 8 elements of their type (32 B f32, 16 B bf16) for both params and grads.
+  // vector path, per tensor: a factored tensor needs C % 8 == 0 and rows aligned to 8
+  // elements of their type (32 B f32, 16 B bf16) for both params and grads (skip_tensor
+  // is the device-side twin).  A call whose tensors all agree runs one instance of each
+  // pass; a mixed call (an odd-sized tensor shifts every later flat offset off the grid)
+  // runs the vector instance over the aligned tensors and the scalar one over the rest,
+  // instead of sending the whole call to the scalar path (a (7,) vector ahead of two 7B
+  // layers: 6.3 vs 2.5 ms before this split).
   const size_t gsz = call.g_dtype == MCO_BF16 ? 2 : 4;
   const size_t psz = call.p_dtype == MCO_BF16 ? 2 : 4;
-  bool vec = true;
-  for (int k = call.t0; k < call.t1 && vec; ++k) {
+  bool any_vec = false, any_scalar = false;
+  for (int k = call.t0; k < call.t1; ++k) {
     const TensorInfo& T = pl.h_tensors[k];
     if (!T.factored) continue;
     const int64_t off = call.single || call.ntab ? 0 : T.elem_off;
     const uintptr_t pb = (uintptr_t)(call.ntab ? call.ptab[k - call.t0] : call.p);
     const uintptr_t gb = (uintptr_t)(call.ntab ? call.gtab[k - call.t0] : call.g);
-    vec = (T.cols % 8 == 0) && ((pb + off * psz) % (8 * psz) == 0) &&
-          ((gb + off * gsz) % (8 * gsz) == 0);
+    const bool v = (T.cols % 8 == 0) && ((pb + off * psz) % (8 * psz) == 0) &&
+                   ((gb + off * gsz) % (8 * gsz) == 0);
+    (v ? any_vec : any_scalar) = true;
   }
-  // (params, grads): (f32, f32), (f32, bf16), (bf16, bf16)
-  if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_F32) {
-    vec ? run_phase<true, float, float>(pl, call, phase, st)
-        : run_phase<false, float, float>(pl, call, phase, st);
-  } else if (call.p_dtype == MCO_F32 && call.g_dtype == MCO_BF16) {
-    vec ? run_phase<true, uint16_t, float>(pl, call, phase, st)
-        : run_phase<false, uint16_t, float>(pl, call, phase, st);
-  } else if (call.p_dtype == MCO_BF16 && call.g_dtype == MCO_BF16) {
-    vec ? run_phase<true, uint16_t, uint16_t>(pl, call, phase, st)
-        : run_phase<false, uint16_t, uint16_t>(pl, call, phase, st);
-  } else {
-    throw Error(MCO_CONTRACT, "adalomo: params / grads must be f32 / f32, f32 / bf16 or bf16 / bf16");
+  const bool mixed = any_vec && any_scalar;
+  const bool vec = !any_scalar;  // uniform call: its one instance
+  const Launch L = make_launch(pl, call);
+  const auto& cfg = pl.cfg;
+  // each tiled pass: one launch (uniform) or the vector + scalar pair (mixed)
+  auto each = [&](auto&& pass) {
+    if (!mixed) {
+      with_types(call, vec, [&](auto V, auto g, auto p) { pass(V, g, p, 0); });
+    } else {
+      with_types(call, true, [&](auto V, auto g, auto p) { pass(V, g, p, 1); });
+      with_types(call, false, [&](auto V, auto g, auto p) { pass(V, g, p, 2); });
+    }
+  };
+
+  if (phase == 1) {  // pass 1 + reduction of the tile partials into the payload
+    each([&](auto V, auto g, auto p, int filt) {
+      launch_k1<decltype(V)::value, decltype(g), decltype(p)>(L, call, filt, st);
+    });
+    const int mode = call.stats_mode ? call.stats_mode : kStatsAll;
+    const int64_t ncols = pl.h_col_off[call.t1] - pl.h_col_off[call.t0];
+    const int ncolblk = (mode & kStatsG) ? (int)((ncols + 31) / 32) : 0;
+    // fused calls (no all-reduce between the phases): KR's scalar block does K2's work
+    launch_pdl(kr_stats, ncolblk + (call.t1 - call.t0), kThreads, st, L.c, call.t0, call.t1,
+               (const int64_t*)pl.d_col_off, ncols, ncolblk, mode, call.fuse_usq, call.lr,
+               cfg.beta2, call.use_clip, pl.grad_clip, call.ext_sumsq);
+    launch_check("adalomo kr_stats");
+  } else if (phase == 2) {  // scalars, moments, pass 2
+    if (!call.fuse_usq) {
+      launch_pdl(k2_scalars, 1, kThreads, st, L.c, call.t0, call.t1, call.lr, cfg.beta2,
+                 call.use_clip, pl.grad_clip, call.ext_sumsq);
+      launch_check("adalomo k2_scalars");
+    }
+    const int64_t nitems = pl.h_item_off[call.t1] - pl.h_item_off[call.t0];
+    if (nitems > 0) {
+      const int64_t blocks = std::min<int64_t>((nitems + kThreads - 1) / kThreads, L.sms * 8);
+      launch_pdl(k3_moments, (unsigned)blocks, kThreads, st, L.c, call.t0, call.t1,
+                 (const int64_t*)pl.d_item_off, pl.h_item_off[call.t0], nitems, cfg.beta2);
+      launch_check("adalomo k3_moments");
+    }
+    // K4's last-CTA reduction counts one grid: a mixed call leaves it to K5 (with_usq)
+    each([&](auto V, auto g, auto p, int filt) {
+      launch_k4<decltype(V)::value, decltype(g), decltype(p)>(L, pl, call, filt,
+                                                             call.fuse_usq && !mixed, st);
+    });
+    if (!call.fuse_usq) {
+      launch_pdl(kr_usq, 1, 1024, st, L.c, call.t0, call.t1);
+      launch_check("adalomo kr_usq");
+    }
+  } else {  // damping + pass 3
+    if (!call.fuse_usq || mixed) {
+      launch_pdl(k5_damp, 1, 1024, st, L.c, call.t0, call.t1, cfg.adalomo_clip,
+                 call.fuse_usq && mixed ? 1 : 0);
+      launch_check("adalomo k5_damp");
+    }
+    each([&](auto V, auto g, auto p, int filt) {
+      launch_k6<decltype(V)::value, decltype(g), decltype(p)>(L, pl, call, filt, st);
+    });
   }
 }
+
 
 void launch_adalomo_gsumsq(const AdaLomoPlan& pl, int t0, int t1, double* out, cudaStream_t st) {
   Ctx c{};
@@ -1330,6 +1608,40 @@ void launch_adalomo_gsumsq(const AdaLomoPlan& pl, int t0, int t1, double* out, c
 }
 
 void launch_adalomo(const AdaLomoPlan& pl, const AdaLomoCall& call, cudaStream_t st) {
+  static const bool small_on = [] {  // MCO_ADALOMO_SMALL=0: the 4-launch chain (A/B knob)
+    const char* e = getenv("MCO_ADALOMO_SMALL");
+    return !(e && atoi(e) == 0);
+  }();
+  if (small_on && call.t1 == call.t0 + 1 && !call.stats_mode && small_vec_ok(pl, call.t0)) {
+    Launch L = make_launch(pl, call);
+    const auto& cfg = pl.cfg;
+    const TensorInfo& T = pl.h_tensors[call.t0];
+    const unsigned cs = (unsigned)std::min<int64_t>(kSmallCluster, T.tile_end - T.tile_begin);
+    auto go = [&](auto kk) {
+      cudaLaunchConfig_t lc{};
+      lc.gridDim = dim3(cs);
+      lc.blockDim = dim3(kThreads);
+      lc.stream = st;
+      cudaLaunchAttribute attr[2];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = MCO_PDL;
+      attr[1].id = cudaLaunchAttributeClusterDimension;
+      attr[1].val.clusterDim.x = cs;
+      attr[1].val.clusterDim.y = 1;
+      attr[1].val.clusterDim.z = 1;
+      lc.attrs = attr;
+      lc.numAttrs = 2;
+      cuda_check(cudaLaunchKernelEx(&lc, kk, L.c, L.P, call.t0, call.lr, cfg.beta2, cfg.eps,
+                                    call.use_clip, pl.grad_clip, call.ext_sumsq,
+                                    cfg.adalomo_clip, call.trigger),
+                 "cudaLaunchKernelEx (k_small_vec)");
+    };
+    with_types(call, false, [&](auto, auto g, auto p) {
+      go(k_small_vec<decltype(g), decltype(p)>);
+    });
+    launch_check("adalomo k_small_vec");
+    return;
+  }
   AdaLomoCall c = call;
   c.fuse_usq = 1;  // no all-reduce between the phases
   for (int phase = 1; phase <= 3; ++phase) launch_adalomo_phase(pl, c, phase, st);
@@ -1380,6 +1692,10 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
   pl.h_col_off.assign(1, 0);
   int64_t elem = 0, state = 0, colpart = 0, rowpart = 0, fa = 0, fb = 0;
   const int64_t min_tiles = 2LL * sms;
+  // tile heights: "waves" (default) or "pow2" (round 1: h halved from 128 until >= 2
+  // tiles per SM); MCO_ADALOMO_TILES, an A/B knob read at plan build
+  const char* tk = getenv("MCO_ADALOMO_TILES");
+  const bool waves = !(tk && std::string(tk) == "pow2");
   for (size_t k = 0; k < shapes.size(); ++k) {
     const auto& s = shapes[k];
     TensorInfo T{};
@@ -1402,7 +1718,21 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
       T.tc = tc;
       T.kc = (int32_t)((T.cols + w - 1) / w);
       int64_t h = kMaxTileRows;
-      while (h > 8 && ((T.rows + h - 1) / h) * T.kc < min_tiles) h >>= 1;
+      if (waves) {
+        // whole waves: the tensor's tile count is the smallest multiple m of the resident
+        // tile-kernel CTAs (3 per SM) that keeps h <= 128, so a one-tensor call (hook
+        // form) runs every pass in m full rounds -- 4096^2: 444 tiles of 37 rows (one round
+        // of 444 CTAs) instead of 512 tiles of 32 rows (two rounds of 256 CTAs, 1.7 per SM:
+        // K1 36.7 us against a 20.5 us traffic floor, ncu)
+        const int64_t wave = 3LL * sms;
+        const int64_t need = ((T.rows + kMaxTileRows - 1) / kMaxTileRows) * T.kc;
+        const int64_t m = std::max<int64_t>(1, (need + wave - 1) / wave);
+        const int64_t nrb_max = std::max<int64_t>(1, (m * wave) / T.kc);
+        h = std::max<int64_t>((T.rows + nrb_max - 1) / nrb_max, 8);
+        h = std::min<int64_t>(h, kMaxTileRows);
+      } else {
+        while (h > 8 && ((T.rows + h - 1) / h) * T.kc < min_tiles) h >>= 1;
+      }
       h = std::min<int64_t>(h, std::max<int64_t>(T.rows, 1));
       T.nrb = (T.rows + h - 1) / h;
       T.vrow_off = state;

@@ -426,6 +426,30 @@ def test_adalomo_list_form_equals_per_tensor():
     assert [b.steps(k) for k in range(len(shapes))] == [2] * len(shapes)
 
 
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_adalomo_mixed_alignment_call_equals_per_tensor(dt):
+    """A multi-tensor call whose tensors disagree on the vector path (an odd-sized 1-D
+    tensor shifts every later flat offset off the 8-element grid; a 13-column matrix
+    never qualifies) runs the vector instance of each pass over the aligned tensors and
+    the scalar instance over the rest: == one hook-form call per tensor, bit for bit."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = [(64, 256), (7,), (96, 512), (33, 13), (128, 1024), (5,), (40, 264), (300,)]
+    n = sum(int(np.prod(s)) for s in shapes)
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    p = (torch.randn(n, device="cuda") * 0.02).to(tdt)
+    q = p.clone()
+    offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+    a, b = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    for t in range(3):
+        g = (torch.randn(n, device="cuda") * 1e-3).to(tdt)
+        a.apply_all(p, g, 1e-3)
+        for k in range(len(shapes)):
+            lo, hi = int(offs[k]), int(offs[k + 1])
+            b.apply(k, q[lo:hi], g[lo:hi], 1e-3)
+    torch.cuda.synchronize()
+    assert torch.equal(p.view(torch.uint8), q.view(torch.uint8))
+
+
 def test_adalomo_and_lomo_replay_from_a_cuda_graph():
     """AdaLomo's chain (step counter, scalars and clip scale on the device, PDL launches)
     and LOMO capture into a CUDA graph: three replays == three eager steps, bit for bit,
@@ -485,3 +509,54 @@ def test_lomo_apply_list_equals_per_tensor(dt, clip):
     torch.cuda.synchronize()
     for p, q in zip(ps, qs):
         assert torch.equal(p, q)
+
+
+K6_CHILD = r"""
+import hashlib, sys
+import torch
+sys.path.insert(0, sys.argv[1])
+from paper_2312_00407_b200 import optim, registry
+from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+shapes = registry.CONFIG1.shapes()[:12]
+n = sum(int(torch.tensor(s).prod()) for s in shapes)
+h = hashlib.sha256()
+for pdt, gdt in ((torch.float32, torch.float32), (torch.float32, torch.bfloat16),
+                 (torch.bfloat16, torch.bfloat16)):
+    p = torch.empty(n, device="cuda")
+    registry.fill_params(p, shapes)
+    p = p.to(pdt)
+    g = torch.empty(n, device="cuda")
+    registry.fill_grads(g, shapes, 1)
+    g = g.to(gdt)
+    st = optim.AdaLomoState(cfg, shapes)
+    st.apply_all(p, g, 1e-3)
+    q = p.clone()
+    offs = [0]
+    for s in shapes:
+        offs.append(offs[-1] + int(torch.tensor(s).prod()))
+    for k in range(len(shapes)):
+        st.apply(k, q[offs[k]:offs[k + 1]], g[offs[k]:offs[k + 1]], 1e-3)
+    torch.cuda.synchronize()
+    h.update(p.view(torch.uint8).cpu().numpy().tobytes())
+    h.update(q.view(torch.uint8).cpu().numpy().tobytes())
+print(h.hexdigest())
+"""
+
+
+def test_adalomo_k6_traversals_bit_identical():
+    """K6's three traversals (tiles, flat chunks, the cp.async.bulk pipeline; the
+    MCO_ADALOMO_K6 A/B knob, read once per process) give the same bits, multi-tensor and
+    hook forms, every (params, grads) dtype pair."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for v in ("tiles", "chunks", "tma"):
+        r = subprocess.run([sys.executable, "-c", K6_CHILD, root], capture_output=True,
+                           text=True, timeout=600, env=dict(os.environ, MCO_ADALOMO_K6=v))
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[v] = r.stdout.strip().splitlines()[-1]
+    assert len(set(out.values())) == 1, out

@@ -57,7 +57,7 @@ def main():
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     W, K = 2, 5
-    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks", "bf16"]
+    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks", "bf16", "cliff"]
 
     if "c3" in which:
         m = registry.LLAMA_13B
@@ -115,6 +115,9 @@ def main():
     if "hooks" in which:
         hooks_7b(W, K)
 
+    if "cliff" in which:
+        cliff(W, K)
+
     if "bf16" in which:  # AdaLomo on bf16 parameters and gradients (12 B/param)
         m = registry.LLAMA_7B
         shapes, n = m.shapes(), m.param_count()
@@ -139,6 +142,30 @@ def main():
         st = optim.AdaLomoState(cfg, shapes)
         ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
         line("adalomo bf16 params + bf16 grads, llama-7b", n, ms, 12)
+
+
+def cliff(W, K):
+    """AdaLomo's per-tensor vector path: a (7,) vector ahead of two 7B decoder layers
+    shifts every later flat offset off the 8-element grid.  Before the per-tensor split
+    the whole call ran scalar (6.3 vs 2.5 ms); now only the shifted tensors do."""
+    import torch
+
+    from paper_2312_00407_b200 import optim, registry
+    from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+    layer = registry.LLAMA_7B.shapes()[1:10]  # one decoder layer (9 tensors)
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    for name, shapes in (("aligned", layer + layer), ("(7,) first", [(7,)] + layer + layer),
+                         ("(7,) mid", layer + [(7,)] + layer)):
+        n = sum(int(torch.tensor(s_).prod()) for s_ in shapes)
+        p = torch.empty(n, device="cuda")
+        g = torch.empty(n, device="cuda")
+        registry.fill_params(p, shapes)
+        registry.fill_grads(g, shapes, 1)
+        st = optim.AdaLomoState(cfg, shapes)
+        ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
+        line(f"adalomo 2 llama-7b layers, {name}", n, ms, 24, {"tensors": len(shapes)})
+        del st, p, g
 
 
 def hooks_7b(W, K):
