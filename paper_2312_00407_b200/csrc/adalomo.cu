@@ -732,6 +732,20 @@ __device__ __forceinline__ float u_fact(float g, float s, float a, float b, floa
   return gs * rsqrt_ftz(__fmaf_rn(a, b, eps));
 }
 
+// K6's update of one 8-element row vector, every K6 traversal (tiles, flat chunks, the
+// bulk-copy pipeline): p <- fma(-f, u, p) with u = u_fact(g, s, a, b_j, eps) -- one
+// rounding for p - f*u.  (A packed-pair FMUL2 / FFMA2 form halved the FP issue slots but
+// measured no faster on bf16 data -- 7B: 14.2 vs 14.1 ms -- and is not kept.)
+__device__ __forceinline__ void k6_row8(float (&pv)[8], const float (&gv)[8], float a,
+                                        const float (&bv)[8], float sf, float ff, float eps) {
+#pragma unroll
+  for (int j = 0; j < 8; ++j) pv[j] = __fmaf_rn(-ff, u_fact(gv[j], sf, a, bv[j], eps), pv[j]);
+}
+__device__ __forceinline__ float k6_one(float p, float g, float a, float b, float sf, float ff,
+                                        float eps) {
+  return __fmaf_rn(-ff, u_fact(g, sf, a, b, eps), p);  // == one element of k6_row8
+}
+
 // row / col of element e of a factored tensor: e / C by multiply-high with the
 // per-tensor magic (set_fast_div; exact for e < 2^31) instead of the ~20-instruction
 // 32-bit udiv -- K4 is issue-bound (ncu: 68 % issue active).
@@ -780,45 +794,60 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
           bv[j] = j < valid ? (sep ? c.frb : c.fb)[T.fb_off + col + j] : 0.f;
         constexpr int RB = k4_rows<GT>();
         const int64_t rstep = (int64_t)TR * T.cols;  // row pointers advance by adds
-        const GT* grow = g + (tl.r0 + tr) * T.cols + col;
-        for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
-          RowVec<VEC, GT, true> gr[RB];
-          const GT* gb = grow;
+        uint64_t bv2[VW / 2];
 #pragma unroll
-          for (int b = 0; b < RB; ++b, gb += rstep) {
-            if (r0 + (int64_t)b * TR < tl.r1)
-              gr[b].load(gb, valid);
-            else
-              gr[b].zero();
-          }
-          grow = gb;
-          float su = 0.f;
+        for (int j = 0; j < VW; j += 2) bv2[j / 2] = pk2(bv[j], bv[j + 1]);
+        // one row loop per form of u (the per-row branch is gone from the hot loop); a_i
+        // is loaded with its row, and rows past the tile read as zeros (exact zero terms)
+        auto rows = [&](auto sep_tag) {
+          constexpr bool SEP = decltype(sep_tag)::value;
+          const GT* grow = g + (tl.r0 + tr) * T.cols + col;
+          for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
+            RowVec<VEC, GT, true> gr[RB];
+            float av[RB];
+            const GT* gb = grow;
 #pragma unroll
-          for (int b = 0; b < RB; ++b) {
-            const int64_t r = r0 + (int64_t)b * TR;
-            if (r < tl.r1) {
-              const float a = fa[r];
+            for (int b = 0; b < RB; ++b, gb += rstep) {
+              const int64_t r = r0 + (int64_t)b * TR;
+              if (r < tl.r1) {
+                gr[b].load(gb, valid);
+                av[b] = fa[r];
+              } else {
+                gr[b].zero();
+                av[b] = 0.f;
+              }
+            }
+            grow = gb;
+            float su = 0.f;
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
               float gv[VW];
               gr[b].get(gv);
-              if (sep) {  // a = 1/sqrt(a_i), bv = 1/sqrt(b_j): ra^2 sum_j (g rb)^2
-                float rs = 0.f;
+              if constexpr (SEP) {  // a = 1/sqrt(a_i), bv = 1/sqrt(b_j): ra^2 sum_j (g rb)^2
+                uint64_t rs2 = 0;  // even / odd column partials (FMUL2 / FFMA2)
 #pragma unroll
-                for (int j = 0; j < VW; ++j) {
-                  const float x = gv[j] * bv[j];
-                  rs = __fmaf_rn(x, x, rs);
+                for (int j = 0; j < VW; j += 2) {
+                  const uint64_t x = mul2(pk2(gv[j], gv[j + 1]), bv2[j / 2]);
+                  rs2 = fma2(x, x, rs2);
                 }
-                su = __fmaf_rn(a * a, rs, su);
+                float re, ro;
+                up2(rs2, re, ro);
+                su = __fmaf_rn(av[b] * av[b], re + ro, su);
               } else {
 #pragma unroll
                 for (int j = 0; j < VW; ++j) {  // s is applied once per tile (s^2 below)
-                  const float x = gv[j] * rsqrt_ftz(__fmaf_rn(a, bv[j], epsf));
+                  const float x = gv[j] * rsqrt_ftz(__fmaf_rn(av[b], bv[j], epsf));
                   su = __fmaf_rn(x, x, su);
                 }
               }
             }
+            usq += (double)su;
           }
-          usq += (double)su;
-        }
+        };
+        if (sep)
+          rows(std::true_type{});
+        else
+          rows(std::false_type{});
       }
       usq *= (double)sf * (double)sf;  // sum (s g r)^2 = s^2 sum (g r)^2
     } else {  // optim.cpp:262-267 with fp64 state
@@ -929,7 +958,7 @@ __global__ void __launch_bounds__(kThreads)
               const float4 b1 = *reinterpret_cast<const float4*>(fb + col + 4);
               const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-              for (int j = 0; j < VW; ++j) pv[u][j] = pv[u][j] - ff * u_fact(gv[u][j], sf, a, bv[j], epsf);
+              k6_row8(pv[u], gv[u], a, bv, sf, ff, epsf);
               store_p<VEC, PT>(p + e, pv[u], VW);
             } else {
 #pragma unroll
@@ -938,7 +967,7 @@ __global__ void __launch_bounds__(kThreads)
                 if (ej < ch.e1) {
                   uint32_t row, col;
                   row_col((uint32_t)ej, T, C, row, col);
-                  stp1(p + ej, pv[u][j] - ff * u_fact(gv[u][j], sf, fa[row], fb[col], epsf));
+                  stp1(p + ej, k6_one(pv[u][j], gv[u][j], fa[row], fb[col], sf, ff, epsf));
                 }
               }
             }
@@ -1110,7 +1139,7 @@ __global__ void __launch_bounds__(kK6Consumers + 32, 1)
           pv[4] = x1.x, pv[5] = x1.y, pv[6] = x1.z, pv[7] = x1.w;
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
+        k6_row8(pv, gv, a, bv, sf, ff, epsf);
         if constexpr (sizeof(PT) == 2) {
           uint4 w;
           w.x = f2bf2_bits(pv[0], pv[1]);
@@ -1163,6 +1192,7 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
       float bv[VW];
 #pragma unroll
       for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
+      const float* fa = c.fa + T.fa_off;
       constexpr int RB = rows_in_flight<GT, PT>();
       const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
       int64_t roff = (tl.r0 + tr) * T.cols + col;
@@ -1180,14 +1210,11 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
         o = roff;
 #pragma unroll
         for (int b = 0; b < RB; ++b, o += rstep) {
-          const int64_t r = r0 + (int64_t)b * TR;
-          if (r < tl.r1) {
-            const float a = c.fa[T.fa_off + r];
+          if (r0 + (int64_t)b * TR < tl.r1) {
             float gv[VW], pv[VW];
             gr[b].get(gv);
             pr[b].get(pv);
-#pragma unroll
-            for (int j = 0; j < VW; ++j) pv[j] = pv[j] - ff * u_fact(gv[j], sf, a, bv[j], epsf);
+            k6_row8(pv, gv, fa[r0 + (int64_t)b * TR], bv, sf, ff, epsf);
             store_p<VEC, PT>(p + o, pv, VEC ? VW : valid);
           }
         }

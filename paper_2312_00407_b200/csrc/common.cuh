@@ -330,6 +330,29 @@ __device__ __forceinline__ void st_stream_bf16x16(uint16_t* p, const float (&r)[
 }
 __device__ __forceinline__ float bf2f(uint16_t h) { return __uint_as_float((uint32_t)h << 16); }
 
+// ---- packed fp32 pairs (sm_100: FMUL2 / FFMA2, two IEEE fp32 operations per issue) ----
+// Each lane of a pair is rounded exactly as the scalar instruction would round it.  Only
+// mul and fma are used: ptxas contracts a packed mul feeding a packed add into FFMA2
+// even under --fmad=false, so a packed add never follows a packed mul here.
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t mul2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 // ---- deterministic reductions --------------------------------------------------
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {

@@ -28,3 +28,18 @@ def pytest_collection_modifyitems(config, items):
     for it in items:
         if "gpu" in it.keywords:
             it.add_marker(skip)
+
+
+def pytest_runtest_teardown(item, nextitem):
+    """MCO_MEMLOG=path: device memory in use after every GPU test (leak hunting)."""
+    path = os.environ.get("MCO_MEMLOG")
+    if not path or "gpu" not in item.keywords or not _has_gpu():
+        return
+    import gc
+
+    import torch
+    gc.collect()
+    torch.cuda.empty_cache()
+    free, total = torch.cuda.mem_get_info()
+    with open(path, "a") as f:
+        f.write(f"{(total - free) / 1e9:.2f} GB {item.nodeid}\n")

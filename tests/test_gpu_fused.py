@@ -479,6 +479,41 @@ def test_adalomo_and_lomo_replay_from_a_cuda_graph():
     assert [sg.steps(k) for k in range(len(shapes))] == [3] * len(shapes)
 
 
+def test_adalomo_hook_form_replays_from_a_cuda_graph():
+    """The per-tensor hook form (PDL chains, the early-started next K1, the one-launch
+    cluster kernel of small 1-D tensors) captured on a side stream: three replays ==
+    three eager rounds of hook calls, bit for bit."""
+    cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
+    shapes = registry.CONFIG1.shapes()[:12]
+    n = sum(int(np.prod(s)) for s in shapes)
+    offs = np.concatenate([[0], np.cumsum([int(np.prod(s)) for s in shapes])])
+    p = torch.empty(n, device="cuda")
+    g = torch.empty(n, device="cuda")
+    registry.fill_params(p, shapes)
+    registry.fill_grads(g, shapes, 1)
+    pe, pg = p.clone(), p.clone()
+    se, sg = optim.AdaLomoState(cfg, shapes), optim.AdaLomoState(cfg, shapes)
+    s = torch.cuda.Stream()
+
+    def hooks(st, q):
+        for k in reversed(range(len(shapes))):
+            a, b = int(offs[k]), int(offs[k + 1])
+            st.apply(k, q[a:b], g[a:b], 1e-3, stream=s)
+
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            hooks(se, pe)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        hooks(sg, pg)
+    for _ in range(3):
+        graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(pe, pg)
+    assert [sg.steps(k) for k in range(len(shapes))] == [3] * len(shapes)
+
+
 @pytest.mark.parametrize("dt", ["f32", "bf16", "f32_bf16g", "f64"])
 @pytest.mark.parametrize("clip", [None, 0.5])
 def test_lomo_apply_list_equals_per_tensor(dt, clip):
