@@ -15,7 +15,7 @@ REP=/tmp/prof_${TAG}
     python bench.py --steps 2 --warmup 1 --repeats 1 --no-e2e --no-cpu-baseline --no-extra \
     > gpurun_out/launches_bench_${TAG}.json
 ncu --set full --clock-control none --import-source on \
-    -k regex:"flat_tma_kernel|flat_step_kernel|sophia_m64|lomo_kernel|lomo_tma_kernel|sumsq_kernel|k1_stats|kr_stats|k2_scalars|k3_moments|k4_usq|k5_damp|k6_update|peer_step_kernel" \
+    -k regex:"flat_tma_kernel|flat_step_kernel|sophia_m64|lomo_kernel|lomo_tma_kernel|sumsq_kernel|k1_stats|kr_stats|k2_scalars|k3_moments|k4_usq|k5_damp|k6_update|k_small_vec|peer_step_kernel" \
     -c 60 -o ${REP} -f python tools/profile_kernels.py ${ONLY:+--only $ONLY} > gpurun_out/prof_${TAG}.log 2>&1
 echo ncu_rc=$?
 python profiles/summarize_full_r02.py ${REP}.ncu-rep > gpurun_out/ncu_full_${TAG}.md

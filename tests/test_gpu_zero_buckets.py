@@ -7,13 +7,10 @@ double-buffered staging slots, the mixed (bf16 replica + fp32 master) and ring m
 every form is bit-identical to the plain FlatOptimizer step.  The multi-rank piece
 layout is pinned against ZeroPlan in tests/test_zero_buckets_plan.py (CPU); the C4
 per-rank footprints at N = 2 / 8 are allocated and stepped in test_gpu_00_footprint.py."""
-import os
-
-import numpy as np
 import pytest
 
 import oracle as O
-from paper_2312_00407_b200 import optim, registry, zero
+from paper_2312_00407_b200 import optim, zero
 from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
 pytestmark = pytest.mark.gpu
