@@ -574,8 +574,15 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
   }
   const size_t ps = dtype_bytes(a.p_dtype), gs = dtype_bytes(a.g_dtype),
                ss = dtype_bytes(a.state_dtype);
-  const int ph = common_phase({{a.p, ps}, {a.g, gs}, {a.s[0], ss}, {a.s[1], ss},
-                               {a.s[2], ss}, {a.s[3], ss}, {a.p_out_bf16, 2}});
+  int ph = common_phase({{a.p, ps}, {a.g, gs}, {a.s[0], ss}, {a.s[1], ss},
+                         {a.s[2], ss}, {a.s[3], ss}, {a.p_out_bf16, 2}});
+  if (ph < 0 && ((uintptr_t)a.g % gs) == 0) {
+    // only the (read-only) gradient disagrees -- a gradient buffer at another offset than
+    // the parameters, e.g. a reduce-scattered shard against an odd ZeroPlan slice: align
+    // the other streams as below, the TMA pipeline reads the gradient shifted
+    ph = common_phase({{a.p, ps}, {a.s[0], ss}, {a.s[1], ss}, {a.s[2], ss}, {a.s[3], ss},
+                       {a.p_out_bf16, 2}});
+  }
   if (ph <= 0 || a.n <= (uint64_t)(8 - ph)) {
     launch_flat_one(a, kf, kd, st);
     return;
@@ -606,7 +613,8 @@ void launch_lomo(void* p, int p_dtype, const void* g, int g_dtype, uint64_t n, d
                  double scale, const double* dev_sumsq, double clip, cudaStream_t st) {
   if (n == 0) return;
   const size_t ps = dtype_bytes(p_dtype), gs = dtype_bytes(g_dtype);
-  const int ph = common_phase({{p, ps}, {g, gs}});
+  int ph = common_phase({{p, ps}, {g, gs}});
+  if (ph < 0 && ((uintptr_t)g % gs) == 0) ph = common_phase({{p, ps}});  // gradient read shifted
   if (ph <= 0 || n <= (uint64_t)(8 - ph)) {
     launch_lomo_one(p, p_dtype, g, g_dtype, n, lr, scale, dev_sumsq, clip, st);
     return;

@@ -49,9 +49,15 @@ template <int KIND>
 constexpr int n_in() {  // p, g, s0 [, s1 [, s2, s3]]
   return KIND == K_ADAN ? 6 : (KIND == K_LION ? 3 : 4);
 }
+// A stream slot holds one tile plus 16 B: a gradient at a different 16 B phase than the
+// other streams is copied from its aligned-down address (flat_tma_kernel, gsh).
+template <class C>
+constexpr int slot_floats() {
+  return C::kTile + 4;
+}
 template <class C, int KIND, bool MIXED>
 constexpr int stage_bytes() {
-  return n_in<KIND>() * C::kTile * 4 + (MIXED ? C::kTile * 2 : 0);
+  return n_in<KIND>() * slot_floats<C>() * 4 + (MIXED ? C::kTile * 2 : 0);
 }
 template <class C, int KIND, bool MIXED>
 constexpr int stages() {
@@ -104,14 +110,19 @@ template <class C, int KIND, bool MIXED, typename GT, bool DEV = false>
 __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     flat_tma_kernel(float* p, const GT* g, float* s0, float* s1, float* s2, float* s3,
                     uint16_t* pout, uint64_t ntiles, uint64_t n, const StepConsts<float> kv,
-                    const GraphStep gs) {
+                    const GraphStep gs, int gsh) {
+  // gsh: the gradient's element phase within 16 B when it differs from every other
+  // stream's (those are 16 B aligned): its tiles are copied from the aligned-down address
+  // (one 16 B granule more) and read gsh elements into the slot -- same bits, no scalar
+  // fallback for a gradient view at another offset than the parameters
   const StepConsts<float> k = step_consts<DEV>(kv, gs);  // DEV: graph mode (common.cuh)
   constexpr int NIN = n_in<KIND>();
   constexpr int NS = stages<C, KIND, MIXED>();
   constexpr int kTile = C::kTile, kConsumers = C::kConsumers, kConsumerWarps = C::CW;
+  constexpr int kSlot = slot_floats<C>();
   extern __shared__ __align__(128) uint8_t smem[];
-  float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kTile]
-  uint16_t* obuf = reinterpret_cast<uint16_t*>(buf + NS * NIN * kTile);  // [NS][kTile]
+  float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kSlot]
+  uint16_t* obuf = reinterpret_cast<uint16_t*>(buf + NS * NIN * kSlot);  // [NS][kTile]
   uint64_t* full = reinterpret_cast<uint64_t*>(obuf + (MIXED ? NS * kTile : 0));
   uint64_t* done = full + NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -135,15 +146,15 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
       const uint64_t pol = C::kHint ? evict_first_policy() : 0;
       const bool skip_gp = (KIND == K_ADAN) && k.first;  // g_prev unused at t == 1
       const int nload = skip_gp ? NIN - 1 : NIN;
+      const uint32_t gbytes = kTile * sizeof(GT) + (gsh ? 16u : 0u);
       auto issue = [&](uint64_t i) {
         const int s = (int)(i % NS);
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
-        constexpr uint32_t gbytes = kTile * sizeof(GT);
         mbar_expect_tx(&full[s], (uint32_t)((nload - 1) * kTile * 4) + gbytes);
         for (int j = 0; j < nload; ++j) {
-          float* dst = buf + ((size_t)s * NIN + j) * kTile;
+          float* dst = buf + ((size_t)s * NIN + j) * kSlot;
           if (j == 1)
-            bulk_g2s<C::kHint>(dst, g + e, gbytes, &full[s], pol);
+            bulk_g2s<C::kHint>(dst, g + e - gsh, gbytes, &full[s], pol);
           else
             bulk_g2s<C::kHint>(dst, src[j] + e, kTile * 4, &full[s], pol);
         }
@@ -153,16 +164,16 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         const int s = (int)(i % NS);
         mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
-        float* st = buf + (size_t)s * NIN * kTile;
+        float* st = buf + (size_t)s * NIN * kSlot;
         bulk_s2g<C::kHint>(p + e, st, kTile * 4, pol);
-        bulk_s2g<C::kHint>(s0 + e, st + 2 * kTile, kTile * 4, pol);
-        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) bulk_s2g<C::kHint>(s1 + e, st + 3 * kTile, kTile * 4, pol);
+        bulk_s2g<C::kHint>(s0 + e, st + 2 * kSlot, kTile * 4, pol);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) bulk_s2g<C::kHint>(s1 + e, st + 3 * kSlot, kTile * 4, pol);
         if constexpr (KIND == K_SOPHIA) {
-          if (k.refresh) bulk_s2g<C::kHint>(s1 + e, st + 3 * kTile, kTile * 4, pol);
+          if (k.refresh) bulk_s2g<C::kHint>(s1 + e, st + 3 * kSlot, kTile * 4, pol);
         }
         if constexpr (KIND == K_ADAN) {
-          bulk_s2g<C::kHint>(s2 + e, st + 4 * kTile, kTile * 4, pol);
-          bulk_s2g<C::kHint>(s3 + e, st + 5 * kTile, kTile * 4, pol);
+          bulk_s2g<C::kHint>(s2 + e, st + 4 * kSlot, kTile * 4, pol);
+          bulk_s2g<C::kHint>(s3 + e, st + 5 * kSlot, kTile * 4, pol);
         }
         if constexpr (MIXED) bulk_s2g<C::kHint>(pout + e, obuf + (size_t)s * kTile, kTile * 2, pol);
         bulk_commit();
@@ -182,18 +193,24 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     for (uint64_t i = 0; i < mine; ++i) {
       const int s = (int)(i % NS);
       mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
-      float* st = buf + (size_t)s * NIN * kTile + c0;
+      float* st = buf + (size_t)s * NIN * kSlot + c0;
       float pv[E], gv[E], a[E], b[E], c[E], d[E];
       lds<E>(st, pv);
-      if constexpr (sizeof(GT) == 4)
-        lds<E>(st + kTile, gv);
-      else
-        lds_grad_bf16<E>(buf + (size_t)s * NIN * kTile + kTile, c0, gv);
-      lds<E>(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) lds<E>(st + 3 * kTile, b);
+      if (gsh == 0) {
+        if constexpr (sizeof(GT) == 4)
+          lds<E>(st + kSlot, gv);
+        else
+          lds_grad_bf16<E>(buf + (size_t)s * NIN * kSlot + kSlot, c0, gv);
+      } else {  // shifted gradient tile: element-wise reads
+        const GT* gslot = reinterpret_cast<const GT*>(buf + (size_t)s * NIN * kSlot + kSlot) + gsh + c0;
+#pragma unroll
+        for (int j = 0; j < E; ++j) gv[j] = load_grad1(gslot + j);
+      }
+      lds<E>(st + 2 * kSlot, a);
+      if constexpr (KIND != K_LION) lds<E>(st + 3 * kSlot, b);
       if constexpr (KIND == K_ADAN) {
-        lds<E>(st + 4 * kTile, c);
-        if (!k.first) lds<E>(st + 5 * kTile, d);
+        lds<E>(st + 4 * kSlot, c);
+        if (!k.first) lds<E>(st + 5 * kSlot, d);
       }
 #pragma unroll
       for (int j = 0; j < E; ++j) {
@@ -205,11 +222,11 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
       }
       sts<E>(st, pv);
-      sts<E>(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) sts<E>(st + 3 * kTile, b);
+      sts<E>(st + 2 * kSlot, a);
+      if constexpr (KIND != K_LION) sts<E>(st + 3 * kSlot, b);
       if constexpr (KIND == K_ADAN) {
-        sts<E>(st + 4 * kTile, c);
-        sts<E>(st + 5 * kTile, d);
+        sts<E>(st + 4 * kSlot, c);
+        sts<E>(st + 5 * kSlot, d);
       }
       if constexpr (MIXED) {
         uint32_t* o = reinterpret_cast<uint32_t*>(obuf + (size_t)s * kTile + c0);
@@ -261,13 +278,16 @@ constexpr int lomo_tile() {
 template <typename ET, int NS>
 __global__ void __launch_bounds__(kLomoConsumers + 32, 1)
     lomo_tma_kernel(ET* p, const ET* g, uint64_t ntiles, uint64_t n, double lr, double scale,
-                    const double* sumsq, double clip) {
+                    const double* sumsq, double clip, int gsh) {
+  // gsh: the gradient's element phase within 16 B when it differs from the parameters'
+  // (flat_tma_kernel): copied from the aligned-down address, read shifted
   constexpr int EPT = 16 / (int)sizeof(ET);
   constexpr int kTile = lomo_tile<ET>();
+  constexpr int kStage = 2 * kTile + EPT;  // p tile | g tile + 16 B
   constexpr uint32_t kBytes = kTile * sizeof(ET);
   extern __shared__ __align__(128) uint8_t smem[];
-  ET* buf = reinterpret_cast<ET*>(smem);  // [NS][2][kTile]
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * 2 * kTile);
+  ET* buf = reinterpret_cast<ET*>(smem);  // [NS][kStage]
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * kStage);
   uint64_t* done = full + NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -283,19 +303,20 @@ __global__ void __launch_bounds__(kLomoConsumers + 32, 1)
       ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
   if (warp == kLomoWarps) {  // ---------------- producer ----------------
     if (lane == 0) {
+      const uint32_t gbytes = kBytes + (gsh ? 16u : 0u);
       auto issue = [&](uint64_t i) {
         const int s = (int)(i % NS);
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
-        mbar_expect_tx(&full[s], 2 * kBytes);
-        bulk_g2s<false>(buf + (size_t)s * 2 * kTile, p + e, kBytes, &full[s], 0);
-        bulk_g2s<false>(buf + ((size_t)s * 2 + 1) * kTile, g + e, kBytes, &full[s], 0);
+        mbar_expect_tx(&full[s], kBytes + gbytes);
+        bulk_g2s<false>(buf + (size_t)s * kStage, p + e, kBytes, &full[s], 0);
+        bulk_g2s<false>(buf + (size_t)s * kStage + kTile, g + e - gsh, gbytes, &full[s], 0);
       };
       for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
       for (uint64_t i = 0; i < mine; ++i) {
         const int s = (int)(i % NS);
         mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
         const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile;
-        bulk_s2g<false>(p + e, buf + (size_t)s * 2 * kTile, kBytes, 0);
+        bulk_s2g<false>(p + e, buf + (size_t)s * kStage, kBytes, 0);
         bulk_commit();
         if (i >= 1 && i - 1 + NS < mine) {  // refill the previous tile's stage
           bulk_wait_read_1();
@@ -310,11 +331,15 @@ __global__ void __launch_bounds__(kLomoConsumers + 32, 1)
     for (uint64_t i = 0; i < mine; ++i) {
       const int s = (int)(i % NS);
       mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
-      ET* sp = buf + (size_t)s * 2 * kTile + c0;
+      ET* sp = buf + (size_t)s * kStage + c0;
       const ET* sg = sp + kTile;
       if constexpr (sizeof(ET) == 4) {
         float4 pv = *reinterpret_cast<const float4*>(sp);
-        const float4 gv = *reinterpret_cast<const float4*>(sg);
+        float4 gv;
+        if (gsh == 0)
+          gv = *reinterpret_cast<const float4*>(sg);
+        else
+          gv = make_float4(sg[gsh], sg[gsh + 1], sg[gsh + 2], sg[gsh + 3]);
         pv.x = pv.x - f * gv.x;
         pv.y = pv.y - f * gv.y;
         pv.z = pv.z - f * gv.z;
@@ -322,7 +347,16 @@ __global__ void __launch_bounds__(kLomoConsumers + 32, 1)
         *reinterpret_cast<float4*>(sp) = pv;
       } else {
         uint4 pw = *reinterpret_cast<const uint4*>(sp);
-        const uint4 gw = *reinterpret_cast<const uint4*>(sg);
+        uint4 gw;
+        if (gsh == 0) {
+          gw = *reinterpret_cast<const uint4*>(sg);
+        } else {
+          const uint16_t* h = reinterpret_cast<const uint16_t*>(sg) + gsh;
+          gw.x = (uint32_t)h[0] | ((uint32_t)h[1] << 16);
+          gw.y = (uint32_t)h[2] | ((uint32_t)h[3] << 16);
+          gw.z = (uint32_t)h[4] | ((uint32_t)h[5] << 16);
+          gw.w = (uint32_t)h[6] | ((uint32_t)h[7] << 16);
+        }
         uint32_t* pa = &pw.x;
         const uint32_t* ga = &gw.x;
 #pragma unroll
@@ -352,14 +386,18 @@ template <typename ET, int NS>
 void run_lomo_tma(void* p, const void* g, uint64_t n, double lr, double scale,
                   const double* sumsq, double clip, cudaStream_t st) {
   auto kern = lomo_tma_kernel<ET, NS>;
-  constexpr int smem = NS * 2 * lomo_tile<ET>() * (int)sizeof(ET) + 2 * NS * 8;
+  constexpr int smem = NS * (2 * lomo_tile<ET>() * (int)sizeof(ET) + 16) + 2 * NS * 8;
   const int dev = current_device();
   static std::atomic<uint64_t> attr_set{0};
   if (!(attr_set.load() & (1ull << dev))) {
     MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set.fetch_or(1ull << dev);
   }
-  const uint64_t ntiles = n / lomo_tile<ET>();
+  const int gsh = (int)(((uintptr_t)g % 16) / sizeof(ET));
+  uint64_t ntiles = n / lomo_tile<ET>();
+  // a shifted gradient's copies reach 16 - gsh * sizeof(ET) bytes past the tile
+  if (gsh && ntiles && (n - ntiles * lomo_tile<ET>()) * sizeof(ET) < 16 - gsh * sizeof(ET))
+    --ntiles;
   const int grid = (int)std::max<uint64_t>(
       1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
   cudaLaunchConfig_t cfg{};
@@ -373,7 +411,7 @@ void run_lomo_tma(void* p, const void* g, uint64_t n, double lr, double scale,
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   MCO_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, (ET*)p, (const ET*)g, ntiles, n, lr, scale,
-                                    sumsq, clip));
+                                    sumsq, clip, gsh));
   launch_check("lomo_tma_kernel");
 }
 
@@ -387,12 +425,16 @@ void run_kern(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
     MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_set.fetch_or(1ull << dev);
   }
-  const uint64_t ntiles = a.n / C::kTile;
+  const int gsh = (int)(((uintptr_t)a.g % 16) / sizeof(GT));
+  uint64_t ntiles = a.n / C::kTile;
+  // a shifted gradient's copies reach 16 - gsh * sizeof(GT) bytes past the tile: the last
+  // tile needs that many valid bytes after it, else it joins the scalar tail
+  if (gsh && ntiles && (a.n - ntiles * C::kTile) * sizeof(GT) < 16 - gsh * sizeof(GT)) --ntiles;
   const int grid = (int)std::max<uint64_t>(
       1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
   kern<<<grid, C::kConsumers + 32, smem, st>>>((float*)a.p, (const GT*)a.g, (float*)a.s[0],
                                                (float*)a.s[1], (float*)a.s[2], (float*)a.s[3],
-                                               a.p_out_bf16, ntiles, a.n, k, a.gs);
+                                               a.p_out_bf16, ntiles, a.n, k, a.gs, gsh);
   launch_check("flat_tma_kernel");
 }
 
@@ -638,9 +680,11 @@ bool flat_tma_eligible(const FlatArgs& a, int cfg) {
   if (a.state_dtype != MCO_F32 || a.p_dtype != MCO_F32) return false;
   if (a.g_dtype != MCO_F32 && a.g_dtype != MCO_BF16) return false;
   auto al = [](const void* q) { return q == nullptr || ((uintptr_t)q % 16) == 0; };
-  bool ok = al(a.p) && al(a.g) && al(a.p_out_bf16);
+  // every stream but the gradient 16 B aligned; the gradient element-aligned (its 16 B
+  // phase may differ: flat_tma_kernel's gsh)
+  bool ok = al(a.p) && al(a.p_out_bf16) && ((uintptr_t)a.g % (a.g_dtype == MCO_BF16 ? 2 : 4)) == 0;
   for (int i = 0; i < 4; ++i) ok = ok && al(a.s[i]);
-  return ok && a.n >= (uint64_t)tma_tile(cfg);
+  return ok && a.n >= (uint64_t)tma_tile(cfg) + (al(a.g) ? 0 : (uint64_t)tma_tile(cfg));
 }
 
 #define MCO_UNPAREN(...) __VA_ARGS__
@@ -676,8 +720,11 @@ void launch_flat_tma(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t
 
 bool lomo_tma_eligible(const void* p, int p_dtype, const void* g, int g_dtype, uint64_t n) {
   if (p_dtype != g_dtype || (p_dtype != MCO_F32 && p_dtype != MCO_BF16)) return false;
-  if (((uintptr_t)p % 16) || ((uintptr_t)g % 16)) return false;
-  return n >= (uint64_t)(p_dtype == MCO_F32 ? lomo_tile<float>() : lomo_tile<uint16_t>());
+  const size_t es = p_dtype == MCO_F32 ? 4 : 2;
+  // parameters 16 B aligned; the gradient element-aligned (its phase may differ: gsh)
+  if (((uintptr_t)p % 16) || ((uintptr_t)g % es)) return false;
+  const uint64_t tile = p_dtype == MCO_F32 ? lomo_tile<float>() : lomo_tile<uint16_t>();
+  return n >= tile * (((uintptr_t)g % 16) ? 2 : 1);
 }
 
 void launch_lomo_tma(void* p, int p_dtype, const void* g, uint64_t n, double lr, double scale,

@@ -395,3 +395,59 @@ def test_bf16_grads_both_paths_bit_exact(flat_variant, variant, kind):
     assert bits_equal(tpo.view(torch.int16).cpu().numpy().view(np.uint16), O.f32_to_bf16(p))
     for name, t in opt.buffers():
         assert bits_equal(t.cpu().numpy(), orc.state[name]), name
+
+
+@pytest.mark.parametrize("gdt", ["f32", "bf16"])
+@pytest.mark.parametrize("kind", FLAT)
+@pytest.mark.parametrize("n", [4 * 2048, 5 * 2048 + 13])
+def test_gradient_phase_shift_bit_exact(kind, gdt, n):
+    """A gradient at another alignment phase than the parameters (every pair of phases
+    0..7; fp32 and bf16 gradients): the TMA pipeline reads the gradient shifted
+    (flat_tma_kernel gsh) instead of falling back to the scalar path -- same bits as the
+    restatement, including n a whole number of tiles (the shifted last tile joins the
+    scalar tail)."""
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=2)
+    P = O.synth(n + 16, 12, 0, 6, 0, 0, -6, 0, False)
+    G = [O.synth(n + 16, 12, 1, 6, t, 0, -7, 10, False) for t in (1, 2, 3)]
+    if gdt == "bf16":  # bf16-valued: the restatement reads the same gradients as floats
+        G = [O.bf16_to_f32(O.f32_to_bf16(x)) for x in G]
+    tG = [dev(x) if gdt == "f32" else dev(x).to(torch.bfloat16) for x in G]
+    for po in range(8):
+        for go in range(8):
+            if po == go:
+                continue
+            p = P[po:po + n].copy()
+            tp = dev(P)[po:po + n]
+            opt = optim.FlatOptimizer(cfg, n)
+            orc = O.OracleFlat(cfg, n, np.float32)
+            for t in range(3):
+                opt.step(tp, tG[t][go:go + n], 1e-3)
+                orc.step(p, G[t][go:go + n].copy(), 1e-3)
+            torch.cuda.synchronize()
+            assert bits_equal(tp.cpu().numpy(), p), (po, go)
+            for name, buf in opt.buffers():
+                assert bits_equal(buf.cpu().numpy(), orc.state[name]), (po, go, name)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_lomo_gradient_phase_shift_bit_exact(dt):
+    """LOMO with the gradient at another phase than the parameters (lomo_tma_kernel
+    gsh), every pair of phases: the restatement's bits."""
+    n = 3 * 4096 + 8  # whole tiles (+8: the shifted last tile fits for some phases only)
+    sd = np.float32 if dt == "f32" else "bf16"
+    P = O.synth(n + 16, 13, 0, 0, 0, 0, -6, 0, False, sd)
+    G = O.synth(n + 16, 13, 1, 0, 1, 0, -7, 10, False, sd)
+    orc = O.orc.orc_lomo_f32 if dt == "f32" else O.orc.orc_lomo_bf16
+    for po in range(8):
+        for go in range(8):
+            if po == go:
+                continue
+            tp = dev(P) if dt == "f32" else dev(P).view(torch.bfloat16)
+            tg = dev(G) if dt == "f32" else dev(G).view(torch.bfloat16)
+            optim.lomo_apply(tp[po:po + n], tg[go:go + n], 1e-2, 0.5)
+            p = P[po:po + n].copy()
+            orc(O._ptr(p), O._ptr(G[go:go + n].copy()), n, 1e-2, 0.5)
+            torch.cuda.synchronize()
+            got = tp[po:po + n].cpu().numpy() if dt == "f32" else \
+                tp[po:po + n].view(torch.int16).cpu().numpy()
+            assert bits_equal(got, p), (po, go)

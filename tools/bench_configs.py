@@ -57,7 +57,7 @@ def main():
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     W, K = 2, 5
-    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks", "bf16", "cliff"]
+    which = sys.argv[1:] or ["c3", "c4", "c5", "hooks", "bf16", "cliff", "phases"]
 
     if "c3" in which:
         m = registry.LLAMA_13B
@@ -118,6 +118,9 @@ def main():
     if "cliff" in which:
         cliff(W, K)
 
+    if "phases" in which:
+        phases(W, K)
+
     if "bf16" in which:  # AdaLomo on bf16 parameters and gradients (12 B/param)
         m = registry.LLAMA_7B
         shapes, n = m.shapes(), m.param_count()
@@ -142,6 +145,34 @@ def main():
         st = optim.AdaLomoState(cfg, shapes)
         ms = timed(lambda: st.apply_all(p, g, 5e-4), W, K)
         line("adalomo bf16 params + bf16 grads, llama-7b", n, ms, 12)
+
+
+def phases(W, K):
+    """Stored-state / LOMO steps whose gradient sits at another alignment phase than the
+    parameters (a gradient view one element in): the TMA pipeline reads it shifted
+    (round 1: the whole step took the scalar path)."""
+    import torch
+
+    from paper_2312_00407_b200 import optim
+    from paper_2312_00407_b200.optim import Kind, OptimizerConfig
+
+    n = 1 << 30
+    p = torch.empty(n, device="cuda")
+    gb = torch.empty(n + 8, device="cuda")
+    optim.synth_fill(p, 1, 0, 0, 0, 0, -6)
+    optim.synth_fill(gb, 1, 1, 0, 1, 0, -7, 10)
+    for kind, bpp in ((Kind.ADAMW, 28), (Kind.ADAN, 44)):
+        cfg = OptimizerConfig.defaults_for(kind)
+        opt = optim.FlatOptimizer(cfg, n)
+        for go in (0, 1):
+            g = gb[go:go + n]
+            ms = timed(lambda: opt.step(p, g, 1e-5), W, K)
+            line(f"{optim.kind_name(kind)} 2^30, gradient at element offset {go}", n, ms, bpp)
+        del opt
+    for go in (0, 1):
+        g = gb[go:go + n]
+        ms = timed(lambda: optim.lomo_apply(p, g, 1e-3, 1.0), W, K)
+        line(f"lomo 2^30, gradient at element offset {go}", n, ms, 12)
 
 
 def cliff(W, K):
