@@ -1255,6 +1255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ double red[32];
   __shared__ double sc[3][kSmallTiles];  // CTA 0: per tile sum p^2, sum g^2, sum u^2
   __shared__ double bc[3];               // s, corr, f from CTA 0
+  // every CTA of the cluster must have started before any DSMEM access: arrive now,
+  // wait just before the first remote write (the loads below overlap the barrier)
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   pdl_wait();
   if (trigger) pdl_trigger();  // the next tensor's K1 may start (see k1_stats)
   const TensorInfo T = c.tensors[k];
@@ -1279,6 +1282,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     pv[q] = ev[q] >= 0 ? ldp1(p + ev[q]) : 0.f;
     vv[q] = ev[q] >= 0 ? c.state[T.vfull_off + ev[q]] : 0.0;
   }
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   // K1 (1-D branch): per tile sum p^2, sum g^2 -> CTA 0
 #pragma unroll
   for (int q = 0; q < kSmallPer; ++q) {
