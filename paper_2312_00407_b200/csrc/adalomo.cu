@@ -319,21 +319,28 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
       for (int j = 0; j < VW; ++j) cacc[j] = 0.f;
       // RB rows per iteration: all their loads are in flight before any math
       constexpr int RB = rows_in_flight<GT, PT>();
-      const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
-      int64_t roff = (tl.r0 + tr) * T.cols + col;
-      for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
+      // 32-bit row indices within the tile (h <= 128), row pointers advanced by adds
+      // (fp32 7B: K1 833 -> 820 us under ncu; the bf16 tile loops of K4 / K6 measured no
+      // better this way and keep their 64-bit form)
+      const int h = (int)(tl.r1 - tl.r0);
+      const int64_t rstep = (int64_t)TR * T.cols;
+      const GT* gq = g + (tl.r0 + tr) * T.cols + col;
+      const PT* pq = p + (tl.r0 + tr) * T.cols + col;
+      for (int lr0 = tr; lr0 < h; lr0 += RB * TR) {
         RowVec<VEC, GT, true> gr[RB];
         RowVec<VEC, PT, false> pr[RB];
 #pragma unroll
-        for (int b = 0; b < RB; ++b, roff += rstep) {
-          if (valid > 0 && r0 + (int64_t)b * TR < tl.r1) {
-            if constexpr (SG) gr[b].load(g + roff, valid);
-            if constexpr (SP) pr[b].load(p + roff, valid);
+        for (int b = 0; b < RB; ++b) {
+          if (valid > 0 && lr0 + b * TR < h) {
+            if constexpr (SG) gr[b].load(gq + b * rstep, valid);
+            if constexpr (SP) pr[b].load(pq + b * rstep, valid);
           } else {
             gr[b].zero();
             pr[b].zero();
           }
         }
+        gq += RB * rstep;
+        pq += RB * rstep;
         float sg[RB];
 #pragma unroll
         for (int b = 0; b < RB; ++b) {
@@ -357,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
           // warp never straddles two rows: TC >= 32); lane group of row b writes it
           const float tot = warp_sum_rows<RB>(sg);
           const int lane = threadIdx.x & 31, b = warp_rows_index<RB>(lane);
-          const int64_t r = r0 + (int64_t)b * TR;
-          if ((lane & (32 / RB - 1)) == 0 && r < tl.r1) rowbuf[(r - tl.r0) * nwr + wrow] = tot;
+          const int lr = lr0 + b * TR;
+          if ((lane & (32 / RB - 1)) == 0 && lr < h) rowbuf[lr * nwr + wrow] = tot;
         }
       }
       if constexpr (!SG) {  // parameter statistics only
@@ -380,7 +387,6 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
         c.colpart[T.colpart_off + tl.rb * T.cols + tl.c0 + q] = s;
       }
       // row partials
-      const int64_t h = tl.r1 - tl.r0;
       double vrs = 0.0;
       for (int64_t i = threadIdx.x; i < h; i += kThreads) {
         double s = 0.0;
