@@ -170,11 +170,34 @@ void list_chunks(const FlatListArgs& a, const StepConsts<T>& k, cudaStream_t st)
   for (int i = 0; i < a.count; ++i) {
     const uint64_t n = a.len[i];
     if (n) {
-      bool vec = aligned(a.p[i], align) && aligned(a.g[i], tma ? 16 : sizeof(GT) * W);
-      for (int j = 0; j < 4; ++j)
-        vec = vec && aligned(a.s[j] ? (const char*)a.s[j] + soff * sizeof(T) : nullptr, align);
-      const uint64_t items = vec ? n / unit : 0;
+      uint64_t items = 0;
       const int t = L.n++;
+      if (tma) {
+        // every stream element-aligned; each may sit at its own phase within 16 B
+        // (list_tma_kernel reads / writes it shifted): the state slots must share one
+        const size_t gsz = sizeof(GT);
+        const auto ph = [](const void* q, size_t es) { return (int)(((uintptr_t)q % 16) / es); };
+        bool ok = aligned(a.p[i], sizeof(T)) && aligned(a.g[i], gsz);
+        int ss = -1;
+        for (int j = 0; j < 4; ++j) {
+          if (!a.s[j]) continue;
+          const void* q = (const char*)a.s[j] + soff * sizeof(T);
+          ok = ok && aligned(q, sizeof(T)) && (ss < 0 || ph(q, sizeof(T)) == ss);
+          ss = ph(q, sizeof(T));
+        }
+        L.shp[t] = (uint8_t)ph(a.p[i], sizeof(T));
+        L.shg[t] = (uint8_t)ph(a.g[i], gsz);
+        L.shs[t] = (uint8_t)std::max(ss, 0);
+        const bool shifted = L.shp[t] || L.shg[t] || L.shs[t];
+        // a shifted stream's copies reach up to 16 B past the tile: keep them inside the
+        // tensor (the last tile joins the scalar elements otherwise)
+        if (ok) items = shifted ? (n >= 8 ? (n - 8) / unit : 0) : n / unit;
+      } else {
+        bool vec = aligned(a.p[i], align) && aligned(a.g[i], sizeof(GT) * W);
+        for (int j = 0; j < 4; ++j)
+          vec = vec && aligned(a.s[j] ? (const char*)a.s[j] + soff * sizeof(T) : nullptr, align);
+        items = vec ? n / unit : 0;
+      }
       L.p[t] = a.p[i];
       L.g[t] = a.g[i];
       L.soff[t] = soff;

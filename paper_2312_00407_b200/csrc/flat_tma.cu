@@ -478,9 +478,58 @@ void launch_cfg(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) 
 // FlatList.vbeg holds tile prefix sums here: tile t belongs to tensor list_find(t) and
 // starts at element (t - vbeg[i]) * kTile of it; the producer resolves every tile's
 // addresses (p_i, g_i, state + soff_i), the consumers run exactly the flat kernel's
-// update.  Scalar elements (tensor tails, tensors not 16 B aligned) are spread over the
-// consumer threads of every CTA afterwards.
-template <class C, int KIND, typename GT, bool DEV>
+// update.  Scalar elements (tensor tails) are spread over the consumer threads of every
+// CTA afterwards.
+//
+// Streams off the 16 B grid (round 2): a tensor's parameters, gradients and state may
+// each sit at their own element phase within 16 B -- separate parameter allocations
+// against a state at the running sum of the preceding lengths, which an odd-sized tensor
+// shifts.  Such a stream's tile is copied from its aligned-down address, one 16 B
+// granule longer, into a slot 16 B larger, and read / written `sh` elements in.  Its
+// write-back is a bulk store of the tile's 16 B-aligned interior plus element stores of
+// the partial granules at both ends by the consumer threads that hold them (thread 0 the
+// first 4 - sh elements, the last thread the last sh): every element is written by
+// exactly one tile, and the granule a tile shares with its neighbour is only read by the
+// neighbour, never written from its stale copy.
+struct ListStage {  // per stage, written by the producer before the stage is armed
+  float* p;          // this tile's first parameter
+  uint64_t so;       // its state offset
+  int shp, shg, shs;  // stream phases (elements within 16 B)
+};
+
+template <int E>
+__device__ __forceinline__ void lds_sh(const float* s, int sh, float (&r)[E]) {
+  if (sh == 0) {
+    lds<E>(s, r);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) r[j] = s[sh + j];
+  }
+}
+template <int E>
+__device__ __forceinline__ void sts_sh(float* s, int sh, const float (&r)[E]) {
+  if (sh == 0) {
+    sts<E>(s, r);
+  } else {
+#pragma unroll
+    for (int j = 0; j < E; ++j) s[sh + j] = r[j];
+  }
+}
+// the partial 16 B granules of a shifted written stream: global element c0 + j of the
+// tile goes out directly when it lies before the first / after the last aligned granule
+template <int E, int kTile>
+__device__ __forceinline__ void edge_st(float* dst, int c0, int sh, const float (&r)[E]) {
+  if (sh == 0) return;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int cidx = c0 + j;
+    if (cidx < 4 - sh || cidx >= kTile - sh) dst[cidx] = r[j];
+  }
+}
+
+// SH: the launch has shifted streams (an instantiation apart, so that aligned lists keep
+// the unshifted kernel: the runtime phase checks cost 6 % on 24 aligned 4096^2 tensors)
+template <class C, int KIND, typename GT, bool DEV, bool SH>
 __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     list_tma_kernel(const __grid_constant__ FlatList L, float* s0, float* s1, float* s2,
                     float* s3, const StepConsts<float> kv, const GraphStep gs) {
@@ -488,11 +537,14 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
   constexpr int NIN = n_in<KIND>();
   constexpr int NS = stages<C, KIND, false>();
   constexpr int kTile = C::kTile, kConsumers = C::kConsumers, kConsumerWarps = C::CW;
+  constexpr int kSlot = slot_floats<C>();
+  static_assert(C::kEPT == 4, "edge stores assume 4 elements per consumer thread");
   extern __shared__ __align__(128) uint8_t smem[];
-  float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kTile]
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * NIN * kTile);
+  float* buf = reinterpret_cast<float*>(smem);  // [NS][NIN][kSlot]
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + NS * NIN * kSlot);
   uint64_t* done = full + NS;
   __shared__ uint64_t tb[kListMax + 1], eb[kListMax + 1];
+  __shared__ ListStage meta[NS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
@@ -511,9 +563,9 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     if (lane == 0) {
       const bool skip_gp = (KIND == K_ADAN) && k.first;  // g_prev unused at t == 1
       const int nload = skip_gp ? NIN - 1 : NIN;
-      auto where = [&](uint64_t i, float*& p, const GT*& g, uint64_t& so) {
+      auto where = [&](uint64_t i, float*& p, const GT*& g, uint64_t& so, int& q) {
         const uint64_t t = blockIdx.x + i * gridDim.x;
-        const int q = list_find(tb, L.n, t);
+        q = list_find(tb, L.n, t);
         const uint64_t e = (t - tb[q]) * (uint64_t)kTile;
         p = static_cast<float*>(L.p[q]) + e;
         g = static_cast<const GT*>(L.g[q]) + e;
@@ -524,17 +576,30 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         float* p;
         const GT* g;
         uint64_t so;
-        where(i, p, g, so);
-        const float* src[6] = {p, nullptr, s0 + so, s1 + so, s2 + so, s3 + so};
-        constexpr uint32_t gbytes = kTile * sizeof(GT);
-        mbar_expect_tx(&full[s], (uint32_t)((nload - 1) * kTile * 4) + gbytes);
+        int q;
+        where(i, p, g, so, q);
+        const int sp = SH ? L.shp[q] : 0, sg = SH ? L.shg[q] : 0, ss = SH ? L.shs[q] : 0;
+        if constexpr (SH) meta[s] = ListStage{p, so, sp, sg, ss};  // ordered before the arrive
+        const float* src[6] = {p - sp, nullptr, s0 + so - ss, s1 + so - ss, s2 + so - ss,
+                               s3 + so - ss};
+        const uint32_t gbytes = kTile * sizeof(GT) + (sg ? 16u : 0u);
+        const uint32_t pbytes = kTile * 4 + (sp ? 16u : 0u);
+        const uint32_t sbytes = kTile * 4 + (ss ? 16u : 0u);
+        mbar_expect_tx(&full[s], pbytes + gbytes + (uint32_t)(nload - 2) * sbytes);
         for (int j = 0; j < nload; ++j) {
-          float* dst = buf + ((size_t)s * NIN + j) * kTile;
+          float* dst = buf + ((size_t)s * NIN + j) * kSlot;
           if (j == 1)
-            bulk_g2s<false>(dst, g, gbytes, &full[s], 0);
+            bulk_g2s<false>(dst, g - sg, gbytes, &full[s], 0);
           else
-            bulk_g2s<false>(dst, src[j], kTile * 4, &full[s], 0);
+            bulk_g2s<false>(dst, src[j], j == 0 ? pbytes : sbytes, &full[s], 0);
         }
+      };
+      // the tile's 16 B-aligned interior of a written stream (all of it when unshifted)
+      auto store = [&](float* dst, const float* slot, int sh) {
+        if (sh == 0)
+          bulk_s2g<false>(dst, slot, kTile * 4, 0);
+        else
+          bulk_s2g<false>(dst + (4 - sh), slot + 4, (kTile - 4) * 4, 0);
       };
       for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
       for (uint64_t i = 0; i < mine; ++i) {
@@ -543,18 +608,19 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         float* p;
         const GT* g;
         uint64_t so;
-        where(i, p, g, so);
-        float* st = buf + (size_t)s * NIN * kTile;
-        bulk_s2g<false>(p, st, kTile * 4, 0);
-        bulk_s2g<false>(s0 + so, st + 2 * kTile, kTile * 4, 0);
-        if constexpr (KIND == K_ADAMW || KIND == K_ADAN)
-          bulk_s2g<false>(s1 + so, st + 3 * kTile, kTile * 4, 0);
+        int q;
+        where(i, p, g, so, q);
+        const int sp = SH ? L.shp[q] : 0, ss = SH ? L.shs[q] : 0;
+        float* st = buf + (size_t)s * NIN * kSlot;
+        store(p, st, sp);
+        store(s0 + so, st + 2 * kSlot, ss);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) store(s1 + so, st + 3 * kSlot, ss);
         if constexpr (KIND == K_SOPHIA) {
-          if (k.refresh) bulk_s2g<false>(s1 + so, st + 3 * kTile, kTile * 4, 0);
+          if (k.refresh) store(s1 + so, st + 3 * kSlot, ss);
         }
         if constexpr (KIND == K_ADAN) {
-          bulk_s2g<false>(s2 + so, st + 4 * kTile, kTile * 4, 0);
-          bulk_s2g<false>(s3 + so, st + 5 * kTile, kTile * 4, 0);
+          store(s2 + so, st + 4 * kSlot, ss);
+          store(s3 + so, st + 5 * kSlot, ss);
         }
         bulk_commit();
         if (i >= 1 && i - 1 + NS < mine) {  // refill the previous tile's stage (flat kernel)
@@ -570,18 +636,26 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     for (uint64_t i = 0; i < mine; ++i) {
       const int s = (int)(i % NS);
       mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
-      float* st = buf + (size_t)s * NIN * kTile + c0;
+      ListStage m{nullptr, 0, 0, 0, 0};
+      if constexpr (SH) m = meta[s];
+      float* st = buf + (size_t)s * NIN * kSlot + c0;
       float pv[E], gv[E], a[E], b[E], c[E], d[E];
-      lds<E>(st, pv);
-      if constexpr (sizeof(GT) == 4)
-        lds<E>(st + kTile, gv);
-      else
-        lds_grad_bf16<E>(buf + (size_t)s * NIN * kTile + kTile, c0, gv);
-      lds<E>(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) lds<E>(st + 3 * kTile, b);
+      lds_sh<E>(st, m.shp, pv);
+      if (m.shg == 0) {
+        if constexpr (sizeof(GT) == 4)
+          lds<E>(st + kSlot, gv);
+        else
+          lds_grad_bf16<E>(buf + (size_t)s * NIN * kSlot + kSlot, c0, gv);
+      } else {
+        const GT* gslot = reinterpret_cast<const GT*>(buf + (size_t)s * NIN * kSlot + kSlot) + m.shg + c0;
+#pragma unroll
+        for (int j = 0; j < E; ++j) gv[j] = load_grad1(gslot + j);
+      }
+      lds_sh<E>(st + 2 * kSlot, m.shs, a);
+      if constexpr (KIND != K_LION) lds_sh<E>(st + 3 * kSlot, m.shs, b);
       if constexpr (KIND == K_ADAN) {
-        lds<E>(st + 4 * kTile, c);
-        if (!k.first) lds<E>(st + 5 * kTile, d);
+        lds_sh<E>(st + 4 * kSlot, m.shs, c);
+        if (!k.first) lds_sh<E>(st + 5 * kSlot, m.shs, d);
       }
 #pragma unroll
       for (int j = 0; j < E; ++j) {
@@ -592,12 +666,24 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         }
         update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
       }
-      sts<E>(st, pv);
-      sts<E>(st + 2 * kTile, a);
-      if constexpr (KIND != K_LION) sts<E>(st + 3 * kTile, b);
+      sts_sh<E>(st, m.shp, pv);
+      sts_sh<E>(st + 2 * kSlot, m.shs, a);
+      if constexpr (KIND != K_LION) sts_sh<E>(st + 3 * kSlot, m.shs, b);
       if constexpr (KIND == K_ADAN) {
-        sts<E>(st + 4 * kTile, c);
-        sts<E>(st + 5 * kTile, d);
+        sts_sh<E>(st + 4 * kSlot, m.shs, c);
+        sts_sh<E>(st + 5 * kSlot, m.shs, d);
+      }
+      if constexpr (SH) {  // partial granules of shifted written streams, to global memory
+        edge_st<E, kTile>(m.p, c0, m.shp, pv);
+        edge_st<E, kTile>(s0 + m.so, c0, m.shs, a);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) edge_st<E, kTile>(s1 + m.so, c0, m.shs, b);
+        if constexpr (KIND == K_SOPHIA) {
+          if (k.refresh) edge_st<E, kTile>(s1 + m.so, c0, m.shs, b);
+        }
+        if constexpr (KIND == K_ADAN) {
+          edge_st<E, kTile>(s2 + m.so, c0, m.shs, c);
+          edge_st<E, kTile>(s3 + m.so, c0, m.shs, d);
+        }
       }
       fence_proxy_async();
       mbar_arrive(&done[s]);
@@ -634,11 +720,11 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
 
 using ListCfg = TmaCfg<16, 4>;
 
-template <int KIND, typename GT, bool DEV>
-void run_list_tma(const FlatList& L, float* const* s, const StepConsts<float>& k,
-                  const GraphStep& gs, cudaStream_t st) {
+template <int KIND, typename GT, bool DEV, bool SH>
+void run_list_tma_sh(const FlatList& L, float* const* s, const StepConsts<float>& k,
+                     const GraphStep& gs, cudaStream_t st) {
   using C = ListCfg;
-  auto kern = list_tma_kernel<C, KIND, GT, DEV>;
+  auto kern = list_tma_kernel<C, KIND, GT, DEV, SH>;
   constexpr int smem = smem_bytes<C, KIND, false>();
   const int dev = current_device();
   static std::atomic<uint64_t> attr_set{0};
@@ -651,6 +737,18 @@ void run_list_tma(const FlatList& L, float* const* s, const StepConsts<float>& k
   const int grid = (int)std::min<uint64_t>(want, (uint64_t)device_info(dev).sms);
   kern<<<grid, C::kConsumers + 32, smem, st>>>(L, s[0], s[1], s[2], s[3], k, gs);
   launch_check("list_tma_kernel");
+}
+
+template <int KIND, typename GT, bool DEV>
+void run_list_tma(const FlatList& L, float* const* s, const StepConsts<float>& k,
+                  const GraphStep& gs, cudaStream_t st) {
+  bool sh = false;
+  for (int i = 0; i < L.n && !sh; ++i)
+    sh = L.vbeg[i + 1] > L.vbeg[i] && (L.shp[i] || L.shg[i] || L.shs[i]);
+  if (sh)
+    run_list_tma_sh<KIND, GT, DEV, true>(L, s, k, gs, st);
+  else
+    run_list_tma_sh<KIND, GT, DEV, false>(L, s, k, gs, st);
 }
 
 template <int KIND, typename GT>

@@ -46,6 +46,9 @@ struct FlatList {  // one launch (kernel parameter)
   void* p[kListMax];
   const void* g[kListMax];
   uint64_t soff[kListMax];          // state offset (elements)
+  // TMA list form: each stream's element phase within 16 B (params, grads, state) --
+  // streams off the 16 B grid are copied from their aligned-down address (list_tma_kernel)
+  uint8_t shp[kListMax], shg[kListMax], shs[kListMax];
 };
 struct FlatListArgs {
   int kind;

@@ -173,6 +173,20 @@ def phases(W, K):
         g = gb[go:go + n]
         ms = timed(lambda: optim.lomo_apply(p, g, 1e-3, 1.0), W, K)
         line(f"lomo 2^30, gradient at element offset {go}", n, ms, 12)
+    del p, gb
+    # list form over separate tensors: a (7,) tensor first shifts every later tensor's
+    # state off its parameters' 16 B phase (round 1: those tensors took the scalar path)
+    for lead in (0, 7):
+        shapes = ([(lead,)] if lead else []) + [(4096, 4096)] * 24
+        ps = [torch.empty(s_, device="cuda").normal_(0, 0.02) for s_ in shapes]
+        gs = [torch.empty(s_, device="cuda").normal_(0, 1e-3) for s_ in shapes]
+        m = sum(x.numel() for x in ps)
+        cfg = OptimizerConfig.defaults_for(Kind.ADAMW)
+        opt = optim.FlatOptimizer(cfg, m)
+        ms = timed(lambda: opt.step_list(ps, gs, 1e-5), W, K)
+        line(f"adamw list form, 24 x 4096^2 tensors{' after a (7,) tensor' if lead else ''}",
+             m, ms, 28)
+        del ps, gs, opt
 
 
 def cliff(W, K):
