@@ -582,6 +582,27 @@ void launch_flat_step(const FlatArgs& a, const StepConsts<float>& kf,
     // the other streams as below, the TMA pipeline reads the gradient shifted
     ph = common_phase({{a.p, ps}, {a.s[0], ss}, {a.s[1], ss}, {a.s[2], ss}, {a.s[3], ss},
                        {a.p_out_bf16, 2}});
+    if (ph < 0 && !a.p_out_bf16 && a.state_dtype == MCO_F32 && a.p_dtype == MCO_F32 &&
+        flat_variant() == V_TMA) {
+      // parameters and state disagree too (a caller-laid-out state): a one-tensor list
+      // step -- the list pipeline reads and writes every stream at its own phase
+      FlatListArgs la{};
+      la.kind = a.kind;
+      la.state_dtype = a.state_dtype;
+      la.p_dtype = a.p_dtype;
+      la.g_dtype = a.g_dtype;
+      la.count = 1;
+      void* pp[1] = {a.p};
+      const void* gp[1] = {a.g};
+      const uint64_t len[1] = {a.n};
+      la.p = pp;
+      la.g = gp;
+      la.len = len;
+      for (int i = 0; i < 4; ++i) la.s[i] = a.s[i];
+      la.gs = a.gs;
+      launch_flat_step_list(la, kf, kd, st);
+      return;
+    }
   }
   if (ph <= 0 || a.n <= (uint64_t)(8 - ph)) {
     launch_flat_one(a, kf, kd, st);

@@ -451,3 +451,29 @@ def test_lomo_gradient_phase_shift_bit_exact(dt):
             got = tp[po:po + n].cpu().numpy() if dt == "f32" else \
                 tp[po:po + n].view(torch.int16).cpu().numpy()
             assert bits_equal(got, p), (po, go)
+
+
+@pytest.mark.parametrize("kind", FLAT)
+def test_params_and_state_at_different_phases_bit_exact(kind):
+    """State laid out before the first step (buffers() handed out: its phase is frozen at
+    the allocation's) against parameters / gradients at other phases: the step runs as a
+    one-tensor list step on the TMA list pipeline (every stream read and written at its
+    own phase) -- the restatement's bits, state included."""
+    n = 5 * 2048 + 13
+    cfg = cfg_for(kind, weight_decay=0.01, update_interval=2)
+    P = O.synth(n + 16, 21, 0, 7, 0, 0, -6, 0, False)
+    G = [O.synth(n + 16, 21, 1, 7, t, 0, -7, 10, False) for t in (1, 2, 3)]
+    for po, go in [(3, 3), (1, 6), (5, 0), (0, 7)]:
+        p = P[po:po + n].copy()
+        tp = dev(P)[po:po + n]
+        tG = [dev(x) for x in G]
+        opt = optim.FlatOptimizer(cfg, n)
+        _ = opt.buffers()  # layout frozen at phase 0
+        orc = O.OracleFlat(cfg, n, np.float32)
+        for t in range(3):
+            opt.step(tp, tG[t][go:go + n], 1e-3)
+            orc.step(p, G[t][go:go + n].copy(), 1e-3)
+        torch.cuda.synchronize()
+        assert bits_equal(tp.cpu().numpy(), p), (po, go)
+        for name, buf in opt.buffers():
+            assert bits_equal(buf.cpu().numpy(), orc.state[name]), (po, go, name)
