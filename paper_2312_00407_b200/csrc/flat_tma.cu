@@ -34,7 +34,11 @@ using namespace upd;
 // (measured: fewer starve the loads, more lose bandwidth for AdamW / Sophia).
 // EPT: elements per consumer thread per stream and stage (4: float4, 2: float2);
 // HINT: bulk copies carry an L2 evict-first cache policy (streams are touched once).
-template <int CW_, int NS_, int EPT_ = 4, bool HINT_ = false>
+// DS: direct stores -- the consumers copy a stage into registers, release it at once
+// and write their results straight to global memory (coalesced 16 B stores) instead of
+// staging them back through shared memory for the producer's bulk stores: a stage is
+// busy only while it loads, so more of the pipeline's bytes are loads in flight.
+template <int CW_, int NS_, int EPT_ = 4, bool HINT_ = false, bool DS_ = false>
 struct TmaCfg {
   static constexpr int CW = CW_;
   static constexpr int kConsumers = CW * 32;
@@ -42,6 +46,7 @@ struct TmaCfg {
   static constexpr int kTile = CW * 32 * EPT_;  // elements per stream per stage
   static constexpr int kStages = NS_;
   static constexpr bool kHint = HINT_;
+  static constexpr bool kDS = DS_;
 };
 constexpr int kSmemMax = 220 * 1024;
 
@@ -160,6 +165,13 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         }
       };
       for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
+      if constexpr (C::kDS) {  // consumers store directly: refill each stage once released
+        for (uint64_t i = 0; i + NS < mine; ++i) {
+          mbar_wait(&done[(int)(i % NS)], (uint32_t)((i / NS) & 1));
+          issue(i + NS);
+        }
+        return;
+      }
       for (uint64_t i = 0; i < mine; ++i) {
         const int s = (int)(i % NS);
         mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
@@ -212,6 +224,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         lds<E>(st + 4 * kSlot, c);
         if (!k.first) lds<E>(st + 5 * kSlot, d);
       }
+      if constexpr (C::kDS) mbar_arrive(&done[s]);  // the stage is in registers: release it
 #pragma unroll
       for (int j = 0; j < E; ++j) {
         if constexpr (KIND == K_LION) b[j] = 0.f;
@@ -220,6 +233,29 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
           if (k.first) d[j] = 0.f;
         }
         update<KIND, float>(pv[j], gv[j], a[j], b[j], c[j], d[j], k);
+      }
+      if constexpr (C::kDS) {
+        const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kTile + c0;
+        st_stream(p + e, pv);
+        st_stream(s0 + e, a);
+        if constexpr (KIND == K_ADAMW || KIND == K_ADAN) st_stream(s1 + e, b);
+        if constexpr (KIND == K_SOPHIA) {
+          if (k.refresh) st_stream(s1 + e, b);
+        }
+        if constexpr (KIND == K_ADAN) {
+          st_stream(s2 + e, c);
+          st_stream(s3 + e, d);
+        }
+        if constexpr (MIXED) {
+          uint32_t w[E / 2];
+#pragma unroll
+          for (int j = 0; j < E / 2; ++j) w[j] = f2bf2_bits(pv[2 * j], pv[2 * j + 1]);
+          if constexpr (E == 4)
+            *reinterpret_cast<uint2*>(pout + e) = make_uint2(w[0], w[1]);
+          else
+            *reinterpret_cast<uint32_t*>(pout + e) = w[0];
+        }
+        continue;
       }
       sts<E>(st, pv);
       sts<E>(st + 2 * kSlot, a);
@@ -794,7 +830,8 @@ bool flat_tma_eligible(const FlatArgs& a, int cfg) {
   X(4, (TmaCfg<8, 4>))              \
   X(5, (TmaCfg<16, 8, 2>))          \
   X(6, (TmaCfg<16, 4, 4, true>))    \
-  X(7, (TmaCfg<24, 6, 2>))
+  X(7, (TmaCfg<24, 6, 2>))          \
+  X(8, (TmaCfg<16, 4, 4, false, true>))
 
 int tma_tile(int cfg) {
   switch (cfg) {

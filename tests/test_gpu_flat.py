@@ -265,7 +265,7 @@ def flat_variant():
     optim.set_flat_variant(prev)
 
 
-@pytest.mark.parametrize("variant", ["ldg", "tma", "tma_s3", "tma24", "tma8", "tma_e2", "tma_hint", "pf", "w4m4", "l2pf2"])
+@pytest.mark.parametrize("variant", ["ldg", "tma", "tma_s3", "tma24", "tma8", "tma_e2", "tma_hint", "tma_ds", "pf", "w4m4", "l2pf2"])
 @pytest.mark.parametrize("kind", FLAT)
 @pytest.mark.parametrize("n", [2048, 3 * 3072 + 77, (1 << 20) + 5])
 def test_kernel_variants_bit_exact(flat_variant, variant, kind, n):
