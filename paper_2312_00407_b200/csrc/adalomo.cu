@@ -182,19 +182,72 @@ __device__ __forceinline__ void store_p(PT* p, const float (&r)[VW], int valid) 
     if (j < valid) stp1(p + j, r[j]);
 }
 
-// One lane's 8-column chunk of one row, held in load form until it is consumed: fp32
-// as 8 floats, bf16 as the 4 raw 32-bit words (half the registers), so the bf16 tile
-// kernels can keep twice the rows in flight (rows_in_flight) without spilling.
-// On the vector path (C % 8 == 0, so a lane's chunk is either whole or outside the tile)
-// a load is always a whole 8-element vector: callers load only lanes with valid > 0.
+constexpr int kLaneStride = 32;  // scalar-path tile lanes: column stride (lane_cols)
+// a tile lane's 8 columns back (vector or strided scalar layout, lane_cols)
+template <bool VEC, typename PT>
+__device__ __forceinline__ void store_tile(PT* p, const float (&r)[VW], int valid) {
+  if constexpr (VEC) {
+    store_p<VEC, PT>(p, r, VW);
+  } else {
+#pragma unroll
+    for (int j = 0; j < VW; ++j)
+      if (j < valid) stp1(p + kLaneStride * j, r[j]);
+  }
+}
+
+// A tile lane's 8 columns of one row.  Vector path: 8 contiguous columns, one 256-bit
+// (fp32) / 128-bit (bf16) access.  Scalar path (rows off the 8-element grid: C % 8 != 0,
+// or a tensor behind an odd-sized one in a flat buffer): the warp's 256 columns are dealt
+// out strided -- lane l of warp w in the row group takes columns 256 w + l + 32 j -- so
+// every load / store instruction of the warp covers 32 consecutive elements (coalesced,
+// any alignment) instead of 32 lanes each touching its own 32 B (round 1: 8 scalar
+// accesses per lane 32 B apart, 0.5 of the copy bandwidth).  `valid` = how many of the
+// lane's 8 columns lie in the tile (always a prefix in either layout).
+template <bool VEC>
+__device__ __forceinline__ void lane_cols(const Tile& tl, int lane_c, int64_t& col, int& cs,
+                                          int& valid) {
+  if constexpr (VEC) {
+    col = tl.c0 + (int64_t)lane_c * VW;
+    cs = 1;
+    valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+  } else {
+    col = tl.c0 + (int64_t)(lane_c >> 5) * (32 * VW) + (lane_c & 31);
+    cs = kLaneStride;
+    valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, (tl.c1 - col + kLaneStride - 1) /
+                                                                kLaneStride));
+  }
+}
+// column offset within the tile -> (lane, element) of the layout above
+template <bool VEC>
+__device__ __forceinline__ void col_lane(int q, int& lane_c, int& j) {
+  if constexpr (VEC) {
+    lane_c = q / VW;
+    j = q % VW;
+  } else {
+    lane_c = (q / (32 * VW)) * 32 + (q % 32);
+    j = (q % (32 * VW)) / 32;
+  }
+}
+
+// Held in load form until consumed: fp32 as 8 floats, bf16 as the 4 raw 32-bit words
+// (half the registers), so the bf16 tile kernels can keep twice the rows in flight
+// (rows_in_flight) without spilling.  On the vector path (C % 8 == 0, so a lane's chunk
+// is either whole or outside the tile) a load is always a whole 8-element vector:
+// callers load only lanes with valid > 0.
 template <bool VEC, typename T, bool RO>
 struct RowVec {
   float v[VW];
   __device__ __forceinline__ void load(const T* src, int valid) {
-    if constexpr (RO)
-      load_vec<VEC, T>(src, v, VEC ? VW : valid);
-    else
-      load_p<VEC, T>(src, v, VEC ? VW : valid);
+    if constexpr (VEC) {
+      if constexpr (RO)
+        load_vec<VEC, T>(src, v, VW);
+      else
+        load_p<VEC, T>(src, v, VW);
+    } else {
+#pragma unroll
+      for (int j = 0; j < VW; ++j)
+        v[j] = j < valid ? (RO ? ld1(src + kLaneStride * j) : ldp1(src + kLaneStride * j)) : 0.f;
+    }
   }
   __device__ __forceinline__ void get(float (&r)[VW]) const {
 #pragma unroll
@@ -221,9 +274,9 @@ struct RowVec<VEC, uint16_t, RO> {
       return;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const uint32_t lo = 2 * k < valid ? src[2 * k] : 0u;
-      const uint32_t hi = 2 * k + 1 < valid ? src[2 * k + 1] : 0u;
+    for (int k = 0; k < 4; ++k) {  // strided scalar layout (lane_cols)
+      const uint32_t lo = 2 * k < valid ? src[kLaneStride * (2 * k)] : 0u;
+      const uint32_t hi = 2 * k + 1 < valid ? src[kLaneStride * (2 * k + 1)] : 0u;
       w[k] = lo | (hi << 16);
     }
   }
@@ -310,8 +363,9 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
     if (T.factored) {
       const int TC = T.tc, TR = kThreads / T.tc;
       const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
-      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
-      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      int64_t col;
+      int cs, valid;
+      lane_cols<VEC>(tl, lane_c, col, cs, valid);
       const int wrow = (threadIdx.x % TC) >> 5;  // warp index within the row group
       const int nwr = TC >> 5;
       float cacc[VW];
@@ -381,7 +435,8 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
       __syncthreads();
       const int64_t w = tl.c1 - tl.c0;
       for (int64_t q = threadIdx.x; q < w; q += kThreads) {
-        const int lc = (int)(q / VW), j = (int)(q % VW);
+        int lc, j;
+        col_lane<VEC>((int)q, lc, j);
         float s = 0.f;
         for (int k = 0; k < TR; ++k) s += colbuf[(k * TC + lc) * VW + j];
         c.colpart[T.colpart_off + tl.rb * T.cols + tl.c0 + q] = s;
@@ -789,15 +844,16 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
     if (T.factored) {
       const int TC = T.tc, TR = kThreads / T.tc;
       const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
-      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
-      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      int64_t col;
+      int cs, valid;
+      lane_cols<VEC>(tl, lane_c, col, cs, valid);
       if (valid > 0) {
         const bool sep = sep_ok(c, tl.tensor, eps);
         const float* fa = (sep ? c.fra : c.fa) + T.fa_off;
         float bv[VW];
 #pragma unroll
         for (int j = 0; j < VW; ++j)
-          bv[j] = j < valid ? (sep ? c.frb : c.fb)[T.fb_off + col + j] : 0.f;
+          bv[j] = j < valid ? (sep ? c.frb : c.fb)[T.fb_off + col + j * cs] : 0.f;
         constexpr int RB = k4_rows<GT>();
         const int64_t rstep = (int64_t)TR * T.cols;  // row pointers advance by adds
         uint64_t bv2[VW / 2];
@@ -1192,12 +1248,13 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
       const float ff = (float)f;
       const int TC = T.tc, TR = kThreads / T.tc;
       const int lane_c = threadIdx.x % TC, tr = threadIdx.x / TC;
-      const int64_t col = tl.c0 + (int64_t)lane_c * VW;
-      const int valid = (int)std::min<int64_t>(VW, std::max<int64_t>(0, tl.c1 - col));
+      int64_t col;
+      int cs, valid;
+      lane_cols<VEC>(tl, lane_c, col, cs, valid);
       if (valid <= 0) continue;
       float bv[VW];
 #pragma unroll
-      for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j] : 0.f;
+      for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j * cs] : 0.f;
       const float* fa = c.fa + T.fa_off;
       constexpr int RB = rows_in_flight<GT, PT>();
       const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
@@ -1221,7 +1278,7 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
             gr[b].get(gv);
             pr[b].get(pv);
             k6_row8(pv, gv, fa[r0 + (int64_t)b * TR], bv, sf, ff, epsf);
-            store_p<VEC, PT>(p + o, pv, VEC ? VW : valid);
+            store_tile<VEC, PT>(p + o, pv, valid);
           }
         }
         roff = o;
@@ -1507,7 +1564,7 @@ void launch_k6(Launch L, const AdaLomoPlan& pl, const AdaLomoCall& call, int fil
   const bool tma_ok = VEC && !filt && k6_tma_ok(pl, call, sizeof(GT), sizeof(PT));
   const int k6 = k6_force == 3 && tma_ok               ? 3
                  : k6_force == 1 || k6_force == 2      ? k6_force
-                 : call.single                         ? 2
+                 : call.single && VEC                  ? 2  // scalar rows: strided tiles
                                                        : 1;
   const double eps = pl.cfg.eps;
   if (k6 == 3) {

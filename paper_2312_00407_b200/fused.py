@@ -86,12 +86,18 @@ class _GradPath:
             return
         if self.buf is None or self.buf.dtype != p.grad.dtype or self.buf.device != p.grad.device:
             self.flush()
-            self.buf = torch.empty(self.bucket_elems, dtype=p.grad.dtype, device=p.grad.device)
-        if self.used + n > self.bucket_elems:
+            # zeros: the alignment gaps below only ever hold finite values
+            self.buf = torch.zeros(self.bucket_elems, dtype=p.grad.dtype, device=p.grad.device)
+        # every packed gradient starts on the 8-element grid, as a separately allocated
+        # gradient would: the update kernels take their vector path for it, and the
+        # result equals the per-parameter path bit for bit
+        start = (self.used + 7) // 8 * 8
+        if start + n > self.bucket_elems:
             self.flush()
-        self.buf[self.used:self.used + n].copy_(p.grad.reshape(-1))
-        self.items.append((p, self.used, n))
-        self.used += n
+            start = 0
+        self.buf[start:start + n].copy_(p.grad.reshape(-1))
+        self.items.append((p, start, n))
+        self.used = start + n
         p.grad = None
 
     def flush(self) -> None:
