@@ -72,7 +72,10 @@ constexpr int kMinCtasK4 = MCO_K4_MINB;
 #define MCO_K6_MINB 3
 #endif
 #ifndef MCO_K6_MINB_BF16
-#define MCO_K6_MINB_BF16 4  // 64 registers (56 B spilled): 16.93 -> 16.50 ms on 7B bf16
+// round 1: 4 (64 registers, 56 B spilled) won, 16.93 -> 16.50 ms on 7B bf16; after the
+// round-2 K6 (one FMA for p - f u) 3 CTAs with 80 registers and no spills win: 7B bf16
+// 13.95-14.06 -> 13.68 ms, same box (K1 / K4 caps re-measured: 3 stays best)
+#define MCO_K6_MINB_BF16 3
 #endif
 #ifndef MCO_K1_MINB_BF16
 #define MCO_K1_MINB_BF16 MCO_K1_MINB
