@@ -20,9 +20,15 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "launch.cuh"
+#include "tma.cuh"
 
 namespace mco {
 namespace {
@@ -97,12 +103,159 @@ __global__ void __launch_bounds__(256) sophia_m64_kernel(float* __restrict__ p,
   }
 }
 
+// The same update on the cp.async.bulk pipeline (flat_tma.cu's design): one producer
+// lane copies a 2048-element tile of p, g, m (fp64) and h into stage s (mbarrier
+// complete_tx), 16 consumer warps update it in shared memory (4 elements per thread, the
+// fp64 arithmetic of sm64_one), and the producer writes p, m (and h on refresh steps)
+// back with bulk stores, refilling the previous tile's stage.  40 KB per stage (fp32 g),
+// 5 stages.  The < 1-tile tail is done by CTA 0's consumers with plain accesses.
+constexpr int kM64Warps = 16, kM64Consumers = kM64Warps * 32, kM64Tile = kM64Consumers * 4;
+template <typename GT>
+constexpr int m64_stage_bytes() {
+  return kM64Tile * (4 + (int)sizeof(GT) + 8 + 4);  // p | g | m | h
+}
+template <typename GT>
+constexpr int m64_stages() {
+  return std::min(5, (210 * 1024) / m64_stage_bytes<GT>());
+}
+template <typename GT>
+constexpr int m64_smem() {
+  return m64_stages<GT>() * m64_stage_bytes<GT>() + 2 * m64_stages<GT>() * 8;
+}
+
+template <typename GT>
+__global__ void __launch_bounds__(kM64Consumers + 32, 1)
+    sophia_m64_tma(float* __restrict__ p, const GT* __restrict__ g, double* __restrict__ m,
+                   float* __restrict__ h, uint64_t ntiles, uint64_t n, SophiaM64Consts k) {
+  constexpr int NS = m64_stages<GT>();
+  constexpr int SB = m64_stage_bytes<GT>();
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * SB);
+  uint64_t* done = full + NS;
+  // stage layout: m (fp64, 16 KB, first: 8 B aligned) | p | h | g
+  auto sm = [&](int s) { return reinterpret_cast<double*>(smem + s * SB); };
+  auto sp = [&](int s) { return reinterpret_cast<float*>(smem + s * SB + kM64Tile * 8); };
+  auto sh = [&](int s) { return reinterpret_cast<float*>(smem + s * SB + kM64Tile * 12); };
+  auto sg = [&](int s) { return reinterpret_cast<GT*>(smem + s * SB + kM64Tile * 16); };
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&done[s], kM64Consumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint64_t mine =
+      ntiles > blockIdx.x ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  if (warp == kM64Warps) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      constexpr uint32_t bytes = kM64Tile * (4 + (uint32_t)sizeof(GT) + 8 + 4);
+      auto issue = [&](uint64_t i) {
+        const int s = (int)(i % NS);
+        const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kM64Tile;
+        mbar_expect_tx(&full[s], bytes);
+        bulk_g2s<false>(sm(s), m + e, kM64Tile * 8, &full[s], 0);
+        bulk_g2s<false>(sp(s), p + e, kM64Tile * 4, &full[s], 0);
+        bulk_g2s<false>(sh(s), h + e, kM64Tile * 4, &full[s], 0);
+        bulk_g2s<false>(sg(s), g + e, kM64Tile * (uint32_t)sizeof(GT), &full[s], 0);
+      };
+      for (uint64_t i = 0; i < mine && i < (uint64_t)NS; ++i) issue(i);
+      for (uint64_t i = 0; i < mine; ++i) {
+        const int s = (int)(i % NS);
+        mbar_wait(&done[s], (uint32_t)((i / NS) & 1));
+        const uint64_t e = (blockIdx.x + i * gridDim.x) * (uint64_t)kM64Tile;
+        bulk_s2g<false>(m + e, sm(s), kM64Tile * 8, 0);
+        bulk_s2g<false>(p + e, sp(s), kM64Tile * 4, 0);
+        if (k.refresh) bulk_s2g<false>(h + e, sh(s), kM64Tile * 4, 0);
+        bulk_commit();
+        if (i >= 1 && i - 1 + NS < mine) {  // refill the previous tile's stage
+          bulk_wait_read_1();
+          issue(i - 1 + NS);
+        }
+      }
+      bulk_wait_all();
+    }
+  } else {  // ---------------- consumers ----------------
+    const int c0 = threadIdx.x * 4;
+    for (uint64_t i = 0; i < mine; ++i) {
+      const int s = (int)(i % NS);
+      mbar_wait(&full[s], (uint32_t)((i / NS) & 1));
+      float4 pv = *reinterpret_cast<const float4*>(sp(s) + c0);
+      float4 hv = *reinterpret_cast<const float4*>(sh(s) + c0);
+      double2 m01 = *reinterpret_cast<const double2*>(sm(s) + c0);
+      double2 m23 = *reinterpret_cast<const double2*>(sm(s) + c0 + 2);
+      float gv[4];
+      if constexpr (sizeof(GT) == 4) {
+        const float4 x = *reinterpret_cast<const float4*>(sg(s) + c0);
+        gv[0] = x.x, gv[1] = x.y, gv[2] = x.z, gv[3] = x.w;
+      } else {
+        const uint2 w = *reinterpret_cast<const uint2*>(sg(s) + c0);
+        gv[0] = __uint_as_float(w.x << 16), gv[1] = __uint_as_float(w.x & 0xffff0000u);
+        gv[2] = __uint_as_float(w.y << 16), gv[3] = __uint_as_float(w.y & 0xffff0000u);
+      }
+      pv.x = sm64_one(pv.x, gv[0], m01.x, hv.x, k);
+      pv.y = sm64_one(pv.y, gv[1], m01.y, hv.y, k);
+      pv.z = sm64_one(pv.z, gv[2], m23.x, hv.z, k);
+      pv.w = sm64_one(pv.w, gv[3], m23.y, hv.w, k);
+      *reinterpret_cast<float4*>(sp(s) + c0) = pv;
+      *reinterpret_cast<double2*>(sm(s) + c0) = m01;
+      *reinterpret_cast<double2*>(sm(s) + c0 + 2) = m23;
+      if (k.refresh) *reinterpret_cast<float4*>(sh(s) + c0) = hv;
+      fence_proxy_async();
+      mbar_arrive(&done[s]);
+    }
+    if (blockIdx.x == 0) {  // tail (< one tile)
+      for (uint64_t e = ntiles * kM64Tile + threadIdx.x; e < n; e += kM64Consumers) {
+        double mm = m[e];
+        float hh = h[e];
+        p[e] = sm64_one(p[e], load_g(g, e), mm, hh, k);
+        m[e] = mm;
+        if (k.refresh) h[e] = hh;
+      }
+    }
+  }
+}
+
+template <typename GT>
+void run_m64_tma(float* p, const GT* g, double* m, float* h, uint64_t n,
+                 const SophiaM64Consts& k, cudaStream_t st) {
+  auto kern = sophia_m64_tma<GT>;
+  constexpr int smem = m64_smem<GT>();
+  const int dev = current_device();
+  static std::atomic<uint64_t> attr_set{0};  // per device: dynamic smem opt-in done
+  if (!(attr_set.load() & (1ull << dev))) {
+    MCO_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_set.fetch_or(1ull << dev);
+  }
+  const uint64_t ntiles = n / kM64Tile;
+  const int grid = (int)std::max<uint64_t>(
+      1, std::min<uint64_t>(ntiles ? ntiles : 1, (uint64_t)device_info(dev).sms));
+  kern<<<grid, kM64Consumers + 32, smem, st>>>(p, g, m, h, ntiles, n, k);
+  launch_check("sophia_m64_tma");
+}
+
 }  // namespace
 
 void launch_sophia_m64(float* p, const void* g, int g_dtype, double* m, float* h, uint64_t n,
                        const StepConsts<double>& kd, cudaStream_t st) {
   if (n == 0) return;
   SophiaM64Consts k{kd.b1, kd.omb1, kd.b2, kd.omb2, kd.rho, kd.eps, kd.lr, kd.lrwd, kd.refresh};
+  // the bulk-copy pipeline when every stream is 16 B aligned and there is a whole tile
+  // (MCO_SOPHIA_M64=ldg keeps the LDG kernel: A/B knob)
+  static const bool ldg_only = [] {
+    const char* e = getenv("MCO_SOPHIA_M64");
+    return e && std::string(e) == "ldg";
+  }();
+  const size_t gsz0 = g_dtype == MCO_BF16 ? 2 : 4;
+  if (!ldg_only && n >= (uint64_t)kM64Tile && (uintptr_t)p % 16 == 0 && (uintptr_t)h % 16 == 0 &&
+      (uintptr_t)m % 16 == 0 && (uintptr_t)g % 16 == 0 && gsz0) {
+    if (g_dtype == MCO_BF16)
+      run_m64_tma<uint16_t>(p, (const uint16_t*)g, m, h, n, k, st);
+    else
+      run_m64_tma<float>(p, (const float*)g, m, h, n, k, st);
+    return;
+  }
   // head: elements until p is 16 B aligned; the vector path needs every stream aligned
   // at that element (same element phase), else everything is scalar
   const uint64_t ph = ((uintptr_t)p / 4) % 4;

@@ -477,3 +477,29 @@ def test_params_and_state_at_different_phases_bit_exact(kind):
         assert bits_equal(tp.cpu().numpy(), p), (po, go)
         for name, buf in opt.buffers():
             assert bits_equal(buf.cpu().numpy(), orc.state[name]), (po, go, name)
+
+
+@pytest.mark.parametrize("gdt", ["f32", "bf16"])
+@pytest.mark.parametrize("n,off", [(2048, 0), (5 * 2048 + 77, 0), (3 * 2048 + 5, 3), (1000, 0)])
+def test_sophia_precise_m_paths_bit_exact(gdt, n, off):
+    """Sophia precise-m (fp64 m) on the bulk-copy pipeline (aligned, whole tiles + tail)
+    and on the LDG kernel (views off the 16 B grid, less than a tile): the restatement's
+    bits for p, m and h over refresh and non-refresh steps, fp32 and bf16 gradients."""
+    cfg = cfg_for(Kind.SOPHIA, weight_decay=0.01, update_interval=2)
+    P = O.synth(n + 8, 31, 0, 2, 0, 0, -6, 0, False)
+    p = P[off:off + n].copy()
+    tp = dev(P)[off:off + n]
+    opt = optim.FlatOptimizer(cfg, n, state_dtype="f32m64")
+    orc = O.OracleSophiaM64(cfg, n)
+    for t in range(1, 5):
+        g = O.synth(n + 8, 31, 1, 2, t, 0, -7, 10, False)
+        if gdt == "bf16":
+            g = O.bf16_to_f32(O.f32_to_bf16(g))
+        tg = dev(g) if gdt == "f32" else dev(g).to(torch.bfloat16)
+        opt.step(tp, tg[off:off + n], 1e-3)
+        orc.step(p, g[off:off + n].copy(), 1e-3)
+    torch.cuda.synchronize()
+    assert bits_equal(tp.cpu().numpy(), p)
+    st = dict(opt.buffers())
+    assert bits_equal(st["m"].cpu().numpy(), orc.state["m"])
+    assert bits_equal(st["h"].cpu().numpy(), orc.state["h"])
