@@ -393,12 +393,12 @@ __global__ void synth_kernel(void* dst, int dtype, uint64_t n, uint64_t key, int
 // produces the same bits.
 enum Variant {
   V_TMA, V_LDG, V_W4M4, V_W8M4, V_W4M1, V_PF, V_U1M3, V_U2M3, V_L2PF1, V_L2PF2, V_L2PF4,
-  V_TMA_S3, V_TMA_S5, V_TMA24, V_TMA8, V_TMA_E2, V_TMA_HINT, V_TMA24_E2, V_TMA_DS, V_COUNT
+  V_TMA_S3, V_TMA_S5, V_TMA24, V_TMA8, V_TMA_E2, V_TMA_HINT, V_TMA24_E2, V_TMA_DS, V_TMA_S2, V_COUNT
 };
 const char* const kVariantNames[V_COUNT] = {
     "tma",   "ldg",   "w4m4",  "w8m4",   "w4m1",   "pf",    "u1m3", "u2m3",
     "l2pf1", "l2pf2", "l2pf4", "tma_s3", "tma_s5", "tma24", "tma8",
-    "tma_e2", "tma_hint", "tma24_e2", "tma_ds"};
+    "tma_e2", "tma_hint", "tma24_e2", "tma_ds", "tma_s2"};
 std::atomic<int> g_variant{-1};
 
 int parse_flat_variant(const char* name) {
@@ -435,7 +435,9 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
     const int variant = dev_step ? (flat_variant() == V_LDG ? V_LDG : V_TMA) : flat_variant();
     int tma_cfg = -1;  // flat_tma.h configurations
     switch (variant) {
-      case V_TMA: tma_cfg = 0; break;
+      // Adan: 3 stages (7B, same box: 45.52 vs 46.62 ms at 4; the other kinds lose 15-30 %
+      // with 3 -- AdamW 34.2 vs 29.2 ms -- and keep 4)
+      case V_TMA: tma_cfg = KIND == K_ADAN ? 1 : 0; break;
       case V_TMA_S3: tma_cfg = 1; break;
       case V_TMA_S5: tma_cfg = 2; break;
       case V_TMA24: tma_cfg = 3; break;
@@ -444,6 +446,7 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       case V_TMA_HINT: tma_cfg = 6; break;
       case V_TMA24_E2: tma_cfg = 7; break;
       case V_TMA_DS: tma_cfg = 8; break;
+      case V_TMA_S2: tma_cfg = 9; break;
       case V_W4M4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 4>; W = 4; break;
       case V_W8M4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 4, 8>; break;
       case V_W4M1: kern = flat_step_kernel<KIND, T, GT, MIXED, U, 1, 4>; W = 4; break;

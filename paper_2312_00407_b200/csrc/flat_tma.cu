@@ -474,10 +474,12 @@ void run_kern(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
   launch_check("flat_tma_kernel");
 }
 
-// graph mode (a.dk set) is instantiated for the default configuration only
+// graph mode (a.dk set) is instantiated for the default configurations only (4 stages;
+// Adan's 3)
 template <class C, int KIND, bool MIXED, typename GT>
 void run(const FlatArgs& a, const StepConsts<float>& k, cudaStream_t st) {
-  if constexpr (std::is_same_v<C, TmaCfg<16, 4>>) {
+  if constexpr (std::is_same_v<C, TmaCfg<16, 4>> ||
+                (KIND == K_ADAN && std::is_same_v<C, TmaCfg<16, 3>>)) {
     if (a.gs.d) return run_kern<C, KIND, MIXED, GT, true>(a, k, st);
   }
   if (a.gs.d) throw Error(MCO_CONFIG, "flat_tma: graph mode runs the default configuration");
@@ -831,7 +833,8 @@ bool flat_tma_eligible(const FlatArgs& a, int cfg) {
   X(5, (TmaCfg<16, 8, 2>))          \
   X(6, (TmaCfg<16, 4, 4, true>))    \
   X(7, (TmaCfg<24, 6, 2>))          \
-  X(8, (TmaCfg<16, 4, 4, false, true>))
+  X(8, (TmaCfg<16, 4, 4, false, true>)) \
+  X(9, (TmaCfg<16, 2>))
 
 int tma_tile(int cfg) {
   switch (cfg) {

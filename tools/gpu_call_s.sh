@@ -1,0 +1,10 @@
+# GPU call: every TMA configuration on Adan / AdamW (7B), interleaved twice: is a per-kind
+# configuration worth it?
+for rep in 1 2; do
+for v in tma tma_s3 tma_s5 tma24 tma8 tma_e2 tma_hint tma24_e2; do
+  MCO_FLAT_VARIANT=$v timeout 300 python bench.py --optimizers adan,adamw --no-e2e --no-cpu-baseline --no-extra --steps 10 --warmup 3 --repeats 2 > gpurun_out/v_$v.json 2>/dev/null
+  python -c "
+import json; d=json.load(open('gpurun_out/v_$v.json'))
+print('$v', {k:(v['ms'],v['frac_of_measured_hbm']) for k,v in d['per_optimizer'].items()}, d['clocks']['sm_mhz'])"
+done
+done
