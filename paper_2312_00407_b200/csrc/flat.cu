@@ -458,6 +458,11 @@ void run_flat(const FlatArgs& a, const StepConsts<T>& k, cudaStream_t st) {
       case V_L2PF4: kern = flat_step_kernel<KIND, T, GT, MIXED, U, MINB, 8, 4>; break;
       default: break;  // V_LDG
     }
+    static const int cfg_force = [] {  // MCO_TMA_CFG=<id>: force a configuration (A/B)
+      const char* e = getenv("MCO_TMA_CFG");
+      return e ? atoi(e) : -1;
+    }();
+    if (tma_cfg >= 0 && cfg_force >= 0 && !dev_step) tma_cfg = cfg_force;
     if (tma_cfg >= 0 && flat_tma_eligible(a, tma_cfg)) {
       launch_flat_tma(a, k, st, tma_cfg);
       return;
