@@ -13,7 +13,7 @@ from paper_2312_00407_b200 import optim  # noqa: E402
 from paper_2312_00407_b200.optim import Kind, OptimizerConfig  # noqa: E402
 
 BYTES = {Kind.ADAMW: 28, Kind.LION: 20, Kind.ADAN: 44, Kind.SOPHIA: 24}
-PEAK = 6540.5
+PEAK = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
 
 
 def timed(fn, warm=3, it=20):
