@@ -501,7 +501,7 @@ def bench_ours(args, rank, world, local_rank):
         extra["sophia_precise_m"] = {
             "ms": round(ms, 4), "params_per_s": P / (ms * 1e-3), "bytes_per_param": 32,
             "frac_of_measured_hbm": round(gbs / hbm_peak, 4),
-            "what": "Sophia with an fp64 first moment (state f32m64, sophia_m64_kernel); "
+            "what": "Sophia with an fp64 first moment (state f32m64, sophia_m64_tma); "
                     "refresh steps write h too (+4 B)", "parity": load_parity("sophia_m64")}
         per["sophia"]["parity_fp32_m"] = load_parity("sophia")
         del opt
