@@ -1,5 +1,6 @@
 """Randomised parity sweep (fixed seed): random optimizer kind, length, element
-offset (alignment), gradient dtype, hyper-parameters, step count and graph mode -- the
+offsets (alignment; the gradient's drawn apart from the parameters' in 40 % of the
+cases), gradient dtype, hyper-parameters, step count and graph mode -- the
 fp32 kernels must stay bit-exact with the restatement for every draw.
 MCO_RANDOM_CASES=N / MCO_RANDOM_ADA_CASES=N widen the stored-state / AdaLomo sweeps
 (defaults 40 / 12)."""
@@ -17,6 +18,7 @@ torch = pytest.importorskip("torch")
 
 rng = np.random.default_rng(20260)
 grng = np.random.default_rng(7)  # graph-mode draws (keeps the other draws unchanged)
+orng = np.random.default_rng(11)  # gradient offsets apart from the parameters' (round 2)
 CASES = []
 for i in range(int(os.environ.get("MCO_RANDOM_CASES", "40"))):
     CASES.append(dict(kind=int(rng.integers(0, 4)), n=int(rng.choice([1, 7, 8, 9, 63, 4096,
@@ -27,6 +29,7 @@ for i in range(int(os.environ.get("MCO_RANDOM_CASES", "40"))):
                       b2=float(rng.uniform(0.9, 0.9999)), b3=float(rng.uniform(0.9, 0.999)),
                       k=int(rng.integers(1, 5)), steps=int(rng.integers(1, 5)), seed=i,
                       graph=bool(grng.random() < 0.3)))
+    CASES[-1]["goff"] = int(orng.integers(0, 9)) if orng.random() < 0.4 else CASES[-1]["off"]
 
 
 @pytest.mark.parametrize("c", CASES, ids=[f"case{i}" for i in range(len(CASES))])
@@ -34,7 +37,7 @@ def test_random_case_bit_exact(c):
     cfg = OptimizerConfig.defaults_for(Kind(c["kind"]))
     cfg.weight_decay, cfg.beta1, cfg.beta2, cfg.beta3 = c["wd"], c["b1"], c["b2"], c["b3"]
     cfg.update_interval = c["k"]
-    n, off = c["n"], c["off"]
+    n, off, goff = c["n"], c["off"], c["goff"]
     pbig = O.synth(n + off, c["seed"], 0, 0, 0, 0, -6, 0, False)
     tp = torch.from_numpy(pbig.copy()).cuda()
     p = pbig[off:].copy()
@@ -44,13 +47,13 @@ def test_random_case_bit_exact(c):
     out = torch.empty(n, dtype=torch.bfloat16, device="cuda") if c["mixed"] else None
     for t in range(1, c["steps"] + 1):
         if c["bf16"]:
-            gb = O.synth(n + off, c["seed"], 1, 0, t, 0, -7, 10, False, "bf16")
-            tg = torch.from_numpy(gb.view(np.int16)).cuda().view(torch.bfloat16)[off:]
-            g = O.bf16_to_f32(gb[off:])
+            gb = O.synth(n + goff, c["seed"], 1, 0, t, 0, -7, 10, False, "bf16")
+            tg = torch.from_numpy(gb.view(np.int16)).cuda().view(torch.bfloat16)[goff:]
+            g = O.bf16_to_f32(gb[goff:])
         else:
-            gbig = O.synth(n + off, c["seed"], 1, 0, t, 0, -7, 10, False)
-            tg = torch.from_numpy(gbig).cuda()[off:]
-            g = gbig[off:].copy()
+            gbig = O.synth(n + goff, c["seed"], 1, 0, t, 0, -7, 10, False)
+            tg = torch.from_numpy(gbig).cuda()[goff:]
+            g = gbig[goff:].copy()
         if out is not None:
             opt.step_mixed(tp[off:], tg, out, c["lr"])
         else:
