@@ -601,9 +601,13 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
     if (lane == 0) {
       const bool skip_gp = (KIND == K_ADAN) && k.first;  // g_prev unused at t == 1
       const int nload = skip_gp ? NIN - 1 : NIN;
-      auto where = [&](uint64_t i, float*& p, const GT*& g, uint64_t& so, int& q) {
+      // tensor cursors of the load and store sequences: a CTA's tiles only increase, so
+      // the owning tensor is found by stepping forward, not by a binary search per tile
+      int q_ld = 0, q_st = 0;
+      auto where = [&](uint64_t i, int& cur, float*& p, const GT*& g, uint64_t& so, int& q) {
         const uint64_t t = blockIdx.x + i * gridDim.x;
-        q = list_find(tb, L.n, t);
+        while (cur + 1 < L.n && tb[cur + 1] <= t) ++cur;  // largest q with tb[q] <= t
+        q = cur;
         const uint64_t e = (t - tb[q]) * (uint64_t)kTile;
         p = static_cast<float*>(L.p[q]) + e;
         g = static_cast<const GT*>(L.g[q]) + e;
@@ -615,7 +619,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         const GT* g;
         uint64_t so;
         int q;
-        where(i, p, g, so, q);
+        where(i, q_ld, p, g, so, q);
         const int sp = SH ? L.shp[q] : 0, sg = SH ? L.shg[q] : 0, ss = SH ? L.shs[q] : 0;
         if constexpr (SH) meta[s] = ListStage{p, so, sp, sg, ss};  // ordered before the arrive
         const float* src[6] = {p - sp, nullptr, s0 + so - ss, s1 + so - ss, s2 + so - ss,
@@ -647,7 +651,7 @@ __global__ void __launch_bounds__(C::kConsumers + 32, 1)
         const GT* g;
         uint64_t so;
         int q;
-        where(i, p, g, so, q);
+        where(i, q_st, p, g, so, q);
         const int sp = SH ? L.shp[q] : 0, ss = SH ? L.shs[q] : 0;
         float* st = buf + (size_t)s * NIN * kSlot;
         store(p, st, sp);

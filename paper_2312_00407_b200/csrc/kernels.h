@@ -37,7 +37,10 @@ void launch_sophia_m64(float* p, const void* g, int g_dtype, double* m, float* h
 
 // List form: separate parameter / gradient tensors over the flat state (tensor i's state
 // at the sum of the preceding lengths).  One launch per kListMax tensors.
-constexpr int kListMax = 40;
+#ifndef MCO_LIST_MAX
+#define MCO_LIST_MAX 40
+#endif
+constexpr int kListMax = MCO_LIST_MAX;
 struct FlatList {  // one launch (kernel parameter)
   int n;
   uint64_t vbeg[kListMax + 1];      // prefix sums: vector-path vectors
