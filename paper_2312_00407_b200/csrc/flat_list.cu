@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t nv = vb[L.n];
+  int cur = 0;  // the thread's vectors only increase: step the owning tensor forward
   for (uint64_t base = tid; base < nv; base += stride * U) {
     T pv[U][W], gv[U][W], a[U][W], b[U][W], c[U][W], d[U][W];
     T* pp[U];
@@ -48,7 +49,8 @@ __global__ void __launch_bounds__(kThreads, MINB)
     for (int u = 0; u < U; ++u) {
       const uint64_t vi = base + (uint64_t)u * stride;
       if (vi < nv) {
-        const int i = list_find(vb, L.n, vi);
+        while (cur + 1 < L.n && vb[cur + 1] <= vi) ++cur;
+        const int i = cur;
         const uint64_t e = (vi - vb[i]) * W;
         pp[u] = static_cast<T*>(L.p[i]) + e;
         so[u] = L.soff[i] + e;
@@ -246,8 +248,10 @@ __global__ void __launch_bounds__(kThreads)
   const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t nv = vb[L.n];
+  int cur = 0;  // the thread's vectors only increase: step the owning tensor forward
   for (uint64_t vi = tid; vi < nv; vi += stride) {
-    const int i = list_find(vb, L.n, vi);
+    while (cur + 1 < L.n && vb[cur + 1] <= vi) ++cur;
+    const int i = cur;
     const uint64_t e = (vi - vb[i]) * W;
     PT* p = static_cast<PT*>(L.p[i]) + e;
     const GT* g = static_cast<const GT*>(L.g[i]) + e;
