@@ -66,13 +66,20 @@ constexpr int rows_in_flight() {
 // 4 CTAs: 14.22)
 #define MCO_K1_RB_BF16 8
 #endif
+#ifndef MCO_K1_RB_F32
+// K1 on fp32 parameters: 4 rows in flight at 2 CTAs / SM (MCO_K1_MINB, 128 registers)
+// instead of 2 at 3 -- same box: 7B multi-tensor 25.05 -> 24.55 ms, list form 25.4 ->
+// 24.8, hook form 29.54 -> 29.00, C3 (13B + clip) 47.56 -> 46.77
+#define MCO_K1_RB_F32 4
+#endif
 template <typename GT, typename PT>
 constexpr int k1_rows() {
   return (MCO_K1_RB_BF16 && sizeof(GT) == 2 && sizeof(PT) == 2) ? MCO_K1_RB_BF16
+         : (MCO_K1_RB_F32 && sizeof(PT) == 4)                    ? MCO_K1_RB_F32
                                                                  : rows_in_flight<GT, PT>();
 }
 #ifndef MCO_K1_MINB
-#define MCO_K1_MINB 3
+#define MCO_K1_MINB 2  // with MCO_K1_RB_F32 = 4 (below)
 #endif
 #ifndef MCO_K4_MINB
 #define MCO_K4_MINB 3
@@ -839,9 +846,20 @@ __device__ __forceinline__ void row_col(uint32_t e, const TensorInfo& T, uint32_
 #ifndef MCO_K4_RB_BF16
 #define MCO_K4_RB_BF16 (4 * kRB)
 #endif
+#ifndef MCO_K4_RB_F32
+#define MCO_K4_RB_F32 (2 * kRB)
+#endif
 template <typename GT>
 constexpr int k4_rows() {
-  return sizeof(GT) == 2 ? MCO_K4_RB_BF16 : 2 * kRB;
+  return sizeof(GT) == 2 ? MCO_K4_RB_BF16 : MCO_K4_RB_F32;
+}
+#ifndef MCO_K6_RB_F32
+#define MCO_K6_RB_F32 0  // A/B knob: K6 tiles' rows in flight on fp32 data (0: kRB)
+#endif
+template <typename GT, typename PT>
+constexpr int k6_rows() {
+  return (MCO_K6_RB_F32 && sizeof(GT) == 4 && sizeof(PT) == 4) ? MCO_K6_RB_F32
+                                                               : rows_in_flight<GT, PT>();
 }
 
 template <bool VEC, typename GT>
@@ -1273,7 +1291,7 @@ __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
 #pragma unroll
       for (int j = 0; j < VW; ++j) bv[j] = j < valid ? c.fb[T.fb_off + col + j * cs] : 0.f;
       const float* fa = c.fa + T.fa_off;
-      constexpr int RB = rows_in_flight<GT, PT>();
+      constexpr int RB = k6_rows<GT, PT>();
       const int64_t rstep = (int64_t)TR * T.cols;  // row offsets advance by adds
       int64_t roff = (tl.r0 + tr) * T.cols + col;
       for (int64_t r0 = tl.r0 + tr; r0 < tl.r1; r0 += (int64_t)RB * TR) {
