@@ -1825,6 +1825,8 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
   // tiles per SM); MCO_ADALOMO_TILES, an A/B knob read at plan build
   const char* tk = getenv("MCO_ADALOMO_TILES");
   const bool waves = !(tk && std::string(tk) == "pow2");
+  const char* wk = getenv("MCO_ADALOMO_WAVE");  // tile-kernel CTAs per SM of a wave (A/B)
+  const int wave_ctas = wk ? std::max(1, atoi(wk)) : 3;
   for (size_t k = 0; k < shapes.size(); ++k) {
     const auto& s = shapes[k];
     TensorInfo T{};
@@ -1853,7 +1855,7 @@ void build_adalomo_plan(AdaLomoPlan& pl, const std::vector<std::vector<int64_t>>
         // form) runs every pass in m full rounds -- 4096^2: 444 tiles of 37 rows (one round
         // of 444 CTAs) instead of 512 tiles of 32 rows (two rounds of 256 CTAs, 1.7 per SM:
         // K1 36.7 us against a 20.5 us traffic floor, ncu)
-        const int64_t wave = 3LL * sms;
+        const int64_t wave = (int64_t)wave_ctas * sms;
         const int64_t need = ((T.rows + kMaxTileRows - 1) / kMaxTileRows) * T.kc;
         const int64_t m = std::max<int64_t>(1, (need + wave - 1) / wave);
         const int64_t nrb_max = std::max<int64_t>(1, (m * wave) / T.kc);
