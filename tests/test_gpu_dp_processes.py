@@ -1,7 +1,8 @@
 """Multi-process parity of the sharded C3 / C5 paths on the one GPU a test
 box has: N OS processes share cuda:0 over a gloo process group (NCCL refuses two ranks
 on one device), each holding its own local gradients, and the result is checked
-against the compiled reference on the rank-summed gradient.
+against the compiled reference on the rank-summed gradient.  tests/test_multigpu.py
+runs the same checks over NCCL with one GPU per rank (check_* with backend "nccl").
 
 * C3: zero.RowShardedAdaLomo.step_dp -- every matrix split by rows (uneven row counts
   included), replicated 1-D tensors, the global grad-norm clip; reduce-scatter of the
@@ -52,7 +53,7 @@ def _lomo_grad(rank, t, n=LOMO_P):
     return O.synth(n, 61, 1, rank, t, 0, -7, 10, False)
 
 
-def _worker(what, rank, world, port, arg, q):
+def _worker(what, rank, world, port, arg, q, backend="gloo"):
     for p in (ROOT, os.path.join(ROOT, "oracle")):
         sys.path.insert(0, p)
     import torch
@@ -63,8 +64,13 @@ def _worker(what, rank, world, port, arg, q):
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    dist.init_process_group("gloo", rank=rank, world_size=world)
-    torch.cuda.set_device(0)
+    if backend == "nccl":  # one GPU per rank (tests/test_multigpu.py)
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", rank))
+    else:  # ranks sharing cuda:0
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
     try:
         if what == "ada":
             cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
@@ -101,13 +107,13 @@ def _worker(what, rank, world, port, arg, q):
         dist.destroy_process_group()
 
 
-def _run(what, world, arg):
+def _run(what, world, arg, backend="gloo"):
     import torch.multiprocessing as mp
 
     port = _port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(what, r, world, port, arg, q))
+    procs = [ctx.Process(target=_worker, args=(what, r, world, port, arg, q, backend))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -122,7 +128,11 @@ def _run(what, world, arg):
 @pytest.mark.parametrize("world", [2, 3])
 @pytest.mark.parametrize("clip", [1e-3, None])
 def test_row_sharded_adalomo_processes_match_reference(world, clip):
-    res = _run("ada", world, clip)
+    check_row_sharded_adalomo(world, clip, "gloo")
+
+
+def check_row_sharded_adalomo(world, clip, backend):
+    res = _run("ada", world, clip, backend)
     from paper_2312_00407_b200.optim import Kind, OptimizerConfig
 
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
@@ -152,8 +162,12 @@ def test_row_sharded_adalomo_processes_match_reference(world, clip):
 @needs_ref
 @pytest.mark.parametrize("world", [2, 3])
 def test_zero_sharded_lomo_clip_processes_match_reference(world):
+    check_zero_sharded_lomo(world, "gloo")
+
+
+def check_zero_sharded_lomo(world, backend):
     clip = 0.05
-    res = _run("lomo32", world, clip)
+    res = _run("lomo32", world, clip, backend)
     want = O.synth(LOMO_P, 61, 0, 0, 0, 0, -6, 0, False).astype(np.float64)
     p0 = want.copy()
     for t in range(1, LOMO_STEPS + 1):
@@ -173,8 +187,12 @@ def test_sharded_lomo_bf16_clip_processes_match_restatement(world):
     all-reduce of the ranks' partial sums; vs the bf16 restatement with the serial
     clip scale -- equal up to one bf16 ulp where the two fp64 norms (different
     summation order) round the fp32 factor differently."""
+    check_sharded_lomo_bf16(world, "gloo")
+
+
+def check_sharded_lomo_bf16(world, backend):
     clip = 0.05
-    res = _run("lomo_bf16", world, clip)
+    res = _run("lomo_bf16", world, clip, backend)
     from paper_2312_00407_b200 import zero
 
     want = O.f32_to_bf16(O.synth(LOMO_P, 62, 0, 0, 0, 0, -6, 0, False))

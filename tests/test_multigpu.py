@@ -7,9 +7,12 @@ rounding of the sum otherwise (NCCL's reduction order).
 
 Paths: zero.ZeroShardedOptimizer (torch.distributed RS / AG), zero.NativeZeroOptimizer
 (mco_shard_step over the library's NCCL communicator; mco_shard_step_mixed with bf16
-replicas), zero.PeerShardedOptimizer (one
-kernel over NVLink peer memory), zero.RowShardedAdaLomo (two statistic all-reduces),
-and bench.py under torchrun with NCCL."""
+replicas), zero.BucketedZeroOptimizer (the bucketed, double-buffered mco_zb step: fp32
+replicas and the C4 mixed layout), zero.PeerShardedOptimizer (one kernel over NVLink
+peer memory); the C3 / C5 paths of tests/test_gpu_dp_processes.py over NCCL
+(zero.RowShardedAdaLomo with its statistic all-reduces and the clip, zero.ZeroShardedLomo
+and the bf16 owned-shard LOMO with the global clip); and bench.py under torchrun with
+NCCL (the rank count NCCL reports checked against --gpus)."""
 import json
 import os
 import socket
@@ -83,6 +86,23 @@ def _worker(rank, world, port, q):
         torch.cuda.synchronize()
         out["native_mixed"] = rep.float().cpu().numpy()
 
+        zb = zero.BucketedZeroOptimizer(cfg, P, comm, bucket_elems=100000)
+        p = p0.clone()
+        for t in range(1, STEPS + 1):
+            zb.step(p, torch.from_numpy(_grad(rank, t)).cuda(), 1e-3)
+        torch.cuda.synchronize()
+        comm.check()
+        out["bucketed"] = p.cpu().numpy()
+
+        zm = zero.BucketedZeroOptimizer(cfg, P, comm, bucket_elems=100000,
+                                        replica_dtype=torch.bfloat16)
+        zm.load_master(p0)
+        rep = torch.zeros(P, dtype=torch.bfloat16, device="cuda")
+        for t in range(1, STEPS + 1):
+            zm.step(rep, torch.from_numpy(_grad(rank, t)).cuda(), 1e-3)
+        torch.cuda.synchronize()
+        out["bucketed_mixed"] = rep.float().cpu().numpy()
+
         ps = zero.PeerShardedOptimizer(cfg, P)
         ps.params.copy_(p0)
         for t in range(1, STEPS + 1):
@@ -132,10 +152,11 @@ def _serial():
 
 
 @needs_multi
-@pytest.mark.parametrize("path", ["zero", "native", "peer", "native_mixed"])
+@pytest.mark.parametrize("path", ["zero", "native", "peer", "native_mixed", "bucketed",
+                                  "bucketed_mixed"])
 def test_sharded_paths_equal_serial(results, path):
     want = _serial()
-    if path == "native_mixed":  # bf16 replicas of the fp32 master (RNE)
+    if path.endswith("_mixed"):  # bf16 replicas of the fp32 master (RNE)
         want = torch.from_numpy(want).bfloat16().float().numpy()
     for r in range(WORLD):
         got = results[r][path]
@@ -147,16 +168,51 @@ def test_sharded_paths_equal_serial(results, path):
 
 
 @needs_multi
+@pytest.mark.parametrize("clip", [1e-3, None])
+def test_row_sharded_adalomo_nccl_matches_reference(clip):
+    from test_gpu_dp_processes import check_row_sharded_adalomo
+    if O.ref is None:
+        pytest.skip("oracle/_ref not built")
+    check_row_sharded_adalomo(WORLD, clip, "nccl")
+
+
+@needs_multi
+def test_zero_sharded_lomo_nccl_matches_reference():
+    from test_gpu_dp_processes import check_zero_sharded_lomo
+    if O.ref is None:
+        pytest.skip("oracle/_ref not built")
+    check_zero_sharded_lomo(WORLD, "nccl")
+
+
+@needs_multi
+def test_sharded_lomo_bf16_nccl_matches_restatement():
+    from test_gpu_dp_processes import check_sharded_lomo_bf16
+    check_sharded_lomo_bf16(WORLD, "nccl")
+
+
+@needs_multi
 def test_bench_under_torchrun_nccl():
+    """bench.py --gpus N under torchrun: one line, n_gpus = N = the rank count NCCL's own
+    init log reports, the value = 6 P / the summed whole-DP-step times, every kind with
+    its shard-local time and NVLink bytes."""
+    import re
+
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
            f"--nproc-per-node={WORLD}", "--master-addr", "127.0.0.1", "--master-port",
            str(_port()), "bench.py", "--gpus", str(WORLD), "--steps", "2", "--warmup", "1",
-           "--layers", "2", "--no-e2e", "--no-cpu-baseline"]
+           "--layers", "2", "--no-e2e", "--no-cpu-baseline", "--repeats", "1"]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
     assert len(lines) == 1
     d = json.loads(lines[0])
-    assert d["n_gpus"] == WORLD and d["value"] > 0
-    assert d["collectives"]["ms"] > 0
-    assert "nccl_baseline" in d["collectives"]
+    assert d["n_gpus"] == WORLD and d["value"] > 0 and d["scaling"] == "strong"
+    assert d["collectives"]["backend"] == "nccl"
+    assert d["collectives"]["nccl_allgather_busbw_gbs"] > 0
+    nr = {int(m) for m in re.findall(r"nRanks (\d+)", r.stderr)}
+    assert nr == {WORLD}, sorted(nr)  # NCCL_DEBUG=INFO (bench.py sets it for N > 1)
+    P = d["config"]["params"]
+    for k, e in d["per_optimizer"].items():
+        assert e["shard_local"]["ms"] > 0 and e["nvlink"]["bytes_per_rank_per_direction"] > 0, k
+    total = sum(e["ms"] for e in d["per_optimizer"].values())
+    assert abs(d["value"] - len(d["per_optimizer"]) * P / (total * 1e-3)) / d["value"] < 1e-4
