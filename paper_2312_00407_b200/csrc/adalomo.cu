@@ -620,16 +620,18 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// tensor k's sum u^2 from K4's tile sums, by one warp (lane-strided, warp_sum)
+__device__ __forceinline__ void usq_one(const Ctx& c, int k, int lane) {
+  const TensorInfo T = c.tensors[k];
+  // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
+  double us = strided_sum(T.tile_begin + lane, T.tile_end, 32,
+                          [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); });
+  us = warp_sum(us);
+  if (lane == 0) c.pay_usq[k] = T.weight * us;
+}
 __device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = t0 + warp; k < t1; k += nw) {
-    const TensorInfo T = c.tensors[k];
-    // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
-    double us = strided_sum(T.tile_begin + lane, T.tile_end, 32,
-                            [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); });
-    us = warp_sum(us);
-    if (lane == 0) c.pay_usq[k] = T.weight * us;
-  }
+  for (int k = t0 + warp; k < t1; k += nw) usq_one(c, k, lane);
 }
 
 __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
@@ -862,13 +864,11 @@ constexpr int k6_rows() {
                                                                : rows_in_flight<GT, PT>();
 }
 
+// K4's tile loop (k4_usq)
 template <bool VEC, typename GT>
-__global__ void __launch_bounds__(kThreads, k4_minb<GT>())
-    k4_usq(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double b2, double eps, int t0, int t1,
-           int fuse5, double adalomo_clip) {
-  pdl_wait();
-  __shared__ double scratch[32];
-  __shared__ bool last;
+__device__ __forceinline__ void k4_tiles(const Ctx& c, const Ptrs& P, int64_t tile0,
+                                         int64_t ntiles, double b2, double eps,
+                                         double* scratch) {
   const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const Tile tl = c.tiles[tile0 + ti];
@@ -961,6 +961,16 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
     const double b = block_sum(usq, scratch);
     if (threadIdx.x == 0) c.tile_sc[(tile0 + ti) * 4 + 3] = b;
   }
+}
+
+template <bool VEC, typename GT>
+__global__ void __launch_bounds__(kThreads, k4_minb<GT>())
+    k4_usq(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double b2, double eps, int t0, int t1,
+           int fuse5, double adalomo_clip) {
+  pdl_wait();
+  __shared__ double scratch[32];
+  __shared__ bool last;
+  k4_tiles<VEC, GT>(c, P, tile0, ntiles, b2, eps, scratch);
   if (fuse5) {  // unsharded call: the last CTA to finish does K5's reduction and damping
     unsigned* ticket = reinterpret_cast<unsigned*>(c.glob + 3);
     if (threadIdx.x == 0) {
@@ -979,15 +989,16 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
 }
 
 // ============================ K5: damping ==============================================
+__device__ __forceinline__ void k5_one(const Ctx& c, int k, double adalomo_clip) {
+  const TensorInfo T = c.tensors[k];  // optim.cpp:269-273
+  const double us = __ldcg(&c.pay_usq[k]);
+  const double rms_u = sqrt(us / (double)T.numel_global);
+  const double damp = fmax(1.0, rms_u / adalomo_clip);
+  c.tens_sc[k * kTensScalars + TS_USQ] = us;
+  c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
+}
 __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip) {
-  for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) {  // optim.cpp:269-273
-    const TensorInfo T = c.tensors[k];
-    const double us = __ldcg(&c.pay_usq[k]);
-    const double rms_u = sqrt(us / (double)T.numel_global);
-    const double damp = fmax(1.0, rms_u / adalomo_clip);
-    c.tens_sc[k * kTensScalars + TS_USQ] = us;
-    c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
-  }
+  for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) k5_one(c, k, adalomo_clip);
 }
 
 __global__ void __launch_bounds__(1024)
@@ -1265,10 +1276,21 @@ __global__ void __launch_bounds__(kK6Consumers + 32, 1)
 
 // K6 over the statistics tiles (alternative traversal; identical arithmetic and result)
 template <bool VEC, typename GT, typename PT>
+__device__ __forceinline__ void k6_tiles(const Ctx& c, const Ptrs& P, int64_t tile0,
+                                         int64_t ntiles, double eps);
+
+template <bool VEC, typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads, k6_minb<GT, PT>())
     k6_update_tiles(Ctx c, Ptrs P, int64_t tile0, int64_t ntiles, double eps, int trigger) {
   pdl_wait();
   if (trigger) pdl_trigger();
+  k6_tiles<VEC, GT, PT>(c, P, tile0, ntiles, eps);
+}
+
+// K6's tile loop (k6_update_tiles)
+template <bool VEC, typename GT, typename PT>
+__device__ __forceinline__ void k6_tiles(const Ctx& c, const Ptrs& P, int64_t tile0,
+                                         int64_t ntiles, double eps) {
   const float sf = (float)c.glob[0], epsf = ada_eps(eps);
   // reverse tile order: the tail of K4's gradient reads is still L2-resident
   for (int64_t k = blockIdx.x; k < ntiles; k += gridDim.x) {
