@@ -207,9 +207,14 @@ mco_status mco_lomo_apply_clipped(void* params, int param_dtype, const void* gra
                                   double clip, void* stream);
 /* lomo_apply over HOST arrays (the reference's Tensor data is host memory),
  * pipelined through the device in chunks; clip >= 0 adds the global-norm pass
- * (lomo_fused_backward_step's two passes, optim.cpp:291-316). Synchronous. */
+ * (lomo_fused_backward_step's two passes, optim.cpp:291-316). Synchronous.
+ * With clip >= 0 and room on the device, the gradient is held in a device buffer that
+ * the library keeps for the next call (see mco_host_release). */
 mco_status mco_lomo_apply_host(void* params, int param_dtype, const void* grads, int grad_dtype,
                                uint64_t n, double lr, double scale, double clip);
+/* Frees the device buffers the host-span calls keep between calls on every device
+ * (mco_lomo_apply_host's resident gradient); waits for a running call to finish. */
+mco_status mco_host_release(void);
 /* Σx² into *dev_out (fp64, deterministic fixed-order reduction);
  * accumulate != 0 adds to the existing value (optim.cpp:294-300 hook sum). */
 mco_status mco_sumsq(const void* x, int dtype, uint64_t n, double* dev_out, int accumulate,

@@ -54,6 +54,7 @@ _SIGS = {
     "mco_last_error": (C.c_char_p, []),
     "mco_version": (C.c_char_p, []),
     "mco_launch_count": (_u64, []),
+    "mco_host_release": (_i, []),
     "mco_parse_kind": (_i, [C.c_char_p, C.POINTER(_i)]),
     "mco_kind_name": (C.c_char_p, [_i]),
     "mco_is_fused": (_i, [_i]),

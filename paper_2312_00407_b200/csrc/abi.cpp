@@ -150,11 +150,30 @@ void host_trace(const char* what) {
   t0 = now;
 }
 
+static std::mutex g_stage_mu;
+static std::unordered_map<int, HostStage*> g_stages;
+
+void host_release_all() {
+  std::vector<std::pair<int, HostStage*>> all;
+  {
+    std::lock_guard<std::mutex> lock(g_stage_mu);  // not held below: a running call takes
+    all.assign(g_stages.begin(), g_stages.end());  // gres_mu, then g_stage_mu
+  }
+  for (auto& kv : all) {
+    HostStage& hs = *kv.second;
+    std::lock_guard<std::mutex> g(hs.gres_mu);  // waits for a running call
+    if (hs.gres) {
+      DeviceGuard dg(kv.first);
+      MCO_CUDA_CHECK(cudaFree(hs.gres));
+      hs.gres = nullptr;
+      hs.gres_bytes = 0;
+    }
+  }
+}
+
 HostStage& host_stage(int dev) {
-  static std::mutex mu;
-  static std::unordered_map<int, HostStage*> stages;
-  std::lock_guard<std::mutex> lock(mu);
-  auto& s = stages[dev];
+  std::lock_guard<std::mutex> lock(g_stage_mu);
+  auto& s = g_stages[dev];
   if (!s) {
     s = new HostStage;
     s->chunk_bytes = 8ull << 24;  // 16 Mi elements of <= 8 bytes
@@ -177,6 +196,7 @@ extern "C" {
 const char* mco_last_error(void) { return g_err.c_str(); }
 const char* mco_version(void) { return "mco 0.1 (sm_100a)"; }
 uint64_t mco_launch_count(void) { return g_launches.load(); }
+mco_status mco_host_release(void) { return guard([&] { host_release_all(); }); }
 
 mco_status mco_parse_kind(const char* name, int* out) {
   return guard([&] {

@@ -536,7 +536,7 @@ mco_status mco_lomo_apply_clipped(void* p, int pdt, const void* g, int gdt, uint
 // clip >= 0: the norm needs every gradient before any parameter moves.  When the device
 // has room, the gradient goes up once into a resident buffer (its sum of squares chunk by
 // chunk as it lands), then the parameters stream up / update / down against it: 8 B/param
-// up instead of 12.  Otherwise two passes over the host gradient.  The chunking and the
+// up instead of 12.  The buffer stays allocated for the next call (mco_host_release).  Otherwise two passes over the host gradient.  The chunking and the
 // accumulation order are the same either way (bit-identical norms).
 mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_t n, double lr,
                                double scale, double clip) {
@@ -547,19 +547,33 @@ mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_
     host_trace(nullptr);
     const double* dnorm = nullptr;
     double* acc = nullptr;
-    void* gres = nullptr;  // device-resident gradient (clip only)
+    void* gres = nullptr;  // device-resident gradient (clip only), HostStage::gres
+    HostStage& hs = host_stage(dev);
+    std::unique_lock<std::mutex> gres_lock(hs.gres_mu, std::defer_lock);
     if (clip >= 0) {
       MCO_CUDA_CHECK(cudaMalloc(&acc, sizeof(double)));
       MCO_CUDA_CHECK(cudaMemset(acc, 0, sizeof(double)));
-      HostStage& hs = host_stage(dev);
-      size_t free_b = 0, total_b = 0;
-      MCO_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-      if (n * gsz + (2ull << 30) < free_b) {
-        if (cudaMalloc(&gres, n * gsz) != cudaSuccess) {
-          cudaGetLastError();  // out of memory: fall back to the two-pass form
-          gres = nullptr;
+      gres_lock.lock();
+      const uint64_t need = n * gsz;
+      if (hs.gres_bytes < need) {  // grow (or first use): only with room to spare
+        if (hs.gres) {
+          MCO_CUDA_CHECK(cudaFree(hs.gres));
+          hs.gres = nullptr;
+          hs.gres_bytes = 0;
+        }
+        size_t free_b = 0, total_b = 0;
+        MCO_CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+        if (need + (2ull << 30) < free_b) {
+          if (cudaMalloc(&hs.gres, need) == cudaSuccess) {
+            hs.gres_bytes = need;
+          } else {
+            cudaGetLastError();  // out of memory: the two-pass form
+            hs.gres = nullptr;
+          }
         }
       }
+      gres = hs.gres;
+      if (!gres) gres_lock.unlock();
       if (gres) {
         std::lock_guard<std::mutex> lock(hs.mu);
         const uint64_t C = hs.chunk_bytes / 8;
@@ -616,7 +630,6 @@ mco_status mco_lomo_apply_host(void* p, int pdt, const void* g, int gdt, uint64_
                     });
     }
     host_trace("lomo_apply_host: parameters up / update / down");
-    if (gres) cudaFree(gres);
     if (acc) cudaFree(acc);
   });
 }

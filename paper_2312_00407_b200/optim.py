@@ -636,6 +636,12 @@ def flat_variant() -> str:
     return lib.mco_flat_variant().decode()
 
 
+def host_release() -> None:
+    """Free the device buffers the host-span calls keep between calls (lomo_step on host
+    arrays with the clip keeps its resident gradient, mco_host_release)."""
+    _check(lib.mco_host_release())
+
+
 def launch_count() -> int:
     """Kernel launches issued by libmco in this process."""
     return int(lib.mco_launch_count())

@@ -384,6 +384,28 @@ def test_lomo_host_path_equals_device_path():
     np.testing.assert_allclose(hp2, tp2.cpu().numpy(), rtol=0, atol=1e-9)
 
 
+def test_lomo_host_clip_reuses_its_resident_gradient_buffer():
+    """mco_lomo_apply_host keeps the device-resident gradient between calls (grown when a
+    call needs more, freed by mco_host_release): every call -- smaller, larger, fp64
+    (8 B gradients), after a release -- equals the device path."""
+    free0 = torch.cuda.mem_get_info()[0]
+    for n, dt in [(1 << 22, np.float32), (1000, np.float32), ((1 << 23) + 5, np.float32),
+                  ((1 << 22) + 3, np.float64), ("release", None), (1 << 21, np.float32)]:
+        if n == "release":
+            optim.host_release()
+            assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)
+            continue
+        p = O.synth(n, 12, 0, 0, 0, 0, -6, 0, False).astype(dt)
+        g = O.synth(n, 12, 1, 0, 1, 0, -7, 10, False).astype(dt)
+        hg, dg = g, torch.from_numpy(g).cuda()
+        hp, tp = p.copy(), torch.from_numpy(p).cuda()
+        optim.lomo_step(hp, hg, 1e-2, clip=0.1)
+        optim.lomo_step(tp, dg, 1e-2, clip=0.1)
+        torch.cuda.synchronize()
+        assert bits_equal(hp, tp.cpu().numpy()), (n, dt)
+    optim.host_release()
+
+
 @pytest.mark.parametrize("clip", [None, 1e-3])
 def test_adalomo_host_path_equals_device_path(clip):
     cfg = OptimizerConfig.defaults_for(Kind.ADALOMO)
