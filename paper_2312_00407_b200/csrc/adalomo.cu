@@ -510,20 +510,44 @@ __global__ void __launch_bounds__(kThreads, k1_minb<GT, PT>())
 // latencies overlap (a one-tensor call reduces ~450 tile partials per tensor in one warp:
 // 14 dependent L2 round trips per lane before).  The padding adds +0.0, which leaves
 // every sum here (of squares / of non-negative statistics) bit-unchanged.
-template <typename F>
+// B loads per batch (16 where one lane walks ~14 partials of a one-tensor call: one L2
+// round trip instead of two); the batch size never changes the order of the additions.
+template <int B = 8, typename F>
 __device__ __forceinline__ double strided_sum(int64_t i0, int64_t end, int64_t stride, F x) {
   double acc = 0.0;
-  for (int64_t i = i0; i < end; i += 8 * stride) {
-    double v[8];
+  for (int64_t i = i0; i < end; i += B * stride) {
+    double v[B];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
+    for (int q = 0; q < B; ++q) {
       const int64_t j = i + q * stride;
       v[q] = j < end ? x(j) : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < 8; ++q) acc += v[q];
+    for (int q = 0; q < B; ++q) acc += v[q];
   }
   return acc;
+}
+// three strided sums over the same index set in one walk (each in strided_sum's order):
+// the loads of all three are in flight together
+template <typename F>
+__device__ __forceinline__ void strided_sum3(int64_t i0, int64_t end, int64_t stride, F x,
+                                             double& a0, double& a1, double& a2) {
+  a0 = a1 = a2 = 0.0;
+  for (int64_t i = i0; i < end; i += 8 * stride) {
+    double v[8][3];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t j = i + q * stride;
+#pragma unroll
+      for (int r = 0; r < 3; ++r) v[q][r] = j < end ? x(j, r) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      a0 += v[q][0];
+      a1 += v[q][1];
+      a2 += v[q][2];
+    }
+  }
 }
 
 // K2's / K5's work, also run inside KR / K4 by unsharded (fused) calls
@@ -541,12 +565,19 @@ __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip);
 // weight (1, or 0 on ranks that hold a replica another rank already contributes), so an
 // all-reduce of the payload yields global sums.  fuse2 (no all-reduce between the
 // phases): the last tensor block to finish (ticket) runs K2's body for the call.
-__device__ __forceinline__ void tensor_stats(const Ctx& c, int k, int mode, double* red) {
+__device__ __forceinline__ void tensor_stats(const Ctx& c, int k, int mode, bool one,
+                                             double* red) {
   const TensorInfo T = c.tensors[k];
   const int64_t i0 = T.tile_begin + threadIdx.x;
-  double ps = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 0]; });
-  double gs = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 1]; });
-  double vr = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 2]; });
+  double ps, gs, vr;
+  if (one) {  // one-tensor call (hook form): the three walks' loads in flight together
+    strided_sum3(i0, T.tile_end, blockDim.x, [&](int64_t i, int r) { return c.tile_sc[i * 4 + r]; },
+                 ps, gs, vr);
+  } else {  // (measured: the fused walk slows multi-tensor calls slightly)
+    ps = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 0]; });
+    gs = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 1]; });
+    vr = strided_sum(i0, T.tile_end, blockDim.x, [&](int64_t i) { return c.tile_sc[i * 4 + 2]; });
+  }
   ps = block_sum(ps, red);
   gs = block_sum(gs, red);
   vr = block_sum(vr, red);
@@ -589,7 +620,8 @@ __global__ void __launch_bounds__(kThreads)
       const int64_t j = gi - col_off[lo];
       const float* src = c.colpart + T.colpart_off + j;
       const int64_t nrb = T.nrb, C = T.cols;
-      acc = strided_sum(warp, nrb, nw, [&](int64_t rb) { return (double)src[rb * C]; });
+      auto ld = [&](int64_t rb) { return (double)src[rb * C]; };
+      acc = t1 - t0 == 1 ? strided_sum<16>(warp, nrb, nw, ld) : strided_sum(warp, nrb, nw, ld);
       slot = 3 * c.ntens + T.fb_off + j;
       w = T.weight;
     }
@@ -603,7 +635,7 @@ __global__ void __launch_bounds__(kThreads)
     return;
   }
   __shared__ double red[32];
-  tensor_stats(c, t0 + (int)blockIdx.x - ncolblk, mode, red);
+  tensor_stats(c, t0 + (int)blockIdx.x - ncolblk, mode, t1 - t0 == 1, red);
   if (fuse2) {  // unsharded call: the last tensor block does K2's work
     __shared__ bool last;
     unsigned* ticket = reinterpret_cast<unsigned*>(c.glob + 4);
@@ -621,17 +653,18 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // tensor k's sum u^2 from K4's tile sums, by one warp (lane-strided, warp_sum)
-__device__ __forceinline__ void usq_one(const Ctx& c, int k, int lane) {
+__device__ __forceinline__ void usq_one(const Ctx& c, int k, int lane, bool one) {
   const TensorInfo T = c.tensors[k];
   // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
-  double us = strided_sum(T.tile_begin + lane, T.tile_end, 32,
-                          [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); });
+  auto ld = [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); };
+  double us = one ? strided_sum<16>(T.tile_begin + lane, T.tile_end, 32, ld)
+                  : strided_sum(T.tile_begin + lane, T.tile_end, 32, ld);
   us = warp_sum(us);
   if (lane == 0) c.pay_usq[k] = T.weight * us;
 }
 __device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int k = t0 + warp; k < t1; k += nw) usq_one(c, k, lane);
+  for (int k = t0 + warp; k < t1; k += nw) usq_one(c, k, lane, t1 - t0 == 1);
 }
 
 __global__ void __launch_bounds__(1024) kr_usq(Ctx c, int t0, int t1) {
