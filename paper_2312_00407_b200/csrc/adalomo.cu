@@ -554,6 +554,10 @@ __device__ __forceinline__ void strided_sum3(int64_t i0, int64_t end, int64_t st
 __device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
                         double clip, const double* ext_sumsq, double* red);
 __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip);
+__device__ void k2_one(const Ctx& c, int k, double gsq, double psq, double vrs, double lr,
+                       double b2, int use_clip, double clip, const double* ext_sumsq);
+__device__ __forceinline__ void k5_val(const Ctx& c, int k, double us, double numel, double lrt,
+                                       double adalomo_clip);
 
 // ============================ KR: tile partials -> payload ===========================
 // Blocks [0, ncolblk): one thread per column of the factored tensors in [t0,t1):
@@ -566,7 +570,7 @@ __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip);
 // all-reduce of the payload yields global sums.  fuse2 (no all-reduce between the
 // phases): the last tensor block to finish (ticket) runs K2's body for the call.
 __device__ __forceinline__ void tensor_stats(const Ctx& c, int k, int mode, bool one,
-                                             double* red) {
+                                             double* red, double* out = nullptr) {
   const TensorInfo T = c.tensors[k];
   const int64_t i0 = T.tile_begin + threadIdx.x;
   double ps, gs, vr;
@@ -587,6 +591,11 @@ __device__ __forceinline__ void tensor_stats(const Ctx& c, int k, int mode, bool
       c.pay[k * 3 + 2] = T.weight * vr;
     }
     if (mode & kStatsP) c.pay[k * 3 + 1] = T.weight * ps;
+    if (out) {  // thread 0: the payload values, for k2_one
+      out[0] = T.weight * gs;
+      out[1] = T.weight * ps;
+      out[2] = T.weight * vr;
+    }
   }
 }
 
@@ -635,6 +644,12 @@ __global__ void __launch_bounds__(kThreads)
     return;
   }
   __shared__ double red[32];
+  if (fuse2 && t1 - t0 == 1 && mode == kStatsAll) {  // one-tensor fused call (hook form)
+    double v[3];
+    tensor_stats(c, t0, mode, true, red, v);
+    if (threadIdx.x == 0) k2_one(c, t0, v[0], v[1], v[2], lr, b2, use_clip, clip, ext_sumsq);
+    return;
+  }
   tensor_stats(c, t0 + (int)blockIdx.x - ncolblk, mode, t1 - t0 == 1, red);
   if (fuse2) {  // unsharded call: the last tensor block does K2's work
     __shared__ bool last;
@@ -653,7 +668,7 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 // tensor k's sum u^2 from K4's tile sums, by one warp (lane-strided, warp_sum)
-__device__ __forceinline__ void usq_one(const Ctx& c, int k, int lane, bool one) {
+__device__ __forceinline__ double usq_one(const Ctx& c, int k, int lane, bool one) {
   const TensorInfo T = c.tensors[k];
   // L2 reads (__ldcg): K4's tile sums, written by other CTAs of its grid
   auto ld = [&](int64_t i) { return __ldcg(&c.tile_sc[i * 4 + 3]); };
@@ -661,6 +676,7 @@ __device__ __forceinline__ void usq_one(const Ctx& c, int k, int lane, bool one)
                   : strided_sum(T.tile_begin + lane, T.tile_end, 32, ld);
   us = warp_sum(us);
   if (lane == 0) c.pay_usq[k] = T.weight * us;
+  return T.weight * us;  // the payload value (lane 0)
 }
 __device__ __forceinline__ void usq_payload(const Ctx& c, int t0, int t1) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -689,6 +705,40 @@ __global__ void __launch_bounds__(kThreads) kg_sumsq(Ctx c, int t0, int t1, doub
 // i handles tensors i, i + kThreads, ...: the per-tensor sums, then the global sum of g^2
 // over the call's tensors (fixed order: block_sum), the clip scale and the per-tensor
 // scalars.
+// K2's clip rule (optim.cpp:302-303 on the global norm) and per-tensor scalars, shared by
+// k2_body and k2_one so both compute them with the same operations
+__device__ __forceinline__ double k2_clip_scale(double G, int use_clip, double clip,
+                                                const double* ext_sumsq) {
+  double s = 1.0;
+  if (use_clip) {
+    const double sumsq = ext_sumsq ? *ext_sumsq : G;
+    const double norm = sqrt(sumsq);
+    if (norm > clip && norm > 0) s = clip / norm;
+  }
+  return s;
+}
+__device__ __forceinline__ void k2_tensor(const Ctx& c, int k, double s, double lr, double b2,
+                                          double gsq_k, double psq_k, double vrs_k) {
+  TensorInfo* Tm = const_cast<TensorInfo*>(&c.tensors[k]);
+  const TensorInfo T = *Tm;
+  const int64_t t = T.t + 1;  // optim.cpp:219
+  Tm->t = t;
+  const double corr = 1.0 - pow(b2, (double)t);
+  const double n = (double)T.numel_global;
+  const double rms_theta = sqrt(psq_k / n);
+  const double lr_t = lr * fmax(1e-3, rms_theta);
+  double row_mean = 0.0;
+  if (T.factored) {  // mean of the new v_row, by linearity of the EMA
+    const double gsq = s * s * gsq_k;
+    const double sum_new = b2 * vrs_k + (1 - b2) * (gsq / (double)T.cols);
+    row_mean = sum_new / ((double)T.rows_global * corr);
+  }
+  c.tens_sc[k * kTensScalars + TS_CORR] = corr;
+  c.tens_sc[k * kTensScalars + TS_LRT] = lr_t;
+  c.tens_sc[k * kTensScalars + TS_ROWMEAN] = row_mean;
+  c.mins[2 * k] = c.mins[2 * k + 1] = 0x7f800000u;  // +inf: K3 lowers them
+}
+
 __device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int use_clip,
                         double clip, const double* ext_sumsq, double* red) {
   // per-tensor sums arrive (already all-reduced across ranks when sharded) in the payload
@@ -703,38 +753,30 @@ __device__ void k2_body(const Ctx& c, int t0, int t1, double lr, double b2, int 
   for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) G += c.tens_sc[k * kTensScalars + TS_GSQ];
   G = block_sum(G, red);
   if (threadIdx.x == 0) {
-    double s = 1.0;
-    if (use_clip) {  // optim.cpp:302-303 rule on the global norm
-      const double sumsq = ext_sumsq ? *ext_sumsq : G;
-      const double norm = sqrt(sumsq);
-      if (norm > clip && norm > 0) s = clip / norm;
-    }
-    c.glob[0] = s;
+    c.glob[0] = k2_clip_scale(G, use_clip, clip, ext_sumsq);
     c.glob[1] = G;
   }
   __syncthreads();
   const double s = c.glob[0];
-  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x) {
-    TensorInfo* Tm = const_cast<TensorInfo*>(&c.tensors[k]);
-    const TensorInfo T = *Tm;
-    const int64_t t = T.t + 1;  // optim.cpp:219
-    Tm->t = t;
-    const double corr = 1.0 - pow(b2, (double)t);
-    const double n = (double)T.numel_global;
-    const double rms_theta = sqrt(c.tens_sc[k * kTensScalars + TS_PSQ] / n);
-    const double lr_t = lr * fmax(1e-3, rms_theta);
-    double row_mean = 0.0;
-    if (T.factored) {  // mean of the new v_row, by linearity of the EMA
-      const double gsq = s * s * c.tens_sc[k * kTensScalars + TS_GSQ];
-      const double sum_new =
-          b2 * c.tens_sc[k * kTensScalars + TS_VRS] + (1 - b2) * (gsq / (double)T.cols);
-      row_mean = sum_new / ((double)T.rows_global * corr);
-    }
-    c.tens_sc[k * kTensScalars + TS_CORR] = corr;
-    c.tens_sc[k * kTensScalars + TS_LRT] = lr_t;
-    c.tens_sc[k * kTensScalars + TS_ROWMEAN] = row_mean;
-    c.mins[2 * k] = c.mins[2 * k + 1] = 0x7f800000u;  // +inf: K3 lowers them
-  }
+  for (int k = t0 + threadIdx.x; k < t1; k += blockDim.x)
+    k2_tensor(c, k, s, lr, b2, c.tens_sc[k * kTensScalars + TS_GSQ],
+              c.tens_sc[k * kTensScalars + TS_PSQ], c.tens_sc[k * kTensScalars + TS_VRS]);
+}
+
+// K2 for a one-tensor fused call, by thread 0 of KR's tensor block, from the payload values
+// it has just formed (gsq, psq, vrs -- what k2_body would read back): the same bits as
+// k2_body (its block sum over one tensor adds only zeros) without the ticket and three
+// dependent L2 round trips on the hook form's critical path.
+__device__ void k2_one(const Ctx& c, int k, double gsq, double psq, double vrs, double lr,
+                       double b2, int use_clip, double clip, const double* ext_sumsq) {
+  c.tens_sc[k * kTensScalars + TS_GSQ] = gsq;
+  c.tens_sc[k * kTensScalars + TS_PSQ] = psq;
+  c.tens_sc[k * kTensScalars + TS_VRS] = vrs;
+  const double G = gsq;
+  const double s = k2_clip_scale(G, use_clip, clip, ext_sumsq);
+  c.glob[0] = s;
+  c.glob[1] = G;
+  k2_tensor(c, k, s, lr, b2, gsq, psq, vrs);
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -1013,22 +1055,34 @@ __global__ void __launch_bounds__(kThreads, k4_minb<GT>())
     __syncthreads();
     if (last) {
       __threadfence();
-      usq_payload(c, t0, t1);
-      __syncthreads();
-      k5_body(c, t0, t1, adalomo_clip);
+      if (t1 - t0 == 1) {  // one tensor: K5 from warp 0's sum in registers (same bits)
+        if (threadIdx.x < 32) {
+          const double lrt = c.tens_sc[t0 * kTensScalars + TS_LRT];  // in flight with the sum
+          const double numel = (double)c.tensors[t0].numel_global;
+          const double us = usq_one(c, t0, threadIdx.x, true);
+          if (threadIdx.x == 0) k5_val(c, t0, us, numel, lrt, adalomo_clip);
+        }
+      } else {
+        usq_payload(c, t0, t1);
+        __syncthreads();
+        k5_body(c, t0, t1, adalomo_clip);
+      }
       if (threadIdx.x == 0) *ticket = 0u;
     }
   }
 }
 
 // ============================ K5: damping ==============================================
-__device__ __forceinline__ void k5_one(const Ctx& c, int k, double adalomo_clip) {
-  const TensorInfo T = c.tensors[k];  // optim.cpp:269-273
-  const double us = __ldcg(&c.pay_usq[k]);
-  const double rms_u = sqrt(us / (double)T.numel_global);
+__device__ __forceinline__ void k5_val(const Ctx& c, int k, double us, double numel, double lrt,
+                                       double adalomo_clip) {  // optim.cpp:269-273
+  const double rms_u = sqrt(us / numel);
   const double damp = fmax(1.0, rms_u / adalomo_clip);
   c.tens_sc[k * kTensScalars + TS_USQ] = us;
-  c.tens_sc[k * kTensScalars + TS_F] = c.tens_sc[k * kTensScalars + TS_LRT] / damp;
+  c.tens_sc[k * kTensScalars + TS_F] = lrt / damp;
+}
+__device__ __forceinline__ void k5_one(const Ctx& c, int k, double adalomo_clip) {
+  k5_val(c, k, __ldcg(&c.pay_usq[k]), (double)c.tensors[k].numel_global,
+         c.tens_sc[k * kTensScalars + TS_LRT], adalomo_clip);
 }
 __device__ void k5_body(const Ctx& c, int t0, int t1, double adalomo_clip) {
   for (int k = t0 + (int)threadIdx.x; k < t1; k += blockDim.x) k5_one(c, k, adalomo_clip);
