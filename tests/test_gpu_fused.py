@@ -388,12 +388,14 @@ def test_lomo_host_clip_reuses_its_resident_gradient_buffer():
     """mco_lomo_apply_host keeps the device-resident gradient between calls (grown when a
     call needs more, freed by mco_host_release): every call -- smaller, larger, fp64
     (8 B gradients), after a release -- equals the device path."""
-    free0 = torch.cuda.mem_get_info()[0]
+    import os
     for n, dt in [(1 << 22, np.float32), (1000, np.float32), ((1 << 23) + 5, np.float32),
                   ((1 << 22) + 3, np.float64), ("release", None), (1 << 21, np.float32)]:
-        if n == "release":
+        if n == "release":  # the 32 MiB buffer goes back to the driver
+            before = torch.cuda.mem_get_info()[0]
             optim.host_release()
-            assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)
+            if not os.environ.get("MCO_UNDER_SANITIZER"):  # (memcheck defers frees)
+                assert torch.cuda.mem_get_info()[0] - before >= (16 << 20)
             continue
         p = O.synth(n, 12, 0, 0, 0, 0, -6, 0, False).astype(dt)
         g = O.synth(n, 12, 1, 0, 1, 0, -7, 10, False).astype(dt)

@@ -3,6 +3,7 @@
 # (flat_tma_kernel / lomo_tma_kernel gsh: aligned-down copies one granule longer), the
 # AdaLomo per-tensor vector/scalar split, KR's per-tensor blocks with the ticketed K2,
 # K4's packed-pair form, and the one-launch cluster kernel for small 1-D tensors (DSMEM).
+export MCO_UNDER_SANITIZER=1
 for tool in memcheck racecheck synccheck; do
   echo "## $tool: shifted gradient reads (flat kinds + LOMO, every phase pair, fp32)"
   timeout 1500 compute-sanitizer --tool $tool --print-limit 20 python -m pytest tests/test_gpu_flat.py -q -x \
