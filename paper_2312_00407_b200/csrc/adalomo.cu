@@ -1451,6 +1451,9 @@ __device__ __forceinline__ void k6_tiles(const Ctx& c, const Ptrs& P, int64_t ti
 // equal the multi-kernel path's, which every other form shares.  (A first version on
 // one 1024-thread CTA was issue-latency-bound on one SM: 22 us per call.)
 constexpr int kSmallTiles = 32, kSmallCluster = 8, kSmallPer = kSmallTiles / kSmallCluster;
+#ifndef MCO_SMALL_EARLY
+#define MCO_SMALL_EARLY 1  // A/B: k_small_vec triggers its dependents before its own wait
+#endif
 
 template <typename GT, typename PT>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -1465,8 +1468,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   // every CTA of the cluster must have started before any DSMEM access: arrive now,
   // wait just before the first remote write (the loads below overlap the barrier)
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+  // the next tensor's K1 may start now, before this kernel's own wait: it touches only its
+  // own tensor and waits at its end (k1_stats early), so it overlaps the previous tensor's
+  // K6 as it would without this small call in between
+  if (MCO_SMALL_EARLY && trigger) pdl_trigger();
   pdl_wait();
-  if (trigger) pdl_trigger();  // the next tensor's K1 may start (see k1_stats)
+  if (!MCO_SMALL_EARLY && trigger) pdl_trigger();
   const TensorInfo T = c.tensors[k];
   const GT* g = gptr<GT>(P, T, k);
   PT* p = pptr<PT>(P, T, k);
